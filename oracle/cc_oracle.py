@@ -1,0 +1,506 @@
+"""CPU oracle for the CompactFusion residual-compression path — TEST INFRASTRUCTURE ONLY.
+
+This module is a numpy restatement of the reference package `compactcomm`
+(arXiv 2507.17511, `/root/reference/pkg/src/compactcomm`) for the codecs and
+the residual/error-feedback protocol that the B200 kernels implement.  It is
+the *checker*: only `tests/`, `__graft_entry__.smoke()` and the `cpu_baseline`
+/ `--impl reference` legs of `bench.py` may import it.  The product package
+`paper_2507_17511_b200` never imports it and has no CPU fallback.
+
+Parity pinning: every function here is checked bit-for-bit against fixtures
+produced by running the reference itself (`tests/golden/make_golden.py`,
+outputs committed under `tests/golden/`), see `tests/test_oracle_golden.py`.
+
+Everything operates on *bodies*: the little-endian codec body bytes that the
+reference serializes after its 9-byte frame header (`cx:580-603`).  The body is
+exactly what crosses NVLink on the device path, so the oracle and the CUDA
+kernels are compared on the same byte strings.
+
+Citations: cx = compressors.py, pl = pipeline.py, la = linalg.py (all under
+/root/reference/pkg/src/compactcomm/).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# cx:52 / cx:54 / la:13
+ROW_SCALE_FLOOR = 1e-30
+LEVELS_2BIT = np.array([-2.0, -0.5, 0.5, 2.0], dtype=np.float64)
+DEGENERATE_TOL = 1e-12
+
+# codec tags, cx:56-62
+RAW, SIGN1, QUANT2, LOWRANK, LOWRANK4, NMBLOCK, TOPK = range(7)
+
+
+# ---------------------------------------------------------------------------
+# rank-1 magnitude scales (cx:135-149)
+# ---------------------------------------------------------------------------
+
+def rank1_scales(t):
+    """Return (u f32[n], v f32[C]) for target t (f32 [n, C]).
+
+    g = mean|t| over all entries (f64); u_i = max(rowmean_i / g, 1e-30) -> f32;
+    v_j = colmean_j -> f32; all-zero t gives u = 1, v = 0 (cx:141-149).
+    """
+    mag = np.abs(np.asarray(t, dtype=np.float64))
+    n, c = mag.shape
+    g = float(mag.mean())
+    if g == 0.0:
+        return np.ones(n, np.float32), np.zeros(c, np.float32)
+    row = mag.mean(axis=1)
+    col = mag.mean(axis=0)
+    return np.maximum(row / g, ROW_SCALE_FLOOR).astype(np.float32), col.astype(np.float32)
+
+
+def _scale_grid(u, v):
+    # cx:131-132: exact f64 outer product of the f32 scales
+    return np.outer(u.astype(np.float64), v.astype(np.float64))
+
+
+# ---------------------------------------------------------------------------
+# code assignment (cx:373-391) and bit packing (cx:523-538, np.packbits little)
+# ---------------------------------------------------------------------------
+
+def sign_codes(t):
+    """1 where t < 0 (so -0.0 and +0.0 both give 0), flat row-major (cx:375)."""
+    return (np.asarray(t) < 0).astype(np.uint8).ravel()
+
+
+def quant2_codes(t, u, v):
+    """Nearest of {-2,-0.5,+0.5,+2} to t/(u v^T), ties to the smaller level,
+    zero scale -> code 2 (cx:379-391)."""
+    s = _scale_grid(u, v)
+    x = np.asarray(t, dtype=np.float64)
+    q = np.zeros_like(s)
+    live = s != 0.0
+    q[live] = x[live] / s[live]
+    out = np.full(x.shape, 2, np.uint8)
+    out[q > 1.25] = 3
+    out[(q < 0) & (q >= -1.25)] = 1
+    out[q < -1.25] = 0
+    return out.ravel()
+
+
+def pack_bits(bits):
+    return np.packbits(np.asarray(bits, np.uint8), bitorder="little")
+
+
+def unpack_bits(buf, count):
+    return np.unpackbits(np.frombuffer(bytes(buf), np.uint8), count=count, bitorder="little")
+
+
+def pack_crumbs(codes):
+    """Four 2-bit codes per byte, first code in the low bits (cx:523-529)."""
+    codes = np.asarray(codes, np.uint8)
+    pad = np.zeros(-(-codes.size // 4) * 4, np.uint8)
+    pad[: codes.size] = codes
+    q = pad.reshape(-1, 4)
+    return (q[:, 0] | (q[:, 1] << 2) | (q[:, 2] << 4) | (q[:, 3] << 6)).astype(np.uint8)
+
+
+def unpack_crumbs(buf, count):
+    b = np.frombuffer(bytes(buf), np.uint8)
+    q = np.stack([(b >> s) & 3 for s in (0, 2, 4, 6)], axis=1)
+    return q.ravel()[:count].astype(np.uint8)
+
+
+def pack_nibbles(codes):
+    """Two 4-bit codes per byte, low nibble first (cx:541-546)."""
+    codes = np.asarray(codes, np.uint8)
+    pad = np.zeros(-(-codes.size // 2) * 2, np.uint8)
+    pad[: codes.size] = codes
+    q = pad.reshape(-1, 2)
+    return (q[:, 0] | (q[:, 1] << 4)).astype(np.uint8)
+
+
+def unpack_nibbles(buf, count):
+    b = np.frombuffer(bytes(buf), np.uint8)
+    return np.stack([b & 15, b >> 4], axis=1).ravel()[:count].astype(np.uint8)
+
+
+def _f32le(a):
+    return np.ascontiguousarray(a, dtype="<f4").tobytes()
+
+
+# ---------------------------------------------------------------------------
+# body sizes (bit_size, cx:167-348) and ledger helpers (cx:500-515)
+# ---------------------------------------------------------------------------
+
+def body_bits(tag, n, c, rank=0, k=0, nm=(0, 0)):
+    if tag == RAW:
+        return 32 * n * c
+    if tag == SIGN1:
+        return n * c + 32 * (n + c)
+    if tag == QUANT2:
+        return 2 * n * c + 32 * (n + c)
+    if tag == LOWRANK:
+        return 16 * rank * (n + c)
+    if tag == LOWRANK4:
+        return 4 * rank * (n + c) + 64 * rank
+    if tag == TOPK:
+        return 48 * k
+    if tag == NMBLOCK:
+        nn, m = nm
+        return n * (-(-c // m)) * (m + 16 * nn)
+    raise ValueError(tag)
+
+
+def body_bytes(tag, n, c, **kw):
+    return -(-body_bits(tag, n, c, **kw) // 8)
+
+
+def nominal_bits(tag, n, c, **kw):
+    # raw is charged at the 16-bit baseline (cx:170-173)
+    return 16 * n * c if tag == RAW else body_bits(tag, n, c, **kw)
+
+
+def topk_count(n, c, keep_fraction):
+    size = n * c
+    return min(size, int(np.ceil(keep_fraction * size)))  # cx:451
+
+
+# ---------------------------------------------------------------------------
+# quantizer bodies (cx:373-391 encode, cx:206-211 / cx:237-242 decode)
+# ---------------------------------------------------------------------------
+
+def sign1_body(t):
+    u, v = rank1_scales(t)
+    return pack_bits(sign_codes(t)).tobytes() + _f32le(u) + _f32le(v)
+
+
+def quant2_body(t):
+    u, v = rank1_scales(t)
+    return pack_crumbs(quant2_codes(t, u, v)).tobytes() + _f32le(u) + _f32le(v)
+
+
+def _split_scales(body, off, n, c):
+    u = np.frombuffer(body, "<f4", n, off).astype(np.float32)
+    v = np.frombuffer(body, "<f4", c, off + 4 * n).astype(np.float32)
+    return u, v
+
+
+def sign1_decode(body, n, c):
+    nb = -(-n * c // 8)
+    u, v = _split_scales(body, nb, n, c)
+    neg = unpack_bits(body[:nb], n * c).reshape(n, c)
+    sgn = np.where(neg == 1, -1.0, 1.0)
+    return (sgn * _scale_grid(u, v)).astype(np.float32)
+
+
+def quant2_decode(body, n, c):
+    nb = -(-2 * n * c // 8)
+    u, v = _split_scales(body, nb, n, c)
+    lv = LEVELS_2BIT[unpack_crumbs(body[:nb], n * c)].reshape(n, c)
+    return (lv * _scale_grid(u, v)).astype(np.float32)
+
+
+# ---------------------------------------------------------------------------
+# top-k (cx:446-456 encode, cx:358-361 decode)
+# ---------------------------------------------------------------------------
+
+def topk_body(t, keep_fraction):
+    n, c = t.shape
+    k = topk_count(n, c, keep_fraction)
+    flat = np.asarray(t, np.float32).ravel()
+    order = np.lexsort((np.arange(flat.size), -np.abs(flat)))[:k]
+    idx = np.sort(order).astype("<u4")
+    vals = flat[idx.astype(np.int64)].astype("<f2")
+    return idx.tobytes() + vals.tobytes()
+
+
+def topk_decode(body, n, c):
+    k = len(body) // 6
+    idx = np.frombuffer(body, "<u4", k, 0).astype(np.int64)
+    vals = np.frombuffer(body, "<f2", k, 4 * k).astype(np.float32)
+    out = np.zeros(n * c, np.float32)
+    out[idx] = vals
+    return out.reshape(n, c)
+
+
+# ---------------------------------------------------------------------------
+# low-rank (la:49-112, cx:394-426, cx:556-572, cx:589-595, cx:278-288)
+# ---------------------------------------------------------------------------
+
+def mm(a, b):
+    """f64-accumulated product stored as f32 (la:49-58)."""
+    return (np.asarray(a, np.float64) @ np.asarray(b, np.float64)).astype(np.float32)
+
+
+def gaussian(rng, rows, cols):
+    return rng.standard_normal((rows, cols), dtype=np.float64).astype(np.float32)  # la:67-74
+
+
+def cgs2(m, rng):
+    """Column-by-column Gram-Schmidt with two projection passes, degenerate
+    columns replaced by fresh N(0,1) draws from `rng` (la:77-112)."""
+    q = np.array(m, dtype=np.float64)
+    rows, cols = q.shape
+    for j in range(cols):
+        prev = q[:, :j]
+        col = q[:, j]
+        if j:
+            col = col - prev @ (prev.T @ col)
+            col = col - prev @ (prev.T @ col)
+        nsq = np.dot(col, col)
+        while nsq < DEGENERATE_TOL:
+            col = rng.standard_normal(rows)
+            if j:
+                col = col - prev @ (prev.T @ col)
+                col = col - prev @ (prev.T @ col)
+            nsq = np.dot(col, col)
+        q[:, j] = col / np.sqrt(nsq)
+    return q.astype(np.float32)
+
+
+def subspace(a, r, iters, rng):
+    """Randomized rank-r range finder (cx:394-412). Returns (U, Q)."""
+    rows, cols = a.shape
+    if not 1 <= r <= min(rows, cols):
+        raise ValueError(f"rank {r} out of range for {a.shape}")
+    q = cgs2(gaussian(rng, cols, r), rng)
+    for _ in range(iters):
+        q = cgs2(mm(a.T, mm(a, q)), rng)
+    return cgs2(mm(a, q), rng), q
+
+
+def int4_columns(f):
+    """Per-column symmetric 16-level codes + f32 ranges (cx:556-566)."""
+    f = np.asarray(f, np.float64)
+    rng_ = np.abs(f).max(axis=0)
+    step = 2.0 * rng_ / 15.0
+    codes = np.zeros(f.shape, np.uint8)
+    live = rng_ > 0
+    if np.any(live):
+        codes[:, live] = np.clip(np.rint((f[:, live] + rng_[live]) / step[live]), 0, 15).astype(np.uint8)
+    return codes, rng_.astype(np.float32)
+
+
+def int4_values(codes, ranges):
+    r = np.asarray(ranges, np.float32).astype(np.float64)
+    return -r[None, :] + codes.astype(np.float64) * (2.0 * r / 15.0)[None, :]  # cx:569-572
+
+
+def lowrank_factors(a, r, iters, rng):
+    u, _ = subspace(a, r, iters, rng)
+    return u, mm(a.T, u)  # cx:419
+
+
+def lowrank_body(a, r, iters, rng, int4=False):
+    u, w = lowrank_factors(a, r, iters, rng)
+    return lowrank_body_from_factors(u, w, int4)
+
+
+def lowrank_body_from_factors(u, w, int4):
+    if not int4:
+        # column-major f16 U then W (cx:591, cx:698-699)
+        return (np.asarray(u, "<f2").tobytes(order="F") + np.asarray(w, "<f2").tobytes(order="F"))
+    uc, ur = int4_columns(u)
+    wc, wr = int4_columns(w)
+    nib = pack_nibbles(np.concatenate([uc.ravel(order="F"), wc.ravel(order="F")]))
+    return _f32le(ur) + _f32le(wr) + nib.tobytes()
+
+
+def lowrank_unpack(body, n, c, r, int4):
+    """Dequantized (U, W) in f64 (cx:278-284, cx:642-657)."""
+    if not int4:
+        u = np.frombuffer(body, "<f2", n * r, 0).reshape(n, r, order="F")
+        w = np.frombuffer(body, "<f2", c * r, 2 * n * r).reshape(c, r, order="F")
+        return u.astype(np.float64), w.astype(np.float64)
+    ur = np.frombuffer(body, "<f4", r, 0)
+    wr = np.frombuffer(body, "<f4", r, 4 * r)
+    codes = unpack_nibbles(body[8 * r:], r * (n + c))
+    uc = codes[: n * r].reshape(n, r, order="F")
+    wc = codes[n * r:].reshape(c, r, order="F")
+    return int4_values(uc, ur), int4_values(wc, wr)
+
+
+def lowrank_decode(body, n, c, r, int4):
+    u, w = lowrank_unpack(body, n, c, r, int4)
+    return (u @ w.T).astype(np.float32)  # cx:286-288
+
+
+# ---------------------------------------------------------------------------
+# N:M block sparsifier (cx:429-443, cx:323-329)
+# ---------------------------------------------------------------------------
+
+def nm_body(t, nn, m):
+    rows, cols = t.shape
+    pad = (-cols) % m
+    blk = np.pad(np.asarray(t, np.float32), ((0, 0), (0, pad))).reshape(-1, m)
+    keep = np.sort(np.argsort(-np.abs(blk), axis=1, kind="stable")[:, :nn], axis=1)
+    mask = np.zeros(blk.shape, np.uint8)
+    np.put_along_axis(mask, keep, 1, axis=1)
+    vals = np.take_along_axis(blk, keep, axis=1).astype("<f2").ravel()
+    return pack_bits(mask.ravel()).tobytes() + vals.tobytes()
+
+
+def nm_decode(body, n, c, nn, m):
+    pc = -(-c // m) * m
+    total = n * pc
+    mb = -(-total // 8)
+    mask = unpack_bits(body[:mb], total).astype(bool)
+    vals = np.frombuffer(body, "<f2", (total // m) * nn, mb).astype(np.float32)
+    flat = np.zeros(total, np.float32)
+    flat[mask] = vals
+    return np.ascontiguousarray(flat.reshape(n, pc)[:, :c])
+
+
+# ---------------------------------------------------------------------------
+# codec dispatch over bodies
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class Codec:
+    """Mirror of CompressorSpec fields that shape a body (cx:80-100)."""
+
+    tag: int
+    rank: int = 0
+    iters: int = 1
+    keep_fraction: float = 0.0
+    nm: tuple = (0, 0)
+
+
+def encode_body(t, codec, rng=None):
+    tag = codec.tag
+    if tag == RAW:
+        return _f32le(t)
+    if tag == SIGN1:
+        return sign1_body(t)
+    if tag == QUANT2:
+        return quant2_body(t)
+    if tag in (LOWRANK, LOWRANK4):
+        return lowrank_body(t, codec.rank, codec.iters, rng, int4=(tag == LOWRANK4))
+    if tag == TOPK:
+        return topk_body(t, codec.keep_fraction)
+    if tag == NMBLOCK:
+        return nm_body(t, *codec.nm)
+    raise ValueError(tag)
+
+
+def decode_body(body, codec, n, c):
+    tag = codec.tag
+    if tag == RAW:
+        return np.frombuffer(body, "<f4", n * c).reshape(n, c).astype(np.float32)
+    if tag == SIGN1:
+        return sign1_decode(body, n, c)
+    if tag == QUANT2:
+        return quant2_decode(body, n, c)
+    if tag in (LOWRANK, LOWRANK4):
+        return lowrank_decode(body, n, c, codec.rank, tag == LOWRANK4)
+    if tag == TOPK:
+        return topk_decode(body, n, c)
+    if tag == NMBLOCK:
+        return nm_decode(body, n, c, *codec.nm)
+    raise ValueError(tag)
+
+
+def sqnorm(a):
+    d = np.asarray(a, np.float64).ravel()
+    return float(np.dot(d, d))  # la:61-64
+
+
+# ---------------------------------------------------------------------------
+# residual / error-feedback protocol (pl:55-165)
+# ---------------------------------------------------------------------------
+
+NAIVE, NO_FEEDBACK, WITH_FEEDBACK = "naive", "residual_no_feedback", "residual_with_feedback"
+
+
+@dataclass
+class Channel:
+    """One (layer, peer) stream end: mirrors LayerState (pl:55-73)."""
+
+    mode: str
+    warmup: int
+    base: np.ndarray
+    fb: np.ndarray = None
+    ref: np.ndarray = None
+    step: int = 0
+    log: list = field(default_factory=list)
+
+    def __post_init__(self):
+        self.base = np.asarray(self.base, np.float32)
+        if self.fb is None:
+            self.fb = np.zeros_like(self.base)
+        if self.ref is None:
+            self.ref = self.base
+
+
+def send(ch, x, codec, rng=None):
+    """Sender step (pl:84-121). Returns (tag, body, record dict)."""
+    x = np.asarray(x, np.float32)
+    if x.shape != ch.base.shape:
+        raise ValueError("shape mismatch")
+    t_no = ch.step + 1
+    n, c = x.shape
+    if t_no <= ch.warmup or codec.tag == RAW:
+        tag, body = RAW, _f32le(x)
+        target = x
+        dec = x.copy()
+        ch.base = dec
+        ch.fb = np.zeros_like(x)
+    else:
+        if ch.mode == NAIVE:
+            target = x
+        elif ch.mode == NO_FEEDBACK:
+            target = x - ch.ref
+        else:
+            target = (x - ch.base) + ch.fb
+        tag = codec.tag
+        body = encode_body(target, codec, rng)
+        dec = decode_body(body, codec, n, c)
+        if ch.mode == WITH_FEEDBACK:
+            ch.fb = target - dec
+        ch.base = dec if ch.mode == NAIVE else ch.base + dec
+    ch.ref = x
+    ch.step = t_no
+    err = sqnorm(dec.astype(np.float64) - target.astype(np.float64))
+    tot = sqnorm(target)
+    if tot == 0.0:
+        dh = 1.0 if err == 0.0 else -math.inf
+    else:
+        dh = 1.0 - err / tot
+    rec = {"step": t_no, "compression_error": err, "bits": nominal_bits(tag, n, c, **_kw(codec, n, c, tag)),
+           "delta_hat": dh, "target_sqnorm": tot}
+    return tag, body, rec
+
+
+def _kw(codec, n, c, tag):
+    if tag in (LOWRANK, LOWRANK4):
+        return {"rank": codec.rank}
+    if tag == TOPK:
+        return {"k": topk_count(n, c, codec.keep_fraction)}
+    if tag == NMBLOCK:
+        return {"nm": codec.nm}
+    return {}
+
+
+def receive(ch, step, warm, tag, body, codec):
+    """Receiver step (pl:146-165): validate before touching state."""
+    if step != ch.step + 1:
+        raise RuntimeError("step desynchronization")
+    if (step <= ch.warmup) != warm:
+        raise RuntimeError("warmup flag mismatch")
+    n, c = ch.base.shape
+    dec = decode_body(body, codec if tag != RAW else Codec(RAW), n, c)
+    if warm or tag == RAW or ch.mode == NAIVE:
+        ch.base = dec
+    else:
+        ch.base = ch.base + dec
+    ch.step = step
+    return ch.base
+
+
+# ---------------------------------------------------------------------------
+# patch-parallel all-gather step (mesh:125-135, mesh:188-237)
+# ---------------------------------------------------------------------------
+
+def shard_rows(rows, parts):
+    q = rows // parts
+    if q == 0:
+        raise ValueError("cannot shard")
+    return [(d * q, rows if d == parts - 1 else (d + 1) * q) for d in range(parts)]
