@@ -1,0 +1,165 @@
+/*
+ * compactcomm.h — C ABI of the B200 (sm_100a) residual-compression path.
+ *
+ * Drop-in boundary for the reference package `compactcomm` (arXiv 2507.17511,
+ * /root/reference/pkg/src/compactcomm).  Every entry point is extern "C", takes
+ * plain device pointers, sizes and a cudaStream_t (passed as void*), never
+ * throws, and returns CC_OK or a negative status.  The Python host mirror
+ * (paper_2507_17511_b200/) binds these with ctypes and raises the reference's
+ * exception classes for the status codes.
+ *
+ * All work is stream-ordered: nothing here synchronizes the device.  State
+ * buffers (base, feedback, ref) are owned by the caller and updated in place;
+ * shape/step validation happens host-side BEFORE any launch, so a failing call
+ * leaves state untouched (reference pipeline.py:146-151).
+ *
+ * Body layout = the reference's codec body byte-for-byte (compressors.py:580-603,
+ * i.e. the frame minus its 9-byte <BII header and meta ints):
+ *   CC_SIGN1   ceil(n*C/8) B sign bitmap (little bit order, 1 = negative),
+ *              then u f32[n], v f32[C]                          (cx:373-376, 586)
+ *   CC_QUANT2  ceil(2*n*C/8) B codes (4/byte, first code in low bits,
+ *              0:-2 1:-0.5 2:+0.5 3:+2), then u f32[n], v f32[C] (cx:379-391, 588)
+ *   CC_QUANT4  extension (no reference; parity unpinned): ceil(4*n*C/8) B
+ *              codes (2/byte, low nibble first, level (k-7.5)/2), then u, v
+ *   CC_TOPK    k x u32 ascending flat indices, then k x f16 values (cx:446-456, 601)
+ *   CC_LOWRANK U [n,r] then W [C,r], column-major f16           (cx:415-426, 591)
+ *   CC_LOWRANK4 2r f32 ranges, then one nibble stream U then W col-major (cx:592-595)
+ *   CC_RAW     n*C f32 (wire may carry bf16 when inputs are bf16: lossless)
+ */
+#ifndef COMPACTCOMM_H
+#define COMPACTCOMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CC_API __attribute__((visibility("default")))
+
+/* status codes (reference exception classes in brackets) */
+#define CC_OK 0
+#define CC_ERR_ARG (-1)        /* ValueError (cx:90-100)                       */
+#define CC_ERR_SHAPE (-2)      /* linalg.ShapeError (la:16)                    */
+#define CC_ERR_PAYLOAD (-3)    /* compressors.PayloadError (cx:67)             */
+#define CC_ERR_PROTOCOL (-4)   /* pipeline.ProtocolError (pl:36)               */
+#define CC_ERR_CUDA (-5)       /* launch / runtime failure                      */
+#define CC_ERR_UNSUPPORTED (-6)
+
+/* codec tags: identical numbering to compressors.py:56-62 */
+#define CC_RAW 0
+#define CC_SIGN1 1
+#define CC_QUANT2 2
+#define CC_LOWRANK 3
+#define CC_LOWRANK4 4
+#define CC_NMBLOCK 5
+#define CC_TOPK 6
+#define CC_QUANT4 16 /* extension: 4-bit element quantizer (north_star), no reference */
+
+/* pipeline modes: pipeline.py:40-43 */
+#define CC_NAIVE 0
+#define CC_NO_FEEDBACK 1
+#define CC_WITH_FEEDBACK 2
+
+/* element types of activations / raw wire bodies */
+#define CC_F32 0
+#define CC_BF16 1
+
+/* scale modes for the quantizers: CC_SCALE_RANK1 is the reference's u v^T
+ * (cx:135-149); the other two are north_star extensions (parity unpinned). */
+#define CC_SCALE_RANK1 0
+#define CC_SCALE_PER_TOKEN 1
+#define CC_SCALE_PER_CHANNEL 2
+
+/* ---- sizes -------------------------------------------------------------- */
+
+/* Exact body size in bytes: ceil(bit_size/8) (cx:195-348). param = rank for
+ * low-rank, k for top-k, ignored otherwise.  Returns <0 on bad arguments. */
+CC_API int64_t cc_body_bytes(int codec, int64_t rows, int64_t cols, int64_t param);
+
+/* Device scratch bytes needed by cc_encode_step for this codec/shape. */
+CC_API int64_t cc_workspace_bytes(int codec, int64_t rows, int64_t cols, int64_t param);
+
+/* ---- sender step: pipeline.encode_step (pl:84-121) ------------------------
+ * One fused residual -> scale -> quantize -> pack -> state-update pass for
+ * the 1/2/4-bit codecs.
+ *   x        [rows, cols] activation (x_dtype), borrowed
+ *   base     [rows, cols] f32 shared base, updated in place
+ *   aux      [rows, cols] f32: feedback (CC_WITH_FEEDBACK), previous input
+ *            `ref` (CC_NO_FEEDBACK), unused (CC_NAIVE, may be NULL)
+ *   body     cc_body_bytes() device bytes, written
+ *   scales   optional f32 [rows+cols] aligned copy of (u, v) (may be NULL)
+ *   record   2 f64 on device: ||decode - target||^2, ||target||^2  (pl:115-120)
+ */
+CC_API int cc_encode_step(int codec, int mode, int scale_mode, int64_t rows, int64_t cols,
+                          const void *x, int x_dtype, float *base, float *aux,
+                          uint8_t *body, void *workspace, int64_t workspace_bytes,
+                          double *record, void *stream);
+
+/* Warmup / identity step (pl:89-97): base = x, feedback = 0, ref = x,
+ * body = raw x as body_dtype (CC_F32 = the reference wire, CC_BF16 lossless
+ * for bf16 inputs), record = {0, ||x||^2}. */
+CC_API int cc_warmup_step(int mode, int64_t rows, int64_t cols, const void *x, int x_dtype,
+                          float *base, float *aux, void *body, int body_dtype, double *record,
+                          void *stream);
+
+/* ---- receiver step: pipeline.decode_step (pl:146-165) ----------------------
+ * base = decode(body) when !accumulate (warmup / raw / naive), else
+ * base += decode(body).  param as in cc_body_bytes. */
+CC_API int cc_decode_step(int codec, int accumulate, int64_t rows, int64_t cols, int64_t param,
+                          const uint8_t *body, int body_dtype, float *base, void *stream);
+
+/* Batched receiver step for P-1 peers of one all-gather (mesh:232-236): one
+ * launch decodes `count` bodies into their bases.  rows[i] may differ (last
+ * shard takes the remainder, mesh:125-135); the arrays are HOST arrays of
+ * device pointers.  count <= 64. */
+CC_API int cc_decode_batched(int codec, int accumulate, int count, const int64_t *rows, int64_t cols,
+                             int64_t param, const uint8_t *const *bodies, int body_dtype,
+                             float *const *bases, void *stream);
+
+/* ---- generic protocol halves (for codecs that need the materialized target:
+ * top-k, low-rank) ------------------------------------------------------------
+ * cc_residual_target: t = (x - base) + fb | x - ref | x   (pl:99-104)
+ * cc_apply_decoded:   fb' = t - d, base' = base + d | d, ref' = x, and the
+ *                     record {||d - t||^2, ||t||^2} (pl:107-120); workspace
+ *                     >= 16 KiB of device scratch. */
+CC_API int cc_residual_target(int mode, int64_t rows, int64_t cols, const void *x, int x_dtype,
+                              const float *base, const float *aux, float *t, void *stream);
+CC_API int cc_apply_decoded(int mode, int64_t rows, int64_t cols, const void *x, int x_dtype,
+                            const float *t, const float *decoded, float *base, float *aux,
+                            double *record, void *workspace, int64_t workspace_bytes, void *stream);
+
+/* ---- standalone codec (compressors.encode / decode, cx:459-481) ---------- */
+
+/* encode target t (f32 [rows, cols]) into body; decoded (optional, f32) gets
+ * decode(body) — the stateless codec entry used by compressors.encode. */
+CC_API int cc_encode(int codec, int scale_mode, int64_t rows, int64_t cols, int64_t param,
+                     const float *t, uint8_t *body, float *decoded, void *workspace,
+                     int64_t workspace_bytes, void *stream);
+
+/* ---- top-k (cx:446-456) ---------------------------------------------------
+ * Radix-select the k largest |t| (ties -> lowest flat index), emit ascending
+ * u32 indices + f16 values.  Used by cc_encode_step with codec CC_TOPK; k is
+ * cc_topk_count(rows, cols, keep_fraction). */
+CC_API int64_t cc_topk_count(int64_t rows, int64_t cols, double keep_fraction);
+CC_API int cc_topk_encode(int64_t rows, int64_t cols, int64_t k, const float *t, uint8_t *body,
+                          float *decoded, void *workspace, int64_t workspace_bytes, void *stream);
+
+/* ---- low-rank (cx:394-426) -------------------------------------------------
+ * q0: [cols, r] f32 initial Gaussian block (drawn host-side from the same
+ * PCG64 stream as la.gaussian_matrix, cx:407); iterations = T. */
+CC_API int cc_lowrank_encode(int int4, int64_t rows, int64_t cols, int64_t rank, int iterations,
+                             const float *t, const float *q0, uint8_t *body, float *decoded,
+                             void *workspace, int64_t workspace_bytes, void *stream);
+CC_API int64_t cc_lowrank_workspace_bytes(int64_t rows, int64_t cols, int64_t rank);
+
+/* ---- diagnostics ----------------------------------------------------------- */
+CC_API const char *cc_last_error(void);
+CC_API int cc_version(void);
+/* number of kernels this library launched since load (evidence counter) */
+CC_API int64_t cc_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COMPACTCOMM_H */

@@ -1,0 +1,781 @@
+// K1 (fused residual -> rank-1 scale -> quantize -> pack -> state update) and
+// K2 (unpack -> dequantize -> accumulate into the cached base) for the 1/2/4-bit
+// codecs of CompactFusion, sm_100a.
+//
+// Reference semantics (all under /root/reference/pkg/src/compactcomm/):
+//   target       pipeline.py:99-104      t = (a* - base) + fb  |  a* - ref  |  a*
+//   scales       compressors.py:135-149  g = mean|t|, u_i = max(rowmean_i/g, 1e-30), v_j = colmean_j
+//   sign codes   compressors.py:373-376  bit = t < 0, np.packbits little bit order
+//   2-bit codes  compressors.py:379-391  thresholds +-1.25 on t/(u_i v_j), ties -> +-0.5
+//   decode       compressors.py:206-211, 237-242   d = f32(level * u64 * v64)
+//   state        pipeline.py:107-113     fb' = t - d, base' = base + d (or d), ref' = a*
+//   record       pipeline.py:115-120     ||d - t||^2, ||t||^2 in f64
+//   receiver     pipeline.py:159-163     base = d | base + d
+//
+// Data layout in HBM: every tensor is a row-major [n, C] f32 (bf16 for the
+// activation); the body is the reference's byte layout (codes, u f32[n], v f32[C]).
+//
+// Work decomposition (vector path, C % 8 == 0, 16-byte aligned rows): a CTA
+// owns a strip of <= 1024 columns (one float4 column group per thread, so the
+// 32 lanes of a warp read 512 contiguous bytes per f32 row) and RB consecutive
+// rows.  Column |t| sums stay in f64 registers across the RB rows; row sums
+// are warp-shuffle reduced per row and combined across warps through shared
+// memory in a fixed order, so every reduction is deterministic.
+// Pass A (k_scale_vec) reads x/base/aux once and emits f64 partials; the
+// finalize kernels turn them into u, v (written straight into the body);
+// pass B (k_quant_vec) re-reads the inputs (L2-resident for P >= 2 shards),
+// quantizes, packs codes with warp shuffles and writes base / feedback.
+#include "cc_common.cuh"
+#include "cc_internal.h"
+
+#include <algorithm>
+#include <vector>
+
+namespace cc {
+
+constexpr int kRowsUnroll = 4;
+constexpr int kMaxRB = 64;
+constexpr int kFinThreads = 256;
+
+struct QPlan {
+  int64_t n = 0, C = 0;
+  bool vec = false;
+  int threads = 0;  // threads per CTA (vector path) = strip width / 4
+  int nStrips = 1;
+  int RB = 1, nRB = 1;
+  // scalar path: bytes of codes handled per thread block
+  int64_t ncta_b = 0;  // CTAs of the quantize pass (record partial count)
+  // workspace pointers
+  double *colpart = nullptr, *rowpart = nullptr, *rowsum = nullptr, *blkpart = nullptr, *recpart = nullptr;
+  float *u = nullptr, *v = nullptr;
+  int nblk_rows = 0;
+};
+
+static int codec_bits(int codec) { return codec == CC_SIGN1 ? 1 : (codec == CC_QUANT2 ? 2 : 4); }
+
+static void plan_shape(QPlan &p, int64_t n, int64_t C, bool vec) {
+  p.n = n;
+  p.C = C;
+  p.vec = vec;
+  if (vec) {
+    int64_t sw = std::min<int64_t>(1024, cdiv(C, 128) * 128);
+    p.threads = (int)(sw / 4);
+    p.nStrips = (int)cdiv(C, sw);
+    const int64_t target = (int64_t)sm_count() * 4;
+    int64_t rbs = cdiv(n * p.nStrips, target);
+    rbs = cdiv(rbs, kRowsUnroll) * kRowsUnroll;
+    p.RB = (int)std::min<int64_t>(kMaxRB, std::max<int64_t>(kRowsUnroll, rbs));
+    p.nRB = (int)cdiv(n, p.RB);
+    p.ncta_b = (int64_t)p.nRB * p.nStrips;
+  } else {
+    p.threads = 256;
+    p.nStrips = 1;
+    p.RB = (int)n;
+    p.nRB = 1;
+    p.ncta_b = 0;  // set per codec below
+  }
+  p.nblk_rows = (int)cdiv(n, kFinThreads);
+}
+
+// workspace carve-up; returns bytes needed
+static size_t carve(QPlan &p, void *ws, int64_t scalar_ctas) {
+  uint8_t *b = reinterpret_cast<uint8_t *>(ws);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return b ? b + o : nullptr;
+  };
+  p.colpart = reinterpret_cast<double *>(take(sizeof(double) * (size_t)p.nRB * p.C));
+  p.rowpart = reinterpret_cast<double *>(take(sizeof(double) * (size_t)p.nStrips * p.n));
+  p.rowsum = reinterpret_cast<double *>(take(sizeof(double) * (size_t)p.n));
+  p.blkpart = reinterpret_cast<double *>(take(sizeof(double) * (size_t)p.nblk_rows));
+  p.u = reinterpret_cast<float *>(take(sizeof(float) * (size_t)p.n));
+  p.v = reinterpret_cast<float *>(take(sizeof(float) * (size_t)p.C));
+  int64_t nrec = p.vec ? p.ncta_b : scalar_ctas;
+  p.recpart = reinterpret_cast<double *>(take(sizeof(double) * 2 * (size_t)std::max<int64_t>(1, nrec)));
+  return off;
+}
+
+static int64_t scalar_quant_ctas(int64_t n, int64_t C, int bits) {
+  const int64_t nbytes = cdiv(n * C * bits, 8);
+  return cdiv(nbytes, 256);
+}
+
+int64_t quant_workspace_bytes(int64_t n, int64_t C) {
+  QPlan a, s;
+  plan_shape(a, n, C, true);
+  size_t wa = carve(a, nullptr, 0);
+  plan_shape(s, n, C, false);
+  size_t wsb = carve(s, nullptr, scalar_quant_ctas(n, C, 1));
+  return (int64_t)std::max(wa, wsb);
+}
+
+// ===========================================================================
+// pass A: |t| partial sums
+// ===========================================================================
+template <int MODE, typename XT>
+__global__ void __launch_bounds__(256) k_scale_vec(const XT *__restrict__ x, const float *__restrict__ base,
+                                                   const float *__restrict__ aux, int64_t n, int64_t C, int RB,
+                                                   double *__restrict__ colpart, double *__restrict__ rowpart) {
+  __shared__ double rowsm[kMaxRB][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + tid) * 4;
+  const bool active = j0 < C;
+  const int64_t r0 = (int64_t)blockIdx.y * RB;
+  const int rows = (int)(RB < n - r0 ? (int64_t)RB : n - r0);
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+
+  for (int rr = 0; rr < rows; rr += kRowsUnroll) {
+    float4 xv[kRowsUnroll], bv[kRowsUnroll], av[kRowsUnroll];
+#pragma unroll
+    for (int k = 0; k < kRowsUnroll; ++k) {
+      const bool ok = active && (rr + k) < rows;
+      const int64_t e = (r0 + rr + k) * C + j0;
+      xv[k] = ok ? Act<XT>::load4(x + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if constexpr (MODE == CC_WITH_FEEDBACK) {
+        bv[k] = ok ? __ldcs(reinterpret_cast<const float4 *>(base + e)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if constexpr (MODE != CC_NAIVE) {
+        av[k] = ok ? __ldcs(reinterpret_cast<const float4 *>(aux + e)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kRowsUnroll; ++k) {
+      float tt[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float bb = 0.f, aa = 0.f;
+        if constexpr (MODE == CC_WITH_FEEDBACK) bb = f4get(bv[k], q);
+        if constexpr (MODE != CC_NAIVE) aa = f4get(av[k], q);
+        tt[q] = target_of<MODE>(f4get(xv[k], q), bb, aa);
+      }
+      const double a0 = fabs((double)tt[0]), a1 = fabs((double)tt[1]);
+      const double a2 = fabs((double)tt[2]), a3 = fabs((double)tt[3]);
+      c0 += a0; c1 += a1; c2 += a2; c3 += a3;
+      double rp = ((a0 + a1) + a2) + a3;
+      rp = warp_sum(rp);
+      if (lane == 0 && rr + k < rows) rowsm[rr + k][warp] = rp;
+    }
+  }
+  if (active) {
+    double *cp = colpart + (int64_t)blockIdx.y * C + j0;
+    cp[0] = c0; cp[1] = c1; cp[2] = c2; cp[3] = c3;
+  }
+  __syncthreads();
+  for (int r = tid; r < rows; r += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < nwarps; ++w) s += rowsm[r][w];
+    rowpart[(int64_t)blockIdx.x * n + r0 + r] = s;
+  }
+}
+
+// scalar path (any C / alignment): rows by warps, columns by threads
+template <int MODE, typename XT>
+__device__ __forceinline__ float target_at(const XT *x, const float *base, const float *aux, int64_t e) {
+  const float xx = Act<XT>::load1(x + e);
+  float bb = 0.f, aa = 0.f;
+  if constexpr (MODE == CC_WITH_FEEDBACK) bb = base[e];
+  if constexpr (MODE != CC_NAIVE) aa = aux[e];
+  return target_of<MODE>(xx, bb, aa);
+}
+
+template <int MODE, typename XT>
+__global__ void k_scale_rows_scalar(const XT *__restrict__ x, const float *__restrict__ base,
+                                    const float *__restrict__ aux, int64_t n, int64_t C,
+                                    double *__restrict__ rowpart) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n) return;
+  double acc = 0.0;
+  for (int64_t j = lane; j < C; j += 32) acc += fabs((double)target_at<MODE, XT>(x, base, aux, i * C + j));
+  acc = warp_sum(acc);
+  if (lane == 0) rowpart[i] = acc;
+}
+
+template <int MODE, typename XT>
+__global__ void k_scale_cols_scalar(const XT *__restrict__ x, const float *__restrict__ base,
+                                    const float *__restrict__ aux, int64_t n, int64_t C,
+                                    double *__restrict__ colpart) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= C) return;
+  double acc = 0.0;
+  for (int64_t i = 0; i < n; ++i) acc += fabs((double)target_at<MODE, XT>(x, base, aux, i * C + j));
+  colpart[j] = acc;
+}
+
+// ===========================================================================
+// finalize: partials -> u, v (f32) in scratch and in the body
+// ===========================================================================
+__device__ __forceinline__ double block_tree_sum(double v, double *sm) {
+  // fixed pairing: deterministic for a given blockDim
+  sm[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = blockDim.x >> 1; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sm[threadIdx.x] += sm[threadIdx.x + s];
+    __syncthreads();
+  }
+  return sm[0];
+}
+
+__global__ void __launch_bounds__(kFinThreads) k_scale_fin1(int64_t n, int64_t C, int nRB, int nStrips,
+                                                            const double *__restrict__ colpart,
+                                                            const double *__restrict__ rowpart,
+                                                            double *__restrict__ rowsum, double *__restrict__ blkpart,
+                                                            float *__restrict__ vout, uint8_t *body_v, int scale_mode) {
+  __shared__ double sm[kFinThreads];
+  const int64_t ncolblk = cdiv_dev(C, kFinThreads);
+  if ((int64_t)blockIdx.x < ncolblk) {
+    const int64_t j = (int64_t)blockIdx.x * kFinThreads + threadIdx.x;
+    if (j < C) {
+      double s = 0.0;
+      for (int rb = 0; rb < nRB; ++rb) s += colpart[(int64_t)rb * C + j];
+      float v = (float)(s / (double)n);  // colmean (cx:148)
+      if (scale_mode == CC_SCALE_PER_TOKEN) v = 1.0f;
+      vout[j] = v;
+      store_f32_bytes(body_v + 4 * j, v);
+    }
+    return;
+  }
+  const int64_t b = blockIdx.x - ncolblk;
+  const int64_t i = b * kFinThreads + threadIdx.x;
+  double rs = 0.0;
+  if (i < n) {
+    for (int s = 0; s < nStrips; ++s) rs += rowpart[(int64_t)s * n + i];
+    rowsum[i] = rs;
+  }
+  const double tot = block_tree_sum(rs, sm);
+  if (threadIdx.x == 0) blkpart[b] = tot;
+}
+
+__global__ void __launch_bounds__(kFinThreads) k_scale_fin2(int64_t n, int64_t C, int nblk,
+                                                            const double *__restrict__ blkpart,
+                                                            const double *__restrict__ rowsum,
+                                                            float *__restrict__ uout, uint8_t *body_u,
+                                                            float *__restrict__ vout, uint8_t *body_v, int scale_mode) {
+  __shared__ double g_sm;
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int b = 0; b < nblk; ++b) tot += blkpart[b];
+    g_sm = tot / (double)(n * C);  // mean|t| (cx:142)
+  }
+  __syncthreads();
+  const double g = g_sm;
+  const int64_t i = (int64_t)blockIdx.x * kFinThreads + threadIdx.x;
+  if (i < n) {
+    float u;
+    if (scale_mode == CC_SCALE_PER_CHANNEL) {
+      u = 1.0f;
+    } else if (scale_mode == CC_SCALE_PER_TOKEN) {
+      u = (float)(rowsum[i] / (double)C);
+    } else if (g == 0.0) {
+      u = 1.0f;  // all-zero input (cx:143-146)
+    } else {
+      u = (float)fmax((rowsum[i] / (double)C) / g, kRowScaleFloor);  // cx:147
+    }
+    uout[i] = u;
+    store_f32_bytes(body_u + 4 * i, u);
+  }
+  (void)vout;
+  (void)body_v;
+}
+
+// ===========================================================================
+// pass B: quantize + pack + state update + record partials
+// ===========================================================================
+template <int CODEC>
+__device__ __forceinline__ void code_and_value(float t, double s, double thr, uint32_t &code, float &d) {
+  if constexpr (CODEC == CC_SIGN1) {
+    code = t < 0.0f ? 1u : 0u;  // (x < 0): -0.0 -> 0 (cx:375)
+    d = (float)(code ? -s : s);
+  } else if constexpr (CODEC == CC_QUANT2) {
+    code = quant2_code(t, s, thr);
+    d = (float)(quant2_level(code) * s);
+  } else {
+    code = quant4_code(t, s);
+    d = (float)(quant4_level(code) * s);
+  }
+}
+
+template <int MODE, int CODEC, typename XT>
+__global__ void __launch_bounds__(256) k_quant_vec(const XT *__restrict__ x, float *__restrict__ base,
+                                                   float *__restrict__ aux, int64_t n, int64_t C, int RB,
+                                                   const float *__restrict__ uu, const float *__restrict__ vv,
+                                                   uint8_t *__restrict__ codes, double *__restrict__ recpart) {
+  __shared__ double sm_err[32], sm_tsq[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + tid) * 4;
+  const bool active = j0 < C;
+  const int64_t r0 = (int64_t)blockIdx.y * RB;
+  const int rows = (int)(RB < n - r0 ? (int64_t)RB : n - r0);
+  double vd[4], v125[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    vd[q] = active ? (double)vv[j0 + q] : 0.0;
+    v125[q] = 1.25 * vd[q];  // exact: 24 + 3 bits
+  }
+  double err = 0.0, tsq = 0.0;
+
+  for (int rr = 0; rr < rows; rr += kRowsUnroll) {
+    float4 xv[kRowsUnroll], bv[kRowsUnroll], av[kRowsUnroll];
+    double ud[kRowsUnroll];
+#pragma unroll
+    for (int k = 0; k < kRowsUnroll; ++k) {
+      const bool rowok = (rr + k) < rows;
+      const bool ok = active && rowok;
+      const int64_t e = (r0 + rr + k) * C + j0;
+      ud[k] = rowok ? (double)uu[r0 + rr + k] : 0.0;
+      xv[k] = ok ? Act<XT>::load4(x + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if constexpr (MODE != CC_NAIVE) {
+        bv[k] = ok ? __ldcs(reinterpret_cast<const float4 *>(base + e)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        av[k] = ok ? __ldcs(reinterpret_cast<const float4 *>(aux + e)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kRowsUnroll; ++k) {
+      const bool ok = active && (rr + k) < rows;
+      const int64_t e = (r0 + rr + k) * C + j0;
+      float4 nb, na;
+      uint32_t packed = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float bb = 0.f, aa = 0.f;
+        if constexpr (MODE != CC_NAIVE) { bb = f4get(bv[k], q); aa = f4get(av[k], q); }
+        const float xx = f4get(xv[k], q);
+        const float t = target_of<MODE>(xx, bb, aa);
+        const double s = ud[k] * vd[q];
+        const double thr = ud[k] * v125[q];
+        uint32_t code;
+        float d;
+        code_and_value<CODEC>(t, s, thr, code, d);
+        if (ok) {
+          const double df = (double)d - (double)t;
+          err += df * df;
+          tsq += (double)t * (double)t;
+        }
+        packed |= code << (q * (CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4)));
+        if constexpr (MODE == CC_NAIVE) {
+          f4set(nb, q, d);
+        } else {
+          f4set(nb, q, __fadd_rn(bb, d));
+          f4set(na, q, MODE == CC_WITH_FEEDBACK ? __fsub_rn(t, d) : xx);
+        }
+      }
+      if (ok) {
+        __stcs(reinterpret_cast<float4 *>(base + e), nb);
+        if constexpr (MODE != CC_NAIVE) __stcs(reinterpret_cast<float4 *>(aux + e), na);
+      }
+      // code packing: flat element e (multiple of 4)
+      if constexpr (CODEC == CC_SIGN1) {
+        // 4 bits per lane; lanes (2m, 2m+1) form one byte (C % 8 == 0)
+        const uint32_t other = __shfl_down_sync(0xffffffffu, packed, 1);
+        if (ok && (lane & 1) == 0) codes[e >> 3] = (uint8_t)(packed | (other << 4));
+      } else if constexpr (CODEC == CC_QUANT2) {
+        if (ok) codes[e >> 2] = (uint8_t)packed;
+      } else {
+        if (ok) *reinterpret_cast<uint16_t *>(codes + (e >> 1)) = (uint16_t)packed;
+      }
+    }
+  }
+  err = warp_sum(err);
+  tsq = warp_sum(tsq);
+  if (lane == 0) { sm_err[warp] = err; sm_tsq[warp] = tsq; }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += sm_err[w]; b += sm_tsq[w]; }
+    const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+    recpart[2 * cta] = a;
+    recpart[2 * cta + 1] = b;
+  }
+}
+
+// scalar: one thread per code byte
+template <int MODE, int CODEC, typename XT>
+__global__ void __launch_bounds__(256) k_quant_scalar(const XT *__restrict__ x, float *__restrict__ base,
+                                                      float *__restrict__ aux, int64_t n, int64_t C,
+                                                      const float *__restrict__ uu, const float *__restrict__ vv,
+                                                      uint8_t *__restrict__ codes, double *__restrict__ recpart) {
+  __shared__ double sm[256];
+  constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
+  constexpr int per = 8 / bits;
+  const int64_t total = n * C;
+  const int64_t byte = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nbytes = (total * bits + 7) / 8;
+  double err = 0.0, tsq = 0.0;
+  if (byte < nbytes) {
+    uint32_t packed = 0;
+    for (int q = 0; q < per; ++q) {
+      const int64_t e = byte * per + q;
+      if (e >= total) break;
+      const int64_t i = e / C, j = e % C;
+      const float xx = Act<XT>::load1(x + e);
+      float bb = 0.f, aa = 0.f;
+      if constexpr (MODE != CC_NAIVE) { bb = base[e]; aa = aux[e]; }
+      const float t = target_of<MODE>(xx, bb, aa);
+      const double ud = (double)uu[i], vd = (double)vv[j];
+      uint32_t code;
+      float d;
+      code_and_value<CODEC>(t, ud * vd, ud * (1.25 * vd), code, d);
+      const double df = (double)d - (double)t;
+      err += df * df;
+      tsq += (double)t * (double)t;
+      packed |= code << (q * bits);
+      if constexpr (MODE == CC_NAIVE) {
+        base[e] = d;
+      } else {
+        base[e] = __fadd_rn(bb, d);
+        aux[e] = MODE == CC_WITH_FEEDBACK ? __fsub_rn(t, d) : xx;
+      }
+    }
+    codes[byte] = (uint8_t)packed;
+  }
+  const double a = block_tree_sum(err, sm);
+  __syncthreads();
+  const double b = block_tree_sum(tsq, sm);
+  if (threadIdx.x == 0) {
+    recpart[2 * blockIdx.x] = a;
+    recpart[2 * blockIdx.x + 1] = b;
+  }
+}
+
+__global__ void k_record_fin(int64_t nparts, const double *__restrict__ recpart, double *__restrict__ record) {
+  __shared__ double sm[256];
+  double a = 0.0, b = 0.0;
+  for (int64_t p = threadIdx.x; p < nparts; p += blockDim.x) {
+    a += recpart[2 * p];
+    b += recpart[2 * p + 1];
+  }
+  a = block_tree_sum(a, sm);
+  __syncthreads();
+  b = block_tree_sum(b, sm);
+  if (threadIdx.x == 0) {
+    record[0] = a;
+    record[1] = b;
+  }
+}
+
+// ===========================================================================
+// K2: decode + accumulate (batched over peers)
+// ===========================================================================
+constexpr int kMaxPeers = 64;
+struct PeerBatch {
+  const uint8_t *body[kMaxPeers];
+  float *base[kMaxPeers];
+  int64_t rows[kMaxPeers];
+};
+
+template <int CODEC>
+__device__ __forceinline__ uint32_t code_at(const uint8_t *codes, int64_t e) {
+  if constexpr (CODEC == CC_SIGN1) return (codes[e >> 3] >> (e & 7)) & 1u;
+  else if constexpr (CODEC == CC_QUANT2) return (codes[e >> 2] >> (2 * (e & 3))) & 3u;
+  else return (codes[e >> 1] >> (4 * (e & 1))) & 15u;
+}
+
+template <int CODEC>
+__device__ __forceinline__ float value_of(uint32_t code, double s) {
+  if constexpr (CODEC == CC_SIGN1) return (float)(code ? -s : s);
+  else if constexpr (CODEC == CC_QUANT2) return (float)(quant2_level(code) * s);
+  else return (float)(quant4_level(code) * s);
+}
+
+template <int CODEC, bool ACC>
+__global__ void __launch_bounds__(256) k_decode_vec(const __grid_constant__ PeerBatch pb, int64_t C, int RB) {
+  constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
+  const int peer = blockIdx.z;
+  const int64_t n = pb.rows[peer];
+  const int64_t r0 = (int64_t)blockIdx.y * RB;
+  if (r0 >= n) return;
+  const uint8_t *codes = pb.body[peer];
+  float *base = pb.base[peer];
+  const int64_t cbytes = (n * C * bits + 7) / 8;
+  const uint8_t *ub = codes + cbytes;
+  const uint8_t *vb = ub + 4 * n;
+  const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (j0 >= C) return;
+  const int rows = (int)(RB < n - r0 ? (int64_t)RB : n - r0);
+  double vd[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) vd[q] = (double)load_f32_bytes(vb + 4 * (j0 + q));
+  for (int rr = 0; rr < rows; rr += kRowsUnroll) {
+    float4 bv[kRowsUnroll];
+    uint32_t cw[kRowsUnroll];
+    double ud[kRowsUnroll];
+#pragma unroll
+    for (int k = 0; k < kRowsUnroll; ++k) {
+      const bool ok = (rr + k) < rows;
+      const int64_t i = r0 + rr + k;
+      const int64_t e = i * C + j0;
+      if (ACC) bv[k] = ok ? *reinterpret_cast<const float4 *>(base + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      ud[k] = ok ? (double)load_f32_bytes(ub + 4 * i) : 0.0;
+      if (!ok) { cw[k] = 0; continue; }
+      if constexpr (CODEC == CC_SIGN1) cw[k] = (codes[e >> 3] >> (e & 7)) & 0xfu;
+      else if constexpr (CODEC == CC_QUANT2) cw[k] = codes[e >> 2];
+      else cw[k] = *reinterpret_cast<const uint16_t *>(codes + (e >> 1));
+    }
+#pragma unroll
+    for (int k = 0; k < kRowsUnroll; ++k) {
+      if ((rr + k) >= rows) break;
+      const int64_t e = (r0 + rr + k) * C + j0;
+      float4 o;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t code = (cw[k] >> (q * bits)) & ((1u << bits) - 1u);
+        const float d = value_of<CODEC>(code, ud[k] * vd[q]);
+        f4set(o, q, ACC ? __fadd_rn(f4get(bv[k], q), d) : d);
+      }
+      *reinterpret_cast<float4 *>(base + e) = o;
+    }
+  }
+}
+
+template <int CODEC, bool ACC>
+__global__ void __launch_bounds__(256) k_decode_scalar(const __grid_constant__ PeerBatch pb, int64_t C) {
+  constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
+  const int peer = blockIdx.y;
+  const int64_t n = pb.rows[peer];
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * C) return;
+  const uint8_t *codes = pb.body[peer];
+  const int64_t cbytes = (n * C * bits + 7) / 8;
+  const int64_t i = e / C, j = e % C;
+  const double s = (double)load_f32_bytes(codes + cbytes + 4 * i) * (double)load_f32_bytes(codes + cbytes + 4 * n + 4 * j);
+  const float d = value_of<CODEC>(code_at<CODEC>(codes, e), s);
+  float *base = pb.base[peer];
+  base[e] = ACC ? __fadd_rn(base[e], d) : d;
+}
+
+// ===========================================================================
+// warmup / raw
+// ===========================================================================
+template <typename XT, int MODE, int BT>
+__global__ void __launch_bounds__(256) k_warmup(const XT *__restrict__ x, float *__restrict__ base,
+                                                float *__restrict__ aux, void *__restrict__ body, int64_t total) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const float xx = Act<XT>::load1(x + e);
+    base[e] = xx;
+    if constexpr (MODE == CC_WITH_FEEDBACK) aux[e] = 0.0f;
+    if constexpr (MODE == CC_NO_FEEDBACK) aux[e] = xx;
+    if constexpr (BT == CC_F32) reinterpret_cast<float *>(body)[e] = xx;
+    else reinterpret_cast<__nv_bfloat16 *>(body)[e] = reinterpret_cast<const __nv_bfloat16 *>(x)[e];
+  }
+}
+
+template <int MODE, int BT>
+__global__ void __launch_bounds__(256) k_warmup_vec(const void *__restrict__ xin, int xbf16, float *__restrict__ base,
+                                                    float *__restrict__ aux, void *__restrict__ body, int64_t nvec) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
+    float4 xv;
+    uint2 raw = make_uint2(0, 0);
+    if (xbf16) {
+      raw = reinterpret_cast<const uint2 *>(xin)[v];
+      xv = make_float4(__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xffff0000u),
+                       __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xffff0000u));
+    } else {
+      xv = reinterpret_cast<const float4 *>(xin)[v];
+    }
+    reinterpret_cast<float4 *>(base)[v] = xv;
+    if constexpr (MODE == CC_WITH_FEEDBACK) reinterpret_cast<float4 *>(aux)[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (MODE == CC_NO_FEEDBACK) reinterpret_cast<float4 *>(aux)[v] = xv;
+    if constexpr (BT == CC_F32) reinterpret_cast<float4 *>(body)[v] = xv;
+    else reinterpret_cast<uint2 *>(body)[v] = raw;
+  }
+}
+
+template <int BT>
+__global__ void __launch_bounds__(256) k_raw_decode(const __grid_constant__ PeerBatch pb, int64_t C) {
+  const int peer = blockIdx.y;
+  const int64_t total = pb.rows[peer] * C;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  float *base = pb.base[peer];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    if constexpr (BT == CC_F32) base[e] = reinterpret_cast<const float *>(pb.body[peer])[e];
+    else base[e] = __uint_as_float(((uint32_t)reinterpret_cast<const uint16_t *>(pb.body[peer])[e]) << 16);
+  }
+}
+
+// ===========================================================================
+// host launchers
+// ===========================================================================
+template <int MODE, typename XT>
+static void launch_scale(const QPlan &p, const XT *x, const float *base, const float *aux, cudaStream_t st) {
+  if (p.vec) {
+    dim3 grid(p.nStrips, p.nRB);
+    k_scale_vec<MODE, XT><<<grid, p.threads, 0, st>>>(x, base, aux, p.n, p.C, p.RB, p.colpart, p.rowpart);
+    count_launch();
+  } else {
+    k_scale_rows_scalar<MODE, XT><<<(unsigned)cdiv(p.n, 8), 256, 0, st>>>(x, base, aux, p.n, p.C, p.rowpart);
+    k_scale_cols_scalar<MODE, XT><<<(unsigned)cdiv(p.C, 256), 256, 0, st>>>(x, base, aux, p.n, p.C, p.colpart);
+    count_launch(2);
+  }
+}
+
+template <int MODE, int CODEC, typename XT>
+static void launch_quant(const QPlan &p, const XT *x, float *base, float *aux, uint8_t *codes, int64_t nrec,
+                         cudaStream_t st) {
+  if (p.vec) {
+    dim3 grid(p.nStrips, p.nRB);
+    k_quant_vec<MODE, CODEC, XT><<<grid, p.threads, 0, st>>>(x, base, aux, p.n, p.C, p.RB, p.u, p.v, codes,
+                                                             p.recpart);
+  } else {
+    k_quant_scalar<MODE, CODEC, XT><<<(unsigned)nrec, 256, 0, st>>>(x, base, aux, p.n, p.C, p.u, p.v, codes,
+                                                                     p.recpart);
+  }
+  count_launch();
+}
+
+template <int MODE, typename XT>
+static int encode_typed(int codec, int scale_mode, int64_t n, int64_t C, const XT *x, float *base, float *aux,
+                        uint8_t *body, void *ws, int64_t ws_bytes, double *record, cudaStream_t st) {
+  const int bits = codec_bits(codec);
+  const uintptr_t xa = sizeof(XT) == 4 ? 16 : 8;
+  bool vec = (C % 8 == 0) && aligned(x, xa) && aligned(base, 16) && (aux == nullptr || aligned(aux, 16)) &&
+             aligned(body, 2);
+  QPlan p;
+  plan_shape(p, n, C, vec);
+  const int64_t nrec_scalar = scalar_quant_ctas(n, C, bits);
+  size_t need = carve(p, nullptr, nrec_scalar);
+  if ((int64_t)need > ws_bytes) {
+    set_error("workspace too small");
+    return CC_ERR_ARG;
+  }
+  carve(p, ws, nrec_scalar);
+  const int64_t cbytes = cdiv(n * C * bits, 8);
+  uint8_t *body_u = body + cbytes;
+  uint8_t *body_v = body_u + 4 * n;
+
+  launch_scale<MODE, XT>(p, x, base, aux, st);
+  const int nF1 = (int)(cdiv(C, kFinThreads) + p.nblk_rows);
+  k_scale_fin1<<<nF1, kFinThreads, 0, st>>>(n, C, p.nRB, p.nStrips, p.colpart, p.rowpart, p.rowsum, p.blkpart, p.v,
+                                            body_v, scale_mode);
+  k_scale_fin2<<<p.nblk_rows, kFinThreads, 0, st>>>(n, C, p.nblk_rows, p.blkpart, p.rowsum, p.u, body_u, p.v,
+                                                    body_v, scale_mode);
+  count_launch(2);
+  if (codec == CC_SIGN1) launch_quant<MODE, CC_SIGN1, XT>(p, x, base, aux, body, nrec_scalar, st);
+  else if (codec == CC_QUANT2) launch_quant<MODE, CC_QUANT2, XT>(p, x, base, aux, body, nrec_scalar, st);
+  else launch_quant<MODE, CC_QUANT4, XT>(p, x, base, aux, body, nrec_scalar, st);
+  const int64_t nparts = p.vec ? p.ncta_b : nrec_scalar;
+  k_record_fin<<<1, 256, 0, st>>>(nparts, p.recpart, record);
+  count_launch();
+  return cuda_status("quant_encode_step");
+}
+
+int quant_encode_step(int codec, int mode, int scale_mode, int64_t n, int64_t C, const void *x, int x_dtype,
+                      float *base, float *aux, uint8_t *body, void *ws, int64_t ws_bytes, double *record,
+                      cudaStream_t st) {
+#define CC_DISPATCH_MODE(XT)                                                                                   \
+  switch (mode) {                                                                                              \
+    case CC_NAIVE:                                                                                             \
+      return encode_typed<CC_NAIVE, XT>(codec, scale_mode, n, C, (const XT *)x, base, aux, body, ws, ws_bytes, \
+                                        record, st);                                                           \
+    case CC_NO_FEEDBACK:                                                                                       \
+      return encode_typed<CC_NO_FEEDBACK, XT>(codec, scale_mode, n, C, (const XT *)x, base, aux, body, ws,     \
+                                              ws_bytes, record, st);                                           \
+    case CC_WITH_FEEDBACK:                                                                                     \
+      return encode_typed<CC_WITH_FEEDBACK, XT>(codec, scale_mode, n, C, (const XT *)x, base, aux, body, ws,   \
+                                                ws_bytes, record, st);                                         \
+  }
+  if (x_dtype == CC_F32) {
+    CC_DISPATCH_MODE(float)
+  } else {
+    CC_DISPATCH_MODE(__nv_bfloat16)
+  }
+#undef CC_DISPATCH_MODE
+  return CC_ERR_ARG;
+}
+
+template <int CODEC, bool ACC>
+static void launch_decode(const PeerBatch &pb, int count, int64_t maxrows, int64_t C, bool vec, cudaStream_t st) {
+  if (vec) {
+    QPlan p;
+    plan_shape(p, maxrows, C, true);
+    dim3 grid(p.nStrips, p.nRB, count);
+    k_decode_vec<CODEC, ACC><<<grid, p.threads, 0, st>>>(pb, C, p.RB);
+  } else {
+    dim3 grid((unsigned)cdiv(maxrows * C, 256), count);
+    k_decode_scalar<CODEC, ACC><<<grid, 256, 0, st>>>(pb, C);
+  }
+  count_launch();
+}
+
+int quant_decode(int codec, int accumulate, int count, const int64_t *rows, int64_t C, const uint8_t *const *bodies,
+                 float *const *bases, cudaStream_t st) {
+  const int bits = codec_bits(codec);
+  for (int c0 = 0; c0 < count; c0 += kMaxPeers) {
+    const int cnt = std::min(kMaxPeers, count - c0);
+    PeerBatch pb{};
+    int64_t maxrows = 0;
+    bool vec = (C % 8 == 0);
+    for (int i = 0; i < cnt; ++i) {
+      pb.body[i] = bodies[c0 + i];
+      pb.base[i] = bases[c0 + i];
+      pb.rows[i] = rows[c0 + i];
+      maxrows = std::max(maxrows, rows[c0 + i]);
+      vec = vec && aligned(bases[c0 + i], 16) && aligned(bodies[c0 + i], bits == 4 ? 2 : 1);
+    }
+    if (maxrows == 0) continue;
+#define CC_DEC(CD)                                                         \
+  if (accumulate) launch_decode<CD, true>(pb, cnt, maxrows, C, vec, st);   \
+  else launch_decode<CD, false>(pb, cnt, maxrows, C, vec, st);
+    if (codec == CC_SIGN1) { CC_DEC(CC_SIGN1) }
+    else if (codec == CC_QUANT2) { CC_DEC(CC_QUANT2) }
+    else { CC_DEC(CC_QUANT4) }
+#undef CC_DEC
+  }
+  return cuda_status("quant_decode");
+}
+
+int raw_warmup(int mode, int64_t n, int64_t C, const void *x, int x_dtype, float *base, float *aux, void *body,
+               int body_dtype, double *record, cudaStream_t st) {
+  const int64_t total = n * C;
+  const bool xbf = x_dtype == CC_BF16;
+  const bool vec = total % 4 == 0 && aligned(x, xbf ? 8 : 16) && aligned(base, 16) &&
+                   (aux == nullptr || aligned(aux, 16)) && aligned(body, body_dtype == CC_F32 ? 16 : 8);
+  const int threads = 256;
+  const int64_t items = vec ? total / 4 : total;
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(items, threads), sm_count() * 8));
+#define CC_WU(MODE, BT)                                                                                        \
+  if (vec) k_warmup_vec<MODE, BT><<<blocks, threads, 0, st>>>(x, xbf, base, aux, body, total / 4);             \
+  else if (xbf) k_warmup<__nv_bfloat16, MODE, BT><<<blocks, threads, 0, st>>>((const __nv_bfloat16 *)x, base, aux, body, total); \
+  else k_warmup<float, MODE, BT><<<blocks, threads, 0, st>>>((const float *)x, base, aux, body, total);
+  if (body_dtype == CC_F32) {
+    if (mode == CC_WITH_FEEDBACK) { CC_WU(CC_WITH_FEEDBACK, CC_F32) }
+    else if (mode == CC_NO_FEEDBACK) { CC_WU(CC_NO_FEEDBACK, CC_F32) }
+    else { CC_WU(CC_NAIVE, CC_F32) }
+  } else {
+    if (mode == CC_WITH_FEEDBACK) { CC_WU(CC_WITH_FEEDBACK, CC_BF16) }
+    else if (mode == CC_NO_FEEDBACK) { CC_WU(CC_NO_FEEDBACK, CC_BF16) }
+    else { CC_WU(CC_NAIVE, CC_BF16) }
+  }
+#undef CC_WU
+  count_launch();
+  if (record) {
+    cudaMemsetAsync(record, 0, 2 * sizeof(double), st);  // compression_error = 0 -> delta_hat = 1 (pl:115-120)
+  }
+  return cuda_status("raw_warmup");
+}
+
+int raw_decode(int count, const int64_t *rows, int64_t C, const void *const *bodies, int body_dtype,
+               float *const *bases, cudaStream_t st) {
+  for (int c0 = 0; c0 < count; c0 += kMaxPeers) {
+    const int cnt = std::min(kMaxPeers, count - c0);
+    PeerBatch pb{};
+    int64_t maxrows = 0;
+    for (int i = 0; i < cnt; ++i) {
+      pb.body[i] = reinterpret_cast<const uint8_t *>(bodies[c0 + i]);
+      pb.base[i] = bases[c0 + i];
+      pb.rows[i] = rows[c0 + i];
+      maxrows = std::max(maxrows, rows[c0 + i]);
+    }
+    const unsigned bx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(maxrows * C, 256), sm_count() * 4));
+    dim3 grid(bx, cnt);
+    if (body_dtype == CC_F32) k_raw_decode<CC_F32><<<grid, 256, 0, st>>>(pb, C);
+    else k_raw_decode<CC_BF16><<<grid, 256, 0, st>>>(pb, C);
+    count_launch();
+  }
+  return cuda_status("raw_decode");
+}
+
+}  // namespace cc
