@@ -158,6 +158,9 @@ CC_API const char *cc_last_error(void);
 CC_API int cc_version(void);
 /* number of kernels this library launched since load (evidence counter) */
 CC_API int64_t cc_launch_count(void);
+/* encode-path selection for tests/benchmarks: -1 auto (persistent fused K1
+ * when C % 1024 == 0 and aligned), 0 force the multi-kernel K1, 1 prefer fused */
+CC_API void cc_set_quant_path(int path);
 
 #ifdef __cplusplus
 }

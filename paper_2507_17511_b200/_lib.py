@@ -43,6 +43,7 @@ SIGNATURES = {
     "cc_last_error": (ctypes.c_char_p, []),
     "cc_version": (_i32, []),
     "cc_launch_count": (_i64, []),
+    "cc_set_quant_path": (None, [_i32]),
 }
 
 _LIB = None

@@ -102,13 +102,15 @@ static int64_t scalar_quant_ctas(int64_t n, int64_t C, int bits) {
   return cdiv(nbytes, 256);
 }
 
+int64_t fused_workspace_bytes(int64_t n, int64_t C);
+
 int64_t quant_workspace_bytes(int64_t n, int64_t C) {
   QPlan a, s;
   plan_shape(a, n, C, true);
   size_t wa = carve(a, nullptr, 0);
   plan_shape(s, n, C, false);
   size_t wsb = carve(s, nullptr, scalar_quant_ctas(n, C, 1));
-  return (int64_t)std::max(wa, wsb);
+  return std::max<int64_t>((int64_t)std::max(wa, wsb), fused_workspace_bytes(n, C));
 }
 
 // ===========================================================================
@@ -662,9 +664,19 @@ static int encode_typed(int codec, int scale_mode, int64_t n, int64_t C, const X
   return cuda_status("quant_encode_step");
 }
 
+bool fused_supported(int64_t n, int64_t C, const void *x, int x_dtype, const float *base, const float *aux,
+                     const uint8_t *body);
+int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, const void *x, int x_dtype, float *base,
+                 float *aux, uint8_t *body, void *ws, int64_t ws_bytes, double *record, cudaStream_t st);
+int64_t fused_workspace_bytes(int64_t n, int64_t C);
+static int g_force_path = -1;  // -1 auto, 0 multi-kernel, 1 fused (tests / benchmarks)
+void set_quant_path(int v) { g_force_path = v; }
+
 int quant_encode_step(int codec, int mode, int scale_mode, int64_t n, int64_t C, const void *x, int x_dtype,
                       float *base, float *aux, uint8_t *body, void *ws, int64_t ws_bytes, double *record,
                       cudaStream_t st) {
+  if (g_force_path != 0 && fused_supported(n, C, x, x_dtype, base, aux, body))
+    return fused_encode(codec, mode, scale_mode, n, C, x, x_dtype, base, aux, body, ws, ws_bytes, record, st);
 #define CC_DISPATCH_MODE(XT)                                                                                   \
   switch (mode) {                                                                                              \
     case CC_NAIVE:                                                                                             \

@@ -336,3 +336,50 @@ def test_kernels_really_launch():
     n0 = _lib.load().cc_launch_count()
     cx.encode_quant2bit(torch.randn(64, 256, device="cuda"))
     assert _lib.load().cc_launch_count() - n0 >= 4
+
+
+# --------------------------------------------------------------------------
+# the persistent fused K1 (C % 1024 == 0) against the multi-kernel K1 and the oracle
+# --------------------------------------------------------------------------
+
+@pytest.fixture
+def quant_path():
+    from paper_2507_17511_b200 import _lib
+
+    lib = _lib.load()
+    yield lib.cc_set_quant_path
+    lib.cc_set_quant_path(-1)
+
+
+@pytest.mark.parametrize("shape", [(1, 1024), (3, 2048), (64, 3072), (513, 3072), (2048, 3072), (7, 4096)],
+                         ids=lambda s: f"{s[0]}x{s[1]}")
+@pytest.mark.parametrize("codec", QUANT_CODECS + ("quant4bit",))
+@pytest.mark.parametrize("mode", ["naive", "residual_no_feedback", "residual_with_feedback"])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32], ids=["bf16", "f32"])
+def test_fused_k1_matches_multikernel_and_oracle(shape, codec, mode, dtype, quant_path):
+    cx, pl = _mods()
+    n, c = shape
+    xs = _flux_torch(n, c, 4, seed=n * 7 + c)
+    states = {}
+    bodies = {}
+    for path in (0, 1):
+        quant_path(path)
+        st = pl.LayerState(mode, 1, torch.zeros(n, c, device="cuda"))
+        bl = []
+        for x in xs:
+            p, rec = pl.encode_step(st, x.to(dtype), _spec(codec))
+            bl.append((p.body_bytes(), rec.compression_error))
+        states[path] = st
+        bodies[path] = bl
+    for (b0, e0), (b1, e1) in zip(bodies[0], bodies[1]):
+        assert b0 == b1
+        assert e1 == pytest.approx(e0, rel=1e-6, abs=1e-30)
+    assert torch.equal(states[0].base, states[1].base)
+    if mode == "residual_with_feedback":
+        assert torch.equal(states[0].feedback, states[1].feedback)
+    if codec != "quant4bit" and n <= 513:
+        och = O.Channel(mode, 1, np.zeros((n, c), np.float32))
+        for x, (b1, _) in zip(xs, bodies[1]):
+            _, body, _ = O.send(och, x.to(dtype).float().cpu().numpy(), O.Codec(_otag(codec)))
+            assert b1 == body
+        assert np.array_equal(states[1].base.cpu().numpy(), och.base)
