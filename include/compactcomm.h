@@ -144,6 +144,14 @@ CC_API int cc_encode(int codec, int scale_mode, int64_t rows, int64_t cols, int6
 CC_API int64_t cc_topk_count(int64_t rows, int64_t cols, double keep_fraction);
 CC_API int cc_topk_encode(int64_t rows, int64_t cols, int64_t k, const float *t, uint8_t *body,
                           float *decoded, void *workspace, int64_t workspace_bytes, void *stream);
+/* Fused top-k sender step: target -> radix select -> ordered body -> sparse
+ * state update + record, straight from (x, base, aux).  Receivers decode with
+ * cc_decode_step(CC_TOPK, accumulate, ..., param = k): accumulate 0 = replace
+ * (zero + scatter), 1 = sparse add, 2 = dense `base + 0.0` (-0.0 -> +0.0, the
+ * reference's dense add, pl:163) then sparse add. */
+CC_API int cc_topk_encode_step(int mode, int64_t rows, int64_t cols, int64_t k, const void *x, int x_dtype,
+                               float *base, float *aux, uint8_t *body, void *workspace,
+                               int64_t workspace_bytes, double *record, void *stream);
 
 /* ---- low-rank (cx:394-426) -------------------------------------------------
  * q0: [cols, r] f32 initial Gaussian block (drawn host-side from the same

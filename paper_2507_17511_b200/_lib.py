@@ -38,6 +38,7 @@ SIGNATURES = {
     "cc_encode": (_i32, [_i32, _i32, _i64, _i64, _i64, _p, _p, _p, _p, _i64, _p]),
     "cc_topk_count": (_i64, [_i64, _i64, _d]),
     "cc_topk_encode": (_i32, [_i64, _i64, _i64, _p, _p, _p, _p, _i64, _p]),
+    "cc_topk_encode_step": (_i32, [_i32, _i64, _i64, _i64, _p, _i32, _p, _p, _p, _p, _i64, _p, _p]),
     "cc_lowrank_encode": (_i32, [_i32, _i64, _i64, _i64, _i32, _p, _p, _p, _p, _p, _i64, _p]),
     "cc_lowrank_workspace_bytes": (_i64, [_i64, _i64, _i64]),
     "cc_last_error": (ctypes.c_char_p, []),

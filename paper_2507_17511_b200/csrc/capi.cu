@@ -44,6 +44,8 @@ int sm_count() {
 int64_t topk_workspace_bytes(int64_t n, int64_t C, int64_t k);
 int topk_encode(int64_t n, int64_t C, int64_t k, const float *t, uint8_t *body, float *decoded, void *ws,
                 int64_t ws_bytes, cudaStream_t st);
+int topk_encode_step(int mode, int64_t n, int64_t C, int64_t k, const void *x, int x_dtype, float *base, float *aux,
+                     uint8_t *body, void *ws, int64_t ws_bytes, double *record, cudaStream_t st);
 int topk_decode(int count, const int64_t *rows, int64_t C, int64_t k, const uint8_t *const *bodies, int accumulate,
                 float *const *bases, cudaStream_t st);
 int64_t lowrank_workspace_bytes(int64_t n, int64_t C, int64_t r);
@@ -176,6 +178,20 @@ CC_API int cc_topk_encode(int64_t rows, int64_t cols, int64_t k, const float *t,
   if (k < 0 || k > rows * cols || !t || !body) { set_error("bad top-k args"); return CC_ERR_ARG; }
   if (rows * cols > (int64_t)UINT32_MAX) { set_error("top-k indices are u32"); return CC_ERR_SHAPE; }
   return topk_encode(rows, cols, k, t, body, decoded, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+CC_API int cc_topk_encode_step(int mode, int64_t rows, int64_t cols, int64_t k, const void *x, int x_dtype,
+                               float *base, float *aux, uint8_t *body, void *workspace, int64_t workspace_bytes,
+                               double *record, void *stream) {
+  if (rows < 1 || cols < 1) { set_error("empty shape"); return CC_ERR_SHAPE; }
+  if (!valid_mode(mode) || (x_dtype != CC_F32 && x_dtype != CC_BF16)) { set_error("bad mode/dtype"); return CC_ERR_ARG; }
+  if (k < 1 || k > rows * cols || !x || !base || !body || !record || (mode != CC_NAIVE && !aux)) {
+    set_error("bad top-k step args");
+    return CC_ERR_ARG;
+  }
+  if (rows * cols > (int64_t)UINT32_MAX) { set_error("top-k indices are u32"); return CC_ERR_SHAPE; }
+  return topk_encode_step(mode, rows, cols, k, x, x_dtype, base, aux, body, workspace, workspace_bytes, record,
+                          (cudaStream_t)stream);
 }
 
 CC_API int64_t cc_lowrank_workspace_bytes(int64_t rows, int64_t cols, int64_t rank) {

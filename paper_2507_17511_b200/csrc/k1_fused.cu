@@ -34,10 +34,13 @@ namespace cg = cooperative_groups;
 namespace cc {
 namespace fused {
 
-constexpr int kConsumers = 256;  // 8 warps x 32 lanes x 4 columns = 1024-column strip
+constexpr int kGroupThreads = 256;  // one row group: 8 warps x 32 lanes x 4 columns = 1024-column strip
+constexpr int kGroups = 2;          // row groups (alternate rows of a tile) -> 16 consumer warps
+constexpr int kGWarps = kGroupThreads / 32;
+constexpr int kConsumers = kGroups * kGroupThreads;
 constexpr int kCWarps = kConsumers / 32;
 constexpr int kThreads = kConsumers + 32;  // + producer warp
-constexpr int kStrip = 4 * kConsumers;
+constexpr int kStrip = 4 * kGroupThreads;
 constexpr int kRowsBuffered = 16;  // stages * rows-per-tile
 
 struct Params {
@@ -53,9 +56,22 @@ struct Params {
   int scale_mode;
 };
 
+// f32 state arrays staged per tile: base + aux (feedback or ref); naive mode none
 template <int MODE>
 constexpr int n_f32_arrays() {
-  return MODE == CC_WITH_FEEDBACK ? 2 : (MODE == CC_NO_FEEDBACK ? 1 : 0);
+  return MODE == CC_NAIVE ? 0 : 2;
+}
+
+// exact f32 -> f64 on the integer pipes for normal numbers and zero; the XU
+// conversion (F2F, quarter rate) only for subnormal / non-finite inputs
+__device__ __forceinline__ double f64_of(float a) {
+  const uint32_t b = __float_as_uint(a);
+  const uint32_t e = b & 0x7f800000u;
+  if (__builtin_expect(e == 0x7f800000u || (e == 0u && (b & 0x7fffffu) != 0u), 0)) return (double)a;
+  if (e == 0u) return __longlong_as_double((long long)((uint64_t)(b & 0x80000000u) << 32));
+  const uint64_t hi = ((uint64_t)(b & 0x80000000u) << 32) |
+                      ((((uint64_t)(b & 0x7fffffffu)) << 29) + ((uint64_t)(1023 - 127) << 52));
+  return __longlong_as_double((long long)hi);
 }
 
 // deterministic block sum over all kThreads threads (fixed pairing)
@@ -75,38 +91,79 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
   return s;
 }
 
+// exact slow path for one element (f64 scale math as in quant.cu)
+template <int CODEC>
+__device__ __noinline__ void quantize1_exact(float t, double ud, double vd, uint32_t &code, float &d) {
+  const double s = ud * vd;
+  if constexpr (CODEC == CC_QUANT2) {
+    code = quant2_code(t, s, ud * (1.25 * vd));
+    d = (float)(quant2_level(code) * s);
+  } else {
+    code = quant4_code(t, s);
+    d = (float)(quant4_level(code) * s);
+  }
+}
+
+// 4 elements of one row.  Fast path is pure f32: p = RN32(u v) (== f32(u64 v64)),
+// the 2-bit thresholds are classified against 1.25 p with a 2^-20 guard band on
+// either side (exact outside it), d = level * p (exact: power-of-two levels in
+// the normal range).  Elements in the guard band or with |p| outside
+// [2^-100, 2^100] take the exact f64 path (quantize1_exact).
 template <int CODEC>
 __device__ __forceinline__ void quantize4(const float (&t)[4], double ud, float uf, const double (&vd)[4],
-                                          const double (&v125)[4], const float (&vf)[4], uint32_t &packed,
-                                          float (&d)[4], double &err, double &tsq) {
+                                          const float (&vf)[4], uint32_t &packed, float (&d)[4]) {
   constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
   packed = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const double xd = (double)t[q];
-    const double s = ud * vd[q];
     uint32_t code;
+    const float p = __fmul_rn(uf, vf[q]);
     if constexpr (CODEC == CC_SIGN1) {
       code = t[q] < 0.0f ? 1u : 0u;
-      const float p = __fmul_rn(uf, vf[q]);  // RN32(u v) == f32(u64 v64)
       d[q] = code ? -p : p;
     } else if constexpr (CODEC == CC_QUANT2) {
-      const double thr = ud * v125[q];
-      code = s == 0.0 ? 2u : (xd > thr ? 3u : (xd < -thr ? 0u : (xd < 0.0 ? 1u : 2u)));
-      const float p = __fmul_rn(uf, vf[q]);
-      const float ap = fabsf(p);
-      const float lv = code == 0 ? -2.0f : (code == 1 ? -0.5f : (code == 2 ? 0.5f : 2.0f));
-      // power-of-two level: RN32(L u v) == L * RN32(u v) while both stay normal
-      d[q] = (ap >= 0x1p-124f && ap <= 0x1p+126f) ? lv * p : (float)(quant2_level(code) * s);
+      const float ap = fabsf(p), ax = fabsf(t[q]);
+      const float thr = __fmul_rn(ap, 1.25f);
+      const bool big = ax > __fmul_ru(thr, 1.00000095367431640625f);    // 1 + 2^-20
+      const bool small = ax < __fmul_rd(thr, 0.99999904632568359375f);  // 1 - 2^-20
+      const bool neg = t[q] < 0.0f;
+      code = big ? (neg ? 0u : 3u) : (neg ? 1u : 2u);
+      const float lv = big ? 2.0f : 0.5f;
+      d[q] = (neg ? -lv : lv) * p;
+      if (__builtin_expect(!(big || small) || !(ap >= 0x1p-100f && ap <= 0x1p+100f), 0))
+        quantize1_exact<CODEC>(t[q], ud, vd[q], code, d[q]);
     } else {
-      code = quant4_code(t[q], s);
-      d[q] = (float)(quant4_level(code) * s);
+      quantize1_exact<CODEC>(t[q], ud, vd[q], code, d[q]);
     }
     packed |= code << (q * bits);
+  }
+}
+
+// ||d - t||^2 and ||t||^2 of 4 elements: f32 quad sums (rel. err < 2^-21) added in
+// f64; quads with huge magnitudes are redone in f64
+__device__ __forceinline__ void record4(const float (&t)[4], const float (&d)[4], double &err, double &tsq) {
+  float e2 = 0.f, t2 = 0.f;
+  float mx = 0.f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
     const float e = __fsub_rn(t[q], d[q]);
-    const double ed = (double)e;
-    err += ed * ed;
-    tsq += xd * xd;
+    e2 = __fmaf_rn(e, e, e2);
+    t2 = __fmaf_rn(t[q], t[q], t2);
+    mx = fmaxf(mx, fmaxf(fabsf(e), fabsf(t[q])));
+  }
+  if (__builtin_expect(mx > 0x1p+60f || (mx < 0x1p-60f && mx > 0.f), 0)) {
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double e = (double)__fsub_rn(t[q], d[q]);
+      a += e * e;
+      b += (double)t[q] * (double)t[q];
+    }
+    err += a;
+    tsq += b;
+  } else {
+    err += f64_of(e2);
+    tsq += f64_of(t2);
   }
 }
 
@@ -121,14 +178,18 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   const int strip = cta % p.nStrips;
   const int64_t c0 = (int64_t)strip * kStrip;
   const int width = (int)min64(kStrip, C - c0);
+  const bool producer = warp == kCWarps;
+  const int grp = producer ? 0 : tid / kGroupThreads;  // consumer row group
+  const int gtid = tid % kGroupThreads;
+  const int gwarp = gtid >> 5;
 
   // ---- shared memory carve-up ----
   const size_t xs_bytes = (size_t)R * kStrip * sizeof(XT);
   const size_t fs_bytes = (size_t)R * kStrip * sizeof(float);
   const size_t stage_bytes = xs_bytes + NF * fs_bytes;
   uint8_t *tiles = smem;
-  double *rp = reinterpret_cast<double *>(smem + (size_t)S * stage_bytes);  // [S][R][kCWarps]
-  double *red = rp + (size_t)S * R * kCWarps;                                // [kThreads/32 + 1]
+  double *rp = reinterpret_cast<double *>(smem + (size_t)S * stage_bytes);  // [S][R][kGWarps]
+  double *red = rp + (size_t)S * R * kGWarps;                               // block-sum scratch
   uint64_t *full = reinterpret_cast<uint64_t *>(red + 64);
   uint64_t *empty = full + S;
 
@@ -147,47 +208,51 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   auto stage_x = [&](int s) { return reinterpret_cast<XT *>(tiles + (size_t)s * stage_bytes); };
   auto stage_b = [&](int s) { return reinterpret_cast<float *>(tiles + (size_t)s * stage_bytes + xs_bytes); };
   auto stage_a = [&](int s) {
-    return reinterpret_cast<float *>(tiles + (size_t)s * stage_bytes + xs_bytes + (NF == 2 ? fs_bytes : 0));
+    return reinterpret_cast<float *>(tiles + (size_t)s * stage_bytes + xs_bytes + fs_bytes);
+  };
+  auto finish_rows = [&](int s, int64_t k) {  // producer lanes: per-row sums over the 8 warps of a group
+    const int64_t r0p = tile_r0(k);
+    if (lane < R && r0p + lane < n) {
+      double acc = 0.0;
+      for (int w = 0; w < kGWarps; ++w) acc += rp[((size_t)s * R + lane) * kGWarps + w];
+      p.rowpart[(int64_t)strip * n + r0p + lane] = acc;
+    }
   };
 
   const XT *X = reinterpret_cast<const XT *>(p.x);
   // ---------------- producer warp ----------------
-  auto produce = [&](int64_t seq0, bool reverse, uint64_t policy, bool rowparts) {
+  // phaseB: stage base too in no-feedback mode (t only needs x - ref, the update needs base)
+  auto produce = [&](int64_t seq0, bool phaseB, uint64_t policy) {
     for (int64_t k = 0; k < K; ++k) {
       const int64_t seq = seq0 + k;
       const int s = (int)(seq % S);
       const int64_t use = seq / S;
       if (use > 0) {
         mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
-        if (rowparts && k >= S) {  // row partials of the phase-A tile that last used stage s
-          const int64_t r0p = tile_r0(k - S);
-          if (lane < R && r0p + lane < n) {
-            double acc = 0.0;
-            for (int w = 0; w < kCWarps; ++w) acc += rp[((size_t)s * R + lane) * kCWarps + w];
-            p.rowpart[(int64_t)strip * n + r0p + lane] = acc;
-          }
-        }
+        if (!phaseB && k >= S) finish_rows(s, k - S);
       }
       if (lane == 0) {
-        const int64_t kk = reverse ? (K - 1 - k) : k;
+        const int64_t kk = phaseB ? (K - 1 - k) : k;
         const int64_t r0 = tile_r0(kk);
         const int nrows = (int)min64(R, n - r0);
+        const bool need_base = MODE == CC_WITH_FEEDBACK || (MODE == CC_NO_FEEDBACK && phaseB);
         const uint32_t xrow = (uint32_t)(width * sizeof(XT)), frow = (uint32_t)(width * sizeof(float));
-        mbar_expect_tx(&full[s], (uint32_t)nrows * (xrow + NF * frow));
+        const uint32_t per = xrow + (need_base ? frow : 0u) + (NF ? frow : 0u);
+        mbar_expect_tx(&full[s], (uint32_t)nrows * per);
         for (int r = 0; r < nrows; ++r) {
           const int64_t e = (r0 + r) * C + c0;
           bulk_g2s(stage_x(s) + (size_t)r * kStrip, X + e, xrow, &full[s], policy);
-          if constexpr (NF == 2) bulk_g2s(stage_b(s) + (size_t)r * kStrip, p.base + e, frow, &full[s], policy);
-          if constexpr (NF >= 1) bulk_g2s(stage_a(s) + (size_t)r * kStrip, p.aux + e, frow, &full[s], policy);
+          if (need_base) bulk_g2s(stage_b(s) + (size_t)r * kStrip, p.base + e, frow, &full[s], policy);
+          if constexpr (NF) bulk_g2s(stage_a(s) + (size_t)r * kStrip, p.aux + e, frow, &full[s], policy);
         }
       }
       __syncwarp();
     }
   };
 
-  const int col = 4 * tid;  // consumer's first column inside the strip
-  const bool active = tid < kConsumers && col < width;
-  auto load_tile_row = [&](int s, int r, float (&xx)[4], float (&bb)[4], float (&aa)[4]) {
+  const int col = 4 * gtid;  // consumer's first column inside the strip
+  const bool active = !producer && col < width;
+  auto load_row = [&](int s, int r, float (&xx)[4], float (&bb)[4], float (&aa)[4], bool with_base) {
     if constexpr (sizeof(XT) == 2) {
       const uint2 raw = *reinterpret_cast<const uint2 *>(stage_x(s) + (size_t)r * kStrip + col);
       xx[0] = __uint_as_float(raw.x << 16);
@@ -198,29 +263,23 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       const float4 v = lds4(reinterpret_cast<const float *>(stage_x(s)) + (size_t)r * kStrip + col);
       xx[0] = v.x; xx[1] = v.y; xx[2] = v.z; xx[3] = v.w;
     }
-    if constexpr (NF == 2) {
+    if (NF && with_base) {
       const float4 v = lds4(stage_b(s) + (size_t)r * kStrip + col);
       bb[0] = v.x; bb[1] = v.y; bb[2] = v.z; bb[3] = v.w;
     }
-    if constexpr (NF >= 1) {
+    if constexpr (NF) {
       const float4 v = lds4(stage_a(s) + (size_t)r * kStrip + col);
       aa[0] = v.x; aa[1] = v.y; aa[2] = v.z; aa[3] = v.w;
     }
   };
 
   // ================= phase A: |t| partial sums =================
-  if (warp == kCWarps) {
-    produce(0, false, l2_policy_evict_last(), true);
-    // drain: row partials of the last min(S, K) tiles
-    for (int64_t k = K - min64(S, K); k < K; ++k) {
+  if (producer) {
+    produce(0, false, l2_policy_evict_last());
+    for (int64_t k = K - min64(S, K); k < K; ++k) {  // drain the last tiles' row sums
       const int s = (int)(k % S);
       mbar_wait(&empty[s], (uint32_t)((k / S) & 1));
-      const int64_t r0p = tile_r0(k);
-      if (lane < R && r0p + lane < n) {
-        double acc = 0.0;
-        for (int w = 0; w < kCWarps; ++w) acc += rp[((size_t)s * R + lane) * kCWarps + w];
-        p.rowpart[(int64_t)strip * n + r0p + lane] = acc;
-      }
+      finish_rows(s, k);
     }
   } else {
     double cs[4] = {0.0, 0.0, 0.0, 0.0};
@@ -229,25 +288,25 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       mbar_wait(&full[s], (uint32_t)((k / S) & 1));
       const int64_t r0 = tile_r0(k);
       const int nrows = (int)min64(R, n - r0);
-      for (int r = 0; r < nrows; ++r) {
-        float xx[4], bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int r = grp; r < nrows; r += kGroups) {
+        float xx[4] = {0.f, 0.f, 0.f, 0.f}, bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f};
         double a[4] = {0.0, 0.0, 0.0, 0.0};
         if (active) {
-          load_tile_row(s, r, xx, bb, aa);
+          load_row(s, r, xx, bb, aa, MODE == CC_WITH_FEEDBACK);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) a[q] = fabs((double)target_of<MODE>(xx[q], bb[q], aa[q]));
+          for (int q = 0; q < 4; ++q) a[q] = f64_of(fabsf(target_of<MODE>(xx[q], bb[q], aa[q])));
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) cs[q] += a[q];
         double rs = ((a[0] + a[1]) + a[2]) + a[3];
         rs = warp_sum(rs);
-        if (lane == 0) rp[((size_t)s * R + r) * kCWarps + warp] = rs;
+        if (lane == 0) rp[((size_t)s * R + r) * kGWarps + gwarp] = rs;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
     if (active) {
-      double *cp = p.colpart + (int64_t)(cta / p.nStrips) * C + c0 + col;
+      double *cp = p.colpart + (int64_t)((cta / p.nStrips) * kGroups + grp) * C + c0 + col;
       cp[0] = cs[0]; cp[1] = cs[1]; cp[2] = cs[2]; cp[3] = cs[3];
     }
   }
@@ -256,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   grid.sync();
 
   // ================= phase F1: column means, row sums =================
-  const int slots = G / p.nStrips;
+  const int slots = (G / p.nStrips) * kGroups;
   if (cta == 0 && tid == 0) *p.ticket = 0u;
   for (int64_t j = (int64_t)cta * kThreads + tid; j < C; j += (int64_t)G * kThreads) {
     double s = 0.0;
@@ -283,8 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
 
   // ================= phase F2: g and u =================
   {
-    const double part = tid < G ? __ldcg(p.blkpart + tid) : 0.0;
-    // G <= kThreads is guaranteed by the launcher
+    const double part = tid < G ? __ldcg(p.blkpart + tid) : 0.0;  // G <= kThreads (launcher)
     const double tot = block_sum(part, red);
     const double g = tot / (double)(n * C);
     for (int64_t i = i0 + tid; i < i1; i += kThreads) {
@@ -302,17 +360,15 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
 
   // ================= phase B: quantize, pack, update state =================
   double err = 0.0, tsq = 0.0;
-  if (warp == kCWarps) {
-    produce(K, true, l2_policy_evict_first(), false);
+  if (producer) {
+    produce(K, true, l2_policy_evict_first());
   } else {
-    constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
-    double vd[4], v125[4];
+    double vd[4];
     float vf[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       vf[q] = active ? __ldcg(p.v + c0 + col + q) : 0.0f;
       vd[q] = (double)vf[q];
-      v125[q] = 1.25 * vd[q];
     }
     for (int64_t k = 0; k < K; ++k) {
       const int64_t seq = K + k;
@@ -320,21 +376,19 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       mbar_wait(&full[s], (uint32_t)((seq / S) & 1));
       const int64_t r0 = tile_r0(K - 1 - k);
       const int nrows = (int)min64(R, n - r0);
-      for (int r = 0; r < nrows; ++r) {
+      for (int r = grp; r < nrows; r += kGroups) {
         const int64_t row = r0 + r;
         const float uf = __ldcg(p.u + row);
         const double ud = (double)uf;
         float xx[4] = {0.f, 0.f, 0.f, 0.f}, bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f};
-        if (active) load_tile_row(s, r, xx, bb, aa);
+        if (active) load_row(s, r, xx, bb, aa, true);
         float t[4], d[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) t[q] = target_of<MODE>(xx[q], bb[q], aa[q]);
         uint32_t packed = 0;
-        double e0 = 0.0, t0 = 0.0;
-        quantize4<CODEC>(t, ud, uf, vd, v125, vf, packed, d, e0, t0);
+        quantize4<CODEC>(t, ud, uf, vd, vf, packed, d);
         if (active) {
-          err += e0;
-          tsq += t0;
+          record4(t, d, err, tsq);
           const int64_t e = row * C + c0 + col;
           float4 nb, na;
           if constexpr (MODE == CC_NAIVE) {
@@ -359,7 +413,6 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
         } else {
           if (active) *reinterpret_cast<uint16_t *>(p.codes + ((row * C + c0 + col) >> 1)) = (uint16_t)packed;
         }
-        (void)bits;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -393,9 +446,9 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
 // host side
 // ---------------------------------------------------------------------------
 static size_t fused_smem(int mode, int xsize, int R, int S) {
-  const int NF = mode == CC_WITH_FEEDBACK ? 2 : (mode == CC_NO_FEEDBACK ? 1 : 0);
+  const int NF = mode == CC_NAIVE ? 0 : 2;
   const size_t stage = (size_t)R * fused::kStrip * (xsize + 4 * NF);
-  const size_t rp = (size_t)S * R * fused::kCWarps * sizeof(double);
+  const size_t rp = (size_t)S * R * fused::kGWarps * sizeof(double);
   const size_t red = 64 * sizeof(double);  // block-sum scratch
   return (size_t)S * stage + rp + red + 2 * S * sizeof(uint64_t) + 256;
 }
@@ -430,7 +483,7 @@ int64_t fused_workspace_bytes(int64_t n, int64_t C) {
   const int G = fused::kThreads;  // upper bound on the grid
   size_t b = 0;
   auto add = [&](size_t x) { b += align_up(x, 256); };
-  add(sizeof(double) * (size_t)G * C);  // colpart (slots <= G)
+  add(sizeof(double) * (size_t)G * fused::kGroups * C);  // colpart (slots <= G * groups)
   add(sizeof(double) * (size_t)cdiv(C, fused::kStrip) * n);
   add(sizeof(double) * n);
   add(sizeof(double) * G);
@@ -455,7 +508,7 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   G -= G % p.nStrips;
   if (G > fused::kThreads) G = fused::kThreads - (fused::kThreads % p.nStrips);
   const int64_t per1 = cdiv(n * p.nStrips, G);
-  p.R = per1 >= 32 ? 4 : (per1 >= 16 ? 2 : 1);
+  p.R = per1 >= 32 ? 4 : 2;
   p.S = fused::kRowsBuffered / p.R;
   p.G = G;
   p.nTiles = cdiv(n, p.R) * p.nStrips;
@@ -474,7 +527,7 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
     off = align_up(off + bytes, 256);
     return q;
   };
-  const int slots = G / p.nStrips;
+  const int slots = (G / p.nStrips) * fused::kGroups;
   p.colpart = reinterpret_cast<double *>(take(sizeof(double) * (size_t)slots * C));
   p.rowpart = reinterpret_cast<double *>(take(sizeof(double) * (size_t)p.nStrips * n));
   p.rowsum = reinterpret_cast<double *>(take(sizeof(double) * n));

@@ -4,15 +4,7 @@
 
 namespace cc {
 
-int64_t topk_workspace_bytes(int64_t, int64_t, int64_t) { return 0; }
-int topk_encode(int64_t, int64_t, int64_t, const float *, uint8_t *, float *, void *, int64_t, cudaStream_t) {
-  set_error("top-k not built");
-  return CC_ERR_UNSUPPORTED;
-}
-int topk_decode(int, const int64_t *, int64_t, int64_t, const uint8_t *const *, int, float *const *, cudaStream_t) {
-  set_error("top-k not built");
-  return CC_ERR_UNSUPPORTED;
-}
+
 int64_t lowrank_workspace_bytes(int64_t, int64_t, int64_t) { return 0; }
 int lowrank_encode(int, int64_t, int64_t, int64_t, int, const float *, const float *, uint8_t *, float *, void *,
                    int64_t, cudaStream_t) {

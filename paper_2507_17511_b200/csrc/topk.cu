@@ -1,0 +1,568 @@
+// K4: global top-k residual sparsifier (compressors.py:446-456) on sm_100a.
+//
+// Reference order: |v| descending, then flat index ascending (np.lexsort);
+// k = min(size, ceil(f * size)); indices emitted ascending as u32, values as
+// f16 (RNE, overflow -> inf).  Decode = dense zero + scatter (cx:358-361).
+//
+// Device algorithm (radix select on the f32 magnitude bits, key = bits & 0x7fffffff,
+// which orders exactly like |v| for finite values, +0 and -0 alike):
+//   pass H1  t = target(x, base, aux) written once (into the feedback buffer in
+//            residual_with_feedback mode, else into scratch), 4096-bin histogram
+//            of key[30:19] in shared memory -> global; ||t||^2 partials.
+//   find     one CTA: suffix scan of the histogram -> bin b1, remaining need
+//   pass H2  keys in bin b1: 4096-bin histogram of key[18:7] + candidate list
+//   find     -> b2;   H3 over candidates (or all keys if the list overflowed):
+//            128-bin histogram of key[6:0] -> threshold key T and the number of
+//            ties at T to take (lowest indices first)
+//   pass C   per-chunk counts of key > T and key == T
+//   scan     exclusive scans -> each chunk's output offset and tie offset
+//   pass W   in index order: selected = key > T || (key == T && tie-rank < ties);
+//            block scans give each selected element its output slot, so indices
+//            come out ascending with no sort; f16 values; sparse state update
+//            base[e] += d, fb[e] = t - d (pipeline.py:107-112).
+// Every pass streams t once (4 B/elem) with 128-bit loads.
+#include "cc_common.cuh"
+#include "cc_internal.h"
+
+#include <algorithm>
+
+namespace cc {
+namespace topk {
+
+constexpr int kBins = 4096;
+constexpr int kBins3 = 128;
+constexpr int kThreads = 256;
+constexpr int64_t kChunk = 8192;  // elements per CTA in passes C and W
+
+struct State {
+  uint32_t need;        // remaining elements to take at the current level
+  uint32_t b1, b2;      // selected bins
+  uint32_t T;           // threshold key
+  uint32_t ties;        // elements with key == T to take
+  uint32_t cand;        // candidate count (keys in bin b1)
+  uint32_t pad[2];
+};
+
+struct Work {
+  uint32_t *hist1, *hist2, *hist3;
+  State *st;
+  uint32_t *cand;
+  int64_t cap;
+  uint32_t *cnt_gt, *cnt_eq, *sel_pref, *eq_pref;
+  double *part;  // [nH1 + nChunks][2]
+  float *tscratch;
+  int nH1;
+  int64_t nChunks;
+};
+
+__device__ __forceinline__ uint32_t key_of(float t) { return __float_as_uint(t) & 0x7fffffffu; }
+
+// ---- pass H1 ---------------------------------------------------------------
+template <int MODE, typename XT, bool FROM_T>
+__global__ void __launch_bounds__(kThreads) k_h1(const XT *__restrict__ x, float *__restrict__ base,
+                                                  float *__restrict__ aux, const float *__restrict__ tin,
+                                                  float *__restrict__ tout, float *__restrict__ decoded,
+                                                  int64_t total, uint32_t *__restrict__ hist1,
+                                                  double *__restrict__ part) {
+  __shared__ uint32_t h[kBins];
+  __shared__ double red[kThreads / 32];
+  for (int i = threadIdx.x; i < kBins; i += kThreads) h[i] = 0;
+  __syncthreads();
+  double tsq = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total; e += stride) {
+    float t;
+    if constexpr (FROM_T) {
+      t = tin[e];
+    } else {
+      const float xx = Act<XT>::load1(x + e);
+      float bb = 0.f, aa = 0.f;
+      if constexpr (MODE != CC_NAIVE) {
+        bb = base[e];
+        if (__float_as_uint(bb) == 0x80000000u) base[e] = 0.0f;  // dense base + 0.0 semantics
+      }
+      if constexpr (MODE != CC_NAIVE) aa = aux[e];
+      t = target_of<MODE>(xx, bb, aa);
+      tout[e] = t;
+      if constexpr (MODE == CC_NO_FEEDBACK) aux[e] = xx;  // ref' = a*
+      if constexpr (MODE == CC_NAIVE) base[e] = 0.0f;     // base' = dense decode: zero, then scatter
+    }
+    if (decoded) decoded[e] = 0.0f;
+    tsq += (double)t * (double)t;
+    atomicAdd(&h[key_of(t) >> 19], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBins; i += kThreads)
+    if (h[i]) atomicAdd(&hist1[i], h[i]);
+  tsq = warp_sum(tsq);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = tsq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < kThreads / 32; ++i) s += red[i];
+    part[2 * blockIdx.x] = 0.0;
+    part[2 * blockIdx.x + 1] = s;
+  }
+}
+
+// ---- find: suffix scan of a histogram from the top bin ---------------------
+template <int NB>
+__global__ void __launch_bounds__(1024) k_find(const uint32_t *__restrict__ hist, State *st, int level, uint32_t k) {
+  constexpr int PER = (NB + 1023) / 1024;
+  __shared__ uint32_t tot[1024];
+  const int t = threadIdx.x;
+  // thread t owns bins [NB-1-t*PER ... NB-PER-t*PER] (descending order)
+  uint32_t local = 0;
+  uint32_t v[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int b = NB - 1 - (t * PER + q);
+    v[q] = b >= 0 ? hist[b] : 0u;
+    local += v[q];
+  }
+  tot[t] = local;
+  __syncthreads();
+  // inclusive scan over threads (Hillis-Steele; NB is small)
+  for (int off = 1; off < 1024; off <<= 1) {
+    const uint32_t add = t >= off ? tot[t - off] : 0u;
+    __syncthreads();
+    tot[t] += add;
+    __syncthreads();
+  }
+  const uint32_t need = level == 1 ? k : st->need;
+  uint32_t before = t > 0 ? tot[t - 1] : 0u;
+  if (before < need && tot[t] >= need) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int b = NB - 1 - (t * PER + q);
+      if (b < 0) break;
+      if (before + v[q] >= need) {
+        const uint32_t rem = need - before;
+        if (level == 1) {
+          st->b1 = (uint32_t)b;
+          st->cand = 0;
+        } else if (level == 2) {
+          st->b2 = (uint32_t)b;
+        } else {
+          st->T = (st->b1 << 19) | (st->b2 << 7) | (uint32_t)b;
+          st->ties = rem;
+        }
+        st->need = rem;
+        break;
+      }
+      before += v[q];
+    }
+  }
+}
+
+// ---- pass H2: histogram of key[18:7] inside bin b1 + candidate list ----------
+__global__ void __launch_bounds__(kThreads) k_h2(const float *__restrict__ t, int64_t total, const State *st,
+                                                  uint32_t *__restrict__ hist2, uint32_t *__restrict__ cand,
+                                                  int64_t cap, uint32_t *cand_count) {
+  __shared__ uint32_t h[kBins];
+  for (int i = threadIdx.x; i < kBins; i += kThreads) h[i] = 0;
+  __syncthreads();
+  const uint32_t b1 = st->b1;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int lane = threadIdx.x & 31;
+  for (int64_t e0 = (int64_t)blockIdx.x * kThreads; e0 < total; e0 += stride) {
+    const int64_t e = e0 + threadIdx.x;
+    uint32_t key = 0;
+    bool in = false;
+    if (e < total) {
+      key = key_of(__ldcs(t + e));
+      in = (key >> 19) == b1;
+    }
+    if (in) atomicAdd(&h[(key >> 7) & 0xfffu], 1u);
+    const uint32_t m = __ballot_sync(0xffffffffu, in);
+    if (m) {
+      uint32_t basei = 0;
+      if (lane == 0) basei = atomicAdd(cand_count, (uint32_t)__popc(m));
+      basei = __shfl_sync(0xffffffffu, basei, 0);
+      const uint32_t pos = basei + __popc(m & ((1u << lane) - 1u));
+      if (in && pos < cap) cand[pos] = key;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBins; i += kThreads)
+    if (h[i]) atomicAdd(&hist2[i], h[i]);
+}
+
+// ---- pass H3: 128-bin histogram of key[6:0] among keys with key>>7 == prefix
+__global__ void __launch_bounds__(kThreads) k_h3(const float *__restrict__ t, int64_t total,
+                                                  const uint32_t *__restrict__ cand, int64_t cap, const State *st,
+                                                  uint32_t *__restrict__ hist3) {
+  __shared__ uint32_t h[kBins3];
+  for (int i = threadIdx.x; i < kBins3; i += kThreads) h[i] = 0;
+  __syncthreads();
+  const uint32_t prefix = (st->b1 << 12) | st->b2;
+  const bool use_cand = st->cand <= cap;
+  const int64_t n = use_cand ? (int64_t)st->cand : total;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < n; e += stride) {
+    const uint32_t key = use_cand ? cand[e] : key_of(t[e]);
+    if ((key >> 7) == prefix) atomicAdd(&h[key & 127u], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBins3; i += kThreads)
+    if (h[i]) atomicAdd(&hist3[i], h[i]);
+}
+
+// ---- pass C: per-chunk counts ------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_count(const float *__restrict__ t, int64_t total, const State *st,
+                                                     uint32_t *__restrict__ cnt_gt, uint32_t *__restrict__ cnt_eq) {
+  __shared__ uint32_t sg[kThreads / 32], se[kThreads / 32];
+  const uint32_t T = st->T;
+  const int64_t c0 = (int64_t)blockIdx.x * kChunk;
+  const int64_t c1 = min64(total, c0 + kChunk);
+  uint32_t gt = 0, eq = 0;
+  for (int64_t e = c0 + threadIdx.x; e < c1; e += kThreads) {
+    const uint32_t key = key_of(__ldcs(t + e));
+    gt += key > T;
+    eq += key == T;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    gt += __shfl_xor_sync(0xffffffffu, gt, o);
+    eq += __shfl_xor_sync(0xffffffffu, eq, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sg[threadIdx.x >> 5] = gt;
+    se[threadIdx.x >> 5] = eq;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t a = 0, b = 0;
+    for (int i = 0; i < kThreads / 32; ++i) {
+      a += sg[i];
+      b += se[i];
+    }
+    cnt_gt[blockIdx.x] = a;
+    cnt_eq[blockIdx.x] = b;
+  }
+}
+
+// ---- scan: chunk offsets --------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_scan(int64_t nch, const State *st, const uint32_t *__restrict__ cnt_gt,
+                                               const uint32_t *__restrict__ cnt_eq, uint32_t *__restrict__ sel_pref,
+                                               uint32_t *__restrict__ eq_pref) {
+  __shared__ uint32_t s_eq[1024], s_sel[1024];
+  __shared__ uint32_t carry_eq, carry_sel;
+  const uint32_t ties = st->ties;
+  if (threadIdx.x == 0) carry_eq = carry_sel = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nch; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const uint32_t eq = i < nch ? cnt_eq[i] : 0u;
+    s_eq[threadIdx.x] = eq;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      const uint32_t add = threadIdx.x >= off ? s_eq[threadIdx.x - off] : 0u;
+      __syncthreads();
+      s_eq[threadIdx.x] += add;
+      __syncthreads();
+    }
+    const uint32_t eq_before = carry_eq + s_eq[threadIdx.x] - eq;
+    uint32_t take = 0;
+    if (eq_before < ties) take = min(eq, ties - eq_before);
+    const uint32_t sel = (i < nch ? cnt_gt[i] : 0u) + take;
+    s_sel[threadIdx.x] = sel;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      const uint32_t add = threadIdx.x >= off ? s_sel[threadIdx.x - off] : 0u;
+      __syncthreads();
+      s_sel[threadIdx.x] += add;
+      __syncthreads();
+    }
+    if (i < nch) {
+      eq_pref[i] = eq_before;
+      sel_pref[i] = carry_sel + s_sel[threadIdx.x] - sel;
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) {
+      carry_eq += s_eq[1023];
+      carry_sel += s_sel[1023];
+    }
+    __syncthreads();
+  }
+}
+
+// block-wide exclusive scan of a per-thread count; returns the block total
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t &excl, uint32_t *sm) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) sm[w] = inc;
+  __syncthreads();
+  uint32_t wpre = 0, tot = 0;
+  for (int i = 0; i < kThreads / 32; ++i) {
+    if (i < w) wpre += sm[i];
+    tot += sm[i];
+  }
+  __syncthreads();
+  excl = wpre + inc - v;
+  return tot;
+}
+
+// ---- pass W: ordered write + sparse state update ------------------------------
+template <int MODE, typename XT>
+__global__ void __launch_bounds__(kThreads) k_write(const float *__restrict__ t, const XT *__restrict__ x,
+                                                     float *__restrict__ base, float *__restrict__ aux,
+                                                     float *__restrict__ decoded, int64_t total, int64_t k,
+                                                     const State *st, const uint32_t *__restrict__ sel_pref,
+                                                     const uint32_t *__restrict__ eq_pref, uint8_t *__restrict__ body,
+                                                     double *__restrict__ part, int stateful) {
+  __shared__ uint32_t sm[kThreads / 32];
+  __shared__ double red[kThreads / 32];
+  const uint32_t T = st->T, ties = st->ties;
+  const int64_t c0 = (int64_t)blockIdx.x * kChunk;
+  const int64_t c1 = min64(total, c0 + kChunk);
+  uint32_t sel_run = sel_pref[blockIdx.x], eq_run = eq_pref[blockIdx.x];
+  uint32_t *idx_out = reinterpret_cast<uint32_t *>(body);
+  __half *val_out = reinterpret_cast<__half *>(body + 4 * k);
+  double adj = 0.0;  // sum over selected of (d - t)^2 - t^2
+  for (int64_t e0 = c0; e0 < c1; e0 += kThreads) {
+    const int64_t e = e0 + threadIdx.x;
+    float tv = 0.f;
+    uint32_t key = 0;
+    const bool ok = e < c1;
+    if (ok) {
+      tv = t[e];
+      key = key_of(tv);
+    }
+    const uint32_t is_eq = ok && key == T;
+    uint32_t eq_ex;
+    const uint32_t eq_tot = block_excl_scan(is_eq, eq_ex, sm);
+    const bool sel = ok && (key > T || (is_eq && eq_run + eq_ex < ties));
+    uint32_t sel_ex;
+    const uint32_t sel_tot = block_excl_scan(sel ? 1u : 0u, sel_ex, sm);
+    if (sel) {
+      const uint32_t pos = sel_run + sel_ex;
+      idx_out[pos] = (uint32_t)e;
+      const __half h = __float2half_rn(tv);
+      val_out[pos] = h;
+      const float d = __half2float(h);
+      const double df = (double)d - (double)tv;
+      adj += df * df - (double)tv * (double)tv;
+      if (decoded) decoded[e] = d;
+      if (stateful) {
+        if constexpr (MODE == CC_NAIVE) {
+          base[e] = d;
+        } else {
+          base[e] = __fadd_rn(base[e], d);
+          if constexpr (MODE == CC_WITH_FEEDBACK) aux[e] = __fsub_rn(tv, d);
+        }
+      }
+    }
+    sel_run += sel_tot;
+    eq_run += eq_tot;
+  }
+  adj = warp_sum(adj);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = adj;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < kThreads / 32; ++i) s += red[i];
+    part[2 * blockIdx.x] = s;
+    part[2 * blockIdx.x + 1] = 0.0;
+  }
+  (void)x;
+}
+
+__global__ void k_record(int nparts, const double *__restrict__ part, double *__restrict__ record) {
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < nparts; ++i) {
+      a += part[2 * i];
+      b += part[2 * i + 1];
+    }
+    record[0] = b + a;  // ||t||^2 + sum_sel((d-t)^2 - t^2) = ||d - t||^2
+    record[1] = b;
+  }
+}
+
+// ---- receiver: sparse scatter (and -0.0 canonicalisation) ------------------------
+constexpr int kMaxPeers = 64;
+struct Peers {
+  const uint8_t *body[kMaxPeers];
+  float *base[kMaxPeers];
+  int64_t total[kMaxPeers];
+  int64_t k[kMaxPeers];
+};
+
+__global__ void __launch_bounds__(kThreads) k_canon(const __grid_constant__ Peers pp, int replace) {
+  const int peer = blockIdx.y;
+  float *base = pp.base[peer];
+  const int64_t total = pp.total[peer];
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total; e += stride) {
+    if (replace) base[e] = 0.0f;
+    else if (__float_as_uint(base[e]) == 0x80000000u) base[e] = 0.0f;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Peers pp, int replace) {
+  const int peer = blockIdx.y;
+  const int64_t k = pp.k[peer];
+  const uint32_t *idx = reinterpret_cast<const uint32_t *>(pp.body[peer]);
+  const __half *val = reinterpret_cast<const __half *>(pp.body[peer] + 4 * k);
+  float *base = pp.base[peer];
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < k; i += stride) {
+    const uint32_t e = idx[i];
+    const float d = __half2float(val[i]);
+    base[e] = replace ? d : __fadd_rn(base[e], d);
+  }
+}
+
+}  // namespace topk
+
+// ---------------------------------------------------------------------------
+// host
+// ---------------------------------------------------------------------------
+static topk::Work carve_topk(void *ws, int64_t total, bool need_t, int nH1, size_t *bytes) {
+  topk::Work w{};
+  uint8_t *b = reinterpret_cast<uint8_t *>(ws);
+  size_t off = 0;
+  auto take = [&](size_t n) {
+    uint8_t *q = b ? b + off : nullptr;
+    off = align_up(off + n, 256);
+    return q;
+  };
+  w.nH1 = nH1;
+  w.nChunks = cdiv(total, topk::kChunk);
+  w.cap = std::max<int64_t>(65536, total / 16);
+  // zeroed region first: hist1, hist2, hist3, state
+  w.hist1 = reinterpret_cast<uint32_t *>(take(4 * topk::kBins));
+  w.hist2 = reinterpret_cast<uint32_t *>(take(4 * topk::kBins));
+  w.hist3 = reinterpret_cast<uint32_t *>(take(4 * topk::kBins3));
+  w.st = reinterpret_cast<topk::State *>(take(sizeof(topk::State)));
+  w.cand = reinterpret_cast<uint32_t *>(take(4 * w.cap));
+  w.cnt_gt = reinterpret_cast<uint32_t *>(take(4 * w.nChunks));
+  w.cnt_eq = reinterpret_cast<uint32_t *>(take(4 * w.nChunks));
+  w.sel_pref = reinterpret_cast<uint32_t *>(take(4 * w.nChunks));
+  w.eq_pref = reinterpret_cast<uint32_t *>(take(4 * w.nChunks));
+  w.part = reinterpret_cast<double *>(take(16 * (size_t)(nH1 + w.nChunks)));
+  w.tscratch = need_t ? reinterpret_cast<float *>(take(4 * (size_t)total)) : nullptr;
+  if (bytes) *bytes = off;
+  return w;
+}
+
+static int h1_blocks(int64_t total) { return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), sm_count() * 4)); }
+
+int64_t topk_workspace_bytes(int64_t n, int64_t C, int64_t) {
+  size_t b = 0;
+  carve_topk(nullptr, n * C, true, h1_blocks(n * C), &b);
+  return (int64_t)b;
+}
+
+static const size_t kZeroBytes = 2 * 4 * topk::kBins + 4 * topk::kBins3 + 3 * 256;
+
+// common tail after the H1 pass: select T, count, scan, write
+template <int MODE, typename XT>
+static void select_and_write(const topk::Work &w, const float *t, const XT *x, float *base, float *aux,
+                             float *decoded, int64_t total, int64_t k, uint8_t *body, double *record, int stateful,
+                             cudaStream_t st) {
+  using namespace topk;
+  const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, kThreads), sm_count() * 8));
+  k_find<kBins><<<1, 1024, 0, st>>>(w.hist1, w.st, 1, (uint32_t)k);
+  k_h2<<<nb, kThreads, 0, st>>>(t, total, w.st, w.hist2, w.cand, w.cap, &w.st->cand);
+  k_find<kBins><<<1, 1024, 0, st>>>(w.hist2, w.st, 2, 0);
+  k_h3<<<nb, kThreads, 0, st>>>(t, total, w.cand, w.cap, w.st, w.hist3);
+  k_find<kBins3><<<1, 1024, 0, st>>>(w.hist3, w.st, 3, 0);
+  k_count<<<(unsigned)w.nChunks, kThreads, 0, st>>>(t, total, w.st, w.cnt_gt, w.cnt_eq);
+  k_scan<<<1, 1024, 0, st>>>(w.nChunks, w.st, w.cnt_gt, w.cnt_eq, w.sel_pref, w.eq_pref);
+  k_write<MODE, XT><<<(unsigned)w.nChunks, kThreads, 0, st>>>(t, x, base, aux, decoded, total, k, w.st, w.sel_pref,
+                                                             w.eq_pref, body, w.part + 2 * w.nH1, stateful);
+  k_record<<<1, 32, 0, st>>>((int)(w.nH1 + w.nChunks), w.part, record);
+  count_launch(9);
+}
+
+int topk_encode(int64_t n, int64_t C, int64_t k, const float *t, uint8_t *body, float *decoded, void *ws,
+                int64_t ws_bytes, cudaStream_t st) {
+  const int64_t total = n * C;
+  size_t need = 0;
+  const int nH1 = h1_blocks(total);
+  carve_topk(nullptr, total, false, nH1, &need);
+  if ((int64_t)need + 256 > ws_bytes) {
+    set_error("top-k workspace too small");
+    return CC_ERR_ARG;
+  }
+  topk::Work w = carve_topk(ws, total, false, nH1, nullptr);
+  double *record = reinterpret_cast<double *>(reinterpret_cast<uint8_t *>(ws) + need);
+  cudaMemsetAsync(ws, 0, kZeroBytes, st);
+  topk::k_h1<CC_NAIVE, float, true><<<nH1, topk::kThreads, 0, st>>>(nullptr, nullptr, nullptr, t, nullptr, decoded,
+                                                                    total, w.hist1, w.part);
+  count_launch();
+  select_and_write<CC_NAIVE, float>(w, t, nullptr, nullptr, nullptr, decoded, total, k, body, record, 0, st);
+  return cuda_status("topk_encode");
+}
+
+int topk_encode_step(int mode, int64_t n, int64_t C, int64_t k, const void *x, int x_dtype, float *base, float *aux,
+                     uint8_t *body, void *ws, int64_t ws_bytes, double *record, cudaStream_t st) {
+  const int64_t total = n * C;
+  size_t need = 0;
+  const int nH1 = h1_blocks(total);
+  const bool need_t = mode != CC_WITH_FEEDBACK;
+  carve_topk(nullptr, total, need_t, nH1, &need);
+  if ((int64_t)need > ws_bytes) {
+    set_error("top-k workspace too small");
+    return CC_ERR_ARG;
+  }
+  topk::Work w = carve_topk(ws, total, need_t, nH1, nullptr);
+  float *t = mode == CC_WITH_FEEDBACK ? aux : w.tscratch;
+  cudaMemsetAsync(ws, 0, kZeroBytes, st);
+#define CC_TK(MODE, XT)                                                                                      \
+  do {                                                                                                       \
+    topk::k_h1<MODE, XT, false><<<nH1, topk::kThreads, 0, st>>>((const XT *)x, base, aux, nullptr, t, nullptr, \
+                                                                total, w.hist1, w.part);                    \
+    count_launch();                                                                                          \
+    select_and_write<MODE, XT>(w, t, (const XT *)x, base, aux, nullptr, total, k, body, record, 1, st);      \
+  } while (0)
+  if (x_dtype == CC_BF16) {
+    if (mode == CC_WITH_FEEDBACK) CC_TK(CC_WITH_FEEDBACK, __nv_bfloat16);
+    else if (mode == CC_NO_FEEDBACK) CC_TK(CC_NO_FEEDBACK, __nv_bfloat16);
+    else CC_TK(CC_NAIVE, __nv_bfloat16);
+  } else {
+    if (mode == CC_WITH_FEEDBACK) CC_TK(CC_WITH_FEEDBACK, float);
+    else if (mode == CC_NO_FEEDBACK) CC_TK(CC_NO_FEEDBACK, float);
+    else CC_TK(CC_NAIVE, float);
+  }
+#undef CC_TK
+  return cuda_status("topk_encode_step");
+}
+
+// accumulate: 0 replace (zero + scatter), 1 sparse add, 2 canonicalise -0.0 then sparse add
+int topk_decode(int count, const int64_t *rows, int64_t C, int64_t k, const uint8_t *const *bodies, int accumulate,
+                float *const *bases, cudaStream_t st) {
+  for (int c0 = 0; c0 < count; c0 += topk::kMaxPeers) {
+    const int cnt = std::min(topk::kMaxPeers, count - c0);
+    topk::Peers pp{};
+    int64_t maxk = 0, maxt = 0;
+    for (int i = 0; i < cnt; ++i) {
+      pp.body[i] = bodies[c0 + i];
+      pp.base[i] = bases[c0 + i];
+      pp.total[i] = rows[c0 + i] * C;
+      pp.k[i] = k;
+      maxk = std::max(maxk, k);
+      maxt = std::max(maxt, pp.total[i]);
+    }
+    if (accumulate != 1) {
+      dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(maxt, topk::kThreads), sm_count() * 4)), cnt);
+      topk::k_canon<<<g, topk::kThreads, 0, st>>>(pp, accumulate == 0);
+      count_launch();
+    }
+    if (maxk > 0) {
+      dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(maxk, topk::kThreads), sm_count() * 4)), cnt);
+      topk::k_scatter<<<g, topk::kThreads, 0, st>>>(pp, accumulate == 0);
+      count_launch();
+    }
+  }
+  return cuda_status("topk_decode");
+}
+
+}  // namespace cc

@@ -150,7 +150,16 @@ def encode_step(state, a_star, codec, rng=None, body_out=None):
         payload = cx.RawPayload(rows, cols, body, wire_dtype=wire)
     else:
         tag = cx._spec_tag(codec)
-        if tag is not None:
+        if kind == cx.CompressorKind.TOPK:
+            k = cx.topk_count(rows, cols, codec.keep_fraction)
+            nbytes = 6 * k
+            body = body_out[:nbytes] if body_out is not None else cx._empty_body(nbytes)
+            ws = cx.workspace(_lib.check(lib.cc_workspace_bytes(_lib.CC_TOPK, rows, cols, k)), "topk")
+            _lib.check(lib.cc_topk_encode_step(mode, rows, cols, k, _lib.ptr(x), cx.dtype_code(x),
+                                               _lib.ptr(state.base), _lib.ptr(aux), _lib.ptr(body), _lib.ptr(ws),
+                                               ws.numel(), _lib.ptr(rec), stream), "topk encode_step")
+            payload = cx.TopKPayload(rows, cols, body, k)
+        elif tag is not None:
             nbytes = lib.cc_body_bytes(tag, rows, cols, 0)
             body = body_out[:nbytes] if body_out is not None else cx._empty_body(nbytes)
             ws = cx.workspace(_lib.check(lib.cc_workspace_bytes(tag, rows, cols, 0)))
@@ -246,8 +255,11 @@ def decode_step(state, message):
     if (payload.rows, payload.cols) != state.shape:
         raise ProtocolError(f"payload shape {(payload.rows, payload.cols)} != state shape {state.shape}")
     replace = is_warmup or payload.tag == cx.TAG_RAW or state.mode == PipelineMode.NAIVE
+    acc = 0 if replace else 1
+    if payload.tag == cx.TAG_TOPK and acc:
+        acc = 2  # dense `base + decoded` semantics for the sparse codec (-0.0 -> +0.0)
     lib = _lib.load()
-    _lib.check(lib.cc_decode_step(payload.tag, 0 if replace else 1, payload.rows, payload.cols, payload._param(),
+    _lib.check(lib.cc_decode_step(payload.tag, acc, payload.rows, payload.cols, payload._param(),
                                   _lib.ptr(payload.body), payload._body_dtype(), _lib.ptr(state.base),
                                   _lib.stream_ptr()), "decode_step")
     state.step = step
