@@ -169,6 +169,9 @@ CC_API int64_t cc_launch_count(void);
 /* encode-path selection for tests/benchmarks: -1 auto (persistent fused K1
  * when C % 1024 == 0 and aligned), 0 force the multi-kernel K1, 1 prefer fused */
 CC_API void cc_set_quant_path(int path);
+/* profiling only: stop the persistent K1 after phase 1 (scale partials) or
+ * 2 (scales); 0 = full step.  Results are incomplete when != 0. */
+CC_API void cc_debug_fused_stop(int phase);
 
 #ifdef __cplusplus
 }

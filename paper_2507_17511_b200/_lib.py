@@ -45,6 +45,7 @@ SIGNATURES = {
     "cc_version": (_i32, []),
     "cc_launch_count": (_i64, []),
     "cc_set_quant_path": (None, [_i32]),
+    "cc_debug_fused_stop": (None, [_i32]),
 }
 
 _LIB = None

@@ -54,6 +54,7 @@ int lowrank_encode(int int4, int64_t n, int64_t C, int64_t r, int iters, const f
 int lowrank_decode(int int4, int count, const int64_t *rows, int64_t C, int64_t r, const uint8_t *const *bodies,
                    int accumulate, float *const *bases, cudaStream_t st);
 void set_quant_path(int v);
+void set_fused_stop(int v);
 int residual_target(int mode, int64_t n, int64_t C, const void *x, int x_dtype, const float *base, const float *aux,
                     float *t, cudaStream_t st);
 int apply_decoded(int mode, int64_t n, int64_t C, const void *x, int x_dtype, const float *t, const float *dec,
@@ -72,6 +73,7 @@ CC_API const char *cc_last_error(void) { return g_err.c_str(); }
 CC_API int cc_version(void) { return 1; }
 CC_API int64_t cc_launch_count(void) { return g_launches.load(); }
 CC_API void cc_set_quant_path(int path) { set_quant_path(path); }
+CC_API void cc_debug_fused_stop(int phase) { set_fused_stop(phase); }
 
 CC_API int64_t cc_topk_count(int64_t rows, int64_t cols, double keep_fraction) {
   if (rows < 1 || cols < 1 || !(keep_fraction > 0.0 && keep_fraction <= 1.0)) return CC_ERR_ARG;

@@ -54,7 +54,10 @@ struct Params {
   uint8_t *codes, *body_u, *body_v;
   unsigned int *ticket;
   int scale_mode;
+  int stop_after;  // profiling: 1 = phase A only, 2 = A + scales, 0 = full
 };
+
+constexpr int kUCache = 512;  // cached u_i per CTA for phase B
 
 // f32 state arrays staged per tile: base + aux (feedback or ref); naive mode none
 template <int MODE>
@@ -190,7 +193,8 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   uint8_t *tiles = smem;
   double *rp = reinterpret_cast<double *>(smem + (size_t)S * stage_bytes);  // [S][R][kGWarps]
   double *red = rp + (size_t)S * R * kGWarps;                               // block-sum scratch
-  uint64_t *full = reinterpret_cast<uint64_t *>(red + 64);
+  float *ucache = reinterpret_cast<float *>(red + 64);                        // [kUCache]
+  uint64_t *full = reinterpret_cast<uint64_t *>(ucache + kUCache);
   uint64_t *empty = full + S;
 
   if (tid == 0) {
@@ -210,12 +214,14 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   auto stage_a = [&](int s) {
     return reinterpret_cast<float *>(tiles + (size_t)s * stage_bytes + xs_bytes + fs_bytes);
   };
+  double cta_total = 0.0;  // producer lanes: running sum of this CTA's row partials
   auto finish_rows = [&](int s, int64_t k) {  // producer lanes: per-row sums over the 8 warps of a group
     const int64_t r0p = tile_r0(k);
     if (lane < R && r0p + lane < n) {
       double acc = 0.0;
       for (int w = 0; w < kGWarps; ++w) acc += rp[((size_t)s * R + lane) * kGWarps + w];
       p.rowpart[(int64_t)strip * n + r0p + lane] = acc;
+      cta_total += acc;
     }
   };
 
@@ -311,10 +317,16 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     }
   }
 
+  // per-CTA |t| total (deterministic: fixed lane order) -> blkpart
+  {
+    const double b = block_sum(producer ? cta_total : 0.0, red);
+    if (tid == 0) p.blkpart[cta] = b;
+  }
   cg::grid_group grid = cg::this_grid();
   grid.sync();
+  if (p.stop_after == 1) return;
 
-  // ================= phase F1: column means, row sums =================
+  // ================= phase F: v_j (column means), g, u_i =================
   const int slots = (G / p.nStrips) * kGroups;
   if (cta == 0 && tid == 0) *p.ticket = 0u;
   for (int64_t j = (int64_t)cta * kThreads + tid; j < C; j += (int64_t)G * kThreads) {
@@ -325,38 +337,36 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     p.v[j] = v;
     store_f32_bytes(p.body_v + 4 * j, v);
   }
-  const int64_t ch = (n + G - 1) / G;
-  const int64_t i0 = (int64_t)cta * ch, i1 = min64(n, i0 + ch);
-  {
-    double local = 0.0;
-    for (int64_t i = i0 + tid; i < i1; i += kThreads) {
-      double rs = 0.0;
-      for (int s = 0; s < p.nStrips; ++s) rs += p.rowpart[(int64_t)s * n + i];
-      p.rowsum[i] = rs;
-      local += rs;
-    }
-    const double b = block_sum(local, red);
-    if (tid == 0) p.blkpart[cta] = b;
-  }
-  grid.sync();
-
-  // ================= phase F2: g and u =================
   {
     const double part = tid < G ? __ldcg(p.blkpart + tid) : 0.0;  // G <= kThreads (launcher)
     const double tot = block_sum(part, red);
-    const double g = tot / (double)(n * C);
+    const double g = tot / (double)(n * C);  // mean|t| (cx:142)
+    const int64_t ch = (n + G - 1) / G;
+    const int64_t i0 = (int64_t)cta * ch, i1 = min64(n, i0 + ch);
     for (int64_t i = i0 + tid; i < i1; i += kThreads) {
-      const double rs = __ldcg(p.rowsum + i);
+      double rs = 0.0;
+      for (int s = 0; s < p.nStrips; ++s) rs += __ldcg(p.rowpart + (int64_t)s * n + i);
       float u;
       if (p.scale_mode == CC_SCALE_PER_CHANNEL) u = 1.0f;
       else if (p.scale_mode == CC_SCALE_PER_TOKEN) u = (float)(rs / (double)C);
       else if (g == 0.0) u = 1.0f;
-      else u = (float)fmax((rs / (double)C) / g, kRowScaleFloor);
+      else u = (float)fmax((rs / (double)C) / g, kRowScaleFloor);  // cx:147
       p.u[i] = u;
       store_f32_bytes(p.body_u + 4 * i, u);
     }
   }
   grid.sync();
+  if (p.stop_after == 2) return;
+
+  // u_i of every row this CTA quantizes, in phase-B order
+  const bool ucached = K * R <= kUCache;
+  if (ucached) {
+    for (int i = tid; i < K * R; i += kThreads) {
+      const int64_t row = tile_r0(K - 1 - i / R) + i % R;
+      ucache[i] = row < n ? __ldcg(p.u + row) : 0.0f;
+    }
+  }
+  __syncthreads();
 
   // ================= phase B: quantize, pack, update state =================
   double err = 0.0, tsq = 0.0;
@@ -378,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       const int nrows = (int)min64(R, n - r0);
       for (int r = grp; r < nrows; r += kGroups) {
         const int64_t row = r0 + r;
-        const float uf = __ldcg(p.u + row);
+        const float uf = ucached ? ucache[k * R + r] : __ldcg(p.u + row);
         const double ud = (double)uf;
         float xx[4] = {0.f, 0.f, 0.f, 0.f}, bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f};
         if (active) load_row(s, r, xx, bb, aa, true);
@@ -449,7 +459,7 @@ static size_t fused_smem(int mode, int xsize, int R, int S) {
   const int NF = mode == CC_NAIVE ? 0 : 2;
   const size_t stage = (size_t)R * fused::kStrip * (xsize + 4 * NF);
   const size_t rp = (size_t)S * R * fused::kGWarps * sizeof(double);
-  const size_t red = 64 * sizeof(double);  // block-sum scratch
+  const size_t red = 64 * sizeof(double) + fused::kUCache * sizeof(float);  // block-sum scratch + u cache
   return (size_t)S * stage + rp + red + 2 * S * sizeof(uint64_t) + 256;
 }
 
@@ -469,6 +479,9 @@ static int launch_fused(fused::Params &p, cudaStream_t st) {
   count_launch();
   return CC_OK;
 }
+
+static int g_fused_stop = 0;
+void set_fused_stop(int v) { g_fused_stop = v; }
 
 bool fused_supported(int64_t n, int64_t C, const void *x, int x_dtype, const float *base, const float *aux,
                      const uint8_t *body) {
@@ -513,6 +526,7 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   p.G = G;
   p.nTiles = cdiv(n, p.R) * p.nStrips;
   p.scale_mode = scale_mode;
+  p.stop_after = g_fused_stop;
   const int bits = codec == CC_SIGN1 ? 1 : (codec == CC_QUANT2 ? 2 : 4);
   const int64_t cbytes = cdiv(n * C * bits, 8);
   p.codes = body;

@@ -1,0 +1,96 @@
+"""Kernel microbenchmarks (CUDA events, warm, L2-cold by rotating over layers).
+
+python scripts/microbench.py [--rows 4096] [--cols 3072] [--layers 16] [--codec quant2bit]
+Prints one line per kernel variant: mean µs and GB/s of algorithmic bytes.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2507_17511_b200 import _lib  # noqa: E402
+from paper_2507_17511_b200 import compressors as cx  # noqa: E402
+from paper_2507_17511_b200 import pipeline as pl  # noqa: E402
+
+
+def timed(fn, reps):
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record()
+    for i in range(reps):
+        fn(i)
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) * 1e3 / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rows", type=int, default=4096)
+    ap.add_argument("--cols", type=int, default=3072)
+    ap.add_argument("--layers", type=int, default=16)
+    ap.add_argument("--codec", default="quant2bit")
+    ap.add_argument("--reps", type=int, default=48)
+    a = ap.parse_args()
+    lib = _lib.load()
+    n, c, L = a.rows, a.cols, a.layers
+    spec = cx.CompressorSpec(cx.CompressorKind(a.codec))
+    bits = {"sign1bit": 1, "quant2bit": 2, "quant4bit": 4}[a.codec]
+    xs = [(torch.randn(n, c, device="cuda") * torch.rand(1, c, device="cuda") * 3).to(torch.bfloat16)
+          for _ in range(L)]
+    sts = [pl.LayerState("residual_with_feedback", 1, torch.zeros(n, c, device="cuda")) for _ in range(L)]
+    for st, x in zip(sts, xs):  # warmup protocol step
+        pl.encode_step(st, x, spec)
+        pl.encode_step(st, x, spec)
+    tag = cx._spec_tag(spec)
+    wsb = lib.cc_workspace_bytes(tag, n, c, 0)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    body = torch.empty(lib.cc_body_bytes(tag, n, c, 0) + 64, dtype=torch.uint8, device="cuda")
+    rec = torch.zeros(2, dtype=torch.float64, device="cuda")
+    stream = _lib.stream_ptr()
+
+    def enc(i):
+        st = sts[i % L]
+        lib.cc_encode_step(tag, 2, 0, n, c, _lib.ptr(xs[i % L]), _lib.CC_BF16, _lib.ptr(st.base),
+                           _lib.ptr(st.feedback), _lib.ptr(body), _lib.ptr(ws), wsb, _lib.ptr(rec), stream)
+
+    out = {}
+    alg = n * c * (18 + bits / 8)
+    for name, path, stop in (("k1_multikernel", 0, 0), ("k1_fused", -1, 0), ("k1_fused_phaseA", -1, 1),
+                             ("k1_fused_phaseA+F", -1, 2)):
+        lib.cc_set_quant_path(path)
+        lib.cc_debug_fused_stop(stop)
+        for i in range(L):
+            enc(i)
+        us = timed(enc, a.reps)
+        out[name] = {"us": round(us, 2), "alg_GBps": round(alg / us / 1e3, 1)}
+    lib.cc_set_quant_path(-1)
+    lib.cc_debug_fused_stop(0)
+    # K2: accumulate decode of the last body into each layer's base
+    bases = [st.base for st in sts]
+
+    def dec(i):
+        lib.cc_decode_step(tag, 1, n, c, 0, _lib.ptr(body), _lib.CC_F32, _lib.ptr(bases[i % L]), stream)
+
+    us = timed(dec, a.reps)
+    out["k2_decode"] = {"us": round(us, 2), "alg_GBps": round(n * c * (8 + bits / 8) / us / 1e3, 1)}
+    # plain copy roofline reference: base -> feedback of another layer
+    def cp(i):
+        sts[(i + 1) % L].feedback.copy_(sts[i % L].base)
+
+    us = timed(cp, a.reps)
+    out["torch_copy_f32"] = {"us": round(us, 2), "GBps": round(2 * n * c * 4 / us / 1e3, 1)}
+    print(json.dumps({"shape": [n, c], "codec": a.codec, **out}))
+
+
+if __name__ == "__main__":
+    main()
