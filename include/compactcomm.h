@@ -172,6 +172,9 @@ CC_API void cc_set_quant_path(int path);
 /* profiling only: stop the persistent K1 after phase 1 (scale partials) or
  * 2 (scales); 0 = full step.  Results are incomplete when != 0. */
 CC_API void cc_debug_fused_stop(int phase);
+/* profiling only: device buffer of [grid][8] u64 %globaltimer stamps written by
+ * every CTA of the persistent K1 at its phase boundaries (NULL disables). */
+CC_API void cc_debug_fused_timer(void *dev_buf);
 
 #ifdef __cplusplus
 }

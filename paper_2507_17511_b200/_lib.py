@@ -46,6 +46,7 @@ SIGNATURES = {
     "cc_launch_count": (_i64, []),
     "cc_set_quant_path": (None, [_i32]),
     "cc_debug_fused_stop": (None, [_i32]),
+    "cc_debug_fused_timer": (None, [_p]),
 }
 
 _LIB = None

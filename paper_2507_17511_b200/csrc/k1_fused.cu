@@ -55,7 +55,14 @@ struct Params {
   unsigned int *ticket;
   int scale_mode;
   int stop_after;  // profiling: 1 = phase A only, 2 = A + scales, 0 = full
+  unsigned long long *timer;  // profiling: [G][8] globaltimer stamps, or null
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 constexpr int kUCache = 512;  // cached u_i per CTA for phase B
 
@@ -63,18 +70,6 @@ constexpr int kUCache = 512;  // cached u_i per CTA for phase B
 template <int MODE>
 constexpr int n_f32_arrays() {
   return MODE == CC_NAIVE ? 0 : 2;
-}
-
-// exact f32 -> f64 on the integer pipes for normal numbers and zero; the XU
-// conversion (F2F, quarter rate) only for subnormal / non-finite inputs
-__device__ __forceinline__ double f64_of(float a) {
-  const uint32_t b = __float_as_uint(a);
-  const uint32_t e = b & 0x7f800000u;
-  if (__builtin_expect(e == 0x7f800000u || (e == 0u && (b & 0x7fffffu) != 0u), 0)) return (double)a;
-  if (e == 0u) return __longlong_as_double((long long)((uint64_t)(b & 0x80000000u) << 32));
-  const uint64_t hi = ((uint64_t)(b & 0x80000000u) << 32) |
-                      ((((uint64_t)(b & 0x7fffffffu)) << 29) + ((uint64_t)(1023 - 127) << 52));
-  return __longlong_as_double((long long)hi);
 }
 
 // deterministic block sum over all kThreads threads (fixed pairing)
@@ -94,80 +89,120 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
   return s;
 }
 
-// exact slow path for one element (f64 scale math as in quant.cu)
+struct CodeVal {
+  uint32_t code;
+  float d;
+};
+
+// exact path for one element (f64 scale math, identical to quant.cu)
 template <int CODEC>
-__device__ __noinline__ void quantize1_exact(float t, double ud, double vd, uint32_t &code, float &d) {
+__device__ __noinline__ CodeVal quantize1_exact(float t, double ud, double vd) {
   const double s = ud * vd;
-  if constexpr (CODEC == CC_QUANT2) {
-    code = quant2_code(t, s, ud * (1.25 * vd));
-    d = (float)(quant2_level(code) * s);
+  CodeVal r;
+  if constexpr (CODEC == CC_SIGN1) {
+    r.code = t < 0.0f ? 1u : 0u;
+    r.d = (float)(r.code ? -s : s);
+  } else if constexpr (CODEC == CC_QUANT2) {
+    r.code = quant2_code(t, s, ud * (1.25 * vd));
+    r.d = (float)(quant2_level(r.code) * s);
   } else {
-    code = quant4_code(t, s);
-    d = (float)(quant4_level(code) * s);
+    r.code = quant4_code(t, s);
+    r.d = (float)(quant4_level(r.code) * s);
   }
+  return r;
 }
 
-// 4 elements of one row.  Fast path is pure f32: p = RN32(u v) (== f32(u64 v64)),
-// the 2-bit thresholds are classified against 1.25 p with a 2^-20 guard band on
-// either side (exact outside it), d = level * p (exact: power-of-two levels in
-// the normal range).  Elements in the guard band or with |p| outside
-// [2^-100, 2^100] take the exact f64 path (quantize1_exact).
+// Per-column constants of the fast 2-bit path: v, and 1.25 v scaled by
+// (1 +- 2^-20) and rounded outward, so that for |u| in range
+//   RN(u * vhi) > 1.25 u v  and  RN(u * vlo) < 1.25 u v  (exactly),
+// i.e. |t| > RN(u vhi) proves code 0/3 and |t| < RN(u vlo) proves code 1/2.
+struct ColConst {
+  float v[4], vhi[4], vlo[4];
+  bool ok;  // all 4 columns have |v| in [2^-50, 2^50] (and v != 0)
+};
+
+__device__ __forceinline__ bool scale_in_range(float a) { return a >= 0x1p-50f && a <= 0x1p+50f; }
+
+// 4 elements of one row.  Fast path: pure f32 (p = RN32(u v) == f32(u64 v64);
+// d = level * p exact for power-of-two levels while u, v are in range);
+// elements inside the 2^-20 guard band around the thresholds, and rows/columns
+// with extreme scales, take the exact f64 path.
 template <int CODEC>
-__device__ __forceinline__ void quantize4(const float (&t)[4], double ud, float uf, const double (&vd)[4],
-                                          const float (&vf)[4], uint32_t &packed, float (&d)[4]) {
+__device__ __forceinline__ uint32_t quantize4(const float (&t)[4], float uf, bool row_ok, const ColConst &cc,
+                                              float (&d)[4]) {
   constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
-  packed = 0;
+  uint32_t packed = 0;
+  if constexpr (CODEC == CC_SIGN1) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint32_t code;
-    const float p = __fmul_rn(uf, vf[q]);
-    if constexpr (CODEC == CC_SIGN1) {
-      code = t[q] < 0.0f ? 1u : 0u;
-      d[q] = code ? -p : p;
-    } else if constexpr (CODEC == CC_QUANT2) {
-      const float ap = fabsf(p), ax = fabsf(t[q]);
-      const float thr = __fmul_rn(ap, 1.25f);
-      const bool big = ax > __fmul_ru(thr, 1.00000095367431640625f);    // 1 + 2^-20
-      const bool small = ax < __fmul_rd(thr, 0.99999904632568359375f);  // 1 - 2^-20
-      const bool neg = t[q] < 0.0f;
-      code = big ? (neg ? 0u : 3u) : (neg ? 1u : 2u);
-      const float lv = big ? 2.0f : 0.5f;
-      d[q] = (neg ? -lv : lv) * p;
-      if (__builtin_expect(!(big || small) || !(ap >= 0x1p-100f && ap <= 0x1p+100f), 0))
-        quantize1_exact<CODEC>(t[q], ud, vd[q], code, d[q]);
-    } else {
-      quantize1_exact<CODEC>(t[q], ud, vd[q], code, d[q]);
+    for (int q = 0; q < 4; ++q) {
+      const float p = __fmul_rn(uf, cc.v[q]);
+      const uint32_t neg = t[q] < 0.0f;
+      d[q] = neg ? -p : p;
+      packed |= neg << q;
     }
-    packed |= code << (q * bits);
+    return packed;
+  } else if constexpr (CODEC == CC_QUANT2) {
+    bool ambiguous = !(row_ok && cc.ok);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float p = __fmul_rn(uf, cc.v[q]);
+      const float ax = fabsf(t[q]);
+      const bool big = ax > __fmul_rn(uf, cc.vhi[q]);
+      ambiguous |= !big && !(ax < __fmul_rn(uf, cc.vlo[q]));
+      const bool neg = t[q] < 0.0f;
+      // code: big -> (neg ? 0 : 3), else (neg ? 1 : 2)
+      const uint32_t code = big ? (neg ? 0u : 3u) : (neg ? 1u : 2u);
+      const float lv = big ? 2.0f : 0.5f;
+      d[q] = __fmul_rn(neg ? -lv : lv, p);
+      packed |= code << (2 * q);
+    }
+    if (__builtin_expect(ambiguous, 0)) {
+      packed = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const CodeVal r = quantize1_exact<CODEC>(t[q], (double)uf, (double)cc.v[q]);
+        d[q] = r.d;
+        packed |= r.code << (2 * q);
+      }
+    }
+    return packed;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const CodeVal r = quantize1_exact<CODEC>(t[q], (double)uf, (double)cc.v[q]);
+      d[q] = r.d;
+      packed |= r.code << (bits * q);
+    }
+    return packed;
   }
 }
 
-// ||d - t||^2 and ||t||^2 of 4 elements: f32 quad sums (rel. err < 2^-21) added in
-// f64; quads with huge magnitudes are redone in f64
-__device__ __forceinline__ void record4(const float (&t)[4], const float (&d)[4], double &err, double &tsq) {
-  float e2 = 0.f, t2 = 0.f;
-  float mx = 0.f;
+// ||d - t||^2 and ||t||^2 of 4 elements: f32 quad sums (rel. err < 2^-21)
+// added in f64; quads that overflow f32 are redone in f64
+__device__ __forceinline__ void record4(const float (&t)[4], const float (&e)[4], double &err, double &tsq) {
+  float e2 = e[0] * e[0], t2 = t[0] * t[0];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float e = __fsub_rn(t[q], d[q]);
-    e2 = __fmaf_rn(e, e, e2);
+  for (int q = 1; q < 4; ++q) {
+    e2 = __fmaf_rn(e[q], e[q], e2);
     t2 = __fmaf_rn(t[q], t[q], t2);
-    mx = fmaxf(mx, fmaxf(fabsf(e), fabsf(t[q])));
   }
-  if (__builtin_expect(mx > 0x1p+60f || (mx < 0x1p-60f && mx > 0.f), 0)) {
+  if (__builtin_expect(!(e2 + t2 <= 3.0e38f), 0)) {
     double a = 0.0, b = 0.0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const double e = (double)__fsub_rn(t[q], d[q]);
-      a += e * e;
+      a += (double)e[q] * (double)e[q];
       b += (double)t[q] * (double)t[q];
     }
     err += a;
     tsq += b;
   } else {
-    err += f64_of(e2);
-    tsq += f64_of(t2);
+    err += (double)e2;
+    tsq += (double)t2;
   }
+}
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 template <int MODE, int CODEC, typename XT>
@@ -197,6 +232,10 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   uint64_t *full = reinterpret_cast<uint64_t *>(ucache + kUCache);
   uint64_t *empty = full + S;
 
+  auto stamp = [&](int i) {
+    if (p.timer && tid == 0) p.timer[(size_t)cta * 8 + i] = gtimer();
+  };
+  stamp(0);
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -300,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
         if (active) {
           load_row(s, r, xx, bb, aa, MODE == CC_WITH_FEEDBACK);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) a[q] = f64_of(fabsf(target_of<MODE>(xx[q], bb[q], aa[q])));
+          for (int q = 0; q < 4; ++q) a[q] = fabs((double)target_of<MODE>(xx[q], bb[q], aa[q]));
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) cs[q] += a[q];
@@ -311,9 +350,18 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (active) {
-      double *cp = p.colpart + (int64_t)((cta / p.nStrips) * kGroups + grp) * C + c0 + col;
-      cp[0] = cs[0]; cp[1] = cs[1]; cp[2] = cs[2]; cp[3] = cs[3];
+    // merge the two row groups' column partials (fixed order g0 + g1) through smem
+    double *xchg = reinterpret_cast<double *>(tiles);
+    named_sync(1, kConsumers);  // all consumers done with the last stage
+    if (grp == 1) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) xchg[4 * gtid + q] = cs[q];
+    }
+    named_sync(1, kConsumers);
+    if (grp == 0 && active) {
+      double *cp = p.colpart + (int64_t)(cta / p.nStrips) * C + c0 + col;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cp[q] = cs[q] + xchg[4 * gtid + q];
     }
   }
 
@@ -322,20 +370,34 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     const double b = block_sum(producer ? cta_total : 0.0, red);
     if (tid == 0) p.blkpart[cta] = b;
   }
+  stamp(1);
   cg::grid_group grid = cg::this_grid();
   grid.sync();
+  stamp(2);
   if (p.stop_after == 1) return;
 
   // ================= phase F: v_j (column means), g, u_i =================
-  const int slots = (G / p.nStrips) * kGroups;
+  const int slots = G / p.nStrips;
   if (cta == 0 && tid == 0) *p.ticket = 0u;
-  for (int64_t j = (int64_t)cta * kThreads + tid; j < C; j += (int64_t)G * kThreads) {
-    double s = 0.0;
-    for (int q = 0; q < slots; ++q) s += p.colpart[(int64_t)q * C + j];
-    float v = (float)(s / (double)n);
-    if (p.scale_mode == CC_SCALE_PER_TOKEN) v = 1.0f;
-    p.v[j] = v;
-    store_f32_bytes(p.body_v + 4 * j, v);
+  {
+    // 8 lanes per column, fixed split of the slots, fixed butterfly combine
+    const int64_t gid = (int64_t)cta * kThreads + tid;
+    const int64_t nthr = (int64_t)G * kThreads;
+    for (int64_t base_id = gid - (gid & 7); base_id < C * 8; base_id += nthr - (nthr & 7)) {
+      const int64_t j = base_id / 8;
+      const int part = (int)(gid & 7);
+      double sacc = 0.0;
+      for (int q = part; q < slots; q += 8) sacc += __ldcg(p.colpart + (int64_t)q * C + j);
+      sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+      sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+      sacc += __shfl_xor_sync(0xffffffffu, sacc, 4);
+      if (part == 0) {
+        float v = (float)(sacc / (double)n);  // colmean (cx:148)
+        if (p.scale_mode == CC_SCALE_PER_TOKEN) v = 1.0f;
+        p.v[j] = v;
+        store_f32_bytes(p.body_v + 4 * j, v);
+      }
+    }
   }
   {
     const double part = tid < G ? __ldcg(p.blkpart + tid) : 0.0;  // G <= kThreads (launcher)
@@ -355,7 +417,9 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       store_f32_bytes(p.body_u + 4 * i, u);
     }
   }
+  stamp(3);
   grid.sync();
+  stamp(4);
   if (p.stop_after == 2) return;
 
   // u_i of every row this CTA quantizes, in phase-B order
@@ -373,12 +437,15 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   if (producer) {
     produce(K, true, l2_policy_evict_first());
   } else {
-    double vd[4];
-    float vf[4];
+    ColConst cc;
+    cc.ok = true;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      vf[q] = active ? __ldcg(p.v + c0 + col + q) : 0.0f;
-      vd[q] = (double)vf[q];
+      const float v = active ? __ldcg(p.v + c0 + col + q) : 1.0f;
+      cc.v[q] = v;
+      cc.vhi[q] = __fmul_ru(__fmul_ru(v, 1.25f), 1.00000095367431640625f);  // (1 + 2^-20)
+      cc.vlo[q] = __fmul_rd(__fmul_rd(v, 1.25f), 0.99999904632568359375f);  // (1 - 2^-20)
+      cc.ok = cc.ok && scale_in_range(fabsf(v));
     }
     for (int64_t k = 0; k < K; ++k) {
       const int64_t seq = K + k;
@@ -389,31 +456,27 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       for (int r = grp; r < nrows; r += kGroups) {
         const int64_t row = r0 + r;
         const float uf = ucached ? ucache[k * R + r] : __ldcg(p.u + row);
-        const double ud = (double)uf;
         float xx[4] = {0.f, 0.f, 0.f, 0.f}, bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f};
         if (active) load_row(s, r, xx, bb, aa, true);
-        float t[4], d[4];
+        float t[4], d[4], e[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) t[q] = target_of<MODE>(xx[q], bb[q], aa[q]);
-        uint32_t packed = 0;
-        quantize4<CODEC>(t, ud, uf, vd, vf, packed, d);
+        const uint32_t packed = quantize4<CODEC>(t, uf, scale_in_range(fabsf(uf)), cc, d);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) e[q] = __fsub_rn(t[q], d[q]);
         if (active) {
-          record4(t, d, err, tsq);
-          const int64_t e = row * C + c0 + col;
-          float4 nb, na;
+          record4(t, e, err, tsq);
+          const int64_t eo = row * C + c0 + col;
           if constexpr (MODE == CC_NAIVE) {
-            nb = make_float4(d[0], d[1], d[2], d[3]);
+            stg_cs4(p.base + eo, make_float4(d[0], d[1], d[2], d[3]));
           } else {
-            nb = make_float4(__fadd_rn(bb[0], d[0]), __fadd_rn(bb[1], d[1]), __fadd_rn(bb[2], d[2]),
-                             __fadd_rn(bb[3], d[3]));
+            stg_cs4(p.base + eo, make_float4(__fadd_rn(bb[0], d[0]), __fadd_rn(bb[1], d[1]), __fadd_rn(bb[2], d[2]),
+                                             __fadd_rn(bb[3], d[3])));
             if constexpr (MODE == CC_WITH_FEEDBACK)
-              na = make_float4(__fsub_rn(t[0], d[0]), __fsub_rn(t[1], d[1]), __fsub_rn(t[2], d[2]),
-                               __fsub_rn(t[3], d[3]));
+              stg_cs4(p.aux + eo, make_float4(e[0], e[1], e[2], e[3]));
             else
-              na = make_float4(xx[0], xx[1], xx[2], xx[3]);
-            stg_cs4(p.aux + e, na);
+              stg_cs4(p.aux + eo, make_float4(xx[0], xx[1], xx[2], xx[3]));
           }
-          stg_cs4(p.base + e, nb);
         }
         if constexpr (CODEC == CC_SIGN1) {
           const uint32_t other = __shfl_down_sync(0xffffffffu, packed, 1);
@@ -428,6 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       if (lane == 0) mbar_arrive(&empty[s]);
     }
   }
+  stamp(5);
   {
     const double es = block_sum(err, red);
     const double ts = block_sum(tsq, red);
@@ -448,6 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       }
     }
   }
+  stamp(6);
 }
 
 }  // namespace fused
@@ -481,7 +546,9 @@ static int launch_fused(fused::Params &p, cudaStream_t st) {
 }
 
 static int g_fused_stop = 0;
+static unsigned long long *g_fused_timer = nullptr;
 void set_fused_stop(int v) { g_fused_stop = v; }
+void set_fused_timer(void *buf) { g_fused_timer = reinterpret_cast<unsigned long long *>(buf); }
 
 bool fused_supported(int64_t n, int64_t C, const void *x, int x_dtype, const float *base, const float *aux,
                      const uint8_t *body) {
@@ -527,6 +594,7 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   p.nTiles = cdiv(n, p.R) * p.nStrips;
   p.scale_mode = scale_mode;
   p.stop_after = g_fused_stop;
+  p.timer = g_fused_timer;
   const int bits = codec == CC_SIGN1 ? 1 : (codec == CC_QUANT2 ? 2 : 4);
   const int64_t cbytes = cdiv(n * C * bits, 8);
   p.codes = body;
@@ -541,7 +609,7 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
     off = align_up(off + bytes, 256);
     return q;
   };
-  const int slots = (G / p.nStrips) * fused::kGroups;
+  const int slots = G / p.nStrips;
   p.colpart = reinterpret_cast<double *>(take(sizeof(double) * (size_t)slots * C));
   p.rowpart = reinterpret_cast<double *>(take(sizeof(double) * (size_t)p.nStrips * n));
   p.rowsum = reinterpret_cast<double *>(take(sizeof(double) * n));

@@ -75,6 +75,21 @@ def main():
         out[name] = {"us": round(us, 2), "alg_GBps": round(alg / us / 1e3, 1)}
     lib.cc_set_quant_path(-1)
     lib.cc_debug_fused_stop(0)
+    # per-phase timeline of one fused launch (globaltimer stamps per CTA)
+    tbuf = torch.zeros(1024 * 8, dtype=torch.int64, device="cuda")
+    lib.cc_debug_fused_timer(_lib.ptr(tbuf))
+    for i in range(3):
+        enc(i)
+    torch.cuda.synchronize()
+    lib.cc_debug_fused_timer(None)
+    tb = tbuf.view(1024, 8).cpu()
+    g = int((tb[:, 0] > 0).sum())
+    tb = tb[:g].double()
+    t0 = tb[:, 0].min()
+    names = ["start", "A_done", "sync1", "F_done", "sync2", "B_done", "end"]
+    out["fused_timeline_us"] = {nm: [round(float((tb[:, i] - t0).min()) / 1e3, 2),
+                                     round(float((tb[:, i] - t0).max()) / 1e3, 2)] for i, nm in enumerate(names)}
+    out["fused_grid"] = g
     # K2: accumulate decode of the last body into each layer's base
     bases = [st.base for st in sts]
 
