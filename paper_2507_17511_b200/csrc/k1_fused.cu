@@ -1,26 +1,28 @@
 // K1, persistent form: ONE cooperative kernel per encode_step for the 1/2/4-bit
-// codecs on row strips of 1024 columns (C % 1024 == 0, e.g. FLUX's 3072).
+// codecs (C % 128 == 0 and C <= 3072, e.g. FLUX's 3072 or a Ulysses chunk of 384).
 //
-//   phase A  stream (x, base, aux) tiles global->smem with cp.async.bulk (1-D TMA)
-//            on a multi-stage mbarrier ring fed by a producer warp; 8 consumer
-//            warps form t = target(x, base, aux) (pipeline.py:99-104) and
-//            accumulate |t| in f64: column partials in registers (each CTA owns
-//            a fixed strip), row partials per tile through shared memory.
+// Tiles are R FULL rows, so every array of a tile is one contiguous range and
+// moves with a single cp.async.bulk (1-D TMA) per array:
+//   phase A  producer warp: TMA loads of (x, base, aux) tiles into a multi-stage
+//            mbarrier ring (L2::evict_last); 12 consumer warps form
+//            t = target(x, base, aux) (pipeline.py:99-104) and accumulate |t| in
+//            f64: column partials in registers, row partials through shared
+//            memory (summed by the producer lanes in a fixed order).
 //   grid.sync
-//   phase F1 column sums -> v_j = colmean (f32), row sums, per-CTA row-sum partials
+//   phase F  v_j = colmean (8 lanes per column, fixed split), g = mean|t| (same
+//            fixed-order tree in every CTA), u_i = max(rowmean_i / g, 1e-30)
+//            (compressors.py:135-149); u, v straight into the body.
 //   grid.sync
-//   phase F2 g = mean|t| (identical fixed-order tree in every CTA),
-//            u_i = max(rowmean_i / g, 1e-30) (compressors.py:135-149)
-//   grid.sync
-//   phase B  stream the SAME tiles in reverse order (the tail of phase A is
-//            still L2-resident; phase-A loads carry L2::evict_last, phase-B loads
-//            evict_first), quantize (compressors.py:373-391), pack codes, write
-//            base' / feedback' / ref' with streaming stores (pipeline.py:107-113),
+//   phase B  the SAME tiles in reverse order (the tail of phase A is still
+//            L2-resident): consumers quantize (compressors.py:373-391) and write
+//            base' / feedback' / ref' (pipeline.py:107-113) and the packed codes
+//            IN PLACE into the stage; the producer drains each stage to HBM with
+//            TMA bulk stores (cp.async.bulk.global.shared) before refilling it.
 //            StepRecord partials -> last-CTA ticket reduction (pipeline.py:115-120).
 //
 // Results are bit-identical to the multi-kernel path in quant.cu (same f64
-// reduction trees per element group, same code/decode arithmetic); the parity
-// tests run both.
+// element arithmetic; reductions are deterministic f64 trees), pinned by the
+// parity tests that run both paths against the oracle.
 #include <cooperative_groups.h>
 
 #include "cc_async.cuh"
@@ -28,33 +30,34 @@
 #include "cc_internal.h"
 
 #include <algorithm>
+#include <string>
 
 namespace cg = cooperative_groups;
 
 namespace cc {
 namespace fused {
 
-constexpr int kGroupThreads = 256;  // one row group: 8 warps x 32 lanes x 4 columns = 1024-column strip
-constexpr int kGroups = 2;          // row groups (alternate rows of a tile) -> 16 consumer warps
-constexpr int kGWarps = kGroupThreads / 32;
-constexpr int kConsumers = kGroups * kGroupThreads;
-constexpr int kCWarps = kConsumers / 32;
-constexpr int kThreads = kConsumers + 32;  // + producer warp
-constexpr int kStrip = 4 * kGroupThreads;
-constexpr int kRowsBuffered = 16;  // stages * rows-per-tile
+constexpr int kCons = 384;             // consumer threads (12 warps)
+constexpr int kCW = kCons / 32;
+constexpr int kThreads = kCons + 32;   // + producer warp
+constexpr int kMaxC = 2 * 4 * kCons;   // 3072 columns: two column quads per consumer thread
+constexpr int kUCache = 512;           // cached u_i per CTA for phase B
+constexpr size_t kSmemBudget = 190 * 1024;
 
 struct Params {
   const void *x;
   float *base, *aux;
   int64_t n, C;
-  int nStrips, R, S, G;
+  int G4, groups, wpg;  // column quads, row groups, warps per group
+  int R, S, G;
+  int cb_row;           // code bytes per row
   int64_t nTiles;
-  double *colpart, *rowpart, *rowsum, *blkpart, *recpart, *record;
+  double *colpart, *rowpart, *blkpart, *recpart, *record;
   float *u, *v;
   uint8_t *codes, *body_u, *body_v;
   unsigned int *ticket;
   int scale_mode;
-  int stop_after;  // profiling: 1 = phase A only, 2 = A + scales, 0 = full
+  int stop_after;             // profiling: 1 = phase A only, 2 = A + scales, 0 = full
   unsigned long long *timer;  // profiling: [G][8] globaltimer stamps, or null
 };
 
@@ -62,14 +65,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
-}
-
-constexpr int kUCache = 512;  // cached u_i per CTA for phase B
-
-// f32 state arrays staged per tile: base + aux (feedback or ref); naive mode none
-template <int MODE>
-constexpr int n_f32_arrays() {
-  return MODE == CC_NAIVE ? 0 : 2;
 }
 
 // deterministic block sum over all kThreads threads (fixed pairing)
@@ -205,30 +200,59 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int MODE, int CODEC, typename XT>
+template <int MODE>
+constexpr bool has_aux() {
+  return MODE != CC_NAIVE;
+}
+
+struct StageLayout {
+  uint32_t x, base, aux, codes, bytes;  // byte offsets inside one stage
+};
+
+template <int MODE, typename XT>
+__host__ __device__ inline StageLayout stage_layout(int R, int64_t C, int cb_row) {
+  auto al = [](uint32_t v) { return (v + 127u) & ~127u; };
+  StageLayout L;
+  L.x = 0;
+  L.base = al((uint32_t)(R * C * sizeof(XT)));
+  L.aux = al(L.base + (uint32_t)(R * C * 4));
+  L.codes = has_aux<MODE>() ? al(L.aux + (uint32_t)(R * C * 4)) : L.aux;
+  L.bytes = al(L.codes + (uint32_t)(R * cb_row));
+  return L;
+}
+
+// Q = column quads per consumer thread (1: C <= 1536, row groups; 2: C <= 3072)
+template <int MODE, int CODEC, typename XT, int Q>
 __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ Params p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int NF = n_f32_arrays<MODE>();
+  constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
   const int R = p.R, S = p.S, G = p.G;
   const int64_t n = p.n, C = p.C;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cta = blockIdx.x;
-  const int strip = cta % p.nStrips;
-  const int64_t c0 = (int64_t)strip * kStrip;
-  const int width = (int)min64(kStrip, C - c0);
-  const bool producer = warp == kCWarps;
-  const int grp = producer ? 0 : tid / kGroupThreads;  // consumer row group
-  const int gtid = tid % kGroupThreads;
-  const int gwarp = gtid >> 5;
+  const bool producer = warp == kCW;
+  // consumer mapping
+  int grp = 0, quad0 = tid, wig = warp;
+  if constexpr (Q == 1) {
+    grp = tid / p.G4;
+    quad0 = tid % p.G4;
+    wig = quad0 >> 5;
+  }
+  const bool in_group = !producer && grp < p.groups;
+  bool qact[Q];
+  int qcol[Q];
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {
+    const int qd = quad0 + j * kCons;
+    qact[j] = in_group && qd < p.G4;
+    qcol[j] = 4 * qd;
+  }
 
-  // ---- shared memory carve-up ----
-  const size_t xs_bytes = (size_t)R * kStrip * sizeof(XT);
-  const size_t fs_bytes = (size_t)R * kStrip * sizeof(float);
-  const size_t stage_bytes = xs_bytes + NF * fs_bytes;
+  const StageLayout L = stage_layout<MODE, XT>(R, C, p.cb_row);
   uint8_t *tiles = smem;
-  double *rp = reinterpret_cast<double *>(smem + (size_t)S * stage_bytes);  // [S][R][kGWarps]
-  double *red = rp + (size_t)S * R * kGWarps;                               // block-sum scratch
-  float *ucache = reinterpret_cast<float *>(red + 64);                        // [kUCache]
+  double *rp = reinterpret_cast<double *>(smem + (size_t)S * L.bytes);  // [S][R][kCW]
+  double *red = rp + (size_t)S * R * kCW;                               // block-sum scratch [64]
+  float *ucache = reinterpret_cast<float *>(red + 64);                   // [kUCache]
   uint64_t *full = reinterpret_cast<uint64_t *>(ucache + kUCache);
   uint64_t *empty = full + S;
 
@@ -239,133 +263,140 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kCWarps);
+      mbar_init(&empty[s], kCW);
     }
     mbar_fence_init();
   }
   __syncthreads();
 
-  // tiles of this CTA: T_k = cta + k*G, k < K (strip fixed because G % nStrips == 0)
-  const int64_t K = p.nTiles > cta ? (p.nTiles - 1 - cta) / G + 1 : 0;
-  auto tile_r0 = [&](int64_t k) -> int64_t { return ((cta + k * G) / p.nStrips) * (int64_t)R; };
-  auto stage_x = [&](int s) { return reinterpret_cast<XT *>(tiles + (size_t)s * stage_bytes); };
-  auto stage_b = [&](int s) { return reinterpret_cast<float *>(tiles + (size_t)s * stage_bytes + xs_bytes); };
-  auto stage_a = [&](int s) {
-    return reinterpret_cast<float *>(tiles + (size_t)s * stage_bytes + xs_bytes + fs_bytes);
-  };
-  double cta_total = 0.0;  // producer lanes: running sum of this CTA's row partials
-  auto finish_rows = [&](int s, int64_t k) {  // producer lanes: per-row sums over the 8 warps of a group
-    const int64_t r0p = tile_r0(k);
-    if (lane < R && r0p + lane < n) {
+  const int64_t K = p.nTiles > cta ? (p.nTiles - 1 - cta) / G + 1 : 0;  // tiles cta, cta+G, ...
+  auto tile_r0 = [&](int64_t k) -> int64_t { return (cta + k * G) * (int64_t)R; };
+  auto sx = [&](int s) { return reinterpret_cast<XT *>(tiles + (size_t)s * L.bytes + L.x); };
+  auto sb = [&](int s) { return reinterpret_cast<float *>(tiles + (size_t)s * L.bytes + L.base); };
+  auto sa = [&](int s) { return reinterpret_cast<float *>(tiles + (size_t)s * L.bytes + L.aux); };
+  auto sc = [&](int s) { return tiles + (size_t)s * L.bytes + L.codes; };
+  const XT *X = reinterpret_cast<const XT *>(p.x);
+
+  double cta_total = 0.0;  // producer lanes (phase A)
+  auto finish_rows = [&](int s, int64_t k) {
+    const int64_t r0 = tile_r0(k);
+    if (lane < R && r0 + lane < n) {
       double acc = 0.0;
-      for (int w = 0; w < kGWarps; ++w) acc += rp[((size_t)s * R + lane) * kGWarps + w];
-      p.rowpart[(int64_t)strip * n + r0p + lane] = acc;
+      for (int w = 0; w < p.wpg; ++w) acc += rp[((size_t)s * R + lane) * kCW + w];
+      p.rowpart[r0 + lane] = acc;
       cta_total += acc;
     }
   };
-
-  const XT *X = reinterpret_cast<const XT *>(p.x);
-  // ---------------- producer warp ----------------
-  // phaseB: stage base too in no-feedback mode (t only needs x - ref, the update needs base)
-  auto produce = [&](int64_t seq0, bool phaseB, uint64_t policy) {
-    for (int64_t k = 0; k < K; ++k) {
-      const int64_t seq = seq0 + k;
-      const int s = (int)(seq % S);
-      const int64_t use = seq / S;
-      if (use > 0) {
-        mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
-        if (!phaseB && k >= S) finish_rows(s, k - S);
-      }
-      if (lane == 0) {
-        const int64_t kk = phaseB ? (K - 1 - k) : k;
-        const int64_t r0 = tile_r0(kk);
-        const int nrows = (int)min64(R, n - r0);
-        const bool need_base = MODE == CC_WITH_FEEDBACK || (MODE == CC_NO_FEEDBACK && phaseB);
-        const uint32_t xrow = (uint32_t)(width * sizeof(XT)), frow = (uint32_t)(width * sizeof(float));
-        const uint32_t per = xrow + (need_base ? frow : 0u) + (NF ? frow : 0u);
-        mbar_expect_tx(&full[s], (uint32_t)nrows * per);
-        for (int r = 0; r < nrows; ++r) {
-          const int64_t e = (r0 + r) * C + c0;
-          bulk_g2s(stage_x(s) + (size_t)r * kStrip, X + e, xrow, &full[s], policy);
-          if (need_base) bulk_g2s(stage_b(s) + (size_t)r * kStrip, p.base + e, frow, &full[s], policy);
-          if constexpr (NF) bulk_g2s(stage_a(s) + (size_t)r * kStrip, p.aux + e, frow, &full[s], policy);
-        }
-      }
-      __syncwarp();
-    }
+  auto issue_loads = [&](int s, int64_t kk, bool with_base, uint64_t pol) {
+    const int64_t r0 = tile_r0(kk);
+    const int nrows = (int)min64(R, n - r0);
+    const uint32_t xb = (uint32_t)(nrows * C * sizeof(XT)), fb = (uint32_t)(nrows * C * 4);
+    const bool aux = has_aux<MODE>();
+    mbar_expect_tx(&full[s], xb + (with_base ? fb : 0u) + (aux ? fb : 0u));
+    bulk_g2s(sx(s), X + r0 * C, xb, &full[s], pol);
+    if (with_base) bulk_g2s(sb(s), p.base + r0 * C, fb, &full[s], pol);
+    if (aux) bulk_g2s(sa(s), p.aux + r0 * C, fb, &full[s], pol);
   };
-
-  const int col = 4 * gtid;  // consumer's first column inside the strip
-  const bool active = !producer && col < width;
-  auto load_row = [&](int s, int r, float (&xx)[4], float (&bb)[4], float (&aa)[4], bool with_base) {
-    if constexpr (sizeof(XT) == 2) {
-      const uint2 raw = *reinterpret_cast<const uint2 *>(stage_x(s) + (size_t)r * kStrip + col);
-      xx[0] = __uint_as_float(raw.x << 16);
-      xx[1] = __uint_as_float(raw.x & 0xffff0000u);
-      xx[2] = __uint_as_float(raw.y << 16);
-      xx[3] = __uint_as_float(raw.y & 0xffff0000u);
-    } else {
-      const float4 v = lds4(reinterpret_cast<const float *>(stage_x(s)) + (size_t)r * kStrip + col);
-      xx[0] = v.x; xx[1] = v.y; xx[2] = v.z; xx[3] = v.w;
-    }
-    if (NF && with_base) {
-      const float4 v = lds4(stage_b(s) + (size_t)r * kStrip + col);
-      bb[0] = v.x; bb[1] = v.y; bb[2] = v.z; bb[3] = v.w;
-    }
-    if constexpr (NF) {
-      const float4 v = lds4(stage_a(s) + (size_t)r * kStrip + col);
-      aa[0] = v.x; aa[1] = v.y; aa[2] = v.z; aa[3] = v.w;
-    }
+  auto issue_stores = [&](int s, int64_t kk) {  // phase-B results of tile kk sitting in stage s
+    const int64_t r0 = tile_r0(kk);
+    const int nrows = (int)min64(R, n - r0);
+    bulk_s2g(p.base + r0 * C, sb(s), (uint32_t)(nrows * C * 4));
+    if constexpr (has_aux<MODE>()) bulk_s2g(p.aux + r0 * C, sa(s), (uint32_t)(nrows * C * 4));
+    bulk_s2g(p.codes + r0 * p.cb_row, sc(s), (uint32_t)(nrows * p.cb_row));
+    bulk_commit();
   };
 
   // ================= phase A: |t| partial sums =================
   if (producer) {
-    produce(0, false, l2_policy_evict_last());
-    for (int64_t k = K - min64(S, K); k < K; ++k) {  // drain the last tiles' row sums
+    const uint64_t pol = l2_policy_evict_last();
+    for (int64_t k = 0; k < K; ++k) {
+      const int s = (int)(k % S);
+      if (k >= S) {
+        mbar_wait(&empty[s], (uint32_t)(((k / S) - 1) & 1));
+        finish_rows(s, k - S);
+      }
+      if (lane == 0) issue_loads(s, k, MODE == CC_WITH_FEEDBACK, pol);
+      __syncwarp();
+    }
+    for (int64_t k = K - min64(S, K); k < K; ++k) {  // drain: row sums of the last tiles
       const int s = (int)(k % S);
       mbar_wait(&empty[s], (uint32_t)((k / S) & 1));
       finish_rows(s, k);
     }
   } else {
-    double cs[4] = {0.0, 0.0, 0.0, 0.0};
+    double cs[Q][4];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) cs[j][0] = cs[j][1] = cs[j][2] = cs[j][3] = 0.0;
     for (int64_t k = 0; k < K; ++k) {
       const int s = (int)(k % S);
       mbar_wait(&full[s], (uint32_t)((k / S) & 1));
-      const int64_t r0 = tile_r0(k);
-      const int nrows = (int)min64(R, n - r0);
-      for (int r = grp; r < nrows; r += kGroups) {
-        float xx[4] = {0.f, 0.f, 0.f, 0.f}, bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f};
-        double a[4] = {0.0, 0.0, 0.0, 0.0};
-        if (active) {
-          load_row(s, r, xx, bb, aa, MODE == CC_WITH_FEEDBACK);
+      const int nrows = (int)min64(R, n - tile_r0(k));
+      if (grp < p.groups) {
+        for (int r = grp; r < nrows; r += p.groups) {
+          double rs = 0.0;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) a[q] = fabs((double)target_of<MODE>(xx[q], bb[q], aa[q]));
+          for (int j = 0; j < Q; ++j) {
+            if (!qact[j]) continue;
+            const size_t o = (size_t)r * C + qcol[j];
+            float xx[4], bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f};
+            if constexpr (sizeof(XT) == 2) {
+              const uint2 raw = *reinterpret_cast<const uint2 *>(sx(s) + o);
+              xx[0] = __uint_as_float(raw.x << 16); xx[1] = __uint_as_float(raw.x & 0xffff0000u);
+              xx[2] = __uint_as_float(raw.y << 16); xx[3] = __uint_as_float(raw.y & 0xffff0000u);
+            } else {
+              const float4 v = lds4(reinterpret_cast<const float *>(sx(s)) + o);
+              xx[0] = v.x; xx[1] = v.y; xx[2] = v.z; xx[3] = v.w;
+            }
+            if constexpr (MODE == CC_WITH_FEEDBACK) {
+              const float4 v = lds4(sb(s) + o);
+              bb[0] = v.x; bb[1] = v.y; bb[2] = v.z; bb[3] = v.w;
+            }
+            if constexpr (has_aux<MODE>()) {
+              const float4 v = lds4(sa(s) + o);
+              aa[0] = v.x; aa[1] = v.y; aa[2] = v.z; aa[3] = v.w;
+            }
+            double a[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              a[q] = fabs((double)target_of<MODE>(xx[q], bb[q], aa[q]));
+              cs[j][q] += a[q];
+            }
+            rs += ((a[0] + a[1]) + a[2]) + a[3];
+          }
+          rs = warp_sum(rs);
+          if (lane == 0) rp[((size_t)s * R + r) * kCW + wig] = rs;
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) cs[q] += a[q];
-        double rs = ((a[0] + a[1]) + a[2]) + a[3];
-        rs = warp_sum(rs);
-        if (lane == 0) rp[((size_t)s * R + r) * kGWarps + gwarp] = rs;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    // merge the two row groups' column partials (fixed order g0 + g1) through smem
-    double *xchg = reinterpret_cast<double *>(tiles);
-    named_sync(1, kConsumers);  // all consumers done with the last stage
-    if (grp == 1) {
+    // column partials; row groups merged in a fixed order through smem
+    if constexpr (Q == 1) {
+      double *xchg = reinterpret_cast<double *>(tiles);
+      named_sync(1, kCons);
+      if (in_group && qact[0]) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) xchg[4 * gtid + q] = cs[q];
-    }
-    named_sync(1, kConsumers);
-    if (grp == 0 && active) {
-      double *cp = p.colpart + (int64_t)(cta / p.nStrips) * C + c0 + col;
+        for (int q = 0; q < 4; ++q) xchg[((size_t)grp * p.G4 + quad0) * 4 + q] = cs[0][q];
+      }
+      named_sync(1, kCons);
+      if (in_group && grp == 0 && qact[0]) {
+        double *cp = p.colpart + (int64_t)cta * C + qcol[0];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) cp[q] = cs[q] + xchg[4 * gtid + q];
+        for (int q = 0; q < 4; ++q) {
+          double v = cs[0][q];
+          for (int g2 = 1; g2 < p.groups; ++g2) v += xchg[((size_t)g2 * p.G4 + quad0) * 4 + q];
+          cp[q] = v;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        if (!qact[j]) continue;
+        double *cp = p.colpart + (int64_t)cta * C + qcol[j];
+        cp[0] = cs[j][0]; cp[1] = cs[j][1]; cp[2] = cs[j][2]; cp[3] = cs[j][3];
+      }
     }
   }
-
-  // per-CTA |t| total (deterministic: fixed lane order) -> blkpart
   {
     const double b = block_sum(producer ? cta_total : 0.0, red);
     if (tid == 0) p.blkpart[cta] = b;
@@ -376,23 +407,21 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   stamp(2);
   if (p.stop_after == 1) return;
 
-  // ================= phase F: v_j (column means), g, u_i =================
-  const int slots = G / p.nStrips;
+  // ================= phase F: v_j, g, u_i =================
   if (cta == 0 && tid == 0) *p.ticket = 0u;
   {
-    // 8 lanes per column, fixed split of the slots, fixed butterfly combine
     const int64_t gid = (int64_t)cta * kThreads + tid;
-    const int64_t nthr = (int64_t)G * kThreads;
-    for (int64_t base_id = gid - (gid & 7); base_id < C * 8; base_id += nthr - (nthr & 7)) {
-      const int64_t j = base_id / 8;
+    const int64_t nthr = (int64_t)G * kThreads;  // multiple of 32
+    for (int64_t b8 = gid & ~7LL; b8 < C * 8; b8 += nthr) {
+      const int64_t j = b8 >> 3;
       const int part = (int)(gid & 7);
-      double sacc = 0.0;
-      for (int q = part; q < slots; q += 8) sacc += __ldcg(p.colpart + (int64_t)q * C + j);
-      sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
-      sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
-      sacc += __shfl_xor_sync(0xffffffffu, sacc, 4);
+      double acc = 0.0;
+      for (int q = part; q < G; q += 8) acc += __ldcg(p.colpart + (int64_t)q * C + j);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
       if (part == 0) {
-        float v = (float)(sacc / (double)n);  // colmean (cx:148)
+        float v = (float)(acc / (double)n);  // colmean (cx:148)
         if (p.scale_mode == CC_SCALE_PER_TOKEN) v = 1.0f;
         p.v[j] = v;
         store_f32_bytes(p.body_v + 4 * j, v);
@@ -406,8 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     const int64_t ch = (n + G - 1) / G;
     const int64_t i0 = (int64_t)cta * ch, i1 = min64(n, i0 + ch);
     for (int64_t i = i0 + tid; i < i1; i += kThreads) {
-      double rs = 0.0;
-      for (int s = 0; s < p.nStrips; ++s) rs += __ldcg(p.rowpart + (int64_t)s * n + i);
+      const double rs = __ldcg(p.rowpart + i);
       float u;
       if (p.scale_mode == CC_SCALE_PER_CHANNEL) u = 1.0f;
       else if (p.scale_mode == CC_SCALE_PER_TOKEN) u = (float)(rs / (double)C);
@@ -422,7 +450,6 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   stamp(4);
   if (p.stop_after == 2) return;
 
-  // u_i of every row this CTA quantizes, in phase-B order
   const bool ucached = K * R <= kUCache;
   if (ucached) {
     for (int i = tid; i < K * R; i += kThreads) {
@@ -432,20 +459,44 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   }
   __syncthreads();
 
-  // ================= phase B: quantize, pack, update state =================
+  // ================= phase B: quantize, pack, update state (in place) =================
   double err = 0.0, tsq = 0.0;
   if (producer) {
-    produce(K, true, l2_policy_evict_first());
+    const uint64_t pol = l2_policy_evict_first();
+    for (int64_t k = 0; k < K; ++k) {
+      const int64_t seq = K + k;
+      const int s = (int)(seq % S);
+      if (seq >= S) mbar_wait(&empty[s], (uint32_t)(((seq / S) - 1) & 1));
+      if (lane == 0) {
+        if (seq - S >= K) {  // previous occupant was a phase-B tile: drain it first
+          issue_stores(s, K - 1 - (k - S));
+          bulk_wait_read<0>();
+        }
+        issue_loads(s, K - 1 - k, has_aux<MODE>(), pol);
+      }
+      __syncwarp();
+    }
+    for (int64_t k = K - min64(S, K); k < K; ++k) {
+      const int64_t seq = K + k;
+      const int s = (int)(seq % S);
+      mbar_wait(&empty[s], (uint32_t)((seq / S) & 1));
+      if (lane == 0) issue_stores(s, K - 1 - k);
+    }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
   } else {
-    ColConst cc;
-    cc.ok = true;
+    ColConst cc[Q];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float v = active ? __ldcg(p.v + c0 + col + q) : 1.0f;
-      cc.v[q] = v;
-      cc.vhi[q] = __fmul_ru(__fmul_ru(v, 1.25f), 1.00000095367431640625f);  // (1 + 2^-20)
-      cc.vlo[q] = __fmul_rd(__fmul_rd(v, 1.25f), 0.99999904632568359375f);  // (1 - 2^-20)
-      cc.ok = cc.ok && scale_in_range(fabsf(v));
+    for (int j = 0; j < Q; ++j) {
+      cc[j].ok = true;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float v = qact[j] ? __ldcg(p.v + qcol[j] + q) : 1.0f;
+        cc[j].v[q] = v;
+        cc[j].vhi[q] = __fmul_ru(__fmul_ru(v, 1.25f), 1.00000095367431640625f);  // (1 + 2^-20)
+        cc[j].vlo[q] = __fmul_rd(__fmul_rd(v, 1.25f), 0.99999904632568359375f);  // (1 - 2^-20)
+        cc[j].ok = cc[j].ok && scale_in_range(fabsf(v));
+      }
     }
     for (int64_t k = 0; k < K; ++k) {
       const int64_t seq = K + k;
@@ -453,40 +504,63 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       mbar_wait(&full[s], (uint32_t)((seq / S) & 1));
       const int64_t r0 = tile_r0(K - 1 - k);
       const int nrows = (int)min64(R, n - r0);
-      for (int r = grp; r < nrows; r += kGroups) {
-        const int64_t row = r0 + r;
-        const float uf = ucached ? ucache[k * R + r] : __ldcg(p.u + row);
-        float xx[4] = {0.f, 0.f, 0.f, 0.f}, bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f};
-        if (active) load_row(s, r, xx, bb, aa, true);
-        float t[4], d[4], e[4];
+      if (grp < p.groups) {
+        for (int r = grp; r < nrows; r += p.groups) {
+          const float uf = ucached ? ucache[k * R + r] : __ldcg(p.u + r0 + r);
+          const bool row_ok = scale_in_range(fabsf(uf));
 #pragma unroll
-        for (int q = 0; q < 4; ++q) t[q] = target_of<MODE>(xx[q], bb[q], aa[q]);
-        const uint32_t packed = quantize4<CODEC>(t, uf, scale_in_range(fabsf(uf)), cc, d);
+          for (int j = 0; j < Q; ++j) {
+            const size_t o = (size_t)r * C + qcol[j];
+            float xx[4] = {0.f, 0.f, 0.f, 0.f}, bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f};
+            if (qact[j]) {
+              if constexpr (sizeof(XT) == 2) {
+                const uint2 raw = *reinterpret_cast<const uint2 *>(sx(s) + o);
+                xx[0] = __uint_as_float(raw.x << 16); xx[1] = __uint_as_float(raw.x & 0xffff0000u);
+                xx[2] = __uint_as_float(raw.y << 16); xx[3] = __uint_as_float(raw.y & 0xffff0000u);
+              } else {
+                const float4 v = lds4(reinterpret_cast<const float *>(sx(s)) + o);
+                xx[0] = v.x; xx[1] = v.y; xx[2] = v.z; xx[3] = v.w;
+              }
+              if constexpr (has_aux<MODE>()) {
+                const float4 v = lds4(sb(s) + o);
+                bb[0] = v.x; bb[1] = v.y; bb[2] = v.z; bb[3] = v.w;
+                const float4 w = lds4(sa(s) + o);
+                aa[0] = w.x; aa[1] = w.y; aa[2] = w.z; aa[3] = w.w;
+              }
+            }
+            float t[4], d[4], e[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) e[q] = __fsub_rn(t[q], d[q]);
-        if (active) {
-          record4(t, e, err, tsq);
-          const int64_t eo = row * C + c0 + col;
-          if constexpr (MODE == CC_NAIVE) {
-            stg_cs4(p.base + eo, make_float4(d[0], d[1], d[2], d[3]));
-          } else {
-            stg_cs4(p.base + eo, make_float4(__fadd_rn(bb[0], d[0]), __fadd_rn(bb[1], d[1]), __fadd_rn(bb[2], d[2]),
-                                             __fadd_rn(bb[3], d[3])));
-            if constexpr (MODE == CC_WITH_FEEDBACK)
-              stg_cs4(p.aux + eo, make_float4(e[0], e[1], e[2], e[3]));
-            else
-              stg_cs4(p.aux + eo, make_float4(xx[0], xx[1], xx[2], xx[3]));
+            for (int q = 0; q < 4; ++q) t[q] = target_of<MODE>(xx[q], bb[q], aa[q]);
+            const uint32_t packed = quantize4<CODEC>(t, uf, row_ok, cc[j], d);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) e[q] = __fsub_rn(t[q], d[q]);
+            if (qact[j]) {
+              record4(t, e, err, tsq);
+              float4 nb;
+              if constexpr (MODE == CC_NAIVE) {
+                nb = make_float4(d[0], d[1], d[2], d[3]);
+              } else {
+                nb = make_float4(__fadd_rn(bb[0], d[0]), __fadd_rn(bb[1], d[1]), __fadd_rn(bb[2], d[2]),
+                                 __fadd_rn(bb[3], d[3]));
+                *reinterpret_cast<float4 *>(sa(s) + o) = MODE == CC_WITH_FEEDBACK
+                                                             ? make_float4(e[0], e[1], e[2], e[3])
+                                                             : make_float4(xx[0], xx[1], xx[2], xx[3]);
+              }
+              *reinterpret_cast<float4 *>(sb(s) + o) = nb;
+            }
+            uint8_t *crow = sc(s) + (size_t)r * p.cb_row;
+            if constexpr (CODEC == CC_SIGN1) {
+              const uint32_t other = __shfl_down_sync(0xffffffffu, packed, 1);
+              if (qact[j] && (lane & 1) == 0) crow[qcol[j] >> 3] = (uint8_t)(packed | (other << 4));
+            } else if constexpr (CODEC == CC_QUANT2) {
+              if (qact[j]) crow[qcol[j] >> 2] = (uint8_t)packed;
+            } else {
+              if (qact[j]) *reinterpret_cast<uint16_t *>(crow + (qcol[j] >> 1)) = (uint16_t)packed;
+            }
           }
         }
-        if constexpr (CODEC == CC_SIGN1) {
-          const uint32_t other = __shfl_down_sync(0xffffffffu, packed, 1);
-          if (active && (lane & 1) == 0) p.codes[(row * C + c0 + col) >> 3] = (uint8_t)(packed | (other << 4));
-        } else if constexpr (CODEC == CC_QUANT2) {
-          if (active) p.codes[(row * C + c0 + col) >> 2] = (uint8_t)packed;
-        } else {
-          if (active) *reinterpret_cast<uint16_t *>(p.codes + ((row * C + c0 + col) >> 1)) = (uint16_t)packed;
-        }
       }
+      fence_proxy_async_smem();  // our smem results -> visible to the TMA store
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
@@ -495,18 +569,19 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   {
     const double es = block_sum(err, red);
     const double ts = block_sum(tsq, red);
+    __shared__ unsigned last;
     if (tid == 0) {
       p.recpart[2 * cta] = es;
       p.recpart[2 * cta + 1] = ts;
       __threadfence();
-      const unsigned prev = atomicAdd(p.ticket, 1u);
-      if (prev == (unsigned)G - 1) {
-        __threadfence();
-        double a = 0.0, b = 0.0;
-        for (int c = 0; c < G; ++c) {
-          a += __ldcg(p.recpart + 2 * c);
-          b += __ldcg(p.recpart + 2 * c + 1);
-        }
+      last = atomicAdd(p.ticket, 1u) == (unsigned)G - 1;
+    }
+    __syncthreads();
+    if (last) {  // the last CTA reduces the per-CTA partials in a fixed order
+      __threadfence();
+      const double a = block_sum(tid < G ? __ldcg(p.recpart + 2 * tid) : 0.0, red);
+      const double b = block_sum(tid < G ? __ldcg(p.recpart + 2 * tid + 1) : 0.0, red);
+      if (tid == 0) {
         p.record[0] = a;
         p.record[1] = b;
       }
@@ -520,22 +595,52 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-static size_t fused_smem(int mode, int xsize, int R, int S) {
-  const int NF = mode == CC_NAIVE ? 0 : 2;
-  const size_t stage = (size_t)R * fused::kStrip * (xsize + 4 * NF);
-  const size_t rp = (size_t)S * R * fused::kGWarps * sizeof(double);
-  const size_t red = 64 * sizeof(double) + fused::kUCache * sizeof(float);  // block-sum scratch + u cache
-  return (size_t)S * stage + rp + red + 2 * S * sizeof(uint64_t) + 256;
+static int g_fused_stop = 0;
+static unsigned long long *g_fused_timer = nullptr;
+void set_fused_stop(int v) { g_fused_stop = v; }
+void set_fused_timer(void *buf) { g_fused_timer = reinterpret_cast<unsigned long long *>(buf); }
+
+bool fused_supported(int64_t n, int64_t C, const void *x, int x_dtype, const float *base, const float *aux,
+                     const uint8_t *body) {
+  (void)n;
+  (void)x_dtype;
+  if (C % 128 != 0 || C > fused::kMaxC) return false;
+  if (!aligned(x, 16) || !aligned(base, 16) || (aux && !aligned(aux, 16)) || !aligned(body, 16)) return false;
+  return true;
 }
 
-template <int MODE, int CODEC, typename XT>
+int64_t fused_workspace_bytes(int64_t n, int64_t C) {
+  const int G = fused::kThreads;  // upper bound on the grid
+  size_t b = 0;
+  auto add = [&](size_t x) { b += align_up(x, 256); };
+  add(sizeof(double) * (size_t)G * C);  // colpart
+  add(sizeof(double) * n);              // rowpart
+  add(sizeof(double) * G);              // blkpart
+  add(sizeof(double) * 2 * G);          // recpart
+  add(sizeof(float) * n);
+  add(sizeof(float) * C);
+  add(256);
+  return (int64_t)b;
+}
+
+template <int MODE, int CODEC, typename XT, int Q>
 static int launch_fused(fused::Params &p, cudaStream_t st) {
-  auto kern = fused::k1_fused<MODE, CODEC, XT>;
-  const size_t smem = fused_smem(MODE, sizeof(XT), p.R, p.S);
+  using namespace fused;
+  auto kern = k1_fused<MODE, CODEC, XT, Q>;
+  const StageLayout L = stage_layout<MODE, XT>(p.R, p.C, p.cb_row);
+  // stages: as many as fit the budget (>= 2)
+  const size_t fixed = (size_t)kCW * 8 * 64 + 64 * 8 + kUCache * 4 + 2 * 32 * 8 + 1024;
+  int S = (int)std::min<size_t>(16, (kSmemBudget - fixed) / (L.bytes + (size_t)p.R * kCW * 8));
+  if (S < 2) {
+    set_error("k1_fused: stage does not fit shared memory");
+    return CC_ERR_UNSUPPORTED;
+  }
+  p.S = S;
+  const size_t smem = (size_t)S * L.bytes + (size_t)S * p.R * kCW * 8 + 64 * 8 + kUCache * 4 + 2 * S * 8 + 128;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return cuda_status("k1_fused attr");
   void *args[] = {&p};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(p.G), dim3(fused::kThreads), args, smem, st);
+  cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(p.G), dim3(kThreads), args, smem, st);
   if (e != cudaSuccess) {
     set_error(std::string("k1_fused launch: ") + cudaGetErrorString(e));
     cudaGetLastError();
@@ -545,63 +650,35 @@ static int launch_fused(fused::Params &p, cudaStream_t st) {
   return CC_OK;
 }
 
-static int g_fused_stop = 0;
-static unsigned long long *g_fused_timer = nullptr;
-void set_fused_stop(int v) { g_fused_stop = v; }
-void set_fused_timer(void *buf) { g_fused_timer = reinterpret_cast<unsigned long long *>(buf); }
-
-bool fused_supported(int64_t n, int64_t C, const void *x, int x_dtype, const float *base, const float *aux,
-                     const uint8_t *body) {
-  (void)n;
-  if (C % fused::kStrip != 0) return false;
-  if (!aligned(x, 16) || !aligned(base, 16) || (aux && !aligned(aux, 16)) || !aligned(body, 2)) return false;
-  (void)x_dtype;
-  return true;
-}
-
-int64_t fused_workspace_bytes(int64_t n, int64_t C) {
-  const int G = fused::kThreads;  // upper bound on the grid
-  size_t b = 0;
-  auto add = [&](size_t x) { b += align_up(x, 256); };
-  add(sizeof(double) * (size_t)G * fused::kGroups * C);  // colpart (slots <= G * groups)
-  add(sizeof(double) * (size_t)cdiv(C, fused::kStrip) * n);
-  add(sizeof(double) * n);
-  add(sizeof(double) * G);
-  add(sizeof(double) * 2 * G);
-  add(sizeof(float) * n);
-  add(sizeof(float) * C);
-  add(256);
-  return (int64_t)b;
-}
-
 int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, const void *x, int x_dtype, float *base,
                  float *aux, uint8_t *body, void *ws, int64_t ws_bytes, double *record, cudaStream_t st) {
-  fused::Params p{};
+  using namespace fused;
+  Params p{};
   p.x = x;
   p.base = base;
   p.aux = aux;
   p.n = n;
   p.C = C;
-  p.nStrips = (int)(C / fused::kStrip);
-  // rows per tile: keep >= ~8 tiles per CTA so the ring reaches steady state
-  int G = sm_count();
-  G -= G % p.nStrips;
-  if (G > fused::kThreads) G = fused::kThreads - (fused::kThreads % p.nStrips);
-  const int64_t per1 = cdiv(n * p.nStrips, G);
-  p.R = per1 >= 32 ? 4 : 2;
-  p.S = fused::kRowsBuffered / p.R;
+  p.G4 = (int)(C / 4);
+  const int Q = p.G4 > kCons ? 2 : 1;
+  p.groups = Q == 2 ? 1 : kCons / p.G4;
+  p.wpg = Q == 2 ? kCW : p.G4 / 32;
+  int G = std::min(sm_count(), kThreads);
+  // rows per tile: a multiple of the row groups; two per group when each CTA has plenty of rows
+  const int64_t rows_per_cta = cdiv(n, G);
+  p.R = p.groups * (rows_per_cta >= 16 * p.groups ? 2 : 1);
   p.G = G;
-  p.nTiles = cdiv(n, p.R) * p.nStrips;
+  p.nTiles = cdiv(n, p.R);
   p.scale_mode = scale_mode;
   p.stop_after = g_fused_stop;
   p.timer = g_fused_timer;
   const int bits = codec == CC_SIGN1 ? 1 : (codec == CC_QUANT2 ? 2 : 4);
+  p.cb_row = (int)(C * bits / 8);
   const int64_t cbytes = cdiv(n * C * bits, 8);
   p.codes = body;
   p.body_u = body + cbytes;
   p.body_v = p.body_u + 4 * n;
   p.record = record;
-  // workspace
   uint8_t *w = reinterpret_cast<uint8_t *>(ws);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -609,10 +686,8 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
     off = align_up(off + bytes, 256);
     return q;
   };
-  const int slots = G / p.nStrips;
-  p.colpart = reinterpret_cast<double *>(take(sizeof(double) * (size_t)slots * C));
-  p.rowpart = reinterpret_cast<double *>(take(sizeof(double) * (size_t)p.nStrips * n));
-  p.rowsum = reinterpret_cast<double *>(take(sizeof(double) * n));
+  p.colpart = reinterpret_cast<double *>(take(sizeof(double) * (size_t)G * C));
+  p.rowpart = reinterpret_cast<double *>(take(sizeof(double) * n));
   p.blkpart = reinterpret_cast<double *>(take(sizeof(double) * G));
   p.recpart = reinterpret_cast<double *>(take(sizeof(double) * 2 * G));
   p.u = reinterpret_cast<float *>(take(sizeof(float) * n));
@@ -622,11 +697,13 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
     set_error("fused workspace too small");
     return CC_ERR_ARG;
   }
-#define CC_FUSED(MODE, XT)                                                          \
-  do {                                                                              \
-    if (codec == CC_SIGN1) return launch_fused<MODE, CC_SIGN1, XT>(p, st);          \
-    if (codec == CC_QUANT2) return launch_fused<MODE, CC_QUANT2, XT>(p, st);        \
-    return launch_fused<MODE, CC_QUANT4, XT>(p, st);                                \
+#define CC_FUSED_Q(MODE, CODEC, XT) \
+  return Q == 2 ? launch_fused<MODE, CODEC, XT, 2>(p, st) : launch_fused<MODE, CODEC, XT, 1>(p, st)
+#define CC_FUSED(MODE, XT)                                          \
+  do {                                                              \
+    if (codec == CC_SIGN1) CC_FUSED_Q(MODE, CC_SIGN1, XT);          \
+    if (codec == CC_QUANT2) CC_FUSED_Q(MODE, CC_QUANT2, XT);        \
+    CC_FUSED_Q(MODE, CC_QUANT4, XT);                                \
   } while (0)
   if (x_dtype == CC_BF16) {
     if (mode == CC_WITH_FEEDBACK) CC_FUSED(CC_WITH_FEEDBACK, __nv_bfloat16);
@@ -638,6 +715,7 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
     CC_FUSED(CC_NAIVE, float);
   }
 #undef CC_FUSED
+#undef CC_FUSED_Q
 }
 
 }  // namespace cc

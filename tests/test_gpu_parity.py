@@ -383,3 +383,24 @@ def test_fused_k1_matches_multikernel_and_oracle(shape, codec, mode, dtype, quan
             _, body, _ = O.send(och, x.to(dtype).float().cpu().numpy(), O.Codec(_otag(codec)))
             assert b1 == body
         assert np.array_equal(states[1].base.cpu().numpy(), och.base)
+
+
+@pytest.mark.parametrize("shape", [(5, 128), (40, 384), (300, 768), (9, 1536), (33, 2560)],
+                         ids=lambda s: f"{s[0]}x{s[1]}")
+@pytest.mark.parametrize("codec", QUANT_CODECS)
+@pytest.mark.parametrize("mode", ["naive", "residual_with_feedback"])
+def test_fused_k1_narrow_widths(shape, codec, mode, quant_path):
+    """Row-group mapping of the persistent K1 (C < 3072, e.g. Ulysses chunks)."""
+    cx, pl = _mods()
+    n, c = shape
+    xs = _flux_torch(n, c, 4, seed=n + 3 * c)
+    res = {}
+    for path in (0, 1):
+        quant_path(path)
+        st = pl.LayerState(mode, 1, torch.zeros(n, c, device="cuda"))
+        res[path] = ([pl.encode_step(st, x, _spec(codec))[0].body_bytes() for x in xs], st.base.clone())
+    assert res[0][0] == res[1][0]
+    assert torch.equal(res[0][1], res[1][1])
+    och = O.Channel(mode, 1, np.zeros((n, c), np.float32))
+    for x, b in zip(xs, res[1][0]):
+        assert O.send(och, x.float().cpu().numpy(), O.Codec(_otag(codec)))[1] == b
