@@ -59,7 +59,14 @@ struct Params {
   int scale_mode;
   int stop_after;             // profiling: 1 = phase A only, 2 = A + scales, 0 = full
   unsigned long long *timer;  // profiling: [G][8] globaltimer stamps, or null
+  int policy;                 // L2 policy experiment: 0 last/first, 1 normal/normal, 2 normal/first, 3 last/normal
 };
+
+__device__ __forceinline__ uint64_t l2_policy_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -308,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
 
   // ================= phase A: |t| partial sums =================
   if (producer) {
-    const uint64_t pol = l2_policy_evict_last();
+    const uint64_t pol = (p.policy == 1 || p.policy == 2) ? l2_policy_normal() : l2_policy_evict_last();
     for (int64_t k = 0; k < K; ++k) {
       const int s = (int)(k % S);
       if (k >= S) {
@@ -462,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   // ================= phase B: quantize, pack, update state (in place) =================
   double err = 0.0, tsq = 0.0;
   if (producer) {
-    const uint64_t pol = l2_policy_evict_first();
+    const uint64_t pol = (p.policy == 1 || p.policy == 3) ? l2_policy_normal() : l2_policy_evict_first();
     for (int64_t k = 0; k < K; ++k) {
       const int64_t seq = K + k;
       const int s = (int)(seq % S);
@@ -596,6 +603,8 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
 // host side
 // ---------------------------------------------------------------------------
 static int g_fused_stop = 0;
+static int g_fused_policy = 0;
+void set_fused_policy(int v) { g_fused_policy = v; }
 static unsigned long long *g_fused_timer = nullptr;
 void set_fused_stop(int v) { g_fused_stop = v; }
 void set_fused_timer(void *buf) { g_fused_timer = reinterpret_cast<unsigned long long *>(buf); }
@@ -672,6 +681,7 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   p.scale_mode = scale_mode;
   p.stop_after = g_fused_stop;
   p.timer = g_fused_timer;
+  p.policy = g_fused_policy;
   const int bits = codec == CC_SIGN1 ? 1 : (codec == CC_QUANT2 ? 2 : 4);
   p.cb_row = (int)(C * bits / 8);
   const int64_t cbytes = cdiv(n * C * bits, 8);
