@@ -175,6 +175,9 @@ CC_API void cc_debug_fused_stop(int phase);
 /* profiling only: device buffer of [grid][8] u64 %globaltimer stamps written by
  * every CTA of the persistent K1 at its phase boundaries (NULL disables). */
 CC_API void cc_debug_fused_timer(void *dev_buf);
+/* profiling only: L2 eviction policy of the persistent K1's TMA loads
+ * (0 evict_last/evict_first (default), 1 normal/normal, 2 normal/first, 3 last/normal) */
+CC_API void cc_debug_fused_policy(int policy);
 
 #ifdef __cplusplus
 }
