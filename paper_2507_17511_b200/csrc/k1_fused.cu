@@ -422,8 +422,16 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     for (int64_t b8 = gid & ~7LL; b8 < C * 8; b8 += nthr) {
       const int64_t j = b8 >> 3;
       const int part = (int)(gid & 7);
+      // issue all loads first (G <= kThreads, so <= 52 per lane), then add in order
+      double vals[(kThreads + 7) / 8];
+#pragma unroll
+      for (int q = 0; q < (kThreads + 7) / 8; ++q) {
+        const int slot = part + 8 * q;
+        vals[q] = slot < G ? __ldcg(p.colpart + (int64_t)slot * C + j) : 0.0;
+      }
       double acc = 0.0;
-      for (int q = part; q < G; q += 8) acc += __ldcg(p.colpart + (int64_t)q * C + j);
+#pragma unroll
+      for (int q = 0; q < (kThreads + 7) / 8; ++q) acc += vals[q];
       acc += __shfl_xor_sync(0xffffffffu, acc, 1);
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
       acc += __shfl_xor_sync(0xffffffffu, acc, 4);
@@ -675,7 +683,7 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   int G = std::min(sm_count(), kThreads);
   // rows per tile: a multiple of the row groups; two per group when each CTA has plenty of rows
   const int64_t rows_per_cta = cdiv(n, G);
-  p.R = p.groups * (rows_per_cta >= 16 * p.groups ? 2 : 1);
+  p.R = p.groups * (rows_per_cta >= 64 * p.groups ? 2 : 1);
   p.G = G;
   p.nTiles = cdiv(n, p.R);
   p.scale_mode = scale_mode;
