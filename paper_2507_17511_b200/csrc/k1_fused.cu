@@ -39,17 +39,19 @@ namespace fused {
 
 constexpr int kCons = 384;             // consumer threads (12 warps)
 constexpr int kCW = kCons / 32;
-constexpr int kThreads = kCons + 32;   // + producer warp
+constexpr int kThreads = kCons + 64;   // + TMA load warp + TMA store warp
 constexpr int kMaxC = 2 * 4 * kCons;   // 3072 columns: two column quads per consumer thread
 constexpr int kUCache = 512;           // cached u_i per CTA for phase B
-constexpr size_t kSmemBudget = 190 * 1024;
+constexpr size_t kSmemBudget = 224 * 1024;
 
 struct Params {
   const void *x;
   float *base, *aux;
   int64_t n, C;
   int G4, groups, wpg;  // column quads, row groups, warps per group
-  int R, S, G;
+  int R, S, G;          // phase A: rows per tile, stages; grid size
+  int S_in, S_out;      // phase B ring depths
+  uint32_t ring_bytes;  // shared bytes of the tile rings
   int cb_row;           // code bytes per row
   int64_t nTiles;
   double *colpart, *rowpart, *blkpart, *recpart, *record;
@@ -212,40 +214,67 @@ constexpr bool has_aux() {
   return MODE != CC_NAIVE;
 }
 
-struct StageLayout {
-  uint32_t x, base, aux, codes, bytes;  // byte offsets inside one stage
+// byte offsets of the arrays of one ring stage holding R rows
+struct InStage {
+  uint32_t x, base, aux, bytes;
 };
+struct OutStage {
+  uint32_t base, aux, codes, bytes;
+};
+__host__ __device__ inline uint32_t al128(uint64_t v) { return (uint32_t)((v + 127u) & ~127ull); }
 
 template <int MODE, typename XT>
-__host__ __device__ inline StageLayout stage_layout(int R, int64_t C, int cb_row) {
-  auto al = [](uint32_t v) { return (v + 127u) & ~127u; };
-  StageLayout L;
+__host__ __device__ inline InStage in_stage(int R, int64_t C, bool with_base) {
+  InStage L;
   L.x = 0;
-  L.base = al((uint32_t)(R * C * sizeof(XT)));
-  L.aux = al(L.base + (uint32_t)(R * C * 4));
-  L.codes = has_aux<MODE>() ? al(L.aux + (uint32_t)(R * C * 4)) : L.aux;
-  L.bytes = al(L.codes + (uint32_t)(R * cb_row));
+  L.base = al128((uint64_t)R * C * sizeof(XT));
+  L.aux = with_base ? al128(L.base + (uint64_t)R * C * 4) : L.base;
+  L.bytes = has_aux<MODE>() ? al128(L.aux + (uint64_t)R * C * 4) : L.aux;
+  return L;
+}
+template <int MODE>
+__host__ __device__ inline OutStage out_stage(int R, int64_t C, int cb_row) {
+  OutStage L;
+  L.base = 0;
+  L.aux = al128((uint64_t)R * C * 4);
+  L.codes = has_aux<MODE>() ? al128(L.aux + (uint64_t)R * C * 4) : L.aux;
+  L.bytes = al128(L.codes + (uint64_t)R * cb_row);
   return L;
 }
 
-// Q = column quads per consumer thread (1: C <= 1536, row groups; 2: C <= 3072)
+__device__ __forceinline__ void unpack_x(const __nv_bfloat16 *p, float (&xx)[4]) {
+  const uint2 raw = *reinterpret_cast<const uint2 *>(p);
+  xx[0] = __uint_as_float(raw.x << 16);
+  xx[1] = __uint_as_float(raw.x & 0xffff0000u);
+  xx[2] = __uint_as_float(raw.y << 16);
+  xx[3] = __uint_as_float(raw.y & 0xffff0000u);
+}
+__device__ __forceinline__ void unpack_x(const float *p, float (&xx)[4]) {
+  const float4 v = lds4(p);
+  xx[0] = v.x; xx[1] = v.y; xx[2] = v.z; xx[3] = v.w;
+}
+__device__ __forceinline__ void unpack_f(const float *p, float (&v)[4]) {
+  const float4 w = lds4(p);
+  v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+}
+
+// Q = column quads per consumer thread (1: C <= 1536 with row groups; 2: C <= 3072)
 template <int MODE, int CODEC, typename XT, int Q>
 __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ Params p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
-  const int R = p.R, S = p.S, G = p.G;
+  const int RA = p.R, SA = p.S, G = p.G;
+  const int RB = p.groups, SI = p.S_in, SO = p.S_out;
   const int64_t n = p.n, C = p.C;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cta = blockIdx.x;
-  const bool producer = warp == kCW;
-  // consumer mapping
+  const bool loader = warp == kCW, storer = warp == kCW + 1, consumer = warp < kCW;
   int grp = 0, quad0 = tid, wig = warp;
   if constexpr (Q == 1) {
     grp = tid / p.G4;
     quad0 = tid % p.G4;
     wig = quad0 >> 5;
   }
-  const bool in_group = !producer && grp < p.groups;
+  const bool in_group = consumer && grp < p.groups;
   bool qact[Q];
   int qcol[Q];
 #pragma unroll
@@ -255,89 +284,89 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     qcol[j] = 4 * qd;
   }
 
-  const StageLayout L = stage_layout<MODE, XT>(R, C, p.cb_row);
-  uint8_t *tiles = smem;
-  double *rp = reinterpret_cast<double *>(smem + (size_t)S * L.bytes);  // [S][R][kCW]
-  double *red = rp + (size_t)S * R * kCW;                               // block-sum scratch [64]
-  float *ucache = reinterpret_cast<float *>(red + 64);                   // [kUCache]
-  uint64_t *full = reinterpret_cast<uint64_t *>(ucache + kUCache);
-  uint64_t *empty = full + S;
+  // ---- shared memory: [ring area][rp][red][ucache][barriers] ----
+  uint8_t *ring = smem;
+  double *rp = reinterpret_cast<double *>(smem + p.ring_bytes);  // [SA][RA][kCW]
+  double *red = rp + (size_t)SA * RA * kCW;                      // [64]
+  float *ucache = reinterpret_cast<float *>(red + 64);            // [kUCache]
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(ucache + kUCache);
+  uint64_t *emptyA = fullA + SA;
+  uint64_t *fullB = emptyA + SA;
+  uint64_t *emptyB = fullB + SI;
+  uint64_t *outFull = emptyB + SI;
+  uint64_t *outFree = outFull + SO;
 
   auto stamp = [&](int i) {
     if (p.timer && tid == 0) p.timer[(size_t)cta * 8 + i] = gtimer();
   };
   stamp(0);
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kCW);
+    for (int s = 0; s < SA; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&emptyA[s], kCW);
+    }
+    for (int s = 0; s < SI; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], kCW);
+    }
+    for (int s = 0; s < SO; ++s) {
+      mbar_init(&outFull[s], kCW);
+      mbar_init(&outFree[s], 1);
     }
     mbar_fence_init();
   }
   __syncthreads();
-
-  const int64_t K = p.nTiles > cta ? (p.nTiles - 1 - cta) / G + 1 : 0;  // tiles cta, cta+G, ...
-  auto tile_r0 = [&](int64_t k) -> int64_t { return (cta + k * G) * (int64_t)R; };
-  auto sx = [&](int s) { return reinterpret_cast<XT *>(tiles + (size_t)s * L.bytes + L.x); };
-  auto sb = [&](int s) { return reinterpret_cast<float *>(tiles + (size_t)s * L.bytes + L.base); };
-  auto sa = [&](int s) { return reinterpret_cast<float *>(tiles + (size_t)s * L.bytes + L.aux); };
-  auto sc = [&](int s) { return tiles + (size_t)s * L.bytes + L.codes; };
   const XT *X = reinterpret_cast<const XT *>(p.x);
 
-  double cta_total = 0.0;  // producer lanes (phase A)
+  // ================= phase A: |t| partial sums over tiles of RA rows =================
+  const InStage LA = in_stage<MODE, XT>(RA, C, MODE == CC_WITH_FEEDBACK);
+  const int64_t KA = p.nTiles > cta ? (p.nTiles - 1 - cta) / G + 1 : 0;
+  auto a_r0 = [&](int64_t k) -> int64_t { return (cta + k * G) * (int64_t)RA; };
+  double cta_total = 0.0;
   auto finish_rows = [&](int s, int64_t k) {
-    const int64_t r0 = tile_r0(k);
-    if (lane < R && r0 + lane < n) {
+    const int64_t r0 = a_r0(k);
+    if (lane < RA && r0 + lane < n) {
       double acc = 0.0;
-      for (int w = 0; w < p.wpg; ++w) acc += rp[((size_t)s * R + lane) * kCW + w];
+      for (int w = 0; w < p.wpg; ++w) acc += rp[((size_t)s * RA + lane) * kCW + w];
       p.rowpart[r0 + lane] = acc;
       cta_total += acc;
     }
   };
-  auto issue_loads = [&](int s, int64_t kk, bool with_base, uint64_t pol) {
-    const int64_t r0 = tile_r0(kk);
-    const int nrows = (int)min64(R, n - r0);
-    const uint32_t xb = (uint32_t)(nrows * C * sizeof(XT)), fb = (uint32_t)(nrows * C * 4);
-    const bool aux = has_aux<MODE>();
-    mbar_expect_tx(&full[s], xb + (with_base ? fb : 0u) + (aux ? fb : 0u));
-    bulk_g2s(sx(s), X + r0 * C, xb, &full[s], pol);
-    if (with_base) bulk_g2s(sb(s), p.base + r0 * C, fb, &full[s], pol);
-    if (aux) bulk_g2s(sa(s), p.aux + r0 * C, fb, &full[s], pol);
-  };
-  auto issue_stores = [&](int s, int64_t kk) {  // phase-B results of tile kk sitting in stage s
-    const int64_t r0 = tile_r0(kk);
-    const int nrows = (int)min64(R, n - r0);
-    bulk_s2g(p.base + r0 * C, sb(s), (uint32_t)(nrows * C * 4));
-    if constexpr (has_aux<MODE>()) bulk_s2g(p.aux + r0 * C, sa(s), (uint32_t)(nrows * C * 4));
-    bulk_s2g(p.codes + r0 * p.cb_row, sc(s), (uint32_t)(nrows * p.cb_row));
-    bulk_commit();
-  };
-
-  // ================= phase A: |t| partial sums =================
-  if (producer) {
-    const uint64_t pol = (p.policy == 1 || p.policy == 2) ? l2_policy_normal() : l2_policy_evict_last();
-    for (int64_t k = 0; k < K; ++k) {
-      const int s = (int)(k % S);
-      if (k >= S) {
-        mbar_wait(&empty[s], (uint32_t)(((k / S) - 1) & 1));
-        finish_rows(s, k - S);
+  if (loader) {
+    const uint64_t pol = l2_policy_evict_last();
+    for (int64_t k = 0; k < KA; ++k) {
+      const int s = (int)(k % SA);
+      if (k >= SA) {
+        mbar_wait(&emptyA[s], (uint32_t)(((k / SA) - 1) & 1));
+        finish_rows(s, k - SA);
       }
-      if (lane == 0) issue_loads(s, k, MODE == CC_WITH_FEEDBACK, pol);
+      if (lane == 0) {
+        uint8_t *st = ring + (size_t)s * LA.bytes;
+        const int64_t r0 = a_r0(k);
+        const int nrows = (int)min64(RA, n - r0);
+        const uint32_t xb = (uint32_t)(nrows * C * sizeof(XT)), fb = (uint32_t)(nrows * C * 4);
+        const bool wb = MODE == CC_WITH_FEEDBACK;
+        mbar_expect_tx(&fullA[s], xb + (wb ? fb : 0u) + (has_aux<MODE>() ? fb : 0u));
+        bulk_g2s(st + LA.x, X + r0 * C, xb, &fullA[s], pol);
+        if (wb) bulk_g2s(st + LA.base, p.base + r0 * C, fb, &fullA[s], pol);
+        if (has_aux<MODE>()) bulk_g2s(st + LA.aux, p.aux + r0 * C, fb, &fullA[s], pol);
+      }
       __syncwarp();
     }
-    for (int64_t k = K - min64(S, K); k < K; ++k) {  // drain: row sums of the last tiles
-      const int s = (int)(k % S);
-      mbar_wait(&empty[s], (uint32_t)((k / S) & 1));
+    for (int64_t k = KA - min64(SA, KA); k < KA; ++k) {
+      const int s = (int)(k % SA);
+      mbar_wait(&emptyA[s], (uint32_t)((k / SA) & 1));
       finish_rows(s, k);
     }
-  } else {
+  } else if (consumer) {
     double cs[Q][4];
 #pragma unroll
     for (int j = 0; j < Q; ++j) cs[j][0] = cs[j][1] = cs[j][2] = cs[j][3] = 0.0;
-    for (int64_t k = 0; k < K; ++k) {
-      const int s = (int)(k % S);
-      mbar_wait(&full[s], (uint32_t)((k / S) & 1));
-      const int nrows = (int)min64(R, n - tile_r0(k));
+    for (int64_t k = 0; k < KA; ++k) {
+      const int s = (int)(k % SA);
+      mbar_wait(&fullA[s], (uint32_t)((k / SA) & 1));
+      const uint8_t *st = ring + (size_t)s * LA.bytes;
+      const int nrows = (int)min64(RA, n - a_r0(k));
       if (grp < p.groups) {
         for (int r = grp; r < nrows; r += p.groups) {
           double rs = 0.0;
@@ -346,22 +375,9 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
             if (!qact[j]) continue;
             const size_t o = (size_t)r * C + qcol[j];
             float xx[4], bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f};
-            if constexpr (sizeof(XT) == 2) {
-              const uint2 raw = *reinterpret_cast<const uint2 *>(sx(s) + o);
-              xx[0] = __uint_as_float(raw.x << 16); xx[1] = __uint_as_float(raw.x & 0xffff0000u);
-              xx[2] = __uint_as_float(raw.y << 16); xx[3] = __uint_as_float(raw.y & 0xffff0000u);
-            } else {
-              const float4 v = lds4(reinterpret_cast<const float *>(sx(s)) + o);
-              xx[0] = v.x; xx[1] = v.y; xx[2] = v.z; xx[3] = v.w;
-            }
-            if constexpr (MODE == CC_WITH_FEEDBACK) {
-              const float4 v = lds4(sb(s) + o);
-              bb[0] = v.x; bb[1] = v.y; bb[2] = v.z; bb[3] = v.w;
-            }
-            if constexpr (has_aux<MODE>()) {
-              const float4 v = lds4(sa(s) + o);
-              aa[0] = v.x; aa[1] = v.y; aa[2] = v.z; aa[3] = v.w;
-            }
+            unpack_x(reinterpret_cast<const XT *>(st + LA.x) + o, xx);
+            if constexpr (MODE == CC_WITH_FEEDBACK) unpack_f(reinterpret_cast<const float *>(st + LA.base) + o, bb);
+            if constexpr (has_aux<MODE>()) unpack_f(reinterpret_cast<const float *>(st + LA.aux) + o, aa);
             double a[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -371,15 +387,14 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
             rs += ((a[0] + a[1]) + a[2]) + a[3];
           }
           rs = warp_sum(rs);
-          if (lane == 0) rp[((size_t)s * R + r) * kCW + wig] = rs;
+          if (lane == 0) rp[((size_t)s * RA + r) * kCW + wig] = rs;
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) mbar_arrive(&emptyA[s]);
     }
-    // column partials; row groups merged in a fixed order through smem
-    if constexpr (Q == 1) {
-      double *xchg = reinterpret_cast<double *>(tiles);
+    if constexpr (Q == 1) {  // merge row groups' column partials in a fixed order
+      double *xchg = reinterpret_cast<double *>(ring);
       named_sync(1, kCons);
       if (in_group && qact[0]) {
 #pragma unroll
@@ -405,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     }
   }
   {
-    const double b = block_sum(producer ? cta_total : 0.0, red);
+    const double b = block_sum(loader ? cta_total : 0.0, red);
     if (tid == 0) p.blkpart[cta] = b;
   }
   stamp(1);
@@ -422,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     for (int64_t b8 = gid & ~7LL; b8 < C * 8; b8 += nthr) {
       const int64_t j = b8 >> 3;
       const int part = (int)(gid & 7);
-      // issue all loads first (G <= kThreads, so <= 52 per lane), then add in order
+      // all loads first (G <= kThreads), then add in a fixed order
       double vals[(kThreads + 7) / 8];
 #pragma unroll
       for (int q = 0; q < (kThreads + 7) / 8; ++q) {
@@ -465,37 +480,62 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   stamp(4);
   if (p.stop_after == 2) return;
 
-  const bool ucached = K * R <= kUCache;
+  // ================= phase B: quantize, pack, update state =================
+  // tiles of RB (= row groups) rows, visited in reverse order (phase A's tail is
+  // L2-resident); a load ring (S_in) and a separate output ring (S_out) drained
+  // by the store warp with TMA bulk stores, so loads never wait for stores.
+  const InStage LI = in_stage<MODE, XT>(RB, C, has_aux<MODE>());
+  const OutStage LO = out_stage<MODE>(RB, C, p.cb_row);
+  uint8_t *in_ring = ring;
+  uint8_t *out_ring = ring + (size_t)SI * LI.bytes;
+  const int64_t nTB = (n + RB - 1) / RB;
+  const int64_t KB = nTB > cta ? (nTB - 1 - cta) / G + 1 : 0;
+  auto b_r0 = [&](int64_t k) -> int64_t { return (cta + (KB - 1 - k) * G) * (int64_t)RB; };  // reversed
+  const bool ucached = KB * RB <= kUCache;
   if (ucached) {
-    for (int i = tid; i < K * R; i += kThreads) {
-      const int64_t row = tile_r0(K - 1 - i / R) + i % R;
+    for (int i = tid; i < KB * RB; i += kThreads) {
+      const int64_t row = b_r0(i / RB) + i % RB;
       ucache[i] = row < n ? __ldcg(p.u + row) : 0.0f;
     }
   }
   __syncthreads();
 
-  // ================= phase B: quantize, pack, update state (in place) =================
   double err = 0.0, tsq = 0.0;
-  if (producer) {
-    const uint64_t pol = (p.policy == 1 || p.policy == 3) ? l2_policy_normal() : l2_policy_evict_first();
-    for (int64_t k = 0; k < K; ++k) {
-      const int64_t seq = K + k;
-      const int s = (int)(seq % S);
-      if (seq >= S) mbar_wait(&empty[s], (uint32_t)(((seq / S) - 1) & 1));
+  if (loader) {
+    const uint64_t pol = l2_policy_evict_first();
+    for (int64_t k = 0; k < KB; ++k) {
+      const int s = (int)(k % SI);
+      if (k >= SI) mbar_wait(&emptyB[s], (uint32_t)(((k / SI) - 1) & 1));
       if (lane == 0) {
-        if (seq - S >= K) {  // previous occupant was a phase-B tile: drain it first
-          issue_stores(s, K - 1 - (k - S));
-          bulk_wait_read<0>();
+        uint8_t *st = in_ring + (size_t)s * LI.bytes;
+        const int64_t r0 = b_r0(k);
+        const int nrows = (int)min64(RB, n - r0);
+        const uint32_t xb = (uint32_t)(nrows * C * sizeof(XT)), fb = (uint32_t)(nrows * C * 4);
+        mbar_expect_tx(&fullB[s], xb + (has_aux<MODE>() ? 2 * fb : 0u));
+        bulk_g2s(st + LI.x, X + r0 * C, xb, &fullB[s], pol);
+        if (has_aux<MODE>()) {
+          bulk_g2s(st + LI.base, p.base + r0 * C, fb, &fullB[s], pol);
+          bulk_g2s(st + LI.aux, p.aux + r0 * C, fb, &fullB[s], pol);
         }
-        issue_loads(s, K - 1 - k, has_aux<MODE>(), pol);
       }
       __syncwarp();
     }
-    for (int64_t k = K - min64(S, K); k < K; ++k) {
-      const int64_t seq = K + k;
-      const int s = (int)(seq % S);
-      mbar_wait(&empty[s], (uint32_t)((seq / S) & 1));
-      if (lane == 0) issue_stores(s, K - 1 - k);
+  } else if (storer) {
+    for (int64_t k = 0; k < KB; ++k) {
+      const int o = (int)(k % SO);
+      mbar_wait(&outFull[o], (uint32_t)((k / SO) & 1));
+      if (lane == 0) {
+        const uint8_t *so = out_ring + (size_t)o * LO.bytes;
+        const int64_t r0 = b_r0(k);
+        const int nrows = (int)min64(RB, n - r0);
+        bulk_s2g(p.base + r0 * C, so + LO.base, (uint32_t)(nrows * C * 4));
+        if constexpr (has_aux<MODE>()) bulk_s2g(p.aux + r0 * C, so + LO.aux, (uint32_t)(nrows * C * 4));
+        bulk_s2g(p.codes + r0 * p.cb_row, so + LO.codes, (uint32_t)(nrows * p.cb_row));
+        bulk_commit();
+        bulk_wait_read<0>();  // smem source consumed -> the slot may be rewritten
+        mbar_arrive(&outFree[o]);
+      }
+      __syncwarp();
     }
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
@@ -513,71 +553,71 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
         cc[j].ok = cc[j].ok && scale_in_range(fabsf(v));
       }
     }
-    for (int64_t k = 0; k < K; ++k) {
-      const int64_t seq = K + k;
-      const int s = (int)(seq % S);
-      mbar_wait(&full[s], (uint32_t)((seq / S) & 1));
-      const int64_t r0 = tile_r0(K - 1 - k);
-      const int nrows = (int)min64(R, n - r0);
-      if (grp < p.groups) {
-        for (int r = grp; r < nrows; r += p.groups) {
-          const float uf = ucached ? ucache[k * R + r] : __ldcg(p.u + r0 + r);
-          const bool row_ok = scale_in_range(fabsf(uf));
+    const int r = grp;  // this thread's row inside a phase-B tile
+    for (int64_t k = 0; k < KB; ++k) {
+      const int s = (int)(k % SI);
+      mbar_wait(&fullB[s], (uint32_t)((k / SI) & 1));
+      const uint8_t *st = in_ring + (size_t)s * LI.bytes;
+      const int64_t r0 = b_r0(k);
+      const bool row_live = in_group && r0 + r < n;
+      float xx[Q][4], bb[Q][4], aa[Q][4];
 #pragma unroll
-          for (int j = 0; j < Q; ++j) {
-            const size_t o = (size_t)r * C + qcol[j];
-            float xx[4] = {0.f, 0.f, 0.f, 0.f}, bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f};
-            if (qact[j]) {
-              if constexpr (sizeof(XT) == 2) {
-                const uint2 raw = *reinterpret_cast<const uint2 *>(sx(s) + o);
-                xx[0] = __uint_as_float(raw.x << 16); xx[1] = __uint_as_float(raw.x & 0xffff0000u);
-                xx[2] = __uint_as_float(raw.y << 16); xx[3] = __uint_as_float(raw.y & 0xffff0000u);
-              } else {
-                const float4 v = lds4(reinterpret_cast<const float *>(sx(s)) + o);
-                xx[0] = v.x; xx[1] = v.y; xx[2] = v.z; xx[3] = v.w;
-              }
-              if constexpr (has_aux<MODE>()) {
-                const float4 v = lds4(sb(s) + o);
-                bb[0] = v.x; bb[1] = v.y; bb[2] = v.z; bb[3] = v.w;
-                const float4 w = lds4(sa(s) + o);
-                aa[0] = w.x; aa[1] = w.y; aa[2] = w.z; aa[3] = w.w;
-              }
-            }
-            float t[4], d[4], e[4];
+      for (int j = 0; j < Q; ++j) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) t[q] = target_of<MODE>(xx[q], bb[q], aa[q]);
-            const uint32_t packed = quantize4<CODEC>(t, uf, row_ok, cc[j], d);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) e[q] = __fsub_rn(t[q], d[q]);
-            if (qact[j]) {
-              record4(t, e, err, tsq);
-              float4 nb;
-              if constexpr (MODE == CC_NAIVE) {
-                nb = make_float4(d[0], d[1], d[2], d[3]);
-              } else {
-                nb = make_float4(__fadd_rn(bb[0], d[0]), __fadd_rn(bb[1], d[1]), __fadd_rn(bb[2], d[2]),
-                                 __fadd_rn(bb[3], d[3]));
-                *reinterpret_cast<float4 *>(sa(s) + o) = MODE == CC_WITH_FEEDBACK
-                                                             ? make_float4(e[0], e[1], e[2], e[3])
-                                                             : make_float4(xx[0], xx[1], xx[2], xx[3]);
-              }
-              *reinterpret_cast<float4 *>(sb(s) + o) = nb;
-            }
-            uint8_t *crow = sc(s) + (size_t)r * p.cb_row;
-            if constexpr (CODEC == CC_SIGN1) {
-              const uint32_t other = __shfl_down_sync(0xffffffffu, packed, 1);
-              if (qact[j] && (lane & 1) == 0) crow[qcol[j] >> 3] = (uint8_t)(packed | (other << 4));
-            } else if constexpr (CODEC == CC_QUANT2) {
-              if (qact[j]) crow[qcol[j] >> 2] = (uint8_t)packed;
-            } else {
-              if (qact[j]) *reinterpret_cast<uint16_t *>(crow + (qcol[j] >> 1)) = (uint16_t)packed;
-            }
+        for (int q = 0; q < 4; ++q) xx[j][q] = bb[j][q] = aa[j][q] = 0.f;
+        if (row_live && qact[j]) {
+          const size_t o = (size_t)r * C + qcol[j];
+          unpack_x(reinterpret_cast<const XT *>(st + LI.x) + o, xx[j]);
+          if constexpr (has_aux<MODE>()) {
+            unpack_f(reinterpret_cast<const float *>(st + LI.base) + o, bb[j]);
+            unpack_f(reinterpret_cast<const float *>(st + LI.aux) + o, aa[j]);
           }
         }
       }
-      fence_proxy_async_smem();  // our smem results -> visible to the TMA store
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) mbar_arrive(&emptyB[s]);  // inputs are in registers: the loader may refill
+      const int o = (int)(k % SO);
+      if (k >= SO) mbar_wait(&outFree[o], (uint32_t)(((k / SO) - 1) & 1));
+      uint8_t *so = out_ring + (size_t)o * LO.bytes;
+      const float uf = row_live ? (ucached ? ucache[k * RB + r] : __ldcg(p.u + r0 + r)) : 1.0f;
+      const bool row_ok = scale_in_range(fabsf(uf));
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        float t[4], d[4], e[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) t[q] = target_of<MODE>(xx[j][q], bb[j][q], aa[j][q]);
+        const uint32_t packed = quantize4<CODEC>(t, uf, row_ok, cc[j], d);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) e[q] = __fsub_rn(t[q], d[q]);
+        const bool live = row_live && qact[j];
+        const size_t oo = (size_t)r * C + qcol[j];
+        if (live) {
+          record4(t, e, err, tsq);
+          float4 nb;
+          if constexpr (MODE == CC_NAIVE) {
+            nb = make_float4(d[0], d[1], d[2], d[3]);
+          } else {
+            nb = make_float4(__fadd_rn(bb[j][0], d[0]), __fadd_rn(bb[j][1], d[1]), __fadd_rn(bb[j][2], d[2]),
+                             __fadd_rn(bb[j][3], d[3]));
+            *reinterpret_cast<float4 *>(reinterpret_cast<float *>(so + LO.aux) + oo) =
+                MODE == CC_WITH_FEEDBACK ? make_float4(e[0], e[1], e[2], e[3])
+                                         : make_float4(xx[j][0], xx[j][1], xx[j][2], xx[j][3]);
+          }
+          *reinterpret_cast<float4 *>(reinterpret_cast<float *>(so + LO.base) + oo) = nb;
+        }
+        uint8_t *crow = so + LO.codes + (size_t)r * p.cb_row;
+        if constexpr (CODEC == CC_SIGN1) {
+          const uint32_t other = __shfl_down_sync(0xffffffffu, packed, 1);
+          if (live && (lane & 1) == 0) crow[qcol[j] >> 3] = (uint8_t)(packed | (other << 4));
+        } else if constexpr (CODEC == CC_QUANT2) {
+          if (live) crow[qcol[j] >> 2] = (uint8_t)packed;
+        } else {
+          if (live) *reinterpret_cast<uint16_t *>(crow + (qcol[j] >> 1)) = (uint16_t)packed;
+        }
+      }
+      fence_proxy_async_smem();  // results -> visible to the TMA store engine
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&outFull[o]);
     }
   }
   stamp(5);
@@ -612,8 +652,8 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
 // ---------------------------------------------------------------------------
 static int g_fused_stop = 0;
 static int g_fused_policy = 0;
-void set_fused_policy(int v) { g_fused_policy = v; }
 static unsigned long long *g_fused_timer = nullptr;
+void set_fused_policy(int v) { g_fused_policy = v; }
 void set_fused_stop(int v) { g_fused_stop = v; }
 void set_fused_timer(void *buf) { g_fused_timer = reinterpret_cast<unsigned long long *>(buf); }
 
@@ -644,16 +684,40 @@ template <int MODE, int CODEC, typename XT, int Q>
 static int launch_fused(fused::Params &p, cudaStream_t st) {
   using namespace fused;
   auto kern = k1_fused<MODE, CODEC, XT, Q>;
-  const StageLayout L = stage_layout<MODE, XT>(p.R, p.C, p.cb_row);
-  // stages: as many as fit the budget (>= 2)
-  const size_t fixed = (size_t)kCW * 8 * 64 + 64 * 8 + kUCache * 4 + 2 * 32 * 8 + 1024;
-  int S = (int)std::min<size_t>(16, (kSmemBudget - fixed) / (L.bytes + (size_t)p.R * kCW * 8));
-  if (S < 2) {
-    set_error("k1_fused: stage does not fit shared memory");
+  const size_t fixed_tail = 64 * 8 + kUCache * 4 + 2 * 16 * 8 + 2 * 8 * 8 + 2 * 8 * 8 + 256;
+  const size_t budget = kSmemBudget;
+  // phase B rings (tiles of `groups` rows): loads S_in, outputs S_out
+  const InStage LI = in_stage<MODE, XT>(p.groups, p.C, has_aux<MODE>());
+  const OutStage LO = out_stage<MODE>(p.groups, p.C, p.cb_row);
+  const InStage LA = in_stage<MODE, XT>(p.R, p.C, MODE == CC_WITH_FEEDBACK);
+  int SO = 2, SI = 0;
+  for (;;) {
+    const size_t avail = budget - fixed_tail - (size_t)3 * p.R * kCW * 8;
+    if ((size_t)SO * LO.bytes + 2 * (size_t)LI.bytes <= avail) {
+      SI = (int)std::min<size_t>(8, (avail - (size_t)SO * LO.bytes) / LI.bytes);
+      break;
+    }
+    if (SO == 1) break;
+    --SO;
+  }
+  if (SI < 2) {
+    set_error("k1_fused: phase-B stages do not fit shared memory");
     return CC_ERR_UNSUPPORTED;
   }
-  p.S = S;
-  const size_t smem = (size_t)S * L.bytes + (size_t)S * p.R * kCW * 8 + 64 * 8 + kUCache * 4 + 2 * S * 8 + 128;
+  const size_t ringB = (size_t)SI * LI.bytes + (size_t)SO * LO.bytes;
+  // phase A ring uses the same area (plus whatever is left)
+  int SA = (int)std::min<size_t>(8, (budget - fixed_tail) / (LA.bytes + (size_t)p.R * kCW * 8));
+  if (SA < 2) {
+    set_error("k1_fused: phase-A stages do not fit shared memory");
+    return CC_ERR_UNSUPPORTED;
+  }
+  const size_t ringA = (size_t)SA * LA.bytes;
+  p.S = SA;
+  p.S_in = SI;
+  p.S_out = SO;
+  p.ring_bytes = (uint32_t)align_up(std::max(ringA, ringB), 128);
+  const size_t smem = p.ring_bytes + (size_t)SA * p.R * kCW * 8 + 64 * 8 + kUCache * 4 +
+                      (size_t)(2 * SA + 2 * SI + 2 * SO) * 8 + 128;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return cuda_status("k1_fused attr");
   void *args[] = {&p};
@@ -683,7 +747,7 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   int G = std::min(sm_count(), kThreads);
   // rows per tile: a multiple of the row groups; two per group when each CTA has plenty of rows
   const int64_t rows_per_cta = cdiv(n, G);
-  p.R = p.groups * (rows_per_cta >= 64 * p.groups ? 2 : 1);
+  p.R = p.groups * (rows_per_cta >= 16 * p.groups ? 2 : 1);
   p.G = G;
   p.nTiles = cdiv(n, p.R);
   p.scale_mode = scale_mode;
