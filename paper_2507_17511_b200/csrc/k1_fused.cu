@@ -122,7 +122,7 @@ __device__ __noinline__ CodeVal quantize1_exact(float t, double ud, double vd) {
 // i.e. |t| > RN(u vhi) proves code 0/3 and |t| < RN(u vlo) proves code 1/2.
 struct ColConst {
   float v[4], vhi[4], vlo[4];
-  bool ok;  // all 4 columns have |v| in [2^-50, 2^50] (and v != 0)
+  bool ok;  // all 4 columns have v == 0 or |v| in [2^-50, 2^50]
 };
 
 __device__ __forceinline__ bool scale_in_range(float a) { return a >= 0x1p-50f && a <= 0x1p+50f; }
@@ -151,13 +151,14 @@ __device__ __forceinline__ uint32_t quantize4(const float (&t)[4], float uf, boo
     for (int q = 0; q < 4; ++q) {
       const float p = __fmul_rn(uf, cc.v[q]);
       const float ax = fabsf(t[q]);
+      const bool zero = cc.v[q] == 0.0f;  // zero scale: code 2, decode +0 (cx:385-387)
       const bool big = ax > __fmul_rn(uf, cc.vhi[q]);
-      ambiguous |= !big && !(ax < __fmul_rn(uf, cc.vlo[q]));
-      const bool neg = t[q] < 0.0f;
+      ambiguous |= !zero && !big && !(ax < __fmul_rn(uf, cc.vlo[q]));
+      const bool neg = t[q] < 0.0f && !zero;
       // code: big -> (neg ? 0 : 3), else (neg ? 1 : 2)
-      const uint32_t code = big ? (neg ? 0u : 3u) : (neg ? 1u : 2u);
+      const uint32_t code = zero ? 2u : (big ? (neg ? 0u : 3u) : (neg ? 1u : 2u));
       const float lv = big ? 2.0f : 0.5f;
-      d[q] = __fmul_rn(neg ? -lv : lv, p);
+      d[q] = zero ? 0.0f : __fmul_rn(neg ? -lv : lv, p);
       packed |= code << (2 * q);
     }
     if (__builtin_expect(ambiguous, 0)) {
@@ -550,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
         cc[j].v[q] = v;
         cc[j].vhi[q] = __fmul_ru(__fmul_ru(v, 1.25f), 1.00000095367431640625f);  // (1 + 2^-20)
         cc[j].vlo[q] = __fmul_rd(__fmul_rd(v, 1.25f), 0.99999904632568359375f);  // (1 - 2^-20)
-        cc[j].ok = cc[j].ok && scale_in_range(fabsf(v));
+        cc[j].ok = cc[j].ok && (v == 0.0f || scale_in_range(fabsf(v)));
       }
     }
     const int r = grp;  // this thread's row inside a phase-B tile
