@@ -58,6 +58,7 @@ struct Params {
   float *u, *v;
   uint8_t *codes, *body_u, *body_v;
   unsigned int *ticket;
+  unsigned long long *ctr;  // dynamic tile counters [phase A, phase B], zeroed before launch
   int scale_mode;
   int stop_after;             // profiling: 1 = phase A only, 2 = A + scales, 0 = full
   unsigned long long *timer;  // profiling: [G][8] globaltimer stamps, or null
@@ -288,14 +289,19 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   // ---- shared memory: [ring area][rp][red][ucache][barriers] ----
   uint8_t *ring = smem;
   double *rp = reinterpret_cast<double *>(smem + p.ring_bytes);  // [SA][RA][kCW]
-  double *red = rp + (size_t)SA * RA * kCW;                      // [64]
-  float *ucache = reinterpret_cast<float *>(red + 64);            // [kUCache]
+  double *red = rp + (size_t)SA * RA * kCW;                      // [512]: block sums + column partials
+  float *ucache = reinterpret_cast<float *>(red + 512);           // [kUCache]
   uint64_t *fullA = reinterpret_cast<uint64_t *>(ucache + kUCache);
   uint64_t *emptyA = fullA + SA;
   uint64_t *fullB = emptyA + SA;
   uint64_t *emptyB = fullB + SI;
   uint64_t *outFull = emptyB + SI;
   uint64_t *outFree = outFull + SO;
+  volatile long long *tileA = reinterpret_cast<volatile long long *>(outFree + SO);  // [SA]
+  volatile long long *tileB = tileA + SA;                                           // [SI]
+  volatile long long *tileO = tileB + SI;                                           // [SO]
+  float *ustage = reinterpret_cast<float *>(
+      (reinterpret_cast<uintptr_t>(const_cast<long long *>(tileO + SO)) + 15) & ~uintptr_t(15));  // [SI][16]
 
   auto stamp = [&](int i) {
     if (p.timer && tid == 0) p.timer[(size_t)cta * 8 + i] = gtimer();
@@ -321,11 +327,9 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
 
   // ================= phase A: |t| partial sums over tiles of RA rows =================
   const InStage LA = in_stage<MODE, XT>(RA, C, MODE == CC_WITH_FEEDBACK);
-  const int64_t KA = p.nTiles > cta ? (p.nTiles - 1 - cta) / G + 1 : 0;
-  auto a_r0 = [&](int64_t k) -> int64_t { return (cta + k * G) * (int64_t)RA; };
   double cta_total = 0.0;
-  auto finish_rows = [&](int s, int64_t k) {
-    const int64_t r0 = a_r0(k);
+  auto finish_rows = [&](int s, long long tile) {  // producer lanes: row sums of a finished tile
+    const int64_t r0 = (int64_t)tile * RA;
     if (lane < RA && r0 + lane < n) {
       double acc = 0.0;
       for (int w = 0; w < p.wpg; ++w) acc += rp[((size_t)s * RA + lane) * kCW + w];
@@ -333,41 +337,60 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       cta_total += acc;
     }
   };
+  // dynamic tile scheduler: the loader claims tiles with an atomic counter and
+  // publishes the tile id with the stage (-1 = no more work)
   if (loader) {
     const uint64_t pol = l2_policy_evict_last();
-    for (int64_t k = 0; k < KA; ++k) {
+    int64_t k = 0;
+    for (;; ++k) {
       const int s = (int)(k % SA);
       if (k >= SA) {
         mbar_wait(&emptyA[s], (uint32_t)(((k / SA) - 1) & 1));
-        finish_rows(s, k - SA);
+        finish_rows(s, tileA[s]);
       }
+      long long tile = 0;
+      if (lane == 0) tile = (long long)atomicAdd(p.ctr, 1ull);
+      tile = __shfl_sync(0xffffffffu, tile, 0);
+      if (tile >= p.nTiles) tile = -1;
       if (lane == 0) {
-        uint8_t *st = ring + (size_t)s * LA.bytes;
-        const int64_t r0 = a_r0(k);
-        const int nrows = (int)min64(RA, n - r0);
-        const uint32_t xb = (uint32_t)(nrows * C * sizeof(XT)), fb = (uint32_t)(nrows * C * 4);
-        const bool wb = MODE == CC_WITH_FEEDBACK;
-        mbar_expect_tx(&fullA[s], xb + (wb ? fb : 0u) + (has_aux<MODE>() ? fb : 0u));
-        bulk_g2s(st + LA.x, X + r0 * C, xb, &fullA[s], pol);
-        if (wb) bulk_g2s(st + LA.base, p.base + r0 * C, fb, &fullA[s], pol);
-        if (has_aux<MODE>()) bulk_g2s(st + LA.aux, p.aux + r0 * C, fb, &fullA[s], pol);
+        tileA[s] = tile;
+        if (tile < 0) {
+          mbar_arrive(&fullA[s]);
+        } else {
+          uint8_t *st = ring + (size_t)s * LA.bytes;
+          const int64_t r0 = (int64_t)tile * RA;
+          const int nrows = (int)min64(RA, n - r0);
+          const uint32_t xb = (uint32_t)(nrows * C * sizeof(XT)), fb = (uint32_t)(nrows * C * 4);
+          const bool wb = MODE == CC_WITH_FEEDBACK;
+          mbar_expect_tx(&fullA[s], xb + (wb ? fb : 0u) + (has_aux<MODE>() ? fb : 0u));
+          bulk_g2s(st + LA.x, X + r0 * C, xb, &fullA[s], pol);
+          if (wb) bulk_g2s(st + LA.base, p.base + r0 * C, fb, &fullA[s], pol);
+          if (has_aux<MODE>()) bulk_g2s(st + LA.aux, p.aux + r0 * C, fb, &fullA[s], pol);
+        }
       }
       __syncwarp();
+      if (tile < 0) break;
     }
-    for (int64_t k = KA - min64(SA, KA); k < KA; ++k) {
-      const int s = (int)(k % SA);
-      mbar_wait(&emptyA[s], (uint32_t)((k / SA) & 1));
-      finish_rows(s, k);
+    for (int64_t q = k - min64(SA - 1, k); q <= k; ++q) {  // drain the stages still in use
+      const int s = (int)(q % SA);
+      mbar_wait(&emptyA[s], (uint32_t)((q / SA) & 1));
+      if (tileA[s] >= 0 && q < k) finish_rows(s, tileA[s]);
     }
   } else if (consumer) {
     double cs[Q][4];
 #pragma unroll
     for (int j = 0; j < Q; ++j) cs[j][0] = cs[j][1] = cs[j][2] = cs[j][3] = 0.0;
-    for (int64_t k = 0; k < KA; ++k) {
+    for (int64_t k = 0;; ++k) {
       const int s = (int)(k % SA);
       mbar_wait(&fullA[s], (uint32_t)((k / SA) & 1));
+      const long long tile = tileA[s];
+      if (tile < 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyA[s]);
+        break;
+      }
       const uint8_t *st = ring + (size_t)s * LA.bytes;
-      const int nrows = (int)min64(RA, n - a_r0(k));
+      const int nrows = (int)min64(RA, n - (int64_t)tile * RA);
       if (grp < p.groups) {
         for (int r = grp; r < nrows; r += p.groups) {
           double rs = 0.0;
@@ -433,32 +456,36 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   // ================= phase F: v_j, g, u_i =================
   if (cta == 0 && tid == 0) *p.ticket = 0u;
   {
-    const int64_t gid = (int64_t)cta * kThreads + tid;
-    const int64_t nthr = (int64_t)G * kThreads;  // multiple of 32
-    for (int64_t b8 = gid & ~7LL; b8 < C * 8; b8 += nthr) {
-      const int64_t j = b8 >> 3;
-      const int part = (int)(gid & 7);
-      // all loads first (G <= kThreads), then add in a fixed order
-      double vals[(kThreads + 7) / 8];
+    // column sums: one CTA per 32-column group; warp w sums slots w, w + nw, ...
+    // (loads issued together), then warp 0 adds the per-warp partials in order
+    constexpr int nw = kThreads / 32;
+    constexpr int kPer = (kThreads + nw - 1) / nw;  // >= ceil(G / nw) since G <= kThreads
+    double *wpart = red + 16;                       // [nw][32] doubles after the block-sum scratch
+    for (int64_t grp32 = cta; grp32 * 32 < C; grp32 += G) {
+      const int64_t j = grp32 * 32 + lane;
+      double vals[kPer];
 #pragma unroll
-      for (int q = 0; q < (kThreads + 7) / 8; ++q) {
-        const int slot = part + 8 * q;
-        vals[q] = slot < G ? __ldcg(p.colpart + (int64_t)slot * C + j) : 0.0;
+      for (int q = 0; q < kPer; ++q) {
+        const int slot = warp + nw * q;
+        vals[q] = (slot < G && j < C) ? __ldcg(p.colpart + (int64_t)slot * C + j) : 0.0;
       }
       double acc = 0.0;
 #pragma unroll
-      for (int q = 0; q < (kThreads + 7) / 8; ++q) acc += vals[q];
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-      if (part == 0) {
-        float v = (float)(acc / (double)n);  // colmean (cx:148)
+      for (int q = 0; q < kPer; ++q) acc += vals[q];
+      wpart[warp * 32 + lane] = acc;
+      __syncthreads();
+      if (warp == 0 && j < C) {
+        double sacc = 0.0;
+        for (int w = 0; w < nw; ++w) sacc += wpart[w * 32 + lane];
+        float v = (float)(sacc / (double)n);  // colmean (cx:148)
         if (p.scale_mode == CC_SCALE_PER_TOKEN) v = 1.0f;
         p.v[j] = v;
         store_f32_bytes(p.body_v + 4 * j, v);
       }
+      __syncthreads();
     }
   }
+  stamp(7);
   {
     const double part = tid < G ? __ldcg(p.blkpart + tid) : 0.0;  // G <= kThreads (launcher)
     const double tot = block_sum(part, red);
@@ -489,45 +516,48 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   const OutStage LO = out_stage<MODE>(RB, C, p.cb_row);
   uint8_t *in_ring = ring;
   uint8_t *out_ring = ring + (size_t)SI * LI.bytes;
-  const int64_t nTB = (n + RB - 1) / RB;
-  const int64_t KB = nTB > cta ? (nTB - 1 - cta) / G + 1 : 0;
-  auto b_r0 = [&](int64_t k) -> int64_t { return (cta + (KB - 1 - k) * G) * (int64_t)RB; };  // reversed
-  const bool ucached = KB * RB <= kUCache;
-  if (ucached) {
-    for (int i = tid; i < KB * RB; i += kThreads) {
-      const int64_t row = b_r0(i / RB) + i % RB;
-      ucache[i] = row < n ? __ldcg(p.u + row) : 0.0f;
-    }
-  }
-  __syncthreads();
-
+  const int64_t nTB = (n + RB - 1) / RB;  // tiles claimed in REVERSE row order
   double err = 0.0, tsq = 0.0;
   if (loader) {
     const uint64_t pol = l2_policy_evict_first();
-    for (int64_t k = 0; k < KB; ++k) {
+    for (int64_t k = 0;; ++k) {
       const int s = (int)(k % SI);
       if (k >= SI) mbar_wait(&emptyB[s], (uint32_t)(((k / SI) - 1) & 1));
+      long long t = 0;
+      if (lane == 0) t = (long long)atomicAdd(p.ctr + 1, 1ull);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      const long long tile = t < nTB ? nTB - 1 - t : -1;
       if (lane == 0) {
-        uint8_t *st = in_ring + (size_t)s * LI.bytes;
-        const int64_t r0 = b_r0(k);
-        const int nrows = (int)min64(RB, n - r0);
-        const uint32_t xb = (uint32_t)(nrows * C * sizeof(XT)), fb = (uint32_t)(nrows * C * 4);
-        mbar_expect_tx(&fullB[s], xb + (has_aux<MODE>() ? 2 * fb : 0u));
-        bulk_g2s(st + LI.x, X + r0 * C, xb, &fullB[s], pol);
-        if (has_aux<MODE>()) {
-          bulk_g2s(st + LI.base, p.base + r0 * C, fb, &fullB[s], pol);
-          bulk_g2s(st + LI.aux, p.aux + r0 * C, fb, &fullB[s], pol);
+        tileB[s] = tile;
+        if (tile < 0) {
+          mbar_arrive(&fullB[s]);
+        } else {
+          uint8_t *st = in_ring + (size_t)s * LI.bytes;
+          const int64_t r0 = (int64_t)tile * RB;
+          const int nrows = (int)min64(RB, n - r0);
+          const uint32_t xb = (uint32_t)(nrows * C * sizeof(XT)), fb = (uint32_t)(nrows * C * 4);
+          const uint32_t ub = (uint32_t)(((r0 & 3) + nrows + 3) / 4 * 16);  // 16B window of u
+          mbar_expect_tx(&fullB[s], xb + (has_aux<MODE>() ? 2 * fb : 0u) + ub);
+          bulk_g2s(ustage + (size_t)s * 16, p.u + (r0 & ~3LL), ub, &fullB[s], pol);
+          bulk_g2s(st + LI.x, X + r0 * C, xb, &fullB[s], pol);
+          if (has_aux<MODE>()) {
+            bulk_g2s(st + LI.base, p.base + r0 * C, fb, &fullB[s], pol);
+            bulk_g2s(st + LI.aux, p.aux + r0 * C, fb, &fullB[s], pol);
+          }
         }
       }
       __syncwarp();
+      if (tile < 0) break;
     }
   } else if (storer) {
-    for (int64_t k = 0; k < KB; ++k) {
+    for (int64_t k = 0;; ++k) {
       const int o = (int)(k % SO);
       mbar_wait(&outFull[o], (uint32_t)((k / SO) & 1));
+      const long long tile = tileO[o];
+      if (tile < 0) break;
       if (lane == 0) {
         const uint8_t *so = out_ring + (size_t)o * LO.bytes;
-        const int64_t r0 = b_r0(k);
+        const int64_t r0 = (int64_t)tile * RB;
         const int nrows = (int)min64(RB, n - r0);
         bulk_s2g(p.base + r0 * C, so + LO.base, (uint32_t)(nrows * C * 4));
         if constexpr (has_aux<MODE>()) bulk_s2g(p.aux + r0 * C, so + LO.aux, (uint32_t)(nrows * C * 4));
@@ -555,11 +585,22 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       }
     }
     const int r = grp;  // this thread's row inside a phase-B tile
-    for (int64_t k = 0; k < KB; ++k) {
+    for (int64_t k = 0;; ++k) {
       const int s = (int)(k % SI);
+      const int o = (int)(k % SO);
       mbar_wait(&fullB[s], (uint32_t)((k / SI) & 1));
+      const long long tile = tileB[s];
+      if (tile < 0) {  // forward the end-of-work marker to the store warp
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyB[s]);
+        if (k >= SO) mbar_wait(&outFree[o], (uint32_t)(((k / SO) - 1) & 1));
+        if (tid == 0) tileO[o] = -1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&outFull[o]);
+        break;
+      }
       const uint8_t *st = in_ring + (size_t)s * LI.bytes;
-      const int64_t r0 = b_r0(k);
+      const int64_t r0 = (int64_t)tile * RB;
       const bool row_live = in_group && r0 + r < n;
       float xx[Q][4], bb[Q][4], aa[Q][4];
 #pragma unroll
@@ -567,20 +608,19 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
 #pragma unroll
         for (int q = 0; q < 4; ++q) xx[j][q] = bb[j][q] = aa[j][q] = 0.f;
         if (row_live && qact[j]) {
-          const size_t o = (size_t)r * C + qcol[j];
-          unpack_x(reinterpret_cast<const XT *>(st + LI.x) + o, xx[j]);
+          const size_t oo = (size_t)r * C + qcol[j];
+          unpack_x(reinterpret_cast<const XT *>(st + LI.x) + oo, xx[j]);
           if constexpr (has_aux<MODE>()) {
-            unpack_f(reinterpret_cast<const float *>(st + LI.base) + o, bb[j]);
-            unpack_f(reinterpret_cast<const float *>(st + LI.aux) + o, aa[j]);
+            unpack_f(reinterpret_cast<const float *>(st + LI.base) + oo, bb[j]);
+            unpack_f(reinterpret_cast<const float *>(st + LI.aux) + oo, aa[j]);
           }
         }
       }
+      const float uf = row_live ? ustage[(size_t)s * 16 + (r0 & 3) + r] : 1.0f;
       __syncwarp();
       if (lane == 0) mbar_arrive(&emptyB[s]);  // inputs are in registers: the loader may refill
-      const int o = (int)(k % SO);
       if (k >= SO) mbar_wait(&outFree[o], (uint32_t)(((k / SO) - 1) & 1));
       uint8_t *so = out_ring + (size_t)o * LO.bytes;
-      const float uf = row_live ? (ucached ? ucache[k * RB + r] : __ldcg(p.u + r0 + r)) : 1.0f;
       const bool row_ok = scale_in_range(fabsf(uf));
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
@@ -616,6 +656,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
           if (live) *reinterpret_cast<uint16_t *>(crow + (qcol[j] >> 1)) = (uint16_t)packed;
         }
       }
+      if (tid == 0) tileO[o] = tile;
       fence_proxy_async_smem();  // results -> visible to the TMA store engine
       __syncwarp();
       if (lane == 0) mbar_arrive(&outFull[o]);
@@ -678,6 +719,7 @@ int64_t fused_workspace_bytes(int64_t n, int64_t C) {
   add(sizeof(float) * n);
   add(sizeof(float) * C);
   add(256);
+  add(256);
   return (int64_t)b;
 }
 
@@ -685,7 +727,7 @@ template <int MODE, int CODEC, typename XT, int Q>
 static int launch_fused(fused::Params &p, cudaStream_t st) {
   using namespace fused;
   auto kern = k1_fused<MODE, CODEC, XT, Q>;
-  const size_t fixed_tail = 64 * 8 + kUCache * 4 + 2 * 16 * 8 + 2 * 8 * 8 + 2 * 8 * 8 + 256;
+  const size_t fixed_tail = 512 * 8 + kUCache * 4 + 3 * 8 * 8 * 3 + 8 * 64 + 256;
   const size_t budget = kSmemBudget;
   // phase B rings (tiles of `groups` rows): loads S_in, outputs S_out
   const InStage LI = in_stage<MODE, XT>(p.groups, p.C, has_aux<MODE>());
@@ -717,11 +759,12 @@ static int launch_fused(fused::Params &p, cudaStream_t st) {
   p.S_in = SI;
   p.S_out = SO;
   p.ring_bytes = (uint32_t)align_up(std::max(ringA, ringB), 128);
-  const size_t smem = p.ring_bytes + (size_t)SA * p.R * kCW * 8 + 64 * 8 + kUCache * 4 +
-                      (size_t)(2 * SA + 2 * SI + 2 * SO) * 8 + 128;
+  const size_t smem = p.ring_bytes + (size_t)SA * p.R * kCW * 8 + 512 * 8 + kUCache * 4 +
+                      (size_t)(3 * SA + 3 * SI + 3 * SO) * 8 + 16 + (size_t)SI * 64 + 128;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return cuda_status("k1_fused attr");
   void *args[] = {&p};
+  cudaMemsetAsync(p.ctr, 0, 2 * sizeof(unsigned long long), st);  // dynamic tile counters
   cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(p.G), dim3(kThreads), args, smem, st);
   if (e != cudaSuccess) {
     set_error(std::string("k1_fused launch: ") + cudaGetErrorString(e));
@@ -776,6 +819,7 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   p.u = reinterpret_cast<float *>(take(sizeof(float) * n));
   p.v = reinterpret_cast<float *>(take(sizeof(float) * C));
   p.ticket = reinterpret_cast<unsigned int *>(take(256));
+  p.ctr = reinterpret_cast<unsigned long long *>(take(256));
   if ((int64_t)off > ws_bytes) {
     set_error("fused workspace too small");
     return CC_ERR_ARG;

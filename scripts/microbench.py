@@ -94,7 +94,7 @@ def main():
     g = int((tb[:, 0] > 0).sum())
     tb = tb[:g].double()
     t0 = tb[:, 0].min()
-    names = ["start", "A_done", "sync1", "F_done", "sync2", "B_done", "end"]
+    names = ["start", "A_done", "sync1", "F_done", "sync2", "B_done", "end", "F_cols"]
     out["fused_timeline_us"] = {nm: [round(float((tb[:, i] - t0).min()) / 1e3, 2),
                                      round(float((tb[:, i] - t0).max()) / 1e3, 2)] for i, nm in enumerate(names)}
     out["fused_grid"] = g
