@@ -178,6 +178,8 @@ CC_API void cc_debug_fused_timer(void *dev_buf);
 /* profiling only: L2 eviction policy of the persistent K1's TMA loads
  * (0 evict_last/evict_first (default), 1 normal/normal, 2 normal/first, 3 last/normal) */
 CC_API void cc_debug_fused_policy(int policy);
+/* profiling only: phase-B ring depths of the persistent K1 (0 = automatic) */
+CC_API void cc_debug_fused_rings(int s_in, int s_out);
 
 #ifdef __cplusplus
 }

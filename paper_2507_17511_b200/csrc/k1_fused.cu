@@ -694,6 +694,11 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
 // ---------------------------------------------------------------------------
 static int g_fused_stop = 0;
 static int g_fused_policy = 0;
+static int g_fused_si = 0, g_fused_so = 0;
+void set_fused_rings(int si, int so) {
+  g_fused_si = si;
+  g_fused_so = so;
+}
 static unsigned long long *g_fused_timer = nullptr;
 void set_fused_policy(int v) { g_fused_policy = v; }
 void set_fused_stop(int v) { g_fused_stop = v; }
@@ -733,11 +738,11 @@ static int launch_fused(fused::Params &p, cudaStream_t st) {
   const InStage LI = in_stage<MODE, XT>(p.groups, p.C, has_aux<MODE>());
   const OutStage LO = out_stage<MODE>(p.groups, p.C, p.cb_row);
   const InStage LA = in_stage<MODE, XT>(p.R, p.C, MODE == CC_WITH_FEEDBACK);
-  int SO = 2, SI = 0;
+  int SO = g_fused_so > 0 ? g_fused_so : 2, SI = 0;
   for (;;) {
     const size_t avail = budget - fixed_tail - (size_t)3 * p.R * kCW * 8;
     if ((size_t)SO * LO.bytes + 2 * (size_t)LI.bytes <= avail) {
-      SI = (int)std::min<size_t>(8, (avail - (size_t)SO * LO.bytes) / LI.bytes);
+      SI = (int)std::min<size_t>(g_fused_si > 0 ? g_fused_si : 8, (avail - (size_t)SO * LO.bytes) / LI.bytes);
       break;
     }
     if (SO == 1) break;

@@ -76,13 +76,13 @@ def main():
         out[name] = {"us": round(us, 2), "alg_GBps": round(alg / us / 1e3, 1)}
     lib.cc_set_quant_path(-1)
     lib.cc_debug_fused_stop(0)
-    for pol in (1, 2, 3):
-        lib.cc_debug_fused_policy(pol)
+    for si, so in ((6, 1), (4, 2), (3, 3), (2, 4)):
+        lib.cc_debug_fused_rings(si, so)
         for i in range(L):
             enc(i)
         us = timed(enc, a.reps)
-        out[f"k1_fused_policy{pol}"] = {"us": round(us, 2), "alg_GBps": round(alg / us / 1e3, 1)}
-    lib.cc_debug_fused_policy(0)
+        out[f"k1_fused_rings{si}_{so}"] = {"us": round(us, 2), "alg_GBps": round(alg / us / 1e3, 1)}
+    lib.cc_debug_fused_rings(0, 0)
     # per-phase timeline of one fused launch (globaltimer stamps per CTA)
     tbuf = torch.zeros(1024 * 8, dtype=torch.int64, device="cuda")
     lib.cc_debug_fused_timer(_lib.ptr(tbuf))
