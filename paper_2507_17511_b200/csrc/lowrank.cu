@@ -1,0 +1,532 @@
+// K3: low-rank residual compressor (compressors.py:394-426, linalg.py:49-112).
+//
+//   Q0 = orth(G)                      G ~ N(0,1)[C, r] drawn on the host (cx:407)
+//   T x { Z = A^T (A Q);  Q = orth(Z) }
+//   U = orth(A Q);  W = A^T U         payload: U, W as column-major f16, or INT4
+//                                     per-column codes + f32 ranges (cx:556-566)
+//   decode: A_hat = U W^T             (cx:286-288), accumulated into the base
+//
+// The projections are skinny GEMMs (N = r <= 32) that stream A once per pass;
+// they accumulate in f64 like the reference's la.matmul (la:49-58).  orth() is
+// CholQR2 in f64: two passes of  G = M^T M (multi-CTA partial Grams, fixed-order
+// reduction) -> Cholesky -> M <- M R^-1.  That computes the same Q as the
+// reference's CGS2 (QR with positive diagonal) up to rounding; if a pivot falls
+// below the reference's degeneracy tolerance (la:13, 1e-12) a single-CTA CGS2
+// with random replacement columns takes over (rank-deficient inputs).
+// Parity is tolerance-based (f64 summation order), see tests/test_gpu_lowrank.py.
+#include "cc_common.cuh"
+#include "cc_internal.h"
+
+#include <algorithm>
+#include <curand_kernel.h>
+
+namespace cc {
+namespace lr {
+
+constexpr int kMaxR = 32;
+constexpr int kThreads = 256;
+constexpr int kRowsAQ = 32;    // rows per CTA in Y = A Q
+constexpr int kKChunk = 96;    // K chunk staged in shared memory
+constexpr int kColsATY = 32;   // columns of A per CTA in Z = A^T Y
+constexpr int kSplitATY = 4;   // row splits (partial Z, fixed-order reduction)
+constexpr int kGramRows = 128; // rows per CTA in the Gram partials
+constexpr double kDegenerate = 1e-12;  // la:13
+
+// ---------------------------------------------------------------------------
+// Y[n, r] = A[n, C] Q[C, r]   (f64 accumulate, f32 store: la.matmul)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_aq(const float *__restrict__ A, const float *__restrict__ Q,
+                                                  float *__restrict__ Y, int64_t n, int64_t C, int r) {
+  __shared__ double qs[kKChunk][kMaxR + 1];
+  __shared__ float as[kRowsAQ][kKChunk + 1];
+  const int64_t i0 = (int64_t)blockIdx.x * kRowsAQ;
+  // thread -> (row ii, output column pair)
+  const int outs = kRowsAQ * r;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t k0 = 0; k0 < C; k0 += kKChunk) {
+    const int kc = (int)min64(kKChunk, C - k0);
+    for (int e = threadIdx.x; e < kc * r; e += kThreads) {
+      const int kk = e / r, j = e % r;
+      qs[kk][j] = (double)Q[(k0 + kk) * r + j];
+    }
+    for (int e = threadIdx.x; e < kRowsAQ * kc; e += kThreads) {
+      const int ii = e / kc, kk = e % kc;
+      as[ii][kk] = (i0 + ii < n) ? A[(i0 + ii) * C + k0 + kk] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int o = threadIdx.x + s * kThreads;
+      if (o < outs) {
+        const int ii = o / r, j = o % r;
+        double a = acc[s];
+        for (int kk = 0; kk < kc; ++kk) a += (double)as[ii][kk] * qs[kk][j];
+        acc[s] = a;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int o = threadIdx.x + s * kThreads;
+    if (o < outs) {
+      const int ii = o / r, j = o % r;
+      if (i0 + ii < n) Y[(i0 + ii) * r + j] = (float)acc[s];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Zpart[split][C, r] = A[rows of split, :]^T Y[rows of split, :]
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_aty(const float *__restrict__ A, const float *__restrict__ Y,
+                                                   double *__restrict__ Zpart, int64_t n, int64_t C, int r) {
+  __shared__ float as[64][kColsATY + 1];
+  __shared__ double ys[64][kMaxR + 1];
+  const int64_t c0 = (int64_t)blockIdx.x * kColsATY;
+  const int split = blockIdx.y;
+  const int64_t rows_per = (n + kSplitATY - 1) / kSplitATY;
+  const int64_t rlo = split * rows_per, rhi = min64(n, rlo + rows_per);
+  const int outs = kColsATY * r;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i0 = rlo; i0 < rhi; i0 += 64) {
+    const int rc = (int)min64(64, rhi - i0);
+    for (int e = threadIdx.x; e < rc * kColsATY; e += kThreads) {
+      const int ii = e / kColsATY, cc = e % kColsATY;
+      as[ii][cc] = (c0 + cc < C) ? A[(i0 + ii) * C + c0 + cc] : 0.0f;
+    }
+    for (int e = threadIdx.x; e < rc * r; e += kThreads) {
+      const int ii = e / r, j = e % r;
+      ys[ii][j] = (double)Y[(i0 + ii) * r + j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int o = threadIdx.x + s * kThreads;
+      if (o < outs) {
+        const int cc = o % kColsATY, j = o / kColsATY;
+        double a = acc[s];
+        for (int ii = 0; ii < rc; ++ii) a += (double)as[ii][cc] * ys[ii][j];
+        acc[s] = a;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int o = threadIdx.x + s * kThreads;
+    if (o < outs) {
+      const int cc = o % kColsATY, j = o / kColsATY;
+      if (c0 + cc < C) Zpart[((int64_t)split * C + c0 + cc) * r + j] = acc[s];
+    }
+  }
+}
+
+// Z[C, r] (f32) = sum over splits in order
+__global__ void k_zsum(const double *__restrict__ Zpart, float *__restrict__ Z, int64_t C, int r) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= C * r) return;
+  double s = 0.0;
+  for (int sp = 0; sp < kSplitATY; ++sp) s += Zpart[sp * C * r + e];
+  Z[e] = (float)s;
+}
+
+// ---------------------------------------------------------------------------
+// CholQR2 (f64): M[m, r] -> orthonormal columns, positive R diagonal
+// ---------------------------------------------------------------------------
+__global__ void k_to64(const float *__restrict__ in, double *__restrict__ out, int64_t cnt) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < cnt) out[e] = (double)in[e];
+}
+
+__global__ void __launch_bounds__(kThreads) k_gram(const double *__restrict__ M, double *__restrict__ Gpart,
+                                                    int64_t m, int r) {
+  __shared__ double ms[kGramRows][kMaxR + 1];
+  const int64_t i0 = (int64_t)blockIdx.x * kGramRows;
+  const int rc = (int)min64(kGramRows, m - i0);
+  for (int e = threadIdx.x; e < rc * r; e += kThreads) ms[e / r][e % r] = M[(i0 + e / r) * r + e % r];
+  __syncthreads();
+  for (int o = threadIdx.x; o < r * r; o += kThreads) {
+    const int a = o / r, b = o % r;
+    double s = 0.0;
+    for (int i = 0; i < rc; ++i) s += ms[i][a] * ms[i][b];
+    Gpart[(int64_t)blockIdx.x * r * r + o] = s;
+  }
+}
+
+// one CTA: G = sum of partials (fixed order); Cholesky G = R^T R; Rinv = R^-1;
+// flag = 1 if any pivot^2 < tol (degenerate column -> CGS2 fallback)
+__global__ void k_chol(const double *__restrict__ Gpart, int nblk, int r, double *__restrict__ Rinv,
+                       int *__restrict__ flag, int pass) {
+  __shared__ double G[kMaxR][kMaxR + 1];
+  __shared__ double R[kMaxR][kMaxR + 1];
+  __shared__ int bad;
+  for (int o = threadIdx.x; o < r * r; o += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += Gpart[(int64_t)b * r * r + o];
+    G[o / r][o % r] = s;
+  }
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < r; ++i)
+      for (int j = 0; j < r; ++j) R[i][j] = 0.0;
+    for (int j = 0; j < r; ++j) {
+      double piv = G[j][j];
+      for (int k = 0; k < j; ++k) piv -= R[k][j] * R[k][j];
+      if (!(piv >= kDegenerate)) {
+        bad = 1;
+        piv = 1.0;
+      }
+      const double d = sqrt(piv);
+      R[j][j] = d;
+      for (int c = j + 1; c < r; ++c) {
+        double s = G[j][c];
+        for (int k = 0; k < j; ++k) s -= R[k][j] * R[k][c];
+        R[j][c] = s / d;
+      }
+    }
+    // Rinv (upper triangular) by back substitution, column by column
+    for (int c = 0; c < r; ++c) {
+      for (int i = r - 1; i >= 0; --i) {
+        double s = (i == c) ? 1.0 : 0.0;
+        for (int k = i + 1; k < r; ++k) s -= R[i][k] * Rinv[k * r + c];
+        Rinv[i * r + c] = (i > c) ? 0.0 : s / R[i][i];
+      }
+    }
+    if (pass == 0) *flag = bad;
+    else *flag |= bad;
+  }
+}
+
+// M <- M Rinv (row-wise, f64)
+__global__ void __launch_bounds__(kThreads) k_apply_rinv(double *__restrict__ M, const double *__restrict__ Rinv,
+                                                          int64_t m, int r) {
+  __shared__ double rs[kMaxR * kMaxR];
+  for (int e = threadIdx.x; e < r * r; e += kThreads) rs[e] = Rinv[e];
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (i >= m) return;
+  double row[kMaxR];
+  for (int k = 0; k < r; ++k) row[k] = M[i * r + k];
+  for (int c = 0; c < r; ++c) {
+    double s = 0.0;
+    for (int k = 0; k <= c; ++k) s += row[k] * rs[k * r + c];
+    M[i * r + c] = s;
+  }
+}
+
+// Fallback (rank-deficient input): CGS2 with two projection passes, degenerate
+// columns replaced by N(0,1) draws (la:77-112).  One CTA, only when flagged.
+__global__ void __launch_bounds__(1024) k_cgs2_fallback(const float *__restrict__ orig, double *__restrict__ M,
+                                                         int64_t m, int r, const int *__restrict__ flag,
+                                                         unsigned long long seed) {
+  if (*flag == 0) return;
+  __shared__ double red[32];
+  __shared__ double coef[kMaxR];
+  auto block_sum = [&](double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+      red[0] = s;
+    }
+    __syncthreads();
+    s = red[0];
+    __syncthreads();
+    return s;
+  };
+  curandStatePhilox4_32_10_t rng;
+  curand_init(seed, threadIdx.x, 0, &rng);
+  for (int64_t e = threadIdx.x; e < m * r; e += blockDim.x) M[e] = (double)orig[e];
+  __syncthreads();
+  for (int j = 0; j < r; ++j) {
+    for (int attempt = 0;; ++attempt) {
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int k = 0; k < j; ++k) {
+          double part = 0.0;
+          for (int64_t i = threadIdx.x; i < m; i += blockDim.x) part += M[i * r + k] * M[i * r + j];
+          const double s = block_sum(part);
+          if (threadIdx.x == 0) coef[k] = s;
+        }
+        __syncthreads();
+        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+          double v = M[i * r + j];
+          for (int k = 0; k < j; ++k) v -= M[i * r + k] * coef[k];
+          M[i * r + j] = v;
+        }
+        __syncthreads();
+      }
+      double part = 0.0;
+      for (int64_t i = threadIdx.x; i < m; i += blockDim.x) part += M[i * r + j] * M[i * r + j];
+      const double nsq = block_sum(part);
+      if (nsq >= kDegenerate || attempt > 16) {
+        const double inv = 1.0 / sqrt(nsq);
+        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) M[i * r + j] *= inv;
+        __syncthreads();
+        break;
+      }
+      for (int64_t i = threadIdx.x; i < m; i += blockDim.x) M[i * r + j] = (double)curand_normal(&rng);
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void k_to32(const double *__restrict__ in, float *__restrict__ out, int64_t cnt) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < cnt) out[e] = (float)in[e];
+}
+
+// ---------------------------------------------------------------------------
+// packing (cx:415-426, 556-566, 589-595)
+// ---------------------------------------------------------------------------
+// f16 body: U column-major [n, r] then W column-major [C, r]
+__global__ void k_pack_f16(const float *__restrict__ F, int64_t m, int r, __half *__restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // column-major index
+  if (e >= m * r) return;
+  const int64_t j = e / m, i = e % m;
+  out[e] = __float2half_rn(F[i * r + j]);
+}
+
+// per-column max |f| -> ranges (f32); one CTA per column
+__global__ void k_colmax(const float *__restrict__ F, int64_t m, int r, float *__restrict__ ranges) {
+  const int j = blockIdx.x;
+  float mx = 0.0f;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) mx = fmaxf(mx, fabsf(F[i * r + j]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  __shared__ float sm[32];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float v = 0.0f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmaxf(v, sm[w]);
+    ranges[j] = v;
+  }
+}
+
+__device__ __forceinline__ uint32_t int4_code(float f, float range) {
+  if (!(range > 0.0f)) return 0u;  // zero column: code 0 (cx:561-562)
+  const double rg = (double)range;
+  const double step = 2.0 * rg / 15.0;
+  double c = rint(((double)f + rg) / step);  // half-even like np.rint
+  c = c < 0.0 ? 0.0 : (c > 15.0 ? 15.0 : c);
+  return (uint32_t)c;
+}
+
+// nibble stream: U column-major then W column-major, low nibble first
+__global__ void k_pack_int4(const float *__restrict__ U, const float *__restrict__ W, int64_t n, int64_t C, int r,
+                            const float *__restrict__ ur, const float *__restrict__ wr, uint8_t *__restrict__ nib) {
+  const int64_t total = (n + C) * r;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // output byte
+  if (2 * b >= total) return;
+  uint32_t byte = 0;
+  for (int h = 0; h < 2; ++h) {
+    const int64_t e = 2 * b + h;
+    if (e >= total) break;
+    uint32_t code;
+    if (e < n * r) {
+      const int64_t j = e / n, i = e % n;
+      code = int4_code(U[i * r + j], ur[j]);
+    } else {
+      const int64_t e2 = e - n * r;
+      const int64_t j = e2 / C, i = e2 % C;
+      code = int4_code(W[i * r + j], wr[j]);
+    }
+    byte |= code << (4 * h);
+  }
+  nib[b] = (uint8_t)byte;
+}
+
+// ---------------------------------------------------------------------------
+// decode: base (+)= U W^T from a body (f16 or INT4 factors), f64 accumulate
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double factor_at(const uint8_t *body, int int4, int64_t n, int64_t C, int r, int which,
+                                            int64_t i, int j) {
+  if (!int4) {
+    const __half *h = reinterpret_cast<const __half *>(body);
+    const int64_t off = which == 0 ? (int64_t)j * n + i : n * r + (int64_t)j * C + i;
+    return (double)__half2float(h[off]);
+  }
+  const float *rg = reinterpret_cast<const float *>(body);
+  const double range = (double)(which == 0 ? rg[j] : rg[r + j]);
+  const int64_t e = which == 0 ? (int64_t)j * n + i : n * r + (int64_t)j * C + i;
+  const uint8_t *nib = body + 8 * r;
+  const uint32_t code = (nib[e >> 1] >> (4 * (e & 1))) & 15u;
+  return -range + (double)code * (2.0 * range / 15.0);  // cx:569-572
+}
+
+// factors -> f64 scratch (Uf [n, r], Wf [C, r]) once, then the outer product
+__global__ void k_unpack_factors(const uint8_t *__restrict__ body, int int4, int64_t n, int64_t C, int r,
+                                 double *__restrict__ Uf, double *__restrict__ Wf) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n * r) Uf[e] = factor_at(body, int4, n, C, r, 0, e / r, (int)(e % r));
+  else if (e < (n + C) * r) {
+    const int64_t e2 = e - n * r;
+    Wf[e2] = factor_at(body, int4, n, C, r, 1, e2 / r, (int)(e2 % r));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_outer(const double *__restrict__ Uf, const double *__restrict__ Wf,
+                                                     int64_t n, int64_t C, int r, float *__restrict__ out, int acc) {
+  __shared__ double us[8][kMaxR];
+  const int64_t i0 = (int64_t)blockIdx.y * 8;
+  for (int e = threadIdx.x; e < 8 * r; e += kThreads) {
+    const int ii = e / r, k = e % r;
+    us[ii][k] = (i0 + ii < n) ? Uf[(i0 + ii) * r + k] : 0.0;
+  }
+  __syncthreads();
+  const int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (j >= C) return;
+  double w[kMaxR];
+  for (int k = 0; k < r; ++k) w[k] = Wf[j * r + k];
+  for (int ii = 0; ii < 8 && i0 + ii < n; ++ii) {
+    double s = 0.0;
+    for (int k = 0; k < r; ++k) s += us[ii][k] * w[k];
+    const int64_t e = (i0 + ii) * C + j;
+    out[e] = acc ? __fadd_rn(out[e], (float)s) : (float)s;
+  }
+}
+
+struct Work {
+  float *Q, *Y, *Z, *U, *W;
+  double *Zpart, *M64, *Gpart, *Rinv, *Uf, *Wf;
+  float *ur, *wr;
+  int *flag;
+};
+
+static Work carve(void *ws, int64_t n, int64_t C, int64_t r, size_t *bytes) {
+  Work w{};
+  uint8_t *b = reinterpret_cast<uint8_t *>(ws);
+  size_t off = 0;
+  auto take = [&](size_t sz) {
+    uint8_t *q = b ? b + off : nullptr;
+    off = align_up(off + sz, 256);
+    return q;
+  };
+  const int64_t m = std::max(n, C);
+  w.Q = reinterpret_cast<float *>(take(4 * C * r));
+  w.Y = reinterpret_cast<float *>(take(4 * n * r));
+  w.Z = reinterpret_cast<float *>(take(4 * C * r));
+  w.U = reinterpret_cast<float *>(take(4 * n * r));
+  w.W = reinterpret_cast<float *>(take(4 * C * r));
+  w.Zpart = reinterpret_cast<double *>(take(8 * kSplitATY * C * r));
+  w.M64 = reinterpret_cast<double *>(take(8 * m * r));
+  w.Gpart = reinterpret_cast<double *>(take(8 * cdiv(m, kGramRows) * r * r));
+  w.Rinv = reinterpret_cast<double *>(take(8 * r * r));
+  w.Uf = reinterpret_cast<double *>(take(8 * n * r));
+  w.Wf = reinterpret_cast<double *>(take(8 * C * r));
+  w.ur = reinterpret_cast<float *>(take(4 * r));
+  w.wr = reinterpret_cast<float *>(take(4 * r));
+  w.flag = reinterpret_cast<int *>(take(256));
+  if (bytes) *bytes = off;
+  return w;
+}
+
+}  // namespace lr
+
+int64_t lowrank_workspace_bytes(int64_t n, int64_t C, int64_t r) {
+  size_t b = 0;
+  lr::carve(nullptr, n, C, r, &b);
+  return (int64_t)b;
+}
+
+static unsigned long long g_lr_seed = 0x5eed5eedULL;
+
+// M (f32 [m, r]) -> orthonormal f32 columns written to out (may alias M)
+static void orth(const float *M, float *out, int64_t m, int r, const lr::Work &w, cudaStream_t st) {
+  using namespace lr;
+  const int64_t cnt = m * r;
+  const unsigned b1 = (unsigned)cdiv(cnt, 256);
+  k_to64<<<b1, 256, 0, st>>>(M, w.M64, cnt);
+  const int nblk = (int)cdiv(m, kGramRows);
+  for (int pass = 0; pass < 2; ++pass) {
+    k_gram<<<nblk, kThreads, 0, st>>>(w.M64, w.Gpart, m, r);
+    k_chol<<<1, 256, 0, st>>>(w.Gpart, nblk, r, w.Rinv, w.flag, pass);
+    k_apply_rinv<<<(unsigned)cdiv(m, kThreads), kThreads, 0, st>>>(w.M64, w.Rinv, m, r);
+  }
+  k_cgs2_fallback<<<1, 1024, 0, st>>>(M, w.M64, m, r, w.flag, g_lr_seed++);
+  k_to32<<<b1, 256, 0, st>>>(w.M64, out, cnt);
+  count_launch(4 + 6);
+}
+
+static void aq(const float *A, const float *Q, float *Y, int64_t n, int64_t C, int r, cudaStream_t st) {
+  lr::k_aq<<<(unsigned)cdiv(n, lr::kRowsAQ), lr::kThreads, 0, st>>>(A, Q, Y, n, C, r);
+  count_launch();
+}
+
+static void aty(const float *A, const float *Y, float *Z, const lr::Work &w, int64_t n, int64_t C, int r,
+                cudaStream_t st) {
+  dim3 g((unsigned)cdiv(C, lr::kColsATY), lr::kSplitATY);
+  lr::k_aty<<<g, lr::kThreads, 0, st>>>(A, Y, w.Zpart, n, C, r);
+  lr::k_zsum<<<(unsigned)cdiv(C * r, 256), 256, 0, st>>>(w.Zpart, Z, C, r);
+  count_launch(2);
+}
+
+static void decode_into(const uint8_t *body, int int4, int64_t n, int64_t C, int r, float *out, int acc,
+                        const lr::Work &w, cudaStream_t st) {
+  lr::k_unpack_factors<<<(unsigned)cdiv((n + C) * r, 256), 256, 0, st>>>(body, int4, n, C, r, w.Uf, w.Wf);
+  dim3 g((unsigned)cdiv(C, lr::kThreads), (unsigned)cdiv(n, 8));
+  lr::k_outer<<<g, lr::kThreads, 0, st>>>(w.Uf, w.Wf, n, C, r, out, acc);
+  count_launch(2);
+}
+
+int lowrank_encode(int int4, int64_t n, int64_t C, int64_t r64, int iters, const float *t, const float *q0,
+                   uint8_t *body, float *decoded, void *ws, int64_t ws_bytes, cudaStream_t st) {
+  const int r = (int)r64;
+  if (r > lr::kMaxR) {
+    set_error("low-rank: rank > 32 not supported on device");
+    return CC_ERR_UNSUPPORTED;
+  }
+  size_t need = 0;
+  lr::carve(nullptr, n, C, r, &need);
+  if ((int64_t)need > ws_bytes) {
+    set_error("low-rank workspace too small");
+    return CC_ERR_ARG;
+  }
+  const lr::Work w = lr::carve(ws, n, C, r, nullptr);
+  orth(q0, w.Q, C, r, w, st);                  // Q0 = orth(G)        (cx:407)
+  for (int it = 0; it < iters; ++it) {         // (cx:408-410)
+    aq(t, w.Q, w.Y, n, C, r, st);
+    aty(t, w.Y, w.Z, w, n, C, r, st);
+    orth(w.Z, w.Q, C, r, w, st);
+  }
+  aq(t, w.Q, w.Y, n, C, r, st);
+  orth(w.Y, w.U, n, r, w, st);                 // U = orth(A Q)       (cx:411)
+  aty(t, w.U, w.W, w, n, C, r, st);            // W = A^T U           (cx:419)
+  if (!int4) {
+    __half *h = reinterpret_cast<__half *>(body);
+    lr::k_pack_f16<<<(unsigned)cdiv(n * r, 256), 256, 0, st>>>(w.U, n, r, h);
+    lr::k_pack_f16<<<(unsigned)cdiv(C * r, 256), 256, 0, st>>>(w.W, C, r, h + n * r);
+    count_launch(2);
+  } else {
+    float *ranges = reinterpret_cast<float *>(body);  // 2r f32: U ranges then W ranges
+    lr::k_colmax<<<r, 256, 0, st>>>(w.U, n, r, ranges);
+    lr::k_colmax<<<r, 256, 0, st>>>(w.W, C, r, ranges + r);
+    lr::k_pack_int4<<<(unsigned)cdiv(cdiv((n + C) * r, 2), 256), 256, 0, st>>>(w.U, w.W, n, C, r, ranges,
+                                                                              ranges + r, body + 8 * r);
+    count_launch(3);
+  }
+  if (decoded) decode_into(body, int4, n, C, r, decoded, 0, w, st);
+  return cuda_status("lowrank_encode");
+}
+
+int lowrank_decode(int int4, int count, const int64_t *rows, int64_t C, int64_t r, const uint8_t *const *bodies,
+                   int accumulate, float *const *bases, cudaStream_t st) {
+  // factor scratch: allocated per call (decode of a received payload)
+  int64_t maxn = 0;
+  for (int i = 0; i < count; ++i) maxn = std::max(maxn, rows[i]);
+  double *scratch = nullptr;
+  const size_t bytes = 8 * (size_t)(maxn + C) * r;
+  if (cudaMallocAsync(&scratch, bytes, st) != cudaSuccess) return cuda_status("lowrank_decode alloc");
+  lr::Work w{};
+  w.Uf = scratch;
+  w.Wf = scratch + maxn * r;
+  for (int i = 0; i < count; ++i)
+    decode_into(bodies[i], int4, rows[i], C, (int)r, bases[i], accumulate ? 1 : 0, w, st);
+  cudaFreeAsync(scratch, st);
+  return cuda_status("lowrank_decode");
+}
+
+}  // namespace cc

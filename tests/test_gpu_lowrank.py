@@ -1,0 +1,166 @@
+"""GPU parity of the low-rank compressor (K3).
+
+The reference accumulates its projections in f64 BLAS (la:49-58) and orthogonalizes
+with CGS2 (la:77-112); the device path accumulates in f64 in a different order and
+orthogonalizes with CholQR2, so parity is stated as a tolerance on the
+reconstruction error: |relerr_device - relerr_reference| <= 1e-4,
+plus the reference's own property tests (T/test_compressors.py:114-177)."""
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from golden_fixtures import codec_arrays, manifest
+from oracle import cc_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    torch.cuda.set_device(0)
+
+
+def _mods():
+    from paper_2507_17511_b200 import compressors as cx
+    from paper_2507_17511_b200 import linalg
+    from paper_2507_17511_b200 import pipeline as pl
+
+    return cx, pl, linalg
+
+
+def _spec(rank, iters=2, int4=False):
+    cx, _, _ = _mods()
+    return cx.CompressorSpec(cx.CompressorKind.LOWRANK, rank=rank, iterations=iters, int4_factors=int4)
+
+
+def _relerr(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.sqrt(((a - b) ** 2).sum() / (b ** 2).sum()))
+
+
+@pytest.mark.parametrize("meta", manifest()["lowrank"],
+                         ids=lambda m: f"{m['rows']}x{m['cols']}-r{m['rank']}T{m['iterations']}{'i4' if m['int4'] else ''}")
+def test_lowrank_error_vs_reference(meta):
+    cx, _, linalg = _mods()
+    x = synth.flux_like(meta["rows"], meta["cols"], 1, meta["seed"])[0]
+    rng = linalg.spawn_rng(meta["seed"], 5, 2)  # same stream as the golden run -> same Q0 draw
+    p = cx.encode_lowrank(torch.from_numpy(x).cuda(), _spec(meta["rank"], meta["iterations"], meta["int4"]), rng)
+    assert p.body.numel() == meta["body_len"] and p.bit_size == meta["bit_size"]
+    err = _relerr(p.decode().cpu().numpy(), x)
+    assert abs(err - meta["rel_err"]) <= TOL, (err, meta["rel_err"])
+
+
+@pytest.mark.parametrize("case", [c for c in manifest()["codec_cases"] if c["codec"].startswith("lowrank")],
+                         ids=lambda c: f"{c['case']}|{c['codec']}")
+def test_lowrank_codec_cases_vs_reference(case):
+    cx, _, linalg = _mods()
+    arr = codec_arrays()
+    x = arr[f"x/{case['case']}"]
+    s = case["spec"]
+    p = cx.encode(torch.from_numpy(x).cuda(), _spec(s["rank"], s["iterations"], s["int4_factors"]),
+                  rng=linalg.make_rng(17))
+    assert p.bit_size == case["bit_size"] and p.body.numel() == case["body_len"]
+    key = f"{case['case']}|{case['codec']}"
+    ref_dec = O.decode_body(arr[f"body/{key}"].tobytes(),
+                            O.Codec(O.LOWRANK4 if s["int4_factors"] else O.LOWRANK, rank=s["rank"]),
+                            case["rows"], case["cols"])
+    if np.sum(x.astype(np.float64) ** 2) == 0:
+        assert np.allclose(p.decode().cpu().numpy(), 0.0)
+        return
+    e_dev = _relerr(p.decode().cpu().numpy(), x)
+    e_ref = _relerr(ref_dec, x)
+    assert abs(e_dev - e_ref) <= 5e-3 * max(1.0, e_ref), (e_dev, e_ref)
+    blob = cx.to_bytes(p)
+    assert cx.to_bytes(cx.from_bytes(blob)) == blob
+
+
+def test_exact_rank_recovery():  # T/test_compressors.py:114-120
+    cx, _, linalg = _mods()
+    rng = np.random.default_rng(3)
+    a = (rng.standard_normal((40, 6)) @ rng.standard_normal((6, 32))).astype(np.float32)
+    p = cx.encode_lowrank(torch.from_numpy(a).cuda(), _spec(6), linalg.make_rng(3))
+    # f16 factors bound the reconstruction at ~1e-3 relative
+    assert _relerr(p.decode().cpu().numpy(), a) < 2e-3
+
+
+def test_near_optimal_vs_svd():  # :123-131 (<= 1.10x the optimal rank-r error)
+    cx, _, linalg = _mods()
+    rng = np.random.default_rng(5)
+    for r in (4, 8, 16):
+        a = rng.standard_normal((64, 64)).astype(np.float32)
+        p = cx.encode_lowrank(torch.from_numpy(a).cuda(), _spec(r), linalg.make_rng(r))
+        err = np.sqrt(((p.decode().cpu().numpy().astype(np.float64) - a) ** 2).sum())
+        s = np.linalg.svd(a.astype(np.float64), compute_uv=False)
+        optimal = np.sqrt((s[r:] ** 2).sum())
+        assert err <= 1.10 * optimal
+
+
+def test_error_non_increasing_in_iterations():  # :134-141
+    cx, _, linalg = _mods()
+    a = torch.from_numpy(np.random.default_rng(8).standard_normal((64, 64)).astype(np.float32)).cuda()
+
+    def err(t):
+        p = cx.encode_lowrank(a, _spec(8, t), linalg.make_rng(99))
+        return float(((p.decode().double() - a.double()) ** 2).sum().sqrt())
+
+    assert err(10) <= err(2) * 1.01
+
+
+def test_rank_deficient_input_uses_replacement():  # :144-149
+    cx, _, linalg = _mods()
+    rng = np.random.default_rng(13)
+    a = (rng.standard_normal((24, 2)) @ rng.standard_normal((2, 24))).astype(np.float32)
+    p = cx.encode_lowrank(torch.from_numpy(a).cuda(), _spec(5), linalg.make_rng(13))
+    assert _relerr(p.decode().cpu().numpy(), a) < 2e-3
+
+
+def test_rank1_near_exact():  # :152-158
+    cx, _, linalg = _mods()
+    a = np.outer([1.0, 2.0, 3.0], [4.0, 5.0, 6.0, 7.0]).astype(np.float32)
+    p = cx.encode_lowrank(torch.from_numpy(a).cuda(), _spec(1), linalg.make_rng(2))
+    assert _relerr(p.decode().cpu().numpy(), a) < 5e-3
+
+
+def test_bit_budget_and_int4_beats_rank8():  # :161-177
+    cx, _, linalg = _mods()
+    rng = np.random.default_rng(4)
+    a = torch.from_numpy(rng.standard_normal((64, 96)).astype(np.float32)).cuda()
+    p32 = cx.encode_lowrank(a, _spec(32, 2, True), linalg.make_rng(4))
+    p8 = cx.encode_lowrank(a, _spec(8), linalg.make_rng(4))
+    assert p32.payload_only_bits == p8.payload_only_bits == 128 * (64 + 96)
+    assert p32.bit_size == 4 * 32 * (64 + 96) + 32 * 2 * 32 and p8.bit_size == 16 * 8 * (64 + 96)
+    b = torch.from_numpy(np.random.default_rng(6).standard_normal((128, 512)).astype(np.float32)).cuda()
+    e32 = _relerr(cx.encode_lowrank(b, _spec(32, 2, True), linalg.make_rng(7)).decode().cpu().numpy(), b.cpu().numpy())
+    e8 = _relerr(cx.encode_lowrank(b, _spec(8), linalg.make_rng(7)).decode().cpu().numpy(), b.cpu().numpy())
+    assert e32 < e8
+
+
+@pytest.mark.parametrize("int4", [False, True])
+def test_lowrank_protocol_sender_receiver_identical(int4):
+    cx, pl, linalg = _mods()
+    xs = synth.flux_like(128, 384, 5, seed=11)
+    spec = _spec(8, 2, int4)
+    snd = pl.LayerState("residual_with_feedback", 1, torch.zeros(128, 384, device="cuda"))
+    rcv = pl.LayerState("residual_with_feedback", 1, torch.zeros(128, 384, device="cuda"))
+    och = O.Channel(O.WITH_FEEDBACK, 1, np.zeros((128, 384), np.float32))
+    for t, x in enumerate(xs, start=1):
+        base0, fb0 = snd.base.clone(), snd.feedback.clone()
+        p, rec = pl.encode_step(snd, x, spec, rng=linalg.spawn_rng(11, 5, t))
+        if t > 1:
+            dec = p.decode()
+            target = (torch.from_numpy(x).cuda() - base0) + fb0
+            assert torch.equal(snd.feedback, target - dec)  # feedback conservation, bit-exact
+            assert torch.equal(snd.base, base0 + dec)
+        msg = pl.message_for(t, 1, p) if t % 2 else pl.device_message(t, 1, p)
+        pl.decode_step(rcv, msg)
+        assert torch.equal(rcv.base, snd.base)
+        O.send(och, x, O.Codec(O.LOWRANK4 if int4 else O.LOWRANK, rank=8, iters=2),
+               rng=linalg.spawn_rng(11, 5, t))
+    # trajectory-level agreement with the reference algorithm (tolerance)
+    assert _relerr(snd.base.cpu().numpy(), och.base) < 2e-2
