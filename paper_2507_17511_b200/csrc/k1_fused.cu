@@ -123,7 +123,7 @@ __device__ __noinline__ CodeVal quantize1_exact(float t, double ud, double vd) {
 // i.e. |t| > RN(u vhi) proves code 0/3 and |t| < RN(u vlo) proves code 1/2.
 struct ColConst {
   float v[4], vhi[4], vlo[4];
-  bool ok;  // all 4 columns have v == 0 or |v| in [2^-50, 2^50]
+  bool ok;  // all 4 columns have |v| in [2^-50, 2^50]
 };
 
 __device__ __forceinline__ bool scale_in_range(float a) { return a >= 0x1p-50f && a <= 0x1p+50f; }
@@ -152,14 +152,13 @@ __device__ __forceinline__ uint32_t quantize4(const float (&t)[4], float uf, boo
     for (int q = 0; q < 4; ++q) {
       const float p = __fmul_rn(uf, cc.v[q]);
       const float ax = fabsf(t[q]);
-      const bool zero = cc.v[q] == 0.0f;  // zero scale: code 2, decode +0 (cx:385-387)
       const bool big = ax > __fmul_rn(uf, cc.vhi[q]);
-      ambiguous |= !zero && !big && !(ax < __fmul_rn(uf, cc.vlo[q]));
-      const bool neg = t[q] < 0.0f && !zero;
+      ambiguous |= !big && !(ax < __fmul_rn(uf, cc.vlo[q]));
+      const bool neg = t[q] < 0.0f;
       // code: big -> (neg ? 0 : 3), else (neg ? 1 : 2)
-      const uint32_t code = zero ? 2u : (big ? (neg ? 0u : 3u) : (neg ? 1u : 2u));
+      const uint32_t code = (big ? 3u : 2u) - (neg ? (big ? 3u : 1u) : 0u);
       const float lv = big ? 2.0f : 0.5f;
-      d[q] = zero ? 0.0f : __fmul_rn(neg ? -lv : lv, p);
+      d[q] = __fmul_rn(neg ? -lv : lv, p);
       packed |= code << (2 * q);
     }
     if (__builtin_expect(ambiguous, 0)) {
@@ -341,11 +340,11 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   // publishes the tile id with the stage (-1 = no more work)
   if (loader) {
     const uint64_t pol = l2_policy_evict_last();
-    int64_t k = 0;
-    for (;; ++k) {
-      const int s = (int)(k % SA);
+    int k = 0, s = 0;
+    uint32_t ph = 0;  // phase parity of stage s's current use
+    for (;;) {
       if (k >= SA) {
-        mbar_wait(&emptyA[s], (uint32_t)(((k / SA) - 1) & 1));
+        mbar_wait(&emptyA[s], ph ^ 1u);
         finish_rows(s, tileA[s]);
       }
       long long tile = 0;
@@ -370,19 +369,28 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       }
       __syncwarp();
       if (tile < 0) break;
+      ++k;
+      if (++s == SA) {
+        s = 0;
+        ph ^= 1u;
+      }
     }
-    for (int64_t q = k - min64(SA - 1, k); q <= k; ++q) {  // drain the stages still in use
-      const int s = (int)(q % SA);
-      mbar_wait(&emptyA[s], (uint32_t)((q / SA) & 1));
-      if (tileA[s] >= 0 && q < k) finish_rows(s, tileA[s]);
+    // drain: the stages still in use are the last min(SA, k+1) (sentinel included)
+    const int used = min(SA, k + 1);
+    for (int q = 0; q < used; ++q) {  // walk backwards from the sentinel stage
+      const int sq = (s - q + SA) % SA;
+      const uint32_t pq = (q <= s) ? ph : (ph ^ 1u);
+      mbar_wait(&emptyA[sq], pq);
+      if (q > 0 && tileA[sq] >= 0) finish_rows(sq, tileA[sq]);
     }
   } else if (consumer) {
     double cs[Q][4];
 #pragma unroll
     for (int j = 0; j < Q; ++j) cs[j][0] = cs[j][1] = cs[j][2] = cs[j][3] = 0.0;
-    for (int64_t k = 0;; ++k) {
-      const int s = (int)(k % SA);
-      mbar_wait(&fullA[s], (uint32_t)((k / SA) & 1));
+    int s = 0;
+    uint32_t ph = 0;
+    for (;; s = (s + 1 == SA) ? 0 : s + 1, ph ^= (s == 0)) {
+      mbar_wait(&fullA[s], ph);
       const long long tile = tileA[s];
       if (tile < 0) {
         __syncwarp();
@@ -520,9 +528,10 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   double err = 0.0, tsq = 0.0;
   if (loader) {
     const uint64_t pol = l2_policy_evict_first();
-    for (int64_t k = 0;; ++k) {
-      const int s = (int)(k % SI);
-      if (k >= SI) mbar_wait(&emptyB[s], (uint32_t)(((k / SI) - 1) & 1));
+    int k = 0, s = 0;
+    uint32_t ph = 0;
+    for (;;) {
+      if (k >= SI) mbar_wait(&emptyB[s], ph ^ 1u);
       long long t = 0;
       if (lane == 0) t = (long long)atomicAdd(p.ctr + 1, 1ull);
       t = __shfl_sync(0xffffffffu, t, 0);
@@ -548,11 +557,17 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       }
       __syncwarp();
       if (tile < 0) break;
+      ++k;
+      if (++s == SI) {
+        s = 0;
+        ph ^= 1u;
+      }
     }
   } else if (storer) {
-    for (int64_t k = 0;; ++k) {
-      const int o = (int)(k % SO);
-      mbar_wait(&outFull[o], (uint32_t)((k / SO) & 1));
+    int o = 0;
+    uint32_t ph = 0;
+    for (;; o = (o + 1 == SO) ? 0 : o + 1, ph ^= (o == 0)) {
+      mbar_wait(&outFull[o], ph);
       const long long tile = tileO[o];
       if (tile < 0) break;
       if (lane == 0) {
@@ -581,19 +596,19 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
         cc[j].v[q] = v;
         cc[j].vhi[q] = __fmul_ru(__fmul_ru(v, 1.25f), 1.00000095367431640625f);  // (1 + 2^-20)
         cc[j].vlo[q] = __fmul_rd(__fmul_rd(v, 1.25f), 0.99999904632568359375f);  // (1 - 2^-20)
-        cc[j].ok = cc[j].ok && (v == 0.0f || scale_in_range(fabsf(v)));
+        cc[j].ok = cc[j].ok && scale_in_range(fabsf(v));  // zero / extreme scales: exact path
       }
     }
     const int r = grp;  // this thread's row inside a phase-B tile
-    for (int64_t k = 0;; ++k) {
-      const int s = (int)(k % SI);
-      const int o = (int)(k % SO);
-      mbar_wait(&fullB[s], (uint32_t)((k / SI) & 1));
+    int s = 0, o = 0, k = 0;
+    uint32_t phs = 0, pho = 0;
+    for (;; ++k, s = (s + 1 == SI) ? 0 : s + 1, phs ^= (s == 0), o = (o + 1 == SO) ? 0 : o + 1, pho ^= (o == 0)) {
+      mbar_wait(&fullB[s], phs);
       const long long tile = tileB[s];
       if (tile < 0) {  // forward the end-of-work marker to the store warp
         __syncwarp();
         if (lane == 0) mbar_arrive(&emptyB[s]);
-        if (k >= SO) mbar_wait(&outFree[o], (uint32_t)(((k / SO) - 1) & 1));
+        if (k >= SO) mbar_wait(&outFree[o], pho ^ 1u);
         if (tid == 0) tileO[o] = -1;
         __syncwarp();
         if (lane == 0) mbar_arrive(&outFull[o]);
@@ -619,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       const float uf = row_live ? ustage[(size_t)s * 16 + (r0 & 3) + r] : 1.0f;
       __syncwarp();
       if (lane == 0) mbar_arrive(&emptyB[s]);  // inputs are in registers: the loader may refill
-      if (k >= SO) mbar_wait(&outFree[o], (uint32_t)(((k / SO) - 1) & 1));
+      if (k >= SO) mbar_wait(&outFree[o], pho ^ 1u);
       uint8_t *so = out_ring + (size_t)o * LO.bytes;
       const bool row_ok = scale_in_range(fabsf(uf));
 #pragma unroll
