@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlap", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch every kernel from Python instead of "
+                                                             "replaying a captured CUDA graph per step")
     return ap.parse_args()
 
 
@@ -297,24 +299,51 @@ def run_b200(a, world, rank):
     barrier(world)
 
     K = a.steps
+    # per-kernel timing pass (events around every K1 on its stream; not the headline)
     evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(L)]
            for _ in range(K)]
+    for s in range(K):
+        one_step(a.warmup + 1 + s, ev=evs[s])
+    streams.compute.wait_stream(streams.decode)
+    barrier(world)
+    k1_ms = statistics.mean(evs[s][l][0].elapsed_time(evs[s][l][1]) for s in range(K) for l in range(L))
+
+    graphs = None
+    if not a.no_graph:
+        # steady state reached: capture one step per input parity and replay it
+        graphs = []
+        for par in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                one_step(par)
+                torch.cuda.current_stream().wait_stream(streams.decode)
+            graphs.append(g)
+        for par in (0, 1):
+            graphs[par].replay()
+        barrier(world)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n0 = lib.cc_launch_count()
     with ClockSampler(torch.cuda.current_device()) as clk:
         barrier(world)
         start.record(streams.compute)
         for s in range(K):
-            one_step(s + 1, ev=evs[s])
+            if graphs is not None:
+                graphs[s % 2].replay()
+            else:
+                one_step(s + 1)
         streams.compute.wait_stream(streams.decode)
         end.record(streams.compute)
         barrier(world)
     launches = lib.cc_launch_count() - n0
+    if graphs is not None:  # kernels inside the graphs: count one captured step per replay
+        n1 = lib.cc_launch_count()
+        one_step(0)
+        torch.cuda.synchronize()
+        launches = (lib.cc_launch_count() - n1) * K
     ms = start.elapsed_time(end) / K
     ms = max_over_ranks(ms, world)
     act_bytes = L * 2 * rows * cols
     value = world * act_bytes / (ms / 1e3) / 1e9
-    k1_ms = statistics.mean(evs[s][l][0].elapsed_time(evs[s][l][1]) for s in range(K) for l in range(L))
 
     # K2 alone (decode stream serialised after K1) for the roofline breakdown
     k2_ms = measure_k2(exs, streams, world)
@@ -369,7 +398,7 @@ def run_b200(a, world, rank):
                                                                   "BASELINE config 1)" if world == 1 else "")),
                    "codec": a.codec, "layers": L, "rows": rows, "cols": cols, "shard_rows": n_own,
                    "parallelism": f"patch{world}", "l2": "per-step working set >> 126 MB L2 (no flush needed)",
-                   "overlap": not a.no_overlap},
+                   "overlap": not a.no_overlap, "cuda_graph": not a.no_graph},
         "per_gpu_gbs": value / world,
         "exposed_comm_us_per_layer": exposed_us,
         "bf16_allgather_us_per_layer": bf16_ag_us,

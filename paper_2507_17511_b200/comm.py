@@ -132,16 +132,31 @@ class CudaEngine:
 
 
 class _Streams:
+    """compute = the caller's current stream at step time (so a CUDA-graph
+    capture stream is honoured); comm / decode are side streams joined back
+    through events."""
+
     def __init__(self, device, overlap):
+        self.device = device
+        self.overlap = overlap
         if device.type != "cuda":
-            self.compute = self.comm = self.decode = None
+            self._comm = self._decode = None
             return
-        self.compute = torch.cuda.current_stream(device)
         if overlap:
-            self.comm = torch.cuda.Stream(device)
-            self.decode = torch.cuda.Stream(device)
-        else:
-            self.comm = self.decode = self.compute
+            self._comm = torch.cuda.Stream(device)
+            self._decode = torch.cuda.Stream(device)
+
+    @property
+    def compute(self):
+        return torch.cuda.current_stream(self.device) if self.device.type == "cuda" else None
+
+    @property
+    def comm(self):
+        return self._comm if self.overlap else self.compute
+
+    @property
+    def decode(self):
+        return self._decode if self.overlap else self.compute
 
 
 class _NullCtx:
@@ -254,7 +269,9 @@ class PatchParallelExchange:
         t = self.sender.step + 1
         warm = t <= self.warmup or cx.CompressorKind(self.codec.kind) == cx.CompressorKind.IDENTITY
         with _on(S.compute):
-            if S.compute is not None:  # the previous decode must not race this K1 on `full`
+            # the previous decode must not race this K1 on `full` (inside a CUDA-graph
+            # capture that order is implied by the ordering of graph launches)
+            if S.compute is not None and not torch.cuda.is_current_stream_capturing():
                 self.ev_decoded.wait(S.compute)
             nbytes, wire16, rec = self.engine.encode(self.sender, x_shard, self.codec, self.sendbuf, rng)
             self.last_record, self.last_nbytes = rec, nbytes

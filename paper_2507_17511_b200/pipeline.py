@@ -116,7 +116,8 @@ class LayerState:
 
 
 def _record_buffer():
-    return torch.zeros(2, dtype=torch.float64, device=cx._device())
+    # every encode path writes both doubles, so no fill kernel is needed
+    return torch.empty(2, dtype=torch.float64, device=cx._device())
 
 
 def encode_step(state, a_star, codec, rng=None, body_out=None):
