@@ -318,6 +318,8 @@ def run_b200(a, world, rank):
                 one_step(par)
                 torch.cuda.current_stream().wait_stream(streams.decode)
             graphs.append(g)
+        for e in exs:
+            e.after_capture()
         for par in (0, 1):
             graphs[par].replay()
         barrier(world)

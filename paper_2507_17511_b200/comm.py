@@ -256,6 +256,11 @@ class PatchParallelExchange:
         self.last_nbytes = 0
         self.comm_bytes = 0
 
+    def after_capture(self):
+        """Events recorded inside a CUDA-graph capture cannot be waited on eagerly:
+        start fresh ones (the captured graph keeps its own copies)."""
+        self.ev_encoded, self.ev_gathered, self.ev_decoded = (_Event(self.cuda) for _ in range(3))
+
     def wire_bytes(self, warm, wire16):
         """Equal-size collective: every rank sends the largest shard's body."""
         if warm:
