@@ -481,9 +481,38 @@ __device__ __forceinline__ float value_of(uint32_t code, double s) {
   else return (float)(quant4_level(code) * s);
 }
 
+__device__ __forceinline__ bool dec_scale_ok(float a) { return a >= 0x1p-50f && a <= 0x1p+50f; }
+
+// d for 4 columns of one row.  Power-of-two levels (1-bit: +-1, 2-bit: +-0.5 / +-2)
+// decode exactly in f32 as level * RN32(u v) while u, v are in range (the product
+// then stays normal); otherwise, and for the 4-bit extension, in f64 (cx:206-242).
+template <int CODEC>
+__device__ __forceinline__ void decode4(uint32_t cw, float uf, bool row_ok, const float (&vf)[4], bool col_ok,
+                                        float (&d)[4]) {
+  constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
+  if (CODEC != CC_QUANT4 && row_ok && col_ok) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t code = (cw >> (q * bits)) & ((1u << bits) - 1u);
+      const float p = __fmul_rn(uf, vf[q]);
+      float lv;
+      if constexpr (CODEC == CC_SIGN1) lv = code ? -1.0f : 1.0f;
+      else lv = (code & 2u) ? ((code & 1u) ? 2.0f : 0.5f) : ((code & 1u) ? -0.5f : -2.0f);
+      d[q] = __fmul_rn(lv, p);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t code = (cw >> (q * bits)) & ((1u << bits) - 1u);
+      d[q] = value_of<CODEC>(code, (double)uf * (double)vf[q]);
+    }
+  }
+}
+
 template <int CODEC, bool ACC>
 __global__ void __launch_bounds__(256) k_decode_vec(const __grid_constant__ PeerBatch pb, int64_t C, int RB) {
   constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
+  constexpr int U = 8;  // rows in flight per thread
   const int peer = blockIdx.z;
   const int64_t n = pb.rows[peer];
   const int64_t r0 = (int64_t)blockIdx.y * RB;
@@ -496,37 +525,44 @@ __global__ void __launch_bounds__(256) k_decode_vec(const __grid_constant__ Peer
   const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (j0 >= C) return;
   const int rows = (int)(RB < n - r0 ? (int64_t)RB : n - r0);
-  double vd[4];
+  float vf[4];
+  bool col_ok = true;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) vd[q] = (double)load_f32_bytes(vb + 4 * (j0 + q));
-  for (int rr = 0; rr < rows; rr += kRowsUnroll) {
-    float4 bv[kRowsUnroll];
-    uint32_t cw[kRowsUnroll];
-    double ud[kRowsUnroll];
+  for (int q = 0; q < 4; ++q) {
+    vf[q] = load_f32_bytes(vb + 4 * (j0 + q));
+    col_ok = col_ok && dec_scale_ok(fabsf(vf[q]));
+  }
+  for (int rr = 0; rr < rows; rr += U) {
+    float4 bv[U];
+    uint32_t cw[U];
+    float uf[U];
 #pragma unroll
-    for (int k = 0; k < kRowsUnroll; ++k) {
+    for (int k = 0; k < U; ++k) {
       const bool ok = (rr + k) < rows;
       const int64_t i = r0 + rr + k;
       const int64_t e = i * C + j0;
       if (ACC) bv[k] = ok ? *reinterpret_cast<const float4 *>(base + e) : make_float4(0.f, 0.f, 0.f, 0.f);
-      ud[k] = ok ? (double)load_f32_bytes(ub + 4 * i) : 0.0;
-      if (!ok) { cw[k] = 0; continue; }
+      uf[k] = ok ? load_f32_bytes(ub + 4 * i) : 1.0f;
+      if (!ok) {
+        cw[k] = 0;
+        continue;
+      }
       if constexpr (CODEC == CC_SIGN1) cw[k] = (codes[e >> 3] >> (e & 7)) & 0xfu;
       else if constexpr (CODEC == CC_QUANT2) cw[k] = codes[e >> 2];
       else cw[k] = *reinterpret_cast<const uint16_t *>(codes + (e >> 1));
     }
 #pragma unroll
-    for (int k = 0; k < kRowsUnroll; ++k) {
-      if ((rr + k) >= rows) break;
-      const int64_t e = (r0 + rr + k) * C + j0;
-      float4 o;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t code = (cw[k] >> (q * bits)) & ((1u << bits) - 1u);
-        const float d = value_of<CODEC>(code, ud[k] * vd[q]);
-        f4set(o, q, ACC ? __fadd_rn(f4get(bv[k], q), d) : d);
+    for (int k = 0; k < U; ++k) {
+      if ((rr + k) < rows) {
+        const int64_t e = (r0 + rr + k) * C + j0;
+        float d[4];
+        decode4<CODEC>(cw[k], uf[k], dec_scale_ok(fabsf(uf[k])), vf, col_ok, d);
+        float4 o;
+        if (ACC) o = make_float4(__fadd_rn(bv[k].x, d[0]), __fadd_rn(bv[k].y, d[1]), __fadd_rn(bv[k].z, d[2]),
+                                 __fadd_rn(bv[k].w, d[3]));
+        else o = make_float4(d[0], d[1], d[2], d[3]);
+        __stcs(reinterpret_cast<float4 *>(base + e), o);
       }
-      *reinterpret_cast<float4 *>(base + e) = o;
     }
   }
 }

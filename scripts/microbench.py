@@ -106,6 +106,25 @@ def main():
 
     us = timed(dec, a.reps)
     out["k2_decode"] = {"us": round(us, 2), "alg_GBps": round(n * c * (8 + bits / 8) / us / 1e3, 1)}
+    # K2 batched over 7 peers of n/8 rows each (P=8 patch-parallel receive)
+    if n % 8 == 0:
+        import ctypes
+        rows8 = n // 8
+        peers = [torch.zeros(rows8, c, device="cuda") for _ in range(7)]
+        bod = torch.empty(lib.cc_body_bytes(tag, rows8, c, 0) + 64, dtype=torch.uint8, device="cuda")
+        st8 = pl.LayerState("naive", 1, torch.zeros(rows8, c, device="cuda"))
+        pl.encode_step(st8, xs[0][:rows8], spec)
+        pl.encode_step(st8, xs[1][:rows8], spec, body_out=bod)
+        ra = (ctypes.c_int64 * 7)(*([rows8] * 7))
+        ba = (ctypes.c_void_p * 7)(*([bod.data_ptr()] * 7))
+        pa = (ctypes.c_void_p * 7)(*[q.data_ptr() for q in peers])
+
+        def dec7(i):
+            lib.cc_decode_batched(tag, 1, 7, ra, c, 0, ba, _lib.CC_F32, pa, stream)
+
+        us = timed(dec7, a.reps)
+        out["k2_decode_7peers_P8"] = {"us": round(us, 2),
+                                      "alg_GBps": round(7 * rows8 * c * (8 + bits / 8) / us / 1e3, 1)}
     # plain copy roofline reference: base -> feedback of another layer
     def cp(i):
         sts[(i + 1) % L].feedback.copy_(sts[i % L].base)
