@@ -180,6 +180,9 @@ CC_API void cc_debug_fused_timer(void *dev_buf);
 CC_API void cc_debug_fused_policy(int policy);
 /* profiling only: phase-B ring depths of the persistent K1 (0 = automatic) */
 CC_API void cc_debug_fused_rings(int s_in, int s_out);
+/* low-rank projections: 1 = tcgen05 tensor cores, 3xTF32 split (default),
+ * 0 = f64-accumulating CUDA-core GEMMs (cross-check) */
+CC_API void cc_set_lowrank_backend(int backend);
 
 #ifdef __cplusplus
 }

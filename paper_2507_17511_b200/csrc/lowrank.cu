@@ -21,6 +21,11 @@
 #include <curand_kernel.h>
 
 namespace cc {
+int64_t tc_partial_floats(int64_t n, int64_t C, int r);
+int tc_project(int mode, const float *A, const float *S, float *D, float *Dpart, int64_t n, int64_t C, int r,
+               cudaStream_t st);
+int lowrank_backend();
+
 namespace lr {
 
 constexpr int kMaxR = 32;
@@ -390,7 +395,7 @@ __global__ void __launch_bounds__(kThreads) k_outer(const double *__restrict__ U
 }
 
 struct Work {
-  float *Q, *Y, *Z, *U, *W;
+  float *Q, *Y, *Z, *U, *W, *TCpart;
   double *Zpart, *M64, *Gpart, *Rinv, *Uf, *Wf;
   float *ur, *wr;
   int *flag;
@@ -420,6 +425,7 @@ static Work carve(void *ws, int64_t n, int64_t C, int64_t r, size_t *bytes) {
   w.ur = reinterpret_cast<float *>(take(4 * r));
   w.wr = reinterpret_cast<float *>(take(4 * r));
   w.flag = reinterpret_cast<int *>(take(256));
+  w.TCpart = reinterpret_cast<float *>(take(4 * (size_t)tc_partial_floats(n, C, (int)r)));
   if (bytes) *bytes = off;
   return w;
 }
@@ -451,13 +457,22 @@ static void orth(const float *M, float *out, int64_t m, int r, const lr::Work &w
   count_launch(4 + 6);
 }
 
-static void aq(const float *A, const float *Q, float *Y, int64_t n, int64_t C, int r, cudaStream_t st) {
+static void aq(const float *A, const float *Q, float *Y, const lr::Work &w, int64_t n, int64_t C, int r,
+               cudaStream_t st) {
+  if (lowrank_backend() == 1) {
+    tc_project(0, A, Q, Y, w.TCpart, n, C, r, st);
+    return;
+  }
   lr::k_aq<<<(unsigned)cdiv(n, lr::kRowsAQ), lr::kThreads, 0, st>>>(A, Q, Y, n, C, r);
   count_launch();
 }
 
 static void aty(const float *A, const float *Y, float *Z, const lr::Work &w, int64_t n, int64_t C, int r,
                 cudaStream_t st) {
+  if (lowrank_backend() == 1) {
+    tc_project(1, A, Y, Z, w.TCpart, n, C, r, st);
+    return;
+  }
   dim3 g((unsigned)cdiv(C, lr::kColsATY), lr::kSplitATY);
   lr::k_aty<<<g, lr::kThreads, 0, st>>>(A, Y, w.Zpart, n, C, r);
   lr::k_zsum<<<(unsigned)cdiv(C * r, 256), 256, 0, st>>>(w.Zpart, Z, C, r);
@@ -488,11 +503,11 @@ int lowrank_encode(int int4, int64_t n, int64_t C, int64_t r64, int iters, const
   const lr::Work w = lr::carve(ws, n, C, r, nullptr);
   orth(q0, w.Q, C, r, w, st);                  // Q0 = orth(G)        (cx:407)
   for (int it = 0; it < iters; ++it) {         // (cx:408-410)
-    aq(t, w.Q, w.Y, n, C, r, st);
+    aq(t, w.Q, w.Y, w, n, C, r, st);
     aty(t, w.Y, w.Z, w, n, C, r, st);
     orth(w.Z, w.Q, C, r, w, st);
   }
-  aq(t, w.Q, w.Y, n, C, r, st);
+  aq(t, w.Q, w.Y, w, n, C, r, st);
   orth(w.Y, w.U, n, r, w, st);                 // U = orth(A Q)       (cx:411)
   aty(t, w.U, w.W, w, n, C, r, st);            // W = A^T U           (cx:419)
   if (!int4) {

@@ -1,0 +1,316 @@
+// K3 projections on the 5th-generation tensor cores (tcgen05, kind::tf32).
+//
+//   mode AQ : Y[n, r]  = A[n, C] Q[C, r]        (cx:409, la:49-58)
+//   mode ATY: Z[C, r]  = A[n, C]^T Y[n, r]      (cx:409, cx:419)
+//
+// Both are skinny (r <= 32) and stream A once, so they are HBM/L2-bound; the tensor
+// cores keep the f32-accurate product off the CUDA cores.  Precision: the reference
+// accumulates in f64 BLAS, so each operand is split x = hi + lo (hi = RNA-tf32(x),
+// lo = tf32(x - hi)) and D += Ahi*Bhi + Ahi*Blo + Alo*Bhi ("3xTF32"), f32 accumulate
+// in TMEM: ~1e-6 relative, far below the tolerance of the low-rank parity tests.
+//
+// CTA = 128 threads (4 warps) owning a 128-row M tile and a K range (split-K for
+// parallelism; partial D tiles reduced in a fixed order).  Per 32-wide K chunk the
+// warps stage hi/lo operand tiles into shared memory in the canonical K-major
+// SWIZZLE_128B layout (8 rows x 128 B atoms, 16-byte chunk index XOR row), thread 0
+// issues 12 tcgen05.mma (4 K-steps x 3 products) and commits to an mbarrier; two
+// stage buffers let the next chunk's staging overlap the tensor-core work.  The
+// epilogue moves D from TMEM with tcgen05.ld (warp w owns TMEM lanes 32w..32w+31).
+#include "cc_async.cuh"
+#include "cc_common.cuh"
+#include "cc_internal.h"
+
+#include <algorithm>
+
+namespace cc {
+namespace tc {
+
+constexpr int kM = 128;     // UMMA M (one CTA)
+constexpr int kKC = 32;     // K chunk: 32 f32 = one 128-byte swizzle row
+constexpr int kThreads = 128;
+constexpr int kTmemCols = 32;
+
+// ---- tcgen05 / UMMA helpers ------------------------------------------------
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  // K-major SWIZZLE_128B: start>>4 [0,14), LBO>>4 = 1 [16,30), SBO>>4 = 1024>>4 [32,46),
+  // version 1 [46,48), layout type 2 (SWIZZLE_128B) [61,64)
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  // c_format F32 [4,6)=1, a_format TF32 [7,10)=2, b_format TF32 [10,13)=2,
+  // a/b K-major, n_dim = N>>3 [17,23), m_dim = M>>4 [24,29)
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, int cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(cols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, int cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// byte offset of element (row, k) inside a K-major SWIZZLE_128B tile of 32-f32 rows
+__device__ __forceinline__ uint32_t sw128(int row, int k) {
+  return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((((k >> 2) ^ (row & 7)) & 7) << 4) + (k & 3) * 4);
+}
+
+struct Stage {
+  // hi / lo operand tiles, each 1024-byte aligned
+  uint8_t *a_hi, *a_lo, *b_hi, *b_lo;
+};
+
+// MODE 0 (AQ): P[m][k] = A[i0+m][k0+k], S[j][k] = Q[k0+k][j]   (K = C)
+// MODE 1 (ATY): P[m][k] = A[k0+k][c0+m], S[j][k] = Y[k0+k][j]  (K = n)
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_tc_gemm(const float *__restrict__ A, const float *__restrict__ S,
+                                                       float *__restrict__ Dpart, int64_t n, int64_t C, int r,
+                                                       int NP, int64_t kper) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-align the tile area
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t Mdim = MODE == 0 ? n : C;
+  const int64_t Kdim = MODE == 0 ? C : n;
+  const int64_t m0 = (int64_t)blockIdx.x * kM;
+  const int split = blockIdx.y;
+  const int64_t klo = split * kper, khi = min64(Kdim, klo + kper);
+  const uint32_t a_bytes = kM * kKC * 4;  // 16 KB
+  const uint32_t b_bytes = (uint32_t)NP * kKC * 4;
+  const uint32_t b_round = (b_bytes + 1023) & ~1023u;
+  Stage st[2];
+  for (int s = 0; s < 2; ++s) {
+    uint8_t *b = smem + s * (2 * a_bytes + 2 * b_round);
+    st[s].a_hi = b;
+    st[s].a_lo = b + a_bytes;
+    st[s].b_hi = b + 2 * a_bytes;
+    st[s].b_lo = b + 2 * a_bytes + b_round;
+  }
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * (2 * a_bytes + 2 * b_round));
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 2);
+  if (warp == 0) tmem_alloc(tmem_slot, kTmemCols);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t idesc = idesc_tf32(kM, NP);
+
+  auto stage_chunk = [&](const Stage &sg, int64_t k0) {
+    const int kc = (int)min64(kKC, khi - k0);
+    // P tile: 128 rows x 32 k
+    if constexpr (MODE == 0) {
+      for (int e = tid; e < kM * (kKC / 4); e += kThreads) {  // one float4 (4 consecutive k) per item
+        const int m = e / (kKC / 4), k4 = (e % (kKC / 4)) * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (m0 + m < Mdim && k4 < kc) {
+          const float *src = A + (m0 + m) * C + k0 + k4;
+          if (k4 + 4 <= kc && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            v = __ldg(reinterpret_cast<const float4 *>(src));
+          } else {
+            float t[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int q = 0; q < 4 && k4 + q < kc; ++q) t[q] = src[q];
+            v = make_float4(t[0], t[1], t[2], t[3]);
+          }
+        }
+        const float h0 = tf32_rna(v.x), h1 = tf32_rna(v.y), h2 = tf32_rna(v.z), h3 = tf32_rna(v.w);
+        const uint32_t off = sw128(m, k4);
+        *reinterpret_cast<float4 *>(sg.a_hi + off) = make_float4(h0, h1, h2, h3);
+        *reinterpret_cast<float4 *>(sg.a_lo + off) = make_float4(tf32_rna(v.x - h0), tf32_rna(v.y - h1),
+                                                                 tf32_rna(v.z - h2), tf32_rna(v.w - h3));
+      }
+    } else {
+      for (int e = tid; e < kKC * (kM / 4); e += kThreads) {  // one float4 of 4 consecutive m per item
+        const int kk = e / (kM / 4), mq = (e % (kM / 4)) * 4;
+        float t[4] = {0.f, 0.f, 0.f, 0.f};
+        if (kk < kc) {
+          const float *src = A + (k0 + kk) * C + m0 + mq;
+          if (m0 + mq + 4 <= Mdim && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(src));
+            t[0] = v.x; t[1] = v.y; t[2] = v.z; t[3] = v.w;
+          } else {
+            for (int q = 0; q < 4; ++q)
+              if (m0 + mq + q < Mdim) t[q] = src[q];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float h = tf32_rna(t[q]);
+          const uint32_t off = sw128(mq + q, kk);
+          *reinterpret_cast<float *>(sg.a_hi + off) = h;
+          *reinterpret_cast<float *>(sg.a_lo + off) = tf32_rna(t[q] - h);
+        }
+      }
+    }
+    // S tile: NP rows (j) x 32 k; rows >= r are zero
+    for (int e = tid; e < NP * kKC; e += kThreads) {
+      const int j = e / kKC, kk = e % kKC;
+      float v = 0.f;
+      if (j < r && kk < kc) v = S[(k0 + kk) * r + j];
+      const float h = tf32_rna(v);
+      const uint32_t off = sw128(j, kk);
+      *reinterpret_cast<float *>(sg.b_hi + off) = h;
+      *reinterpret_cast<float *>(sg.b_lo + off) = tf32_rna(v - h);
+    }
+    fence_proxy_async_smem();
+  };
+
+  const int64_t nchunks = (khi - klo + kKC - 1) / kKC;
+  uint32_t ph[2] = {0u, 0u};
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int s = (int)(c & 1);
+    if (c >= 2) {  // the MMAs that read this stage two chunks ago must be done
+      mbar_wait(&bar[s], ph[s]);
+      ph[s] ^= 1u;
+    }
+    stage_chunk(st[s], klo + c * kKC);
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint64_t ah = umma_desc_sw128(smem_u32(st[s].a_hi)), al = umma_desc_sw128(smem_u32(st[s].a_lo));
+      const uint64_t bh = umma_desc_sw128(smem_u32(st[s].b_hi)), bl = umma_desc_sw128(smem_u32(st[s].b_lo));
+#pragma unroll
+      for (int ks = 0; ks < kKC / 8; ++ks) {  // K = 8 tf32 (32 bytes) per instruction
+        const uint64_t dk = (uint64_t)((ks * 32) >> 4);
+        const uint32_t acc0 = (c > 0 || ks > 0) ? 1u : 0u;
+        mma_tf32(tmem, ah + dk, bh + dk, idesc, acc0);
+        mma_tf32(tmem, ah + dk, bl + dk, idesc, 1u);
+        mma_tf32(tmem, al + dk, bh + dk, idesc, 1u);
+      }
+      mma_commit(&bar[s]);
+    }
+    __syncwarp();
+  }
+  // drain: wait for the last (up to two) commits
+  for (int64_t c = std::max<int64_t>(0, nchunks - 2); c < nchunks; ++c) {
+    const int s = (int)(c & 1);
+    mbar_wait(&bar[s], ph[s]);
+    ph[s] ^= 1u;
+  }
+  tc_fence_after();
+  // epilogue: warp w reads TMEM lanes 32w..32w+31 (rows m0 + 32w + lane)
+  const int64_t m = m0 + warp * 32 + lane;
+  float *out = Dpart + (int64_t)split * Mdim * r;
+  for (int cb = 0; cb < NP; cb += 16) {
+    float v[16];
+    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)cb, v);
+    if (nchunks > 0 && m < Mdim) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (cb + q < r) out[m * r + cb + q] = v[q];
+    } else if (m < Mdim) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (cb + q < r) out[m * r + cb + q] = 0.0f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+}
+
+// fixed-order split reduction -> f32 result
+__global__ void k_tc_reduce(const float *__restrict__ Dpart, float *__restrict__ D, int64_t cnt, int splits) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cnt) return;
+  float s = 0.0f;
+  for (int sp = 0; sp < splits; ++sp) s += Dpart[(int64_t)sp * cnt + e];
+  D[e] = s;
+}
+
+}  // namespace tc
+
+static int g_lr_backend = 1;  // 1 = tcgen05 3xTF32 projections, 0 = f64 CUDA-core projections
+void set_lowrank_backend(int v) { g_lr_backend = v; }
+int lowrank_backend() { return g_lr_backend; }
+
+static size_t tc_smem_bytes(int NP) {
+  const size_t a = tc::kM * tc::kKC * 4;
+  const size_t b = ((size_t)NP * tc::kKC * 4 + 1023) & ~size_t(1023);
+  return 1024 + 2 * (2 * a + 2 * b) + 64;
+}
+
+int64_t tc_partial_floats(int64_t n, int64_t C, int r) {
+  // max over both modes of splits * M * r
+  const int64_t sm = sm_count();
+  auto splits_for = [&](int64_t M, int64_t K) {
+    const int64_t tiles = cdiv(M, tc::kM);
+    return std::max<int64_t>(1, std::min<int64_t>(cdiv(2 * sm, tiles), cdiv(K, 256)));
+  };
+  return std::max(splits_for(n, C) * n, splits_for(C, n) * C) * r;
+}
+
+// D = A Q (mode 0) or A^T Y (mode 1) on the tensor cores; Dpart = scratch of tc_partial_floats()
+int tc_project(int mode, const float *A, const float *S, float *D, float *Dpart, int64_t n, int64_t C, int r,
+               cudaStream_t st) {
+  const int NP = r <= 16 ? 16 : 32;
+  const int64_t M = mode == 0 ? n : C, K = mode == 0 ? C : n;
+  const int64_t tiles = cdiv(M, tc::kM);
+  const int64_t splits = std::max<int64_t>(1, std::min<int64_t>(cdiv(2 * sm_count(), tiles), cdiv(K, 256)));
+  const int64_t kper = cdiv(cdiv(K, splits), tc::kKC) * tc::kKC;
+  const int64_t nsplit = cdiv(K, kper);
+  const size_t smem = tc_smem_bytes(NP);
+  dim3 grid((unsigned)tiles, (unsigned)nsplit);
+  if (mode == 0) {
+    cudaFuncSetAttribute(tc::k_tc_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tc::k_tc_gemm<0><<<grid, tc::kThreads, smem, st>>>(A, S, Dpart, n, C, r, NP, kper);
+  } else {
+    cudaFuncSetAttribute(tc::k_tc_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tc::k_tc_gemm<1><<<grid, tc::kThreads, smem, st>>>(A, S, Dpart, n, C, r, NP, kper);
+  }
+  const int64_t cnt = M * r;
+  tc::k_tc_reduce<<<(unsigned)cdiv(cnt, 256), 256, 0, st>>>(Dpart, D, cnt, (int)nsplit);
+  count_launch(2);
+  return cuda_status("tc_project");
+}
+
+}  // namespace cc

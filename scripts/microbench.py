@@ -125,6 +125,25 @@ def main():
         us = timed(dec7, a.reps)
         out["k2_decode_7peers_P8"] = {"us": round(us, 2),
                                       "alg_GBps": round(7 * rows8 * c * (8 + bits / 8) / us / 1e3, 1)}
+    # low-rank encode (T=2) on this shard: tensor-core vs f64 CUDA-core projections
+    from paper_2507_17511_b200 import linalg as la
+    xt = xs[0].float()
+    for r in (8, 16):
+        sp = cx.CompressorSpec(cx.CompressorKind.LOWRANK, rank=r, iterations=2)
+        for backend in (1, 0):
+            lib.cc_set_lowrank_backend(backend)
+            cx.encode_lowrank(xt, sp, la.make_rng(0))
+            us = timed(lambda i: cx.encode_lowrank(xt, sp, la.make_rng(i)), 5)
+            out[f"lowrank_r{r}_{'tc' if backend else 'f64'}"] = {"us": round(us, 1)}
+    lib.cc_set_lowrank_backend(1)
+    # top-k encode_step (residual + select + ordered write + sparse update)
+    for f in (0.01, 0.1):
+        sp = cx.CompressorSpec(cx.CompressorKind.TOPK, keep_fraction=f)
+        st = pl.LayerState("residual_with_feedback", 1, torch.zeros(n, c, device="cuda"))
+        pl.encode_step(st, xs[0], sp)
+        pl.encode_step(st, xs[1], sp)
+        us = timed(lambda i: pl.encode_step(st, xs[i % 2], sp), 10)
+        out[f"topk_step_{f}"] = {"us": round(us, 1)}
     # plain copy roofline reference: base -> feedback of another layer
     def cp(i):
         sts[(i + 1) % L].feedback.copy_(sts[i % L].base)

@@ -164,3 +164,25 @@ def test_lowrank_protocol_sender_receiver_identical(int4):
                rng=linalg.spawn_rng(11, 5, t))
     # trajectory-level agreement with the reference algorithm (tolerance)
     assert _relerr(snd.base.cpu().numpy(), och.base) < 2e-2
+
+
+@pytest.mark.parametrize("shape", [(64, 384), (200, 1000), (1024, 3072), (4096, 3072)], ids=lambda s: f"{s[0]}x{s[1]}")
+@pytest.mark.parametrize("r", [4, 8, 16, 32])
+def test_tcgen05_backend_matches_f64_backend(shape, r):
+    """The tcgen05 3xTF32 projections vs the f64 CUDA-core projections: same
+    subspace, reconstruction errors equal to ~1e-6 relative."""
+    from paper_2507_17511_b200 import _lib
+
+    cx, _, linalg = _mods()
+    n, c = shape
+    x = torch.from_numpy(synth.flux_like(n, c, 1, seed=n + r)[0]).cuda()
+    lib = _lib.load()
+    errs = {}
+    try:
+        for backend in (0, 1):
+            lib.cc_set_lowrank_backend(backend)
+            p = cx.encode_lowrank(x, _spec(r), linalg.make_rng(r))
+            errs[backend] = _relerr(p.decode().cpu().numpy(), x.cpu().numpy())
+    finally:
+        lib.cc_set_lowrank_backend(1)
+    assert abs(errs[0] - errs[1]) <= 1e-5 * max(1.0, errs[0]), errs
