@@ -159,46 +159,52 @@ __global__ void __launch_bounds__(kThreads) k_gram(const double *__restrict__ M,
   }
 }
 
-// one CTA: G = sum of partials (fixed order); Cholesky G = R^T R; Rinv = R^-1;
-// flag = 1 if any pivot^2 < tol (degenerate column -> CGS2 fallback)
-__global__ void k_chol(const double *__restrict__ Gpart, int nblk, int r, double *__restrict__ Rinv,
-                       int *__restrict__ flag, int pass) {
+// one CTA (1024 threads): G = sum of partials (fixed order); Cholesky G = R^T R
+// (right-looking, one column per step, trailing update in parallel); Rinv = R^-1
+// (one column per thread, back substitution); flag = 1 if any pivot^2 < tol
+// (degenerate column -> CGS2 fallback)
+__global__ void __launch_bounds__(1024) k_chol(const double *__restrict__ Gpart, int nblk, int r,
+                                               double *__restrict__ Rinv, int *__restrict__ flag, int pass) {
   __shared__ double G[kMaxR][kMaxR + 1];
   __shared__ double R[kMaxR][kMaxR + 1];
   __shared__ int bad;
-  for (int o = threadIdx.x; o < r * r; o += blockDim.x) {
+  const int t = threadIdx.x;
+  const int a = t / kMaxR, c = t % kMaxR;  // (row, column) owned by this thread
+  if (a < r && c < r) {
     double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += Gpart[(int64_t)b * r * r + o];
-    G[o / r][o % r] = s;
+    for (int b = 0; b < nblk; ++b) s += Gpart[(int64_t)b * r * r + a * r + c];
+    G[a][c] = s;
+    R[a][c] = 0.0;
   }
-  if (threadIdx.x == 0) bad = 0;
+  if (t == 0) bad = 0;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < r; ++i)
-      for (int j = 0; j < r; ++j) R[i][j] = 0.0;
-    for (int j = 0; j < r; ++j) {
+  for (int j = 0; j < r; ++j) {
+    // G now holds the Schur complement for rows/cols >= j
+    if (t == 0) {
       double piv = G[j][j];
-      for (int k = 0; k < j; ++k) piv -= R[k][j] * R[k][j];
       if (!(piv >= kDegenerate)) {
         bad = 1;
         piv = 1.0;
       }
-      const double d = sqrt(piv);
-      R[j][j] = d;
-      for (int c = j + 1; c < r; ++c) {
-        double s = G[j][c];
-        for (int k = 0; k < j; ++k) s -= R[k][j] * R[k][c];
-        R[j][c] = s / d;
-      }
+      R[j][j] = sqrt(piv);
     }
-    // Rinv (upper triangular) by back substitution, column by column
-    for (int c = 0; c < r; ++c) {
-      for (int i = r - 1; i >= 0; --i) {
-        double s = (i == c) ? 1.0 : 0.0;
-        for (int k = i + 1; k < r; ++k) s -= R[i][k] * Rinv[k * r + c];
-        Rinv[i * r + c] = (i > c) ? 0.0 : s / R[i][i];
-      }
+    __syncthreads();
+    if (t > j && t < r) R[j][t] = G[j][t] / R[j][j];
+    __syncthreads();
+    if (a > j && a < r && c >= a && c < r) G[a][c] -= R[j][a] * R[j][c];
+    if (a > j && a < r && c > j && c < a) G[a][c] -= R[j][a] * R[j][c];  // keep the lower half consistent
+    __syncthreads();
+  }
+  if (t < r) {  // column t of Rinv (upper triangular)
+    double x[kMaxR];
+    for (int i = r - 1; i >= 0; --i) {
+      double s = (i == t) ? 1.0 : 0.0;
+      for (int k = i + 1; k <= t; ++k) s -= R[i][k] * x[k];
+      x[i] = (i > t) ? 0.0 : s / R[i][i];
     }
+    for (int i = 0; i < r; ++i) Rinv[i * r + t] = x[i];
+  }
+  if (t == 0) {
     if (pass == 0) *flag = bad;
     else *flag |= bad;
   }
@@ -449,7 +455,7 @@ static void orth(const float *M, float *out, int64_t m, int r, const lr::Work &w
   const int nblk = (int)cdiv(m, kGramRows);
   for (int pass = 0; pass < 2; ++pass) {
     k_gram<<<nblk, kThreads, 0, st>>>(w.M64, w.Gpart, m, r);
-    k_chol<<<1, 256, 0, st>>>(w.Gpart, nblk, r, w.Rinv, w.flag, pass);
+    k_chol<<<1, 1024, 0, st>>>(w.Gpart, nblk, r, w.Rinv, w.flag, pass);
     k_apply_rinv<<<(unsigned)cdiv(m, kThreads), kThreads, 0, st>>>(w.M64, w.Rinv, m, r);
   }
   k_cgs2_fallback<<<1, 1024, 0, st>>>(M, w.M64, m, r, w.flag, g_lr_seed++);

@@ -57,6 +57,17 @@ struct Work {
 
 __device__ __forceinline__ uint32_t key_of(float t) { return __float_as_uint(t) & 0x7fffffffu; }
 
+// shared-memory histogram increment with warp aggregation: lanes that hit the same
+// bin elect one leader (activation magnitudes pile into a few bins, so plain
+// atomics would serialise up to 32-way)
+__device__ __forceinline__ void hist_add(uint32_t *h, uint32_t bin, bool valid) {
+  const unsigned live = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  const unsigned peers = __match_any_sync(live, bin);
+  const int leader = __ffs(peers) - 1;
+  if ((threadIdx.x & 31) == leader) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+}
+
 // ---- pass H1 ---------------------------------------------------------------
 template <int MODE, typename XT, bool FROM_T>
 __global__ void __launch_bounds__(kThreads) k_h1(const XT *__restrict__ x, float *__restrict__ base,
@@ -70,7 +81,12 @@ __global__ void __launch_bounds__(kThreads) k_h1(const XT *__restrict__ x, float
   __syncthreads();
   double tsq = 0.0;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
-  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total; e += stride) {
+  for (int64_t e0 = (int64_t)blockIdx.x * kThreads; e0 < total; e0 += stride) {
+    const int64_t e = e0 + threadIdx.x;
+    if (e >= total) {
+      hist_add(h, 0u, false);
+      continue;
+    }
     float t;
     if constexpr (FROM_T) {
       t = tin[e];
@@ -89,7 +105,7 @@ __global__ void __launch_bounds__(kThreads) k_h1(const XT *__restrict__ x, float
     }
     if (decoded) decoded[e] = 0.0f;
     tsq += (double)t * (double)t;
-    atomicAdd(&h[key_of(t) >> 19], 1u);
+    hist_add(h, key_of(t) >> 19, true);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kBins; i += kThreads)
@@ -173,7 +189,7 @@ __global__ void __launch_bounds__(kThreads) k_h2(const float *__restrict__ t, in
       key = key_of(__ldcs(t + e));
       in = (key >> 19) == b1;
     }
-    if (in) atomicAdd(&h[(key >> 7) & 0xfffu], 1u);
+    hist_add(h, (key >> 7) & 0xfffu, in);
     const uint32_t m = __ballot_sync(0xffffffffu, in);
     if (m) {
       uint32_t basei = 0;
@@ -199,9 +215,11 @@ __global__ void __launch_bounds__(kThreads) k_h3(const float *__restrict__ t, in
   const bool use_cand = st->cand <= cap;
   const int64_t n = use_cand ? (int64_t)st->cand : total;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
-  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < n; e += stride) {
-    const uint32_t key = use_cand ? cand[e] : key_of(t[e]);
-    if ((key >> 7) == prefix) atomicAdd(&h[key & 127u], 1u);
+  for (int64_t e0 = (int64_t)blockIdx.x * kThreads; e0 < n; e0 += stride) {
+    const int64_t e = e0 + threadIdx.x;
+    uint32_t key = 0;
+    if (e < n) key = use_cand ? cand[e] : key_of(t[e]);
+    hist_add(h, key & 127u, e < n && (key >> 7) == prefix);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kBins3; i += kThreads)
