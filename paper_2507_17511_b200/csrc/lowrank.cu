@@ -171,8 +171,17 @@ __global__ void __launch_bounds__(1024) k_chol(const double *__restrict__ Gpart,
   const int t = threadIdx.x;
   const int a = t / kMaxR, c = t % kMaxR;  // (row, column) owned by this thread
   if (a < r && c < r) {
+    // fixed-order sum of the block partials; 8 independent loads in flight per step
     double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += Gpart[(int64_t)b * r * r + a * r + c];
+    int b = 0;
+    for (; b + 8 <= nblk; b += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = Gpart[(int64_t)(b + q) * r * r + a * r + c];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += v[q];
+    }
+    for (; b < nblk; ++b) s += Gpart[(int64_t)b * r * r + a * r + c];
     G[a][c] = s;
     R[a][c] = 0.0;
   }

@@ -107,10 +107,117 @@ struct Stage {
 
 // MODE 0 (AQ): P[m][k] = A[i0+m][k0+k], S[j][k] = Q[k0+k][j]   (K = C)
 // MODE 1 (ATY): P[m][k] = A[k0+k][c0+m], S[j][k] = Y[k0+k][j]  (K = n)
+//
+// Software pipeline: the raw f32 operands of chunk c+1 are loaded into registers
+// (8 x 128-bit A loads + NP/4 S loads per thread) right after chunk c has been
+// split into hi/lo shared tiles, so the global loads fly while chunk c's sync,
+// MMA issue and the wait for stage reuse go on.
+constexpr int kAItems = kM * kKC / 4 / kThreads;  // 8 float4 per thread per chunk
+template <int MODE, int NP>
+struct Raw {
+  float4 a[kAItems];
+  float s[NP * kKC / kThreads];
+};
+
+// item i of thread tid -> (m, k) of its 4-element group
 template <int MODE>
+__device__ __forceinline__ void a_item(int tid, int i, int &m, int &k) {
+  const int e = tid + i * kThreads;
+  if constexpr (MODE == 0) {  // 4 consecutive k of one row: a warp reads 4 rows x 128 B
+    m = e >> 3;
+    k = (e & 7) * 4;
+  } else {  // 4 consecutive m of one k: a warp covers 8 k x 4 m-quads (2-way smem conflicts)
+    k = (e & 7) | (((e >> 5) & 3) << 3);
+    m = (((e >> 3) & 3) | ((e >> 7) << 2)) * 4;
+  }
+}
+
+template <int MODE, int NP>
+__device__ __forceinline__ void load_raw(Raw<MODE, NP> &rw, const float *__restrict__ A, const float *__restrict__ S,
+                                         int64_t m0, int64_t k0, int64_t khi, int64_t Mdim, int64_t C, int r,
+                                         bool vec) {
+  const int tid = threadIdx.x;
+  const int kc = (int)min64(kKC, khi - k0);
+#pragma unroll
+  for (int i = 0; i < kAItems; ++i) {
+    int m, k;
+    a_item<MODE>(tid, i, m, k);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (MODE == 0) {
+      if (m0 + m < Mdim && k < kc) {
+        const float *src = A + (m0 + m) * C + k0 + k;
+        if (vec && k + 4 <= kc) {
+          v = __ldg(reinterpret_cast<const float4 *>(src));
+        } else {
+          v.x = src[0];
+          if (k + 1 < kc) v.y = src[1];
+          if (k + 2 < kc) v.z = src[2];
+          if (k + 3 < kc) v.w = src[3];
+        }
+      }
+    } else {
+      if (k < kc && m0 + m < Mdim) {
+        const float *src = A + (k0 + k) * C + m0 + m;
+        if (vec && m0 + m + 4 <= Mdim) {
+          v = __ldg(reinterpret_cast<const float4 *>(src));
+        } else {
+          v.x = src[0];
+          if (m0 + m + 1 < Mdim) v.y = src[1];
+          if (m0 + m + 2 < Mdim) v.z = src[2];
+          if (m0 + m + 3 < Mdim) v.w = src[3];
+        }
+      }
+    }
+    rw.a[i] = v;
+  }
+#pragma unroll
+  for (int i = 0; i < NP * kKC / kThreads; ++i) {
+    const int e = tid + i * kThreads;
+    const int j = e / kKC, kk = e % kKC;
+    rw.s[i] = (j < r && kk < kc) ? __ldg(S + (k0 + kk) * r + j) : 0.0f;
+  }
+}
+
+template <int MODE, int NP>
+__device__ __forceinline__ void store_split(const Raw<MODE, NP> &rw, const Stage &sg) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < kAItems; ++i) {
+    int m, k;
+    a_item<MODE>(tid, i, m, k);
+    const float4 v = rw.a[i];
+    const float h0 = tf32_rna(v.x), h1 = tf32_rna(v.y), h2 = tf32_rna(v.z), h3 = tf32_rna(v.w);
+    const float l0 = tf32_rna(v.x - h0), l1 = tf32_rna(v.y - h1), l2 = tf32_rna(v.z - h2), l3 = tf32_rna(v.w - h3);
+    if constexpr (MODE == 0) {
+      const uint32_t off = sw128(m, k);
+      *reinterpret_cast<float4 *>(sg.a_hi + off) = make_float4(h0, h1, h2, h3);
+      *reinterpret_cast<float4 *>(sg.a_lo + off) = make_float4(l0, l1, l2, l3);
+    } else {
+      const float hh[4] = {h0, h1, h2, h3}, ll[4] = {l0, l1, l2, l3};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t off = sw128(m + q, k);
+        *reinterpret_cast<float *>(sg.a_hi + off) = hh[q];
+        *reinterpret_cast<float *>(sg.a_lo + off) = ll[q];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NP * kKC / kThreads; ++i) {
+    const int e = tid + i * kThreads;
+    const int j = e / kKC, kk = e % kKC;
+    const float v = rw.s[i], h = tf32_rna(v);
+    const uint32_t off = sw128(j, kk);
+    *reinterpret_cast<float *>(sg.b_hi + off) = h;
+    *reinterpret_cast<float *>(sg.b_lo + off) = tf32_rna(v - h);
+  }
+  fence_proxy_async_smem();
+}
+
+template <int MODE, int NP>
 __global__ void __launch_bounds__(kThreads) k_tc_gemm(const float *__restrict__ A, const float *__restrict__ S,
                                                        float *__restrict__ Dpart, int64_t n, int64_t C, int r,
-                                                       int NP, int64_t kper) {
+                                                       int64_t kper, int vec) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align the tile area
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -120,19 +227,17 @@ __global__ void __launch_bounds__(kThreads) k_tc_gemm(const float *__restrict__ 
   const int64_t m0 = (int64_t)blockIdx.x * kM;
   const int split = blockIdx.y;
   const int64_t klo = split * kper, khi = min64(Kdim, klo + kper);
-  const uint32_t a_bytes = kM * kKC * 4;  // 16 KB
-  const uint32_t b_bytes = (uint32_t)NP * kKC * 4;
-  const uint32_t b_round = (b_bytes + 1023) & ~1023u;
-  Stage st[2];
-  for (int s = 0; s < 2; ++s) {
-    uint8_t *b = smem + s * (2 * a_bytes + 2 * b_round);
-    st[s].a_hi = b;
-    st[s].a_lo = b + a_bytes;
-    st[s].b_hi = b + 2 * a_bytes;
-    st[s].b_lo = b + 2 * a_bytes + b_round;
-  }
+  constexpr uint32_t a_bytes = kM * kKC * 4;  // 16 KB
+  constexpr uint32_t b_round = ((uint32_t)NP * kKC * 4 + 1023) & ~1023u;
+  auto stage = [&](int s) {  // computed, not indexed: keeps the stage table out of local memory
+    uint8_t *b = smem + (uint32_t)s * (2 * a_bytes + 2 * b_round);
+    return Stage{b, b + a_bytes, b + 2 * a_bytes, b + 2 * a_bytes + b_round};
+  };
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * (2 * a_bytes + 2 * b_round));
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 2);
+  const int64_t nchunks = (khi - klo + kKC - 1) / kKC;
+  Raw<MODE, NP> rw;
+  if (nchunks > 0) load_raw<MODE, NP>(rw, A, S, m0, klo, khi, Mdim, C, r, vec != 0);  // overlaps the setup
   if (warp == 0) tmem_alloc(tmem_slot, kTmemCols);
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -143,81 +248,23 @@ __global__ void __launch_bounds__(kThreads) k_tc_gemm(const float *__restrict__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t idesc = idesc_tf32(kM, NP);
+  constexpr uint32_t idesc = idesc_tf32(kM, NP);
 
-  auto stage_chunk = [&](const Stage &sg, int64_t k0) {
-    const int kc = (int)min64(kKC, khi - k0);
-    // P tile: 128 rows x 32 k
-    if constexpr (MODE == 0) {
-      for (int e = tid; e < kM * (kKC / 4); e += kThreads) {  // one float4 (4 consecutive k) per item
-        const int m = e / (kKC / 4), k4 = (e % (kKC / 4)) * 4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (m0 + m < Mdim && k4 < kc) {
-          const float *src = A + (m0 + m) * C + k0 + k4;
-          if (k4 + 4 <= kc && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-            v = __ldg(reinterpret_cast<const float4 *>(src));
-          } else {
-            float t[4] = {0.f, 0.f, 0.f, 0.f};
-            for (int q = 0; q < 4 && k4 + q < kc; ++q) t[q] = src[q];
-            v = make_float4(t[0], t[1], t[2], t[3]);
-          }
-        }
-        const float h0 = tf32_rna(v.x), h1 = tf32_rna(v.y), h2 = tf32_rna(v.z), h3 = tf32_rna(v.w);
-        const uint32_t off = sw128(m, k4);
-        *reinterpret_cast<float4 *>(sg.a_hi + off) = make_float4(h0, h1, h2, h3);
-        *reinterpret_cast<float4 *>(sg.a_lo + off) = make_float4(tf32_rna(v.x - h0), tf32_rna(v.y - h1),
-                                                                 tf32_rna(v.z - h2), tf32_rna(v.w - h3));
-      }
-    } else {
-      for (int e = tid; e < kKC * (kM / 4); e += kThreads) {  // one float4 of 4 consecutive m per item
-        const int kk = e / (kM / 4), mq = (e % (kM / 4)) * 4;
-        float t[4] = {0.f, 0.f, 0.f, 0.f};
-        if (kk < kc) {
-          const float *src = A + (k0 + kk) * C + m0 + mq;
-          if (m0 + mq + 4 <= Mdim && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-            const float4 v = __ldg(reinterpret_cast<const float4 *>(src));
-            t[0] = v.x; t[1] = v.y; t[2] = v.z; t[3] = v.w;
-          } else {
-            for (int q = 0; q < 4; ++q)
-              if (m0 + mq + q < Mdim) t[q] = src[q];
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float h = tf32_rna(t[q]);
-          const uint32_t off = sw128(mq + q, kk);
-          *reinterpret_cast<float *>(sg.a_hi + off) = h;
-          *reinterpret_cast<float *>(sg.a_lo + off) = tf32_rna(t[q] - h);
-        }
-      }
-    }
-    // S tile: NP rows (j) x 32 k; rows >= r are zero
-    for (int e = tid; e < NP * kKC; e += kThreads) {
-      const int j = e / kKC, kk = e % kKC;
-      float v = 0.f;
-      if (j < r && kk < kc) v = S[(k0 + kk) * r + j];
-      const float h = tf32_rna(v);
-      const uint32_t off = sw128(j, kk);
-      *reinterpret_cast<float *>(sg.b_hi + off) = h;
-      *reinterpret_cast<float *>(sg.b_lo + off) = tf32_rna(v - h);
-    }
-    fence_proxy_async_smem();
-  };
-
-  const int64_t nchunks = (khi - klo + kKC - 1) / kKC;
-  uint32_t ph[2] = {0u, 0u};
+  uint32_t ph = 0u;  // bit s = parity of stage s's barrier
   for (int64_t c = 0; c < nchunks; ++c) {
     const int s = (int)(c & 1);
     if (c >= 2) {  // the MMAs that read this stage two chunks ago must be done
-      mbar_wait(&bar[s], ph[s]);
-      ph[s] ^= 1u;
+      mbar_wait(&bar[s], (ph >> s) & 1u);
+      ph ^= 1u << s;
     }
-    stage_chunk(st[s], klo + c * kKC);
+    const Stage sg = stage(s);
+    store_split<MODE, NP>(rw, sg);
+    if (c + 1 < nchunks) load_raw<MODE, NP>(rw, A, S, m0, klo + (c + 1) * kKC, khi, Mdim, C, r, vec != 0);
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
-      const uint64_t ah = umma_desc_sw128(smem_u32(st[s].a_hi)), al = umma_desc_sw128(smem_u32(st[s].a_lo));
-      const uint64_t bh = umma_desc_sw128(smem_u32(st[s].b_hi)), bl = umma_desc_sw128(smem_u32(st[s].b_lo));
+      const uint64_t ah = umma_desc_sw128(smem_u32(sg.a_hi)), al = umma_desc_sw128(smem_u32(sg.a_lo));
+      const uint64_t bh = umma_desc_sw128(smem_u32(sg.b_hi)), bl = umma_desc_sw128(smem_u32(sg.b_lo));
 #pragma unroll
       for (int ks = 0; ks < kKC / 8; ++ks) {  // K = 8 tf32 (32 bytes) per instruction
         const uint64_t dk = (uint64_t)((ks * 32) >> 4);
@@ -233,24 +280,21 @@ __global__ void __launch_bounds__(kThreads) k_tc_gemm(const float *__restrict__ 
   // drain: wait for the last (up to two) commits
   for (int64_t c = std::max<int64_t>(0, nchunks - 2); c < nchunks; ++c) {
     const int s = (int)(c & 1);
-    mbar_wait(&bar[s], ph[s]);
-    ph[s] ^= 1u;
+    mbar_wait(&bar[s], (ph >> s) & 1u);
+    ph ^= 1u << s;
   }
   tc_fence_after();
   // epilogue: warp w reads TMEM lanes 32w..32w+31 (rows m0 + 32w + lane)
   const int64_t m = m0 + warp * 32 + lane;
   float *out = Dpart + (int64_t)split * Mdim * r;
+#pragma unroll
   for (int cb = 0; cb < NP; cb += 16) {
     float v[16];
     tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)cb, v);
-    if (nchunks > 0 && m < Mdim) {
+    if (m < Mdim) {
 #pragma unroll
       for (int q = 0; q < 16; ++q)
-        if (cb + q < r) out[m * r + cb + q] = v[q];
-    } else if (m < Mdim) {
-#pragma unroll
-      for (int q = 0; q < 16; ++q)
-        if (cb + q < r) out[m * r + cb + q] = 0.0f;
+        if (cb + q < r) out[m * r + cb + q] = nchunks > 0 ? v[q] : 0.0f;
     }
   }
   tc_fence_before();
@@ -279,14 +323,26 @@ static size_t tc_smem_bytes(int NP) {
   return 1024 + 2 * (2 * a + 2 * b) + 64;
 }
 
+// split-K plan: ~4 CTAs per SM (2 resident x 2 waves), >= 4 K chunks per CTA
+static void tc_plan(int64_t M, int64_t K, int64_t *splits, int64_t *kper) {
+  const int64_t tiles = cdiv(M, tc::kM);
+  int64_t sp = std::max<int64_t>(1, std::min<int64_t>(cdiv(4 * sm_count(), tiles), cdiv(K, 4 * tc::kKC)));
+  *kper = cdiv(cdiv(K, sp), tc::kKC) * tc::kKC;
+  *splits = cdiv(K, *kper);
+}
+
 int64_t tc_partial_floats(int64_t n, int64_t C, int r) {
-  // max over both modes of splits * M * r
-  const int64_t sm = sm_count();
-  auto splits_for = [&](int64_t M, int64_t K) {
-    const int64_t tiles = cdiv(M, tc::kM);
-    return std::max<int64_t>(1, std::min<int64_t>(cdiv(2 * sm, tiles), cdiv(K, 256)));
-  };
-  return std::max(splits_for(n, C) * n, splits_for(C, n) * C) * r;
+  int64_t s0, s1, kp;
+  tc_plan(n, C, &s0, &kp);
+  tc_plan(C, n, &s1, &kp);
+  return std::max(s0 * n, s1 * C) * r;
+}
+
+template <int MODE, int NP>
+static void tc_launch(dim3 grid, size_t smem, cudaStream_t st, const float *A, const float *S, float *Dpart,
+                      int64_t n, int64_t C, int r, int64_t kper, int vec) {
+  cudaFuncSetAttribute(tc::k_tc_gemm<MODE, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tc::k_tc_gemm<MODE, NP><<<grid, tc::kThreads, smem, st>>>(A, S, Dpart, n, C, r, kper, vec);
 }
 
 // D = A Q (mode 0) or A^T Y (mode 1) on the tensor cores; Dpart = scratch of tc_partial_floats()
@@ -294,18 +350,17 @@ int tc_project(int mode, const float *A, const float *S, float *D, float *Dpart,
                cudaStream_t st) {
   const int NP = r <= 16 ? 16 : 32;
   const int64_t M = mode == 0 ? n : C, K = mode == 0 ? C : n;
-  const int64_t tiles = cdiv(M, tc::kM);
-  const int64_t splits = std::max<int64_t>(1, std::min<int64_t>(cdiv(2 * sm_count(), tiles), cdiv(K, 256)));
-  const int64_t kper = cdiv(cdiv(K, splits), tc::kKC) * tc::kKC;
-  const int64_t nsplit = cdiv(K, kper);
+  int64_t nsplit, kper;
+  tc_plan(M, K, &nsplit, &kper);
   const size_t smem = tc_smem_bytes(NP);
-  dim3 grid((unsigned)tiles, (unsigned)nsplit);
+  const int vec = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && C % 4 == 0;
+  dim3 grid((unsigned)cdiv(M, tc::kM), (unsigned)nsplit);
   if (mode == 0) {
-    cudaFuncSetAttribute(tc::k_tc_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    tc::k_tc_gemm<0><<<grid, tc::kThreads, smem, st>>>(A, S, Dpart, n, C, r, NP, kper);
+    if (NP == 16) tc_launch<0, 16>(grid, smem, st, A, S, Dpart, n, C, r, kper, vec);
+    else tc_launch<0, 32>(grid, smem, st, A, S, Dpart, n, C, r, kper, vec);
   } else {
-    cudaFuncSetAttribute(tc::k_tc_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    tc::k_tc_gemm<1><<<grid, tc::kThreads, smem, st>>>(A, S, Dpart, n, C, r, NP, kper);
+    if (NP == 16) tc_launch<1, 16>(grid, smem, st, A, S, Dpart, n, C, r, kper, vec);
+    else tc_launch<1, 32>(grid, smem, st, A, S, Dpart, n, C, r, kper, vec);
   }
   const int64_t cnt = M * r;
   tc::k_tc_reduce<<<(unsigned)cdiv(cnt, 256), 256, 0, st>>>(Dpart, D, cnt, (int)nsplit);

@@ -10,8 +10,8 @@
 //            residual_with_feedback mode, else into scratch), 4096-bin histogram
 //            of key[30:19] in shared memory -> global; ||t||^2 partials.
 //   find     one CTA: suffix scan of the histogram -> bin b1, remaining need
-//   pass H2  keys in bin b1: 4096-bin histogram of key[18:7] + candidate list
-//   find     -> b2;   H3 over candidates (or all keys if the list overflowed):
+//   pass H2  keys in bin b1: 4096-bin histogram of key[18:7]
+//   find     -> b2;   H3: keys with key[30:7] == (b1, b2):
 //            128-bin histogram of key[6:0] -> threshold key T and the number of
 //            ties at T to take (lowest indices first)
 //   pass C   per-chunk counts of key > T and key == T
@@ -39,15 +39,12 @@ struct State {
   uint32_t b1, b2;      // selected bins
   uint32_t T;           // threshold key
   uint32_t ties;        // elements with key == T to take
-  uint32_t cand;        // candidate count (keys in bin b1)
-  uint32_t pad[2];
+  uint32_t pad[3];
 };
 
 struct Work {
   uint32_t *hist1, *hist2, *hist3;
   State *st;
-  uint32_t *cand;
-  int64_t cap;
   uint32_t *cnt_gt, *cnt_eq, *sel_pref, *eq_pref;
   double *part;  // [nH1 + nChunks][2]
   float *tscratch;
@@ -57,55 +54,110 @@ struct Work {
 
 __device__ __forceinline__ uint32_t key_of(float t) { return __float_as_uint(t) & 0x7fffffffu; }
 
-// shared-memory histogram increment with warp aggregation: lanes that hit the same
-// bin elect one leader (activation magnitudes pile into a few bins, so plain
-// atomics would serialise up to 32-way)
+// shared-memory histogram increment.  Plain shared atomics: measured on B200 with
+// activation residuals (~28 distinct bins per 32 keys) they run at ~70% of the
+// streaming rate, while __match_any_sync warp aggregation is 4x slower
+// (scripts/exp/hist_bench.cu).
 __device__ __forceinline__ void hist_add(uint32_t *h, uint32_t bin, bool valid) {
-  const unsigned live = __ballot_sync(0xffffffffu, valid);
-  if (!valid) return;
-  const unsigned peers = __match_any_sync(live, bin);
-  const int leader = __ffs(peers) - 1;
-  if ((threadIdx.x & 31) == leader) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+  if (valid) atomicAdd(&h[bin], 1u);
 }
 
 // ---- pass H1 ---------------------------------------------------------------
+// 4 consecutive elements per item (128-bit loads when `vec`), 2 items in flight per
+// thread per iteration: the warp-synchronous histogram update would otherwise leave
+// one load in flight per thread and the pass latency bound.
+constexpr int kH1Unroll = 2;
+template <int MODE, typename XT, bool FROM_T>
+__device__ __forceinline__ void h1_item(const XT *__restrict__ x, float *__restrict__ base, float *__restrict__ aux,
+                                        const float *__restrict__ tin, float *__restrict__ tout,
+                                        float *__restrict__ decoded, int64_t e, int64_t total, bool vec,
+                                        float (&t)[4]) {
+  if (vec && e + 4 <= total) {
+    float4 tv;
+    if constexpr (FROM_T) {
+      tv = __ldcs(reinterpret_cast<const float4 *>(tin + e));
+    } else {
+      const float4 xx = Act<XT>::load4(x + e);
+      float4 bb = make_float4(0.f, 0.f, 0.f, 0.f), aa = bb;
+      if constexpr (MODE != CC_NAIVE) {
+        bb = *reinterpret_cast<const float4 *>(base + e);
+        aa = *reinterpret_cast<const float4 *>(aux + e);
+        const bool neg0 = __float_as_uint(bb.x) == 0x80000000u || __float_as_uint(bb.y) == 0x80000000u ||
+                          __float_as_uint(bb.z) == 0x80000000u || __float_as_uint(bb.w) == 0x80000000u;
+        if (neg0) {  // dense base + 0.0 semantics
+          float4 c = bb;
+          if (__float_as_uint(c.x) == 0x80000000u) c.x = 0.0f;
+          if (__float_as_uint(c.y) == 0x80000000u) c.y = 0.0f;
+          if (__float_as_uint(c.z) == 0x80000000u) c.z = 0.0f;
+          if (__float_as_uint(c.w) == 0x80000000u) c.w = 0.0f;
+          *reinterpret_cast<float4 *>(base + e) = c;
+        }
+      }
+      tv = make_float4(target_of<MODE>(xx.x, bb.x, aa.x), target_of<MODE>(xx.y, bb.y, aa.y),
+                       target_of<MODE>(xx.z, bb.z, aa.z), target_of<MODE>(xx.w, bb.w, aa.w));
+      *reinterpret_cast<float4 *>(tout + e) = tv;
+      if constexpr (MODE == CC_NO_FEEDBACK) *reinterpret_cast<float4 *>(aux + e) = xx;  // ref' = a*
+      if constexpr (MODE == CC_NAIVE) *reinterpret_cast<float4 *>(base + e) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (decoded) *reinterpret_cast<float4 *>(decoded + e) = make_float4(0.f, 0.f, 0.f, 0.f);
+    t[0] = tv.x; t[1] = tv.y; t[2] = tv.z; t[3] = tv.w;
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t ee = e + q;
+    t[q] = 0.0f;
+    if (ee >= total) continue;
+    float tq;
+    if constexpr (FROM_T) {
+      tq = tin[ee];
+    } else {
+      const float xx = Act<XT>::load1(x + ee);
+      float bb = 0.f, aa = 0.f;
+      if constexpr (MODE != CC_NAIVE) {
+        bb = base[ee];
+        if (__float_as_uint(bb) == 0x80000000u) base[ee] = 0.0f;
+        aa = aux[ee];
+      }
+      tq = target_of<MODE>(xx, bb, aa);
+      tout[ee] = tq;
+      if constexpr (MODE == CC_NO_FEEDBACK) aux[ee] = xx;
+      if constexpr (MODE == CC_NAIVE) base[ee] = 0.0f;
+    }
+    if (decoded) decoded[ee] = 0.0f;
+    t[q] = tq;
+  }
+}
+
 template <int MODE, typename XT, bool FROM_T>
 __global__ void __launch_bounds__(kThreads) k_h1(const XT *__restrict__ x, float *__restrict__ base,
                                                   float *__restrict__ aux, const float *__restrict__ tin,
                                                   float *__restrict__ tout, float *__restrict__ decoded,
-                                                  int64_t total, uint32_t *__restrict__ hist1,
+                                                  int64_t total, int vec, uint32_t *__restrict__ hist1,
                                                   double *__restrict__ part) {
   __shared__ uint32_t h[kBins];
   __shared__ double red[kThreads / 32];
   for (int i = threadIdx.x; i < kBins; i += kThreads) h[i] = 0;
   __syncthreads();
   double tsq = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * kThreads;
-  for (int64_t e0 = (int64_t)blockIdx.x * kThreads; e0 < total; e0 += stride) {
-    const int64_t e = e0 + threadIdx.x;
-    if (e >= total) {
-      hist_add(h, 0u, false);
-      continue;
-    }
-    float t;
-    if constexpr (FROM_T) {
-      t = tin[e];
-    } else {
-      const float xx = Act<XT>::load1(x + e);
-      float bb = 0.f, aa = 0.f;
-      if constexpr (MODE != CC_NAIVE) {
-        bb = base[e];
-        if (__float_as_uint(bb) == 0x80000000u) base[e] = 0.0f;  // dense base + 0.0 semantics
+  const int64_t nitems = (total + 3) / 4;
+  const int64_t stride = (int64_t)gridDim.x * kThreads * kH1Unroll;
+  for (int64_t i0 = (int64_t)blockIdx.x * kThreads * kH1Unroll; i0 < nitems; i0 += stride) {
+    float t[kH1Unroll][4];
+#pragma unroll
+    for (int u = 0; u < kH1Unroll; ++u)
+      h1_item<MODE, XT, FROM_T>(x, base, aux, tin, tout, decoded, (i0 + u * kThreads + threadIdx.x) * 4, total,
+                                vec != 0, t[u]);
+#pragma unroll
+    for (int u = 0; u < kH1Unroll; ++u) {
+      const int64_t e = (i0 + u * kThreads + threadIdx.x) * 4;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool ok = e + q < total;
+        tsq += (double)t[u][q] * (double)t[u][q];
+        hist_add(h, key_of(t[u][q]) >> 19, ok);
       }
-      if constexpr (MODE != CC_NAIVE) aa = aux[e];
-      t = target_of<MODE>(xx, bb, aa);
-      tout[e] = t;
-      if constexpr (MODE == CC_NO_FEEDBACK) aux[e] = xx;  // ref' = a*
-      if constexpr (MODE == CC_NAIVE) base[e] = 0.0f;     // base' = dense decode: zero, then scatter
     }
-    if (decoded) decoded[e] = 0.0f;
-    tsq += (double)t * (double)t;
-    hist_add(h, key_of(t) >> 19, true);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kBins; i += kThreads)
@@ -156,7 +208,6 @@ __global__ void __launch_bounds__(1024) k_find(const uint32_t *__restrict__ hist
         const uint32_t rem = need - before;
         if (level == 1) {
           st->b1 = (uint32_t)b;
-          st->cand = 0;
         } else if (level == 2) {
           st->b2 = (uint32_t)b;
         } else {
@@ -171,59 +222,43 @@ __global__ void __launch_bounds__(1024) k_find(const uint32_t *__restrict__ hist
   }
 }
 
-// ---- pass H2: histogram of key[18:7] inside bin b1 + candidate list ----------
-__global__ void __launch_bounds__(kThreads) k_h2(const float *__restrict__ t, int64_t total, const State *st,
-                                                  uint32_t *__restrict__ hist2, uint32_t *__restrict__ cand,
-                                                  int64_t cap, uint32_t *cand_count) {
-  __shared__ uint32_t h[kBins];
-  for (int i = threadIdx.x; i < kBins; i += kThreads) h[i] = 0;
+// ---- passes H2 / H3: histograms of the keys inside the selected prefix ---------
+// H2: key[18:7] of keys with key[30:19] == b1;  H3: key[6:0] of keys with
+// key[30:7] == (b1, b2).  Both re-stream t (8 keys per thread per iteration).
+template <int LEVEL>
+__global__ void __launch_bounds__(kThreads) k_hsub(const float *__restrict__ t, int64_t total, int vec,
+                                                    const State *st, uint32_t *__restrict__ hist) {
+  constexpr int NB = LEVEL == 2 ? kBins : kBins3;
+  __shared__ uint32_t h[NB];
+  for (int i = threadIdx.x; i < NB; i += kThreads) h[i] = 0;
   __syncthreads();
-  const uint32_t b1 = st->b1;
-  const int64_t stride = (int64_t)gridDim.x * kThreads;
-  const int lane = threadIdx.x & 31;
-  for (int64_t e0 = (int64_t)blockIdx.x * kThreads; e0 < total; e0 += stride) {
-    const int64_t e = e0 + threadIdx.x;
-    uint32_t key = 0;
-    bool in = false;
-    if (e < total) {
-      key = key_of(__ldcs(t + e));
-      in = (key >> 19) == b1;
+  const uint32_t prefix = LEVEL == 2 ? st->b1 : ((st->b1 << 12) | st->b2);
+  constexpr int shift = LEVEL == 2 ? 19 : 7;
+  const int64_t nitems = (total + 3) / 4;
+  const int64_t stride = (int64_t)gridDim.x * kThreads * 2;
+  for (int64_t i0 = (int64_t)blockIdx.x * kThreads * 2; i0 < nitems; i0 += stride) {
+    uint32_t key[8];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t e = (i0 + u * kThreads + threadIdx.x) * 4;
+      if (vec && e + 4 <= total) {
+        const float4 v = __ldcs(reinterpret_cast<const float4 *>(t + e));
+        key[4 * u] = key_of(v.x); key[4 * u + 1] = key_of(v.y);
+        key[4 * u + 2] = key_of(v.z); key[4 * u + 3] = key_of(v.w);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) key[4 * u + q] = e + q < total ? key_of(t[e + q]) : 0xffffffffu;
+      }
     }
-    hist_add(h, (key >> 7) & 0xfffu, in);
-    const uint32_t m = __ballot_sync(0xffffffffu, in);
-    if (m) {
-      uint32_t basei = 0;
-      if (lane == 0) basei = atomicAdd(cand_count, (uint32_t)__popc(m));
-      basei = __shfl_sync(0xffffffffu, basei, 0);
-      const uint32_t pos = basei + __popc(m & ((1u << lane) - 1u));
-      if (in && pos < cap) cand[pos] = key;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool in = key[j] != 0xffffffffu && (key[j] >> shift) == prefix;
+      hist_add(h, LEVEL == 2 ? (key[j] >> 7) & 0xfffu : key[j] & 127u, in);
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kBins; i += kThreads)
-    if (h[i]) atomicAdd(&hist2[i], h[i]);
-}
-
-// ---- pass H3: 128-bin histogram of key[6:0] among keys with key>>7 == prefix
-__global__ void __launch_bounds__(kThreads) k_h3(const float *__restrict__ t, int64_t total,
-                                                  const uint32_t *__restrict__ cand, int64_t cap, const State *st,
-                                                  uint32_t *__restrict__ hist3) {
-  __shared__ uint32_t h[kBins3];
-  for (int i = threadIdx.x; i < kBins3; i += kThreads) h[i] = 0;
-  __syncthreads();
-  const uint32_t prefix = (st->b1 << 12) | st->b2;
-  const bool use_cand = st->cand <= cap;
-  const int64_t n = use_cand ? (int64_t)st->cand : total;
-  const int64_t stride = (int64_t)gridDim.x * kThreads;
-  for (int64_t e0 = (int64_t)blockIdx.x * kThreads; e0 < n; e0 += stride) {
-    const int64_t e = e0 + threadIdx.x;
-    uint32_t key = 0;
-    if (e < n) key = use_cand ? cand[e] : key_of(t[e]);
-    hist_add(h, key & 127u, e < n && (key >> 7) == prefix);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kBins3; i += kThreads)
-    if (h[i]) atomicAdd(&hist3[i], h[i]);
+  for (int i = threadIdx.x; i < NB; i += kThreads)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
 // ---- pass C: per-chunk counts ------------------------------------------------
@@ -327,6 +362,11 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t &excl, 
 }
 
 // ---- pass W: ordered write + sparse state update ------------------------------
+// Each CTA stages its 8192-element chunk in shared memory (coalesced), every
+// thread owns a run of 32 consecutive elements: two block scans per chunk give the
+// tie ranks and the output slots, then each thread emits its selected elements in
+// index order.  (Run index i of thread r lives at smem[33 r + i]: conflict-free.)
+constexpr int kRun = kChunk / kThreads;  // 32
 template <int MODE, typename XT>
 __global__ void __launch_bounds__(kThreads) k_write(const float *__restrict__ t, const XT *__restrict__ x,
                                                      float *__restrict__ base, float *__restrict__ aux,
@@ -334,50 +374,63 @@ __global__ void __launch_bounds__(kThreads) k_write(const float *__restrict__ t,
                                                      const State *st, const uint32_t *__restrict__ sel_pref,
                                                      const uint32_t *__restrict__ eq_pref, uint8_t *__restrict__ body,
                                                      double *__restrict__ part, int stateful) {
+  __shared__ float tv_s[kThreads * (kRun + 1)];
   __shared__ uint32_t sm[kThreads / 32];
   __shared__ double red[kThreads / 32];
   const uint32_t T = st->T, ties = st->ties;
   const int64_t c0 = (int64_t)blockIdx.x * kChunk;
   const int64_t c1 = min64(total, c0 + kChunk);
-  uint32_t sel_run = sel_pref[blockIdx.x], eq_run = eq_pref[blockIdx.x];
+  for (int64_t e = c0 + threadIdx.x; e < c0 + kChunk; e += kThreads) {
+    const int i = (int)(e - c0);
+    tv_s[(i / kRun) * (kRun + 1) + i % kRun] = e < c1 ? __ldcs(t + e) : 0.0f;
+  }
+  __syncthreads();
+  const float *run = tv_s + threadIdx.x * (kRun + 1);
+  const int64_t e_run = c0 + (int64_t)threadIdx.x * kRun;
+  const int64_t rem = c1 - e_run;
+  const int valid = rem <= 0 ? 0 : (int)min64(kRun, rem);
+  uint32_t n_eq = 0, n_gt = 0;
+  for (int i = 0; i < valid; ++i) {
+    const uint32_t key = key_of(run[i]);
+    n_eq += key == T;
+    n_gt += key > T;
+  }
+  uint32_t eq_ex;
+  block_excl_scan(n_eq, eq_ex, sm);
+  uint32_t tie_rank = eq_pref[blockIdx.x] + eq_ex;  // ties before this run
+  const uint32_t ties_here = tie_rank < ties ? min(n_eq, ties - tie_rank) : 0u;
+  uint32_t sel_ex;
+  block_excl_scan(n_gt + ties_here, sel_ex, sm);
+  uint32_t pos = sel_pref[blockIdx.x] + sel_ex;
   uint32_t *idx_out = reinterpret_cast<uint32_t *>(body);
   __half *val_out = reinterpret_cast<__half *>(body + 4 * k);
   double adj = 0.0;  // sum over selected of (d - t)^2 - t^2
-  for (int64_t e0 = c0; e0 < c1; e0 += kThreads) {
-    const int64_t e = e0 + threadIdx.x;
-    float tv = 0.f;
-    uint32_t key = 0;
-    const bool ok = e < c1;
-    if (ok) {
-      tv = t[e];
-      key = key_of(tv);
+  for (int i = 0; i < valid; ++i) {
+    const float tv = run[i];
+    const uint32_t key = key_of(tv);
+    bool sel = key > T;
+    if (key == T) {
+      sel = tie_rank < ties;
+      ++tie_rank;
     }
-    const uint32_t is_eq = ok && key == T;
-    uint32_t eq_ex;
-    const uint32_t eq_tot = block_excl_scan(is_eq, eq_ex, sm);
-    const bool sel = ok && (key > T || (is_eq && eq_run + eq_ex < ties));
-    uint32_t sel_ex;
-    const uint32_t sel_tot = block_excl_scan(sel ? 1u : 0u, sel_ex, sm);
-    if (sel) {
-      const uint32_t pos = sel_run + sel_ex;
-      idx_out[pos] = (uint32_t)e;
-      const __half h = __float2half_rn(tv);
-      val_out[pos] = h;
-      const float d = __half2float(h);
-      const double df = (double)d - (double)tv;
-      adj += df * df - (double)tv * (double)tv;
-      if (decoded) decoded[e] = d;
-      if (stateful) {
-        if constexpr (MODE == CC_NAIVE) {
-          base[e] = d;
-        } else {
-          base[e] = __fadd_rn(base[e], d);
-          if constexpr (MODE == CC_WITH_FEEDBACK) aux[e] = __fsub_rn(tv, d);
-        }
+    if (!sel) continue;
+    const int64_t e = e_run + i;
+    idx_out[pos] = (uint32_t)e;
+    const __half h = __float2half_rn(tv);
+    val_out[pos] = h;
+    ++pos;
+    const float d = __half2float(h);
+    const double df = (double)d - (double)tv;
+    adj += df * df - (double)tv * (double)tv;
+    if (decoded) decoded[e] = d;
+    if (stateful) {
+      if constexpr (MODE == CC_NAIVE) {
+        base[e] = d;
+      } else {
+        base[e] = __fadd_rn(base[e], d);
+        if constexpr (MODE == CC_WITH_FEEDBACK) aux[e] = __fsub_rn(tv, d);
       }
     }
-    sel_run += sel_tot;
-    eq_run += eq_tot;
   }
   adj = warp_sum(adj);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = adj;
@@ -391,15 +444,28 @@ __global__ void __launch_bounds__(kThreads) k_write(const float *__restrict__ t,
   (void)x;
 }
 
-__global__ void k_record(int nparts, const double *__restrict__ part, double *__restrict__ record) {
-  if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (int i = 0; i < nparts; ++i) {
-      a += part[2 * i];
-      b += part[2 * i + 1];
+// fixed-order tree reduction of the (adj, ||t||^2) partials (one CTA)
+__global__ void __launch_bounds__(1024) k_record(int nparts, const double *__restrict__ part,
+                                                 double *__restrict__ record) {
+  __shared__ double sa[1024], sb[1024];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += 1024) {
+    a += part[2 * i];
+    b += part[2 * i + 1];
+  }
+  sa[threadIdx.x] = a;
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  for (int s2 = 512; s2 > 0; s2 >>= 1) {
+    if (threadIdx.x < s2) {
+      sa[threadIdx.x] += sa[threadIdx.x + s2];
+      sb[threadIdx.x] += sb[threadIdx.x + s2];
     }
-    record[0] = b + a;  // ||t||^2 + sum_sel((d-t)^2 - t^2) = ||d - t||^2
-    record[1] = b;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    record[0] = sb[0] + sa[0];  // ||t||^2 + sum_sel((d-t)^2 - t^2) = ||d - t||^2
+    record[1] = sb[0];
   }
 }
 
@@ -453,13 +519,11 @@ static topk::Work carve_topk(void *ws, int64_t total, bool need_t, int nH1, size
   };
   w.nH1 = nH1;
   w.nChunks = cdiv(total, topk::kChunk);
-  w.cap = std::max<int64_t>(65536, total / 16);
   // zeroed region first: hist1, hist2, hist3, state
   w.hist1 = reinterpret_cast<uint32_t *>(take(4 * topk::kBins));
   w.hist2 = reinterpret_cast<uint32_t *>(take(4 * topk::kBins));
   w.hist3 = reinterpret_cast<uint32_t *>(take(4 * topk::kBins3));
   w.st = reinterpret_cast<topk::State *>(take(sizeof(topk::State)));
-  w.cand = reinterpret_cast<uint32_t *>(take(4 * w.cap));
   w.cnt_gt = reinterpret_cast<uint32_t *>(take(4 * w.nChunks));
   w.cnt_eq = reinterpret_cast<uint32_t *>(take(4 * w.nChunks));
   w.sel_pref = reinterpret_cast<uint32_t *>(take(4 * w.nChunks));
@@ -470,7 +534,10 @@ static topk::Work carve_topk(void *ws, int64_t total, bool need_t, int nH1, size
   return w;
 }
 
-static int h1_blocks(int64_t total) { return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), sm_count() * 4)); }
+static bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// histogram passes: few, fat CTAs (each zeroes / flushes a 4096-bin shared histogram)
+static int h1_blocks(int64_t total) { return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), sm_count() * 2)); }
 
 int64_t topk_workspace_bytes(int64_t n, int64_t C, int64_t) {
   size_t b = 0;
@@ -486,17 +553,18 @@ static void select_and_write(const topk::Work &w, const float *t, const XT *x, f
                              float *decoded, int64_t total, int64_t k, uint8_t *body, double *record, int stateful,
                              cudaStream_t st) {
   using namespace topk;
-  const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, kThreads), sm_count() * 8));
+  const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, kThreads), sm_count() * 2));
   k_find<kBins><<<1, 1024, 0, st>>>(w.hist1, w.st, 1, (uint32_t)k);
-  k_h2<<<nb, kThreads, 0, st>>>(t, total, w.st, w.hist2, w.cand, w.cap, &w.st->cand);
+  const int vec = al16(t);
+  k_hsub<2><<<nb, kThreads, 0, st>>>(t, total, vec, w.st, w.hist2);
   k_find<kBins><<<1, 1024, 0, st>>>(w.hist2, w.st, 2, 0);
-  k_h3<<<nb, kThreads, 0, st>>>(t, total, w.cand, w.cap, w.st, w.hist3);
+  k_hsub<3><<<nb, kThreads, 0, st>>>(t, total, vec, w.st, w.hist3);
   k_find<kBins3><<<1, 1024, 0, st>>>(w.hist3, w.st, 3, 0);
   k_count<<<(unsigned)w.nChunks, kThreads, 0, st>>>(t, total, w.st, w.cnt_gt, w.cnt_eq);
   k_scan<<<1, 1024, 0, st>>>(w.nChunks, w.st, w.cnt_gt, w.cnt_eq, w.sel_pref, w.eq_pref);
   k_write<MODE, XT><<<(unsigned)w.nChunks, kThreads, 0, st>>>(t, x, base, aux, decoded, total, k, w.st, w.sel_pref,
                                                              w.eq_pref, body, w.part + 2 * w.nH1, stateful);
-  k_record<<<1, 32, 0, st>>>((int)(w.nH1 + w.nChunks), w.part, record);
+  k_record<<<1, 1024, 0, st>>>((int)(w.nH1 + w.nChunks), w.part, record);
   count_launch(9);
 }
 
@@ -514,7 +582,7 @@ int topk_encode(int64_t n, int64_t C, int64_t k, const float *t, uint8_t *body, 
   double *record = reinterpret_cast<double *>(reinterpret_cast<uint8_t *>(ws) + need);
   cudaMemsetAsync(ws, 0, kZeroBytes, st);
   topk::k_h1<CC_NAIVE, float, true><<<nH1, topk::kThreads, 0, st>>>(nullptr, nullptr, nullptr, t, nullptr, decoded,
-                                                                    total, w.hist1, w.part);
+                                                                    total, al16(t) && al16(decoded), w.hist1, w.part);
   count_launch();
   select_and_write<CC_NAIVE, float>(w, t, nullptr, nullptr, nullptr, decoded, total, k, body, record, 0, st);
   return cuda_status("topk_encode");
@@ -533,11 +601,13 @@ int topk_encode_step(int mode, int64_t n, int64_t C, int64_t k, const void *x, i
   }
   topk::Work w = carve_topk(ws, total, need_t, nH1, nullptr);
   float *t = mode == CC_WITH_FEEDBACK ? aux : w.tscratch;
+  const int vec = al16(t) && al16(base) && al16(aux) &&
+                  (reinterpret_cast<uintptr_t>(x) & (x_dtype == CC_BF16 ? 7 : 15)) == 0;
   cudaMemsetAsync(ws, 0, kZeroBytes, st);
 #define CC_TK(MODE, XT)                                                                                      \
   do {                                                                                                       \
     topk::k_h1<MODE, XT, false><<<nH1, topk::kThreads, 0, st>>>((const XT *)x, base, aux, nullptr, t, nullptr, \
-                                                                total, w.hist1, w.part);                    \
+                                                                total, vec, w.hist1, w.part);               \
     count_launch();                                                                                          \
     select_and_write<MODE, XT>(w, t, (const XT *)x, base, aux, nullptr, total, k, body, record, 1, st);      \
   } while (0)

@@ -1,2 +1,3 @@
 set -x
-timeout 600 python bench.py > gpurun_out/bench7.json 2> gpurun_out/bench7.err; tail -5 gpurun_out/bench7.err; cat gpurun_out/bench7.json
+timeout 900 python -m pytest tests/test_gpu_topk.py tests/test_gpu_lowrank.py -x -q 2>&1 | tail -15
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/codec_trace2.csv python scripts/codec_trace.py > /dev/null 2>&1; echo ncu=$?
