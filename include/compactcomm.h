@@ -24,6 +24,9 @@
  *   CC_TOPK    k x u32 ascending flat indices, then k x f16 values (cx:446-456, 601)
  *   CC_LOWRANK U [n,r] then W [C,r], column-major f16           (cx:415-426, 591)
  *   CC_LOWRANK4 2r f32 ranges, then one nibble stream U then W col-major (cx:592-595)
+ *   CC_NMBLOCK ceil(blocks*m/8) B keep-mask (m bits per 1 x m block of the
+ *              column-padded matrix, little bit order), then n f16 values per
+ *              block in index order                            (cx:429-443, 596)
  *   CC_RAW     n*C f32 (wire may carry bf16 when inputs are bf16: lossless)
  */
 #ifndef COMPACTCOMM_H
@@ -71,10 +74,15 @@ extern "C" {
 #define CC_SCALE_PER_TOKEN 1
 #define CC_SCALE_PER_CHANNEL 2
 
+/* `param` of the N:M codec: n (kept per block) and m (block width), 1 <= n <= m
+ * <= 65535 — the frame meta <HH n, m> of cx:596-597. */
+#define CC_NM_PARAM(n, m) ((((int64_t)(n)) << 16) | (int64_t)(m))
+
 /* ---- sizes -------------------------------------------------------------- */
 
 /* Exact body size in bytes: ceil(bit_size/8) (cx:195-348). param = rank for
- * low-rank, k for top-k, ignored otherwise.  Returns <0 on bad arguments. */
+ * low-rank, k for top-k, CC_NM_PARAM(n, m) for N:M, ignored otherwise.
+ * Returns <0 on bad arguments. */
 CC_API int64_t cc_body_bytes(int codec, int64_t rows, int64_t cols, int64_t param);
 
 /* Device scratch bytes needed by cc_encode_step for this codec/shape. */
@@ -152,6 +160,18 @@ CC_API int cc_topk_encode(int64_t rows, int64_t cols, int64_t k, const float *t,
 CC_API int cc_topk_encode_step(int mode, int64_t rows, int64_t cols, int64_t k, const void *x, int x_dtype,
                                float *base, float *aux, uint8_t *body, void *workspace,
                                int64_t workspace_bytes, double *record, void *stream);
+
+/* ---- N:M block sparsifier (cx:429-443) ----------------------------------------
+ * Keep the n largest-|t| entries of every 1 x m column block (ties -> lowest
+ * index), columns zero-padded to a multiple of m.  One pass: the selection is
+ * block-local.  cc_nm_encode_step fuses target -> select -> body -> state update
+ * + record (pl:99-120); receivers decode with cc_decode_step(CC_NMBLOCK,
+ * accumulate, ..., CC_NM_PARAM(n, m)) (accumulate = dense base + decode). */
+CC_API int cc_nm_encode(int64_t rows, int64_t cols, int n, int m, const float *t, uint8_t *body,
+                        float *decoded, void *workspace, int64_t workspace_bytes, void *stream);
+CC_API int cc_nm_encode_step(int mode, int64_t rows, int64_t cols, int n, int m, const void *x, int x_dtype,
+                             float *base, float *aux, uint8_t *body, void *workspace,
+                             int64_t workspace_bytes, double *record, void *stream);
 
 /* ---- low-rank (cx:394-426) -------------------------------------------------
  * q0: [cols, r] f32 initial Gaussian block (drawn host-side from the same

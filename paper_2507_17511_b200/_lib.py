@@ -23,6 +23,11 @@ CC_NAIVE, CC_NO_FEEDBACK, CC_WITH_FEEDBACK = 0, 1, 2
 CC_F32, CC_BF16 = 0, 1
 CC_SCALE_RANK1, CC_SCALE_PER_TOKEN, CC_SCALE_PER_CHANNEL = 0, 1, 2
 
+
+def nm_param(n, m):
+    """CC_NM_PARAM(n, m) of include/compactcomm.h."""
+    return (int(n) << 16) | int(m)
+
 _i64, _i32, _p, _d = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_double
 
 SIGNATURES = {
@@ -39,6 +44,8 @@ SIGNATURES = {
     "cc_topk_count": (_i64, [_i64, _i64, _d]),
     "cc_topk_encode": (_i32, [_i64, _i64, _i64, _p, _p, _p, _p, _i64, _p]),
     "cc_topk_encode_step": (_i32, [_i32, _i64, _i64, _i64, _p, _i32, _p, _p, _p, _p, _i64, _p, _p]),
+    "cc_nm_encode": (_i32, [_i64, _i64, _i32, _i32, _p, _p, _p, _p, _i64, _p]),
+    "cc_nm_encode_step": (_i32, [_i32, _i64, _i64, _i32, _i32, _p, _i32, _p, _p, _p, _p, _i64, _p, _p]),
     "cc_lowrank_encode": (_i32, [_i32, _i64, _i64, _i64, _i32, _p, _p, _p, _p, _p, _i64, _p]),
     "cc_lowrank_workspace_bytes": (_i64, [_i64, _i64, _i64]),
     "cc_last_error": (ctypes.c_char_p, []),

@@ -57,6 +57,8 @@ def codec_tag(spec):
         return tag
     if k == cx.CompressorKind.TOPK:
         return _lib.CC_TOPK
+    if k == cx.CompressorKind.NM_BLOCK:
+        return _lib.CC_NMBLOCK
     if k == cx.CompressorKind.LOWRANK:
         return _lib.CC_LOWRANK4 if spec.int4_factors else _lib.CC_LOWRANK
     if k == cx.CompressorKind.IDENTITY:
@@ -70,6 +72,8 @@ def codec_param(spec, rows, cols):
         return cx.topk_count(rows, cols, spec.keep_fraction)
     if tag in (_lib.CC_LOWRANK, _lib.CC_LOWRANK4):
         return spec.rank
+    if tag == _lib.CC_NMBLOCK:
+        return _lib.nm_param(spec.n, spec.m)
     return 0
 
 
@@ -87,6 +91,9 @@ def body_bytes_for(spec, rows, cols):
         return (2 * s + 7) // 8 + 4 * (rows + cols)
     if tag == _lib.CC_QUANT4:
         return (4 * s + 7) // 8 + 4 * (rows + cols)
+    if tag == _lib.CC_NMBLOCK:
+        blocks = rows * (-(-cols // spec.m))
+        return -(-blocks * spec.m // 8) + 2 * blocks * spec.n
     if tag == _lib.CC_LOWRANK:
         return 2 * spec.rank * (rows + cols)
     if tag == _lib.CC_LOWRANK4:

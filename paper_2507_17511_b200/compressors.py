@@ -331,6 +331,49 @@ class TopKPayload(_Payload):
         return self.body[4 * self.k: 6 * self.k].clone().view(torch.float16)
 
 
+class NMBlockPayload(_Payload):
+    """N:M block payload (cx:291-329): body = packed keep-mask + f16 values."""
+
+    tag = TAG_NMBLOCK
+    kind_label = "nmblock"
+
+    def __init__(self, rows, cols, body, n, m):
+        super().__init__(rows, cols, body)
+        self.n = int(n)
+        self.m = int(m)
+
+    @property
+    def padded_cols(self):
+        return -(-self.cols // self.m) * self.m
+
+    @property
+    def block_count(self):
+        return self.rows * (self.padded_cols // self.m)
+
+    @property
+    def mask_bytes(self):
+        return -(-self.block_count * self.m // 8)
+
+    @property
+    def bit_size(self):
+        return self.block_count * (self.m + 16 * self.n)  # cx:318-319
+
+    @property
+    def payload_only_bits(self):
+        return self.block_count * 16 * self.n
+
+    def _param(self):
+        return _lib.nm_param(self.n, self.m)
+
+    @property
+    def masks(self):
+        return self.body[: self.mask_bytes]
+
+    @property
+    def values(self):
+        return self.body[self.mask_bytes:].clone().view(torch.float16)
+
+
 class LowRankPayload(_Payload):
     kind_label = "lowrank"
 
@@ -426,6 +469,26 @@ def encode_topk(x, keep_fraction, decoded=None):
     return TopKPayload(rows, cols, body[: 6 * k], k)
 
 
+def nm_body_bytes(rows, cols, n, m):
+    return _lib.check(_lib.load().cc_body_bytes(_lib.CC_NMBLOCK, rows, cols, _lib.nm_param(n, m)))
+
+
+def encode_nm_block(x, n, m, decoded=None):
+    """Keep the n largest-|value| entries of every 1 x m column block (cx:429-443)."""
+    if not (1 <= n <= m):
+        raise ValueError("need 1 <= n <= m")
+    if m > 65535:
+        raise ValueError("m must fit the u16 frame meta (cx:596)")
+    t = as_device_matrix(x, torch.float32)
+    rows, cols = t.shape
+    lib = _lib.load()
+    body = _empty_body(nm_body_bytes(rows, cols, n, m))
+    ws = workspace(_lib.check(lib.cc_workspace_bytes(_lib.CC_NMBLOCK, rows, cols, _lib.nm_param(n, m))), "nm")
+    _lib.check(lib.cc_nm_encode(rows, cols, n, m, _lib.ptr(t), _lib.ptr(body), _lib.ptr(decoded), _lib.ptr(ws),
+                                ws.numel(), _lib.stream_ptr()), "encode_nm_block")
+    return NMBlockPayload(rows, cols, body, n, m)
+
+
 def subspace_init(rng, cols, rank):
     """Host draw of the initial block Q0 ~ N(0,1)[cols, r] (cx:407 / la:67-74)."""
     from .linalg import gaussian_matrix
@@ -467,7 +530,7 @@ def encode(x, spec, rng=None):
     if k == CompressorKind.TOPK:
         return encode_topk(x, spec.keep_fraction)
     if k == CompressorKind.NM_BLOCK:
-        raise NotImplementedError("nm_block is outside the B200 hot path (SURVEY §8f, rank 1 next)")
+        return encode_nm_block(x, spec.n, spec.m)
     raise ValueError(f"unknown codec kind {k}")
 
 
@@ -518,6 +581,8 @@ def to_bytes(p):
         head += struct.pack("<I", p.rank)
     elif p.tag == TAG_TOPK:
         head += struct.pack("<I", p.kept)
+    elif p.tag == TAG_NMBLOCK:
+        head += struct.pack("<HH", p.n, p.m)  # cx:596-597
     return head + p.body_bytes()
 
 
@@ -589,8 +654,21 @@ def from_bytes(buf):
             if k and int(idx.max()) >= rows * cols:
                 raise PayloadError("topk: index out of range")
             return TopKPayload(rows, cols, dev(rest), k)
-        if tag == TAG_NMBLOCK:
-            raise PayloadError("nmblock: codec not built on the B200 path")
+        if tag == TAG_NMBLOCK:  # cx:658-674
+            if len(body) < 4:
+                raise PayloadError("nmblock: missing n:m meta")
+            n, m = struct.unpack_from("<HH", body, 0)
+            if not (1 <= n <= m):
+                raise PayloadError("nmblock: bad n:m")
+            rest = body[4:]
+            blocks = rows * (-(-cols // m))
+            mask_bytes = -(-blocks * m // 8)
+            if len(rest) < mask_bytes or (len(rest) - mask_bytes) % 2 or (len(rest) - mask_bytes) // 2 != blocks * n:
+                raise PayloadError("nmblock: truncated body")
+            masks = np.frombuffer(rest, np.uint8, mask_bytes, 0)
+            if int(np.unpackbits(masks, count=blocks * m, bitorder="little").sum()) != blocks * n:
+                raise PayloadError("nmblock: mask popcount mismatch")
+            return NMBlockPayload(rows, cols, dev(rest), n, m)
     except PayloadError:
         raise
     except Exception as exc:  # struct errors, bad slices

@@ -53,6 +53,14 @@ int lowrank_encode(int int4, int64_t n, int64_t C, int64_t r, int iters, const f
                    uint8_t *body, float *decoded, void *ws, int64_t ws_bytes, cudaStream_t st);
 int lowrank_decode(int int4, int count, const int64_t *rows, int64_t C, int64_t r, const uint8_t *const *bodies,
                    int accumulate, float *const *bases, cudaStream_t st);
+int64_t nm_body_bytes(int64_t rows, int64_t C, int n, int m);
+int64_t nm_workspace_bytes(int64_t rows, int64_t C, int n, int m);
+int nm_encode(int64_t rows, int64_t C, int n, int m, const float *t, uint8_t *body, float *decoded, void *ws,
+              int64_t ws_bytes, cudaStream_t st);
+int nm_encode_step(int mode, int64_t rows, int64_t C, int n, int m, const void *x, int x_dtype, float *base,
+                   float *aux, uint8_t *body, void *ws, int64_t ws_bytes, double *record, cudaStream_t st);
+int nm_decode(int count, const int64_t *rows, int64_t C, int n, int m, const uint8_t *const *bodies, int accumulate,
+              float *const *bases, cudaStream_t st);
 void set_quant_path(int v);
 void set_fused_stop(int v);
 void set_fused_timer(void *buf);
@@ -69,6 +77,11 @@ int apply_decoded(int mode, int64_t n, int64_t C, const void *x, int x_dtype, co
 using namespace cc;
 
 static bool quant_codec(int c) { return c == CC_SIGN1 || c == CC_QUANT2 || c == CC_QUANT4; }
+static bool nm_split(int64_t param, int *n, int *m) {
+  *n = (int)(param >> 16);
+  *m = (int)(param & 0xffff);
+  return param >= 0 && (param >> 32) == 0 && *n >= 1 && *n <= *m;
+}
 static bool valid_mode(int m) { return m == CC_NAIVE || m == CC_NO_FEEDBACK || m == CC_WITH_FEEDBACK; }
 
 extern "C" {
@@ -103,6 +116,10 @@ CC_API int64_t cc_body_bytes(int codec, int64_t rows, int64_t cols, int64_t para
     case CC_LOWRANK: return param < 1 ? CC_ERR_ARG : 2 * param * (rows + cols);
     case CC_LOWRANK4: return param < 1 ? CC_ERR_ARG : (4 * param * (rows + cols) + 7) / 8 + 8 * param;
     case CC_TOPK: return param < 0 ? CC_ERR_ARG : 6 * param;
+    case CC_NMBLOCK: {
+      int n, m;
+      return nm_split(param, &n, &m) ? nm_body_bytes(rows, cols, n, m) : CC_ERR_ARG;
+    }
     default: return CC_ERR_ARG;
   }
 }
@@ -112,6 +129,10 @@ CC_API int64_t cc_workspace_bytes(int codec, int64_t rows, int64_t cols, int64_t
   if (quant_codec(codec)) return quant_workspace_bytes(rows, cols) + 256;
   if (codec == CC_TOPK) return topk_workspace_bytes(rows, cols, param);
   if (codec == CC_LOWRANK || codec == CC_LOWRANK4) return lowrank_workspace_bytes(rows, cols, param);
+  if (codec == CC_NMBLOCK) {
+    int n, m;
+    return nm_split(param, &n, &m) ? nm_workspace_bytes(rows, cols, n, m) : CC_ERR_ARG;
+  }
   if (codec == CC_RAW) return 0;
   return CC_ERR_ARG;
 }
@@ -149,6 +170,11 @@ CC_API int cc_decode_batched(int codec, int accumulate, int count, const int64_t
   if (codec == CC_RAW) return raw_decode(count, rows, cols, reinterpret_cast<const void *const *>(bodies), body_dtype, bases, st);
   if (quant_codec(codec)) return quant_decode(codec, accumulate, count, rows, cols, bodies, bases, st);
   if (codec == CC_TOPK) return topk_decode(count, rows, cols, param, bodies, accumulate, bases, st);
+  if (codec == CC_NMBLOCK) {
+    int n, m;
+    if (!nm_split(param, &n, &m)) { set_error("bad n:m"); return CC_ERR_ARG; }
+    return nm_decode(count, rows, cols, n, m, bodies, accumulate, bases, st);
+  }
   if (codec == CC_LOWRANK || codec == CC_LOWRANK4)
     return lowrank_decode(codec == CC_LOWRANK4, count, rows, cols, param, bodies, accumulate, bases, st);
   set_error("unsupported codec");
@@ -204,6 +230,24 @@ CC_API int cc_topk_encode_step(int mode, int64_t rows, int64_t cols, int64_t k, 
                           (cudaStream_t)stream);
 }
 
+CC_API int cc_nm_encode(int64_t rows, int64_t cols, int n, int m, const float *t, uint8_t *body, float *decoded,
+                        void *workspace, int64_t workspace_bytes, void *stream) {
+  if (rows < 1 || cols < 1) { set_error("empty shape"); return CC_ERR_SHAPE; }
+  if (!(1 <= n && n <= m && m <= 65535) || !t || !body) { set_error("need 1 <= n <= m <= 65535"); return CC_ERR_ARG; }
+  return nm_encode(rows, cols, n, m, t, body, decoded, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+CC_API int cc_nm_encode_step(int mode, int64_t rows, int64_t cols, int n, int m, const void *x, int x_dtype,
+                             float *base, float *aux, uint8_t *body, void *workspace, int64_t workspace_bytes,
+                             double *record, void *stream) {
+  if (rows < 1 || cols < 1) { set_error("empty shape"); return CC_ERR_SHAPE; }
+  if (!valid_mode(mode) || (x_dtype != CC_F32 && x_dtype != CC_BF16)) { set_error("bad mode/dtype"); return CC_ERR_ARG; }
+  if (!(1 <= n && n <= m && m <= 65535)) { set_error("need 1 <= n <= m <= 65535"); return CC_ERR_ARG; }
+  if (!x || !base || !body || !record || (mode != CC_NAIVE && !aux)) { set_error("null pointer"); return CC_ERR_ARG; }
+  return nm_encode_step(mode, rows, cols, n, m, x, x_dtype, base, aux, body, workspace, workspace_bytes, record,
+                        (cudaStream_t)stream);
+}
+
 CC_API int64_t cc_lowrank_workspace_bytes(int64_t rows, int64_t cols, int64_t rank) {
   if (rows < 1 || cols < 1) return CC_ERR_SHAPE;
   if (rank < 1 || rank > (rows < cols ? rows : cols)) return CC_ERR_SHAPE;
@@ -235,6 +279,11 @@ CC_API int cc_encode(int codec, int scale_mode, int64_t rows, int64_t cols, int6
                              workspace, wsq, rec, st);
   }
   if (codec == CC_TOPK) return topk_encode(rows, cols, param, t, body, decoded, workspace, workspace_bytes, st);
+  if (codec == CC_NMBLOCK) {
+    int n, m;
+    if (!nm_split(param, &n, &m)) { set_error("bad n:m"); return CC_ERR_ARG; }
+    return nm_encode(rows, cols, n, m, t, body, decoded, workspace, workspace_bytes, st);
+  }
   set_error("cc_encode: use cc_lowrank_encode for low-rank");
   return CC_ERR_UNSUPPORTED;
 }

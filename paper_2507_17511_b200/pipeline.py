@@ -160,6 +160,16 @@ def encode_step(state, a_star, codec, rng=None, body_out=None):
                                                _lib.ptr(state.base), _lib.ptr(aux), _lib.ptr(body), _lib.ptr(ws),
                                                ws.numel(), _lib.ptr(rec), stream), "topk encode_step")
             payload = cx.TopKPayload(rows, cols, body, k)
+        elif kind == cx.CompressorKind.NM_BLOCK:
+            n, m = codec.n, codec.m
+            nbytes = cx.nm_body_bytes(rows, cols, n, m)
+            body = body_out[:nbytes] if body_out is not None else cx._empty_body(nbytes)
+            ws = cx.workspace(_lib.check(lib.cc_workspace_bytes(_lib.CC_NMBLOCK, rows, cols, _lib.nm_param(n, m))),
+                              "nm")
+            _lib.check(lib.cc_nm_encode_step(mode, rows, cols, n, m, _lib.ptr(x), cx.dtype_code(x),
+                                             _lib.ptr(state.base), _lib.ptr(aux), _lib.ptr(body), _lib.ptr(ws),
+                                             ws.numel(), _lib.ptr(rec), stream), "nm encode_step")
+            payload = cx.NMBlockPayload(rows, cols, body, n, m)
         elif tag is not None:
             nbytes = lib.cc_body_bytes(tag, rows, cols, 0)
             body = body_out[:nbytes] if body_out is not None else cx._empty_body(nbytes)

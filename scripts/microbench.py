@@ -144,6 +144,32 @@ def main():
         pl.encode_step(st, xs[1], sp)
         us = timed(lambda i: pl.encode_step(st, xs[i % 2], sp), 10)
         out[f"topk_step_{f}"] = {"us": round(us, 1)}
+    # N:M encode_step (one fused pass) and its K2 decode, L2-cold layer rotation
+    for (nn, mm) in ((2, 4), (1, 4), (4, 8), (8, 16), (16, 32), (3, 5)):
+        prm = _lib.nm_param(nn, mm)
+        nb = lib.cc_body_bytes(_lib.CC_NMBLOCK, n, c, prm)
+        nbody = torch.empty(nb + 64, dtype=torch.uint8, device="cuda")
+        nws_b = lib.cc_workspace_bytes(_lib.CC_NMBLOCK, n, c, prm)
+        nws = torch.empty(max(nws_b, 1), dtype=torch.uint8, device="cuda")
+
+        def nenc(i, nn=nn, mm=mm, nbody=nbody, nws=nws, nws_b=nws_b):
+            st = sts[i % L]
+            lib.cc_nm_encode_step(2, n, c, nn, mm, _lib.ptr(xs[2 * (i % L) + (i // L) % 2]), _lib.CC_BF16,
+                                  _lib.ptr(st.base), _lib.ptr(st.feedback), _lib.ptr(nbody), _lib.ptr(nws), nws_b,
+                                  _lib.ptr(rec), stream)
+
+        for i in range(L):
+            nenc(i)
+        us = timed(nenc, a.reps)
+        alg_nm = n * c * 18 + nb
+        out[f"nm{nn}:{mm}_step"] = {"us": round(us, 2), "alg_GBps": round(alg_nm / us / 1e3, 1)}
+
+        def ndec(i, prm=prm, nbody=nbody):
+            lib.cc_decode_step(_lib.CC_NMBLOCK, 1, n, c, prm, _lib.ptr(nbody), _lib.CC_F32,
+                               _lib.ptr(bases[i % L]), stream)
+
+        us = timed(ndec, a.reps)
+        out[f"nm{nn}:{mm}_decode"] = {"us": round(us, 2), "alg_GBps": round((n * c * 8 + nb) / us / 1e3, 1)}
     # plain copy roofline reference: base -> feedback of another layer
     def cp(i):
         sts[(i + 1) % L].feedback.copy_(sts[i % L].base)

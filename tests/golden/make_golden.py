@@ -10,6 +10,7 @@ decode_step / message_for) on seeded inputs, and writes:
 
   tests/golden/codec_cases.npz      per-codec KAT + random cases: input, body, decode
   tests/golden/traj_small.npz       full per-step bodies/base/fb for small trajectories
+  tests/golden/traj_nm.npz          the same for the N:M block sparsifier
   tests/golden/manifest.json        digests for every case, incl. FLUX-width trajectories
 
 The fixtures are the parity anchor for both the oracle (tests/test_oracle_golden.py)
@@ -62,6 +63,14 @@ CODEC_SPECS = {
     "lowrank-r3-f16": S(K.LOWRANK, rank=3, iterations=2),
     "lowrank-r3-int4": S(K.LOWRANK, rank=3, iterations=2, int4_factors=True),
     "nm2:4": S(K.NM_BLOCK, n=2, m=4),
+    "nm1:4": S(K.NM_BLOCK, n=1, m=4),
+    "nm1:2": S(K.NM_BLOCK, n=1, m=2),
+    "nm4:8": S(K.NM_BLOCK, n=4, m=8),
+    "nm8:16": S(K.NM_BLOCK, n=8, m=16),
+    "nm5:32": S(K.NM_BLOCK, n=5, m=32),
+    "nm3:5": S(K.NM_BLOCK, n=3, m=5),      # generic (non power-of-two) path
+    "nm7:40": S(K.NM_BLOCK, n=7, m=40),    # generic (m > 32) path
+    "nm4:4": S(K.NM_BLOCK, n=4, m=4),      # keep everything
 }
 
 
@@ -147,6 +156,8 @@ TRAJ_SMALL = [
     ("t37x100", 37, 100, 6, 22, 2),
 ]
 TRAJ_CODECS = {"sign1bit": SIGN, "quant2bit": Q2}
+NM_TRAJ_CODECS = {"nm2:4": S(K.NM_BLOCK, n=2, m=4), "nm3:5": S(K.NM_BLOCK, n=3, m=5),
+                  "nm4:16": S(K.NM_BLOCK, n=4, m=16)}
 MODES = ["naive", "residual_no_feedback", "residual_with_feedback"]
 
 
@@ -172,6 +183,45 @@ def build_traj_fixture(out):
                              "inputs_sha256": synth.digest(np.stack(xs))})
     np.savez_compressed(os.path.join(HERE, "traj_small.npz"), **arrays)
     out["traj_small"] = meta
+
+
+def build_nm_traj_fixture(out):
+    """N:M sparsifier trajectories (all modes): per-step bodies, final base/fb."""
+    arrays = {}
+    meta = []
+    for name, r, c, steps, seed, warmup in TRAJ_SMALL:
+        xs = synth.flux_like(r, c, steps, seed)
+        for sname, spec in NM_TRAJ_CODECS.items():
+            for mode in MODES:
+                key = f"{name}|{sname}|{mode}"
+                res = run_traj(xs, spec, mode, warmup)
+                recs = []
+                for i, s in enumerate(res):
+                    arrays[f"body/{key}/{i}"] = np.frombuffer(s["body"], np.uint8).copy()
+                    recs.append({"base_sha256": synth.digest(s["base"]), "fb_sha256": synth.digest(s["fb"]),
+                                 "step": s["rec"].step, "compression_error": s["rec"].compression_error,
+                                 "bits": s["rec"].bits, "delta_hat": s["rec"].delta_hat, "tag": s["payload"].tag})
+                arrays[f"base/{key}"] = res[-1]["base"]
+                arrays[f"fb/{key}"] = res[-1]["fb"]
+                meta.append({"key": key, "traj": name, "rows": r, "cols": c, "steps": steps, "seed": seed,
+                             "warmup": warmup, "codec": sname, "spec": spec_dict(spec), "mode": mode,
+                             "records": recs, "inputs_sha256": synth.digest(np.stack(xs))})
+    # FLUX-width shard (P=8 height), 2:4, digests only
+    xs = synth.flux_like(512, 3072, 4, 34)
+    spec = S(K.NM_BLOCK, n=2, m=4)
+    res = run_traj(xs, spec, "residual_with_feedback", 1)
+    out["nm_digest"] = [{
+        "key": "d512x3072|nm2:4", "rows": 512, "cols": 3072, "steps": 4, "seed": 34, "warmup": 1,
+        "codec": "nm2:4", "spec": spec_dict(spec), "mode": "residual_with_feedback",
+        "inputs_sha256": synth.digest(np.stack(xs)),
+        "body_sha256": [synth.digest(s["body"]) for s in res],
+        "base_sha256": [synth.digest(s["base"]) for s in res],
+        "fb_sha256": [synth.digest(s["fb"]) for s in res],
+        "records": [{"compression_error": s["rec"].compression_error, "delta_hat": s["rec"].delta_hat,
+                     "bits": s["rec"].bits, "tag": s["payload"].tag} for s in res],
+    }]
+    np.savez_compressed(os.path.join(HERE, "traj_nm.npz"), **arrays)
+    out["traj_nm"] = meta
 
 
 TRAJ_DIGEST = [
@@ -234,6 +284,7 @@ def main():
            "numpy": np.__version__}
     build_codec_fixture(out)
     build_traj_fixture(out)
+    build_nm_traj_fixture(out)
     build_digest_fixture(out)
     build_topk_digest(out)
     build_lowrank_cases(out)

@@ -30,6 +30,11 @@ def traj_arrays():
     return dict(np.load(os.path.join(GOLDEN, "traj_small.npz")))
 
 
+@functools.lru_cache(maxsize=None)
+def traj_nm_arrays():
+    return dict(np.load(os.path.join(GOLDEN, "traj_nm.npz")))
+
+
 def oracle_codec(spec):
     """Map a reference spec dict to an oracle Codec."""
     from oracle import cc_oracle as O

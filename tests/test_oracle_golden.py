@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import synth
-from golden_fixtures import codec_arrays, manifest, oracle_codec, traj_arrays
+from golden_fixtures import codec_arrays, manifest, oracle_codec, traj_arrays, traj_nm_arrays
 from oracle import cc_oracle as O
 
 REF = "/root/reference/pkg/src"
@@ -77,6 +77,40 @@ def test_protocol_trajectory_matches_reference(meta):
         assert np.array_equal(rcv.base, snd.base)
     assert np.array_equal(snd.base, arr[f"base/{meta['key']}"])
     assert np.array_equal(snd.fb, arr[f"fb/{meta['key']}"])
+
+
+@pytest.mark.parametrize("meta", manifest()["traj_nm"], ids=lambda m: m["key"])
+def test_nm_trajectory_matches_reference(meta):
+    arr = traj_nm_arrays()
+    xs = _traj_inputs(meta)
+    codec = oracle_codec(meta["spec"])
+    n, c = meta["rows"], meta["cols"]
+    snd = O.Channel(meta["mode"], meta["warmup"], np.zeros((n, c), np.float32))
+    rcv = O.Channel(meta["mode"], meta["warmup"], np.zeros((n, c), np.float32))
+    for i, x in enumerate(xs):
+        tag, body, rec = O.send(snd, x, codec)
+        exp = meta["records"][i]
+        assert tag == exp["tag"]
+        assert body == arr[f"body/{meta['key']}/{i}"].tobytes()
+        assert synth.digest(snd.base) == exp["base_sha256"]
+        assert synth.digest(snd.fb) == exp["fb_sha256"]
+        assert rec["bits"] == exp["bits"]
+        assert rec["compression_error"] == pytest.approx(exp["compression_error"], rel=1e-12, abs=1e-300)
+        O.receive(rcv, i + 1, i + 1 <= meta["warmup"], tag, body, codec)
+        assert np.array_equal(rcv.base, snd.base)
+    assert np.array_equal(snd.base, arr[f"base/{meta['key']}"])
+
+
+@pytest.mark.parametrize("meta", manifest()["nm_digest"], ids=lambda m: m["key"])
+def test_nm_flux_width_digests(meta):
+    xs = _traj_inputs(meta)
+    codec = oracle_codec(meta["spec"])
+    snd = O.Channel(meta["mode"], meta["warmup"], np.zeros((meta["rows"], meta["cols"]), np.float32))
+    for i, x in enumerate(xs):
+        _, body, rec = O.send(snd, x, codec)
+        assert synth.digest(body) == meta["body_sha256"][i]
+        assert synth.digest(snd.base) == meta["base_sha256"][i]
+        assert synth.digest(snd.fb) == meta["fb_sha256"][i]
 
 
 @pytest.mark.parametrize("meta", manifest()["traj_digest"], ids=lambda m: m["key"])
