@@ -14,10 +14,13 @@
 // values, +0 and -0 alike); entry j is kept iff rank_j < n, which is exactly the
 // stable-argsort choice.
 //
-//   fast path  m in {2, 4, 8, 16, 32}: one thread per block, keys in registers;
-//              the m-bit masks of 32/m consecutive lanes form one u32 word (warp
-//              shuffle OR), written directly.
-//   generic    any other m (<= 65535): one warp per block; t staged in a scratch
+//   quad path  m in {1, 2, 4, 8, 16, 32}, C % 4 == 0, aligned: one thread per
+//              128-bit quad, m/4 lanes per block exchanging keys by shuffle (the
+//              production path: every load / store is a coalesced float4).
+//   small-m    any other m <= 32 (unaligned / odd C, non-power-of-two m): one thread
+//              per block, keys in registers, mask words by shuffle OR (power of
+//              two) or atomic OR into a scratch (otherwise).
+//   generic    m > 32 (<= 65535): one warp per block; t staged in a scratch
 //              [n, C], mask bits atomically OR-ed into a zeroed scratch, then copied to the
 //              body.
 #include "cc_common.cuh"
@@ -40,9 +43,10 @@ struct Geo {
 
 __device__ __forceinline__ uint32_t key_of(float t) { return __float_as_uint(t) & 0x7fffffffu; }
 
-// record partials: per-CTA (||d - t||^2, ||t||^2), last CTA reduces in fixed order
+// record partials: per-CTA (||d - t||^2, ||t||^2); the last CTA to finish reduces
+// them in a fixed order (thread i sums partials i, i+256, ...; then a fixed tree)
 __device__ __forceinline__ void record_tail(double err, double tsq, double *part, unsigned *ticket, double *record) {
-  __shared__ double se[kThreads / 32], st[kThreads / 32];
+  __shared__ double se[kThreads], st[kThreads];
   __shared__ bool last;
   err = warp_sum(err);
   tsq = warp_sum(tsq);
@@ -63,15 +67,26 @@ __device__ __forceinline__ void record_tail(double err, double tsq, double *part
     last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double a = 0.0, b = 0.0;
-    for (unsigned i = 0; i < gridDim.x; ++i) {
-      a += __ldcg(part + 2 * i);
-      b += __ldcg(part + 2 * i + 1);
+  if (!last) return;
+  __threadfence();
+  double a = 0.0, b = 0.0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += kThreads) {
+    a += __ldcg(part + 2 * i);
+    b += __ldcg(part + 2 * i + 1);
+  }
+  se[threadIdx.x] = a;
+  st[threadIdx.x] = b;
+  __syncthreads();
+  for (int h = kThreads / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+      se[threadIdx.x] += se[threadIdx.x + h];
+      st[threadIdx.x] += st[threadIdx.x + h];
     }
-    record[0] = a;
-    record[1] = b;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    record[0] = se[0];
+    record[1] = st[0];
     *ticket = 0u;
   }
 }
@@ -133,14 +148,18 @@ __device__ __forceinline__ float get_half(const uint8_t *p) {
   return __half2float(__ushort_as_half(u));
 }
 
-// ---- fast encode: m in {2,4,8,16,32}, one thread per block ---------------------
+// ---- small-m encode (scalar fallback): one thread per block -----------------
+// M > 0: m = M (power of two <= 32), the masks of 32/M consecutive lanes form one
+// u32 word (shuffle OR), written directly.  M == 0: runtime m <= 32 (any value);
+// mask bits are OR-ed into a zeroed scratch word array (blocks straddle words).
 template <int MODE, typename XT, bool STEP, int M>
-__global__ void __launch_bounds__(kThreads) k_nm_fast(const XT *__restrict__ x, float *__restrict__ base,
-                                                       float *__restrict__ aux, const float *__restrict__ tin,
-                                                       float *__restrict__ decoded, Geo g, uint8_t *__restrict__ body,
-                                                       int vec, double *__restrict__ part, unsigned *ticket,
-                                                       double *__restrict__ record) {
-  constexpr int L = 32 / M;  // lanes per mask word
+__global__ void __launch_bounds__(kThreads) k_nm_small(const XT *__restrict__ x, float *__restrict__ base,
+                                                        float *__restrict__ aux, const float *__restrict__ tin,
+                                                        float *__restrict__ decoded, Geo g, uint8_t *__restrict__ body,
+                                                        uint32_t *__restrict__ mwords, double *__restrict__ part,
+                                                        unsigned *ticket, double *__restrict__ record) {
+  constexpr int MM = M > 0 ? M : 32;  // register array width
+  const int m = M > 0 ? M : g.M;
   const int lane = threadIdx.x & 31;
   uint8_t *vals = body + g.mask_bytes;
   double err = 0.0, tsq = 0.0;
@@ -149,115 +168,236 @@ __global__ void __launch_bounds__(kThreads) k_nm_fast(const XT *__restrict__ x, 
     uint32_t mask = 0;
     if (gb < g.nblocks) {
       const int64_t row = gb / g.bpr;
-      const int64_t c0 = (gb - row * g.bpr) * M;
+      const int64_t c0 = (gb - row * g.bpr) * m;
       const int64_t e0 = row * g.C + c0;
-      const int nreal = (int)min64(M, g.C - c0);
-      float t[M];
-      if constexpr (M >= 4) {
-        if (vec) {  // C % 4 == 0 and 16-byte aligned rows: whole float4 groups are in or out
+      const int nreal = (int)min64(m, g.C - c0);
+      float t[MM];
+      uint32_t k[MM];
 #pragma unroll
-          for (int q = 0; q < M / 4; ++q) {
-            if (4 * q < nreal) {
-              float4 v;
-              if constexpr (!STEP) {
-                v = __ldcs(reinterpret_cast<const float4 *>(tin + e0 + 4 * q));
-              } else {
-                const float4 xx = Act<XT>::load4(x + e0 + 4 * q);
-                float4 bb = make_float4(0.f, 0.f, 0.f, 0.f), aa = bb;
-                if constexpr (MODE == CC_WITH_FEEDBACK) bb = *reinterpret_cast<const float4 *>(base + e0 + 4 * q);
-                if constexpr (MODE != CC_NAIVE) aa = *reinterpret_cast<const float4 *>(aux + e0 + 4 * q);
-                v = make_float4(target_of<MODE>(xx.x, bb.x, aa.x), target_of<MODE>(xx.y, bb.y, aa.y),
-                                target_of<MODE>(xx.z, bb.z, aa.z), target_of<MODE>(xx.w, bb.w, aa.w));
-              }
-              t[4 * q] = v.x; t[4 * q + 1] = v.y; t[4 * q + 2] = v.z; t[4 * q + 3] = v.w;
-            } else {
-              t[4 * q] = t[4 * q + 1] = t[4 * q + 2] = t[4 * q + 3] = 0.0f;
-            }
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < M; ++j) t[j] = j < nreal ? target1<MODE, XT, STEP>(x, base, aux, tin, e0 + j) : 0.0f;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < M; ++j) t[j] = j < nreal ? target1<MODE, XT, STEP>(x, base, aux, tin, e0 + j) : 0.0f;
+      for (int j = 0; j < MM; ++j) {
+        t[j] = j < nreal ? target1<MODE, XT, STEP>(x, base, aux, tin, e0 + j) : 0.0f;
+        k[j] = key_of(t[j]);
       }
-      uint32_t k[M];
 #pragma unroll
-      for (int j = 0; j < M; ++j) k[j] = key_of(t[j]);
-#pragma unroll
-      for (int j = 0; j < M; ++j) {
+      for (int j = 0; j < MM; ++j) {
         int rank = 0;
 #pragma unroll
-        for (int i = 0; i < M; ++i) {
+        for (int i = 0; i < MM; ++i) {
+          if (i >= m) continue;
           if (i < j) rank += k[i] >= k[j];
           else if (i > j) rank += k[i] > k[j];
         }
-        if (rank < g.N) mask |= 1u << j;
+        if (j < m && rank < g.N) mask |= 1u << j;
       }
       // values + state update, ascending index order
       uint8_t *vp = vals + 2 * gb * g.N;
       int slot = 0;
-      float d[M];
 #pragma unroll
-      for (int j = 0; j < M; ++j) {
-        d[j] = 0.0f;
+      for (int j = 0; j < MM; ++j) {
+        float d = 0.0f;
         if (mask & (1u << j)) {
           const __half h = __float2half_rn(t[j]);
           put_half(vp + 2 * slot, h);
           ++slot;
-          d[j] = __half2float(h);
+          d = __half2float(h);
+        }
+        if (j < nreal) {
+          const double df = (double)d - (double)t[j];
+          err += df * df;
+          tsq += (double)t[j] * (double)t[j];
+          update1<MODE, XT, STEP>(x, base, aux, decoded, e0 + j, t[j], d);
         }
       }
+    }
+    if constexpr (M == 0) {  // CTA-local mask words in shared memory, then one global OR per word
+      __shared__ uint32_t smask[kThreads + 2];
+      const int64_t bit0 = gb0 * m;
+      for (int i = threadIdx.x; i < kThreads + 2; i += kThreads) smask[i] = 0u;
+      __syncthreads();
+      if (mask) {
+        const int64_t lb = (bit0 & 31) + (gb - gb0) * m;
+        const int sh = (int)(lb & 31);
+        atomicOr(&smask[lb >> 5], mask << sh);
+        if (sh + m > 32) atomicOr(&smask[(lb >> 5) + 1], mask >> (32 - sh));
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < kThreads + 2; i += kThreads)
+        if (smask[i]) atomicOr(&mwords[(bit0 >> 5) + i], smask[i]);
+      __syncthreads();
+    }
+    if constexpr (M > 0) {  // assemble the mask words of L consecutive lanes
+      constexpr int L = 32 / M;
+      uint32_t w = mask << ((lane % L) * M);
 #pragma unroll
-      for (int j = 0; j < M; ++j) {
-        if (j < nreal) {
+      for (int o = 1; o < L; o <<= 1) w |= __shfl_xor_sync(0xffffffffu, w, o);
+      if (lane % L == 0 && gb < g.nblocks) put_word(body, (gb / L) * 4, w, g.mask_bytes);
+    }
+  }
+  if (record) record_tail(err, tsq, part, ticket, record);
+}
+
+// ---- quad encode: m in {1,2,4,8,16,32}, C % 4 == 0, 16-byte aligned -----------
+// Every thread owns one 128-bit quad of 4 consecutive padded columns (all loads and
+// stores are float4, perfectly coalesced).  m >= 4: Q = m/4 consecutive lanes share
+// one block and exchange keys with shuffles (4m compares per thread); m < 4: the
+// quad holds 4/m whole blocks.  The 4 keep-bits of 8 consecutive lanes form one u32
+// mask word (the quad's bit offset is 4 * quad index in the padded flat order).
+template <int M>
+__device__ __forceinline__ uint32_t quad_select(const uint32_t (&k)[4], int lane, int N, int &pre_blk) {
+  uint32_t bits = 0;
+  if constexpr (M >= 4) {
+    constexpr int Q = M / 4;
+    const int sub = lane % Q;
+    int rank[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int s = 0; s < Q; ++s) {
+      const int src = lane - sub + s;
+      uint32_t ko[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ko[i] = Q == 1 ? k[i] : __shfl_sync(0xffffffffu, k[i], src);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int ii = 4 * s + i, jj = 4 * sub + j;
+          rank[j] += ii < jj ? (ko[i] >= k[j]) : (ii > jj ? (ko[i] > k[j]) : 0);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (rank[j] < N) bits |= 1u << j;
+    // kept entries of the lower quads of my block
+    const int cnt = __popc(bits);
+    int pre = 0;
+#pragma unroll
+    for (int s = 0; s < Q; ++s) {
+      const int c = Q == 1 ? cnt : __shfl_sync(0xffffffffu, cnt, lane - sub + s);
+      if (s < sub) pre += c;
+    }
+    pre_blk = pre;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int rank = 0;
+#pragma unroll
+      for (int i = (j / M) * M; i < (j / M) * M + M; ++i) rank += i < j ? (k[i] >= k[j]) : (i > j ? (k[i] > k[j]) : 0);
+      if (rank < N) bits |= 1u << j;
+    }
+    pre_blk = 0;
+  }
+  return bits;
+}
+
+// output slot (within the values stream) of quad element j
+template <int M>
+__device__ __forceinline__ int64_t quad_slot(int64_t gq, uint32_t bits, int j, int N, int pre_blk) {
+  if constexpr (M >= 4) {
+    return (gq / (M / 4)) * N + pre_blk + __popc(bits & ((1u << j) - 1u));
+  } else {
+    const int b = j / M;
+    const uint32_t below = bits & ((1u << j) - 1u) & (((1u << M) - 1u) << (b * M));
+    return (gq * (4 / M) + b) * N + __popc(below);
+  }
+}
+
+constexpr int kQuadU = 2;  // quads per thread per iteration (loads of both issued first)
+
+template <int MODE, typename XT, bool STEP, int M>
+__global__ void __launch_bounds__(kThreads) k_nm_quad(const XT *__restrict__ x, float *__restrict__ base,
+                                                       float *__restrict__ aux, const float *__restrict__ tin,
+                                                       float *__restrict__ decoded, Geo g, int64_t nquads,
+                                                       int64_t qpr, uint8_t *__restrict__ body,
+                                                       double *__restrict__ part, unsigned *ticket,
+                                                       double *__restrict__ record) {
+  const int lane = threadIdx.x & 31;
+  uint8_t *vals = body + g.mask_bytes;
+  double err = 0.0, tsq = 0.0;
+  const int64_t tile = (int64_t)kQuadU * kThreads;
+  for (int64_t q0 = (int64_t)blockIdx.x * tile; q0 < nquads; q0 += (int64_t)gridDim.x * tile) {
+    float4 tv[kQuadU], bb[kQuadU], aa[kQuadU], xx[kQuadU];
+    int64_t e0[kQuadU];
+    bool real[kQuadU];
+#pragma unroll
+    for (int u = 0; u < kQuadU; ++u) {
+      const int64_t gq = q0 + u * kThreads + threadIdx.x;
+      tv[u] = bb[u] = aa[u] = xx[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      real[u] = false;
+      e0[u] = 0;
+      if (gq < nquads) {
+        const int64_t row = gq / qpr;
+        const int64_t p0 = (gq - row * qpr) * 4;
+        real[u] = p0 < g.C;  // C % 4 == 0: a quad is all real or all padding
+        e0[u] = row * g.C + p0;
+        if (real[u]) {
+          if constexpr (!STEP) {
+            tv[u] = __ldcs(reinterpret_cast<const float4 *>(tin + e0[u]));
+          } else {
+            xx[u] = Act<XT>::load4(x + e0[u]);
+            if constexpr (MODE != CC_NAIVE) bb[u] = __ldcs(reinterpret_cast<const float4 *>(base + e0[u]));
+            if constexpr (MODE != CC_NAIVE) aa[u] = __ldcs(reinterpret_cast<const float4 *>(aux + e0[u]));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kQuadU; ++u) {
+      const int64_t gq = q0 + u * kThreads + threadIdx.x;
+      const bool live = gq < nquads;
+      if constexpr (STEP) {
+        tv[u] = make_float4(target_of<MODE>(xx[u].x, bb[u].x, aa[u].x), target_of<MODE>(xx[u].y, bb[u].y, aa[u].y),
+                            target_of<MODE>(xx[u].z, bb[u].z, aa[u].z), target_of<MODE>(xx[u].w, bb[u].w, aa[u].w));
+      }
+      const float t[4] = {tv[u].x, tv[u].y, tv[u].z, tv[u].w};
+      const uint32_t k[4] = {key_of(t[0]), key_of(t[1]), key_of(t[2]), key_of(t[3])};
+      int pre = 0;
+      uint32_t bits = quad_select<M>(k, lane, g.N, pre);
+      if (!live) bits = 0;
+      float d[4] = {0.f, 0.f, 0.f, 0.f};
+      if (live) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (bits & (1u << j)) {
+            const __half h = __float2half_rn(t[j]);
+            put_half(vals + 2 * quad_slot<M>(gq, bits, j, g.N, pre), h);
+            d[j] = __half2float(h);
+          }
+        }
+      }
+      if (real[u]) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
           const double df = (double)d[j] - (double)t[j];
           err += df * df;
           tsq += (double)t[j] * (double)t[j];
         }
-      }
-      bool done = false;
-      if constexpr (M >= 4) {
-        if (vec) {
-#pragma unroll
-          for (int q = 0; q < M / 4; ++q) {
-            if (4 * q >= nreal) continue;
-            const int64_t e = e0 + 4 * q;
-            const float4 dv = make_float4(d[4 * q], d[4 * q + 1], d[4 * q + 2], d[4 * q + 3]);
-            if constexpr (STEP) {
-              if constexpr (MODE == CC_NAIVE) {
-                *reinterpret_cast<float4 *>(base + e) = dv;
-              } else {
-                const float4 bb = *reinterpret_cast<const float4 *>(base + e);
-                *reinterpret_cast<float4 *>(base + e) = make_float4(
-                    __fadd_rn(bb.x, dv.x), __fadd_rn(bb.y, dv.y), __fadd_rn(bb.z, dv.z), __fadd_rn(bb.w, dv.w));
-                if constexpr (MODE == CC_WITH_FEEDBACK) {
-                  *reinterpret_cast<float4 *>(aux + e) =
-                      make_float4(__fsub_rn(t[4 * q], dv.x), __fsub_rn(t[4 * q + 1], dv.y),
-                                  __fsub_rn(t[4 * q + 2], dv.z), __fsub_rn(t[4 * q + 3], dv.w));
-                } else {
-                  *reinterpret_cast<float4 *>(aux + e) = Act<XT>::load4(x + e);
-                }
-              }
-            } else if (decoded) {
-              *reinterpret_cast<float4 *>(decoded + e) = dv;
+        const float4 dv = make_float4(d[0], d[1], d[2], d[3]);
+        const int64_t e = e0[u];
+        if constexpr (STEP) {
+          if constexpr (MODE == CC_NAIVE) {
+            __stcs(reinterpret_cast<float4 *>(base + e), dv);
+          } else {
+            __stcs(reinterpret_cast<float4 *>(base + e),
+                   make_float4(__fadd_rn(bb[u].x, dv.x), __fadd_rn(bb[u].y, dv.y), __fadd_rn(bb[u].z, dv.z),
+                               __fadd_rn(bb[u].w, dv.w)));
+            if constexpr (MODE == CC_WITH_FEEDBACK) {
+              __stcs(reinterpret_cast<float4 *>(aux + e),
+                     make_float4(__fsub_rn(tv[u].x, dv.x), __fsub_rn(tv[u].y, dv.y), __fsub_rn(tv[u].z, dv.z),
+                                 __fsub_rn(tv[u].w, dv.w)));
+            } else {
+              __stcs(reinterpret_cast<float4 *>(aux + e), xx[u]);  // ref' = a*
             }
           }
-          done = true;
+        } else if (decoded) {
+          *reinterpret_cast<float4 *>(decoded + e) = dv;
         }
       }
-      if (!done) {
-#pragma unroll
-        for (int j = 0; j < M; ++j)
-          if (j < nreal) update1<MODE, XT, STEP>(x, base, aux, decoded, e0 + j, t[j], d[j]);
-      }
+      uint32_t w = bits << (4 * (lane & 7));
+      w |= __shfl_xor_sync(0xffffffffu, w, 1);
+      w |= __shfl_xor_sync(0xffffffffu, w, 2);
+      w |= __shfl_xor_sync(0xffffffffu, w, 4);
+      if ((lane & 7) == 0 && live) put_word(body, (gq >> 3) * 4, w, g.mask_bytes);
     }
-    // assemble the mask words of L consecutive lanes
-    uint32_t w = mask << ((lane % L) * M);
-#pragma unroll
-    for (int o = 1; o < L; o <<= 1) w |= __shfl_xor_sync(0xffffffffu, w, o);
-    if (lane % L == 0 && gb < g.nblocks) put_word(body, (gb / L) * 4, w, g.mask_bytes);
   }
   if (record) record_tail(err, tsq, part, ticket, record);
 }
@@ -362,26 +502,29 @@ __device__ __forceinline__ uint32_t get_bits(const uint8_t *mask, int64_t bit0, 
   return nbits == 32 ? (uint32_t)w : (uint32_t)(w & ((1ull << nbits) - 1ull));
 }
 
+// M > 0: m = M; M == 0: runtime m <= 32
 template <int M>
 __global__ void __launch_bounds__(kThreads) k_nm_decode_fast(const __grid_constant__ Peers pp, int64_t C, int64_t bpr,
-                                                              int N, int accumulate) {
+                                                              int N, int mr, int accumulate) {
+  constexpr int MM = M > 0 ? M : 32;
+  const int m = M > 0 ? M : mr;
   const int peer = blockIdx.y;
   const int64_t nb = pp.nblocks[peer];
   const uint8_t *body = pp.body[peer];
   float *base = pp.base[peer];
-  const int64_t mask_bytes = (nb * M + 7) / 8;
+  const int64_t mask_bytes = (nb * m + 7) / 8;
   const uint8_t *vals = body + mask_bytes;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   for (int64_t gb = (int64_t)blockIdx.x * kThreads + threadIdx.x; gb < nb; gb += stride) {
-    const uint32_t mask = get_bits(body, gb * M, M);
+    const uint32_t mask = get_bits(body, gb * m, m);
     const int64_t row = gb / bpr;
-    const int64_t c0 = (gb - row * bpr) * M;
+    const int64_t c0 = (gb - row * bpr) * m;
     const int64_t e0 = row * C + c0;
-    const int nreal = (int)min64(M, C - c0);
+    const int nreal = (int)min64(m, C - c0);
     const uint8_t *vp = vals + 2 * gb * N;
     int slot = 0;
 #pragma unroll
-    for (int j = 0; j < M; ++j) {
+    for (int j = 0; j < MM; ++j) {
       float d = 0.0f;
       if (mask & (1u << j)) d = get_half(vp + 2 * slot++);
       if (j < nreal) base[e0 + j] = accumulate ? __fadd_rn(base[e0 + j], d) : d;
@@ -417,12 +560,57 @@ __global__ void __launch_bounds__(kThreads) k_nm_decode_generic(const __grid_con
   }
 }
 
+// quad decode (C % 4 == 0, aligned bases): one float4 of base per thread
+template <int M>
+__global__ void __launch_bounds__(kThreads) k_nm_decode_quad(const __grid_constant__ Peers pp, int64_t C, int64_t qpr,
+                                                              int N, int accumulate) {
+  const int peer = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const uint8_t *body = pp.body[peer];
+  float *base = pp.base[peer];
+  const int64_t nquads = pp.nblocks[peer] * M / 4;
+  const int64_t mask_bytes = (pp.nblocks[peer] * M + 7) / 8;
+  const uint8_t *vals = body + mask_bytes;
+  for (int64_t gq0 = (int64_t)blockIdx.x * kThreads; gq0 < nquads; gq0 += (int64_t)gridDim.x * kThreads) {
+    const int64_t gq = gq0 + threadIdx.x;
+    const bool live = gq < nquads;
+    uint32_t bits = live ? (uint32_t)(body[gq >> 1] >> ((gq & 1) * 4)) & 0xfu : 0u;
+    int pre = 0;
+    if constexpr (M >= 4) {
+      constexpr int Q = M / 4;
+      const int sub = lane % Q;
+      const int cnt = __popc(bits);
+#pragma unroll
+      for (int s = 0; s < Q; ++s) {
+        const int c = Q == 1 ? cnt : __shfl_sync(0xffffffffu, cnt, lane - sub + s);
+        if (s < sub) pre += c;
+      }
+    }
+    if (!live) continue;
+    const int64_t row = gq / qpr;
+    const int64_t p0 = (gq - row * qpr) * 4;
+    if (p0 >= C) continue;
+    float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (bits & (1u << j)) d[j] = get_half(vals + 2 * quad_slot<M>(gq, bits, j, N, pre));
+    float4 *bp = reinterpret_cast<float4 *>(base + row * C + p0);
+    if (accumulate) {
+      const float4 b = *bp;
+      *bp = make_float4(__fadd_rn(b.x, d[0]), __fadd_rn(b.y, d[1]), __fadd_rn(b.z, d[2]), __fadd_rn(b.w, d[3]));
+    } else {
+      *bp = make_float4(d[0], d[1], d[2], d[3]);
+    }
+  }
+}
+
 }  // namespace nm
 
 // ---------------------------------------------------------------------------
 // host
 // ---------------------------------------------------------------------------
 static bool nm_fast(int m) { return m == 2 || m == 4 || m == 8 || m == 16 || m == 32; }
+static bool nm_quad_ok(int m) { return m == 1 || nm_fast(m); }
 
 static nm::Geo nm_geo(int64_t rows, int64_t C, int n, int m) {
   nm::Geo g;
@@ -438,6 +626,11 @@ static nm::Geo nm_geo(int64_t rows, int64_t C, int n, int m) {
 int64_t nm_body_bytes(int64_t rows, int64_t C, int n, int m) {
   const nm::Geo g = nm_geo(rows, C, n, m);
   return g.mask_bytes + 2 * g.nblocks * n;
+}
+
+// quad path: one iteration per thread (enough CTAs in flight to cover HBM latency)
+static unsigned nm_quad_grid(int64_t nquads) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(nquads, (int64_t)nm::kQuadU * nm::kThreads), 1 << 16));
 }
 
 static unsigned nm_grid(int64_t work_items) {
@@ -465,11 +658,10 @@ static NmWork nm_carve(void *ws, int64_t rows, int64_t C, int n, int m, bool nee
   const nm::Geo g = nm_geo(rows, C, n, m);
   w.ticket = reinterpret_cast<unsigned *>(take(16));
   w.rec = reinterpret_cast<double *>(take(16));
-  w.part = reinterpret_cast<double *>(take(16 * (size_t)sm_count() * 8 + 16));
-  if (!nm_fast(m)) {
-    w.mwords = reinterpret_cast<uint32_t *>(take(4 * (size_t)cdiv(g.nblocks * m, 32)));
-    if (need_t) w.tstage = reinterpret_cast<float *>(take(4 * (size_t)(rows * C)));
-  }
+  const int64_t nparts = std::max<int64_t>(sm_count() * 8, nm_quad_grid(g.nblocks * m / 4 + 1));
+  w.part = reinterpret_cast<double *>(take(16 * (size_t)nparts + 16));
+  if (!nm_fast(m)) w.mwords = reinterpret_cast<uint32_t *>(take(4 * (size_t)cdiv(g.nblocks * m, 32)));
+  if (m > 32 && need_t) w.tstage = reinterpret_cast<float *>(take(4 * (size_t)(rows * C)));
   w.bytes = off;
   return w;
 }
@@ -483,22 +675,43 @@ static int nm_run(const nm::Geo &g, int64_t rows, const XT *x, float *base, floa
                   float *decoded, uint8_t *body, const NmWork &w, double *record, cudaStream_t st) {
   using namespace nm;
   const int64_t total = rows * g.C;
-  if (nm_fast(g.M)) {
+  auto al = [](const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const int vec = g.C % 4 == 0 && al(base) && al(aux) && al(tin) && al(decoded) &&
+                  (x == nullptr || (reinterpret_cast<uintptr_t>(x) & (sizeof(XT) == 2 ? 7 : 15)) == 0);
+  if (vec && nm_quad_ok(g.M)) {
+    const int64_t qpr = g.bpr * g.M / 4;  // quads per padded row
+    const int64_t nquads = g.nblocks * g.M / 4;
+    const unsigned grid = nm_quad_grid(nquads);
+#define NM_Q(MM) k_nm_quad<MODE, XT, STEP, MM><<<grid, kThreads, 0, st>>>(x, base, aux, tin, decoded, g, nquads, qpr, \
+                                                                          body, w.part, w.ticket, record)
+    switch (g.M) {
+      case 1: NM_Q(1); break;
+      case 2: NM_Q(2); break;
+      case 4: NM_Q(4); break;
+      case 8: NM_Q(8); break;
+      case 16: NM_Q(16); break;
+      default: NM_Q(32); break;
+    }
+#undef NM_Q
+    count_launch();
+    return CC_OK;
+  }
+  if (g.M <= 32) {
     const unsigned grid = nm_grid(g.nblocks);
-    auto al = [](const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    const int vec = g.C % 4 == 0 && al(base) && al(aux) && al(tin) && al(decoded) &&
-                    (x == nullptr || (reinterpret_cast<uintptr_t>(x) & (sizeof(XT) == 2 ? 7 : 15)) == 0);
-#define NM_L(MM) k_nm_fast<MODE, XT, STEP, MM><<<grid, kThreads, 0, st>>>(x, base, aux, tin, decoded, g, body, vec, \
-                                                                          w.part, w.ticket, record)
+    if (!nm_fast(g.M)) cudaMemsetAsync(w.mwords, 0, 4 * (size_t)cdiv(g.nblocks * g.M, 32), st);
+#define NM_L(MM) k_nm_small<MODE, XT, STEP, MM><<<grid, kThreads, 0, st>>>(x, base, aux, tin, decoded, g, body, \
+                                                                           w.mwords, w.part, w.ticket, record)
     switch (g.M) {
       case 2: NM_L(2); break;
       case 4: NM_L(4); break;
       case 8: NM_L(8); break;
       case 16: NM_L(16); break;
-      default: NM_L(32); break;
+      case 32: NM_L(32); break;
+      default: NM_L(0); break;
     }
 #undef NM_L
     count_launch();
+    if (!nm_fast(g.M)) cudaMemcpyAsync(body, w.mwords, (size_t)g.mask_bytes, cudaMemcpyDeviceToDevice, st);
     return CC_OK;
   }
   // generic path
@@ -573,14 +786,28 @@ int nm_decode(int count, const int64_t *rows, int64_t C, int n, int m, const uin
       maxb = std::max(maxb, pp.nblocks[i]);
     }
     const int acc = accumulate != 0;
-    if (nm_fast(m)) {
+    bool bases_al = true;
+    for (int i = 0; i < cnt; ++i) bases_al = bases_al && (reinterpret_cast<uintptr_t>(pp.base[i]) & 15) == 0;
+    if (C % 4 == 0 && bases_al && nm_quad_ok(m)) {
+      const int64_t qpr = bpr * m / 4;
+      dim3 grid(nm_quad_grid(maxb * m / 4), cnt);
+      switch (m) {
+        case 1: nm::k_nm_decode_quad<1><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc); break;
+        case 2: nm::k_nm_decode_quad<2><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc); break;
+        case 4: nm::k_nm_decode_quad<4><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc); break;
+        case 8: nm::k_nm_decode_quad<8><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc); break;
+        case 16: nm::k_nm_decode_quad<16><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc); break;
+        default: nm::k_nm_decode_quad<32><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc); break;
+      }
+    } else if (m <= 32) {
       dim3 grid(nm_grid(maxb), cnt);
       switch (m) {
-        case 2: nm::k_nm_decode_fast<2><<<grid, nm::kThreads, 0, st>>>(pp, C, bpr, n, acc); break;
-        case 4: nm::k_nm_decode_fast<4><<<grid, nm::kThreads, 0, st>>>(pp, C, bpr, n, acc); break;
-        case 8: nm::k_nm_decode_fast<8><<<grid, nm::kThreads, 0, st>>>(pp, C, bpr, n, acc); break;
-        case 16: nm::k_nm_decode_fast<16><<<grid, nm::kThreads, 0, st>>>(pp, C, bpr, n, acc); break;
-        default: nm::k_nm_decode_fast<32><<<grid, nm::kThreads, 0, st>>>(pp, C, bpr, n, acc); break;
+        case 2: nm::k_nm_decode_fast<2><<<grid, nm::kThreads, 0, st>>>(pp, C, bpr, n, m, acc); break;
+        case 4: nm::k_nm_decode_fast<4><<<grid, nm::kThreads, 0, st>>>(pp, C, bpr, n, m, acc); break;
+        case 8: nm::k_nm_decode_fast<8><<<grid, nm::kThreads, 0, st>>>(pp, C, bpr, n, m, acc); break;
+        case 16: nm::k_nm_decode_fast<16><<<grid, nm::kThreads, 0, st>>>(pp, C, bpr, n, m, acc); break;
+        case 32: nm::k_nm_decode_fast<32><<<grid, nm::kThreads, 0, st>>>(pp, C, bpr, n, m, acc); break;
+        default: nm::k_nm_decode_fast<0><<<grid, nm::kThreads, 0, st>>>(pp, C, bpr, n, m, acc); break;
       }
     } else {
       dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(maxb, nm::kThreads / 32), sm_count() * 8)), cnt);
