@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--codec", default="quant2bit", choices=sorted(BITS))
     ap.add_argument("--layers", type=int, default=57)
+    ap.add_argument("--topology", default="allgather", choices=["allgather", "ring"],
+                    help="patch-parallel all-gather (default) or ring-attention style P-1 hop forwarding")
     ap.add_argument("--rows", type=int, default=ROWS)
     ap.add_argument("--cols", type=int, default=COLS)
     ap.add_argument("--no-e2e", action="store_true")
@@ -268,7 +270,7 @@ def run_b200(a, world, rank):
 
     from paper_2507_17511_b200 import _lib
     from paper_2507_17511_b200 import compressors as cx
-    from paper_2507_17511_b200.comm import PatchParallelExchange, shard_bounds
+    from paper_2507_17511_b200.comm import PatchParallelExchange, RingExchange, shard_bounds
 
     lib = _lib.load()
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -277,7 +279,8 @@ def run_b200(a, world, rank):
     bounds = shard_bounds(rows, world) if world > 1 else [(0, rows)]
     lo, hi = bounds[rank]
     n_own = hi - lo
-    exs = [PatchParallelExchange(rows, cols, spec, overlap=not a.no_overlap) for _ in range(L)]
+    Ex = RingExchange if a.topology == "ring" else PatchParallelExchange
+    exs = [Ex(rows, cols, spec, overlap=not a.no_overlap) for _ in range(L)]
     streams = exs[0].streams
     for e in exs[1:]:
         e.streams = streams  # one compute / comm / decode stream triple for the whole model
@@ -399,7 +402,7 @@ def run_b200(a, world, rank):
                                 f"{L} layer channels per step" + (" (world_size=1: sender + loopback receiver, "
                                                                   "BASELINE config 1)" if world == 1 else "")),
                    "codec": a.codec, "layers": L, "rows": rows, "cols": cols, "shard_rows": n_own,
-                   "parallelism": f"patch{world}", "l2": "per-step working set >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"patch{world}", "topology": a.topology, "l2": "per-step working set >> 126 MB L2 (no flush needed)",
                    "overlap": not a.no_overlap, "cuda_graph": not a.no_graph},
         "per_gpu_gbs": value / world,
         "exposed_comm_us_per_layer": exposed_us,

@@ -257,7 +257,9 @@ class PatchParallelExchange:
                             max(r * self.cols * esz for r in shard_rows))
         self.body_max = (self.body_max + 255) // 256 * 256
         self.sendbuf = torch.zeros(self.body_max, dtype=torch.uint8, device=self.device)
-        self.recvbuf = torch.zeros(self.P, self.body_max, dtype=torch.uint8, device=self.device)
+        # all-gather lands directly here: P contiguous slots of the step's wire size
+        self.recvflat = torch.zeros(self.P * self.body_max, dtype=torch.uint8, device=self.device)
+        self._per = self.body_max
         self.ev_encoded, self.ev_gathered, self.ev_decoded = (_Event(self.cuda) for _ in range(3))
         self.last_record = None
         self.last_nbytes = 0
@@ -293,10 +295,9 @@ class PatchParallelExchange:
             if S.comm is not None:
                 self.ev_encoded.wait(S.comm)
             if self.P > 1:
+                self._per = per
                 if not skip_comm:
-                    flat = torch.empty(self.P * per, dtype=torch.uint8, device=self.device)
-                    _dist().all_gather_into_tensor(flat, self.sendbuf[:per], group=self.group)
-                    self.recvbuf[:, :per].copy_(flat.view(self.P, per))
+                    _dist().all_gather_into_tensor(self.recvflat[:self.P * per], self.sendbuf[:per], group=self.group)
                 self.comm_bytes = per * (self.P - 1)
             self.ev_gathered.record(S.comm)
         with _on(S.decode):
@@ -316,11 +317,15 @@ class PatchParallelExchange:
         rows = [self.bounds[p][1] - self.bounds[p][0] for p in self.peers]
         acc = _receiver_accumulate(self.codec, self.mode, self._canon_pending)
         bases = [self.full[self.bounds[p][0]:self.bounds[p][1]] for p in self.peers]
-        self.engine.decode(self.codec, warm, wire16, acc, rows, self.cols, [self.recvbuf[p] for p in self.peers],
+        self.engine.decode(self.codec, warm, wire16, acc, rows, self.cols, [self.slot(p) for p in self.peers],
                            bases)
         self._canon_pending = warm or (self._canon_pending and acc == 0)
         for p in self.peers:
             self.peer_step[p] = t
+
+    def slot(self, p):
+        """Received body of rank p in the current step's layout."""
+        return self.recvflat[p * self._per:(p + 1) * self._per]
 
     def _loopback_decode(self, t, warm, wire16, nbytes):
         if self.loop_step + 1 != t:
@@ -342,6 +347,79 @@ class PatchParallelExchange:
     def digest(self):
         """blake2b of the full reconstruction (mesh:237)."""
         return hashlib.blake2b(self.reconstruction().cpu().numpy().tobytes(), digest_size=16).digest()
+
+
+class RingExchange(PatchParallelExchange):
+    """Ring-attention style compressed exchange (mesh:214-229).
+
+    The shard is encoded once at its origin; in each of the P-1 hops every rank
+    forwards the body it received in the previous hop verbatim to (rank+1) % P
+    while receiving from (rank-1) % P over NCCL point-to-point.  The body
+    received in hop r originates at (rank - r) % P (the reference's
+    `ring_origin` = (device - rnd + 1) % P is off by one, mesh:138-140, SURVEY
+    §8f).  Hop r's body is decoded on the decode stream while hop r+1 is in
+    flight, and the reconstruction is identical to the all-gather exchange.
+    """
+
+    def __init__(self, *args, **kw):
+        super().__init__(*args, **kw)
+        self.ev_hop = [_Event(self.cuda) for _ in range(max(self.P - 1, 1))]
+
+    def after_capture(self):
+        super().after_capture()
+        self.ev_hop = [_Event(self.cuda) for _ in range(max(self.P - 1, 1))]
+
+    @staticmethod
+    def origin(rank, rnd, P):
+        return (rank - rnd) % P
+
+    def step(self, x_shard, rng=None, skip_comm=False):
+        if self.P == 1:
+            return super().step(x_shard, rng=rng, skip_comm=skip_comm)
+        S = self.streams
+        dist = _dist()
+        t = self.sender.step + 1
+        warm = t <= self.warmup or cx.CompressorKind(self.codec.kind) == cx.CompressorKind.IDENTITY
+        with _on(S.compute):
+            if S.compute is not None and not torch.cuda.is_current_stream_capturing():
+                self.ev_decoded.wait(S.compute)
+            nbytes, wire16, rec = self.engine.encode(self.sender, x_shard, self.codec, self.sendbuf, rng)
+            self.last_record, self.last_nbytes = rec, nbytes
+            self.ev_encoded.record(S.compute)
+        per = self.wire_bytes(warm, wire16)
+        self._per = per
+        for p in self.peers:
+            if self.peer_step[p] + 1 != t:
+                raise pl.ProtocolError(f"peer {p}: step desynchronization")
+        acc = _receiver_accumulate(self.codec, self.mode, self._canon_pending)
+        nxt, prv = (self.rank + 1) % self.P, (self.rank - 1) % self.P
+        carried = self.sendbuf[:per]
+        for rnd in range(1, self.P):
+            o = self.origin(self.rank, rnd, self.P)
+            recv = self.slot(o)
+            with _on(S.comm):
+                if rnd == 1 and S.comm is not None:
+                    self.ev_encoded.wait(S.comm)
+                if not skip_comm:
+                    ops = [dist.P2POp(dist.isend, carried, nxt, group=self.group),
+                           dist.P2POp(dist.irecv, recv, prv, group=self.group)]
+                    for w in dist.batch_isend_irecv(ops):
+                        w.wait()
+                self.ev_hop[rnd - 1].record(S.comm)
+            with _on(S.decode):
+                if S.decode is not None:
+                    self.ev_hop[rnd - 1].wait(S.decode)
+                lo, hi = self.bounds[o]
+                self.engine.decode(self.codec, warm, wire16, acc, [hi - lo], self.cols, [recv],
+                                   [self.full[lo:hi]])
+            carried = recv
+        self.comm_bytes = per * (self.P - 1)
+        with _on(S.decode):
+            self.ev_decoded.record(S.decode)
+        self._canon_pending = warm or (self._canon_pending and acc == 0)
+        for p in self.peers:
+            self.peer_step[p] = t
+        return self.full
 
 
 class UlyssesAllToAll:

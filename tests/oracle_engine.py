@@ -20,6 +20,8 @@ def _ocodec(codec):
     kind = getattr(codec.kind, "value", codec.kind)
     if kind == "topk":
         return O.Codec(O.TOPK, keep_fraction=codec.keep_fraction)
+    if kind == "nm_block":
+        return O.Codec(O.NMBLOCK, nm=(codec.n, codec.m))
     return O.Codec(_TAGS[kind])
 
 
@@ -56,6 +58,8 @@ class OracleEngine:
             if oc.tag == O.TOPK:
                 k = O.topk_count(r, cols, oc.keep_fraction)
                 body = b[: 6 * k].numpy().tobytes()
+            elif oc.tag == O.NMBLOCK:
+                body = b[: O.body_bytes(oc.tag, r, cols, nm=oc.nm)].numpy().tobytes()
             else:
                 body = b[: O.body_bytes(oc.tag, r, cols)].numpy().tobytes()
             dec = torch.from_numpy(O.decode_body(body, oc, r, cols))

@@ -41,18 +41,20 @@ def _spec(name):
 
     if name == "topk":
         return cx.CompressorSpec(cx.CompressorKind.TOPK, keep_fraction=0.1)
+    if name == "nm2:4":
+        return cx.CompressorSpec(cx.CompressorKind.NM_BLOCK, n=2, m=4)
     return cx.CompressorSpec(cx.CompressorKind(name))
 
 
-def _worker_allgather(rank, world, port, codec, mode, out_dir, dtype):
+def _worker_allgather(rank, world, port, codec, mode, out_dir, dtype, topology="allgather"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle_engine import OracleEngine
-        from paper_2507_17511_b200.comm import PatchParallelExchange
+        from paper_2507_17511_b200.comm import PatchParallelExchange, RingExchange
 
-        ex = PatchParallelExchange(ROWS, COLS, _spec(codec), mode=mode, warmup=1, engine=OracleEngine(),
-                                   device="cpu", in_dtype=dtype)
+        cls = RingExchange if topology == "ring" else PatchParallelExchange
+        ex = cls(ROWS, COLS, _spec(codec), mode=mode, warmup=1, engine=OracleEngine(), device="cpu", in_dtype=dtype)
         digests = []
         for x in _inputs(dtype):
             ex.step(x[ex.lo:ex.hi].contiguous())
@@ -68,8 +70,12 @@ def _simulate_mesh(world, codec, mode, dtype):
     """Single-process reference semantics: per-shard sender channel; every
     receiver mirrors its sender bit-exactly, so full = vstack(sender bases)."""
     bounds = O.shard_rows(ROWS, world)
-    oc = O.Codec(O.TOPK, keep_fraction=0.1) if codec == "topk" else O.Codec({"sign1bit": O.SIGN1,
-                                                                             "quant2bit": O.QUANT2}[codec])
+    if codec == "topk":
+        oc = O.Codec(O.TOPK, keep_fraction=0.1)
+    elif codec == "nm2:4":
+        oc = O.Codec(O.NMBLOCK, nm=(2, 4))
+    else:
+        oc = O.Codec({"sign1bit": O.SIGN1, "quant2bit": O.QUANT2}[codec])
     chans = [O.Channel(mode, 1, np.zeros((hi - lo, COLS), np.float32)) for lo, hi in bounds]
     rcv = [O.Channel(mode, 1, np.zeros((hi - lo, COLS), np.float32)) for lo, hi in bounds]
     for t, x in enumerate(_inputs(dtype), start=1):
@@ -82,7 +88,7 @@ def _simulate_mesh(world, codec, mode, dtype):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("codec", ["quant2bit", "sign1bit", "topk"])
+@pytest.mark.parametrize("codec", ["quant2bit", "sign1bit", "topk", "nm2:4"])
 @pytest.mark.parametrize("mode", ["residual_with_feedback", "naive"])
 def test_allgather_exchange_gloo(world, codec, mode):
     if codec == "topk" and mode == "naive" and world == 3:
@@ -96,6 +102,37 @@ def test_allgather_exchange_gloo(world, codec, mode):
     ref = _simulate_mesh(world, codec, mode, dtype)
     for f in fulls:
         assert f.tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("codec", ["quant2bit", "topk", "nm2:4"])
+def test_ring_exchange_gloo(world, codec):
+    """Ring topology (P-1 hops, bodies forwarded verbatim, origin (rank - hop) % P)
+    reconstructs exactly what the all-gather does, on every rank."""
+    dtype, mode = torch.bfloat16, "residual_with_feedback"
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker_allgather, args=(world, _free_port(), codec, mode, d, dtype, "ring"), nprocs=world,
+                 join=True)
+        fulls = [np.load(os.path.join(d, f"full{r}.npy")) for r in range(world)]
+        digs = [open(os.path.join(d, f"dig{r}.bin"), "rb").read() for r in range(world)]
+    assert all(dg == digs[0] for dg in digs)
+    ref = _simulate_mesh(world, codec, mode, dtype)
+    for f in fulls:
+        assert f.tobytes() == ref.tobytes()
+
+
+def test_ring_origin_fixed():
+    """Hop r delivers the shard of (rank - r) % P; every peer exactly once."""
+    from paper_2507_17511_b200.comm import RingExchange
+
+    for P in range(2, 9):
+        for rank in range(P):
+            origins = [RingExchange.origin(rank, r, P) for r in range(1, P)]
+            assert sorted(origins) == sorted(set(range(P)) - {rank})
+            # forwarding: what rank forwards in hop r+1 is what it received in hop r,
+            # which its successor expects as origin (rank + 1 - (r + 1)) % P
+            for r in range(1, P - 1):
+                assert RingExchange.origin((rank + 1) % P, r + 1, P) == origins[r - 1]
 
 
 def _worker_ulysses(rank, world, port, out_dir):
