@@ -302,10 +302,15 @@ def run_b200(a, world, rank):
     barrier(world)
 
     K = a.steps
-    # per-kernel timing pass (events around every K1 on its stream; not the headline)
+    # per-kernel timing pass (events around every K1 on its stream; not the headline).
+    # A spin kernel queued first keeps the GPU busy while Python enqueues the step, so
+    # the events bracket GPU execution only (no host launch gaps inside the intervals).
     evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(L)]
            for _ in range(K)]
+    spin_cycles = int(2.0e9 * 0.001 * L)  # ~1 ms of host enqueue time per layer, generously
     for s in range(K):
+        with torch.cuda.stream(streams.compute):
+            torch.cuda._sleep(spin_cycles)
         one_step(a.warmup + 1 + s, ev=evs[s])
     streams.compute.wait_stream(streams.decode)
     barrier(world)

@@ -200,6 +200,9 @@ CC_API void cc_debug_fused_timer(void *dev_buf);
 CC_API void cc_debug_fused_policy(int policy);
 /* profiling only: phase-B ring depths of the persistent K1 (0 = automatic) */
 CC_API void cc_debug_fused_rings(int s_in, int s_out);
+/* profiling only: phase-A tile height (rows per row group) and ring depth of the
+ * persistent K1 (0 = automatic) */
+CC_API void cc_debug_fused_phase_a(int rows_per_group, int stages);
 /* low-rank projections: 1 = tcgen05 tensor cores, 3xTF32 split (default),
  * 0 = f64-accumulating CUDA-core GEMMs (cross-check) */
 CC_API void cc_set_lowrank_backend(int backend);

@@ -709,7 +709,11 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
 // ---------------------------------------------------------------------------
 static int g_fused_stop = 0;
 static int g_fused_policy = 0;
-static int g_fused_si = 0, g_fused_so = 0;
+static int g_fused_si = 0, g_fused_so = 0, g_fused_ra = 0, g_fused_sa = 0;
+void set_fused_phase_a(int rows_per_tile, int stages) {
+  g_fused_ra = rows_per_tile;
+  g_fused_sa = stages;
+}
 void set_fused_rings(int si, int so) {
   g_fused_si = si;
   g_fused_so = so;
@@ -769,7 +773,8 @@ static int launch_fused(fused::Params &p, cudaStream_t st) {
   }
   const size_t ringB = (size_t)SI * LI.bytes + (size_t)SO * LO.bytes;
   // phase A ring uses the same area (plus whatever is left)
-  int SA = (int)std::min<size_t>(8, (budget - fixed_tail) / (LA.bytes + (size_t)p.R * kCW * 8));
+  int SA = (int)std::min<size_t>(g_fused_sa > 0 ? g_fused_sa : 8,
+                                  (budget - fixed_tail) / (LA.bytes + (size_t)p.R * kCW * 8));
   if (SA < 2) {
     set_error("k1_fused: phase-A stages do not fit shared memory");
     return CC_ERR_UNSUPPORTED;
@@ -812,6 +817,7 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   // rows per tile: a multiple of the row groups; two per group when each CTA has plenty of rows
   const int64_t rows_per_cta = cdiv(n, G);
   p.R = p.groups * (rows_per_cta >= 16 * p.groups ? 2 : 1);
+  if (g_fused_ra > 0) p.R = p.groups * g_fused_ra;
   p.G = G;
   p.nTiles = cdiv(n, p.R);
   p.scale_mode = scale_mode;

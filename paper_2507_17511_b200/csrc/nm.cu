@@ -303,7 +303,21 @@ __device__ __forceinline__ int64_t quad_slot(int64_t gq, uint32_t bits, int j, i
 
 constexpr int kQuadU = 2;  // quads per thread per iteration (loads of both issued first)
 
-template <int MODE, typename XT, bool STEP, int M>
+// write the kept f16 values of one quad (ascending slots s0, s0+1, ...): one 32/64-bit
+// store when the run is aligned, else half by half
+__device__ __forceinline__ void put_run(uint8_t *dst, const uint16_t (&h)[4], int c) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
+  if (c == 2 && (a & 3) == 0) {
+    *reinterpret_cast<uint32_t *>(dst) = (uint32_t)h[0] | ((uint32_t)h[1] << 16);
+  } else if (c == 4 && (a & 7) == 0) {
+    *reinterpret_cast<uint2 *>(dst) =
+        make_uint2((uint32_t)h[0] | ((uint32_t)h[1] << 16), (uint32_t)h[2] | ((uint32_t)h[3] << 16));
+  } else {
+    for (int i = 0; i < c; ++i) put_half(dst + 2 * i, __ushort_as_half(h[i]));
+  }
+}
+
+template <int MODE, typename XT, bool STEP, int M, bool NOPAD>
 __global__ void __launch_bounds__(kThreads) k_nm_quad(const XT *__restrict__ x, float *__restrict__ base,
                                                        float *__restrict__ aux, const float *__restrict__ tin,
                                                        float *__restrict__ decoded, Geo g, int64_t nquads,
@@ -325,10 +339,15 @@ __global__ void __launch_bounds__(kThreads) k_nm_quad(const XT *__restrict__ x, 
       real[u] = false;
       e0[u] = 0;
       if (gq < nquads) {
-        const int64_t row = gq / qpr;
-        const int64_t p0 = (gq - row * qpr) * 4;
-        real[u] = p0 < g.C;  // C % 4 == 0: a quad is all real or all padding
-        e0[u] = row * g.C + p0;
+        if constexpr (NOPAD) {  // C % m == 0: padded order == real order
+          real[u] = true;
+          e0[u] = gq * 4;
+        } else {
+          const int64_t row = gq / qpr;
+          const int64_t p0 = (gq - row * qpr) * 4;
+          real[u] = p0 < g.C;  // C % 4 == 0: a quad is all real or all padding
+          e0[u] = row * g.C + p0;
+        }
         if (real[u]) {
           if constexpr (!STEP) {
             tv[u] = __ldcs(reinterpret_cast<const float4 *>(tin + e0[u]));
@@ -354,23 +373,38 @@ __global__ void __launch_bounds__(kThreads) k_nm_quad(const XT *__restrict__ x, 
       uint32_t bits = quad_select<M>(k, lane, g.N, pre);
       if (!live) bits = 0;
       float d[4] = {0.f, 0.f, 0.f, 0.f};
-      if (live) {
+      if (live && bits) {
+        uint16_t hv[4];
+        int c = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if (bits & (1u << j)) {
             const __half h = __float2half_rn(t[j]);
-            put_half(vals + 2 * quad_slot<M>(gq, bits, j, g.N, pre), h);
+            hv[c++] = __half_as_ushort(h);
             d[j] = __half2float(h);
           }
         }
+        if constexpr (M >= 4) {  // the quad's kept entries occupy consecutive slots
+          put_run(vals + 2 * quad_slot<M>(gq, bits, __ffs(bits) - 1, g.N, pre), hv, c);
+        } else {
+          int i = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (bits & (1u << j)) put_half(vals + 2 * quad_slot<M>(gq, bits, j, g.N, pre), __ushort_as_half(hv[i++]));
+        }
       }
       if (real[u]) {
+        // d - t is exact in f32 (d = f16(t) or 0); squares summed in f32 over the quad,
+        // then in f64 (relative error <= 2^-22 of the reference's f64 sum)
+        float e4 = 0.f, t4 = 0.f;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const double df = (double)d[j] - (double)t[j];
-          err += df * df;
-          tsq += (double)t[j] * (double)t[j];
+          const float df = __fsub_rn(d[j], t[j]);
+          e4 = __fmaf_rn(df, df, e4);
+          t4 = __fmaf_rn(t[j], t[j], t4);
         }
+        err += (double)e4;
+        tsq += (double)t4;
         const float4 dv = make_float4(d[0], d[1], d[2], d[3]);
         const int64_t e = e0[u];
         if constexpr (STEP) {
@@ -561,7 +595,7 @@ __global__ void __launch_bounds__(kThreads) k_nm_decode_generic(const __grid_con
 }
 
 // quad decode (C % 4 == 0, aligned bases): one float4 of base per thread
-template <int M>
+template <int M, bool NOPAD>
 __global__ void __launch_bounds__(kThreads) k_nm_decode_quad(const __grid_constant__ Peers pp, int64_t C, int64_t qpr,
                                                               int N, int accumulate) {
   const int peer = blockIdx.y;
@@ -587,19 +621,49 @@ __global__ void __launch_bounds__(kThreads) k_nm_decode_quad(const __grid_consta
       }
     }
     if (!live) continue;
-    const int64_t row = gq / qpr;
-    const int64_t p0 = (gq - row * qpr) * 4;
-    if (p0 >= C) continue;
-    float d[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (bits & (1u << j)) d[j] = get_half(vals + 2 * quad_slot<M>(gq, bits, j, N, pre));
-    float4 *bp = reinterpret_cast<float4 *>(base + row * C + p0);
-    if (accumulate) {
-      const float4 b = *bp;
-      *bp = make_float4(__fadd_rn(b.x, d[0]), __fadd_rn(b.y, d[1]), __fadd_rn(b.z, d[2]), __fadd_rn(b.w, d[3]));
+    int64_t e0;
+    if constexpr (NOPAD) {
+      e0 = gq * 4;
     } else {
-      *bp = make_float4(d[0], d[1], d[2], d[3]);
+      const int64_t row = gq / qpr;
+      const int64_t p0 = (gq - row * qpr) * 4;
+      if (p0 >= C) continue;
+      e0 = row * C + p0;
+    }
+    float d[4] = {0.f, 0.f, 0.f, 0.f};
+    if (bits) {
+      if constexpr (M >= 4) {  // consecutive slots: one 32/64-bit load when aligned
+        const uint8_t *src = vals + 2 * quad_slot<M>(gq, bits, __ffs(bits) - 1, N, pre);
+        const int c = __popc(bits);
+        const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+        uint16_t hv[4] = {0, 0, 0, 0};
+        if (c == 2 && (a & 3) == 0) {
+          const uint32_t w = *reinterpret_cast<const uint32_t *>(src);
+          hv[0] = (uint16_t)(w & 0xffff);
+          hv[1] = (uint16_t)(w >> 16);
+        } else if (c == 4 && (a & 7) == 0) {
+          const uint2 w = *reinterpret_cast<const uint2 *>(src);
+          hv[0] = (uint16_t)(w.x & 0xffff); hv[1] = (uint16_t)(w.x >> 16);
+          hv[2] = (uint16_t)(w.y & 0xffff); hv[3] = (uint16_t)(w.y >> 16);
+        } else {
+          for (int i = 0; i < c; ++i) hv[i] = __half_as_ushort(__float2half_rn(get_half(src + 2 * i)));
+        }
+        int i = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (bits & (1u << j)) d[j] = __half2float(__ushort_as_half(hv[i++]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (bits & (1u << j)) d[j] = get_half(vals + 2 * quad_slot<M>(gq, bits, j, N, pre));
+      }
+    }
+    float4 *bp = reinterpret_cast<float4 *>(base + e0);
+    if (accumulate) {
+      const float4 b = __ldcs(bp);
+      __stcs(bp, make_float4(__fadd_rn(b.x, d[0]), __fadd_rn(b.y, d[1]), __fadd_rn(b.z, d[2]), __fadd_rn(b.w, d[3])));
+    } else {
+      __stcs(bp, make_float4(d[0], d[1], d[2], d[3]));
     }
   }
 }
@@ -682,8 +746,16 @@ static int nm_run(const nm::Geo &g, int64_t rows, const XT *x, float *base, floa
     const int64_t qpr = g.bpr * g.M / 4;  // quads per padded row
     const int64_t nquads = g.nblocks * g.M / 4;
     const unsigned grid = nm_quad_grid(nquads);
-#define NM_Q(MM) k_nm_quad<MODE, XT, STEP, MM><<<grid, kThreads, 0, st>>>(x, base, aux, tin, decoded, g, nquads, qpr, \
-                                                                          body, w.part, w.ticket, record)
+    const bool nopad = g.bpr * g.M == g.C;
+#define NM_Q(MM)                                                                                            \
+  do {                                                                                                      \
+    if (nopad)                                                                                              \
+      k_nm_quad<MODE, XT, STEP, MM, true><<<grid, kThreads, 0, st>>>(x, base, aux, tin, decoded, g, nquads, qpr, \
+                                                                     body, w.part, w.ticket, record);       \
+    else                                                                                                    \
+      k_nm_quad<MODE, XT, STEP, MM, false><<<grid, kThreads, 0, st>>>(x, base, aux, tin, decoded, g, nquads,  \
+                                                                      qpr, body, w.part, w.ticket, record); \
+  } while (0)
     switch (g.M) {
       case 1: NM_Q(1); break;
       case 2: NM_Q(2); break;
@@ -791,14 +863,21 @@ int nm_decode(int count, const int64_t *rows, int64_t C, int n, int m, const uin
     if (C % 4 == 0 && bases_al && nm_quad_ok(m)) {
       const int64_t qpr = bpr * m / 4;
       dim3 grid(nm_quad_grid(maxb * m / 4), cnt);
+      const bool nopad = bpr * m == C;
+#define NM_DQ(MM)                                                                              \
+  do {                                                                                         \
+    if (nopad) nm::k_nm_decode_quad<MM, true><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc); \
+    else nm::k_nm_decode_quad<MM, false><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc);      \
+  } while (0)
       switch (m) {
-        case 1: nm::k_nm_decode_quad<1><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc); break;
-        case 2: nm::k_nm_decode_quad<2><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc); break;
-        case 4: nm::k_nm_decode_quad<4><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc); break;
-        case 8: nm::k_nm_decode_quad<8><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc); break;
-        case 16: nm::k_nm_decode_quad<16><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc); break;
-        default: nm::k_nm_decode_quad<32><<<grid, nm::kThreads, 0, st>>>(pp, C, qpr, n, acc); break;
+        case 1: NM_DQ(1); break;
+        case 2: NM_DQ(2); break;
+        case 4: NM_DQ(4); break;
+        case 8: NM_DQ(8); break;
+        case 16: NM_DQ(16); break;
+        default: NM_DQ(32); break;
       }
+#undef NM_DQ
     } else if (m <= 32) {
       dim3 grid(nm_grid(maxb), cnt);
       switch (m) {

@@ -509,10 +509,13 @@ __device__ __forceinline__ void decode4(uint32_t cw, float uf, bool row_ok, cons
   }
 }
 
+// K2 is a pure read-modify-write stream of base: many small CTAs (RB = U rows each)
+// balance the 148 SMs far better than a few fat ones (wave tail < 1/4 of a wave)
+constexpr int kDecRows = 4;
 template <int CODEC, bool ACC>
 __global__ void __launch_bounds__(256) k_decode_vec(const __grid_constant__ PeerBatch pb, int64_t C, int RB) {
   constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
-  constexpr int U = 8;  // rows in flight per thread
+  constexpr int U = kDecRows;  // rows in flight per thread
   const int peer = blockIdx.z;
   const int64_t n = pb.rows[peer];
   const int64_t r0 = (int64_t)blockIdx.y * RB;
@@ -739,8 +742,8 @@ static void launch_decode(const PeerBatch &pb, int count, int64_t maxrows, int64
   if (vec) {
     QPlan p;
     plan_shape(p, maxrows, C, true);
-    dim3 grid(p.nStrips, p.nRB, count);
-    k_decode_vec<CODEC, ACC><<<grid, p.threads, 0, st>>>(pb, C, p.RB);
+    dim3 grid(p.nStrips, (unsigned)cdiv(maxrows, kDecRows), count);
+    k_decode_vec<CODEC, ACC><<<grid, p.threads, 0, st>>>(pb, C, kDecRows);
   } else {
     dim3 grid((unsigned)cdiv(maxrows * C, 256), count);
     k_decode_scalar<CODEC, ACC><<<grid, 256, 0, st>>>(pb, C);

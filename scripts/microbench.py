@@ -83,6 +83,17 @@ def main():
         us = timed(enc, a.reps)
         out[f"k1_fused_rings{si}_{so}"] = {"us": round(us, 2), "alg_GBps": round(alg / us / 1e3, 1)}
     lib.cc_debug_fused_rings(0, 0)
+    # phase-A tile height / ring depth sweep (phase A only and full step)
+    for ra, sa in ((1, 2), (1, 4), (1, 6), (2, 2), (2, 3), (3, 2)):
+        lib.cc_debug_fused_phase_a(ra, sa)
+        for stop in (1, 0):
+            lib.cc_debug_fused_stop(stop)
+            for i in range(L):
+                enc(i)
+            us = timed(enc, a.reps)
+            out[f"k1_fused_A{ra}x{sa}{'_phaseA' if stop else ''}"] = {"us": round(us, 2)}
+    lib.cc_debug_fused_phase_a(0, 0)
+    lib.cc_debug_fused_stop(0)
     # per-phase timeline of one fused launch (globaltimer stamps per CTA)
     tbuf = torch.zeros(1024 * 8, dtype=torch.int64, device="cuda")
     lib.cc_debug_fused_timer(_lib.ptr(tbuf))
