@@ -8,6 +8,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "../../include/compactcomm.h"
 #include "cc_internal.h"
@@ -39,6 +40,48 @@ int sm_count() {
     cached[dev] = v;
   }
   return cached[dev];
+}
+
+// Library-owned control words (tile counters, tickets) of the persistent
+// kernels: one zero-initialised 64-byte slot per (device, stream).  Every launch
+// leaves its slot zeroed on exit, so no per-launch memset node is needed;
+// launches on one stream are ordered, launches on different streams use
+// different slots.  Returns null (caller falls back to a memset'd workspace
+// word) if the pool cannot be created now, e.g. during a stream capture.
+uint8_t *stream_control_block(cudaStream_t st) {
+  constexpr int kSlots = 1024, kSlotBytes = 64;
+  struct Pool {
+    uint8_t *base = nullptr;
+    int used = 0;
+    std::unordered_map<cudaStream_t, int> slot;
+  };
+  static std::mutex mu;
+  static Pool pools[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  Pool &P = pools[dev];
+  if (!P.base) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    void *b = nullptr;
+    if (cudaMalloc(&b, (size_t)kSlots * kSlotBytes) != cudaSuccess || cudaMemset(b, 0, (size_t)kSlots * kSlotBytes) !=
+                                                                           cudaSuccess) {
+      cudaGetLastError();
+      if (b) cudaFree(b);
+      return nullptr;
+    }
+    P.base = static_cast<uint8_t *>(b);
+  }
+  auto it = P.slot.find(st);
+  if (it != P.slot.end()) return P.base + (size_t)it->second * kSlotBytes;
+  if (P.used == kSlots) return nullptr;
+  P.slot.emplace(st, P.used);
+  return P.base + (size_t)(P.used++) * kSlotBytes;
 }
 
 int64_t topk_workspace_bytes(int64_t n, int64_t C, int64_t k);

@@ -23,6 +23,10 @@ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // number of SMs of the current device (cached)
 int sm_count();
 
+// zero-initialised 64-byte control slot of `st` on the current device (see capi.cu);
+// persistent kernels must leave it zeroed on exit.  Null when unavailable.
+uint8_t *stream_control_block(cudaStream_t st);
+
 // --- quantizer family (quant.cu) ------------------------------------------
 int64_t quant_workspace_bytes(int64_t n, int64_t C);
 int quant_encode_step(int codec, int mode, int scale_mode, int64_t n, int64_t C, const void *x, int x_dtype,

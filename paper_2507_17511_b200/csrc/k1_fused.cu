@@ -57,12 +57,15 @@ struct Params {
   double *colpart, *rowpart, *blkpart, *recpart, *record;
   float *u, *v;
   uint8_t *codes, *body_u, *body_v;
-  unsigned int *ticket;
+  unsigned int *ticket;     // control words: zero on entry, left zero on exit
   unsigned long long *ctr;  // dynamic tile counters [phase A, phase B], zeroed before launch
   int scale_mode;
-  int stop_after;             // profiling: 1 = phase A only, 2 = A + scales, 0 = full
+  int stop_after;             // profiling: 1 = phase A only, 2 = A + scales, 3 = A w/o sync, 0 = full
+  int ctl_in_ws;              // control words live in the workspace (memset before launch)
   unsigned long long *timer;  // profiling: [G][8] globaltimer stamps, or null
-  int policy;                 // L2 policy experiment: 0 last/first, 1 normal/normal, 2 normal/first, 3 last/normal
+  int policy;  // experiment bits: 1 = phase-B stores without L2 hint, 2 = phase-B loads evict_first,
+               // 4 = phase-A loads evict_normal, 8 = phase-A consumers skip the math (timing only),
+               // 16 = skip phase-A row finishing (timing only), 32 = control words in the workspace
 };
 
 __device__ __forceinline__ uint64_t l2_policy_normal() {
@@ -287,8 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
 
   // ---- shared memory: [ring area][rp][red][ucache][barriers] ----
   uint8_t *ring = smem;
-  double *rp = reinterpret_cast<double *>(smem + p.ring_bytes);  // [SA][RA][kCW]
-  double *red = rp + (size_t)SA * RA * kCW;                      // [512]: block sums + column partials
+  double *rp = reinterpret_cast<double *>(smem + p.ring_bytes);  // [2 use parities][SA][RA][kCW]
+  double *red = rp + (size_t)2 * SA * RA * kCW;                  // [512]: block sums + column partials
   float *ucache = reinterpret_cast<float *>(red + 512);           // [kUCache]
   uint64_t *fullA = reinterpret_cast<uint64_t *>(ucache + kUCache);
   uint64_t *emptyA = fullA + SA;
@@ -327,31 +330,38 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   // ================= phase A: |t| partial sums over tiles of RA rows =================
   const InStage LA = in_stage<MODE, XT>(RA, C, MODE == CC_WITH_FEEDBACK);
   double cta_total = 0.0;
-  auto finish_rows = [&](int s, long long tile) {  // producer lanes: row sums of a finished tile
+  // producer lanes: row sums of a finished tile (stage s, use parity par)
+  auto finish_rows = [&](int s, long long tile, uint32_t par) {
     const int64_t r0 = (int64_t)tile * RA;
     if (lane < RA && r0 + lane < n) {
       double acc = 0.0;
-      for (int w = 0; w < p.wpg; ++w) acc += rp[((size_t)s * RA + lane) * kCW + w];
+      const double *q = rp + (((size_t)par * SA + s) * RA + lane) * kCW;
+      for (int w = 0; w < p.wpg; ++w) acc += q[w];
       p.rowpart[r0 + lane] = acc;
       cta_total += acc;
     }
   };
-  // dynamic tile scheduler: the loader claims tiles with an atomic counter and
-  // publishes the tile id with the stage (-1 = no more work)
+  // dynamic tile scheduler: the loader claims tiles with an atomic counter one
+  // tile AHEAD (the claim's L2 round trip hides behind the ring wait) and
+  // publishes the tile id with the stage (-1 = no more work).  Row sums of the
+  // tile a stage held are finished after its refill is issued (rp is
+  // double-buffered by use parity, so the new tile's partials cannot collide).
   if (loader) {
-    const uint64_t pol = l2_policy_evict_last();
+    const uint64_t pol = (p.policy & 4) ? l2_policy_normal() : l2_policy_evict_last();
     int k = 0, s = 0;
     uint32_t ph = 0;  // phase parity of stage s's current use
+    unsigned long long nxt = 0;
+    if (lane == 0) nxt = atomicAdd(p.ctr, 1ull);
     for (;;) {
+      long long old = -1;
       if (k >= SA) {
         mbar_wait(&emptyA[s], ph ^ 1u);
-        finish_rows(s, tileA[s]);
+        old = tileA[s];
       }
-      long long tile = 0;
-      if (lane == 0) tile = (long long)atomicAdd(p.ctr, 1ull);
-      tile = __shfl_sync(0xffffffffu, tile, 0);
+      long long tile = (long long)__shfl_sync(0xffffffffu, nxt, 0);
       if (tile >= p.nTiles) tile = -1;
       if (lane == 0) {
+        if (tile >= 0) nxt = atomicAdd(p.ctr, 1ull);
         tileA[s] = tile;
         if (tile < 0) {
           mbar_arrive(&fullA[s]);
@@ -368,6 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
         }
       }
       __syncwarp();
+      if (old >= 0 && !(p.policy & 16)) finish_rows(s, old, ph ^ 1u);
       if (tile < 0) break;
       ++k;
       if (++s == SA) {
@@ -381,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       const int sq = (s - q + SA) % SA;
       const uint32_t pq = (q <= s) ? ph : (ph ^ 1u);
       mbar_wait(&emptyA[sq], pq);
-      if (q > 0 && tileA[sq] >= 0) finish_rows(sq, tileA[sq]);
+      if (q > 0 && tileA[sq] >= 0) finish_rows(sq, tileA[sq], pq);
     }
   } else if (consumer) {
     double cs[Q][4];
@@ -399,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       }
       const uint8_t *st = ring + (size_t)s * LA.bytes;
       const int nrows = (int)min64(RA, n - (int64_t)tile * RA);
-      if (grp < p.groups) {
+      if (grp < p.groups && !(p.policy & 8)) {
         for (int r = grp; r < nrows; r += p.groups) {
           double rs = 0.0;
 #pragma unroll
@@ -419,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
             rs += ((a[0] + a[1]) + a[2]) + a[3];
           }
           rs = warp_sum(rs);
-          if (lane == 0) rp[((size_t)s * RA + r) * kCW + wig] = rs;
+          if (lane == 0) rp[(((size_t)ph * SA + s) * RA + r) * kCW + wig] = rs;
         }
       }
       __syncwarp();
@@ -451,6 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       }
     }
   }
+  if (p.stop_after == 3) return;
   {
     const double b = block_sum(loader ? cta_total : 0.0, red);
     if (tid == 0) p.blkpart[cta] = b;
@@ -462,7 +474,16 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   if (p.stop_after == 1) return;
 
   // ================= phase F: v_j, g, u_i =================
-  if (cta == 0 && tid == 0) *p.ticket = 0u;
+  if (cta == 0 && tid == 0) {  // control words are left zeroed for the next launch
+    *p.ticket = 0u;
+    p.ctr[0] = 0ull;  // every phase-A claim happened before the grid sync
+  }
+  // every phase-F load is issued before the first reduction (one L2 round trip):
+  // block partials (g), this CTA's row partials (u), then the column partials (v)
+  const double part = tid < G ? __ldcg(p.blkpart + tid) : 0.0;  // G <= kThreads (launcher)
+  const int64_t uch = (n + G - 1) / G;
+  const int64_t ui0 = (int64_t)cta * uch, ui1 = min64(n, ui0 + uch);
+  const double rs_first = ui0 + tid < ui1 ? __ldcg(p.rowpart + ui0 + tid) : 0.0;
   {
     // column sums: one CTA per 32-column group; warp w sums slots w, w + nw, ...
     // (loads issued together), then warp 0 adds the per-warp partials in order
@@ -495,13 +516,10 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   }
   stamp(7);
   {
-    const double part = tid < G ? __ldcg(p.blkpart + tid) : 0.0;  // G <= kThreads (launcher)
     const double tot = block_sum(part, red);
     const double g = tot / (double)(n * C);  // mean|t| (cx:142)
-    const int64_t ch = (n + G - 1) / G;
-    const int64_t i0 = (int64_t)cta * ch, i1 = min64(n, i0 + ch);
-    for (int64_t i = i0 + tid; i < i1; i += kThreads) {
-      const double rs = __ldcg(p.rowpart + i);
+    for (int64_t i = ui0 + tid; i < ui1; i += kThreads) {
+      const double rs = i == ui0 + tid ? rs_first : __ldcg(p.rowpart + i);
       float u;
       if (p.scale_mode == CC_SCALE_PER_CHANNEL) u = 1.0f;
       else if (p.scale_mode == CC_SCALE_PER_TOKEN) u = (float)(rs / (double)C);
@@ -527,16 +545,18 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   const int64_t nTB = (n + RB - 1) / RB;  // tiles claimed in REVERSE row order
   double err = 0.0, tsq = 0.0;
   if (loader) {
-    const uint64_t pol = l2_policy_evict_first();
+    // phase-B loads: evict_normal (measured ~1 us better than evict_first at [4096, 3072])
+    const uint64_t pol = (p.policy & 2) ? l2_policy_evict_first() : l2_policy_normal();
     int k = 0, s = 0;
     uint32_t ph = 0;
+    unsigned long long nxt = 0;  // claims run one tile ahead (as in phase A)
+    if (lane == 0) nxt = atomicAdd(p.ctr + 1, 1ull);
     for (;;) {
       if (k >= SI) mbar_wait(&emptyB[s], ph ^ 1u);
-      long long t = 0;
-      if (lane == 0) t = (long long)atomicAdd(p.ctr + 1, 1ull);
-      t = __shfl_sync(0xffffffffu, t, 0);
+      const long long t = (long long)__shfl_sync(0xffffffffu, nxt, 0);
       const long long tile = t < nTB ? nTB - 1 - t : -1;
       if (lane == 0) {
+        if (tile >= 0) nxt = atomicAdd(p.ctr + 1, 1ull);
         tileB[s] = tile;
         if (tile < 0) {
           mbar_arrive(&fullB[s]);
@@ -566,6 +586,8 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   } else if (storer) {
     int o = 0;
     uint32_t ph = 0;
+    const bool hint = !(p.policy & 1);  // results are not re-read in this launch: evict_first
+    const uint64_t spol = l2_policy_evict_first();
     for (;; o = (o + 1 == SO) ? 0 : o + 1, ph ^= (o == 0)) {
       mbar_wait(&outFull[o], ph);
       const long long tile = tileO[o];
@@ -574,8 +596,13 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
         const uint8_t *so = out_ring + (size_t)o * LO.bytes;
         const int64_t r0 = (int64_t)tile * RB;
         const int nrows = (int)min64(RB, n - r0);
-        bulk_s2g(p.base + r0 * C, so + LO.base, (uint32_t)(nrows * C * 4));
-        if constexpr (has_aux<MODE>()) bulk_s2g(p.aux + r0 * C, so + LO.aux, (uint32_t)(nrows * C * 4));
+        if (hint) {
+          bulk_s2g_hint(p.base + r0 * C, so + LO.base, (uint32_t)(nrows * C * 4), spol);
+          if constexpr (has_aux<MODE>()) bulk_s2g_hint(p.aux + r0 * C, so + LO.aux, (uint32_t)(nrows * C * 4), spol);
+        } else {
+          bulk_s2g(p.base + r0 * C, so + LO.base, (uint32_t)(nrows * C * 4));
+          if constexpr (has_aux<MODE>()) bulk_s2g(p.aux + r0 * C, so + LO.aux, (uint32_t)(nrows * C * 4));
+        }
         bulk_s2g(p.codes + r0 * p.cb_row, so + LO.codes, (uint32_t)(nrows * p.cb_row));
         bulk_commit();
         bulk_wait_read<0>();  // smem source consumed -> the slot may be rewritten
@@ -583,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       }
       __syncwarp();
     }
-    if (lane == 0) bulk_wait<0>();
+    if (lane == 0) bulk_wait_read<0>();  // smem sources consumed; the global writes complete on their own
     __syncwarp();
   } else {
     ColConst cc[Q];
@@ -696,6 +723,8 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       if (tid == 0) {
         p.record[0] = a;
         p.record[1] = b;
+        p.ctr[1] = 0ull;  // every CTA finished claiming phase-B tiles before taking its ticket
+        *p.ticket = 0u;
       }
     }
   }
@@ -757,9 +786,18 @@ static int launch_fused(fused::Params &p, cudaStream_t st) {
   const InStage LI = in_stage<MODE, XT>(p.groups, p.C, has_aux<MODE>());
   const OutStage LO = out_stage<MODE>(p.groups, p.C, p.cb_row);
   const InStage LA = in_stage<MODE, XT>(p.R, p.C, MODE == CC_WITH_FEEDBACK);
+  // phase A ring + its row-partial scratch (2 use parities x SA stages)
+  int SA = (int)std::min<size_t>(g_fused_sa > 0 ? g_fused_sa : 8,
+                                  (budget - fixed_tail) / (LA.bytes + (size_t)2 * p.R * kCW * 8));
+  if (SA < 2) {
+    set_error("k1_fused: phase-A stages do not fit shared memory");
+    return CC_ERR_UNSUPPORTED;
+  }
+  const size_t rp_bytes = (size_t)2 * SA * p.R * kCW * 8;
+  // phase B rings share the ring area: loads S_in, outputs S_out
   int SO = g_fused_so > 0 ? g_fused_so : 2, SI = 0;
   for (;;) {
-    const size_t avail = budget - fixed_tail - (size_t)3 * p.R * kCW * 8;
+    const size_t avail = budget - fixed_tail - rp_bytes;
     if ((size_t)SO * LO.bytes + 2 * (size_t)LI.bytes <= avail) {
       SI = (int)std::min<size_t>(g_fused_si > 0 ? g_fused_si : 8, (avail - (size_t)SO * LO.bytes) / LI.bytes);
       break;
@@ -772,24 +810,17 @@ static int launch_fused(fused::Params &p, cudaStream_t st) {
     return CC_ERR_UNSUPPORTED;
   }
   const size_t ringB = (size_t)SI * LI.bytes + (size_t)SO * LO.bytes;
-  // phase A ring uses the same area (plus whatever is left)
-  int SA = (int)std::min<size_t>(g_fused_sa > 0 ? g_fused_sa : 8,
-                                  (budget - fixed_tail) / (LA.bytes + (size_t)p.R * kCW * 8));
-  if (SA < 2) {
-    set_error("k1_fused: phase-A stages do not fit shared memory");
-    return CC_ERR_UNSUPPORTED;
-  }
   const size_t ringA = (size_t)SA * LA.bytes;
   p.S = SA;
   p.S_in = SI;
   p.S_out = SO;
   p.ring_bytes = (uint32_t)align_up(std::max(ringA, ringB), 128);
-  const size_t smem = p.ring_bytes + (size_t)SA * p.R * kCW * 8 + 512 * 8 + kUCache * 4 +
+  const size_t smem = p.ring_bytes + rp_bytes + 512 * 8 + kUCache * 4 +
                       (size_t)(3 * SA + 3 * SI + 3 * SO) * 8 + 16 + (size_t)SI * 64 + 128;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return cuda_status("k1_fused attr");
   void *args[] = {&p};
-  cudaMemsetAsync(p.ctr, 0, 2 * sizeof(unsigned long long), st);  // dynamic tile counters
+  if (p.ctl_in_ws) cudaMemsetAsync(p.ctr, 0, 2 * sizeof(unsigned long long), st);  // tile counters
   cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(p.G), dim3(kThreads), args, smem, st);
   if (e != cudaSuccess) {
     set_error(std::string("k1_fused launch: ") + cudaGetErrorString(e));
@@ -846,6 +877,14 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   p.v = reinterpret_cast<float *>(take(sizeof(float) * C));
   p.ticket = reinterpret_cast<unsigned int *>(take(256));
   p.ctr = reinterpret_cast<unsigned long long *>(take(256));
+  // control words: the stream's library-owned slot (kept zero by every launch), or
+  // the workspace + a memset when there is none / a debug stop exits early
+  uint8_t *ctl = (g_fused_stop == 0 && !(g_fused_policy & 32)) ? stream_control_block(st) : nullptr;
+  p.ctl_in_ws = ctl == nullptr;
+  if (ctl) {
+    p.ctr = reinterpret_cast<unsigned long long *>(ctl);
+    p.ticket = reinterpret_cast<unsigned int *>(ctl + 16);
+  }
   if ((int64_t)off > ws_bytes) {
     set_error("fused workspace too small");
     return CC_ERR_ARG;

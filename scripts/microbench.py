@@ -22,13 +22,26 @@ from paper_2507_17511_b200 import compressors as cx  # noqa: E402
 from paper_2507_17511_b200 import pipeline as pl  # noqa: E402
 
 
-def timed(fn, reps):
+def timed(fn, reps, graph=True):
+    """Mean µs per call.  graph=True captures the `reps` calls into one CUDA graph
+    and times a replay, so host launch overhead never leaves the GPU idle."""
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    s.record()
-    for i in range(reps):
-        fn(i)
-    e.record()
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=torch.cuda.current_stream()):
+            for i in range(reps):
+                fn(i)
+        g.replay()
+        torch.cuda.synchronize()
+        s.record()
+        g.replay()
+        e.record()
+    else:
+        s.record()
+        for i in range(reps):
+            fn(i)
+        e.record()
     torch.cuda.synchronize()
     return s.elapsed_time(e) * 1e3 / reps
 
@@ -42,6 +55,7 @@ def main():
     ap.add_argument("--reps", type=int, default=48)
     a = ap.parse_args()
     lib = _lib.load()
+    torch.cuda.set_stream(torch.cuda.Stream())  # a capturable (non-legacy) stream for every launch
     n, c, L = a.rows, a.cols, a.layers
     spec = cx.CompressorSpec(cx.CompressorKind(a.codec))
     bits = {"sign1bit": 1, "quant2bit": 2, "quant4bit": 4}[a.codec]
@@ -76,6 +90,21 @@ def main():
         out[name] = {"us": round(us, 2), "alg_GBps": round(alg / us / 1e3, 1)}
     lib.cc_set_quant_path(-1)
     lib.cc_debug_fused_stop(0)
+    # experiment bits (k1_fused.cu Params::policy): 1 = phase-B stores without L2 hint,
+    # 2 = phase-B loads evict_first, 4 = phase-A loads evict_normal, 8 = phase-A
+    # consumers skip the math, 16 = skip row finishing, 32 = control words in the workspace
+    for pol, stop in ((1, 0), (2, 0), (3, 0), (4, 0), (32, 0), (0, 1), (8, 1), (0, 3), (8, 3), (24, 3)):
+        lib.cc_debug_fused_policy(pol)
+        lib.cc_debug_fused_stop(stop)
+        for i in range(L):
+            enc(i)
+        us = timed(enc, a.reps)
+        out[f"k1_fused_policy{pol}{'_stop%d' % stop if stop else ''}"] = {"us": round(us, 2)}
+    lib.cc_debug_fused_policy(0)
+    lib.cc_debug_fused_stop(0)
+    if os.environ.get("MB_K1_ONLY"):
+        print(json.dumps({"shape": [n, c], "codec": a.codec, **out}))
+        return
     for si, so in ((6, 1), (4, 2), (3, 3), (2, 4)):
         lib.cc_debug_fused_rings(si, so)
         for i in range(L):
@@ -144,7 +173,7 @@ def main():
         for backend in (1, 0):
             lib.cc_set_lowrank_backend(backend)
             cx.encode_lowrank(xt, sp, la.make_rng(0))
-            us = timed(lambda i: cx.encode_lowrank(xt, sp, la.make_rng(i)), 5)
+            us = timed(lambda i: cx.encode_lowrank(xt, sp, la.make_rng(i)), 5, graph=False)
             out[f"lowrank_r{r}_{'tc' if backend else 'f64'}"] = {"us": round(us, 1)}
     lib.cc_set_lowrank_backend(1)
     # top-k encode_step (residual + select + ordered write + sparse update)
@@ -153,7 +182,7 @@ def main():
         st = pl.LayerState("residual_with_feedback", 1, torch.zeros(n, c, device="cuda"))
         pl.encode_step(st, xs[0], sp)
         pl.encode_step(st, xs[1], sp)
-        us = timed(lambda i: pl.encode_step(st, xs[i % 2], sp), 10)
+        us = timed(lambda i: pl.encode_step(st, xs[i % 2], sp), 10, graph=False)
         out[f"topk_step_{f}"] = {"us": round(us, 1)}
     # N:M encode_step (one fused pass) and its K2 decode, L2-cold layer rotation
     for (nn, mm) in ((2, 4), (1, 4), (4, 8), (8, 16), (16, 32), (3, 5)):
