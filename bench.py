@@ -416,7 +416,7 @@ def run_b200(a, world, rank):
                     "k2_gbs": (k2_bytes / (k2_ms / 1e3) / 1e9) if k2_ms else None,
                     "path_ideal_ms_per_layer": path_bytes / (peak * 1e9) * 1e3},
         "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s", "frac": k1_gbs / peak,
-                     "traffic": traffic, "kernel": "K1 encode_step (k_scale_vec + finalize + k_quant_vec)",
+                     "traffic": traffic, "kernel": "K1 encode_step (k1_fused: persistent residual -> scales -> quantize/pack -> state update)",
                      "algorithmic_bytes_per_launch": k1_bytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs"
                      if "hbm_gbs" in peaks else "fallback 6.65 TB/s"},
         "gpu_launches": launches,

@@ -43,13 +43,13 @@ int sm_count() {
 }
 
 // Library-owned control words (tile counters, tickets) of the persistent
-// kernels: one zero-initialised 64-byte slot per (device, stream).  Every launch
+// kernels: one zero-initialised 512-byte slot per (device, stream).  Every launch
 // leaves its slot zeroed on exit, so no per-launch memset node is needed;
 // launches on one stream are ordered, launches on different streams use
 // different slots.  Returns null (caller falls back to a memset'd workspace
 // word) if the pool cannot be created now, e.g. during a stream capture.
 uint8_t *stream_control_block(cudaStream_t st) {
-  constexpr int kSlots = 1024, kSlotBytes = 64;
+  constexpr int kSlots = 1024, kSlotBytes = 512;
   struct Pool {
     uint8_t *base = nullptr;
     int used = 0;

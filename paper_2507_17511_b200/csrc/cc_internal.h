@@ -23,7 +23,7 @@ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // number of SMs of the current device (cached)
 int sm_count();
 
-// zero-initialised 64-byte control slot of `st` on the current device (see capi.cu);
+// zero-initialised 512-byte control slot of `st` on the current device (see capi.cu);
 // persistent kernels must leave it zeroed on exit.  Null when unavailable.
 uint8_t *stream_control_block(cudaStream_t st);
 

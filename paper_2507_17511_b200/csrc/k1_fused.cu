@@ -58,14 +58,18 @@ struct Params {
   float *u, *v;
   uint8_t *codes, *body_u, *body_v;
   unsigned int *ticket;     // control words: zero on entry, left zero on exit
+  unsigned int *bar;        // grid hand-off counters bar1 = bar[0], bar2 = bar[32] (control words)
   unsigned long long *ctr;  // dynamic tile counters [phase A, phase B], zeroed before launch
   int scale_mode;
   int stop_after;             // profiling: 1 = phase A only, 2 = A + scales, 3 = A w/o sync, 0 = full
   int ctl_in_ws;              // control words live in the workspace (memset before launch)
+  long long early_tiles;      // phase-A tiles loaded L2::evict_first (the rest evict_last)
   unsigned long long *timer;  // profiling: [G][8] globaltimer stamps, or null
   int policy;  // experiment bits: 1 = phase-B stores without L2 hint, 2 = phase-B loads evict_first,
                // 4 = phase-A loads evict_normal, 8 = phase-A consumers skip the math (timing only),
-               // 16 = skip phase-A row finishing (timing only), 32 = control words in the workspace
+               // 16 = skip phase-A row finishing (timing only), 32 = control words in the workspace,
+               // 64 = phase-B consumers skip loads/math/results (timing only), 128 = phase-B results
+               // stored directly from registers (no output ring / TMA stores)
 };
 
 __device__ __forceinline__ uint64_t l2_policy_normal() {
@@ -213,6 +217,25 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// grid hand-off wait: spin until *p >= target (acquire)
+__device__ __forceinline__ void spin_until(const unsigned *p, unsigned target) {
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if (v >= target) break;
+  }
+}
+
+// grid hand-off arrival: release-ordered add (cumulative over the CTA's writes
+// ordered before it by a barrier)
+__device__ __forceinline__ void arrive_release(unsigned *p) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 template <int MODE>
 constexpr bool has_aux() {
   return MODE != CC_NAIVE;
@@ -299,7 +322,8 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   uint64_t *emptyB = fullB + SI;
   uint64_t *outFull = emptyB + SI;
   uint64_t *outFree = outFull + SO;
-  volatile long long *tileA = reinterpret_cast<volatile long long *>(outFree + SO);  // [SA]
+  uint64_t *handA = outFree + SO;  // CTA-local relays of the grid hand-offs (bar1, bar2)
+  volatile long long *tileA = reinterpret_cast<volatile long long *>(handA + 2);  // [SA]
   volatile long long *tileB = tileA + SA;                                           // [SI]
   volatile long long *tileO = tileB + SI;                                           // [SO]
   float *ustage = reinterpret_cast<float *>(
@@ -322,6 +346,8 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       mbar_init(&outFull[s], kCW);
       mbar_init(&outFree[s], 1);
     }
+    mbar_init(&handA[0], 1);
+    mbar_init(&handA[1], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -341,13 +367,39 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       cta_total += acc;
     }
   };
-  // dynamic tile scheduler: the loader claims tiles with an atomic counter one
-  // tile AHEAD (the claim's L2 round trip hides behind the ring wait) and
-  // publishes the tile id with the stage (-1 = no more work).  Row sums of the
+  // ---- phase-B ring geometry (shared by every role) ----
+  // Phase-B tiles are RB (= row groups) rows, visited in REVERSE order (phase A's
+  // tail is L2-resident); a load ring (S_in) and a separate output ring (S_out)
+  // drained by the store warp with TMA bulk stores, so loads never wait for stores.
+  const InStage LI = in_stage<MODE, XT>(RB, C, has_aux<MODE>());
+  const OutStage LO = out_stage<MODE>(RB, C, p.cb_row);
+  uint8_t *in_ring = ring;
+  uint8_t *out_ring = ring + (size_t)SI * LI.bytes;
+  const int64_t nTB = (n + RB - 1) / RB;
+  unsigned int *bar1 = p.bar, *bar2 = p.bar + 32;  // separate 128-byte lines
+  double err = 0.0, tsq = 0.0;
+
+  // Grid-wide hand-offs are flag barriers (arrive = fence + atomicAdd, wait = one
+  // thread spinning on ld.acquire, then a CTA-local named barrier) instead of
+  // grid.sync, so the loader never stalls with the rest of the grid:
+  //   bar1 (2 arrivals per CTA: loader rows + consumer columns) = phase A done;
+  //   bar2 (2 arrivals per CTA: consumers v, store warp u) = scales published.
+  // While the consumers run the scale pass, the loader already streams phase B's
+  // first S_in tiles (only their u windows wait for bar2).
+  //
+  // Phase A uses a dynamic tile scheduler: the loader claims tiles with an atomic
+  // counter one tile AHEAD (the claim's L2 round trip hides behind the ring wait)
+  // and publishes the tile id with the stage (-1 = no more work).  Row sums of the
   // tile a stage held are finished after its refill is issued (rp is
   // double-buffered by use parity, so the new tile's partials cannot collide).
   if (loader) {
-    const uint64_t pol = (p.policy & 4) ? l2_policy_normal() : l2_policy_evict_last();
+   {  // phase A
+    const uint64_t pol_late = (p.policy & 4) ? l2_policy_normal() : l2_policy_evict_last();
+    const uint64_t pol_early = l2_policy_evict_first();
+    // Only the last ~kL2KeepBytes of phase A stay L2-resident (evict_last) for the
+    // reverse-order phase B; earlier tiles are loaded evict_first so they do not
+    // compete (measured at [4096, 3072]: 70 % evict_first is ~2 us faster than 0 %).
+    const long long early = p.early_tiles;
     int k = 0, s = 0;
     uint32_t ph = 0;  // phase parity of stage s's current use
     unsigned long long nxt = 0;
@@ -368,6 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
         } else {
           uint8_t *st = ring + (size_t)s * LA.bytes;
           const int64_t r0 = (int64_t)tile * RA;
+          const uint64_t pol = tile < early ? pol_early : pol_late;
           const int nrows = (int)min64(RA, n - r0);
           const uint32_t xb = (uint32_t)(nrows * C * sizeof(XT)), fb = (uint32_t)(nrows * C * 4);
           const bool wb = MODE == CC_WITH_FEEDBACK;
@@ -394,10 +447,143 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       mbar_wait(&emptyA[sq], pq);
       if (q > 0 && tileA[sq] >= 0) finish_rows(sq, tileA[sq], pq);
     }
-  } else if (consumer) {
+   }
+    // CTA |t| total: the row sums live in lanes < RA
+    {
+      const double tot = warp_sum(cta_total);
+      if (lane == 0) p.blkpart[cta] = tot;
+      __syncwarp();
+      if (lane == 0) arrive_release(bar1);
+    }
+    if (p.stop_after) return;
+    // Phase B.  The first S_in tiles are loaded while the consumers still run
+    // the scale pass; their u windows follow once bar2 publishes u.
+    // phase-B loads: evict_normal (measured ~1 us better than evict_first at [4096, 3072])
+    const uint64_t pol = (p.policy & 2) ? l2_policy_evict_first() : l2_policy_normal();
+    int k = 0, s = 0;
+    uint32_t ph = 0;
+    bool u_ready = false;
+    unsigned long long nxt = 0;  // claims run one tile ahead (as in phase A)
+    if (lane == 0) nxt = atomicAdd(p.ctr + 16, 1ull);
+    auto load_u = [&](int st_, long long tile) {  // lane 0: 16B-aligned window of u for the tile's rows
+      const int64_t r0 = (int64_t)tile * RB;
+      const int nrows = (int)min64(RB, n - r0);
+      const uint32_t ub = (uint32_t)(((r0 & 3) + nrows + 3) / 4 * 16);
+      bulk_g2s(ustage + (size_t)st_ * 16, p.u + (r0 & ~3LL), ub, &fullB[st_], pol);
+    };
+    auto publish_u = [&](int nst) {
+      if (lane == 0) {
+        mbar_wait(&handA[1], 0);  // relayed by consumer thread 0, the CTA's only poller
+        fence_proxy_async_global();  // u was written through the generic proxy; TMA reads it
+        for (int q = 0; q < nst; ++q)
+          if (tileB[q] >= 0) load_u(q, tileB[q]);
+      }
+      __syncwarp();
+      u_ready = true;
+    };
+    for (;;) {
+      if (k >= SI) {
+        if (!u_ready) publish_u(SI);
+        mbar_wait(&emptyB[s], ph ^ 1u);
+      }
+      const long long t = (long long)__shfl_sync(0xffffffffu, nxt, 0);
+      const long long tile = t < nTB ? nTB - 1 - t : -1;
+      if (lane == 0) {
+        if (tile >= 0) nxt = atomicAdd(p.ctr + 16, 1ull);
+        tileB[s] = tile;
+        if (tile < 0) {
+          mbar_arrive(&fullB[s]);
+        } else {
+          uint8_t *st = in_ring + (size_t)s * LI.bytes;
+          const int64_t r0 = (int64_t)tile * RB;
+          const int nrows = (int)min64(RB, n - r0);
+          const uint32_t xb = (uint32_t)(nrows * C * sizeof(XT)), fb = (uint32_t)(nrows * C * 4);
+          const uint32_t ub = (uint32_t)(((r0 & 3) + nrows + 3) / 4 * 16);
+          mbar_expect_tx(&fullB[s], xb + (has_aux<MODE>() ? 2 * fb : 0u) + ub);
+          if (u_ready) load_u(s, tile);
+          bulk_g2s(st + LI.x, X + r0 * C, xb, &fullB[s], pol);
+          if (has_aux<MODE>()) {
+            bulk_g2s(st + LI.base, p.base + r0 * C, fb, &fullB[s], pol);
+            bulk_g2s(st + LI.aux, p.aux + r0 * C, fb, &fullB[s], pol);
+          }
+        }
+      }
+      __syncwarp();
+      if (tile < 0) break;
+      ++k;
+      if (++s == SI) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+    if (!u_ready) publish_u(k + 1);  // fewer than S_in tiles: stages 0..k (the last one is the sentinel)
+  } else if (storer) {
+    if (p.stop_after == 1 || p.stop_after == 3) return;
+    // ---- scale pass, row half (the consumers do the columns): g, u_i ----
+    {
+      // every load in flight before the reductions: block partials, then this CTA's row partials
+      mbar_wait(&handA[0], 0);  // bar1, relayed by consumer thread 0
+      double part = 0.0;
+      for (int i = lane; i < G; i += 32) part += __ldcg(p.blkpart + i);
+      const int64_t uch = (n + G - 1) / G;
+      const int64_t ui0 = (int64_t)cta * uch, ui1 = min64(n, ui0 + uch);
+      constexpr int kU = 4;
+      double rs[kU];
+#pragma unroll
+      for (int q = 0; q < kU; ++q) rs[q] = ui0 + lane + 32 * q < ui1 ? __ldcg(p.rowpart + ui0 + lane + 32 * q) : 0.0;
+      const double g = warp_sum(part) / (double)(n * C);  // mean|t| (cx:142); same order in every CTA
+      for (int64_t i0 = ui0; i0 < ui1; i0 += 32 * kU) {
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+          const int64_t i = i0 + lane + 32 * q;
+          if (i >= ui1) continue;
+          const double r = i0 == ui0 ? rs[q] : __ldcg(p.rowpart + i);
+          float u;
+          if (p.scale_mode == CC_SCALE_PER_CHANNEL) u = 1.0f;
+          else if (p.scale_mode == CC_SCALE_PER_TOKEN) u = (float)(r / (double)C);
+          else if (g == 0.0) u = 1.0f;
+          else u = (float)fmax((r / (double)C) / g, kRowScaleFloor);  // cx:147
+          p.u[i] = u;
+          store_f32_bytes(p.body_u + 4 * i, u);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) arrive_release(bar2);
+    }
+    if (p.stop_after) return;
+    int o = 0;
+    uint32_t ph = 0;
+    const bool hint = !(p.policy & 1);  // results are not re-read in this launch: evict_first
+    const uint64_t spol = l2_policy_evict_first();
+    for (;; o = (o + 1 == SO) ? 0 : o + 1, ph ^= (o == 0)) {
+      mbar_wait(&outFull[o], ph);
+      const long long tile = tileO[o];
+      if (tile < 0) break;
+      if (lane == 0 && !(p.policy & 128)) {
+        const uint8_t *so = out_ring + (size_t)o * LO.bytes;
+        const int64_t r0 = (int64_t)tile * RB;
+        const int nrows = (int)min64(RB, n - r0);
+        if (hint) {
+          bulk_s2g_hint(p.base + r0 * C, so + LO.base, (uint32_t)(nrows * C * 4), spol);
+          if constexpr (has_aux<MODE>()) bulk_s2g_hint(p.aux + r0 * C, so + LO.aux, (uint32_t)(nrows * C * 4), spol);
+        } else {
+          bulk_s2g(p.base + r0 * C, so + LO.base, (uint32_t)(nrows * C * 4));
+          if constexpr (has_aux<MODE>()) bulk_s2g(p.aux + r0 * C, so + LO.aux, (uint32_t)(nrows * C * 4));
+        }
+        bulk_s2g(p.codes + r0 * p.cb_row, so + LO.codes, (uint32_t)(nrows * p.cb_row));
+        bulk_commit();
+        bulk_wait_read<0>();  // smem source consumed -> the slot may be rewritten
+      }
+      if (lane == 0) mbar_arrive(&outFree[o]);
+      __syncwarp();
+    }
+    if (lane == 0) bulk_wait_read<0>();  // smem sources consumed; the global writes complete on their own
+    __syncwarp();
+  } else {
     double cs[Q][4];
 #pragma unroll
     for (int j = 0; j < Q; ++j) cs[j][0] = cs[j][1] = cs[j][2] = cs[j][3] = 0.0;
+   {  // phase A
     int s = 0;
     uint32_t ph = 0;
     for (;; s = (s + 1 == SA) ? 0 : s + 1, ph ^= (s == 0)) {
@@ -436,8 +622,9 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       __syncwarp();
       if (lane == 0) mbar_arrive(&emptyA[s]);
     }
+   }
     if constexpr (Q == 1) {  // merge row groups' column partials in a fixed order
-      double *xchg = reinterpret_cast<double *>(ring);
+      double *xchg = reinterpret_cast<double *>(out_ring);  // in_ring is being refilled by the loader
       named_sync(1, kCons);
       if (in_group && qact[0]) {
 #pragma unroll
@@ -461,158 +648,68 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
         cp[0] = cs[j][0]; cp[1] = cs[j][1]; cp[2] = cs[j][2]; cp[3] = cs[j][3];
       }
     }
-  }
-  if (p.stop_after == 3) return;
-  {
-    const double b = block_sum(loader ? cta_total : 0.0, red);
-    if (tid == 0) p.blkpart[cta] = b;
-  }
-  stamp(1);
-  cg::grid_group grid = cg::this_grid();
-  grid.sync();
-  stamp(2);
-  if (p.stop_after == 1) return;
-
-  // ================= phase F: v_j, g, u_i =================
-  if (cta == 0 && tid == 0) {  // control words are left zeroed for the next launch
-    *p.ticket = 0u;
-    p.ctr[0] = 0ull;  // every phase-A claim happened before the grid sync
-  }
-  // every phase-F load is issued before the first reduction (one L2 round trip):
-  // block partials (g), this CTA's row partials (u), then the column partials (v)
-  const double part = tid < G ? __ldcg(p.blkpart + tid) : 0.0;  // G <= kThreads (launcher)
-  const int64_t uch = (n + G - 1) / G;
-  const int64_t ui0 = (int64_t)cta * uch, ui1 = min64(n, ui0 + uch);
-  const double rs_first = ui0 + tid < ui1 ? __ldcg(p.rowpart + ui0 + tid) : 0.0;
-  {
-    // column sums: one CTA per 32-column group; warp w sums slots w, w + nw, ...
-    // (loads issued together), then warp 0 adds the per-warp partials in order
-    constexpr int nw = kThreads / 32;
-    constexpr int kPer = (kThreads + nw - 1) / nw;  // >= ceil(G / nw) since G <= kThreads
-    double *wpart = red + 16;                       // [nw][32] doubles after the block-sum scratch
-    for (int64_t grp32 = cta; grp32 * 32 < C; grp32 += G) {
-      const int64_t j = grp32 * 32 + lane;
-      double vals[kPer];
-#pragma unroll
-      for (int q = 0; q < kPer; ++q) {
-        const int slot = warp + nw * q;
-        vals[q] = (slot < G && j < C) ? __ldcg(p.colpart + (int64_t)slot * C + j) : 0.0;
-      }
-      double acc = 0.0;
-#pragma unroll
-      for (int q = 0; q < kPer; ++q) acc += vals[q];
-      wpart[warp * 32 + lane] = acc;
-      __syncthreads();
-      if (warp == 0 && j < C) {
-        double sacc = 0.0;
-        for (int w = 0; w < nw; ++w) sacc += wpart[w * 32 + lane];
-        float v = (float)(sacc / (double)n);  // colmean (cx:148)
-        if (p.scale_mode == CC_SCALE_PER_TOKEN) v = 1.0f;
-        p.v[j] = v;
-        store_f32_bytes(p.body_v + 4 * j, v);
-      }
-      __syncthreads();
+    // ---- hand-off 1: column partials published, wait for every CTA's phase A ----
+    named_sync(1, kCons);
+    if (tid == 0) arrive_release(bar1);
+    if (p.stop_after == 3) return;
+    stamp(1);
+    if (tid == 0) {
+      spin_until(bar1, 2u * G);
+      mbar_arrive(&handA[0]);  // relay to the store warp
     }
-  }
-  stamp(7);
-  {
-    const double tot = block_sum(part, red);
-    const double g = tot / (double)(n * C);  // mean|t| (cx:142)
-    for (int64_t i = ui0 + tid; i < ui1; i += kThreads) {
-      const double rs = i == ui0 + tid ? rs_first : __ldcg(p.rowpart + i);
-      float u;
-      if (p.scale_mode == CC_SCALE_PER_CHANNEL) u = 1.0f;
-      else if (p.scale_mode == CC_SCALE_PER_TOKEN) u = (float)(rs / (double)C);
-      else if (g == 0.0) u = 1.0f;
-      else u = (float)fmax((rs / (double)C) / g, kRowScaleFloor);  // cx:147
-      p.u[i] = u;
-      store_f32_bytes(p.body_u + 4 * i, u);
-    }
-  }
-  stamp(3);
-  grid.sync();
-  stamp(4);
-  if (p.stop_after == 2) return;
+    named_sync(1, kCons);
+    stamp(2);
+    if (p.stop_after == 1) return;
 
-  // ================= phase B: quantize, pack, update state =================
-  // tiles of RB (= row groups) rows, visited in reverse order (phase A's tail is
-  // L2-resident); a load ring (S_in) and a separate output ring (S_out) drained
-  // by the store warp with TMA bulk stores, so loads never wait for stores.
-  const InStage LI = in_stage<MODE, XT>(RB, C, has_aux<MODE>());
-  const OutStage LO = out_stage<MODE>(RB, C, p.cb_row);
-  uint8_t *in_ring = ring;
-  uint8_t *out_ring = ring + (size_t)SI * LI.bytes;
-  const int64_t nTB = (n + RB - 1) / RB;  // tiles claimed in REVERSE row order
-  double err = 0.0, tsq = 0.0;
-  if (loader) {
-    // phase-B loads: evict_normal (measured ~1 us better than evict_first at [4096, 3072])
-    const uint64_t pol = (p.policy & 2) ? l2_policy_evict_first() : l2_policy_normal();
-    int k = 0, s = 0;
-    uint32_t ph = 0;
-    unsigned long long nxt = 0;  // claims run one tile ahead (as in phase A)
-    if (lane == 0) nxt = atomicAdd(p.ctr + 1, 1ull);
-    for (;;) {
-      if (k >= SI) mbar_wait(&emptyB[s], ph ^ 1u);
-      const long long t = (long long)__shfl_sync(0xffffffffu, nxt, 0);
-      const long long tile = t < nTB ? nTB - 1 - t : -1;
-      if (lane == 0) {
-        if (tile >= 0) nxt = atomicAdd(p.ctr + 1, 1ull);
-        tileB[s] = tile;
-        if (tile < 0) {
-          mbar_arrive(&fullB[s]);
-        } else {
-          uint8_t *st = in_ring + (size_t)s * LI.bytes;
-          const int64_t r0 = (int64_t)tile * RB;
-          const int nrows = (int)min64(RB, n - r0);
-          const uint32_t xb = (uint32_t)(nrows * C * sizeof(XT)), fb = (uint32_t)(nrows * C * 4);
-          const uint32_t ub = (uint32_t)(((r0 & 3) + nrows + 3) / 4 * 16);  // 16B window of u
-          mbar_expect_tx(&fullB[s], xb + (has_aux<MODE>() ? 2 * fb : 0u) + ub);
-          bulk_g2s(ustage + (size_t)s * 16, p.u + (r0 & ~3LL), ub, &fullB[s], pol);
-          bulk_g2s(st + LI.x, X + r0 * C, xb, &fullB[s], pol);
-          if (has_aux<MODE>()) {
-            bulk_g2s(st + LI.base, p.base + r0 * C, fb, &fullB[s], pol);
-            bulk_g2s(st + LI.aux, p.aux + r0 * C, fb, &fullB[s], pol);
+    // ================= phase F: v_j (consumers); g, u_i (store warp) =================
+    if (cta == 0 && tid == 0) p.ctr[0] = 0ull;  // every phase-A claim happened before bar1
+    {
+      // column sums: one CTA per 32-column group; warp w sums CTA slots w, w + kCW, ...
+      // (8 loads in flight per lane), then warp 0 adds the per-warp partials in order
+      double *wpart = red + 16;  // [kCW][32] doubles after the reduction scratch
+      for (int64_t grp32 = cta; grp32 * 32 < C; grp32 += G) {
+        const int64_t j = grp32 * 32 + lane;
+        double acc = 0.0;
+        if (j < C) {
+          constexpr int kB = 16;  // >= ceil(148 / kCW): one L2 round trip on B200
+          for (int s0 = warp; s0 < G; s0 += kB * kCW) {
+            double vals[kB];
+#pragma unroll
+            for (int q = 0; q < kB; ++q) {
+              const int slot = s0 + q * kCW;
+              vals[q] = slot < G ? __ldcg(p.colpart + (int64_t)slot * C + j) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < kB; ++q) acc += vals[q];
           }
         }
-      }
-      __syncwarp();
-      if (tile < 0) break;
-      ++k;
-      if (++s == SI) {
-        s = 0;
-        ph ^= 1u;
-      }
-    }
-  } else if (storer) {
-    int o = 0;
-    uint32_t ph = 0;
-    const bool hint = !(p.policy & 1);  // results are not re-read in this launch: evict_first
-    const uint64_t spol = l2_policy_evict_first();
-    for (;; o = (o + 1 == SO) ? 0 : o + 1, ph ^= (o == 0)) {
-      mbar_wait(&outFull[o], ph);
-      const long long tile = tileO[o];
-      if (tile < 0) break;
-      if (lane == 0) {
-        const uint8_t *so = out_ring + (size_t)o * LO.bytes;
-        const int64_t r0 = (int64_t)tile * RB;
-        const int nrows = (int)min64(RB, n - r0);
-        if (hint) {
-          bulk_s2g_hint(p.base + r0 * C, so + LO.base, (uint32_t)(nrows * C * 4), spol);
-          if constexpr (has_aux<MODE>()) bulk_s2g_hint(p.aux + r0 * C, so + LO.aux, (uint32_t)(nrows * C * 4), spol);
-        } else {
-          bulk_s2g(p.base + r0 * C, so + LO.base, (uint32_t)(nrows * C * 4));
-          if constexpr (has_aux<MODE>()) bulk_s2g(p.aux + r0 * C, so + LO.aux, (uint32_t)(nrows * C * 4));
+        wpart[warp * 32 + lane] = acc;
+        named_sync(1, kCons);
+        if (warp == 0 && j < C) {
+          double sacc = 0.0;
+          for (int w = 0; w < kCW; ++w) sacc += wpart[w * 32 + lane];
+          float v = (float)(sacc / (double)n);  // colmean (cx:148)
+          if (p.scale_mode == CC_SCALE_PER_TOKEN) v = 1.0f;
+          p.v[j] = v;
+          store_f32_bytes(p.body_v + 4 * j, v);
         }
-        bulk_s2g(p.codes + r0 * p.cb_row, so + LO.codes, (uint32_t)(nrows * p.cb_row));
-        bulk_commit();
-        bulk_wait_read<0>();  // smem source consumed -> the slot may be rewritten
-        mbar_arrive(&outFree[o]);
+        named_sync(1, kCons);
       }
-      __syncwarp();
     }
-    if (lane == 0) bulk_wait_read<0>();  // smem sources consumed; the global writes complete on their own
-    __syncwarp();
-  } else {
+    stamp(7);
+    stamp(3);
+    // ---- hand-off 2: v (consumers) and u (store warp) published ----
+    named_sync(1, kCons);
+    if (tid == 0) {
+      arrive_release(bar2);
+      spin_until(bar2, 2u * G);
+      mbar_arrive(&handA[1]);  // relay to the loader
+    }
+    named_sync(1, kCons);
+    stamp(4);
+    if (p.stop_after == 2) return;
+
+    // ================= phase B (consumers): quantize, pack, update state =================
     ColConst cc[Q];
 #pragma unroll
     for (int j = 0; j < Q; ++j) {
@@ -643,7 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       }
       const uint8_t *st = in_ring + (size_t)s * LI.bytes;
       const int64_t r0 = (int64_t)tile * RB;
-      const bool row_live = in_group && r0 + r < n;
+      const bool row_live = in_group && r0 + r < n && !(p.policy & 64);
       float xx[Q][4], bb[Q][4], aa[Q][4];
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
@@ -663,6 +760,10 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       if (lane == 0) mbar_arrive(&emptyB[s]);  // inputs are in registers: the loader may refill
       if (k >= SO) mbar_wait(&outFree[o], pho ^ 1u);
       uint8_t *so = out_ring + (size_t)o * LO.bytes;
+      const bool direct = p.policy & 128;  // experiment: results straight to HBM (generic stores)
+      float *obase = direct ? p.base + r0 * C : reinterpret_cast<float *>(so + LO.base);
+      float *oaux = direct ? p.aux + r0 * C : reinterpret_cast<float *>(so + LO.aux);
+      uint8_t *ocode = direct ? p.codes + r0 * p.cb_row : so + LO.codes;
       const bool row_ok = scale_in_range(fabsf(uf));
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
@@ -682,13 +783,13 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
           } else {
             nb = make_float4(__fadd_rn(bb[j][0], d[0]), __fadd_rn(bb[j][1], d[1]), __fadd_rn(bb[j][2], d[2]),
                              __fadd_rn(bb[j][3], d[3]));
-            *reinterpret_cast<float4 *>(reinterpret_cast<float *>(so + LO.aux) + oo) =
+            *reinterpret_cast<float4 *>(oaux + oo) =
                 MODE == CC_WITH_FEEDBACK ? make_float4(e[0], e[1], e[2], e[3])
                                          : make_float4(xx[j][0], xx[j][1], xx[j][2], xx[j][3]);
           }
-          *reinterpret_cast<float4 *>(reinterpret_cast<float *>(so + LO.base) + oo) = nb;
+          *reinterpret_cast<float4 *>(obase + oo) = nb;
         }
-        uint8_t *crow = so + LO.codes + (size_t)r * p.cb_row;
+        uint8_t *crow = ocode + (size_t)r * p.cb_row;
         if constexpr (CODEC == CC_SIGN1) {
           const uint32_t other = __shfl_down_sync(0xffffffffu, packed, 1);
           if (live && (lane & 1) == 0) crow[qcol[j] >> 3] = (uint8_t)(packed | (other << 4));
@@ -718,13 +819,19 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     __syncthreads();
     if (last) {  // the last CTA reduces the per-CTA partials in a fixed order
       __threadfence();
-      const double a = block_sum(tid < G ? __ldcg(p.recpart + 2 * tid) : 0.0, red);
-      const double b = block_sum(tid < G ? __ldcg(p.recpart + 2 * tid + 1) : 0.0, red);
+      const double pa = tid < G ? __ldcg(p.recpart + 2 * tid) : 0.0;  // both loads in flight together
+      const double pb = tid < G ? __ldcg(p.recpart + 2 * tid + 1) : 0.0;
+      const double a = block_sum(pa, red);
+      const double b = block_sum(pb, red);
       if (tid == 0) {
         p.record[0] = a;
         p.record[1] = b;
-        p.ctr[1] = 0ull;  // every CTA finished claiming phase-B tiles before taking its ticket
+        // every CTA passed both hand-offs and finished claiming before taking its
+        // ticket: leave the control words zeroed for the next launch
+        p.ctr[16] = 0ull;
         *p.ticket = 0u;
+        p.bar[0] = 0u;
+        p.bar[32] = 0u;
       }
     }
   }
@@ -771,8 +878,7 @@ int64_t fused_workspace_bytes(int64_t n, int64_t C) {
   add(sizeof(double) * 2 * G);          // recpart
   add(sizeof(float) * n);
   add(sizeof(float) * C);
-  add(256);
-  add(256);
+  add(512);
   return (int64_t)b;
 }
 
@@ -816,11 +922,11 @@ static int launch_fused(fused::Params &p, cudaStream_t st) {
   p.S_out = SO;
   p.ring_bytes = (uint32_t)align_up(std::max(ringA, ringB), 128);
   const size_t smem = p.ring_bytes + rp_bytes + 512 * 8 + kUCache * 4 +
-                      (size_t)(3 * SA + 3 * SI + 3 * SO) * 8 + 16 + (size_t)SI * 64 + 128;
+                      (size_t)(3 * SA + 3 * SI + 3 * SO + 2) * 8 + 16 + (size_t)SI * 64 + 128;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return cuda_status("k1_fused attr");
   void *args[] = {&p};
-  if (p.ctl_in_ws) cudaMemsetAsync(p.ctr, 0, 2 * sizeof(unsigned long long), st);  // tile counters
+  if (p.ctl_in_ws) cudaMemsetAsync(p.ctr, 0, 512, st);  // control words
   cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(p.G), dim3(kThreads), args, smem, st);
   if (e != cudaSuccess) {
     set_error(std::string("k1_fused launch: ") + cudaGetErrorString(e));
@@ -847,10 +953,17 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   int G = std::min(sm_count(), kThreads);
   // rows per tile: a multiple of the row groups; two per group when each CTA has plenty of rows
   const int64_t rows_per_cta = cdiv(n, G);
+  constexpr double kL2KeepBytes = 40e6;
   p.R = p.groups * (rows_per_cta >= 16 * p.groups ? 2 : 1);
   if (g_fused_ra > 0) p.R = p.groups * g_fused_ra;
   p.G = G;
   p.nTiles = cdiv(n, p.R);
+  {
+    const int pf = (g_fused_policy >> 8) & 15;  // debug override: 1..10 -> tenths, 15 -> none
+    const double tile_bytes = (double)p.R * C * (x_dtype == CC_BF16 ? 10.0 : 12.0);
+    const long long keep = (long long)(kL2KeepBytes / tile_bytes);
+    p.early_tiles = pf == 15 ? 0 : pf ? p.nTiles * pf / 10 : std::max(0LL, (long long)p.nTiles - keep);
+  }
   p.scale_mode = scale_mode;
   p.stop_after = g_fused_stop;
   p.timer = g_fused_timer;
@@ -875,16 +988,17 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   p.recpart = reinterpret_cast<double *>(take(sizeof(double) * 2 * G));
   p.u = reinterpret_cast<float *>(take(sizeof(float) * n));
   p.v = reinterpret_cast<float *>(take(sizeof(float) * C));
-  p.ticket = reinterpret_cast<unsigned int *>(take(256));
-  p.ctr = reinterpret_cast<unsigned long long *>(take(256));
-  // control words: the stream's library-owned slot (kept zero by every launch), or
-  // the workspace + a memset when there is none / a debug stop exits early
+  uint8_t *ctl_ws = take(512);
+  // control words, one 128-byte line each (pollers and atomics never share a line):
+  // ctr0 @0, ctr1 @128, bar1 @256 (+ ticket @260), bar2 @384.  The stream's
+  // library-owned slot (kept zero by every launch), or the workspace + a memset
+  // when there is none / a debug stop exits early
   uint8_t *ctl = (g_fused_stop == 0 && !(g_fused_policy & 32)) ? stream_control_block(st) : nullptr;
   p.ctl_in_ws = ctl == nullptr;
-  if (ctl) {
-    p.ctr = reinterpret_cast<unsigned long long *>(ctl);
-    p.ticket = reinterpret_cast<unsigned int *>(ctl + 16);
-  }
+  if (!ctl) ctl = ctl_ws;
+  p.ctr = reinterpret_cast<unsigned long long *>(ctl);
+  p.ticket = reinterpret_cast<unsigned int *>(ctl + 260);
+  p.bar = reinterpret_cast<unsigned int *>(ctl + 256);
   if ((int64_t)off > ws_bytes) {
     set_error("fused workspace too small");
     return CC_ERR_ARG;

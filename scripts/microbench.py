@@ -93,7 +93,7 @@ def main():
     # experiment bits (k1_fused.cu Params::policy): 1 = phase-B stores without L2 hint,
     # 2 = phase-B loads evict_first, 4 = phase-A loads evict_normal, 8 = phase-A
     # consumers skip the math, 16 = skip row finishing, 32 = control words in the workspace
-    for pol, stop in ((1, 0), (2, 0), (3, 0), (4, 0), (32, 0), (0, 1), (8, 1), (0, 3), (8, 3), (24, 3)):
+    for pol, stop in ((1, 0), (2, 0), (4, 0), (32, 0), (128, 0), (15 << 8, 0), (5 << 8, 0), (6 << 8, 0), (7 << 8, 0), (8 << 8, 0), (0, 1), (8, 1), (0, 3)):
         lib.cc_debug_fused_policy(pol)
         lib.cc_debug_fused_stop(stop)
         for i in range(L):
@@ -102,10 +102,7 @@ def main():
         out[f"k1_fused_policy{pol}{'_stop%d' % stop if stop else ''}"] = {"us": round(us, 2)}
     lib.cc_debug_fused_policy(0)
     lib.cc_debug_fused_stop(0)
-    if os.environ.get("MB_K1_ONLY"):
-        print(json.dumps({"shape": [n, c], "codec": a.codec, **out}))
-        return
-    for si, so in ((6, 1), (4, 2), (3, 3), (2, 4)):
+    for si, so in ((6, 1), (4, 2), (3, 3), (2, 4), (7, 1)):
         lib.cc_debug_fused_rings(si, so)
         for i in range(L):
             enc(i)
@@ -125,19 +122,30 @@ def main():
     lib.cc_debug_fused_stop(0)
     # per-phase timeline of one fused launch (globaltimer stamps per CTA)
     tbuf = torch.zeros(1024 * 8, dtype=torch.int64, device="cuda")
-    lib.cc_debug_fused_timer(_lib.ptr(tbuf))
-    for i in range(3):
+    for pol in (0, 8 | 64):  # 8|64: data movement only (both phases skip the math)
+        lib.cc_debug_fused_policy(pol)
+        lib.cc_debug_fused_timer(_lib.ptr(tbuf))
+        for i in range(2 * L):  # steady state: the previous launch's dirty lines drain during this one
+            enc(i)
+        torch.cuda.synchronize()
+        lib.cc_debug_fused_timer(None)
+        tb = tbuf.view(1024, 8).cpu()
+        g = int((tb[:, 0] > 0).sum())
+        tb = tb[:g].double()
+        t0 = tb[:, 0].min()
+        names = ["start", "A_done", "sync1", "F_done", "sync2", "B_done", "end", "F_cols"]
+        out[f"fused_timeline_us{'_movement_only' if pol else ''}"] = {
+            nm: [round(float((tb[:, i] - t0).min()) / 1e3, 2), round(float((tb[:, i] - t0).max()) / 1e3, 2)]
+            for i, nm in enumerate(names)}
+        out["fused_grid"] = g
+    lib.cc_debug_fused_policy(8 | 64)
+    for i in range(L):
         enc(i)
-    torch.cuda.synchronize()
-    lib.cc_debug_fused_timer(None)
-    tb = tbuf.view(1024, 8).cpu()
-    g = int((tb[:, 0] > 0).sum())
-    tb = tb[:g].double()
-    t0 = tb[:, 0].min()
-    names = ["start", "A_done", "sync1", "F_done", "sync2", "B_done", "end", "F_cols"]
-    out["fused_timeline_us"] = {nm: [round(float((tb[:, i] - t0).min()) / 1e3, 2),
-                                     round(float((tb[:, i] - t0).max()) / 1e3, 2)] for i, nm in enumerate(names)}
-    out["fused_grid"] = g
+    out["k1_fused_movement_only"] = {"us": round(timed(enc, a.reps), 2)}
+    lib.cc_debug_fused_policy(0)
+    if os.environ.get("MB_K1_ONLY"):
+        print(json.dumps({"shape": [n, c], "codec": a.codec, **out}))
+        return
     # K2: accumulate decode of the last body into each layer's base
     bases = [st.base for st in sts]
 
