@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlap", action="store_true")
+    ap.add_argument("--overlap", action="store_true", help="run K2 on its own stream even at N=1 (the "
+                    "loopback receiver has no communication to hide; two HBM-bound kernels gain nothing)")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from Python instead of "
                                                              "replaying a captured CUDA graph per step")
     return ap.parse_args()
@@ -280,7 +282,8 @@ def run_b200(a, world, rank):
     lo, hi = bounds[rank]
     n_own = hi - lo
     Ex = RingExchange if a.topology == "ring" else PatchParallelExchange
-    exs = [Ex(rows, cols, spec, overlap=not a.no_overlap) for _ in range(L)]
+    overlap = (world > 1 or a.overlap) and not a.no_overlap
+    exs = [Ex(rows, cols, spec, overlap=overlap) for _ in range(L)]
     streams = exs[0].streams
     for e in exs[1:]:
         e.streams = streams  # one compute / comm / decode stream triple for the whole model
@@ -289,11 +292,9 @@ def run_b200(a, world, rank):
     # instrumentation: K1 / K2 events per (step, layer)
     def one_step(s, ev=None, skip_comm=False):
         for layer, e in enumerate(exs):
-            if ev is not None:
-                ev[layer][0].record(streams.compute)
-            e.step(inputs[layer][s % 2], skip_comm=skip_comm)
-            if ev is not None:
-                ev[layer][1].record(streams.compute)  # K1 ends before the comm stream starts
+            # K1 events are recorded by the exchange itself around the encode, on the
+            # compute stream (the stream K1 is launched on)
+            e.step(inputs[layer][s % 2], skip_comm=skip_comm, k1_events=None if ev is None else ev[layer])
 
     # protocol warmup (raw) step + bench warmups
     one_step(0)
@@ -408,7 +409,7 @@ def run_b200(a, world, rank):
                                                                   "BASELINE config 1)" if world == 1 else "")),
                    "codec": a.codec, "layers": L, "rows": rows, "cols": cols, "shard_rows": n_own,
                    "parallelism": f"patch{world}", "topology": a.topology, "l2": "per-step working set >> 126 MB L2 (no flush needed)",
-                   "overlap": not a.no_overlap, "cuda_graph": not a.no_graph},
+                   "overlap": overlap, "cuda_graph": not a.no_graph},
         "per_gpu_gbs": value / world,
         "exposed_comm_us_per_layer": exposed_us,
         "bf16_allgather_us_per_layer": bf16_ag_us,

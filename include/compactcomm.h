@@ -195,9 +195,14 @@ CC_API void cc_debug_fused_stop(int phase);
 /* profiling only: device buffer of [grid][8] u64 %globaltimer stamps written by
  * every CTA of the persistent K1 at its phase boundaries (NULL disables). */
 CC_API void cc_debug_fused_timer(void *dev_buf);
-/* profiling only: L2 eviction policy of the persistent K1's TMA loads
- * (0 evict_last/evict_first (default), 1 normal/normal, 2 normal/first, 3 last/normal) */
+/* profiling only: experiment bits of the persistent K1 (0 = production path; see
+ * k1_fused.cu Params::policy: L2 hints, skipped math / stores, workspace control words,
+ * forced phase-A evict_first fraction in bits 8..11) */
 CC_API void cc_debug_fused_policy(int policy);
+/* profiling only: phase-B end-game of the persistent K1: when fewer than mult x grid
+ * tiles remain, a CTA keeps at most `keep` loaded tiles ahead of its consumers
+ * (0, 0 = automatic) */
+CC_API void cc_debug_fused_tail(int mult, int keep);
 /* profiling only: phase-B ring depths of the persistent K1 (0 = automatic) */
 CC_API void cc_debug_fused_rings(int s_in, int s_out);
 /* profiling only: phase-A tile height (rows per row group) and ring depth of the

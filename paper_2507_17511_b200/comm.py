@@ -277,8 +277,10 @@ class PatchParallelExchange:
         return max(body_bytes_for(self.codec, b[1] - b[0], self.cols) for b in self.bounds)
 
     # -- one step ---------------------------------------------------------------
-    def step(self, x_shard, rng=None, skip_comm=False):
-        """Returns the reconstruction tensor (on GPU: valid on the decode stream)."""
+    def step(self, x_shard, rng=None, skip_comm=False, k1_events=None):
+        """Returns the reconstruction tensor (on GPU: valid on the decode stream).
+        k1_events: optional (start, end) CUDA events recorded around the encode
+        (K1) on the compute stream, for per-kernel timing."""
         S = self.streams
         t = self.sender.step + 1
         warm = t <= self.warmup or cx.CompressorKind(self.codec.kind) == cx.CompressorKind.IDENTITY
@@ -287,7 +289,11 @@ class PatchParallelExchange:
             # capture that order is implied by the ordering of graph launches)
             if S.compute is not None and not torch.cuda.is_current_stream_capturing():
                 self.ev_decoded.wait(S.compute)
+            if k1_events is not None:
+                k1_events[0].record()
             nbytes, wire16, rec = self.engine.encode(self.sender, x_shard, self.codec, self.sendbuf, rng)
+            if k1_events is not None:
+                k1_events[1].record()
             self.last_record, self.last_nbytes = rec, nbytes
             self.ev_encoded.record(S.compute)
         per = self.wire_bytes(warm, wire16)
@@ -373,9 +379,9 @@ class RingExchange(PatchParallelExchange):
     def origin(rank, rnd, P):
         return (rank - rnd) % P
 
-    def step(self, x_shard, rng=None, skip_comm=False):
+    def step(self, x_shard, rng=None, skip_comm=False, k1_events=None):
         if self.P == 1:
-            return super().step(x_shard, rng=rng, skip_comm=skip_comm)
+            return super().step(x_shard, rng=rng, skip_comm=skip_comm, k1_events=k1_events)
         S = self.streams
         dist = _dist()
         t = self.sender.step + 1
@@ -383,7 +389,11 @@ class RingExchange(PatchParallelExchange):
         with _on(S.compute):
             if S.compute is not None and not torch.cuda.is_current_stream_capturing():
                 self.ev_decoded.wait(S.compute)
+            if k1_events is not None:
+                k1_events[0].record()
             nbytes, wire16, rec = self.engine.encode(self.sender, x_shard, self.codec, self.sendbuf, rng)
+            if k1_events is not None:
+                k1_events[1].record()
             self.last_record, self.last_nbytes = rec, nbytes
             self.ev_encoded.record(S.compute)
         per = self.wire_bytes(warm, wire16)

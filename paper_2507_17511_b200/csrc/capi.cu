@@ -109,6 +109,7 @@ void set_fused_stop(int v);
 void set_fused_timer(void *buf);
 void set_fused_policy(int v);
 void set_fused_rings(int si, int so);
+void set_fused_tail(int mult, int keep);
 void set_fused_phase_a(int rows_per_tile, int stages);
 void set_lowrank_backend(int v);
 int residual_target(int mode, int64_t n, int64_t C, const void *x, int x_dtype, const float *base, const float *aux,
@@ -138,6 +139,7 @@ CC_API void cc_debug_fused_stop(int phase) { set_fused_stop(phase); }
 CC_API void cc_debug_fused_timer(void *dev_buf) { set_fused_timer(dev_buf); }
 CC_API void cc_debug_fused_policy(int policy) { set_fused_policy(policy); }
 CC_API void cc_debug_fused_rings(int s_in, int s_out) { set_fused_rings(s_in, s_out); }
+CC_API void cc_debug_fused_tail(int mult, int keep) { set_fused_tail(mult, keep); }
 CC_API void cc_debug_fused_phase_a(int rows_per_group, int stages) { set_fused_phase_a(rows_per_group, stages); }
 CC_API void cc_set_lowrank_backend(int backend) { set_lowrank_backend(backend); }
 

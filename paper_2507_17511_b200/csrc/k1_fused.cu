@@ -64,6 +64,7 @@ struct Params {
   int stop_after;             // profiling: 1 = phase A only, 2 = A + scales, 3 = A w/o sync, 0 = full
   int ctl_in_ws;              // control words live in the workspace (memset before launch)
   long long early_tiles;      // phase-A tiles loaded L2::evict_first (the rest evict_last)
+  int tail_mult, tail_keep;   // phase-B end-game: < tail_mult * G tiles left -> <= tail_keep tiles ahead
   unsigned long long *timer;  // profiling: [G][8] globaltimer stamps, or null
   int policy;  // experiment bits: 1 = phase-B stores without L2 hint, 2 = phase-B loads evict_first,
                // 4 = phase-A loads evict_normal, 8 = phase-A consumers skip the math (timing only),
@@ -82,23 +83,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
-}
-
-// deterministic block sum over all kThreads threads (fixed pairing)
-__device__ __forceinline__ double block_sum(double v, double *red) {
-  v = warp_sum(v);
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) red[w] = v;
-  __syncthreads();
-  double s = 0.0;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kThreads / 32; ++i) s += red[i];
-    red[kThreads / 32] = s;
-  }
-  __syncthreads();
-  s = red[kThreads / 32];
-  __syncthreads();
-  return s;
 }
 
 struct CodeVal {
@@ -215,6 +199,32 @@ __device__ __forceinline__ void record4(const float (&t)[4], const float (&e)[4]
 
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// deterministic sums of two values over the kCons consumer threads (named
+// barrier 1): fixed butterfly per warp, then warps in order; all consumers get them
+__device__ __forceinline__ void cons_sum2(double a, double b, double *red, double &sa, double &sb) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[2 * w] = a;
+    red[2 * w + 1] = b;
+  }
+  named_sync(1, kCons);
+  sa = 0.0;
+  sb = 0.0;
+  for (int i = 0; i < kCW; ++i) {
+    sa += red[2 * i];
+    sb += red[2 * i + 1];
+  }
+  named_sync(1, kCons);
+}
+
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned *p) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
 }
 
 // grid hand-off wait: spin until *p >= target (acquire)
@@ -460,10 +470,15 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     // the scale pass; their u windows follow once bar2 publishes u.
     // phase-B loads: evict_normal (measured ~1 us better than evict_first at [4096, 3072])
     const uint64_t pol = (p.policy & 2) ? l2_policy_evict_first() : l2_policy_normal();
-    int k = 0, s = 0;
-    uint32_t ph = 0;
-    bool u_ready = false;
-    unsigned long long nxt = 0;  // claims run one tile ahead (as in phase A)
+    // k = stage uses issued (stage k % SI), w = uses whose release has been awaited.
+    // Claims run one tile ahead while plenty of work is left; in the end-game
+    // (fewer than tail_mult x G tiles unclaimed) a CTA claims only when at most
+    // tail_keep of its tiles are still unconsumed, so the last tiles spread over
+    // the grid instead of queueing behind a few full rings.
+    int k = 0, w = 0;
+    bool u_ready = false, have_nxt = true, near_end = false;
+    const long long tail = (long long)p.tail_mult * G;
+    unsigned long long nxt = 0;
     if (lane == 0) nxt = atomicAdd(p.ctr + 16, 1ull);
     auto load_u = [&](int st_, long long tile) {  // lane 0: 16B-aligned window of u for the tile's rows
       const int64_t r0 = (int64_t)tile * RB;
@@ -482,14 +497,18 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       u_ready = true;
     };
     for (;;) {
-      if (k >= SI) {
-        if (!u_ready) publish_u(SI);
-        mbar_wait(&emptyB[s], ph ^ 1u);
-      }
+      int req = k - SI + 1;  // stage k % SI must be free
+      if (near_end) req = max(req, k - p.tail_keep);
+      if (w < req && !u_ready) publish_u(min(k, SI));  // consumers need u before any release
+      for (; w < req; ++w) mbar_wait(&emptyB[w % SI], (uint32_t)(w / SI) & 1u);
+      if (!have_nxt && lane == 0) nxt = atomicAdd(p.ctr + 16, 1ull);
       const long long t = (long long)__shfl_sync(0xffffffffu, nxt, 0);
       const long long tile = t < nTB ? nTB - 1 - t : -1;
+      near_end = tail > 0 && t + tail >= nTB;
+      have_nxt = tile >= 0 && !near_end;
+      const int s = k % SI;
       if (lane == 0) {
-        if (tile >= 0) nxt = atomicAdd(p.ctr + 16, 1ull);
+        if (have_nxt) nxt = atomicAdd(p.ctr + 16, 1ull);
         tileB[s] = tile;
         if (tile < 0) {
           mbar_arrive(&fullB[s]);
@@ -511,12 +530,8 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       __syncwarp();
       if (tile < 0) break;
       ++k;
-      if (++s == SI) {
-        s = 0;
-        ph ^= 1u;
-      }
     }
-    if (!u_ready) publish_u(k + 1);  // fewer than S_in tiles: stages 0..k (the last one is the sentinel)
+    if (!u_ready) publish_u(min(k + 1, SI));  // stages 0..k (the last one holds the sentinel)
   } else if (storer) {
     if (p.stop_after == 1 || p.stop_after == 3) return;
     // ---- scale pass, row half (the consumers do the columns): g, u_i ----
@@ -805,24 +820,25 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       if (lane == 0) mbar_arrive(&outFull[o]);
     }
   }
+  // ---- StepRecord: consumer warps only (the store warp drains its last stages
+  // meanwhile; the loader made its last claim before publishing the sentinel) ----
+  if (!consumer) return;
   stamp(5);
   {
-    const double es = block_sum(err, red);
-    const double ts = block_sum(tsq, red);
     __shared__ unsigned last;
+    double es, ts;
+    cons_sum2(err, tsq, red, es, ts);
     if (tid == 0) {
       p.recpart[2 * cta] = es;
       p.recpart[2 * cta + 1] = ts;
-      __threadfence();
-      last = atomicAdd(p.ticket, 1u) == (unsigned)G - 1;
+      last = atom_add_acq_rel(p.ticket) == (unsigned)G - 1;  // release: partials; acquire: the others'
     }
-    __syncthreads();
+    named_sync(1, kCons);
     if (last) {  // the last CTA reduces the per-CTA partials in a fixed order
-      __threadfence();
       const double pa = tid < G ? __ldcg(p.recpart + 2 * tid) : 0.0;  // both loads in flight together
       const double pb = tid < G ? __ldcg(p.recpart + 2 * tid + 1) : 0.0;
-      const double a = block_sum(pa, red);
-      const double b = block_sum(pb, red);
+      double a, b;
+      cons_sum2(pa, pb, red, a, b);
       if (tid == 0) {
         p.record[0] = a;
         p.record[1] = b;
@@ -835,6 +851,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       }
     }
   }
+  stamp(6);
   stamp(6);
 }
 
@@ -849,6 +866,11 @@ static int g_fused_si = 0, g_fused_so = 0, g_fused_ra = 0, g_fused_sa = 0;
 void set_fused_phase_a(int rows_per_tile, int stages) {
   g_fused_ra = rows_per_tile;
   g_fused_sa = stages;
+}
+static int g_fused_tail_mult = 0, g_fused_tail_keep = 0;
+void set_fused_tail(int mult, int keep) {
+  g_fused_tail_mult = mult;
+  g_fused_tail_keep = keep;
 }
 void set_fused_rings(int si, int so) {
   g_fused_si = si;
@@ -950,7 +972,7 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   const int Q = p.G4 > kCons ? 2 : 1;
   p.groups = Q == 2 ? 1 : kCons / p.G4;
   p.wpg = Q == 2 ? kCW : p.G4 / 32;
-  int G = std::min(sm_count(), kThreads);
+  int G = std::min(sm_count(), kCons);  // the record / scale reductions assume G <= kCons
   // rows per tile: a multiple of the row groups; two per group when each CTA has plenty of rows
   const int64_t rows_per_cta = cdiv(n, G);
   constexpr double kL2KeepBytes = 40e6;
@@ -966,6 +988,8 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   }
   p.scale_mode = scale_mode;
   p.stop_after = g_fused_stop;
+  p.tail_mult = g_fused_tail_mult > 0 ? g_fused_tail_mult : g_fused_tail_mult < 0 ? 0 : 2;
+  p.tail_keep = g_fused_tail_keep > 0 ? g_fused_tail_keep : 2;
   p.timer = g_fused_timer;
   p.policy = g_fused_policy;
   const int bits = codec == CC_SIGN1 ? 1 : (codec == CC_QUANT2 ? 2 : 4);

@@ -143,6 +143,12 @@ def main():
         enc(i)
     out["k1_fused_movement_only"] = {"us": round(timed(enc, a.reps), 2)}
     lib.cc_debug_fused_policy(0)
+    for mult, keep in ((-1, 1), (1, 1), (2, 1), (-1, 1), (2, 2), (4, 2), (2, 3), (-1, 1)):  # phase-B end-game
+        lib.cc_debug_fused_tail(mult, keep)
+        for i in range(L):
+            enc(i)
+        out[f"k1_fused_tail{mult}_{keep}"] = {"us": round(timed(enc, a.reps), 2)}
+    lib.cc_debug_fused_tail(0, 0)
     if os.environ.get("MB_K1_ONLY"):
         print(json.dumps({"shape": [n, c], "codec": a.codec, **out}))
         return
