@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--cols", type=int, default=COLS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sim", action="store_true", help="skip the single-GPU per-rank simulations of "
+                    "the 2/4/8-GPU patch-parallel and 8-GPU Ulysses configs (`per_rank_sim`)")
     ap.add_argument("--no-overlap", action="store_true")
     ap.add_argument("--overlap", action="store_true", help="run K2 on its own stream even at N=1 (the "
                     "loopback receiver has no communication to hide; two HBM-bound kernels gain nothing)")
@@ -390,6 +392,11 @@ def run_b200(a, world, rank):
     path_bytes = k1_bytes + k2_bytes
 
     e2e = None if a.no_e2e else measure_e2e(exs, inputs, streams, world, K, L, rows, cols, lo, hi, dev)
+    sim = None
+    if world == 1 and not a.no_sim:
+        del graphs
+        sim = {f"patch{P}": sim_rank_measure("patch", P, "quant2bit", L, rows, cols) for P in (2, 4, 8)}
+        sim["ulysses8"] = sim_rank_measure("ulysses", 8, "sign1bit", L, rows, cols)
     cpu = None
     if not a.no_cpu and rank == 0 and world == 1:
         threads = min(os.cpu_count() or 1, 16)
@@ -424,6 +431,7 @@ def run_b200(a, world, rank):
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "per_rank_sim": sim,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -523,6 +531,66 @@ def measure_e2e(exs, inputs, streams, world, K, L, rows, cols, lo, hi, dev):
     value = world * L * 2 * rows * cols / (ms / 1e3) / 1e9
     return {"value": value, "unit": "GB/s", "ms_per_step": ms, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h}
+
+
+def sim_rank_measure(kind, P, codec, L, rows, cols, steps=5, warmup=3):
+    """One rank of a P-rank job on this single GPU (exchange `sim_world=(P, 0)`): K1 on
+    the rank's shard (patch: [rows/P, cols]; Ulysses: P chunks [rows/P, cols/P]), the
+    collective replaced by device copies of the rank's bodies into the receive slots,
+    K2 over the P-1 peer slots (patch) / P chunks (Ulysses).  Returns ms per layer and
+    per-GPU activation GB/s — the per-rank compute + landing-copy cost of configs 2-3,
+    without NVLink transfer time.  CUDA-graph replay, 57 layer channels."""
+    import torch
+
+    from paper_2507_17511_b200 import compressors as cx
+    from paper_2507_17511_b200.comm import PatchParallelExchange, UlyssesAllToAll, shard_bounds
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    spec = cx.CompressorSpec(cx.CompressorKind(codec))
+    n = rows // P
+    if kind == "patch":
+        exs = [PatchParallelExchange(rows, cols, spec, sim_world=(P, 0)) for _ in range(L)]
+        lo, hi = shard_bounds(rows, P)[0]
+    else:
+        exs = [UlyssesAllToAll(n, cols, spec, sim_world=(P, 0)) for _ in range(L)]
+        lo, hi = 0, n
+    streams = exs[0].streams
+    for e in exs[1:]:
+        e.streams = streams
+    inputs = [flux_inputs(rows, cols, lo, hi, layer, dev) for layer in range(L)]
+
+    def one_step(s):
+        for layer, e in enumerate(exs):
+            e.step(inputs[layer][s % 2])
+
+    for s in range(warmup + 1):
+        one_step(s)
+    torch.cuda.synchronize()
+    graphs = []
+    for par in (0, 1):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            one_step(par)
+            torch.cuda.current_stream().wait_stream(streams.decode)
+        graphs.append(g)
+    for e in exs:
+        if hasattr(e, "after_capture"):
+            e.after_capture()
+    for par in (0, 1):
+        graphs[par].replay()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for s in range(steps):
+        graphs[s % 2].replay()
+    t1.record()
+    torch.cuda.synchronize()
+    ms_layer = t0.elapsed_time(t1) / steps / L
+    out = {"ms_per_layer": round(ms_layer, 5), "gbs_per_gpu": round(2 * rows * cols / (ms_layer / 1e3) / 1e9, 1),
+           "codec": codec, "shard": [n, cols if kind == "patch" else cols // P]}
+    del exs, inputs, graphs
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():

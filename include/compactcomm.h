@@ -104,6 +104,21 @@ CC_API int cc_encode_step(int codec, int mode, int scale_mode, int64_t rows, int
                           uint8_t *body, void *workspace, int64_t workspace_bytes,
                           double *record, void *stream);
 
+/* Segmented sender step for Ulysses sequence parallelism (every
+ * directed (src, dst) chunk is its own LayerState channel).  Equivalent to
+ * `segments` independent cc_encode_step calls on the column slices
+ * x[:, d*cw:(d+1)*cw] (cw = cols / segments) with states base/aux[:, slice],
+ * bodies at body + d * body_stride (each the reference body of an [rows, cw]
+ * channel) and records at record + 2 d — in ONE persistent launch over the
+ * full-width rows (no chunk copies).  base / aux / x stay [rows, cols] row-major.
+ * Needs the fused kernel's shapes: cols % 128 == 0, cols <= 3072, cw % 128 == 0,
+ * segments <= 16, 16-byte aligned buffers and body_stride; CC_ERR_UNSUPPORTED
+ * otherwise (the caller then encodes chunk by chunk). */
+CC_API int cc_encode_step_segmented(int codec, int mode, int scale_mode, int64_t rows, int64_t cols,
+                                    int segments, const void *x, int x_dtype, float *base, float *aux,
+                                    uint8_t *body, int64_t body_stride, void *workspace,
+                                    int64_t workspace_bytes, double *record, void *stream);
+
 /* Warmup / identity step (pl:89-97): base = x, feedback = 0, ref = x,
  * body = raw x as body_dtype (CC_F32 = the reference wire, CC_BF16 lossless
  * for bf16 inputs), record = {0, ||x||^2}. */

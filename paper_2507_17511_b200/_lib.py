@@ -34,6 +34,8 @@ SIGNATURES = {
     "cc_body_bytes": (_i64, [_i32, _i64, _i64, _i64]),
     "cc_workspace_bytes": (_i64, [_i32, _i64, _i64, _i64]),
     "cc_encode_step": (_i32, [_i32, _i32, _i32, _i64, _i64, _p, _i32, _p, _p, _p, _p, _i64, _p, _p]),
+    "cc_encode_step_segmented": (_i32, [_i32, _i32, _i32, _i64, _i64, _i32, _p, _i32, _p, _p, _p, _i64, _p, _i64,
+                                        _p, _p]),
     "cc_warmup_step": (_i32, [_i32, _i64, _i64, _p, _i32, _p, _p, _p, _i32, _p, _p]),
     "cc_decode_step": (_i32, [_i32, _i32, _i64, _i64, _i64, _p, _i32, _p, _p]),
     "cc_decode_batched": (_i32, [_i32, _i32, _i32, ctypes.POINTER(_i64), _i64, _i64, ctypes.POINTER(_p), _i32,

@@ -193,6 +193,18 @@ class _Event:
             stream.wait_event(self.ev)
 
 
+def _segmented_ok(codec, n, cols, P):
+    """cc_encode_step_segmented's shape rules (k1_fused.cu fused_segments_supported)."""
+    kind = cx.CompressorKind(codec.kind)
+    if kind not in (cx.CompressorKind.SIGN1BIT, cx.CompressorKind.QUANT2BIT, cx.CompressorKind.QUANT4BIT):
+        return False
+    if cols % 128 or cols > 3072 or cols % P or P > 16:
+        return False
+    cw = cols // P
+    groups = 1 if cols // 4 > 384 else 384 // (cols // 4)
+    return cw % 128 == 0 and 2 * groups * P <= 32
+
+
 def _dist():
     import torch.distributed as dist
 
@@ -216,13 +228,19 @@ class PatchParallelExchange:
     """
 
     def __init__(self, rows, cols, codec, mode="residual_with_feedback", warmup=1, group=None,
-                 in_dtype=torch.bfloat16, overlap=True, streams=None, engine=None, device=None):
+                 in_dtype=torch.bfloat16, overlap=True, streams=None, engine=None, device=None, sim_world=None):
         dist = _dist()
         self.rows, self.cols, self.codec = int(rows), int(cols), codec
         self.mode = pl.PipelineMode(mode)
         self.warmup = int(warmup)
         self.group = group
-        if dist.is_available() and dist.is_initialized():
+        # sim_world = (P, rank): single-GPU stand-in for one rank of a P-rank job (benchmarks
+        # only): the collective is replaced by device copies of this rank's own body into
+        # every peer slot, so K1 / K2 / the copies run at the real per-rank shapes
+        self.sim = sim_world is not None
+        if self.sim:
+            self.P, self.rank = int(sim_world[0]), int(sim_world[1])
+        elif dist.is_available() and dist.is_initialized():
             self.P, self.rank = dist.get_world_size(group), dist.get_rank(group)
         else:
             self.P, self.rank = 1, 0
@@ -302,7 +320,12 @@ class PatchParallelExchange:
                 self.ev_encoded.wait(S.comm)
             if self.P > 1:
                 self._per = per
-                if not skip_comm:
+                if skip_comm:
+                    pass
+                elif self.sim:
+                    for p in self.peers:
+                        self.slot(p)[:per].copy_(self.sendbuf[:per])
+                else:
                     _dist().all_gather_into_tensor(self.recvflat[:self.P * per], self.sendbuf[:per], group=self.group)
                 self.comm_bytes = per * (self.P - 1)
             self.ev_gathered.record(S.comm)
@@ -380,7 +403,7 @@ class RingExchange(PatchParallelExchange):
         return (rank - rnd) % P
 
     def step(self, x_shard, rng=None, skip_comm=False, k1_events=None):
-        if self.P == 1:
+        if self.P == 1 or self.sim:
             return super().step(x_shard, rng=rng, skip_comm=skip_comm, k1_events=k1_events)
         S = self.streams
         dist = _dist()
@@ -444,10 +467,13 @@ class UlyssesAllToAll:
     """
 
     def __init__(self, n_local, cols, codec, mode="residual_with_feedback", warmup=1, group=None,
-                 in_dtype=torch.bfloat16, overlap=True, engine=None, device=None):
+                 in_dtype=torch.bfloat16, overlap=True, engine=None, device=None, sim_world=None):
         dist = _dist()
         self.group = group
-        if dist.is_available() and dist.is_initialized():
+        self.sim = sim_world is not None  # (P, rank): single-GPU stand-in (see PatchParallelExchange)
+        if self.sim:
+            self.P, self.rank = int(sim_world[0]), int(sim_world[1])
+        elif dist.is_available() and dist.is_initialized():
             self.P, self.rank = dist.get_world_size(group), dist.get_rank(group)
         else:
             self.P, self.rank = 1, 0
@@ -462,13 +488,29 @@ class UlyssesAllToAll:
         self.cuda = self.device.type == "cuda"
         self.in_dtype = in_dtype
         f32 = dict(dtype=torch.float32, device=self.device)
+        # Segmented path: all P sender channels in ONE persistent K1 launch over the
+        # full-width rows (cc_encode_step_segmented): the channel states are column
+        # slices of [n, C] arrays and no chunk copies are made.  Otherwise one
+        # encode_step per chunk on contiguous per-chunk states.
+        self.segmented = self.cuda and self.P > 1 and _segmented_ok(codec, self.n, self.C, self.P)
+        nofb = self.mode == pl.PipelineMode.RESIDUAL_NO_FEEDBACK
+        if self.segmented:
+            self.base_full = torch.zeros(self.n, self.C, **f32)
+            self.aux_full = torch.zeros(self.n, self.C, **f32)  # feedback, or ref (no-feedback mode)
+            self.rec_seg = torch.zeros(2 * self.P, dtype=torch.float64, device=self.device)
         self.senders = []
-        for _ in range(self.P):
+        for d in range(self.P):
             st = pl.LayerState.__new__(pl.LayerState)
             st.mode, st.warmup_steps, st.step, st._rec = self.mode, self.warmup, 0, None
-            st.base = torch.zeros(self.n, self.cw, **f32)
-            st.feedback = torch.zeros(self.n, self.cw, **f32)
-            st.ref = torch.zeros(self.n, self.cw, **f32) if self.mode == pl.PipelineMode.RESIDUAL_NO_FEEDBACK else None
+            if self.segmented:
+                sl = slice(d * self.cw, (d + 1) * self.cw)
+                st.base = self.base_full[:, sl]
+                st.feedback = None if nofb else self.aux_full[:, sl]
+                st.ref = self.aux_full[:, sl] if nofb else None
+            else:
+                st.base = torch.zeros(self.n, self.cw, **f32)
+                st.feedback = torch.zeros(self.n, self.cw, **f32)
+                st.ref = torch.zeros(self.n, self.cw, **f32) if nofb else None
             self.senders.append(st)
         # out[src] block: rows of rank src for our heads; receiver bases are views
         self.out = torch.zeros(self.P * self.n, self.cw, **f32)
@@ -487,19 +529,22 @@ class UlyssesAllToAll:
         t = self.senders[0].step + 1
         warm = t <= self.warmup
         with _on(S.compute):
-            for d in range(self.P):
-                chunk = x_local[:, d * self.cw:(d + 1) * self.cw].contiguous()
-                _, wire16, _ = self.engine.encode(self.senders[d], chunk, self.codec, self.sendbuf[d], rng)
+            if self.segmented:
+                wire16 = self._encode_segmented(x_local, t, warm)
+            else:
+                for d in range(self.P):
+                    chunk = x_local[:, d * self.cw:(d + 1) * self.cw].contiguous()
+                    _, wire16, _ = self.engine.encode(self.senders[d], chunk, self.codec, self.sendbuf[d], rng)
             self.ev_encoded.record(S.compute)
         per = self.n * self.cw * (2 if wire16 else 4) if warm else body_bytes_for(self.codec, self.n, self.cw)
         with _on(S.comm):
             if S.comm is not None:
                 self.ev_encoded.wait(S.comm)
-            send = self.sendbuf[:, :per].contiguous()
-            if self.P > 1:
+            send = self.sendbuf[:, :per]
+            if self.P > 1 and not self.sim:
                 recv = torch.empty_like(send)
-                _dist().all_to_all_single(recv.view(-1), send.view(-1), group=self.group)
-            else:
+                _dist().all_to_all_single(recv.view(-1), send.contiguous().view(-1), group=self.group)
+            else:  # loopback / single-GPU stand-in: the body of chunk d lands in slot d
                 recv = send
             self.recvbuf[:, :per].copy_(recv)
             self.ev_gathered.record(S.comm)
@@ -518,3 +563,37 @@ class UlyssesAllToAll:
         if S.decode is not None:
             torch.cuda.current_stream(self.device).wait_stream(S.decode)
         return self.out
+
+    def _encode_segmented(self, x_local, t, warm):
+        """All P chunk channels in one launch (see __init__); returns wire16."""
+        lib = _lib.load()
+        x = x_local if x_local.is_contiguous() else x_local.contiguous()
+        if tuple(x.shape) != (self.n, self.C):
+            raise pl.ShapeError(f"input shape {tuple(x.shape)} != {(self.n, self.C)}")
+        mode = pl._MODE_CODE[self.mode]
+        aux = None if self.mode == pl.PipelineMode.NAIVE else self.aux_full
+        stream = _lib.stream_ptr()
+        wire16 = x.dtype == torch.bfloat16
+        if warm:
+            # raw step (pl:89-97) on the full rows, then each chunk's raw body
+            # (lossless bf16 for bf16 inputs) into its send slot
+            esz = 2 if wire16 else 4
+            tmp = cx._empty_body(self.n * self.C * esz)
+            _lib.check(lib.cc_warmup_step(mode, self.n, self.C, _lib.ptr(x), cx.dtype_code(x),
+                                          _lib.ptr(self.base_full), _lib.ptr(aux), _lib.ptr(tmp), cx.dtype_code(x),
+                                          _lib.ptr(self.rec_seg), stream), "warmup")
+            wdt = torch.bfloat16 if wire16 else torch.float32
+            for d in range(self.P):
+                dst = self.sendbuf[d, :self.n * self.cw * esz].view(wdt).view(self.n, self.cw)
+                dst.copy_(x[:, d * self.cw:(d + 1) * self.cw])
+        else:
+            tag = cx._spec_tag(self.codec)
+            ws = cx.workspace(_lib.check(lib.cc_workspace_bytes(tag, self.n, self.C, 0)))
+            _lib.check(lib.cc_encode_step_segmented(
+                tag, mode, cx._SCALE_MODES[self.codec.scale_mode], self.n, self.C, self.P, _lib.ptr(x),
+                cx.dtype_code(x), _lib.ptr(self.base_full), _lib.ptr(aux), _lib.ptr(self.sendbuf), self.body,
+                _lib.ptr(ws), ws.numel(), _lib.ptr(self.rec_seg), stream), "segmented encode_step")
+            wire16 = False
+        for st in self.senders:
+            st.step = t
+        return wire16

@@ -105,6 +105,12 @@ int nm_encode_step(int mode, int64_t rows, int64_t C, int n, int m, const void *
 int nm_decode(int count, const int64_t *rows, int64_t C, int n, int m, const uint8_t *const *bodies, int accumulate,
               float *const *bases, cudaStream_t st);
 void set_quant_path(int v);
+bool fused_supported(int64_t n, int64_t C, const void *x, int x_dtype, const float *base, const float *aux,
+                     const uint8_t *body);
+bool fused_segments_supported(int64_t n, int64_t C, int nseg, int64_t body_stride, int codec);
+int fused_encode_segments(int codec, int mode, int scale_mode, int64_t n, int64_t C, int nseg, const void *x,
+                          int x_dtype, float *base, float *aux, uint8_t *body, int64_t body_stride, void *ws,
+                          int64_t ws_bytes, double *record, cudaStream_t st);
 void set_fused_stop(int v);
 void set_fused_timer(void *buf);
 void set_fused_policy(int v);
@@ -194,6 +200,29 @@ CC_API int cc_encode_step(int codec, int mode, int scale_mode, int64_t rows, int
   if (!quant_codec(codec)) { set_error("cc_encode_step: codec must be sign1/quant2/quant4"); return CC_ERR_UNSUPPORTED; }
   return quant_encode_step(codec, mode, scale_mode, rows, cols, x, x_dtype, base, aux, body, workspace,
                            workspace_bytes, record, (cudaStream_t)stream);
+}
+
+CC_API int cc_encode_step_segmented(int codec, int mode, int scale_mode, int64_t rows, int64_t cols, int segments,
+                                    const void *x, int x_dtype, float *base, float *aux, uint8_t *body,
+                                    int64_t body_stride, void *workspace, int64_t workspace_bytes, double *record,
+                                    void *stream) {
+  if (rows < 1 || cols < 1) { set_error("empty shape"); return CC_ERR_SHAPE; }
+  if (!valid_mode(mode) || (x_dtype != CC_F32 && x_dtype != CC_BF16)) { set_error("bad mode/dtype"); return CC_ERR_ARG; }
+  if (!x || !base || !body || !record || (mode != CC_NAIVE && !aux)) { set_error("null pointer"); return CC_ERR_ARG; }
+  if (scale_mode < CC_SCALE_RANK1 || scale_mode > CC_SCALE_PER_CHANNEL) { set_error("bad scale mode"); return CC_ERR_ARG; }
+  if (!quant_codec(codec)) { set_error("cc_encode_step_segmented: codec must be sign1/quant2/quant4"); return CC_ERR_UNSUPPORTED; }
+  if (segments < 1 || cols % segments != 0) { set_error("segments must divide cols"); return CC_ERR_SHAPE; }
+  if (segments == 1)
+    return quant_encode_step(codec, mode, scale_mode, rows, cols, x, x_dtype, base, aux, body, workspace,
+                             workspace_bytes, record, (cudaStream_t)stream);
+  if (!fused_supported(rows, cols, x, x_dtype, base, aux, body) ||
+      !fused_segments_supported(rows, cols, segments, body_stride, codec)) {
+    set_error("cc_encode_step_segmented: shape / alignment not supported by the fused kernel "
+              "(needs cols % 128 == 0, cols <= 3072, (cols/segments) % 128 == 0, 16-byte aligned buffers)");
+    return CC_ERR_UNSUPPORTED;
+  }
+  return fused_encode_segments(codec, mode, scale_mode, rows, cols, segments, x, x_dtype, base, aux, body,
+                               body_stride, workspace, workspace_bytes, record, (cudaStream_t)stream);
 }
 
 CC_API int cc_warmup_step(int mode, int64_t rows, int64_t cols, const void *x, int x_dtype, float *base, float *aux,

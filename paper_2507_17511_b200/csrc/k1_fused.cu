@@ -41,7 +41,8 @@ constexpr int kCons = 384;             // consumer threads (12 warps)
 constexpr int kCW = kCons / 32;
 constexpr int kThreads = kCons + 64;   // + TMA load warp + TMA store warp
 constexpr int kMaxC = 2 * 4 * kCons;   // 3072 columns: two column quads per consumer thread
-constexpr int kUCache = 512;           // cached u_i per CTA for phase B
+constexpr int kNB = kMaxC / 128;       // 128-column blocks per row (one warp-quad span each)
+constexpr int kMaxSeg = 16;            // column segments with independent scales (Ulysses chunks)
 constexpr size_t kSmemBudget = 224 * 1024;
 
 struct Params {
@@ -54,9 +55,16 @@ struct Params {
   uint32_t ring_bytes;  // shared bytes of the tile rings
   int cb_row;           // code bytes per row
   int64_t nTiles;
-  double *colpart, *rowpart, *blkpart, *recpart, *record;
-  float *u, *v;
-  uint8_t *codes, *body_u, *body_v;
+  double *colpart, *rowpart, *blkpart, *recpart, *record;  // rowpart [nseg][n], blkpart [G][nseg],
+                                                           // recpart [G][nseg][2], record [nseg][2]
+  float *u, *v;                                            // u [nseg][un], v [C]
+  // Column segments: nseg column slices of width cw (multiple of 128), each an
+  // independent channel with its own scales and body (segment d = columns
+  // [d cw, (d+1) cw), body at body + d * body_stride: codes [n][cbs] | u[n] | v[cw]).
+  // nseg = 1 is the plain encode_step.
+  uint8_t *body;
+  int64_t body_stride, cbytes_seg, un;
+  int nseg, cw, cbs, bps;  // segments, width, code bytes per segment row, 128-col blocks per segment
   unsigned int *ticket;     // control words: zero on entry, left zero on exit
   unsigned int *bar;        // grid hand-off counters bar1 = bar[0], bar2 = bar[32] (control words)
   unsigned long long *ctr;  // dynamic tile counters [phase A, phase B], zeroed before launch
@@ -323,10 +331,9 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
 
   // ---- shared memory: [ring area][rp][red][ucache][barriers] ----
   uint8_t *ring = smem;
-  double *rp = reinterpret_cast<double *>(smem + p.ring_bytes);  // [2 use parities][SA][RA][kCW]
-  double *red = rp + (size_t)2 * SA * RA * kCW;                  // [512]: block sums + column partials
-  float *ucache = reinterpret_cast<float *>(red + 512);           // [kUCache]
-  uint64_t *fullA = reinterpret_cast<uint64_t *>(ucache + kUCache);
+  double *rp = reinterpret_cast<double *>(smem + p.ring_bytes);  // [2 use parities][SA][RA][kNB blocks]
+  double *red = rp + (size_t)2 * SA * RA * kNB;                  // [512]: reductions scratch
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(red + 512);
   uint64_t *emptyA = fullA + SA;
   uint64_t *fullB = emptyA + SA;
   uint64_t *emptyB = fullB + SI;
@@ -337,7 +344,12 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   volatile long long *tileB = tileA + SA;                                           // [SI]
   volatile long long *tileO = tileB + SI;                                           // [SO]
   float *ustage = reinterpret_cast<float *>(
-      (reinterpret_cast<uintptr_t>(const_cast<long long *>(tileO + SO)) + 15) & ~uintptr_t(15));  // [SI][16]
+      (reinterpret_cast<uintptr_t>(const_cast<long long *>(tileO + SO)) + 15) & ~uintptr_t(15));  // [SI][nseg][16]
+  const int nseg = p.nseg, bps = p.bps;
+  // the 128-column block (and so the segment) each of this thread's column quads lies in
+  int qblk[Q];
+#pragma unroll
+  for (int j = 0; j < Q; ++j) qblk[j] = Q == 2 ? j * kCW + warp : wig;
 
   auto stamp = [&](int i) {
     if (p.timer && tid == 0) p.timer[(size_t)cta * 8 + i] = gtimer();
@@ -367,13 +379,15 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   const InStage LA = in_stage<MODE, XT>(RA, C, MODE == CC_WITH_FEEDBACK);
   double cta_total = 0.0;
   // producer lanes: row sums of a finished tile (stage s, use parity par)
+  // lane = d * RA + r owns (row r of the tile, segment d): RA * nseg <= 32 (launcher)
   auto finish_rows = [&](int s, long long tile, uint32_t par) {
     const int64_t r0 = (int64_t)tile * RA;
-    if (lane < RA && r0 + lane < n) {
+    const int r = lane % RA, d = lane / RA;
+    if (d < nseg && r0 + r < n) {
       double acc = 0.0;
-      const double *q = rp + (((size_t)par * SA + s) * RA + lane) * kCW;
-      for (int w = 0; w < p.wpg; ++w) acc += q[w];
-      p.rowpart[r0 + lane] = acc;
+      const double *q = rp + (((size_t)par * SA + s) * RA + r) * kNB + d * bps;
+      for (int b = 0; b < bps; ++b) acc += q[b];
+      p.rowpart[(int64_t)d * n + r0 + r] = acc;
       cta_total += acc;
     }
   };
@@ -387,7 +401,9 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   uint8_t *out_ring = ring + (size_t)SI * LI.bytes;
   const int64_t nTB = (n + RB - 1) / RB;
   unsigned int *bar1 = p.bar, *bar2 = p.bar + 32;  // separate 128-byte lines
-  double err = 0.0, tsq = 0.0;
+  double err[Q], tsq[Q];  // StepRecord partials per column quad (its block's segment)
+#pragma unroll
+  for (int j = 0; j < Q; ++j) err[j] = tsq[j] = 0.0;
 
   // Grid-wide hand-offs are flag barriers (arrive = fence + atomicAdd, wait = one
   // thread spinning on ld.acquire, then a CTA-local named barrier) instead of
@@ -458,10 +474,14 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       if (q > 0 && tileA[sq] >= 0) finish_rows(sq, tileA[sq], pq);
     }
    }
-    // CTA |t| total: the row sums live in lanes < RA
+    // CTA |t| total per segment: lanes d*RA .. d*RA+RA-1 hold segment d's row sums
     {
-      const double tot = warp_sum(cta_total);
-      if (lane == 0) p.blkpart[cta] = tot;
+      double tot = cta_total;
+      for (int o = 1; o < RA; ++o) {
+        const double v = __shfl_down_sync(0xffffffffu, cta_total, o);
+        if (lane % RA == 0) tot += v;
+      }
+      if (lane % RA == 0 && lane / RA < nseg) p.blkpart[(size_t)cta * nseg + lane / RA] = tot;
       __syncwarp();
       if (lane == 0) arrive_release(bar1);
     }
@@ -480,11 +500,12 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     const long long tail = (long long)p.tail_mult * G;
     unsigned long long nxt = 0;
     if (lane == 0) nxt = atomicAdd(p.ctr + 16, 1ull);
-    auto load_u = [&](int st_, long long tile) {  // lane 0: 16B-aligned window of u for the tile's rows
+    auto load_u = [&](int st_, long long tile) {  // lane 0: 16B-aligned windows of u_d for the tile's rows
       const int64_t r0 = (int64_t)tile * RB;
       const int nrows = (int)min64(RB, n - r0);
       const uint32_t ub = (uint32_t)(((r0 & 3) + nrows + 3) / 4 * 16);
-      bulk_g2s(ustage + (size_t)st_ * 16, p.u + (r0 & ~3LL), ub, &fullB[st_], pol);
+      for (int d = 0; d < nseg; ++d)
+        bulk_g2s(ustage + ((size_t)st_ * nseg + d) * 16, p.u + d * p.un + (r0 & ~3LL), ub, &fullB[st_], pol);
     };
     auto publish_u = [&](int nst) {
       if (lane == 0) {
@@ -518,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
           const int nrows = (int)min64(RB, n - r0);
           const uint32_t xb = (uint32_t)(nrows * C * sizeof(XT)), fb = (uint32_t)(nrows * C * 4);
           const uint32_t ub = (uint32_t)(((r0 & 3) + nrows + 3) / 4 * 16);
-          mbar_expect_tx(&fullB[s], xb + (has_aux<MODE>() ? 2 * fb : 0u) + ub);
+          mbar_expect_tx(&fullB[s], xb + (has_aux<MODE>() ? 2 * fb : 0u) + ub * nseg);
           if (u_ready) load_u(s, tile);
           bulk_g2s(st + LI.x, X + r0 * C, xb, &fullB[s], pol);
           if (has_aux<MODE>()) {
@@ -534,32 +555,41 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     if (!u_ready) publish_u(min(k + 1, SI));  // stages 0..k (the last one holds the sentinel)
   } else if (storer) {
     if (p.stop_after == 1 || p.stop_after == 3) return;
-    // ---- scale pass, row half (the consumers do the columns): g, u_i ----
+    // ---- scale pass, row half (the consumers do the columns): g_d, u_{d,i} ----
     {
-      // every load in flight before the reductions: block partials, then this CTA's row partials
+      __shared__ double gseg[kMaxSeg];
       mbar_wait(&handA[0], 0);  // bar1, relayed by consumer thread 0
-      double part = 0.0;
-      for (int i = lane; i < G; i += 32) part += __ldcg(p.blkpart + i);
+      for (int d = 0; d < nseg; ++d) {  // g_d = mean |t| over segment d (cx:142), same order in every CTA
+        double part = 0.0;
+        for (int i = lane; i < G; i += 32) part += __ldcg(p.blkpart + (size_t)i * nseg + d);
+        part = warp_sum(part);
+        if (lane == 0) gseg[d] = part / ((double)n * (double)p.cw);
+      }
+      __syncwarp();
       const int64_t uch = (n + G - 1) / G;
       const int64_t ui0 = (int64_t)cta * uch, ui1 = min64(n, ui0 + uch);
-      constexpr int kU = 4;
-      double rs[kU];
+      const int64_t nr = ui1 > ui0 ? ui1 - ui0 : 0;
+      for (int64_t k0 = 0; k0 < nr * nseg; k0 += 32 * 8) {
+        double rs[8];
 #pragma unroll
-      for (int q = 0; q < kU; ++q) rs[q] = ui0 + lane + 32 * q < ui1 ? __ldcg(p.rowpart + ui0 + lane + 32 * q) : 0.0;
-      const double g = warp_sum(part) / (double)(n * C);  // mean|t| (cx:142); same order in every CTA
-      for (int64_t i0 = ui0; i0 < ui1; i0 += 32 * kU) {
+        for (int q = 0; q < 8; ++q) {  // loads first, then the math
+          const int64_t k = k0 + lane + 32 * q;
+          rs[q] = k < nr * nseg ? __ldcg(p.rowpart + (k / nr) * n + ui0 + k % nr) : 0.0;
+        }
 #pragma unroll
-        for (int q = 0; q < kU; ++q) {
-          const int64_t i = i0 + lane + 32 * q;
-          if (i >= ui1) continue;
-          const double r = i0 == ui0 ? rs[q] : __ldcg(p.rowpart + i);
+        for (int q = 0; q < 8; ++q) {
+          const int64_t k = k0 + lane + 32 * q;
+          if (k >= nr * nseg) continue;
+          const int d = (int)(k / nr);
+          const int64_t i = ui0 + k % nr;
+          const double g = gseg[d];
           float u;
           if (p.scale_mode == CC_SCALE_PER_CHANNEL) u = 1.0f;
-          else if (p.scale_mode == CC_SCALE_PER_TOKEN) u = (float)(r / (double)C);
+          else if (p.scale_mode == CC_SCALE_PER_TOKEN) u = (float)(rs[q] / (double)p.cw);
           else if (g == 0.0) u = 1.0f;
-          else u = (float)fmax((r / (double)C) / g, kRowScaleFloor);  // cx:147
-          p.u[i] = u;
-          store_f32_bytes(p.body_u + 4 * i, u);
+          else u = (float)fmax((rs[q] / (double)p.cw) / g, kRowScaleFloor);  // cx:147
+          p.u[d * p.un + i] = u;
+          store_f32_bytes(p.body + d * p.body_stride + p.cbytes_seg + 4 * i, u);
         }
       }
       __syncwarp();
@@ -585,7 +615,14 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
           bulk_s2g(p.base + r0 * C, so + LO.base, (uint32_t)(nrows * C * 4));
           if constexpr (has_aux<MODE>()) bulk_s2g(p.aux + r0 * C, so + LO.aux, (uint32_t)(nrows * C * 4));
         }
-        bulk_s2g(p.codes + r0 * p.cb_row, so + LO.codes, (uint32_t)(nrows * p.cb_row));
+        if (nseg == 1) {
+          bulk_s2g(p.body + r0 * p.cb_row, so + LO.codes, (uint32_t)(nrows * p.cb_row));
+        } else {  // segment d's code row lives in its own body
+          for (int rr = 0; rr < nrows; ++rr)
+            for (int d = 0; d < nseg; ++d)
+              bulk_s2g(p.body + d * p.body_stride + (r0 + rr) * p.cbs, so + LO.codes + rr * p.cb_row + d * p.cbs,
+                       (uint32_t)p.cbs);
+        }
         bulk_commit();
         bulk_wait_read<0>();  // smem source consumed -> the slot may be rewritten
       }
@@ -613,9 +650,10 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       const int nrows = (int)min64(RA, n - (int64_t)tile * RA);
       if (grp < p.groups && !(p.policy & 8)) {
         for (int r = grp; r < nrows; r += p.groups) {
-          double rs = 0.0;
+          double rs[Q];
 #pragma unroll
           for (int j = 0; j < Q; ++j) {
+            rs[j] = 0.0;
             if (!qact[j]) continue;
             const size_t o = (size_t)r * C + qcol[j];
             float xx[4], bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f};
@@ -628,10 +666,13 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
               a[q] = fabs((double)target_of<MODE>(xx[q], bb[q], aa[q]));
               cs[j][q] += a[q];
             }
-            rs += ((a[0] + a[1]) + a[2]) + a[3];
+            rs[j] = ((a[0] + a[1]) + a[2]) + a[3];
           }
-          rs = warp_sum(rs);
-          if (lane == 0) rp[(((size_t)ph * SA + s) * RA + r) * kCW + wig] = rs;
+#pragma unroll
+          for (int j = 0; j < Q; ++j) {  // one partial per 128-column block
+            const double v = warp_sum(rs[j]);
+            if (lane == 0 && qblk[j] < kNB) rp[(((size_t)ph * SA + s) * RA + r) * kNB + qblk[j]] = v;
+          }
         }
       }
       __syncwarp();
@@ -706,7 +747,8 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
           float v = (float)(sacc / (double)n);  // colmean (cx:148)
           if (p.scale_mode == CC_SCALE_PER_TOKEN) v = 1.0f;
           p.v[j] = v;
-          store_f32_bytes(p.body_v + 4 * j, v);
+          const int d = (int)(j / p.cw);
+          store_f32_bytes(p.body + d * p.body_stride + p.cbytes_seg + 4 * n + 4 * (j - (int64_t)d * p.cw), v);
         }
         named_sync(1, kCons);
       }
@@ -770,7 +812,11 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
           }
         }
       }
-      const float uf = row_live ? ustage[(size_t)s * 16 + (r0 & 3) + r] : 1.0f;
+      float ufj[Q];
+#pragma unroll
+      for (int j = 0; j < Q; ++j)
+        ufj[j] = row_live && qblk[j] < kNB ? ustage[((size_t)s * nseg + min(qblk[j] / bps, nseg - 1)) * 16 + (r0 & 3) + r]
+                                          : 1.0f;
       __syncwarp();
       if (lane == 0) mbar_arrive(&emptyB[s]);  // inputs are in registers: the loader may refill
       if (k >= SO) mbar_wait(&outFree[o], pho ^ 1u);
@@ -778,20 +824,19 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       const bool direct = p.policy & 128;  // experiment: results straight to HBM (generic stores)
       float *obase = direct ? p.base + r0 * C : reinterpret_cast<float *>(so + LO.base);
       float *oaux = direct ? p.aux + r0 * C : reinterpret_cast<float *>(so + LO.aux);
-      uint8_t *ocode = direct ? p.codes + r0 * p.cb_row : so + LO.codes;
-      const bool row_ok = scale_in_range(fabsf(uf));
+      uint8_t *ocode = direct && nseg == 1 ? p.body + r0 * p.cb_row : so + LO.codes;
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
         float t[4], d[4], e[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) t[q] = target_of<MODE>(xx[j][q], bb[j][q], aa[j][q]);
-        const uint32_t packed = quantize4<CODEC>(t, uf, row_ok, cc[j], d);
+        const uint32_t packed = quantize4<CODEC>(t, ufj[j], scale_in_range(fabsf(ufj[j])), cc[j], d);
 #pragma unroll
         for (int q = 0; q < 4; ++q) e[q] = __fsub_rn(t[q], d[q]);
         const bool live = row_live && qact[j];
         const size_t oo = (size_t)r * C + qcol[j];
         if (live) {
-          record4(t, e, err, tsq);
+          record4(t, e, err[j], tsq[j]);
           float4 nb;
           if constexpr (MODE == CC_NAIVE) {
             nb = make_float4(d[0], d[1], d[2], d[3]);
@@ -826,22 +871,51 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   stamp(5);
   {
     __shared__ unsigned last;
-    double es, ts;
-    cons_sum2(err, tsq, red, es, ts);
-    if (tid == 0) {
-      p.recpart[2 * cta] = es;
-      p.recpart[2 * cta + 1] = ts;
-      last = atom_add_acq_rel(p.ticket) == (unsigned)G - 1;  // release: partials; acquire: the others'
+    // per (warp, quad slot) partials, then per segment in a fixed (warp, slot) order
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+      const double a = warp_sum(err[j]), b = warp_sum(tsq[j]);
+      if (lane == 0) {
+        red[(warp * Q + j) * 2] = a;
+        red[(warp * Q + j) * 2 + 1] = b;
+      }
     }
     named_sync(1, kCons);
+    if (tid < nseg) {
+      double a = 0.0, b = 0.0;
+      for (int w = 0; w < kCW; ++w)
+        for (int j = 0; j < Q; ++j) {
+          const int blk = Q == 2 ? j * kCW + w : (w % (int)(p.G4 / 32));
+          if (blk < kNB && blk / bps == tid) {
+            a += red[(w * Q + j) * 2];
+            b += red[(w * Q + j) * 2 + 1];
+          }
+        }
+      p.recpart[((size_t)cta * nseg + tid) * 2] = a;
+      p.recpart[((size_t)cta * nseg + tid) * 2 + 1] = b;
+    }
+    named_sync(1, kCons);
+    if (tid == 0) last = atom_add_acq_rel(p.ticket) == (unsigned)G - 1;  // release: partials; acquire: others'
+    named_sync(1, kCons);
     if (last) {  // the last CTA reduces the per-CTA partials in a fixed order
-      const double pa = tid < G ? __ldcg(p.recpart + 2 * tid) : 0.0;  // both loads in flight together
-      const double pb = tid < G ? __ldcg(p.recpart + 2 * tid + 1) : 0.0;
-      double a, b;
-      cons_sum2(pa, pb, red, a, b);
+      double vals[2 * kMaxSeg];
+#pragma unroll
+      for (int k = 0; k < 2 * kMaxSeg; ++k)  // every load in flight before the sums
+        vals[k] = (k < 2 * nseg && tid < G) ? __ldcg(p.recpart + (size_t)tid * nseg * 2 + k) : 0.0;
+      named_sync(1, kCons);  // red is reused below
+#pragma unroll
+      for (int k = 0; k < 2 * kMaxSeg; ++k) {
+        if (k >= 2 * nseg) break;
+        const double v = warp_sum(vals[k]);
+        if (lane == 0) red[warp * 2 * kMaxSeg + k] = v;
+      }
+      named_sync(1, kCons);
+      if (tid < 2 * nseg) {
+        double a = 0.0;
+        for (int w = 0; w < kCW; ++w) a += red[w * 2 * kMaxSeg + tid];
+        p.record[tid] = a;  // record[2d] = ||d - t||^2, record[2d+1] = ||t||^2 of segment d
+      }
       if (tid == 0) {
-        p.record[0] = a;
-        p.record[1] = b;
         // every CTA passed both hand-offs and finished claiming before taking its
         // ticket: leave the control words zeroed for the next launch
         p.ctr[16] = 0ull;
@@ -851,7 +925,6 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       }
     }
   }
-  stamp(6);
   stamp(6);
 }
 
@@ -890,25 +963,45 @@ bool fused_supported(int64_t n, int64_t C, const void *x, int x_dtype, const flo
   return true;
 }
 
+// workspace layout (any segment count up to kMaxSeg)
+static size_t fused_ws_layout(int64_t n, int64_t C, int G, int nseg, uint8_t *w, fused::Params *p) {
+  size_t off = 0;
+  const int64_t un = (n + 3) & ~int64_t(3);
+  auto take = [&](size_t bytes) {
+    uint8_t *q = w ? w + off : nullptr;
+    off = align_up(off + bytes, 256);
+    return q;
+  };
+  uint8_t *colpart = take(sizeof(double) * (size_t)G * C);
+  uint8_t *rowpart = take(sizeof(double) * nseg * n);
+  uint8_t *blkpart = take(sizeof(double) * (size_t)G * nseg);
+  uint8_t *recpart = take(sizeof(double) * 2 * (size_t)G * nseg);
+  uint8_t *u = take(sizeof(float) * nseg * un);
+  uint8_t *v = take(sizeof(float) * C);
+  uint8_t *ctl = take(512);
+  if (p) {
+    p->colpart = reinterpret_cast<double *>(colpart);
+    p->rowpart = reinterpret_cast<double *>(rowpart);
+    p->blkpart = reinterpret_cast<double *>(blkpart);
+    p->recpart = reinterpret_cast<double *>(recpart);
+    p->u = reinterpret_cast<float *>(u);
+    p->v = reinterpret_cast<float *>(v);
+    p->un = un;
+    p->ctr = reinterpret_cast<unsigned long long *>(ctl);
+  }
+  return off;
+}
+
 int64_t fused_workspace_bytes(int64_t n, int64_t C) {
-  const int G = fused::kThreads;  // upper bound on the grid
-  size_t b = 0;
-  auto add = [&](size_t x) { b += align_up(x, 256); };
-  add(sizeof(double) * (size_t)G * C);  // colpart
-  add(sizeof(double) * n);              // rowpart
-  add(sizeof(double) * G);              // blkpart
-  add(sizeof(double) * 2 * G);          // recpart
-  add(sizeof(float) * n);
-  add(sizeof(float) * C);
-  add(512);
-  return (int64_t)b;
+  return (int64_t)fused_ws_layout(n, C, fused::kCons, fused::kMaxSeg, nullptr, nullptr);
 }
 
 template <int MODE, int CODEC, typename XT, int Q>
 static int launch_fused(fused::Params &p, cudaStream_t st) {
   using namespace fused;
   auto kern = k1_fused<MODE, CODEC, XT, Q>;
-  const size_t fixed_tail = 512 * 8 + kUCache * 4 + 3 * 8 * 8 * 3 + 8 * 64 + 256;
+  const size_t ustage_bytes = (size_t)8 * p.nseg * 64;  // [S_in <= 8][nseg][16] floats
+  const size_t fixed_tail = 512 * 8 + 3 * 8 * 8 * 3 + 8 * 64 + 256 + ustage_bytes;
   const size_t budget = kSmemBudget;
   // phase B rings (tiles of `groups` rows): loads S_in, outputs S_out
   const InStage LI = in_stage<MODE, XT>(p.groups, p.C, has_aux<MODE>());
@@ -916,12 +1009,12 @@ static int launch_fused(fused::Params &p, cudaStream_t st) {
   const InStage LA = in_stage<MODE, XT>(p.R, p.C, MODE == CC_WITH_FEEDBACK);
   // phase A ring + its row-partial scratch (2 use parities x SA stages)
   int SA = (int)std::min<size_t>(g_fused_sa > 0 ? g_fused_sa : 8,
-                                  (budget - fixed_tail) / (LA.bytes + (size_t)2 * p.R * kCW * 8));
+                                  (budget - fixed_tail) / (LA.bytes + (size_t)2 * p.R * kNB * 8));
   if (SA < 2) {
     set_error("k1_fused: phase-A stages do not fit shared memory");
     return CC_ERR_UNSUPPORTED;
   }
-  const size_t rp_bytes = (size_t)2 * SA * p.R * kCW * 8;
+  const size_t rp_bytes = (size_t)2 * SA * p.R * kNB * 8;
   // phase B rings share the ring area: loads S_in, outputs S_out
   int SO = g_fused_so > 0 ? g_fused_so : 2, SI = 0;
   for (;;) {
@@ -943,8 +1036,8 @@ static int launch_fused(fused::Params &p, cudaStream_t st) {
   p.S_in = SI;
   p.S_out = SO;
   p.ring_bytes = (uint32_t)align_up(std::max(ringA, ringB), 128);
-  const size_t smem = p.ring_bytes + rp_bytes + 512 * 8 + kUCache * 4 +
-                      (size_t)(3 * SA + 3 * SI + 3 * SO + 2) * 8 + 16 + (size_t)SI * 64 + 128;
+  const size_t smem = p.ring_bytes + rp_bytes + 512 * 8 + (size_t)(3 * SA + 3 * SI + 3 * SO + 2) * 8 + 16 +
+                      (size_t)SI * p.nseg * 64 + 128;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return cuda_status("k1_fused attr");
   void *args[] = {&p};
@@ -959,8 +1052,28 @@ static int launch_fused(fused::Params &p, cudaStream_t st) {
   return CC_OK;
 }
 
-int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, const void *x, int x_dtype, float *base,
-                 float *aux, uint8_t *body, void *ws, int64_t ws_bytes, double *record, cudaStream_t st) {
+// nseg column segments of width C / nseg (see Params): segment d is an independent
+// encode_step channel over columns [d cw, (d+1) cw) with its body at body + d *
+// body_stride and its record at record + 2 d.  nseg = 1: the plain encode_step.
+bool fused_segments_supported(int64_t n, int64_t C, int nseg, int64_t body_stride, int codec) {
+  using namespace fused;
+  if (nseg < 1 || nseg > kMaxSeg || C % nseg != 0) return false;
+  const int64_t cw = C / nseg;
+  if (nseg > 1) {
+    const int bits = codec == CC_SIGN1 ? 1 : (codec == CC_QUANT2 ? 2 : 4);
+    if (cw % 128 != 0 || (cw * bits / 8) % 16 != 0 || body_stride % 16 != 0) return false;
+    const int64_t body = cdiv(n * cw * bits, 8) + 4 * (n + cw);
+    if (body_stride < body) return false;
+    // rows per phase-A tile x segments must fit one warp (finish_rows lanes)
+    const int groups = C / 4 > kCons ? 1 : kCons / (int)(C / 4);
+    if (2 * groups * nseg > 32) return false;
+  }
+  return true;
+}
+
+int fused_encode_segments(int codec, int mode, int scale_mode, int64_t n, int64_t C, int nseg, const void *x,
+                          int x_dtype, float *base, float *aux, uint8_t *body, int64_t body_stride, void *ws,
+                          int64_t ws_bytes, double *record, cudaStream_t st) {
   using namespace fused;
   Params p{};
   p.x = x;
@@ -994,25 +1107,17 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
   p.policy = g_fused_policy;
   const int bits = codec == CC_SIGN1 ? 1 : (codec == CC_QUANT2 ? 2 : 4);
   p.cb_row = (int)(C * bits / 8);
-  const int64_t cbytes = cdiv(n * C * bits, 8);
-  p.codes = body;
-  p.body_u = body + cbytes;
-  p.body_v = p.body_u + 4 * n;
+  p.nseg = nseg;
+  p.cw = (int)(C / nseg);
+  p.cbs = (int)(p.cw * bits / 8);
+  p.bps = p.cw / 128;
+  if (p.bps < 1) p.bps = kNB;  // nseg = 1 with C < 128 cannot happen (C % 128 == 0); keep finish_rows sane
+  p.cbytes_seg = cdiv(n * p.cw * bits, 8);
+  p.body = body;
+  p.body_stride = nseg > 1 ? body_stride : 0;
   p.record = record;
-  uint8_t *w = reinterpret_cast<uint8_t *>(ws);
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    uint8_t *q = w + off;
-    off = align_up(off + bytes, 256);
-    return q;
-  };
-  p.colpart = reinterpret_cast<double *>(take(sizeof(double) * (size_t)G * C));
-  p.rowpart = reinterpret_cast<double *>(take(sizeof(double) * n));
-  p.blkpart = reinterpret_cast<double *>(take(sizeof(double) * G));
-  p.recpart = reinterpret_cast<double *>(take(sizeof(double) * 2 * G));
-  p.u = reinterpret_cast<float *>(take(sizeof(float) * n));
-  p.v = reinterpret_cast<float *>(take(sizeof(float) * C));
-  uint8_t *ctl_ws = take(512);
+  const size_t off = fused_ws_layout(n, C, G, nseg, reinterpret_cast<uint8_t *>(ws), &p);
+  uint8_t *ctl_ws = reinterpret_cast<uint8_t *>(p.ctr);
   // control words, one 128-byte line each (pollers and atomics never share a line):
   // ctr0 @0, ctr1 @128, bar1 @256 (+ ticket @260), bar2 @384.  The stream's
   // library-owned slot (kept zero by every launch), or the workspace + a memset
@@ -1048,4 +1153,12 @@ int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, cons
 #undef CC_FUSED_Q
 }
 
+}  // namespace cc
+
+namespace cc {
+int fused_encode(int codec, int mode, int scale_mode, int64_t n, int64_t C, const void *x, int x_dtype, float *base,
+                 float *aux, uint8_t *body, void *ws, int64_t ws_bytes, double *record, cudaStream_t st) {
+  return fused_encode_segments(codec, mode, scale_mode, n, C, 1, x, x_dtype, base, aux, body, 0, ws, ws_bytes, record,
+                               st);
+}
 }  // namespace cc
