@@ -14,6 +14,8 @@ import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libcompactcomm_b200.so")
+# experiments only: load an alternative build (A/B of kernel variants in one process)
+LIB_PATH = os.environ.get("CC_LIB_OVERRIDE", LIB_PATH)
 HEADER = os.path.join(os.path.dirname(HERE), "include", "compactcomm.h")
 
 # constants mirrored from include/compactcomm.h (checked by tests/test_abi.py)
