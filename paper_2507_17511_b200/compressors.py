@@ -505,7 +505,10 @@ def encode_lowrank(a, spec, rng, decoded=None):
     if not (1 <= r <= min(rows, cols)):
         raise ShapeError(f"rank {r} out of range for shape {(rows, cols)}")
     lib = _lib.load()
-    q0 = torch.from_numpy(subspace_init(rng, cols, r)).to(t.device)
+    # Q0 is drawn on the host from the reference's PCG64 stream (cx:407); a pinned
+    # staging copy keeps the H2D transfer asynchronous (no stream drain per step)
+    q0 = torch.from_numpy(subspace_init(rng, cols, r))
+    q0 = q0.pin_memory().to(t.device, non_blocking=True) if t.is_cuda else q0.to(t.device)
     tag = _lib.CC_LOWRANK4 if spec.int4_factors else _lib.CC_LOWRANK
     body = _empty_body(lib.cc_body_bytes(tag, rows, cols, r))
     ws = workspace(_lib.check(lib.cc_lowrank_workspace_bytes(rows, cols, r)), "lowrank")

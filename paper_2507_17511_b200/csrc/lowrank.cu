@@ -18,6 +18,7 @@
 #include "cc_internal.h"
 
 #include <algorithm>
+#include <cooperative_groups.h>
 #include <curand_kernel.h>
 
 namespace cc {
@@ -294,6 +295,151 @@ __global__ void __launch_bounds__(1024) k_cgs2_fallback(const float *__restrict_
   }
 }
 
+// ---------------------------------------------------------------------------
+// CholQR2 in ONE cooperative launch (the production orth): nb = ceil(m / 128)
+// CTAs x 256 threads, CTA b keeps rows [128 b, 128 b + 128) of M in shared
+// memory (f64).  Per pass: partial Gram of the CTA's rows -> grid sync -> every
+// CTA sums the partials in the same fixed order, factors G = R^T R and forms
+// R^-1 (identical in every CTA) -> M <- M R^-1 on its rows.  Same arithmetic as
+// k_gram / k_chol / k_apply_rinv (so the same Q bit for bit), without the eight
+// dependent launches.  A degenerate pivot (la:13) in either pass hands the whole
+// matrix to CTA 0's CGS2 with random replacement columns (la:77-112).
+// ---------------------------------------------------------------------------
+constexpr int kOrthThreads = 256;
+
+__device__ void cgs2_block(const float *__restrict__ orig, double *__restrict__ M, float *__restrict__ out,
+                           int64_t m, int r, unsigned long long seed, double *red, double *coef) {
+  auto block_sum = [&](double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    __syncthreads();
+    return s;
+  };
+  curandStatePhilox4_32_10_t rng;
+  curand_init(seed, threadIdx.x, 0, &rng);
+  for (int64_t e = threadIdx.x; e < m * r; e += blockDim.x) M[e] = (double)orig[e];
+  __syncthreads();
+  for (int j = 0; j < r; ++j) {
+    for (int attempt = 0;; ++attempt) {
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int k = 0; k < j; ++k) {
+          double part = 0.0;
+          for (int64_t i = threadIdx.x; i < m; i += blockDim.x) part += M[i * r + k] * M[i * r + j];
+          const double s = block_sum(part);
+          if (threadIdx.x == 0) coef[k] = s;
+        }
+        __syncthreads();
+        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+          double v = M[i * r + j];
+          for (int k = 0; k < j; ++k) v -= M[i * r + k] * coef[k];
+          M[i * r + j] = v;
+        }
+        __syncthreads();
+      }
+      double part = 0.0;
+      for (int64_t i = threadIdx.x; i < m; i += blockDim.x) part += M[i * r + j] * M[i * r + j];
+      const double nsq = block_sum(part);
+      if (nsq >= kDegenerate || attempt > 16) {
+        const double inv = 1.0 / sqrt(nsq);
+        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) M[i * r + j] *= inv;
+        __syncthreads();
+        break;
+      }
+      for (int64_t i = threadIdx.x; i < m; i += blockDim.x) M[i * r + j] = (double)curand_normal(&rng);
+      __syncthreads();
+    }
+  }
+  for (int64_t e = threadIdx.x; e < m * r; e += blockDim.x) out[e] = (float)M[e];
+}
+
+__global__ void __launch_bounds__(kOrthThreads) k_orth(const float *__restrict__ Min, float *__restrict__ out,
+                                                        int64_t m, int r, double *__restrict__ Gpart,
+                                                        double *__restrict__ scratch, unsigned long long seed) {
+  extern __shared__ double osm[];
+  double(*ms)[kMaxR + 1] = reinterpret_cast<double(*)[kMaxR + 1]>(osm);           // [kGramRows][33]
+  double(*G)[kMaxR + 1] = reinterpret_cast<double(*)[kMaxR + 1]>(osm + kGramRows * (kMaxR + 1));
+  double(*R)[kMaxR + 1] = G + kMaxR;
+  double(*Ri)[kMaxR + 1] = R + kMaxR;
+  __shared__ int bad;
+  __shared__ double red[kOrthThreads / 32], coef[kMaxR];
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int tid = threadIdx.x, b = blockIdx.x, nb = gridDim.x;
+  const int64_t i0 = (int64_t)b * kGramRows;
+  const int rc = (int)min64(kGramRows, m - i0);
+  for (int e = tid; e < rc * r; e += kOrthThreads) ms[e / r][e % r] = (double)Min[(i0 + e / r) * r + e % r];
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    double *gp = Gpart + (size_t)pass * nb * r * r;
+    for (int o = tid; o < r * r; o += kOrthThreads) {  // partial Gram of this CTA's rows (as k_gram)
+      const int a = o / r, c = o % r;
+      double acc = 0.0;
+      for (int i = 0; i < rc; ++i) acc += ms[i][a] * ms[i][c];
+      gp[(size_t)b * r * r + o] = acc;
+    }
+    grid.sync();
+    for (int o = tid; o < r * r; o += kOrthThreads) {  // fixed-order sum of the partials (as k_chol)
+      const int a = o / r, c = o % r;
+      double acc = 0.0;
+      int bb = 0;
+      for (; bb + 8 <= nb; bb += 8) {
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = __ldcg(gp + (size_t)(bb + q) * r * r + o);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += v[q];
+      }
+      for (; bb < nb; ++bb) acc += __ldcg(gp + (size_t)bb * r * r + o);
+      G[a][c] = acc;
+      R[a][c] = 0.0;
+    }
+    __syncthreads();
+    if (tid < 32) {  // one warp: right-looking Cholesky (as k_chol) and R^-1, lane c owns column c
+      const int c = tid;
+      for (int j = 0; j < r; ++j) {
+        double piv = G[j][j];  // every lane reads the same pivot
+        if (!(piv >= kDegenerate)) {
+          if (c == 0) bad = 1;
+          piv = 1.0;
+        }
+        const double rjj = sqrt(piv);
+        if (c == j) R[j][j] = rjj;
+        if (c > j && c < r) R[j][c] = G[j][c] / rjj;
+        __syncwarp();
+        if (c > j && c < r)
+          for (int a = j + 1; a < r; ++a) G[a][c] -= R[j][a] * R[j][c];
+        __syncwarp();
+      }
+      if (c < r) {  // column c of R^-1 (upper triangular), back substitution into shared memory
+        for (int i = r - 1; i >= 0; --i) {
+          double sacc = (i == c) ? 1.0 : 0.0;
+          for (int k = i + 1; k <= c; ++k) sacc -= R[i][k] * Ri[k][c];
+          Ri[i][c] = (i > c) ? 0.0 : sacc / R[i][i];
+        }
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < rc; i += kOrthThreads) {  // M <- M R^-1 (as k_apply_rinv)
+      double row[kMaxR];
+      for (int k = 0; k < r; ++k) row[k] = ms[i][k];
+      for (int c = 0; c < r; ++c) {
+        double acc = 0.0;
+        for (int k = 0; k <= c; ++k) acc += row[k] * Ri[k][c];
+        ms[i][c] = acc;
+      }
+    }
+    __syncthreads();
+  }
+  if (!bad) {
+    for (int e = tid; e < rc * r; e += kOrthThreads) out[(i0 + e / r) * r + e % r] = (float)ms[e / r][e % r];
+  } else if (b == 0) {  // every CTA saw the same pivots: CTA 0 alone re-orthogonalizes with CGS2
+    cgs2_block(Min, scratch, out, m, r, seed, red, coef);
+  }
+}
+
 __global__ void k_to32(const double *__restrict__ in, float *__restrict__ out, int64_t cnt) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e < cnt) out[e] = (float)in[e];
@@ -433,7 +579,7 @@ static Work carve(void *ws, int64_t n, int64_t C, int64_t r, size_t *bytes) {
   w.W = reinterpret_cast<float *>(take(4 * C * r));
   w.Zpart = reinterpret_cast<double *>(take(8 * kSplitATY * C * r));
   w.M64 = reinterpret_cast<double *>(take(8 * m * r));
-  w.Gpart = reinterpret_cast<double *>(take(8 * cdiv(m, kGramRows) * r * r));
+  w.Gpart = reinterpret_cast<double *>(take(8 * 2 * cdiv(m, kGramRows) * r * r));
   w.Rinv = reinterpret_cast<double *>(take(8 * r * r));
   w.Uf = reinterpret_cast<double *>(take(8 * n * r));
   w.Wf = reinterpret_cast<double *>(take(8 * C * r));
@@ -458,6 +604,24 @@ static unsigned long long g_lr_seed = 0x5eed5eedULL;
 // M (f32 [m, r]) -> orthonormal f32 columns written to out (may alias M)
 static void orth(const float *M, float *out, int64_t m, int r, const lr::Work &w, cudaStream_t st) {
   using namespace lr;
+  {
+    const int nb = (int)cdiv(m, kGramRows);
+    const size_t smem = sizeof(double) * (size_t)(kGramRows + 3 * kMaxR) * (kMaxR + 1);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_orth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    unsigned long long seed = g_lr_seed++;
+    double *gp = w.Gpart, *scratch = w.M64;
+    void *args[] = {&M, &out, &m, &r, &gp, &scratch, &seed};
+    if (cudaLaunchCooperativeKernel((const void *)k_orth, dim3(nb), dim3(kOrthThreads), args, smem, st) ==
+        cudaSuccess) {
+      count_launch();
+      return;
+    }
+    cudaGetLastError();  // fall through to the multi-kernel CholQR2
+  }
   const int64_t cnt = m * r;
   const unsigned b1 = (unsigned)cdiv(cnt, 256);
   k_to64<<<b1, 256, 0, st>>>(M, w.M64, cnt);

@@ -58,12 +58,31 @@ __global__ void __launch_bounds__(256) k_apply(const XT *__restrict__ x, const f
   }
 }
 
-__global__ void k_sum_parts(int nparts, const double *__restrict__ part, double *__restrict__ record) {
+// fixed-order parallel sum of the per-block partials (256 threads: strided
+// per-thread sums, warp butterflies, warps in order)
+__global__ void __launch_bounds__(256) k_sum_parts(int nparts, const double *__restrict__ part,
+                                                   double *__restrict__ record) {
+  __shared__ double sa[8], sb[8];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += 256) {
+    a += part[2 * i];
+    b += part[2 * i + 1];
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if ((threadIdx.x & 31) == 0) {
+    sa[threadIdx.x >> 5] = a;
+    sb[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (int i = 0; i < nparts; ++i) { a += part[2 * i]; b += part[2 * i + 1]; }
-    record[0] = a;
-    record[1] = b;
+    double x = 0.0, y = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      x += sa[w];
+      y += sb[w];
+    }
+    record[0] = x;
+    record[1] = y;
   }
 }
 
@@ -106,7 +125,7 @@ int apply_decoded(int mode, int64_t n, int64_t C, const void *x, int x_dtype, co
     else CC_A(CC_NAIVE, __nv_bfloat16);
   }
 #undef CC_A
-  k_sum_parts<<<1, 32, 0, st>>>(kApplyBlocks, part, record);
+  k_sum_parts<<<1, 256, 0, st>>>(kApplyBlocks, part, record);
   count_launch(2);
   return cuda_status("apply_decoded");
 }
