@@ -235,14 +235,15 @@ __global__ void __launch_bounds__(kThreads) k_hsub(const float *__restrict__ t, 
   const uint32_t prefix = LEVEL == 2 ? st->b1 : ((st->b1 << 12) | st->b2);
   constexpr int shift = LEVEL == 2 ? 19 : 7;
   const int64_t nitems = (total + 3) / 4;
-  const int64_t stride = (int64_t)gridDim.x * kThreads * 2;
-  for (int64_t i0 = (int64_t)blockIdx.x * kThreads * 2; i0 < nitems; i0 += stride) {
-    uint32_t key[8];
+  constexpr int kU = 4;  // float4 loads in flight per thread
+  const int64_t stride = (int64_t)gridDim.x * kThreads * kU;
+  for (int64_t i0 = (int64_t)blockIdx.x * kThreads * kU; i0 < nitems; i0 += stride) {
+    uint32_t key[4 * kU];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kU; ++u) {
       const int64_t e = (i0 + u * kThreads + threadIdx.x) * 4;
       if (vec && e + 4 <= total) {
-        const float4 v = __ldcs(reinterpret_cast<const float4 *>(t + e));
+        const float4 v = __ldcg(reinterpret_cast<const float4 *>(t + e));  // t is re-read: keep it in L2
         key[4 * u] = key_of(v.x); key[4 * u + 1] = key_of(v.y);
         key[4 * u + 2] = key_of(v.z); key[4 * u + 3] = key_of(v.w);
       } else {
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(kThreads) k_hsub(const float *__restrict__ t, 
       }
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < 4 * kU; ++j) {
       const bool in = key[j] != 0xffffffffu && (key[j] >> shift) == prefix;
       hist_add(h, LEVEL == 2 ? (key[j] >> 7) & 0xfffu : key[j] & 127u, in);
     }
@@ -269,10 +270,32 @@ __global__ void __launch_bounds__(kThreads) k_count(const float *__restrict__ t,
   const int64_t c0 = (int64_t)blockIdx.x * kChunk;
   const int64_t c1 = min64(total, c0 + kChunk);
   uint32_t gt = 0, eq = 0;
-  for (int64_t e = c0 + threadIdx.x; e < c1; e += kThreads) {
-    const uint32_t key = key_of(__ldcs(t + e));
-    gt += key > T;
-    eq += key == T;
+  if (((c1 - c0) & 3) == 0 && (reinterpret_cast<uintptr_t>(t) & 15) == 0) {
+    // kChunk / 4 float4 per CTA: all of a thread's loads in flight together
+    constexpr int kV = kChunk / 4 / kThreads;  // 8
+    float4 v[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int64_t e = c0 + 4 * ((int64_t)u * kThreads + threadIdx.x);
+      v[u] = e < c1 ? __ldcg(reinterpret_cast<const float4 *>(t + e)) : make_float4(-0.f, -0.f, -0.f, -0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int64_t e = c0 + 4 * ((int64_t)u * kThreads + threadIdx.x);
+      if (e >= c1) continue;
+      const uint32_t k4[4] = {key_of(v[u].x), key_of(v[u].y), key_of(v[u].z), key_of(v[u].w)};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        gt += k4[q] > T;
+        eq += k4[q] == T;
+      }
+    }
+  } else {
+    for (int64_t e = c0 + threadIdx.x; e < c1; e += kThreads) {
+      const uint32_t key = key_of(__ldcg(t + e));
+      gt += key > T;
+      eq += key == T;
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -380,9 +403,33 @@ __global__ void __launch_bounds__(kThreads) k_write(const float *__restrict__ t,
   const uint32_t T = st->T, ties = st->ties;
   const int64_t c0 = (int64_t)blockIdx.x * kChunk;
   const int64_t c1 = min64(total, c0 + kChunk);
-  for (int64_t e = c0 + threadIdx.x; e < c0 + kChunk; e += kThreads) {
-    const int i = (int)(e - c0);
-    tv_s[(i / kRun) * (kRun + 1) + i % kRun] = e < c1 ? __ldcs(t + e) : 0.0f;
+  if ((reinterpret_cast<uintptr_t>(t) & 15) == 0) {
+    constexpr int kV = kChunk / 4 / kThreads;  // 8 float4 per thread, all in flight together
+    float4 v[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int64_t e = c0 + 4 * ((int64_t)u * kThreads + threadIdx.x);
+      if (e + 4 <= c1) {
+        v[u] = __ldcs(reinterpret_cast<const float4 *>(t + e));
+      } else {
+        v[u].x = e < c1 ? __ldcs(t + e) : 0.0f;
+        v[u].y = e + 1 < c1 ? __ldcs(t + e + 1) : 0.0f;
+        v[u].z = e + 2 < c1 ? __ldcs(t + e + 2) : 0.0f;
+        v[u].w = e + 3 < c1 ? __ldcs(t + e + 3) : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int i = 4 * (u * kThreads + threadIdx.x);
+      const float vv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tv_s[((i + q) / kRun) * (kRun + 1) + (i + q) % kRun] = vv[q];
+    }
+  } else {
+    for (int64_t e = c0 + threadIdx.x; e < c0 + kChunk; e += kThreads) {
+      const int i = (int)(e - c0);
+      tv_s[(i / kRun) * (kRun + 1) + i % kRun] = e < c1 ? __ldcs(t + e) : 0.0f;
+    }
   }
   __syncthreads();
   const float *run = tv_s + threadIdx.x * (kRun + 1);
@@ -553,7 +600,7 @@ static void select_and_write(const topk::Work &w, const float *t, const XT *x, f
                              float *decoded, int64_t total, int64_t k, uint8_t *body, double *record, int stateful,
                              cudaStream_t st) {
   using namespace topk;
-  const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, kThreads), sm_count() * 2));
+  const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 4 * kThreads), sm_count() * 8));
   k_find<kBins><<<1, 1024, 0, st>>>(w.hist1, w.st, 1, (uint32_t)k);
   const int vec = al16(t);
   k_hsub<2><<<nb, kThreads, 0, st>>>(t, total, vec, w.st, w.hist2);
