@@ -397,6 +397,10 @@ def run_b200(a, world, rank):
         del graphs
         sim = {f"patch{P}": sim_rank_measure("patch", P, "quant2bit", L, rows, cols) for P in (2, 4, 8)}
         sim["ulysses8"] = sim_rank_measure("ulysses", 8, "sign1bit", L, rows, cols)
+        sim["topk1pct_patch8"] = sim_rank_measure("patch", 8, "topk", L, rows, cols, spec_kw={"keep_fraction": 0.01})
+        sim["topk10pct_patch8"] = sim_rank_measure("patch", 8, "topk", L, rows, cols, spec_kw={"keep_fraction": 0.1})
+        sim["lowrank_r8_patch4"] = sim_rank_measure("patch", 4, "lowrank", 8, rows, cols, steps=3, warmup=2,
+                                                    spec_kw={"rank": 8, "iterations": 2}, graph=False)
     cpu = None
     if not a.no_cpu and rank == 0 and world == 1:
         threads = min(os.cpu_count() or 1, 16)
@@ -533,7 +537,7 @@ def measure_e2e(exs, inputs, streams, world, K, L, rows, cols, lo, hi, dev):
             "d2h_bytes_per_step": d2h}
 
 
-def sim_rank_measure(kind, P, codec, L, rows, cols, steps=5, warmup=3):
+def sim_rank_measure(kind, P, codec, L, rows, cols, steps=5, warmup=3, spec_kw=None, graph=True):
     """One rank of a P-rank job on this single GPU (exchange `sim_world=(P, 0)`): K1 on
     the rank's shard (patch: [rows/P, cols]; Ulysses: P chunks [rows/P, cols/P]), the
     collective replaced by device copies of the rank's bodies into the receive slots,
@@ -545,8 +549,11 @@ def sim_rank_measure(kind, P, codec, L, rows, cols, steps=5, warmup=3):
     from paper_2507_17511_b200 import compressors as cx
     from paper_2507_17511_b200.comm import PatchParallelExchange, UlyssesAllToAll, shard_bounds
 
+    from paper_2507_17511_b200 import linalg as la
+
     dev = torch.device("cuda", torch.cuda.current_device())
-    spec = cx.CompressorSpec(cx.CompressorKind(codec))
+    spec = cx.CompressorSpec(cx.CompressorKind(codec), **(spec_kw or {}))
+    lowrank = spec.kind == cx.CompressorKind.LOWRANK
     n = rows // P
     if kind == "patch":
         exs = [PatchParallelExchange(rows, cols, spec, sim_world=(P, 0)) for _ in range(L)]
@@ -561,33 +568,41 @@ def sim_rank_measure(kind, P, codec, L, rows, cols, steps=5, warmup=3):
 
     def one_step(s):
         for layer, e in enumerate(exs):
-            e.step(inputs[layer][s % 2])
+            # low-rank draws Q0 from the host PCG64 stream every step (cx:407), so it runs
+            # eagerly (host launch overhead included); the others replay CUDA graphs
+            e.step(inputs[layer][s % 2], rng=la.make_rng(1000 * layer + s) if lowrank else None)
 
     for s in range(warmup + 1):
         one_step(s)
     torch.cuda.synchronize()
     graphs = []
-    for par in (0, 1):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            one_step(par)
-            torch.cuda.current_stream().wait_stream(streams.decode)
-        graphs.append(g)
-    for e in exs:
-        if hasattr(e, "after_capture"):
-            e.after_capture()
-    for par in (0, 1):
-        graphs[par].replay()
+    if graph:
+        for par in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                one_step(par)
+                torch.cuda.current_stream().wait_stream(streams.decode)
+            graphs.append(g)
+        for e in exs:
+            if hasattr(e, "after_capture"):
+                e.after_capture()
+        for par in (0, 1):
+            graphs[par].replay()
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
     for s in range(steps):
-        graphs[s % 2].replay()
+        if graph:
+            graphs[s % 2].replay()
+        else:
+            one_step(warmup + 1 + s)
+    torch.cuda.current_stream().wait_stream(streams.decode)
     t1.record()
     torch.cuda.synchronize()
     ms_layer = t0.elapsed_time(t1) / steps / L
     out = {"ms_per_layer": round(ms_layer, 5), "gbs_per_gpu": round(2 * rows * cols / (ms_layer / 1e3) / 1e9, 1),
-           "codec": codec, "shard": [n, cols if kind == "patch" else cols // P]}
+           "codec": spec.label() if hasattr(spec, "label") else codec, "shard": [n, cols if kind == "patch" else cols // P],
+           "cuda_graph": graph}
     del exs, inputs, graphs
     torch.cuda.empty_cache()
     return out

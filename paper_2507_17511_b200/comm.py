@@ -289,10 +289,14 @@ class PatchParallelExchange:
         self.ev_encoded, self.ev_gathered, self.ev_decoded = (_Event(self.cuda) for _ in range(3))
 
     def wire_bytes(self, warm, wire16):
-        """Equal-size collective: every rank sends the largest shard's body."""
+        """Equal-size collective: every rank sends the largest shard's body, padded to
+        16 bytes so every receive slot (rank p at p * wire_bytes) stays aligned for the
+        vectorised decoders (top-k bodies are 6k bytes)."""
         if warm:
-            return max(b[1] - b[0] for b in self.bounds) * self.cols * (2 if wire16 else 4)
-        return max(body_bytes_for(self.codec, b[1] - b[0], self.cols) for b in self.bounds)
+            per = max(b[1] - b[0] for b in self.bounds) * self.cols * (2 if wire16 else 4)
+        else:
+            per = max(body_bytes_for(self.codec, b[1] - b[0], self.cols) for b in self.bounds)
+        return (per + 15) // 16 * 16
 
     # -- one step ---------------------------------------------------------------
     def step(self, x_shard, rng=None, skip_comm=False, k1_events=None):
