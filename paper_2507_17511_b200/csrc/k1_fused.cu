@@ -122,6 +122,7 @@ int fused_encode_segments(int codec, int mode, int scale_mode, int64_t n, int64_
   p.stop_after = g_fused_stop;
   p.tail_mult = g_fused_tail_mult > 0 ? g_fused_tail_mult : g_fused_tail_mult < 0 ? 0 : 2;
   p.tail_keep = g_fused_tail_keep > 0 ? g_fused_tail_keep : 2;
+  p.static_sched = (g_fused_policy & 16384) ? 1 : (g_fused_policy & 32768) ? 2 : 0;
   p.timer = g_fused_timer;
   p.policy = g_fused_policy;
   const int bits = codec == CC_SIGN1 ? 1 : (codec == CC_QUANT2 ? 2 : 4);

@@ -80,7 +80,8 @@ struct Params {
   int ctl_in_ws;              // control words live in the workspace (memset before launch)
   long long early_tiles;      // phase-A tiles loaded L2::evict_first (the rest evict_last)
   int tail_mult, tail_keep;   // phase-B end-game: < tail_mult * G tiles left -> <= tail_keep tiles ahead
-  unsigned long long *timer;  // profiling: [G][8] globaltimer stamps, or null
+  int static_sched;           // 0: static rounds then dynamic tail, 1: all static, 2: static prologue only
+  unsigned long long *timer;  // profiling: [G][16] globaltimer stamps, or null
   int policy;  // experiment bits: 1 = phase-B stores without L2 hint, 2 = phase-B loads evict_first,
                // 4 = phase-A loads evict_normal, 8 = phase-A consumers skip the math (timing only),
                // 16 = skip phase-A row finishing (timing only), 32 = control words in the workspace,
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   }
 
   auto stamp = [&](int i) {
-    if (p.timer && tid == 0) p.timer[(size_t)cta * 8 + i] = gtimer();
+    if (p.timer && tid == 0) p.timer[(size_t)cta * 16 + i] = gtimer();
   };
   stamp(0);
   if (tid == 0) {
@@ -440,8 +441,23 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     const long long early = p.early_tiles;
     int k = 0, s = 0;
     uint32_t ph = 0;  // phase parity of stage s's current use
+    // The first proA claims of every CTA are static (cta + k G): the ring fills
+    // without a chain of atomic round trips (what bounds small shards); the rest
+    // come from the counter, offset past the static ones.
+    // (all but the last ~2 rounds static; the tail is claimed dynamically, which keeps
+    // CTAs that share their SM with other kernels from holding up the grid)
+    const int proA = p.static_sched == 1   ? 0x7fffffff
+                     : p.static_sched == 2 ? (int)min64(SA, p.nTiles / G)
+                                           : (int)max64(min64(SA, p.nTiles / G), p.nTiles / G - 2);
+    int kcA = 0;
+    auto claimA = [&]() -> unsigned long long {  // lane 0
+      const unsigned long long v = kcA < proA ? (unsigned long long)(cta + (long long)kcA * G)
+                                              : (unsigned long long)proA * G + atomicAdd(p.ctr, 1ull);
+      ++kcA;
+      return v;
+    };
     unsigned long long nxt = 0;
-    if (lane == 0) nxt = atomicAdd(p.ctr, 1ull);
+    if (lane == 0) nxt = claimA();
     for (;;) {
       long long old = -1;
       if (k >= SA) {
@@ -451,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       long long tile = (long long)__shfl_sync(0xffffffffu, nxt, 0);
       if (tile >= p.nTiles) tile = -1;
       if (lane == 0) {
-        if (tile >= 0) nxt = atomicAdd(p.ctr, 1ull);
+        if (tile >= 0) nxt = claimA();
         tileA[s] = tile;
         if (tile < 0) {
           mbar_arrive(&fullA[s]);
@@ -485,6 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       mbar_wait(&emptyA[sq], pq);
       if (q > 0 && tileA[sq] >= 0) finish_rows(sq, tileA[sq], pq);
     }
+    if (p.timer && lane == 0) p.timer[(size_t)cta * 16 + 10] = gtimer();
    }
     // CTA |t| total per segment: lanes d*RA .. d*RA+RA-1 hold segment d's row sums
     {
@@ -510,8 +527,18 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     int k = 0, w = 0;
     bool u_ready = false, have_nxt = true, near_end = false;
     const long long tail = (long long)p.tail_mult * G;
+    const int proB = p.static_sched == 1   ? 0x7fffffff  // static first claims, as in phase A
+                     : p.static_sched == 2 ? (int)min64(SI, nTB / G)
+                                           : (int)max64(min64(SI, nTB / G), nTB / G - 2);
+    int kcB = 0;
+    auto claimB = [&]() -> unsigned long long {  // lane 0
+      const unsigned long long v = kcB < proB ? (unsigned long long)(cta + (long long)kcB * G)
+                                              : (unsigned long long)proB * G + atomicAdd(p.ctr + 16, 1ull);
+      ++kcB;
+      return v;
+    };
     unsigned long long nxt = 0;
-    if (lane == 0) nxt = atomicAdd(p.ctr + 16, 1ull);
+    if (lane == 0) nxt = claimB();
     auto load_u = [&](int st_, long long tile) {  // lane 0: 16B-aligned windows of u_d for the tile's rows
       const int64_t r0 = (int64_t)tile * RB;
       const int nrows = (int)min64(RB, n - r0);
@@ -534,14 +561,14 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       if (near_end) req = max(req, k - p.tail_keep);
       if (w < req && !u_ready) publish_u(min(k, SI));  // consumers need u before any release
       for (; w < req; ++w) mbar_wait(&emptyB[w % SI], (uint32_t)(w / SI) & 1u);
-      if (!have_nxt && lane == 0) nxt = atomicAdd(p.ctr + 16, 1ull);
+      if (!have_nxt && lane == 0) nxt = claimB();
       const long long t = (long long)__shfl_sync(0xffffffffu, nxt, 0);
       const long long tile = t < nTB ? nTB - 1 - t : -1;
       near_end = tail > 0 && t + tail >= nTB;
       have_nxt = tile >= 0 && !near_end;
       const int s = k % SI;
       if (lane == 0) {
-        if (have_nxt) nxt = atomicAdd(p.ctr + 16, 1ull);
+        if (have_nxt) nxt = claimB();
         tileB[s] = tile;
         if (tile < 0) {
           mbar_arrive(&fullB[s]);
@@ -649,8 +676,13 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
    {  // phase A
     int s = 0;
     uint32_t ph = 0;
+    bool first = true;
     for (;; s = (s + 1 == SA) ? 0 : s + 1, ph ^= (s == 0)) {
       mbar_wait(&fullA[s], ph);
+      if (first) {
+        stamp(8);
+        first = false;
+      }
       const long long tile = tileA[s];
       if (tile < 0) {
         __syncwarp();
@@ -698,6 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       if (lane == 0) mbar_arrive(&emptyA[s]);
     }
    }
+    stamp(9);
     if constexpr (Q == 1) {  // merge row groups' column partials in a fixed order
       double *xchg = reinterpret_cast<double *>(out_ring);  // in_ring is being refilled by the loader
       named_sync(1, kCons);

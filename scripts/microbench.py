@@ -121,7 +121,7 @@ def main():
     lib.cc_debug_fused_phase_a(0, 0)
     lib.cc_debug_fused_stop(0)
     # per-phase timeline of one fused launch (globaltimer stamps per CTA)
-    tbuf = torch.zeros(1024 * 8, dtype=torch.int64, device="cuda")
+    tbuf = torch.zeros(1024 * 16, dtype=torch.int64, device="cuda")
     for pol in (0, 8 | 64):  # 8|64: data movement only (both phases skip the math)
         lib.cc_debug_fused_policy(pol)
         lib.cc_debug_fused_timer(_lib.ptr(tbuf))
@@ -129,11 +129,11 @@ def main():
             enc(i)
         torch.cuda.synchronize()
         lib.cc_debug_fused_timer(None)
-        tb = tbuf.view(1024, 8).cpu()
+        tb = tbuf.view(1024, 16).cpu()
         g = int((tb[:, 0] > 0).sum())
         tb = tb[:g].double()
         t0 = tb[:, 0].min()
-        names = ["start", "A_done", "sync1", "F_done", "sync2", "B_done", "end", "F_cols"]
+        names = ["start", "A_done", "sync1", "F_done", "sync2", "B_done", "end", "F_cols", "A_first_data", "A_cons_done", "A_loader_drained"]
         out[f"fused_timeline_us{'_movement_only' if pol else ''}"] = {
             nm: [round(float((tb[:, i] - t0).min()) / 1e3, 2), round(float((tb[:, i] - t0).max()) / 1e3, 2)]
             for i, nm in enumerate(names)}
@@ -143,7 +143,14 @@ def main():
         enc(i)
     out["k1_fused_movement_only"] = {"us": round(timed(enc, a.reps), 2)}
     lib.cc_debug_fused_policy(0)
-    for mult, keep in ((-1, 1), (1, 1), (2, 1), (-1, 1), (2, 2), (4, 2), (2, 3), (-1, 1)):  # phase-B end-game
+    for pol, nm in ((16384, "static"), (0, "hybrid"), (32768, "dynamic"), (16384, "static"), (0, "hybrid"),
+                    (32768, "dynamic")):  # tile schedules (see Params::static_sched)
+        lib.cc_debug_fused_policy(pol)
+        for i in range(L):
+            enc(i)
+        out.setdefault(f"k1_fused_sched_{nm}", {"us": []})["us"].append(round(timed(enc, a.reps), 2))
+    lib.cc_debug_fused_policy(0)
+    for mult, keep in ((-1, 1), (2, 2)):  # phase-B end-game
         lib.cc_debug_fused_tail(mult, keep)
         for i in range(L):
             enc(i)
