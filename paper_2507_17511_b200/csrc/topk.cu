@@ -396,7 +396,9 @@ __global__ void __launch_bounds__(kThreads) k_write(const float *__restrict__ t,
                                                      float *__restrict__ decoded, int64_t total, int64_t k,
                                                      const State *st, const uint32_t *__restrict__ sel_pref,
                                                      const uint32_t *__restrict__ eq_pref, uint8_t *__restrict__ body,
-                                                     double *__restrict__ part, int stateful) {
+                                                     double *__restrict__ part, int stateful,
+                                                     const double *__restrict__ allpart, int nparts,
+                                                     unsigned int *__restrict__ ticket, double *__restrict__ record) {
   __shared__ float tv_s[kThreads * (kRun + 1)];
   __shared__ uint32_t sm[kThreads / 32];
   __shared__ double red[kThreads / 32];
@@ -482,38 +484,42 @@ __global__ void __launch_bounds__(kThreads) k_write(const float *__restrict__ t,
   adj = warp_sum(adj);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = adj;
   __syncthreads();
+  __shared__ unsigned last;
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int i = 0; i < kThreads / 32; ++i) s += red[i];
     part[2 * blockIdx.x] = s;
     part[2 * blockIdx.x + 1] = 0.0;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
-  (void)x;
-}
-
-// fixed-order tree reduction of the (adj, ||t||^2) partials (one CTA)
-__global__ void __launch_bounds__(1024) k_record(int nparts, const double *__restrict__ part,
-                                                 double *__restrict__ record) {
-  __shared__ double sa[1024], sb[1024];
-  double a = 0.0, b = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += 1024) {
-    a += part[2 * i];
-    b += part[2 * i + 1];
-  }
-  sa[threadIdx.x] = a;
-  sb[threadIdx.x] = b;
   __syncthreads();
-  for (int s2 = 512; s2 > 0; s2 >>= 1) {
-    if (threadIdx.x < s2) {
-      sa[threadIdx.x] += sa[threadIdx.x + s2];
-      sb[threadIdx.x] += sb[threadIdx.x + s2];
+  if (last) {  // the last CTA reduces every (adj, ||t||^2) partial in a fixed order (pl:115-120)
+    __threadfence();
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += kThreads) {
+      a += __ldcg(allpart + 2 * i);
+      b += __ldcg(allpart + 2 * i + 1);
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    __shared__ double ra[kThreads / 32], rb[kThreads / 32];
+    if ((threadIdx.x & 31) == 0) {
+      ra[threadIdx.x >> 5] = a;
+      rb[threadIdx.x >> 5] = b;
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+      double sa = 0.0, sb = 0.0;
+      for (int i = 0; i < kThreads / 32; ++i) {
+        sa += ra[i];
+        sb += rb[i];
+      }
+      record[0] = sb + sa;  // ||d - t||^2 = ||t||^2 + sum over kept of ((d - t)^2 - t^2)
+      record[1] = sb;
+    }
   }
-  if (threadIdx.x == 0) {
-    record[0] = sb[0] + sa[0];  // ||t||^2 + sum_sel((d-t)^2 - t^2) = ||d - t||^2
-    record[1] = sb[0];
-  }
+  (void)x;
 }
 
 // ---- receiver: sparse scatter (and -0.0 canonicalisation) ------------------------
@@ -609,10 +615,11 @@ static void select_and_write(const topk::Work &w, const float *t, const XT *x, f
   k_find<kBins3><<<1, 1024, 0, st>>>(w.hist3, w.st, 3, 0);
   k_count<<<(unsigned)w.nChunks, kThreads, 0, st>>>(t, total, w.st, w.cnt_gt, w.cnt_eq);
   k_scan<<<1, 1024, 0, st>>>(w.nChunks, w.st, w.cnt_gt, w.cnt_eq, w.sel_pref, w.eq_pref);
+  // k_write's last CTA also reduces the StepRecord partials (no separate launch)
   k_write<MODE, XT><<<(unsigned)w.nChunks, kThreads, 0, st>>>(t, x, base, aux, decoded, total, k, w.st, w.sel_pref,
-                                                             w.eq_pref, body, w.part + 2 * w.nH1, stateful);
-  k_record<<<1, 1024, 0, st>>>((int)(w.nH1 + w.nChunks), w.part, record);
-  count_launch(9);
+                                                             w.eq_pref, body, w.part + 2 * w.nH1, stateful, w.part,
+                                                             (int)(w.nH1 + w.nChunks), &w.st->pad[0], record);
+  count_launch(8);
 }
 
 int topk_encode(int64_t n, int64_t C, int64_t k, const float *t, uint8_t *body, float *decoded, void *ws,
