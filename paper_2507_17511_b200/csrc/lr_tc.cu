@@ -20,6 +20,9 @@
 #include "cc_common.cuh"
 #include "cc_internal.h"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
 namespace cc {
@@ -302,6 +305,165 @@ __global__ void __launch_bounds__(kThreads) k_tc_gemm(const float *__restrict__ 
   if (warp == 0) tmem_dealloc(tmem, kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged variant (the production kernel when K % 32 == 0 and A is 16-byte
+// aligned): a fifth warp streams each K chunk's raw f32 operands with 1-D bulk
+// copies (cp.async.bulk, one per A row segment + one for the S rows) into a
+// kRawStages-deep mbarrier ring; the four consumer warps split raw -> hi/lo into
+// the SW128 MMA stages and thread 0 issues the tcgen05.mma chain as above.  The
+// ring keeps ~kRawStages x 20 KB per SM in flight independent of the split work.
+// ---------------------------------------------------------------------------
+constexpr int kRawStages = 4;
+constexpr int kTThreads = kThreads + 32;  // + the TMA producer warp
+constexpr uint32_t kRawA = kM * kKC * 4;  // 16 KB
+constexpr uint32_t kRawS = 32 * kKC * 4;  // S rows of the chunk (NP <= 32)
+
+__device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int MODE, int NP>
+__global__ void __launch_bounds__(kTThreads) k_tc_gemm_tma(const __grid_constant__ CUtensorMap amap,
+                                                           const float *__restrict__ S, float *__restrict__ Dpart,
+                                                           int64_t n, int64_t C, int r, int64_t kper) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t Mdim = MODE == 0 ? n : C;
+  const int64_t Kdim = MODE == 0 ? C : n;
+  const int64_t m0 = (int64_t)blockIdx.x * kM;
+  const int split = blockIdx.y;
+  const int64_t klo = split * kper, khi = min64(Kdim, klo + kper);
+  constexpr uint32_t a_bytes = kM * kKC * 4;
+  constexpr uint32_t b_round = ((uint32_t)NP * kKC * 4 + 1023) & ~1023u;
+  auto stage = [&](int st_) {
+    uint8_t *b = smem + (uint32_t)st_ * (2 * a_bytes + 2 * b_round);
+    return Stage{b, b + a_bytes, b + 2 * a_bytes, b + 2 * a_bytes + b_round};
+  };
+  uint8_t *raw = smem + 2 * (2 * a_bytes + 2 * b_round);  // [kRawStages][kRawA + kRawS]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(raw + kRawStages * (kRawA + kRawS));
+  uint64_t *rfull = bar + 2, *rempty = rfull + kRawStages;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rempty + kRawStages);
+  const int64_t nchunks = (khi - klo + kKC - 1) / kKC;
+  const int64_t mc = min64(kM, Mdim - m0);  // valid rows of this M tile
+  if (warp == 0) tmem_alloc(tmem_slot, kTmemCols);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    for (int q = 0; q < kRawStages; ++q) {
+      mbar_init(&rfull[q], 1);
+      mbar_init(&rempty[q], kThreads / 32);
+    }
+    mbar_fence_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kThreads / 32) {  // ---- TMA producer warp ----
+    const uint64_t pol = l2_policy_evict_first();
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int q = (int)(c % kRawStages);
+      if (c >= kRawStages) mbar_wait(&rempty[q], (uint32_t)((c / kRawStages - 1) & 1));
+      const int64_t k0 = klo + c * kKC;
+      const int kc = (int)min64(kKC, khi - k0);
+      uint8_t *ra = raw + (size_t)q * (kRawA + kRawS);
+      // one 2-D TMA per chunk: the full box always lands (out-of-range rows zero-filled)
+      if (lane == 0) {
+        mbar_expect_tx(&rfull[q], kRawA + (uint32_t)(kc * r * 4));
+        if constexpr (MODE == 0) tma_load_2d(ra, &amap, (int)k0, (int)m0, &rfull[q]);  // box {32 cols, 128 rows}
+        else tma_load_2d(ra, &amap, (int)m0, (int)k0, &rfull[q]);                       // box {128 cols, 32 rows}
+        bulk_g2s(ra + kRawA, S + k0 * r, (uint32_t)(kc * r * 4), &rfull[q], pol);
+      }
+    }
+    return;
+  }
+  // ---- consumer warps 0-3 ----
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t idesc = idesc_tf32(kM, NP);
+  uint32_t ph = 0u;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int q = (int)(c % kRawStages);
+    mbar_wait(&rfull[q], (uint32_t)((c / kRawStages) & 1));
+    const int64_t k0 = klo + c * kKC;
+    const int kc = (int)min64(kKC, khi - k0);
+    const float *ra = reinterpret_cast<const float *>(raw + (size_t)q * (kRawA + kRawS));
+    const float *rs = reinterpret_cast<const float *>(raw + (size_t)q * (kRawA + kRawS) + kRawA);
+    Raw<MODE, NP> rw;
+#pragma unroll
+    for (int i = 0; i < kAItems; ++i) {  // raw tile -> registers (masked at the tile edges)
+      int m, k;
+      a_item<MODE>(tid, i, m, k);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if constexpr (MODE == 0) {
+        if (m < mc && k < kc) v = *reinterpret_cast<const float4 *>(ra + m * kKC + k);  // kc % 4 == 0
+      } else {
+        if (k < kc && m < mc) {  // mc % 4 == 0
+          v = *reinterpret_cast<const float4 *>(ra + k * kM + m);
+        }
+      }
+      rw.a[i] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < NP * kKC / kThreads; ++i) {
+      const int e = tid + i * kThreads;
+      const int j = e / kKC, kk = e % kKC;
+      rw.s[i] = (j < r && kk < kc) ? rs[kk * r + j] : 0.0f;
+    }
+    const int st_ = (int)(c & 1);
+    if (c >= 2) {  // the MMAs that read this MMA stage two chunks ago must be done
+      mbar_wait(&bar[st_], (ph >> st_) & 1u);
+      ph ^= 1u << st_;
+    }
+    const Stage sg = stage(st_);
+    store_split<MODE, NP>(rw, sg);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&rempty[q]);  // raw chunk consumed: the producer may refill the stage
+    cons_sync();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint64_t ah = umma_desc_sw128(smem_u32(sg.a_hi)), al = umma_desc_sw128(smem_u32(sg.a_lo));
+      const uint64_t bh = umma_desc_sw128(smem_u32(sg.b_hi)), bl = umma_desc_sw128(smem_u32(sg.b_lo));
+#pragma unroll
+      for (int ks = 0; ks < kKC / 8; ++ks) {
+        const uint64_t dk = (uint64_t)((ks * 32) >> 4);
+        const uint32_t acc0 = (c > 0 || ks > 0) ? 1u : 0u;
+        mma_tf32(tmem, ah + dk, bh + dk, idesc, acc0);
+        mma_tf32(tmem, ah + dk, bl + dk, idesc, 1u);
+        mma_tf32(tmem, al + dk, bh + dk, idesc, 1u);
+      }
+      mma_commit(&bar[st_]);
+    }
+    __syncwarp();
+  }
+  for (int64_t c = std::max<int64_t>(0, nchunks - 2); c < nchunks; ++c) {
+    const int st_ = (int)(c & 1);
+    mbar_wait(&bar[st_], (ph >> st_) & 1u);
+    ph ^= 1u << st_;
+  }
+  tc_fence_after();
+  const int64_t m = m0 + warp * 32 + lane;
+  float *out = Dpart + (int64_t)split * Mdim * r;
+#pragma unroll
+  for (int cb = 0; cb < NP; cb += 16) {
+    float v[16];
+    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)cb, v);
+    if (m < Mdim) {
+#pragma unroll
+      for (int q2 = 0; q2 < 16; ++q2)
+        if (cb + q2 < r) out[m * r + cb + q2] = nchunks > 0 ? v[q2] : 0.0f;
+    }
+  }
+  tc_fence_before();
+  cons_sync();
+  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+}
+
 // fixed-order split reduction -> f32 result
 __global__ void k_tc_reduce(const float *__restrict__ Dpart, float *__restrict__ D, int64_t cnt, int splits) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -338,6 +500,59 @@ int64_t tc_partial_floats(int64_t n, int64_t C, int r) {
   return std::max(s0 * n, s1 * C) * r;
 }
 
+static size_t tc_tma_smem_bytes(int NP) {
+  return tc_smem_bytes(NP) + (size_t)tc::kRawStages * (tc::kRawA + tc::kRawS) + 8 * 2 * tc::kRawStages + 64;
+}
+
+// 2-D tensor map over A [n, C] f32 (row-major); box {32, 128} (mode 0: K-chunk x M-tile)
+// or {128, 32} (mode 1), no swizzle: the raw staging layout the consumer warps read.
+// The driver entry point is fetched through the runtime (no libcuda link).
+static bool make_amap(CUtensorMap *map, const float *A, int64_t n, int64_t C, int mode) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void **>(&encode), cudaEnableDefault,
+                                &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !encode) {
+      cudaGetLastError();
+      encode = nullptr;
+      return false;
+    }
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)C * 4};
+  const cuuint32_t box[2] = {mode == 0 ? (cuuint32_t)tc::kKC : (cuuint32_t)tc::kM,
+                             mode == 0 ? (cuuint32_t)tc::kM : (cuuint32_t)tc::kKC};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(A), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int MODE, int NP>
+static bool tc_launch_tma(dim3 grid, cudaStream_t st, const float *A, const float *S, float *Dpart, int64_t n,
+                          int64_t C, int r, int64_t kper) {
+  CUtensorMap map;
+  if (!make_amap(&map, A, n, C, MODE)) return false;
+  const size_t smem = tc_tma_smem_bytes(NP);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc::k_tc_gemm_tma<MODE, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  tc::k_tc_gemm_tma<MODE, NP><<<grid, tc::kTThreads, smem, st>>>(map, S, Dpart, n, C, r, kper);
+  return true;
+}
+
+// 0 (default): register-staged operands — measured faster (2-3 CTAs per SM at ~75 KB smem);
+// 1: TMA-staged raw tiles (2-D tensor map + 4-deep ring, ~155 KB smem, 1 CTA per SM):
+// identical results (same split-K plan), 1.2-1.3x slower at [1024 | 4096, 3072] r = 8.
+static int g_tc_tma = 0;
+void set_tc_tma(int v, int waves) {
+  (void)waves;
+  g_tc_tma = v;
+}
+
 template <int MODE, int NP>
 static void tc_launch(dim3 grid, size_t smem, cudaStream_t st, const float *A, const float *S, float *Dpart,
                       int64_t n, int64_t C, int r, int64_t kper, int vec) {
@@ -354,8 +569,24 @@ int tc_project(int mode, const float *A, const float *S, float *D, float *Dpart,
   tc_plan(M, K, &nsplit, &kper);
   const size_t smem = tc_smem_bytes(NP);
   const int vec = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && C % 4 == 0;
+  // TMA path: K chunks of exactly 32 (1-D bulk copies need 16-byte sizes), aligned rows
+  const bool tma = g_tc_tma && vec && n % tc::kKC == 0 && C % tc::kKC == 0 &&
+                   (reinterpret_cast<uintptr_t>(S) & 15) == 0;
+  // (the TMA path uses the same split-K plan as the register-staged one, so both give
+  // the same f32 partial sums; with one CTA resident per SM it runs in several waves)
   dim3 grid((unsigned)cdiv(M, tc::kM), (unsigned)nsplit);
-  if (mode == 0) {
+  bool done = false;
+  if (tma) {
+    if (mode == 0) {
+      done = NP == 16 ? tc_launch_tma<0, 16>(grid, st, A, S, Dpart, n, C, r, kper)
+                      : tc_launch_tma<0, 32>(grid, st, A, S, Dpart, n, C, r, kper);
+    } else {
+      done = NP == 16 ? tc_launch_tma<1, 16>(grid, st, A, S, Dpart, n, C, r, kper)
+                      : tc_launch_tma<1, 32>(grid, st, A, S, Dpart, n, C, r, kper);
+    }
+  }
+  if (done) {
+  } else if (mode == 0) {
     if (NP == 16) tc_launch<0, 16>(grid, smem, st, A, S, Dpart, n, C, r, kper, vec);
     else tc_launch<0, 32>(grid, smem, st, A, S, Dpart, n, C, r, kper, vec);
   } else {

@@ -186,3 +186,24 @@ def test_tcgen05_backend_matches_f64_backend(shape, r):
     finally:
         lib.cc_set_lowrank_backend(1)
     assert abs(errs[0] - errs[1]) <= 1e-5 * max(1.0, errs[0]), errs
+
+
+@pytest.mark.parametrize("shape", [(1024, 3072), (4096, 3072), (64, 384)], ids=lambda s: f"{s[0]}x{s[1]}")
+@pytest.mark.parametrize("r", [4, 16, 32])
+def test_tma_staged_projections_equal_register_staged(shape, r):
+    """The TMA-staged tcgen05 projection kernel (2-D tensor map, 4-deep raw ring) and
+    the register-staged one use the same split-K plan: identical payload bytes."""
+    from paper_2507_17511_b200 import _lib
+
+    cx, _, linalg = _mods()
+    n, c = shape
+    x = torch.from_numpy(synth.flux_like(n, c, 1, seed=n + 7 * r)[0]).cuda()
+    lib = _lib.load()
+    bodies = []
+    try:
+        for tma in (0, 1, 1):
+            lib.cc_debug_lowrank_tma(tma, 0)
+            bodies.append(cx.encode_lowrank(x, _spec(r), linalg.make_rng(r)).body.cpu())
+    finally:
+        lib.cc_debug_lowrank_tma(0, 0)
+    assert torch.equal(bodies[0], bodies[1]) and torch.equal(bodies[1], bodies[2])
