@@ -1028,8 +1028,12 @@ inline int launch_fused(fused::Params &p, cudaStream_t st) {
   p.ring_bytes = (uint32_t)align_up(std::max(ringA, ringB), 128);
   const size_t smem = p.ring_bytes + rp_bytes + 512 * 8 + (size_t)(3 * SA + 3 * SI + 3 * SO + 2) * 8 + 16 +
                       (size_t)SI * p.nseg * 64 + 128;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return cuda_status("k1_fused attr");
+  static int smem_set = 0;  // per instantiation: raise the opt-in limit only when a launch needs more
+  if ((int)smem > smem_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return cuda_status("k1_fused attr");
+    smem_set = (int)smem;
+  }
   void *args[] = {&p};
   if (p.ctl_in_ws) cudaMemsetAsync(p.ctr, 0, 512, st);  // control words
   cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(p.G), dim3(kThreads), args, smem, st);

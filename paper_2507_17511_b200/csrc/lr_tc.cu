@@ -556,7 +556,11 @@ void set_tc_tma(int v, int waves) {
 template <int MODE, int NP>
 static void tc_launch(dim3 grid, size_t smem, cudaStream_t st, const float *A, const float *S, float *Dpart,
                       int64_t n, int64_t C, int r, int64_t kper, int vec) {
-  cudaFuncSetAttribute(tc::k_tc_gemm<MODE, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int smem_set = 0;
+  if ((int)smem > smem_set) {
+    cudaFuncSetAttribute(tc::k_tc_gemm<MODE, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_set = (int)smem;
+  }
   tc::k_tc_gemm<MODE, NP><<<grid, tc::kThreads, smem, st>>>(A, S, Dpart, n, C, r, kper, vec);
 }
 
