@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--no-sim", action="store_true", help="skip the single-GPU per-rank simulations of "
                     "the 2/4/8-GPU patch-parallel and 8-GPU Ulysses configs (`per_rank_sim`)")
     ap.add_argument("--no-overlap", action="store_true")
+    ap.add_argument("--pdl", type=int, default=None, help="programmatic dependent launch for K1/K2 "
+                    "(1 on, 0 off; default: the library default)")
     ap.add_argument("--overlap", action="store_true", help="run K2 on its own stream even at N=1 (the "
                     "loopback receiver has no communication to hide; two HBM-bound kernels gain nothing)")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from Python instead of "
@@ -277,6 +279,8 @@ def run_b200(a, world, rank):
     from paper_2507_17511_b200.comm import PatchParallelExchange, RingExchange, shard_bounds
 
     lib = _lib.load()
+    if a.pdl is not None:
+        lib.cc_set_pdl(int(a.pdl))
     dev = torch.device("cuda", torch.cuda.current_device())
     spec = cx.CompressorSpec(cx.CompressorKind(a.codec))
     L, rows, cols = a.layers, a.rows, a.cols

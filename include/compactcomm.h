@@ -218,6 +218,12 @@ CC_API void cc_debug_fused_policy(int policy);
  * tiles remain, a CTA keeps at most `keep` loaded tiles ahead of its consumers
  * (0, 0 = automatic) */
 CC_API void cc_debug_fused_tail(int mult, int keep);
+/* programmatic dependent launch for the encode (K1) / decode (K2) kernels: each
+ * launches with programmatic stream serialization and waits for its predecessor's
+ * completion (griddepcontrol.wait) before touching memory, so launch and prologue
+ * overlap the previous kernel's tail.  Results are unchanged.  0 = off (default: measured
+ * 2% slower in bench.py's graph replay at [4096, 3072]). */
+CC_API void cc_set_pdl(int enable);
 /* profiling only: phase-B ring depths of the persistent K1 (0 = automatic) */
 CC_API void cc_debug_fused_rings(int s_in, int s_out);
 /* profiling only: phase-A tile height (rows per row group) and ring depth of the

@@ -62,6 +62,7 @@ SIGNATURES = {
     "cc_debug_fused_rings": (None, [_i32, _i32]),
     "cc_debug_fused_tail": (None, [_i32, _i32]),
     "cc_debug_lowrank_tma": (None, [_i32, _i32]),
+    "cc_set_pdl": (None, [_i32]),
     "cc_debug_fused_phase_a": (None, [_i32, _i32]),
     "cc_set_lowrank_backend": (None, [_i32]),
 }

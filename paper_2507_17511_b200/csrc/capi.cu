@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -48,6 +49,12 @@ int sm_count() {
 // launches on one stream are ordered, launches on different streams use
 // different slots.  Returns null (caller falls back to a memset'd workspace
 // word) if the pool cannot be created now, e.g. during a stream capture.
+static int g_pdl = [] {  // default off; CC_PDL=1 in the environment turns it on (tests / benchmarks)
+  const char *e = std::getenv("CC_PDL");
+  return e && e[0] == '1' ? 1 : 0;
+}();
+int pdl_enabled() { return g_pdl; }
+
 uint8_t *stream_control_block(cudaStream_t st) {
   constexpr int kSlots = 1024, kSlotBytes = 512;
   struct Pool {
@@ -147,6 +154,7 @@ CC_API void cc_debug_fused_timer(void *dev_buf) { set_fused_timer(dev_buf); }
 CC_API void cc_debug_fused_policy(int policy) { set_fused_policy(policy); }
 CC_API void cc_debug_fused_rings(int s_in, int s_out) { set_fused_rings(s_in, s_out); }
 CC_API void cc_debug_fused_tail(int mult, int keep) { set_fused_tail(mult, keep); }
+CC_API void cc_set_pdl(int enable) { g_pdl = enable ? 1 : 0; }
 CC_API void cc_debug_fused_phase_a(int rows_per_group, int stages) { set_fused_phase_a(rows_per_group, stages); }
 CC_API void cc_set_lowrank_backend(int backend) { set_lowrank_backend(backend); }
 CC_API void cc_debug_lowrank_tma(int enable, int waves) { set_tc_tma(enable, waves); }

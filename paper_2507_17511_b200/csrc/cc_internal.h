@@ -23,6 +23,11 @@ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // number of SMs of the current device (cached)
 int sm_count();
 
+// programmatic dependent launch (PDL) for the K1 / K2 chain: kernels launch with
+// programmatic stream serialization, trigger their dependents at entry and wait
+// (griddepcontrol.wait) before touching memory, so a kernel's launch and prologue
+// overlap its predecessor's tail.  1 = on.
+int pdl_enabled();
 // zero-initialised 512-byte control slot of `st` on the current device (see capi.cu);
 // persistent kernels must leave it zeroed on exit.  Null when unavailable.
 uint8_t *stream_control_block(cudaStream_t st);

@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();  // PDL launches only: our inputs may come from the previous kernel
   const XT *X = reinterpret_cast<const XT *>(p.x);
 
   // ================= phase A: |t| partial sums over tiles of RA rows =================
@@ -919,6 +920,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   // ---- StepRecord: consumer warps only (the store warp drains its last stages
   // meanwhile; the loader made its last claim before publishing the sentinel) ----
   if (!consumer) return;
+  pdl_launch_dependents();  // phase B done: the next kernel may launch during the record tail
   stamp(5);
   {
     __shared__ unsigned last;
@@ -1036,7 +1038,24 @@ inline int launch_fused(fused::Params &p, cudaStream_t st) {
   }
   void *args[] = {&p};
   if (p.ctl_in_ws) cudaMemsetAsync(p.ctr, 0, 512, st);  // control words
-  cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(p.G), dim3(kThreads), args, smem, st);
+  cudaError_t e;
+  if (pdl_enabled()) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.G);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    e = cudaLaunchKernelExC(&cfg, (const void *)kern, args);
+  } else {
+    e = cudaLaunchCooperativeKernel((const void *)kern, dim3(p.G), dim3(kThreads), args, smem, st);
+  }
   if (e != cudaSuccess) {
     set_error(std::string("k1_fused launch: ") + cudaGetErrorString(e));
     cudaGetLastError();

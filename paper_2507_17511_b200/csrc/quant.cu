@@ -516,6 +516,7 @@ template <int CODEC, bool ACC>
 __global__ void __launch_bounds__(256) k_decode_vec(const __grid_constant__ PeerBatch pb, int64_t C, int RB) {
   constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
   constexpr int U = kDecRows;  // rows in flight per thread
+  pdl_wait();  // PDL launches only: the bodies come from the previous kernel (K1 / the collective)
   const int peer = blockIdx.z;
   const int64_t n = pb.rows[peer];
   const int64_t r0 = (int64_t)blockIdx.y * RB;
@@ -743,7 +744,20 @@ static void launch_decode(const PeerBatch &pb, int count, int64_t maxrows, int64
     QPlan p;
     plan_shape(p, maxrows, C, true);
     dim3 grid(p.nStrips, (unsigned)cdiv(maxrows, kDecRows), count);
-    k_decode_vec<CODEC, ACC><<<grid, p.threads, 0, st>>>(pb, C, kDecRows);
+    if (pdl_enabled()) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(p.threads);
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, k_decode_vec<CODEC, ACC>, pb, C, (int)kDecRows);
+    } else {
+      k_decode_vec<CODEC, ACC><<<grid, p.threads, 0, st>>>(pb, C, kDecRows);
+    }
   } else {
     dim3 grid((unsigned)cdiv(maxrows * C, 256), count);
     k_decode_scalar<CODEC, ACC><<<grid, 256, 0, st>>>(pb, C);
