@@ -438,31 +438,36 @@ __global__ void __launch_bounds__(kThreads) k_write(const float *__restrict__ t,
   const int64_t e_run = c0 + (int64_t)threadIdx.x * kRun;
   const int64_t rem = c1 - e_run;
   const int valid = rem <= 0 ? 0 : (int)min64(kRun, rem);
-  uint32_t n_eq = 0, n_gt = 0;
+  uint32_t m_gt = 0, m_eq = 0;  // bit i of the run: key > T / key == T
   for (int i = 0; i < valid; ++i) {
     const uint32_t key = key_of(run[i]);
-    n_eq += key == T;
-    n_gt += key > T;
+    m_gt |= (uint32_t)(key > T) << i;
+    m_eq |= (uint32_t)(key == T) << i;
   }
+  const uint32_t n_eq = __popc(m_eq), n_gt = __popc(m_gt);
   uint32_t eq_ex;
   block_excl_scan(n_eq, eq_ex, sm);
-  uint32_t tie_rank = eq_pref[blockIdx.x] + eq_ex;  // ties before this run
+  const uint32_t tie_rank = eq_pref[blockIdx.x] + eq_ex;  // ties before this run
   const uint32_t ties_here = tie_rank < ties ? min(n_eq, ties - tie_rank) : 0u;
   uint32_t sel_ex;
   block_excl_scan(n_gt + ties_here, sel_ex, sm);
   uint32_t pos = sel_pref[blockIdx.x] + sel_ex;
   uint32_t *idx_out = reinterpret_cast<uint32_t *>(body);
   __half *val_out = reinterpret_cast<__half *>(body + 4 * k);
+  // the run's selected elements: every key > T plus its first `ties_here` keys == T
+  // (ties go to the lowest index); visited in index order through the bit mask, so a
+  // thread loops over its selections only, not over all 32 elements
+  uint32_t msel = m_gt;
+  for (uint32_t take = ties_here, mm = m_eq; take; --take) {
+    const uint32_t b = mm & (0u - mm);
+    msel |= b;
+    mm ^= b;
+  }
   double adj = 0.0;  // sum over selected of (d - t)^2 - t^2
-  for (int i = 0; i < valid; ++i) {
+  while (msel) {
+    const int i = __ffs(msel) - 1;
+    msel &= msel - 1;
     const float tv = run[i];
-    const uint32_t key = key_of(tv);
-    bool sel = key > T;
-    if (key == T) {
-      sel = tie_rank < ties;
-      ++tie_rank;
-    }
-    if (!sel) continue;
     const int64_t e = e_run + i;
     idx_out[pos] = (uint32_t)e;
     const __half h = __float2half_rn(tv);
