@@ -404,3 +404,33 @@ def test_fused_k1_narrow_widths(shape, codec, mode, quant_path):
     och = O.Channel(mode, 1, np.zeros((n, c), np.float32))
     for x, b in zip(xs, res[1][0]):
         assert O.send(och, x.float().cpu().numpy(), O.Codec(_otag(codec)))[1] == b
+
+
+def test_pdl_launches_give_identical_results():
+    """Programmatic dependent launch (cc_set_pdl) only changes launch scheduling:
+    a K1 + K2 trajectory must be bit-identical with it on and off."""
+    from paper_2507_17511_b200 import _lib
+
+    cx, pl = _mods()
+    lib = _lib.load()
+    n, c = 96, 3072
+    xs = synth.flux_like(n, c, 4, seed=23)
+    outs = []
+    try:
+        for pdl in (0, 1):
+            lib.cc_set_pdl(pdl)
+            snd = pl.LayerState("residual_with_feedback", 1, torch.zeros(n, c, device="cuda"))
+            rcv = pl.LayerState("residual_with_feedback", 1, torch.zeros(n, c, device="cuda"))
+            bodies = []
+            for t, x in enumerate(xs, start=1):
+                payload, _ = pl.encode_step(snd, torch.from_numpy(x).cuda().to(torch.bfloat16), _spec("quant2bit"))
+                pl.decode_step(rcv, pl.device_message(t, 1, payload))
+                bodies.append(payload.body.clone())
+            torch.cuda.synchronize()
+            outs.append((bodies, snd.base.clone(), snd.feedback.clone(), rcv.base.clone()))
+    finally:
+        lib.cc_set_pdl(0)
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert torch.equal(a, b)
+    for i in (1, 2, 3):
+        assert torch.equal(outs[0][i], outs[1][i])
