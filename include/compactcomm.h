@@ -232,8 +232,9 @@ CC_API void cc_debug_fused_phase_a(int rows_per_group, int stages);
 /* low-rank projections: 1 = tcgen05 tensor cores, 3xTF32 split (default),
  * 0 = f64-accumulating CUDA-core GEMMs (cross-check) */
 CC_API void cc_set_lowrank_backend(int backend);
-/* low-rank tcgen05 projections: register-staged operands (0, default, measured faster) or
- * TMA-staged raw tiles through a 2-D tensor map (1); identical results.  waves: unused */
+/* low-rank tcgen05 projections: operand staging — 2 (default) A Q TMA-staged (2-D tensor map)
+ * and A^T Y register-staged, 1 both TMA-staged, 0 both register-staged; identical results.
+ * waves: unused */
 CC_API void cc_debug_lowrank_tma(int enable, int waves);
 
 #ifdef __cplusplus

@@ -313,7 +313,8 @@ __global__ void __launch_bounds__(kThreads) k_tc_gemm(const float *__restrict__ 
 // the SW128 MMA stages and thread 0 issues the tcgen05.mma chain as above.  The
 // ring keeps ~kRawStages x 20 KB per SM in flight independent of the split work.
 // ---------------------------------------------------------------------------
-constexpr int kRawStages = 4;
+constexpr int kRawStages = 3;
+constexpr int kMmaStages = 1;  // one hi/lo MMA stage: ~100 KB of smem, two CTAs per SM overlap each other
 constexpr int kTThreads = kThreads + 32;  // + the TMA producer warp
 constexpr uint32_t kRawA = kM * kKC * 4;  // 16 KB
 constexpr uint32_t kRawS = 32 * kKC * 4;  // S rows of the chunk (NP <= 32)
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(kTThreads) k_tc_gemm_tma(const __grid_constant
     uint8_t *b = smem + (uint32_t)st_ * (2 * a_bytes + 2 * b_round);
     return Stage{b, b + a_bytes, b + 2 * a_bytes, b + 2 * a_bytes + b_round};
   };
-  uint8_t *raw = smem + 2 * (2 * a_bytes + 2 * b_round);  // [kRawStages][kRawA + kRawS]
+  uint8_t *raw = smem + kMmaStages * (2 * a_bytes + 2 * b_round);  // [kRawStages][kRawA + kRawS]
   uint64_t *bar = reinterpret_cast<uint64_t *>(raw + kRawStages * (kRawA + kRawS));
   uint64_t *rfull = bar + 2, *rempty = rfull + kRawStages;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rempty + kRawStages);
@@ -415,8 +416,8 @@ __global__ void __launch_bounds__(kTThreads) k_tc_gemm_tma(const __grid_constant
       const int j = e / kKC, kk = e % kKC;
       rw.s[i] = (j < r && kk < kc) ? rs[kk * r + j] : 0.0f;
     }
-    const int st_ = (int)(c & 1);
-    if (c >= 2) {  // the MMAs that read this MMA stage two chunks ago must be done
+    const int st_ = (int)(c % kMmaStages);
+    if (c >= kMmaStages) {  // the MMAs that read this MMA stage kMmaStages chunks ago must be done
       mbar_wait(&bar[st_], (ph >> st_) & 1u);
       ph ^= 1u << st_;
     }
@@ -441,8 +442,8 @@ __global__ void __launch_bounds__(kTThreads) k_tc_gemm_tma(const __grid_constant
     }
     __syncwarp();
   }
-  for (int64_t c = std::max<int64_t>(0, nchunks - 2); c < nchunks; ++c) {
-    const int st_ = (int)(c & 1);
+  for (int64_t c = std::max<int64_t>(0, nchunks - kMmaStages); c < nchunks; ++c) {
+    const int st_ = (int)(c % kMmaStages);
     mbar_wait(&bar[st_], (ph >> st_) & 1u);
     ph ^= 1u << st_;
   }
@@ -501,7 +502,10 @@ int64_t tc_partial_floats(int64_t n, int64_t C, int r) {
 }
 
 static size_t tc_tma_smem_bytes(int NP) {
-  return tc_smem_bytes(NP) + (size_t)tc::kRawStages * (tc::kRawA + tc::kRawS) + 8 * 2 * tc::kRawStages + 64;
+  const size_t a = tc::kM * tc::kKC * 4;
+  const size_t b = ((size_t)NP * tc::kKC * 4 + 1023) & ~size_t(1023);
+  return 1024 + tc::kMmaStages * (2 * a + 2 * b) + (size_t)tc::kRawStages * (tc::kRawA + tc::kRawS) +
+         8 * (2 + 2 * tc::kRawStages) + 64;
 }
 
 // 2-D tensor map over A [n, C] f32 (row-major); box {32, 128} (mode 0: K-chunk x M-tile)
@@ -544,10 +548,12 @@ static bool tc_launch_tma(dim3 grid, cudaStream_t st, const float *A, const floa
   return true;
 }
 
-// 0 (default): register-staged operands — measured faster (2-3 CTAs per SM at ~75 KB smem);
-// 1: TMA-staged raw tiles (2-D tensor map + 4-deep ring, ~155 KB smem, 1 CTA per SM):
-// identical results (same split-K plan), 1.2-1.3x slower at [1024 | 4096, 3072] r = 8.
-static int g_tc_tma = 0;
+// 2 (default): A Q with TMA-staged raw tiles (2-D tensor map, 3-deep raw ring, one hi/lo MMA
+//    stage, ~100 KB smem -> 2 CTAs per SM), A^T Y register-staged — measured 10% faster than
+//    all register-staged at [1024 | 4096, 3072] r = 8 (A Q: 14.0 -> 11.3 us, 30.7 -> 24.7 us);
+// 1: both TMA-staged (A^T Y 1.35x slower: its transposing split dominates); 0: both register-
+//    staged.  All variants give identical results (same split-K plan).
+static int g_tc_tma = 2;
 void set_tc_tma(int v, int waves) {
   (void)waves;
   g_tc_tma = v;
@@ -574,8 +580,10 @@ int tc_project(int mode, const float *A, const float *S, float *D, float *Dpart,
   const size_t smem = tc_smem_bytes(NP);
   const int vec = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && C % 4 == 0;
   // TMA path: K chunks of exactly 32 (1-D bulk copies need 16-byte sizes), aligned rows
-  const bool tma = g_tc_tma && vec && n % tc::kKC == 0 && C % tc::kKC == 0 &&
-                   (reinterpret_cast<uintptr_t>(S) & 15) == 0;
+  // TMA staging wins for A Q (row tiles, K-major already); A^T Y keeps the register path
+  // (its transposing split dominates and the deeper TMA ring costs occupancy)
+  const bool tma = (g_tc_tma == 1 || (g_tc_tma == 2 && mode == 0)) && vec && n % tc::kKC == 0 &&
+                   C % tc::kKC == 0 && (reinterpret_cast<uintptr_t>(S) & 15) == 0;
   // (the TMA path uses the same split-K plan as the register-staged one, so both give
   // the same f32 partial sums; with one CTA resident per SM it runs in several waves)
   dim3 grid((unsigned)cdiv(M, tc::kM), (unsigned)nsplit);

@@ -201,9 +201,9 @@ def test_tma_staged_projections_equal_register_staged(shape, r):
     lib = _lib.load()
     bodies = []
     try:
-        for tma in (0, 1, 1):
+        for tma in (0, 1, 1, 2):
             lib.cc_debug_lowrank_tma(tma, 0)
             bodies.append(cx.encode_lowrank(x, _spec(r), linalg.make_rng(r)).body.cpu())
     finally:
-        lib.cc_debug_lowrank_tma(0, 0)
-    assert torch.equal(bodies[0], bodies[1]) and torch.equal(bodies[1], bodies[2])
+        lib.cc_debug_lowrank_tma(2, 0)
+    assert all(torch.equal(bodies[0], b) for b in bodies[1:])
