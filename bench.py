@@ -289,10 +289,15 @@ def run_b200(a, world, rank):
     n_own = hi - lo
     Ex = RingExchange if a.topology == "ring" else PatchParallelExchange
     overlap = (world > 1 or a.overlap) and not a.no_overlap
-    exs = [Ex(rows, cols, spec, overlap=overlap) for _ in range(L)]
-    streams = exs[0].streams
-    for e in exs[1:]:
-        e.streams = streams  # one compute / comm / decode stream triple for the whole model
+    exs = []
+
+    def make_exchanges():
+        exs[:] = [Ex(rows, cols, spec, overlap=overlap) for _ in range(L)]
+        for e in exs[1:]:
+            e.streams = exs[0].streams  # one compute / comm / decode stream triple for the whole model
+        return exs[0].streams
+
+    streams = make_exchanges()
     inputs = [flux_inputs(rows, cols, lo, hi, layer, dev) for layer in range(L)]
 
     # instrumentation: K1 / K2 events per (step, layer)
@@ -326,18 +331,31 @@ def run_b200(a, world, rank):
     graphs = None
     if not a.no_graph:
         # steady state reached: capture one step per input parity and replay it
-        graphs = []
-        for par in (0, 1):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                one_step(par)
-                torch.cuda.current_stream().wait_stream(streams.decode)
-            graphs.append(g)
-        for e in exs:
-            e.after_capture()
-        for par in (0, 1):
-            graphs[par].replay()
-        barrier(world)
+        try:
+            graphs = []
+            for par in (0, 1):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    one_step(par)
+                    if os.environ.get("CC_BENCH_FAIL_CAPTURE"):  # exercises the eager fallback
+                        raise RuntimeError("forced capture failure")
+                    torch.cuda.current_stream().wait_stream(streams.decode)
+                graphs.append(g)
+            for e in exs:
+                e.after_capture()
+            for par in (0, 1):
+                graphs[par].replay()
+            barrier(world)
+        except Exception as exc:  # e.g. a collective that cannot be captured: measure eagerly
+            print(f"bench: CUDA-graph capture failed ({type(exc).__name__}: {exc}); timing eager launches",
+                  file=sys.stderr, flush=True)
+            graphs = None
+            torch.cuda.synchronize()
+            streams = make_exchanges()  # host step counters advanced inside the failed capture
+            one_step(0)
+            for s in range(a.warmup):
+                one_step(s + 1)
+            barrier(world)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n0 = lib.cc_launch_count()
     with ClockSampler(torch.cuda.current_device()) as clk:
@@ -424,7 +442,7 @@ def run_b200(a, world, rank):
                                                                   "BASELINE config 1)" if world == 1 else "")),
                    "codec": a.codec, "layers": L, "rows": rows, "cols": cols, "shard_rows": n_own,
                    "parallelism": f"patch{world}", "topology": a.topology, "l2": "per-step working set >> 126 MB L2 (no flush needed)",
-                   "overlap": overlap, "cuda_graph": not a.no_graph},
+                   "overlap": overlap, "cuda_graph": graphs is not None},
         "per_gpu_gbs": value / world,
         "exposed_comm_us_per_layer": exposed_us,
         "bf16_allgather_us_per_layer": bf16_ag_us,
