@@ -377,6 +377,7 @@ def run_b200(a, world, rank):
         launches = (lib.cc_launch_count() - n1) * K
     ms = start.elapsed_time(end) / K
     ms = max_over_ranks(ms, world)
+    used_graph = graphs is not None
     act_bytes = L * 2 * rows * cols
     value = world * act_bytes / (ms / 1e3) / 1e9
 
@@ -442,7 +443,7 @@ def run_b200(a, world, rank):
                                                                   "BASELINE config 1)" if world == 1 else "")),
                    "codec": a.codec, "layers": L, "rows": rows, "cols": cols, "shard_rows": n_own,
                    "parallelism": f"patch{world}", "topology": a.topology, "l2": "per-step working set >> 126 MB L2 (no flush needed)",
-                   "overlap": overlap, "cuda_graph": graphs is not None},
+                   "overlap": overlap, "cuda_graph": used_graph},
         "per_gpu_gbs": value / world,
         "exposed_comm_us_per_layer": exposed_us,
         "bf16_allgather_us_per_layer": bf16_ag_us,

@@ -326,9 +326,13 @@ class PatchParallelExchange:
                 self._per = per
                 if skip_comm:
                     pass
-                elif self.sim:
-                    for p in self.peers:
-                        self.slot(p)[:per].copy_(self.sendbuf[:per])
+                elif self.sim:  # one broadcast copy into every peer slot (stands in for the all-gather)
+                    slots = self.recvflat[:self.P * per].view(self.P, per)
+                    if self.peers == list(range(1, self.P)):
+                        slots[1:].copy_(self.sendbuf[:per].expand(self.P - 1, per))
+                    else:
+                        for p in self.peers:
+                            slots[p].copy_(self.sendbuf[:per])
                 else:
                     _dist().all_gather_into_tensor(self.recvflat[:self.P * per], self.sendbuf[:per], group=self.group)
                 self.comm_bytes = per * (self.P - 1)
