@@ -9,11 +9,12 @@
 //   pass H1  t = target(x, base, aux) written once (into the feedback buffer in
 //            residual_with_feedback mode, else into scratch), 4096-bin histogram
 //            of key[30:19] in shared memory -> global; ||t||^2 partials.
-//   find     one CTA: suffix scan of the histogram -> bin b1, remaining need
-//   pass H2  keys in bin b1: 4096-bin histogram of key[18:7]
-//   find     -> b2;   H3: keys with key[30:7] == (b1, b2):
-//            128-bin histogram of key[6:0] -> threshold key T and the number of
-//            ties at T to take (lowest indices first)
+//   find     the pass's last CTA (ticket): suffix scan of the histogram -> bin b1,
+//            remaining need (no separate launch)
+//   pass H2  keys in bin b1: 4096-bin histogram of key[18:7]; last CTA -> b2
+//   pass H3  keys with key[30:7] == (b1, b2): 128-bin histogram of key[6:0]; last
+//            CTA -> threshold key T and the number of ties at T to take (lowest
+//            indices first)
 //   pass C   per-chunk counts of key > T and key == T
 //   scan     exclusive scans -> each chunk's output offset and tie offset
 //   pass W   in index order: selected = key > T || (key == T && tie-rank < ties);
@@ -39,8 +40,31 @@ struct State {
   uint32_t b1, b2;      // selected bins
   uint32_t T;           // threshold key
   uint32_t ties;        // elements with key == T to take
-  uint32_t pad[3];
+  uint32_t pad[3];      // pad[0]: k_write's record ticket
+  uint32_t tk[4];       // last-CTA tickets of the histogram passes (zeroed with the state)
 };
+
+// The histogram passes end with a last-CTA selection step (no separate 1-CTA
+// launch): every CTA adds its shared histogram into the global one, takes a
+// ticket, and the last CTA scans the complete histogram from the top bin.
+template <int NB>
+__device__ __forceinline__ void block_find(const uint32_t *__restrict__ hist, uint32_t need, uint32_t &bin,
+                                           uint32_t &rem, uint32_t *sm);
+template <int NB>
+__device__ __forceinline__ bool last_cta_find(const uint32_t *__restrict__ hist, unsigned int *ticket,
+                                              uint32_t need, uint32_t &bin, uint32_t &rem, uint32_t *sm) {
+  __shared__ unsigned last;
+  __syncthreads();  // every thread's global histogram adds are issued
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  block_find<NB>(hist, need, bin, rem, sm);
+  return true;
+}
 
 struct Work {
   uint32_t *hist1, *hist2, *hist3;
@@ -134,7 +158,8 @@ __global__ void __launch_bounds__(kThreads) k_h1(const XT *__restrict__ x, float
                                                   float *__restrict__ aux, const float *__restrict__ tin,
                                                   float *__restrict__ tout, float *__restrict__ decoded,
                                                   int64_t total, int vec, uint32_t *__restrict__ hist1,
-                                                  double *__restrict__ part) {
+                                                  double *__restrict__ part, State *st, uint32_t k,
+                                                  int fuse_find) {
   __shared__ uint32_t h[kBins];
   __shared__ double red[kThreads / 32];
   for (int i = threadIdx.x; i < kBins; i += kThreads) h[i] = 0;
@@ -171,6 +196,57 @@ __global__ void __launch_bounds__(kThreads) k_h1(const XT *__restrict__ x, float
     part[2 * blockIdx.x] = 0.0;
     part[2 * blockIdx.x + 1] = s;
   }
+  __shared__ uint32_t fsm[kThreads / 32 + 2];
+  uint32_t bin, rem;
+  if (fuse_find && last_cta_find<kBins>(hist1, &st->tk[0], k, bin, rem, fsm) && threadIdx.x == 0) {  // level 1
+    st->b1 = bin;
+    st->need = rem;
+  }
+}
+
+// suffix scan of a histogram from the top bin by one CTA (kThreads threads): the bin
+// holding the need-th largest key, and how many are still needed inside it
+template <int NB>
+__device__ __forceinline__ void block_find(const uint32_t *__restrict__ hist, uint32_t need, uint32_t &bin,
+                                           uint32_t &rem, uint32_t *sm) {
+  constexpr int PER = (NB + kThreads - 1) / kThreads;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  uint32_t v[PER], local = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {  // thread t owns bins NB-1-t*PER-q (descending)
+    const int b = NB - 1 - (t * PER + q);
+    v[q] = b >= 0 ? __ldcg(hist + b) : 0u;
+    local += v[q];
+  }
+  uint32_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) sm[w] = incl;
+  __syncthreads();
+  uint32_t wpre = 0;
+  for (int i = 0; i < w; ++i) wpre += sm[i];
+  incl += wpre;
+  uint32_t before = incl - local;
+  if (before < need && incl >= need) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int b = NB - 1 - (t * PER + q);
+      if (b < 0) break;
+      if (before + v[q] >= need) {
+        sm[kThreads / 32] = (uint32_t)b;
+        sm[kThreads / 32 + 1] = need - before;
+        break;
+      }
+      before += v[q];
+    }
+  }
+  __syncthreads();
+  bin = sm[kThreads / 32];
+  rem = sm[kThreads / 32 + 1];
+  __syncthreads();
 }
 
 // ---- find: suffix scan of a histogram from the top bin ---------------------
@@ -225,9 +301,10 @@ __global__ void __launch_bounds__(1024) k_find(const uint32_t *__restrict__ hist
 // ---- passes H2 / H3: histograms of the keys inside the selected prefix ---------
 // H2: key[18:7] of keys with key[30:19] == b1;  H3: key[6:0] of keys with
 // key[30:7] == (b1, b2).  Both re-stream t (8 keys per thread per iteration).
-template <int LEVEL>
+template <int LEVEL, bool FUSE>  // FUSE: the last CTA selects the next level (compiled out otherwise)
 __global__ void __launch_bounds__(kThreads) k_hsub(const float *__restrict__ t, int64_t total, int vec,
-                                                    const State *st, uint32_t *__restrict__ hist) {
+                                                    State *st_w, uint32_t *__restrict__ hist) {
+  const State *st = st_w;
   constexpr int NB = LEVEL == 2 ? kBins : kBins3;
   __shared__ uint32_t h[NB];
   for (int i = threadIdx.x; i < NB; i += kThreads) h[i] = 0;
@@ -260,6 +337,19 @@ __global__ void __launch_bounds__(kThreads) k_hsub(const float *__restrict__ t, 
   __syncthreads();
   for (int i = threadIdx.x; i < NB; i += kThreads)
     if (h[i]) atomicAdd(&hist[i], h[i]);
+  if constexpr (FUSE) {
+  __shared__ uint32_t fsm[kThreads / 32 + 2];
+  uint32_t bin, rem;
+  if (last_cta_find<NB>(hist, &st_w->tk[LEVEL - 1], st_w->need, bin, rem, fsm) && threadIdx.x == 0) {
+    if (LEVEL == 2) {
+      st_w->b2 = bin;
+    } else {
+      st_w->T = (st_w->b1 << 19) | (st_w->b2 << 7) | bin;  // exact threshold key
+      st_w->ties = rem;                                    // keys equal to T to take (lowest indices)
+    }
+    st_w->need = rem;
+  }
+  }
 }
 
 // ---- pass C: per-chunk counts ------------------------------------------------
@@ -595,6 +685,10 @@ static topk::Work carve_topk(void *ws, int64_t total, bool need_t, int nH1, size
 static bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // histogram passes: few, fat CTAs (each zeroes / flushes a 4096-bin shared histogram)
+// measured: the last-CTA selection wins below ~4M elements (512 x 3072: 97 -> 86 us per
+// encode_step), the separate 1-CTA launches above (4096 x 3072: 121.6 vs 127.5 us)
+static int fuse_find(int64_t total) { return total <= (int64_t)4 << 20; }
+
 static int h1_blocks(int64_t total) { return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), sm_count() * 2)); }
 
 int64_t topk_workspace_bytes(int64_t n, int64_t C, int64_t) {
@@ -612,19 +706,27 @@ static void select_and_write(const topk::Work &w, const float *t, const XT *x, f
                              cudaStream_t st) {
   using namespace topk;
   const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 4 * kThreads), sm_count() * 8));
-  k_find<kBins><<<1, 1024, 0, st>>>(w.hist1, w.st, 1, (uint32_t)k);
   const int vec = al16(t);
-  k_hsub<2><<<nb, kThreads, 0, st>>>(t, total, vec, w.st, w.hist2);
-  k_find<kBins><<<1, 1024, 0, st>>>(w.hist2, w.st, 2, 0);
-  k_hsub<3><<<nb, kThreads, 0, st>>>(t, total, vec, w.st, w.hist3);
-  k_find<kBins3><<<1, 1024, 0, st>>>(w.hist3, w.st, 3, 0);
+  // small problems: each histogram pass's last CTA selects the next level (no 1-CTA
+  // launches); large ones: the ticket adds would serialise, keep the k_find launches
+  const int fuse = fuse_find(total);
+  if (fuse) {
+    k_hsub<2, true><<<nb, kThreads, 0, st>>>(t, total, vec, w.st, w.hist2);
+    k_hsub<3, true><<<nb, kThreads, 0, st>>>(t, total, vec, w.st, w.hist3);
+  } else {
+    k_find<kBins><<<1, 1024, 0, st>>>(w.hist1, w.st, 1, (uint32_t)k);
+    k_hsub<2, false><<<nb, kThreads, 0, st>>>(t, total, vec, w.st, w.hist2);
+    k_find<kBins><<<1, 1024, 0, st>>>(w.hist2, w.st, 2, 0);
+    k_hsub<3, false><<<nb, kThreads, 0, st>>>(t, total, vec, w.st, w.hist3);
+    k_find<kBins3><<<1, 1024, 0, st>>>(w.hist3, w.st, 3, 0);
+  }
   k_count<<<(unsigned)w.nChunks, kThreads, 0, st>>>(t, total, w.st, w.cnt_gt, w.cnt_eq);
   k_scan<<<1, 1024, 0, st>>>(w.nChunks, w.st, w.cnt_gt, w.cnt_eq, w.sel_pref, w.eq_pref);
   // k_write's last CTA also reduces the StepRecord partials (no separate launch)
   k_write<MODE, XT><<<(unsigned)w.nChunks, kThreads, 0, st>>>(t, x, base, aux, decoded, total, k, w.st, w.sel_pref,
                                                              w.eq_pref, body, w.part + 2 * w.nH1, stateful, w.part,
                                                              (int)(w.nH1 + w.nChunks), &w.st->pad[0], record);
-  count_launch(8);
+  count_launch(fuse ? 5 : 8);
 }
 
 int topk_encode(int64_t n, int64_t C, int64_t k, const float *t, uint8_t *body, float *decoded, void *ws,
@@ -641,7 +743,8 @@ int topk_encode(int64_t n, int64_t C, int64_t k, const float *t, uint8_t *body, 
   double *record = reinterpret_cast<double *>(reinterpret_cast<uint8_t *>(ws) + need);
   cudaMemsetAsync(ws, 0, kZeroBytes, st);
   topk::k_h1<CC_NAIVE, float, true><<<nH1, topk::kThreads, 0, st>>>(nullptr, nullptr, nullptr, t, nullptr, decoded,
-                                                                    total, al16(t) && al16(decoded), w.hist1, w.part);
+                                                                    total, al16(t) && al16(decoded), w.hist1, w.part,
+                                                                    w.st, (uint32_t)k, fuse_find(total));
   count_launch();
   select_and_write<CC_NAIVE, float>(w, t, nullptr, nullptr, nullptr, decoded, total, k, body, record, 0, st);
   return cuda_status("topk_encode");
@@ -666,7 +769,8 @@ int topk_encode_step(int mode, int64_t n, int64_t C, int64_t k, const void *x, i
 #define CC_TK(MODE, XT)                                                                                      \
   do {                                                                                                       \
     topk::k_h1<MODE, XT, false><<<nH1, topk::kThreads, 0, st>>>((const XT *)x, base, aux, nullptr, t, nullptr, \
-                                                                total, vec, w.hist1, w.part);               \
+                                                                total, vec, w.hist1, w.part, w.st, (uint32_t)k, \
+                                                                fuse_find(total));                          \
     count_launch();                                                                                          \
     select_and_write<MODE, XT>(w, t, (const XT *)x, base, aux, nullptr, total, k, body, record, 1, st);      \
   } while (0)
