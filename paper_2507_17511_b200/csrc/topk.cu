@@ -352,9 +352,56 @@ __global__ void __launch_bounds__(kThreads) k_hsub(const float *__restrict__ t, 
   }
 }
 
+// chunk offsets: exclusive scans of the per-chunk tie counts and selected counts (the
+// first `ties` keys equal to T, in index order, are taken), NT threads of one CTA
+template <int NT>
+__device__ __forceinline__ void scan_chunks(int64_t nch, uint32_t ties, const uint32_t *__restrict__ cnt_gt,
+                                            const uint32_t *__restrict__ cnt_eq, uint32_t *__restrict__ sel_pref,
+                                            uint32_t *__restrict__ eq_pref, uint32_t *s_eq, uint32_t *s_sel,
+                                            uint32_t *carry) {
+  if (threadIdx.x == 0) carry[0] = carry[1] = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nch; base += NT) {
+    const int64_t i = base + threadIdx.x;
+    const uint32_t eq = i < nch ? __ldcg(cnt_eq + i) : 0u;
+    s_eq[threadIdx.x] = eq;
+    __syncthreads();
+    for (int off = 1; off < NT; off <<= 1) {
+      const uint32_t add = threadIdx.x >= off ? s_eq[threadIdx.x - off] : 0u;
+      __syncthreads();
+      s_eq[threadIdx.x] += add;
+      __syncthreads();
+    }
+    const uint32_t eq_before = carry[0] + s_eq[threadIdx.x] - eq;
+    uint32_t take = 0;
+    if (eq_before < ties) take = min(eq, ties - eq_before);
+    const uint32_t sel = (i < nch ? __ldcg(cnt_gt + i) : 0u) + take;
+    s_sel[threadIdx.x] = sel;
+    __syncthreads();
+    for (int off = 1; off < NT; off <<= 1) {
+      const uint32_t add = threadIdx.x >= off ? s_sel[threadIdx.x - off] : 0u;
+      __syncthreads();
+      s_sel[threadIdx.x] += add;
+      __syncthreads();
+    }
+    if (i < nch) {
+      eq_pref[i] = eq_before;
+      sel_pref[i] = carry[1] + s_sel[threadIdx.x] - sel;
+    }
+    __syncthreads();
+    if (threadIdx.x == NT - 1) {
+      carry[0] += s_eq[NT - 1];
+      carry[1] += s_sel[NT - 1];
+    }
+    __syncthreads();
+  }
+}
+
 // ---- pass C: per-chunk counts ------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_count(const float *__restrict__ t, int64_t total, const State *st,
-                                                     uint32_t *__restrict__ cnt_gt, uint32_t *__restrict__ cnt_eq) {
+template <bool FUSE>  // FUSE: the last CTA also computes the chunk offsets (replaces k_scan)
+__global__ void __launch_bounds__(kThreads) k_count(const float *__restrict__ t, int64_t total, State *st,
+                                                     uint32_t *__restrict__ cnt_gt, uint32_t *__restrict__ cnt_eq,
+                                                     uint32_t *__restrict__ sel_pref, uint32_t *__restrict__ eq_pref) {
   __shared__ uint32_t sg[kThreads / 32], se[kThreads / 32];
   const uint32_t T = st->T;
   const int64_t c0 = (int64_t)blockIdx.x * kChunk;
@@ -406,51 +453,28 @@ __global__ void __launch_bounds__(kThreads) k_count(const float *__restrict__ t,
     cnt_gt[blockIdx.x] = a;
     cnt_eq[blockIdx.x] = b;
   }
+  if constexpr (FUSE) {
+    __shared__ unsigned last;
+    __shared__ uint32_t s_eq[kThreads], s_sel[kThreads], carry[2];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(&st->tk[3], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      scan_chunks<kThreads>((int64_t)gridDim.x, st->ties, cnt_gt, cnt_eq, sel_pref, eq_pref, s_eq, s_sel, carry);
+    }
+  }
 }
 
 // ---- scan: chunk offsets --------------------------------------------------------
 __global__ void __launch_bounds__(1024) k_scan(int64_t nch, const State *st, const uint32_t *__restrict__ cnt_gt,
                                                const uint32_t *__restrict__ cnt_eq, uint32_t *__restrict__ sel_pref,
                                                uint32_t *__restrict__ eq_pref) {
-  __shared__ uint32_t s_eq[1024], s_sel[1024];
-  __shared__ uint32_t carry_eq, carry_sel;
-  const uint32_t ties = st->ties;
-  if (threadIdx.x == 0) carry_eq = carry_sel = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < nch; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    const uint32_t eq = i < nch ? cnt_eq[i] : 0u;
-    s_eq[threadIdx.x] = eq;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-      const uint32_t add = threadIdx.x >= off ? s_eq[threadIdx.x - off] : 0u;
-      __syncthreads();
-      s_eq[threadIdx.x] += add;
-      __syncthreads();
-    }
-    const uint32_t eq_before = carry_eq + s_eq[threadIdx.x] - eq;
-    uint32_t take = 0;
-    if (eq_before < ties) take = min(eq, ties - eq_before);
-    const uint32_t sel = (i < nch ? cnt_gt[i] : 0u) + take;
-    s_sel[threadIdx.x] = sel;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-      const uint32_t add = threadIdx.x >= off ? s_sel[threadIdx.x - off] : 0u;
-      __syncthreads();
-      s_sel[threadIdx.x] += add;
-      __syncthreads();
-    }
-    if (i < nch) {
-      eq_pref[i] = eq_before;
-      sel_pref[i] = carry_sel + s_sel[threadIdx.x] - sel;
-    }
-    __syncthreads();
-    if (threadIdx.x == 1023) {
-      carry_eq += s_eq[1023];
-      carry_sel += s_sel[1023];
-    }
-    __syncthreads();
-  }
+  __shared__ uint32_t s_eq[1024], s_sel[1024], carry[2];
+  scan_chunks<1024>(nch, st->ties, cnt_gt, cnt_eq, sel_pref, eq_pref, s_eq, s_sel, carry);
 }
 
 // block-wide exclusive scan of a per-thread count; returns the block total
@@ -720,13 +744,18 @@ static void select_and_write(const topk::Work &w, const float *t, const XT *x, f
     k_hsub<3, false><<<nb, kThreads, 0, st>>>(t, total, vec, w.st, w.hist3);
     k_find<kBins3><<<1, 1024, 0, st>>>(w.hist3, w.st, 3, 0);
   }
-  k_count<<<(unsigned)w.nChunks, kThreads, 0, st>>>(t, total, w.st, w.cnt_gt, w.cnt_eq);
-  k_scan<<<1, 1024, 0, st>>>(w.nChunks, w.st, w.cnt_gt, w.cnt_eq, w.sel_pref, w.eq_pref);
+  if (fuse) {
+    k_count<true><<<(unsigned)w.nChunks, kThreads, 0, st>>>(t, total, w.st, w.cnt_gt, w.cnt_eq, w.sel_pref,
+                                                           w.eq_pref);
+  } else {
+    k_count<false><<<(unsigned)w.nChunks, kThreads, 0, st>>>(t, total, w.st, w.cnt_gt, w.cnt_eq, nullptr, nullptr);
+    k_scan<<<1, 1024, 0, st>>>(w.nChunks, w.st, w.cnt_gt, w.cnt_eq, w.sel_pref, w.eq_pref);
+  }
   // k_write's last CTA also reduces the StepRecord partials (no separate launch)
   k_write<MODE, XT><<<(unsigned)w.nChunks, kThreads, 0, st>>>(t, x, base, aux, decoded, total, k, w.st, w.sel_pref,
                                                              w.eq_pref, body, w.part + 2 * w.nH1, stateful, w.part,
                                                              (int)(w.nH1 + w.nChunks), &w.st->pad[0], record);
-  count_launch(fuse ? 5 : 8);
+  count_launch(fuse ? 4 : 8);
 }
 
 int topk_encode(int64_t n, int64_t C, int64_t k, const float *t, uint8_t *body, float *decoded, void *ws,
