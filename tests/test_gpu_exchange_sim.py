@@ -43,3 +43,36 @@ def test_sim_exchange_peers_equal_sender(codec, kw, P):
         for p in range(1, P):
             b0, b1 = ex.bounds[p]
             assert torch.equal(full[b0:b1], own), f"peer {p} differs at step {t}"
+
+
+@pytest.mark.parametrize("codec,kw", [("quant2bit", {}), ("topk", {"keep_fraction": 0.02})], ids=lambda v: str(v))
+def test_graph_replayed_exchange_matches_eager(codec, kw):
+    """bench.py replays CUDA-graph-captured exchange steps: a captured step replayed
+    must give exactly the state an eager step gives (K1's stream control slot is
+    bound at capture time; the replay runs on another stream)."""
+    from paper_2507_17511_b200 import comm
+    from paper_2507_17511_b200 import compressors as cx
+
+    rows, cols, P = 96, 3072, 4
+    spec = cx.CompressorSpec(cx.CompressorKind(codec), **kw)
+    xs = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in synth.flux_like(rows // P, cols, 6, seed=31)]
+    eager = comm.PatchParallelExchange(rows, cols, spec, sim_world=(P, 0))
+    graphed = comm.PatchParallelExchange(rows, cols, spec, sim_world=(P, 0))
+    for t in range(3):  # warmup step + two compressed steps, eagerly on both
+        eager.step(xs[t])
+        graphed.step(xs[t])
+    torch.cuda.synchronize()
+    inp = torch.empty_like(xs[0])
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        graphed.step(inp)
+        torch.cuda.current_stream().wait_stream(graphed.streams.decode)
+    graphed.after_capture()
+    for t in range(3, 6):
+        eager.step(xs[t])
+        eager.synchronize()
+        inp.copy_(xs[t])
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(eager.full, graphed.full), f"step {t}"
+        assert torch.equal(eager.sender.feedback, graphed.sender.feedback), f"step {t}"
