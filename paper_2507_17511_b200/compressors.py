@@ -169,6 +169,35 @@ def workspace(nbytes, key="default"):
     return buf
 
 
+_PIN_RING: dict = {}
+_PIN_SLOTS = 8
+
+
+def _stage_h2d(arr, device):
+    """Asynchronous H2D copy of a small host array through a per-(device, stream, size)
+    ring of pinned slots; a slot is rewritten only after its previous copy completed
+    (its event), so a fresh pinned allocation per call (which can stall the host on
+    cudaHostAlloc) is never needed."""
+    arr = np.ascontiguousarray(arr)
+    src = torch.from_numpy(arr)
+    if torch.cuda.is_current_stream_capturing():  # no host event waits inside a capture
+        return src.pin_memory().to(device, non_blocking=True)
+    stream = torch.cuda.current_stream(device)
+    k = (device.index, stream.cuda_stream, src.dtype, src.numel())
+    ring = _PIN_RING.get(k)
+    if ring is None:
+        ring = _PIN_RING[k] = {"i": 0, "slots": [(torch.empty(src.numel(), dtype=src.dtype).pin_memory(),
+                                                  torch.cuda.Event()) for _ in range(_PIN_SLOTS)]}
+    buf, ev = ring["slots"][ring["i"]]
+    ring["i"] = (ring["i"] + 1) % _PIN_SLOTS
+    ev.synchronize()
+    buf.copy_(src.reshape(-1))
+    out = torch.empty(src.shape, dtype=src.dtype, device=device)
+    out.copy_(buf.view(src.shape), non_blocking=True)
+    ev.record(stream)
+    return out
+
+
 # ---------------------------------------------------------------------------
 # payloads (cx:157-361): bodies live on the device
 # ---------------------------------------------------------------------------
@@ -505,10 +534,10 @@ def encode_lowrank(a, spec, rng, decoded=None):
     if not (1 <= r <= min(rows, cols)):
         raise ShapeError(f"rank {r} out of range for shape {(rows, cols)}")
     lib = _lib.load()
-    # Q0 is drawn on the host from the reference's PCG64 stream (cx:407); a pinned
-    # staging copy keeps the H2D transfer asynchronous (no stream drain per step)
-    q0 = torch.from_numpy(subspace_init(rng, cols, r))
-    q0 = q0.pin_memory().to(t.device, non_blocking=True) if t.is_cuda else q0.to(t.device)
+    # Q0 is drawn on the host from the reference's PCG64 stream (cx:407) and goes up
+    # through a reused pinned staging ring (asynchronous H2D, no per-step host alloc)
+    q0 = subspace_init(rng, cols, r)
+    q0 = _stage_h2d(q0, t.device) if t.is_cuda else torch.from_numpy(q0).to(t.device)
     tag = _lib.CC_LOWRANK4 if spec.int4_factors else _lib.CC_LOWRANK
     body = _empty_body(lib.cc_body_bytes(tag, rows, cols, r))
     ws = workspace(_lib.check(lib.cc_lowrank_workspace_bytes(rows, cols, r)), "lowrank")

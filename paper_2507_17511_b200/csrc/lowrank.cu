@@ -355,6 +355,33 @@ __device__ void cgs2_block(const float *__restrict__ orig, double *__restrict__ 
   for (int64_t e = threadIdx.x; e < m * r; e += blockDim.x) out[e] = (float)M[e];
 }
 
+// one warp: right-looking Cholesky of G (as k_chol) and R^-1 into Ri, lane c owns column c
+__device__ __forceinline__ void chol_rinv_warp(double (*G)[kMaxR + 1], double (*R)[kMaxR + 1],
+                                               double (*Ri)[kMaxR + 1], int r, int *bad) {
+  const int c = threadIdx.x & 31;
+  for (int j = 0; j < r; ++j) {
+    double piv = G[j][j];  // every lane reads the same pivot
+    if (!(piv >= kDegenerate)) {
+      if (c == 0) *bad = 1;
+      piv = 1.0;
+    }
+    const double rjj = sqrt(piv);
+    if (c == j) R[j][j] = rjj;
+    if (c > j && c < r) R[j][c] = G[j][c] / rjj;
+    __syncwarp();
+    if (c > j && c < r)
+      for (int a = j + 1; a < r; ++a) G[a][c] -= R[j][a] * R[j][c];
+    __syncwarp();
+  }
+  if (c < r) {  // column c of R^-1 (upper triangular), back substitution into shared memory
+    for (int i = r - 1; i >= 0; --i) {
+      double sacc = (i == c) ? 1.0 : 0.0;
+      for (int k = i + 1; k <= c; ++k) sacc -= R[i][k] * Ri[k][c];
+      Ri[i][c] = (i > c) ? 0.0 : sacc / R[i][i];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kOrthThreads) k_orth(const float *__restrict__ Min, float *__restrict__ out,
                                                         int64_t m, int r, double *__restrict__ Gpart,
                                                         double *__restrict__ scratch, unsigned long long seed) {
@@ -397,30 +424,7 @@ __global__ void __launch_bounds__(kOrthThreads) k_orth(const float *__restrict__
       R[a][c] = 0.0;
     }
     __syncthreads();
-    if (tid < 32) {  // one warp: right-looking Cholesky (as k_chol) and R^-1, lane c owns column c
-      const int c = tid;
-      for (int j = 0; j < r; ++j) {
-        double piv = G[j][j];  // every lane reads the same pivot
-        if (!(piv >= kDegenerate)) {
-          if (c == 0) bad = 1;
-          piv = 1.0;
-        }
-        const double rjj = sqrt(piv);
-        if (c == j) R[j][j] = rjj;
-        if (c > j && c < r) R[j][c] = G[j][c] / rjj;
-        __syncwarp();
-        if (c > j && c < r)
-          for (int a = j + 1; a < r; ++a) G[a][c] -= R[j][a] * R[j][c];
-        __syncwarp();
-      }
-      if (c < r) {  // column c of R^-1 (upper triangular), back substitution into shared memory
-        for (int i = r - 1; i >= 0; --i) {
-          double sacc = (i == c) ? 1.0 : 0.0;
-          for (int k = i + 1; k <= c; ++k) sacc -= R[i][k] * Ri[k][c];
-          Ri[i][c] = (i > c) ? 0.0 : sacc / R[i][i];
-        }
-      }
-    }
+    if (tid < 32) chol_rinv_warp(G, R, Ri, r, &bad);
     __syncthreads();
     for (int i = tid; i < rc; i += kOrthThreads) {  // M <- M R^-1 (as k_apply_rinv)
       double row[kMaxR];
@@ -706,9 +710,24 @@ int lowrank_encode(int int4, int64_t n, int64_t C, int64_t r64, int iters, const
   return cuda_status("lowrank_encode");
 }
 
+static void keep_default_pool() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
 int lowrank_decode(int int4, int count, const int64_t *rows, int64_t C, int64_t r, const uint8_t *const *bodies,
                    int accumulate, float *const *bases, cudaStream_t st) {
-  // factor scratch: allocated per call (decode of a received payload)
+  // factor scratch: allocated per call from the device's default pool, which keeps its
+  // memory across synchronizations (otherwise every event sync trims it and the next
+  // allocation maps fresh pages on the host's critical path)
+  keep_default_pool();
   int64_t maxn = 0;
   for (int i = 0; i < count; ++i) maxn = std::max(maxn, rows[i]);
   double *scratch = nullptr;
