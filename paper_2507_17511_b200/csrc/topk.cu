@@ -204,6 +204,36 @@ __global__ void __launch_bounds__(kThreads) k_h1(const XT *__restrict__ x, float
   }
 }
 
+// inclusive scan of one value per thread over a CTA of NT threads (warp shuffles, warp
+// totals through `wsum` [NT/32]); `total` = the CTA-wide sum
+template <int NT>
+__device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, uint32_t *wsum, uint32_t &total) {
+  static_assert(NT % 32 == 0 && NT <= 1024, "block size");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t s = lane < NT / 32 ? wsum[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < NT / 32) wsum[lane] = s;
+  }
+  __syncthreads();
+  if (w > 0) incl += wsum[w - 1];
+  total = wsum[NT / 32 - 1];
+  __syncthreads();  // wsum is reused by the next call
+  return incl;
+}
+
 // suffix scan of a histogram from the top bin by one CTA (kThreads threads): the bin
 // holding the need-th largest key, and how many are still needed inside it
 template <int NB>
@@ -253,7 +283,7 @@ __device__ __forceinline__ void block_find(const uint32_t *__restrict__ hist, ui
 template <int NB>
 __global__ void __launch_bounds__(1024) k_find(const uint32_t *__restrict__ hist, State *st, int level, uint32_t k) {
   constexpr int PER = (NB + 1023) / 1024;
-  __shared__ uint32_t tot[1024];
+  __shared__ uint32_t tot[32];
   const int t = threadIdx.x;
   // thread t owns bins [NB-1-t*PER ... NB-PER-t*PER] (descending order)
   uint32_t local = 0;
@@ -264,18 +294,11 @@ __global__ void __launch_bounds__(1024) k_find(const uint32_t *__restrict__ hist
     v[q] = b >= 0 ? hist[b] : 0u;
     local += v[q];
   }
-  tot[t] = local;
-  __syncthreads();
-  // inclusive scan over threads (Hillis-Steele; NB is small)
-  for (int off = 1; off < 1024; off <<= 1) {
-    const uint32_t add = t >= off ? tot[t - off] : 0u;
-    __syncthreads();
-    tot[t] += add;
-    __syncthreads();
-  }
+  uint32_t total;
+  const uint32_t incl = block_incl_scan<1024>(local, tot, total);
   const uint32_t need = level == 1 ? k : st->need;
-  uint32_t before = t > 0 ? tot[t - 1] : 0u;
-  if (before < need && tot[t] >= need) {
+  uint32_t before = incl - local;
+  if (before < need && incl >= need) {
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int b = NB - 1 - (t * PER + q);
@@ -359,41 +382,24 @@ __device__ __forceinline__ void scan_chunks(int64_t nch, uint32_t ties, const ui
                                             const uint32_t *__restrict__ cnt_eq, uint32_t *__restrict__ sel_pref,
                                             uint32_t *__restrict__ eq_pref, uint32_t *s_eq, uint32_t *s_sel,
                                             uint32_t *carry) {
-  if (threadIdx.x == 0) carry[0] = carry[1] = 0;
-  __syncthreads();
+  (void)carry;
+  uint32_t carry_eq = 0, carry_sel = 0;  // identical in every thread
   for (int64_t base = 0; base < nch; base += NT) {
     const int64_t i = base + threadIdx.x;
     const uint32_t eq = i < nch ? __ldcg(cnt_eq + i) : 0u;
-    s_eq[threadIdx.x] = eq;
-    __syncthreads();
-    for (int off = 1; off < NT; off <<= 1) {
-      const uint32_t add = threadIdx.x >= off ? s_eq[threadIdx.x - off] : 0u;
-      __syncthreads();
-      s_eq[threadIdx.x] += add;
-      __syncthreads();
-    }
-    const uint32_t eq_before = carry[0] + s_eq[threadIdx.x] - eq;
+    const uint32_t gt = i < nch ? __ldcg(cnt_gt + i) : 0u;
+    uint32_t tot_eq, tot_sel;
+    const uint32_t eq_before = carry_eq + block_incl_scan<NT>(eq, s_eq, tot_eq) - eq;
     uint32_t take = 0;
     if (eq_before < ties) take = min(eq, ties - eq_before);
-    const uint32_t sel = (i < nch ? __ldcg(cnt_gt + i) : 0u) + take;
-    s_sel[threadIdx.x] = sel;
-    __syncthreads();
-    for (int off = 1; off < NT; off <<= 1) {
-      const uint32_t add = threadIdx.x >= off ? s_sel[threadIdx.x - off] : 0u;
-      __syncthreads();
-      s_sel[threadIdx.x] += add;
-      __syncthreads();
-    }
+    const uint32_t sel = gt + take;
+    const uint32_t sel_incl = block_incl_scan<NT>(sel, s_sel, tot_sel);
     if (i < nch) {
       eq_pref[i] = eq_before;
-      sel_pref[i] = carry[1] + s_sel[threadIdx.x] - sel;
+      sel_pref[i] = carry_sel + sel_incl - sel;
     }
-    __syncthreads();
-    if (threadIdx.x == NT - 1) {
-      carry[0] += s_eq[NT - 1];
-      carry[1] += s_sel[NT - 1];
-    }
-    __syncthreads();
+    carry_eq += tot_eq;
+    carry_sel += tot_sel;
   }
 }
 
@@ -711,7 +717,13 @@ static bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) =
 // histogram passes: few, fat CTAs (each zeroes / flushes a 4096-bin shared histogram)
 // measured: the last-CTA selection wins below ~4M elements (512 x 3072: 97 -> 86 us per
 // encode_step), the separate 1-CTA launches above (4096 x 3072: 121.6 vs 127.5 us)
-static int fuse_find(int64_t total) { return total <= (int64_t)4 << 20; }
+static int fuse_find(int64_t total) {
+  static const int64_t lim = [] {
+    const char *e = getenv("CC_TOPK_FUSE_MAX");  // experiment knob: largest fused-find size
+    return e ? (int64_t)atoll(e) : (int64_t)4 << 20;
+  }();
+  return total <= lim;
+}
 
 static int h1_blocks(int64_t total) { return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), sm_count() * 2)); }
 
