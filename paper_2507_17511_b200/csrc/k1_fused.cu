@@ -108,7 +108,7 @@ int fused_encode_segments(int codec, int mode, int scale_mode, int64_t n, int64_
   // rows per tile: a multiple of the row groups; two per group when each CTA has plenty of rows
   const int64_t rows_per_cta = cdiv(n, G);
   constexpr double kL2KeepBytes = 40e6;
-  p.R = p.groups * (rows_per_cta >= 16 * p.groups ? 2 : 1);
+  p.R = p.groups * ((Q == 2 || rows_per_cta >= 16 * p.groups) ? 2 : 1);
   if (g_fused_ra > 0) p.R = p.groups * g_fused_ra;
   p.G = G;
   p.nTiles = cdiv(n, p.R);

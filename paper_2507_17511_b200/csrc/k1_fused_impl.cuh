@@ -1000,7 +1000,10 @@ inline int launch_fused(fused::Params &p, cudaStream_t st) {
   const OutStage LO = out_stage<MODE>(p.groups, p.C, p.cb_row);
   const InStage LA = in_stage<MODE, XT>(p.R, p.C, MODE == CC_WITH_FEEDBACK);
   // phase A ring + its row-partial scratch (2 use parities x SA stages)
-  int SA = (int)std::min<size_t>(g_fused_sa > 0 ? g_fused_sa : 8,
+  // full-width rows (> 1536 columns): 2-row tiles, 2 stages measured best at every shard height
+  // (512..4096 rows: -0.8 .. -2.2 us vs 8 stages, scripts/microbench.py phase-A sweep)
+  const int sa_default = p.G4 > kCons ? 2 : 8;
+  int SA = (int)std::min<size_t>(g_fused_sa > 0 ? g_fused_sa : sa_default,
                                   (budget - fixed_tail) / (LA.bytes + (size_t)2 * p.R * kNB * 8));
   if (SA < 2) {
     set_error("k1_fused: phase-A stages do not fit shared memory");

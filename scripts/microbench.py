@@ -110,7 +110,7 @@ def main():
         out[f"k1_fused_rings{si}_{so}"] = {"us": round(us, 2), "alg_GBps": round(alg / us / 1e3, 1)}
     lib.cc_debug_fused_rings(0, 0)
     # phase-A tile height / ring depth sweep (phase A only and full step)
-    for ra, sa in ((1, 2), (1, 4), (1, 6), (2, 2), (2, 3), (3, 2)):
+    for ra, sa in ((1, 2), (1, 4), (1, 8), (2, 2), (2, 3), (2, 4), (2, 8), (3, 2), (4, 2)):
         lib.cc_debug_fused_phase_a(ra, sa)
         for stop in (1, 0):
             lib.cc_debug_fused_stop(stop)
