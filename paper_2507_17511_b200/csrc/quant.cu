@@ -715,8 +715,12 @@ void set_quant_path(int v) { g_force_path = v; }
 int quant_encode_step(int codec, int mode, int scale_mode, int64_t n, int64_t C, const void *x, int x_dtype,
                       float *base, float *aux, uint8_t *body, void *ws, int64_t ws_bytes, double *record,
                       cudaStream_t st) {
-  if (g_force_path != 0 && fused_supported(n, C, x, x_dtype, base, aux, body))
-    return fused_encode(codec, mode, scale_mode, n, C, x, x_dtype, base, aux, body, ws, ws_bytes, record, st);
+  if (g_force_path != 0 && fused_supported(n, C, x, x_dtype, base, aux, body)) {
+    const int rc = fused_encode(codec, mode, scale_mode, n, C, x, x_dtype, base, aux, body, ws, ws_bytes, record, st);
+    // a refused cooperative launch (nothing ran) falls through to the multi-kernel path,
+    // which computes the same bytes; forced-fused callers see the error
+    if (rc != CC_ERR_CUDA || g_force_path == 1) return rc;
+  }
 #define CC_DISPATCH_MODE(XT)                                                                                   \
   switch (mode) {                                                                                              \
     case CC_NAIVE:                                                                                             \
