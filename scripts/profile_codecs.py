@@ -33,6 +33,8 @@ def main():
         spec = cx.CompressorSpec(kind, rank=a.rank, iterations=a.iters)
     elif kind == cx.CompressorKind.TOPK:
         spec = cx.CompressorSpec(kind, keep_fraction=a.keep)
+    elif kind == cx.CompressorKind.NM_BLOCK:
+        spec = cx.CompressorSpec(kind, n=2, m=4)
     else:
         spec = cx.CompressorSpec(kind)
     g = torch.Generator(device="cuda").manual_seed(0)
