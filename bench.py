@@ -15,22 +15,29 @@ small step-to-step drift) resident in HBM; the per-step working set (57 layers
 x ~150 MB of state) is far larger than the 126 MB L2, so nothing is L2-warm
 between a layer's consecutive steps.
 
-value   = whole-job activation GB/s = N * layers * 2*4096*3072 B / step time
+value   = whole-job activation GB/s = sum over ranks of the activation bytes each
+          rank reconstructs (the full 2*4096*3072 B per layer) / step time
+          (max over ranks); per_gpu_gbs = value / N.  Every rank rebuilds the
+          full activation whatever N is, so per-GPU work is fixed ("weak").
 e2e     = same metric through the public API with pinned HOST inputs: per layer
           H2D of the bf16 shard, exchange, D2H of the packed body + StepRecord
 roofline: K1 (encode_step: residual -> scales -> quantize/pack -> state update)
           achieved = algorithmic bytes (18 + b/8 B per own element + scales)
-          / K1 duration (CUDA events on its stream, timed region)
-cpu_baseline: the numpy oracle port of the reference encode_step + decode_step
-          (pl:84-165) on the host cores, thread-parallel over layer channels.
+          / K1 duration, measured with CUDA events recorded INSIDE the replayed
+          CUDA graph around every K1 (the headline's launch mode)
+cpu_baseline: the reference's own pipeline.encode_step + decode_step
+          (oracle/_ref, the unmodified reference package; the numpy port in
+          oracle/cc_oracle.py when it is absent) on the host cores, one process
+          per core, per-GPU-equivalent work (own-shard encode + (N-1) decodes).
 
-`--impl reference` times that same CPU path as the reference arm.
+`--gpus N` without a torchrun environment relaunches itself under
+torch.distributed.run with N ranks.  `--impl reference` times that same CPU path
+as the reference arm (rank 0 only).
 """
 
 from __future__ import annotations
 
 import argparse
-import concurrent.futures as cf
 import json
 import os
 import statistics
@@ -45,9 +52,10 @@ ROWS, COLS = 4096, 3072
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC = os.path.join(ROOT, "profiles", "k1_traffic.json")
 BITS = {"sign1bit": 1, "quant2bit": 2, "quant4bit": 4}
+METRIC = "activation GB/s compressed+reconstructed per GPU and exposed comm us/layer"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -70,12 +78,49 @@ def parse():
                     "loopback receiver has no communication to hide; two HBM-bound kernels gain nothing)")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from Python instead of "
                                                              "replaying a captured CUDA graph per step")
-    return ap.parse_args()
+    ap.add_argument("--cpu-procs", type=int, default=None, help="host processes for the CPU path "
+                    "(default: min(cpu_count, 16) for cpu_baseline, cpu_count for --impl reference)")
+    return ap.parse_args(argv)
+
+
+def bench_config(a, world):
+    """The workload both arms run (identical dict in both JSON lines)."""
+    n_own = a.rows // world
+    return {"workload": (f"FLUX.1 [{a.rows}x{a.cols}] {a.codec} residual+EF patch-parallel exchange, "
+                         f"{a.layers} layer channels per step, world_size={world}: per rank-layer encode_step(own "
+                         f"[{n_own},{a.cols}] shard) + {'(N-1) peer decode_steps' if world > 1 else 'loopback receiver decode_step (BASELINE config 1)'}"),
+            "codec": a.codec, "layers": a.layers, "rows": a.rows, "cols": a.cols, "shard_rows": n_own,
+            "parallelism": f"patch{world}", "topology": a.topology, "input_dtype": "bf16", "state_dtype": "f32",
+            "l2": "per-step working set >> 126 MB L2 (no flush needed)"}
 
 
 # ---------------------------------------------------------------------------
 # distributed plumbing
 # ---------------------------------------------------------------------------
+
+def _free_port():
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(a):
+    """`--gpus N` outside torchrun: re-exec this script as N torchrun ranks."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        print(f"bench: --gpus {a.gpus} needs {a.gpus} GPUs, this node has {have}", file=sys.stderr, flush=True)
+        return 1
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
 
 def dist_setup():
     import torch
@@ -84,11 +129,9 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local if world > 1 else 0)
     if world > 1:
-        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
     return world, rank
 
 
@@ -190,78 +233,136 @@ def flux_inputs(rows, cols, lo, hi, layer, device):
 
 
 # ---------------------------------------------------------------------------
-# CPU path (oracle port of the reference) — cpu_baseline and --impl reference
+# CPU path — cpu_baseline and --impl reference
 # ---------------------------------------------------------------------------
 
-def _cpu_unit(rows, cols, world, codec, seed, gate):
-    """One rank-layer-step on the host: encode own shard + (world-1) peer decodes
-    (per-GPU-equivalent work).  Setup and the raw warmup step run
-    before `gate`; returns (start, end) of the timed compressed step."""
+def _cpu_worker(conn, gate, impl):
+    """One host process: per request, build one rank-layer channel set and time
+    one compressed step of it (encode own shard + (world-1) peer decodes, or one
+    loopback decode at world 1).  Setup and the raw warmup step are untimed."""
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = "1"
     import numpy as np
 
-    from oracle import cc_oracle as O
+    if impl == "reference":
+        from oracle.build_ref import import_reference
 
-    n = rows // world
-    rng = np.random.Generator(np.random.PCG64(seed))
-    a = rng.lognormal(0.0, 0.25, (n, 1)).astype(np.float32)
-    c = rng.lognormal(0.0, 1.0, (1, cols)).astype(np.float32)
-    x0 = (a * c * rng.standard_normal((n, cols), dtype=np.float32)).astype(np.float32)
-    x1 = (x0 + 0.1 * a * c * rng.standard_normal((n, cols), dtype=np.float32)).astype(np.float32)
-    tag = {"sign1bit": O.SIGN1, "quant2bit": O.QUANT2}.get(codec, O.QUANT2)
-    cdc = O.Codec(tag)
-    snd = O.Channel(O.WITH_FEEDBACK, 1, np.zeros((n, cols), np.float32))
-    rcv = [O.Channel(O.WITH_FEEDBACK, 1, np.zeros((n, cols), np.float32)) for _ in range(max(1, world - 1))]
-    t0 = O.send(snd, x0, cdc)  # warmup (raw) step, untimed
-    for r in rcv:
-        O.receive(r, 1, True, O.RAW, t0[1], O.Codec(O.RAW))
-    gate.wait()
-    start = time.perf_counter()
-    tg, body, _ = O.send(snd, x1, cdc)
-    for r in rcv:
-        O.receive(r, 2, False, tg, body, cdc)
-    return start, time.perf_counter()
+        cx, pl, _ = import_reference()
+    else:
+        from oracle import cc_oracle as O
+    while True:
+        req = conn.recv()
+        if req is None:
+            return
+        rows, cols, world, codec, seed = req
+        n = rows // world
+        rng = np.random.Generator(np.random.PCG64(seed))
+        a = rng.lognormal(0.0, 0.25, (n, 1)).astype(np.float32)
+        c = rng.lognormal(0.0, 1.0, (1, cols)).astype(np.float32)
+        x0 = (a * c * rng.standard_normal((n, cols), dtype=np.float32)).astype(np.float32)
+        x1 = (x0 + 0.1 * a * c * rng.standard_normal((n, cols), dtype=np.float32)).astype(np.float32)
+        peers = max(1, world - 1)
+        if impl == "reference":
+            spec = cx.CompressorSpec(cx.CompressorKind(codec))
+            mode = pl.PipelineMode.RESIDUAL_WITH_FEEDBACK
+            snd = pl.LayerState(mode, 1, np.zeros((n, cols), np.float32))
+            rcv = [pl.LayerState(mode, 1, np.zeros((n, cols), np.float32)) for _ in range(peers)]
+            p0, _ = pl.encode_step(snd, x0, spec)
+            m0 = pl.message_for(1, 1, p0)
+            for r in rcv:
+                pl.decode_step(r, m0)
+
+            def unit():
+                p1, _ = pl.encode_step(snd, x1, spec)
+                m1 = pl.message_for(2, 1, p1)
+                for r in rcv:
+                    pl.decode_step(r, m1)
+        else:
+            cdc = O.Codec({"sign1bit": O.SIGN1, "quant2bit": O.QUANT2}.get(codec, O.QUANT2))
+            snd = O.Channel(O.WITH_FEEDBACK, 1, np.zeros((n, cols), np.float32))
+            rcv = [O.Channel(O.WITH_FEEDBACK, 1, np.zeros((n, cols), np.float32)) for _ in range(peers)]
+            t0 = O.send(snd, x0, cdc)
+            for r in rcv:
+                O.receive(r, 1, True, O.RAW, t0[1], O.Codec(O.RAW))
+
+            def unit():
+                tg, body, _ = O.send(snd, x1, cdc)
+                for r in rcv:
+                    O.receive(r, 2, False, tg, body, cdc)
+        gate.wait()
+        start = time.perf_counter()
+        unit()
+        conn.send((start, time.perf_counter()))
 
 
-def cpu_measure(rows, cols, world, codec, threads, units):
-    """`units` independent rank-layer-steps on `threads` host threads; returns
-    (activation GB/s, timed wall seconds).  Each unit rebuilds the full
-    [rows, cols] activation once (own shard + world-1 peers)."""
-    import threading
+class CpuPath:
+    """`procs` persistent host processes (spawned, one per core, single-threaded
+    numpy) running the CPU path concurrently; perf_counter is CLOCK_MONOTONIC, so
+    spans from different processes share one time base."""
 
-    units = min(units, threads)
-    gate = threading.Barrier(units)
-    with cf.ThreadPoolExecutor(max_workers=units) as ex:
-        spans = list(ex.map(lambda i: _cpu_unit(rows, cols, world, codec, 17 + i, gate), range(units)))
-    wall = max(e for _, e in spans) - min(s for s, _ in spans)
-    return units * 2 * rows * cols / wall / 1e9, wall
+    def __init__(self, procs):
+        import multiprocessing as mp
+
+        from oracle.build_ref import import_reference
+
+        self.impl = "reference" if import_reference() is not None else "port"
+        ctx = mp.get_context("spawn")
+        self.procs = procs
+        self.gate = ctx.Barrier(procs)
+        self.conns, self.workers = [], []
+        for _ in range(procs):
+            parent, child = ctx.Pipe()
+            w = ctx.Process(target=_cpu_worker, args=(child, self.gate, self.impl), daemon=True)
+            w.start()
+            self.conns.append(parent)
+            self.workers.append(w)
+
+    def measure(self, rows, cols, world, codec, seed=17):
+        """One step of `procs` concurrent rank-layer units: (activation GB/s, wall s)."""
+        for i, c in enumerate(self.conns):
+            c.send((rows, cols, world, codec, seed + i))
+        spans = [c.recv() for c in self.conns]
+        wall = max(e for _, e in spans) - min(s for s, _ in spans)
+        return self.procs * 2 * rows * cols / wall / 1e9, wall
+
+    def close(self):
+        for c in self.conns:
+            c.send(None)
+        for w in self.workers:
+            w.join(timeout=10)
+
+    def describe(self, rows, cols, world, codec, wall):
+        src = ("oracle/_ref: the unmodified reference package (compactcomm.pipeline.encode_step / decode_step)"
+               if self.impl == "reference" else "oracle/cc_oracle.py numpy restatement of pipeline.encode_step/decode_step")
+        work = (f"encode_step own [{rows // world},{cols}] shard + {world - 1} peer decode_step" if world > 1
+                else f"encode_step + loopback decode_step [{rows},{cols}]")
+        return (f"{self.procs} concurrent rank-layer units ({work}, {codec} residual+EF) on {self.procs} "
+                f"single-threaded host processes, {wall:.2f} s wall per step; {src}")
 
 
 def run_reference(a, world, rank):
-    """Reference arm: the CPU implementation of the path (numpy oracle port of
-    pipeline.encode_step / decode_step) on all host threads."""
+    """Reference arm: the reference's CPU path on the host cores (rank 0 only)."""
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    for _ in range(a.warmup):
-        cpu_measure(a.rows, a.cols, world, a.codec, threads, threads)
-    walls = []
-    for _ in range(a.steps):
-        _, w = cpu_measure(a.rows, a.cols, world, a.codec, threads, threads)
-        walls.append(w)
-    ms = sum(walls) / len(walls) * 1e3
-    value = threads * 2 * a.rows * a.cols / (ms / 1e3) / 1e9
+    procs = a.cpu_procs or os.cpu_count() or 1
+    cpu = CpuPath(procs)
+    try:
+        for _ in range(a.warmup):
+            cpu.measure(a.rows, a.cols, world, a.codec)
+        walls = [cpu.measure(a.rows, a.cols, world, a.codec)[1] for _ in range(a.steps)]
+    finally:
+        cpu.close()
+    ms = statistics.mean(walls) * 1e3
+    value = procs * 2 * a.rows * a.cols / (ms / 1e3) / 1e9
     line = {
-        "impl": "reference", "metric": "activation GB/s compressed+reconstructed per GPU",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic FLUX-like activations",
-        "config": {"workload": f"patch-parallel {a.codec} residual+EF, [{a.rows},{a.cols}] activation, "
-                               f"world_size={world}: per rank-layer-step encode_step(own shard) + "
-                               f"{max(0, world - 1) or 1} decode_step (peer shards / loopback receiver)",
-                   "codec": a.codec, "parallelism": f"patch{world}"},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"{threads} rank-layer-steps per step, one per host thread "
-                                   f"(oracle/cc_oracle.py numpy restatement of pipeline.encode_step/decode_step)"},
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic FLUX-like activations (log-normal token x channel "
+                                                     "scales, 10% step drift)",
+        "config": bench_config(a, world),
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": procs, "kind": cpu.impl,
+                         "sample": cpu.describe(a.rows, a.cols, world, a.codec, statistics.mean(walls))},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -300,51 +401,47 @@ def run_b200(a, world, rank):
     streams = make_exchanges()
     inputs = [flux_inputs(rows, cols, lo, hi, layer, dev) for layer in range(L)]
 
-    # instrumentation: K1 / K2 events per (step, layer)
-    def one_step(s, ev=None, skip_comm=False):
+    def one_step(par, skip_comm=False, k1=None, k2=None):
         for layer, e in enumerate(exs):
-            # K1 events are recorded by the exchange itself around the encode, on the
-            # compute stream (the stream K1 is launched on)
-            e.step(inputs[layer][s % 2], skip_comm=skip_comm, k1_events=None if ev is None else ev[layer])
+            e.step(inputs[layer][par], skip_comm=skip_comm, k1_events=None if k1 is None else k1[layer],
+                   k2_events=None if k2 is None else k2[layer])
 
-    # protocol warmup (raw) step + bench warmups
-    one_step(0)
-    for s in range(a.warmup):
-        one_step(s + 1)
-    barrier(world)
+    def warm_up():
+        one_step(0)  # protocol warmup (raw) step
+        for s in range(a.warmup):
+            one_step((s + 1) % 2)
+        barrier(world)
 
-    K = a.steps
-    # per-kernel timing pass (events around every K1 on its stream; not the headline).
-    # A spin kernel queued first keeps the GPU busy while Python enqueues the step, so
-    # the events bracket GPU execution only (no host launch gaps inside the intervals).
-    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(L)]
-           for _ in range(K)]
-    spin_cycles = int(2.0e9 * 0.001 * L)  # ~1 ms of host enqueue time per layer, generously
-    for s in range(K):
-        with torch.cuda.stream(streams.compute):
-            torch.cuda._sleep(spin_cycles)
-        one_step(a.warmup + 1 + s, ev=evs[s])
-    streams.compute.wait_stream(streams.decode)
-    barrier(world)
-    k1_ms = statistics.mean(evs[s][l][0].elapsed_time(evs[s][l][1]) for s in range(K) for l in range(L))
+    warm_up()
 
+    def tev():
+        # external: recorded as event nodes inside a CUDA-graph capture, so they time
+        # the kernels of every replay
+        return torch.cuda.Event(enable_timing=True, external=True)
+
+    k1ev = [[(tev(), tev()) for _ in range(L)] for _ in range(2)]
+    k2ev = [[(tev(), tev()) for _ in range(L)] for _ in range(2)]
     graphs = None
     if not a.no_graph:
-        # steady state reached: capture one step per input parity and replay it
+        def capture(fn):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+                if os.environ.get("CC_BENCH_FAIL_CAPTURE"):  # exercises the eager fallback
+                    raise RuntimeError("forced capture failure")
+                torch.cuda.current_stream().wait_stream(streams.decode)
+            return g
+
         try:
-            graphs = []
-            for par in (0, 1):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    one_step(par)
-                    if os.environ.get("CC_BENCH_FAIL_CAPTURE"):  # exercises the eager fallback
-                        raise RuntimeError("forced capture failure")
-                    torch.cuda.current_stream().wait_stream(streams.decode)
-                graphs.append(g)
+            graphs = {"main": [capture(lambda p=p: one_step(p)) for p in (0, 1)],
+                      "timed": [capture(lambda p=p: one_step(p, k1=k1ev[p], k2=k2ev[p])) for p in (0, 1)]}
+            if world > 1:
+                graphs["nocomm"] = [capture(lambda p=p: one_step(p, skip_comm=True)) for p in (0, 1)]
             for e in exs:
                 e.after_capture()
-            for par in (0, 1):
-                graphs[par].replay()
+            for gs in graphs.values():
+                for g in gs:
+                    g.replay()
             barrier(world)
         except Exception as exc:  # e.g. a collective that cannot be captured: measure eagerly
             print(f"bench: CUDA-graph capture failed ({type(exc).__name__}: {exc}); timing eager launches",
@@ -352,69 +449,79 @@ def run_b200(a, world, rank):
             graphs = None
             torch.cuda.synchronize()
             streams = make_exchanges()  # host step counters advanced inside the failed capture
-            one_step(0)
-            for s in range(a.warmup):
-                one_step(s + 1)
-            barrier(world)
+            warm_up()
+
+    def run(kind, steps):
+        for s in range(steps):
+            if graphs is not None:
+                graphs[kind][s % 2].replay()
+            elif kind == "main":
+                one_step(s % 2)
+            elif kind == "nocomm":
+                one_step(s % 2, skip_comm=True)
+            else:
+                one_step(s % 2, k1=k1ev[s % 2], k2=k2ev[s % 2])
+
+    K = a.steps
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n0 = lib.cc_launch_count()
     with ClockSampler(torch.cuda.current_device()) as clk:
         barrier(world)
         start.record(streams.compute)
-        for s in range(K):
-            if graphs is not None:
-                graphs[s % 2].replay()
-            else:
-                one_step(s + 1)
+        run("main", K)
         streams.compute.wait_stream(streams.decode)
         end.record(streams.compute)
         barrier(world)
-    launches = lib.cc_launch_count() - n0
-    if graphs is not None:  # kernels inside the graphs: count one captured step per replay
-        n1 = lib.cc_launch_count()
-        one_step(0)
+    ms = max_over_ranks(start.elapsed_time(end) / K, world)
+    # kernels launched inside the timed region: one captured step's launches per replay
+    n1 = lib.cc_launch_count()
+    one_step(0)
+    barrier(world)
+    launches = (lib.cc_launch_count() - n1) * K
+
+    # per-kernel durations: events recorded inside the replayed graphs around every
+    # K1 (compute stream) and K2 (decode stream); read after each replay
+    k1s, k2s = [], []
+    for s in range(K):
+        run("timed", 1) if graphs is None else graphs["timed"][s % 2].replay()
         torch.cuda.synchronize()
-        launches = (lib.cc_launch_count() - n1) * K
-    ms = start.elapsed_time(end) / K
-    ms = max_over_ranks(ms, world)
-    used_graph = graphs is not None
+        k1s += [b.elapsed_time(e) for b, e in k1ev[s % 2]]
+        k2s += [b.elapsed_time(e) for b, e in k2ev[s % 2]]
+    k1_ms, k2_ms = statistics.mean(k1s), statistics.mean(k2s)
+    barrier(world)
+
     act_bytes = L * 2 * rows * cols
     value = world * act_bytes / (ms / 1e3) / 1e9
 
-    # K2 alone (decode stream serialised after K1) for the roofline breakdown
-    k2_ms = measure_k2(exs, streams, world)
-
-    # exposed comm: same step without the collective
-    exposed_us = None
-    bf16_ag_us = None
+    exposed_us = bf16_ag = comp_ag = None
     if world > 1:
-        barrier(world)
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(world)
         t0.record(streams.compute)
-        for s in range(K):
-            one_step(K + 1 + s, skip_comm=True)
+        run("nocomm", K)
         streams.compute.wait_stream(streams.decode)
         t1.record(streams.compute)
         barrier(world)
         ms_nc = max_over_ranks(t0.elapsed_time(t1) / K, world)
         exposed_us = max(0.0, (ms - ms_nc)) * 1e3 / L
-        bf16_ag_us = bf16_allgather_us(rows, cols, world, L, K)
+        bf16_ag = allgather_us(n_own * cols * 2, world, L, K)
+        comp_ag = allgather_us(exs[0].wire_bytes(False, False), world, L, K)
 
     bits = BITS[a.codec]
     s_own = n_own * cols
     k1_bytes = s_own * (18 + bits / 8) + 4 * (n_own + cols)
+    n_peer_elems = (rows - n_own) * cols if world > 1 else rows * cols
+    k2_bytes = n_peer_elems * (8 + bits / 8)
+    path_bytes = k1_bytes + k2_bytes
     peaks = json.load(open(MEASURED)) if os.path.exists(MEASURED) else {}
-    peak = peaks.get("hbm_gbs", 6650.0)
+    peak = peaks.get("hbm_gbs", 7672.0)
     k1_gbs = k1_bytes / (k1_ms / 1e3) / 1e9
     traffic = None
     if os.path.exists(TRAFFIC):
         tr = json.load(open(TRAFFIC))
-        traffic = tr.get(f"{a.codec}_{world}") or tr.get(a.codec)
-    n_peer_elems = (rows - n_own) * cols if world > 1 else rows * cols
-    k2_bytes = n_peer_elems * (8 + bits / 8)
-    path_bytes = k1_bytes + k2_bytes
+        traffic = tr.get(f"{a.codec}_{world}")
 
-    e2e = None if a.no_e2e else measure_e2e(exs, inputs, streams, world, K, L, rows, cols, lo, hi, dev)
+    consistency = check_consistency(exs, inputs, world)
+    e2e = None if a.no_e2e else measure_e2e(exs, inputs, streams, world, K, L, rows, cols)
     sim = None
     if world == 1 and not a.no_sim:
         del graphs
@@ -425,37 +532,42 @@ def run_b200(a, world, rank):
         sim["lowrank_r8_patch4"] = sim_rank_measure("patch", 4, "lowrank", 8, rows, cols, steps=3, warmup=2,
                                                     spec_kw={"rank": 8, "iterations": 2}, graph=False)
     cpu = None
-    if not a.no_cpu and rank == 0 and world == 1:
-        threads = min(os.cpu_count() or 1, 16)
-        v, wall = cpu_measure(rows, cols, world, a.codec, threads, threads)
-        cpu = {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
-               "sample": f"{threads} layer-steps (encode_step + decode_step, [{rows},{cols}] 2-bit residual+EF) "
-                         f"on {threads} threads, {wall:.1f} s wall; oracle/cc_oracle.py numpy port"}
+    if not a.no_cpu and rank == 0:
+        procs = a.cpu_procs or min(os.cpu_count() or 1, 16)
+        cp = CpuPath(procs)
+        try:
+            v, wall = cp.measure(rows, cols, world, a.codec)
+        finally:
+            cp.close()
+        cpu = {"value": v, "unit": "GB/s", "cores": procs, "kind": cp.impl,
+               "sample": cp.describe(rows, cols, world, a.codec, wall)}
+    barrier(world)
 
     line = {
-        "metric": "activation GB/s compressed+reconstructed per GPU",
+        "metric": METRIC,
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": a.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic FLUX-like activations (log-normal token x channel scales, 10% step drift)",
-        "config": {"workload": ("FLUX.1 [4096x3072] 2-bit residual+EF patch-parallel exchange, "
-                                f"{L} layer channels per step" + (" (world_size=1: sender + loopback receiver, "
-                                                                  "BASELINE config 1)" if world == 1 else "")),
-                   "codec": a.codec, "layers": L, "rows": rows, "cols": cols, "shard_rows": n_own,
-                   "parallelism": f"patch{world}", "topology": a.topology, "l2": "per-step working set >> 126 MB L2 (no flush needed)",
-                   "overlap": overlap, "cuda_graph": used_graph},
+        "config": bench_config(a, world),
+        "value_is": "aggregate over ranks: every rank reconstructs the full activation per layer (per_gpu_gbs x n_gpus)",
         "per_gpu_gbs": value / world,
         "exposed_comm_us_per_layer": exposed_us,
-        "bf16_allgather_us_per_layer": bf16_ag_us,
+        "bf16_allgather_us_per_layer": bf16_ag,
+        "compressed_allgather_us_per_layer": comp_ag,
+        "run": {"overlap": overlap, "cuda_graph": graphs is not None},
         "kernels": {"k1_encode_ms": k1_ms, "k1_gbs": k1_gbs, "k2_decode_ms": k2_ms,
-                    "k2_gbs": (k2_bytes / (k2_ms / 1e3) / 1e9) if k2_ms else None,
-                    "path_ideal_ms_per_layer": path_bytes / (peak * 1e9) * 1e3},
+                    "k2_gbs": k2_bytes / (k2_ms / 1e3) / 1e9, "k2_frac": k2_bytes / (k2_ms / 1e3) / 1e9 / peak,
+                    "timing": "CUDA events recorded inside the replayed graph around every K1 / K2 launch",
+                    "path_ideal_ms_per_layer": path_bytes / (peak * 1e9) * 1e3,
+                    "path_frac": (path_bytes / (peak * 1e9) * 1e3) / (ms / L)},
         "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s", "frac": k1_gbs / peak,
-                     "traffic": traffic, "kernel": "K1 encode_step (k1_fused: persistent residual -> scales -> quantize/pack -> state update)",
+                     "traffic": traffic, "kernel": "K1 encode_step (k1_fused: residual -> scales -> quantize/pack -> state update)",
                      "algorithmic_bytes_per_launch": k1_bytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs"
-                     if "hbm_gbs" in peaks else "fallback 6.65 TB/s"},
+                     if "hbm_gbs" in peaks else "B200_PROFILING.md fallback"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "consistency": consistency,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "per_rank_sim": sim,
@@ -464,54 +576,59 @@ def run_b200(a, world, rank):
         print(json.dumps(line), flush=True)
 
 
-def measure_k2(exs, streams, world):
-    """Average K2 (batched peer decode / loopback decode) duration, serialised."""
-    import torch
-
-    from paper_2507_17511_b200 import _lib
-
-    e = exs[0]
-    torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = min(len(exs), 20)
-    # decode the last body again into a scratch base so state is untouched
-    lib = _lib.load()
-    import ctypes
-
-    if world == 1:
-        tag = _lib.CC_QUANT2 if e.codec.kind == "quant2bit" else _lib.CC_SIGN1 if e.codec.kind == "sign1bit" else _lib.CC_QUANT4
-        scratch = [torch.zeros_like(x.loop_base) for x in exs[:reps]]
-        with torch.cuda.stream(streams.decode):
-            t0.record()
-            for i in range(reps):
-                _lib.check(lib.cc_decode_step(tag, 1, e.rows, e.cols, 0, ctypes.c_void_p(exs[i].sendbuf.data_ptr()),
-                                              _lib.CC_F32, ctypes.c_void_p(scratch[i].data_ptr()), _lib.stream_ptr()))
-            t1.record()
-        torch.cuda.synchronize()
-        return t0.elapsed_time(t1) / reps
-    return None
-
-
-def bf16_allgather_us(rows, cols, world, L, K):
+def check_consistency(exs, inputs, world):
+    """Outside the timed region: two more eager steps; every rank's blake2b digest
+    of the full reconstruction must agree (mesh.py:237, 320-324), and at world 1 the
+    loopback receiver must mirror the sender bit for bit (pipeline.py:193-194)."""
     import torch
     import torch.distributed as dist
 
-    n = rows // world
-    src = torch.randn(n, cols, device="cuda").to(torch.bfloat16)
-    dst = torch.empty(world * n, cols, device="cuda", dtype=torch.bfloat16)
+    L = len(exs)
+    layers = sorted({0, L // 2, L - 1})
+    agree, checks = True, 0
+    for s in range(2):
+        for layer, e in enumerate(exs):
+            e.step(inputs[layer][s])
+        torch.cuda.synchronize()
+        digs = [exs[i].digest() for i in layers]
+        if world > 1:
+            allv = [None] * world
+            dist.all_gather_object(allv, digs)
+            agree &= all(v == allv[0] for v in allv)
+        else:
+            agree &= all(torch.equal(exs[i].loop_base, exs[i].sender.base) for i in layers)
+        checks += len(layers)
+    return {"digests_agree" if world > 1 else "receiver_mirrors_sender": bool(agree), "layer_steps_checked": checks}
+
+
+def allgather_us(nbytes, world, L, K):
+    """µs per layer of L back-to-back NCCL all-gathers of `nbytes` per rank,
+    replayed from a CUDA graph (the bf16 baseline the compression replaces, or the
+    compressed bodies alone)."""
+    import torch
+    import torch.distributed as dist
+
+    src = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    dst = torch.empty(world * nbytes, dtype=torch.uint8, device="cuda")
     for _ in range(3):
         dist.all_gather_into_tensor(dst, src)
     barrier(world)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(L):
+            dist.all_gather_into_tensor(dst, src)
+    g.replay()
+    barrier(world)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
-    for _ in range(K * L):
-        dist.all_gather_into_tensor(dst, src)
+    for _ in range(K):
+        g.replay()
     t1.record()
     barrier(world)
     return max_over_ranks(t0.elapsed_time(t1) * 1e3 / (K * L), world)
 
 
-def measure_e2e(exs, inputs, streams, world, K, L, rows, cols, lo, hi, dev):
+def measure_e2e(exs, inputs, streams, world, K, L, rows, cols):
     """Public API with HOST buffers: H2D of each layer's bf16 shard from pinned
     memory, exchange step, D2H of the packed body and the StepRecord."""
     import torch
@@ -521,7 +638,7 @@ def measure_e2e(exs, inputs, streams, world, K, L, rows, cols, lo, hi, dev):
     body_n = [e.sendbuf.numel() for e in exs]
     host_body = [torch.empty(n, dtype=torch.uint8).pin_memory() for n in body_n]
     host_rec = [torch.empty(2, dtype=torch.float64).pin_memory() for _ in exs]
-    copy = torch.cuda.Stream(dev)
+    copy = torch.cuda.Stream(exs[0].device)
     h2d = d2h = 0
     ev_in = [torch.cuda.Event() for _ in exs]
 
@@ -543,18 +660,16 @@ def measure_e2e(exs, inputs, streams, world, K, L, rows, cols, lo, hi, dev):
             d2h += nb + 16
         streams.compute.wait_stream(streams.decode)
 
-    base_s = exs[0].sender.step
     for s in range(2):
-        step(base_s + s)
+        step(s)
     barrier(world)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(streams.compute)
     for s in range(K):
-        step(base_s + 2 + s)
+        step(s)
     t1.record(streams.compute)
     barrier(world)
     ms = max_over_ranks(t0.elapsed_time(t1) / K, world)
-    # bytes actually needed on the wire for the body = codec body size
     value = world * L * 2 * rows * cols / (ms / 1e3) / 1e9
     return {"value": value, "unit": "GB/s", "ms_per_step": ms, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h}
@@ -570,9 +685,8 @@ def sim_rank_measure(kind, P, codec, L, rows, cols, steps=5, warmup=3, spec_kw=N
     import torch
 
     from paper_2507_17511_b200 import compressors as cx
-    from paper_2507_17511_b200.comm import PatchParallelExchange, UlyssesAllToAll, shard_bounds
-
     from paper_2507_17511_b200 import linalg as la
+    from paper_2507_17511_b200.comm import PatchParallelExchange, UlyssesAllToAll, shard_bounds
 
     dev = torch.device("cuda", torch.cuda.current_device())
     spec = cx.CompressorSpec(cx.CompressorKind(codec), **(spec_kw or {}))
@@ -634,17 +748,22 @@ def sim_rank_measure(kind, P, codec, L, rows, cols, steps=5, warmup=3, spec_kw=N
 def main():
     a = parse()
     if a.impl == "reference":
-        world = int(os.environ.get("WORLD_SIZE", "1"))
+        world = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
         rank = int(os.environ.get("RANK", "0"))
         run_reference(a, world, rank)
-        return
+        return 0
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(a)
     world, rank = dist_setup()
+    if world != a.gpus:
+        print(f"bench: --gpus {a.gpus} but WORLD_SIZE={world}; measuring {world} ranks", file=sys.stderr, flush=True)
     run_b200(a, world, rank)
     if world > 1:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

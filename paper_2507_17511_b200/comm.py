@@ -211,6 +211,60 @@ def _dist():
     return dist
 
 
+def _backend(group):
+    dist = _dist()
+    try:
+        return dist.get_backend(group)
+    except Exception:
+        return None
+
+
+def all_gather_flat(out, inp, group=None):
+    """all_gather_into_tensor of equal-size byte slots.  NCCL moves device memory
+    directly; a gloo group (multi-process tests that share one GPU, or CPU runs)
+    carries CUDA tensors through host staging on the current stream."""
+    dist = _dist()
+    if inp.is_cuda and _backend(group) == "gloo":
+        o = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(o, inp.cpu(), group=group)
+        out.copy_(o)
+        return
+    dist.all_gather_into_tensor(out, inp, group=group)
+
+
+def all_to_all_flat(out, inp, group=None):
+    """all_to_all_single with equal splits (see all_gather_flat for gloo)."""
+    dist = _dist()
+    if inp.is_cuda and _backend(group) == "gloo":
+        o = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(o, inp.cpu(), group=group)
+        out.copy_(o)
+        return
+    dist.all_to_all_single(out, inp, group=group)
+
+
+def sendrecv(send, dst, recv, src, group=None):
+    """One ring hop: send `send` to dst while receiving `recv` from src."""
+    dist = _dist()
+    if send.is_cuda and _backend(group) == "gloo":
+        hs, hr = send.cpu(), torch.empty(recv.shape, dtype=recv.dtype)
+        ops = [dist.P2POp(dist.isend, hs, dst, group=group), dist.P2POp(dist.irecv, hr, src, group=group)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        recv.copy_(hr)
+        return
+    ops = [dist.P2POp(dist.isend, send, dst, group=group), dist.P2POp(dist.irecv, recv, src, group=group)]
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+
+
+def _check_dtype(x, in_dtype):
+    """Send buffers are sized for raw (warmup) bodies of `in_dtype`; a wider input
+    would overrun them."""
+    if x.dtype != in_dtype:
+        raise ValueError(f"input dtype {x.dtype} != the exchange's in_dtype {in_dtype}")
+
+
 def _receiver_accumulate(codec, mode, canon_pending):
     if mode == pl.PipelineMode.NAIVE:
         return 0
@@ -299,11 +353,13 @@ class PatchParallelExchange:
         return (per + 15) // 16 * 16
 
     # -- one step ---------------------------------------------------------------
-    def step(self, x_shard, rng=None, skip_comm=False, k1_events=None):
+    def step(self, x_shard, rng=None, skip_comm=False, k1_events=None, k2_events=None):
         """Returns the reconstruction tensor (on GPU: valid on the decode stream).
-        k1_events: optional (start, end) CUDA events recorded around the encode
-        (K1) on the compute stream, for per-kernel timing."""
+        k1_events / k2_events: optional (start, end) CUDA events recorded around the
+        encode (K1, compute stream) / the peer decode (K2, decode stream), for
+        per-kernel timing (also inside a CUDA-graph capture, with external events)."""
         S = self.streams
+        _check_dtype(x_shard, self.in_dtype)
         t = self.sender.step + 1
         warm = t <= self.warmup or cx.CompressorKind(self.codec.kind) == cx.CompressorKind.IDENTITY
         with _on(S.compute):
@@ -334,16 +390,20 @@ class PatchParallelExchange:
                         for p in self.peers:
                             slots[p].copy_(self.sendbuf[:per])
                 else:
-                    _dist().all_gather_into_tensor(self.recvflat[:self.P * per], self.sendbuf[:per], group=self.group)
+                    all_gather_flat(self.recvflat[:self.P * per], self.sendbuf[:per], group=self.group)
                 self.comm_bytes = per * (self.P - 1)
             self.ev_gathered.record(S.comm)
         with _on(S.decode):
             if S.decode is not None:
                 self.ev_gathered.wait(S.decode)
+            if k2_events is not None:
+                k2_events[0].record(S.decode)
             if self.P == 1:
                 self._loopback_decode(t, warm, wire16, nbytes)
             else:
                 self._decode_peers(t, warm, wire16)
+            if k2_events is not None:
+                k2_events[1].record(S.decode)
             self.ev_decoded.record(S.decode)
         return self.full if self.P > 1 else self.loop_base
 
@@ -410,11 +470,11 @@ class RingExchange(PatchParallelExchange):
     def origin(rank, rnd, P):
         return (rank - rnd) % P
 
-    def step(self, x_shard, rng=None, skip_comm=False, k1_events=None):
+    def step(self, x_shard, rng=None, skip_comm=False, k1_events=None, k2_events=None):
         if self.P == 1 or self.sim:
-            return super().step(x_shard, rng=rng, skip_comm=skip_comm, k1_events=k1_events)
+            return super().step(x_shard, rng=rng, skip_comm=skip_comm, k1_events=k1_events, k2_events=k2_events)
         S = self.streams
-        dist = _dist()
+        _check_dtype(x_shard, self.in_dtype)
         t = self.sender.step + 1
         warm = t <= self.warmup or cx.CompressorKind(self.codec.kind) == cx.CompressorKind.IDENTITY
         with _on(S.compute):
@@ -442,10 +502,7 @@ class RingExchange(PatchParallelExchange):
                 if rnd == 1 and S.comm is not None:
                     self.ev_encoded.wait(S.comm)
                 if not skip_comm:
-                    ops = [dist.P2POp(dist.isend, carried, nxt, group=self.group),
-                           dist.P2POp(dist.irecv, recv, prv, group=self.group)]
-                    for w in dist.batch_isend_irecv(ops):
-                        w.wait()
+                    sendrecv(carried, nxt, recv, prv, group=self.group)
                 self.ev_hop[rnd - 1].record(S.comm)
             with _on(S.decode):
                 if S.decode is not None:
@@ -529,13 +586,18 @@ class UlyssesAllToAll:
         self.body = (self.body + 255) // 256 * 256
         self.sendbuf = torch.zeros(self.P, self.body, dtype=torch.uint8, device=self.device)
         self.recvbuf = torch.zeros(self.P, self.body, dtype=torch.uint8, device=self.device)
+        # packed wire staging (bodies shorter than the slot stride), allocated once
+        self.sendflat = torch.zeros(self.P * self.body, dtype=torch.uint8, device=self.device)
+        self.recvflat = torch.zeros(self.P * self.body, dtype=torch.uint8, device=self.device)
         self.streams = _Streams(self.device, overlap)
         self.ev_encoded, self.ev_gathered = _Event(self.cuda), _Event(self.cuda)
 
     def step(self, x_local, rng=None):
         S = self.streams
+        _check_dtype(x_local, self.in_dtype)
         t = self.senders[0].step + 1
-        warm = t <= self.warmup
+        # identity sends raw bodies every step, exactly like warmup (pl:89-97)
+        warm = t <= self.warmup or cx.CompressorKind(self.codec.kind) == cx.CompressorKind.IDENTITY
         with _on(S.compute):
             if self.segmented:
                 wire16 = self._encode_segmented(x_local, t, warm)
@@ -548,13 +610,19 @@ class UlyssesAllToAll:
         with _on(S.comm):
             if S.comm is not None:
                 self.ev_encoded.wait(S.comm)
-            send = self.sendbuf[:, :per]
             if self.P > 1 and not self.sim:
-                recv = torch.empty_like(send)
-                _dist().all_to_all_single(recv.view(-1), send.contiguous().view(-1), group=self.group)
+                # bodies are packed back to back at the step's wire size: slot d of the
+                # send / receive staging is [d * per, (d + 1) * per)
+                if per == self.body:
+                    all_to_all_flat(self.recvbuf.view(-1), self.sendbuf.view(-1), group=self.group)
+                else:
+                    sflat = self.sendflat[:self.P * per]
+                    sflat.view(self.P, per).copy_(self.sendbuf[:, :per])
+                    rflat = self.recvflat[:self.P * per]
+                    all_to_all_flat(rflat, sflat, group=self.group)
+                    self.recvbuf[:, :per].copy_(rflat.view(self.P, per))
             else:  # loopback / single-GPU stand-in: the body of chunk d lands in slot d
-                recv = send
-            self.recvbuf[:, :per].copy_(recv)
+                self.recvbuf[:, :per].copy_(self.sendbuf[:, :per])
             self.ev_gathered.record(S.comm)
         with _on(S.decode):
             if S.decode is not None:
@@ -597,11 +665,32 @@ class UlyssesAllToAll:
         else:
             tag = cx._spec_tag(self.codec)
             ws = cx.workspace(_lib.check(lib.cc_workspace_bytes(tag, self.n, self.C, 0)))
-            _lib.check(lib.cc_encode_step_segmented(
-                tag, mode, cx._SCALE_MODES[self.codec.scale_mode], self.n, self.C, self.P, _lib.ptr(x),
-                cx.dtype_code(x), _lib.ptr(self.base_full), _lib.ptr(aux), _lib.ptr(self.sendbuf), self.body,
-                _lib.ptr(ws), ws.numel(), _lib.ptr(self.rec_seg), stream), "segmented encode_step")
+            try:
+                _lib.check(lib.cc_encode_step_segmented(
+                    tag, mode, cx._SCALE_MODES[self.codec.scale_mode], self.n, self.C, self.P, _lib.ptr(x),
+                    cx.dtype_code(x), _lib.ptr(self.base_full), _lib.ptr(aux), _lib.ptr(self.sendbuf), self.body,
+                    _lib.ptr(ws), ws.numel(), _lib.ptr(self.rec_seg), stream), "segmented encode_step")
+            except _lib.CudaError:
+                # the persistent launch was refused (e.g. SMs held by another context):
+                # encode every chunk channel on contiguous copies of its column slice
+                # with the multi-kernel path — the same bytes, P launches instead of one
+                self._encode_chunks_copied(x, t)
             wire16 = False
         for st in self.senders:
             st.step = t
         return wire16
+
+    def _encode_chunks_copied(self, x, t):
+        for d, st in enumerate(self.senders):
+            sl = slice(d * self.cw, (d + 1) * self.cw)
+            tmp = pl.LayerState.__new__(pl.LayerState)
+            tmp.mode, tmp.warmup_steps, tmp.step, tmp._rec = self.mode, self.warmup, t - 1, None
+            tmp.base = st.base.contiguous()
+            tmp.feedback = st.feedback.contiguous() if st.feedback is not None else None
+            tmp.ref = st.ref.contiguous() if st.ref is not None else None
+            pl.encode_step(tmp, x[:, sl].contiguous(), self.codec, body_out=self.sendbuf[d])
+            st.base.copy_(tmp.base)
+            if st.feedback is not None:
+                st.feedback.copy_(tmp.feedback)
+            if st.ref is not None:
+                st.ref.copy_(tmp.ref)

@@ -698,7 +698,11 @@ def from_bytes(buf):
             if len(rest) < mask_bytes or (len(rest) - mask_bytes) % 2 or (len(rest) - mask_bytes) // 2 != blocks * n:
                 raise PayloadError("nmblock: truncated body")
             masks = np.frombuffer(rest, np.uint8, mask_bytes, 0)
-            if int(np.unpackbits(masks, count=blocks * m, bitorder="little").sum()) != blocks * n:
+            # every 1 x m block keeps exactly n entries: the device decoders place a block's
+            # values at block * n + local rank, so an uneven mask (which the reference would
+            # fill in global flat order, cx:672) must not reach them
+            bits = np.unpackbits(masks, count=blocks * m, bitorder="little")
+            if blocks and not np.all(bits.reshape(blocks, m).sum(axis=1) == n):
                 raise PayloadError("nmblock: mask popcount mismatch")
             return NMBlockPayload(rows, cols, dev(rest), n, m)
     except PayloadError:

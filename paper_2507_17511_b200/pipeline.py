@@ -115,6 +115,17 @@ class LayerState:
         return None
 
 
+def _body_slice(body_out, nbytes):
+    """The caller's body buffer cut to this step's body, or a fresh one.  A buffer
+    shorter than the body is refused before any launch (the kernels write
+    `nbytes` unconditionally)."""
+    if body_out is None:
+        return cx._empty_body(nbytes)
+    if body_out.numel() < nbytes:
+        raise ValueError(f"body buffer holds {body_out.numel()} bytes, this step's body needs {nbytes}")
+    return body_out[:nbytes]
+
+
 def _record_buffer():
     # every encode path writes both doubles, so no fill kernel is needed
     return torch.empty(2, dtype=torch.float64, device=cx._device())
@@ -144,7 +155,7 @@ def encode_step(state, a_star, codec, rng=None, body_out=None):
         # warmup / identity: raw tensor, base <- a*, fb <- 0 (pl:89-97)
         wire = torch.bfloat16 if x.dtype == torch.bfloat16 else torch.float32
         nbytes = rows * cols * (2 if wire == torch.bfloat16 else 4)
-        body = body_out[:nbytes] if body_out is not None else cx._empty_body(nbytes)
+        body = _body_slice(body_out, nbytes)
         _lib.check(lib.cc_warmup_step(mode, rows, cols, _lib.ptr(x), cx.dtype_code(x), _lib.ptr(state.base),
                                       _lib.ptr(aux), _lib.ptr(body), cx.dtype_code(x), _lib.ptr(rec), stream),
                    "warmup")
@@ -154,7 +165,7 @@ def encode_step(state, a_star, codec, rng=None, body_out=None):
         if kind == cx.CompressorKind.TOPK:
             k = cx.topk_count(rows, cols, codec.keep_fraction)
             nbytes = 6 * k
-            body = body_out[:nbytes] if body_out is not None else cx._empty_body(nbytes)
+            body = _body_slice(body_out, nbytes)
             ws = cx.workspace(_lib.check(lib.cc_workspace_bytes(_lib.CC_TOPK, rows, cols, k)), "topk")
             _lib.check(lib.cc_topk_encode_step(mode, rows, cols, k, _lib.ptr(x), cx.dtype_code(x),
                                                _lib.ptr(state.base), _lib.ptr(aux), _lib.ptr(body), _lib.ptr(ws),
@@ -163,7 +174,7 @@ def encode_step(state, a_star, codec, rng=None, body_out=None):
         elif kind == cx.CompressorKind.NM_BLOCK:
             n, m = codec.n, codec.m
             nbytes = cx.nm_body_bytes(rows, cols, n, m)
-            body = body_out[:nbytes] if body_out is not None else cx._empty_body(nbytes)
+            body = _body_slice(body_out, nbytes)
             ws = cx.workspace(_lib.check(lib.cc_workspace_bytes(_lib.CC_NMBLOCK, rows, cols, _lib.nm_param(n, m))),
                               "nm")
             _lib.check(lib.cc_nm_encode_step(mode, rows, cols, n, m, _lib.ptr(x), cx.dtype_code(x),
@@ -172,7 +183,7 @@ def encode_step(state, a_star, codec, rng=None, body_out=None):
             payload = cx.NMBlockPayload(rows, cols, body, n, m)
         elif tag is not None:
             nbytes = lib.cc_body_bytes(tag, rows, cols, 0)
-            body = body_out[:nbytes] if body_out is not None else cx._empty_body(nbytes)
+            body = _body_slice(body_out, nbytes)
             ws = cx.workspace(_lib.check(lib.cc_workspace_bytes(tag, rows, cols, 0)))
             _lib.check(lib.cc_encode_step(tag, mode, cx._SCALE_MODES[codec.scale_mode], rows, cols, _lib.ptr(x),
                                           cx.dtype_code(x), _lib.ptr(state.base), _lib.ptr(aux), _lib.ptr(body),
@@ -203,6 +214,7 @@ def _encode_step_generic(state, x, codec, rng, mode, aux, rec, body_out):
     else:
         raise NotImplementedError(f"codec {kind} not on the device path")
     if body_out is not None:
+        _body_slice(body_out, payload.body.numel())
         body_out[: payload.body.numel()].copy_(payload.body)
         payload.body = body_out[: payload.body.numel()]
     ws = cx.workspace(1 << 16, "apply")

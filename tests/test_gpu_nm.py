@@ -226,6 +226,15 @@ def test_nm_from_bytes_validation():  # cx:658-674
     bad[13] ^= 0x01  # flip one mask bit -> popcount mismatch
     with pytest.raises(cx.PayloadError):
         cx.from_bytes(bytes(bad))
+    # total popcount preserved but uneven per block: block 0 keeps 3, block 1 keeps 1
+    bad = bytearray(blob)
+    masks = np.unpackbits(np.frombuffer(bytes(bad[13:14]), np.uint8), bitorder="little")
+    b0, b1 = masks[:4].copy(), masks[4:8].copy()
+    b0[np.flatnonzero(b0 == 0)[0]] = 1
+    b1[np.flatnonzero(b1 == 1)[0]] = 0
+    bad[13] = int(np.packbits(np.concatenate([b0, b1]), bitorder="little")[0])
+    with pytest.raises(cx.PayloadError):
+        cx.from_bytes(bytes(bad))
 
 
 def test_nm_exchange_loopback():
