@@ -137,6 +137,8 @@ def body_bits(tag, n, c, rank=0, k=0, nm=(0, 0)):
         return n * c + 32 * (n + c)
     if tag == QUANT2:
         return 2 * n * c + 32 * (n + c)
+    if tag == 16:  # QUANT4 extension
+        return 4 * n * c + 32 * (n + c)
     if tag == LOWRANK:
         return 16 * rank * (n + c)
     if tag == LOWRANK4:
@@ -195,6 +197,80 @@ def quant2_decode(body, n, c):
     nb = -(-2 * n * c // 8)
     u, v = _split_scales(body, nb, n, c)
     lv = LEVELS_2BIT[unpack_crumbs(body[:nb], n * c)].reshape(n, c)
+    return (lv * _scale_grid(u, v)).astype(np.float32)
+
+
+# ---------------------------------------------------------------------------
+# Extensions north_star names that the reference does not have (SURVEY §0 gaps
+# 1 and 3): a 4-bit element quantizer and per-token-only / per-channel-only
+# scales.  The definitions below ARE the specification the CUDA path is tested
+# against (parity "defined by this repo", not pinned to reference code); they
+# follow the reference's 1/2-bit conventions wherever one exists:
+#   * scales in f64, stored f32 (cx:141-148): per_token u_i = rowmean_i|t|, v = 1;
+#     per_channel u = 1, v_j = colmean_j|t|; rank1 = the reference's (g-normalised,
+#     floored u, all-zero -> u = 1, v = 0);
+#   * 4-bit codes k = 0..15 at levels (k - 7.5)/2 (units of u_i v_j): the nearest
+#     level, ties toward the smaller magnitude (the 2-bit rule, cx:387-390), the
+#     sign from t < 0 (so -0.0 and a zero scale give +0.25, code 8 — the 2-bit
+#     zero-scale rule maps to code 2, +0.5); codes packed two per byte, low nibble
+#     first (the INT4 factor packing, cx:541-546), flat row-major, then u, v f32;
+#   * decode f32(level * u64 * v64), exact in f64 before the one rounding (as
+#     cx:237-242).
+# ---------------------------------------------------------------------------
+
+QUANT4 = 16  # CC_QUANT4 (include/compactcomm.h)
+SCALE_MODES = ("rank1", "per_token", "per_channel")
+
+
+def scales(t, scale_mode="rank1"):
+    if scale_mode == "rank1":
+        return rank1_scales(t)
+    mag = np.abs(np.asarray(t, dtype=np.float64))
+    n, c = mag.shape
+    if scale_mode == "per_token":
+        return mag.mean(axis=1).astype(np.float32), np.ones(c, np.float32)
+    if scale_mode == "per_channel":
+        return np.ones(n, np.float32), mag.mean(axis=0).astype(np.float32)
+    raise ValueError(scale_mode)
+
+
+def quant4_codes(t, u, v):
+    s = _scale_grid(u, v)
+    x = np.asarray(t, dtype=np.float64)
+    ax = np.abs(x)
+    m = np.zeros(x.shape, np.int64)
+    for k in range(1, 8):  # m = #{k in 1..7 : |x| > k s / 2}; k s / 2 is exact in f64
+        m += ax > (0.5 * k) * s
+    neg = np.asarray(t) < 0
+    codes = np.where(neg, 7 - m, 8 + m)
+    codes[s == 0.0] = 8
+    return codes.astype(np.uint8).ravel()
+
+
+LEVELS_4BIT = (np.arange(16, dtype=np.float64) - 7.5) * 0.5
+
+
+def code_bytes(tag, n, c):
+    bits = {SIGN1: 1, QUANT2: 2, QUANT4: 4}[tag]
+    return -(-bits * n * c // 8)
+
+
+def quant_body(t, tag, scale_mode="rank1"):
+    """Body of a 1/2/4-bit quantizer with any scale mode."""
+    u, v = scales(t, scale_mode)
+    if tag == SIGN1:
+        packed = pack_bits(sign_codes(t))
+    elif tag == QUANT2:
+        packed = pack_crumbs(quant2_codes(t, u, v))
+    else:
+        packed = pack_nibbles(quant4_codes(t, u, v))
+    return packed.tobytes() + _f32le(u) + _f32le(v)
+
+
+def quant4_decode(body, n, c):
+    nb = code_bytes(QUANT4, n, c)
+    u, v = _split_scales(body, nb, n, c)
+    lv = LEVELS_4BIT[unpack_nibbles(body[:nb], n * c)].reshape(n, c)
     return (lv * _scale_grid(u, v)).astype(np.float32)
 
 
@@ -355,23 +431,23 @@ def nm_decode(body, n, c, nn, m):
 
 @dataclass(frozen=True)
 class Codec:
-    """Mirror of CompressorSpec fields that shape a body (cx:80-100)."""
+    """Mirror of CompressorSpec fields that shape a body (cx:80-100); scale_mode
+    is the repo's extension (see quant_body)."""
 
     tag: int
     rank: int = 0
     iters: int = 1
     keep_fraction: float = 0.0
     nm: tuple = (0, 0)
+    scale_mode: str = "rank1"
 
 
 def encode_body(t, codec, rng=None):
     tag = codec.tag
     if tag == RAW:
         return _f32le(t)
-    if tag == SIGN1:
-        return sign1_body(t)
-    if tag == QUANT2:
-        return quant2_body(t)
+    if tag in (SIGN1, QUANT2, QUANT4):
+        return quant_body(t, tag, codec.scale_mode)
     if tag in (LOWRANK, LOWRANK4):
         return lowrank_body(t, codec.rank, codec.iters, rng, int4=(tag == LOWRANK4))
     if tag == TOPK:
@@ -389,6 +465,8 @@ def decode_body(body, codec, n, c):
         return sign1_decode(body, n, c)
     if tag == QUANT2:
         return quant2_decode(body, n, c)
+    if tag == QUANT4:
+        return quant4_decode(body, n, c)
     if tag in (LOWRANK, LOWRANK4):
         return lowrank_decode(body, n, c, codec.rank, tag == LOWRANK4)
     if tag == TOPK:

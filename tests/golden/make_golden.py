@@ -252,6 +252,25 @@ def build_digest_fixture(out):
     out["traj_digest"] = meta
 
 
+def build_config1_digest(out):
+    """BASELINE config 1 at full length: [4096, 3072], 2-bit, residual with feedback,
+    28 steps (warmup 1), sender + receiver (pl:168-199) — per-step digests of the
+    body, base and feedback.  Pins the benchmarked exchange path to the reference."""
+    r, c, steps, seed, warmup = 4096, 3072, 28, 35, 1
+    xs = synth.flux_like(r, c, steps, seed)
+    res = run_traj(xs, Q2, "residual_with_feedback", warmup)
+    out["config1_digest"] = [{
+        "key": "c4096x3072|quant2bit|28", "rows": r, "cols": c, "steps": steps, "seed": seed, "warmup": warmup,
+        "codec": "quant2bit", "mode": "residual_with_feedback",
+        "inputs_sha256": synth.digest(np.stack(xs)),
+        "body_sha256": [synth.digest(s["body"]) for s in res],
+        "base_sha256": [synth.digest(s["base"]) for s in res],
+        "fb_sha256": [synth.digest(s["fb"]) for s in res],
+        "records": [{"compression_error": s["rec"].compression_error, "delta_hat": s["rec"].delta_hat,
+                     "bits": s["rec"].bits} for s in res],
+    }]
+
+
 def build_topk_digest(out):
     """Top-k at a P=8-like shard: exact body digest (indices + f16 values)."""
     meta = []
@@ -288,6 +307,7 @@ def main():
     build_digest_fixture(out)
     build_topk_digest(out)
     build_lowrank_cases(out)
+    build_config1_digest(out)
     with open(os.path.join(HERE, "manifest.json"), "w") as f:
         json.dump(out, f, indent=1)
     print("wrote fixtures to", HERE)
