@@ -201,41 +201,9 @@ CC_API const char *cc_last_error(void);
 CC_API int cc_version(void);
 /* number of kernels this library launched since load (evidence counter) */
 CC_API int64_t cc_launch_count(void);
-/* encode-path selection for tests/benchmarks: -1 auto (persistent fused K1
- * when C % 1024 == 0 and aligned), 0 force the multi-kernel K1, 1 prefer fused */
-CC_API void cc_set_quant_path(int path);
-/* profiling only: stop the persistent K1 after phase 1 (scale partials) or
- * 2 (scales); 0 = full step.  Results are incomplete when != 0. */
-CC_API void cc_debug_fused_stop(int phase);
-/* profiling only: device buffer of [grid][8] u64 %globaltimer stamps written by
- * every CTA of the persistent K1 at its phase boundaries (NULL disables). */
-CC_API void cc_debug_fused_timer(void *dev_buf);
-/* profiling only: experiment bits of the persistent K1 (0 = production path; see
- * k1_fused.cu Params::policy: L2 hints, skipped math / stores, workspace control words,
- * forced phase-A evict_first fraction in bits 8..11) */
-CC_API void cc_debug_fused_policy(int policy);
-/* profiling only: phase-B end-game of the persistent K1: when fewer than mult x grid
- * tiles remain, a CTA keeps at most `keep` loaded tiles ahead of its consumers
- * (0, 0 = automatic) */
-CC_API void cc_debug_fused_tail(int mult, int keep);
-/* programmatic dependent launch for the encode (K1) / decode (K2) kernels: each
- * launches with programmatic stream serialization and waits for its predecessor's
- * completion (griddepcontrol.wait) before touching memory, so launch and prologue
- * overlap the previous kernel's tail.  Results are unchanged.  0 = off (default: measured
- * 2% slower in bench.py's graph replay at [4096, 3072]). */
-CC_API void cc_set_pdl(int enable);
-/* profiling only: phase-B ring depths of the persistent K1 (0 = automatic) */
-CC_API void cc_debug_fused_rings(int s_in, int s_out);
-/* profiling only: phase-A tile height (rows per row group) and ring depth of the
- * persistent K1 (0 = automatic) */
-CC_API void cc_debug_fused_phase_a(int rows_per_group, int stages);
-/* low-rank projections: 1 = tcgen05 tensor cores, 3xTF32 split (default),
- * 0 = f64-accumulating CUDA-core GEMMs (cross-check) */
-CC_API void cc_set_lowrank_backend(int backend);
-/* low-rank tcgen05 projections: operand staging — 2 (default) A Q TMA-staged (2-D tensor map)
- * and A^T Y register-staged, 1 both TMA-staged, 0 both register-staged; identical results.
- * waves: unused */
-CC_API void cc_debug_lowrank_tma(int enable, int waves);
+/* Test / profiling knobs (encode-path selection, K1 experiment switches, PDL,
+ * low-rank backends) are NOT part of this ABI: they are declared in the private
+ * header paper_2507_17511_b200/csrc/cc_debug.h. */
 
 #ifdef __cplusplus
 }

@@ -65,14 +65,18 @@ SIGNATURES = {
     "cc_set_pdl": (None, [_i32]),
     "cc_debug_fused_phase_a": (None, [_i32, _i32]),
     "cc_set_lowrank_backend": (None, [_i32]),
+    "cc_debug_k1_resident": (None, [_i32]),
+    "cc_debug_k1_resident_count": (_i64, []),
 }
+# private test / profiling knobs (csrc/cc_debug.h), not part of the public ABI
+DEBUG_HEADER = os.path.join(HERE, "csrc", "cc_debug.h")
 
 _LIB = None
 
 
-def header_symbols():
-    """Every CC_API function declared in include/compactcomm.h."""
-    with open(HEADER) as f:
+def header_symbols(path=None):
+    """Every CC_API function declared in include/compactcomm.h (or `path`)."""
+    with open(path or HEADER) as f:
         txt = f.read()
     return sorted(set(re.findall(r"CC_API\s+[\w\s\*]+?\b(cc_\w+)\s*\(", txt)))
 

@@ -12,6 +12,7 @@
 #include <unordered_map>
 
 #include "../../include/compactcomm.h"
+#include "cc_debug.h"
 #include "cc_internal.h"
 
 namespace cc {
@@ -126,6 +127,8 @@ void set_fused_tail(int mult, int keep);
 void set_fused_phase_a(int rows_per_tile, int stages);
 void set_lowrank_backend(int v);
 void set_tc_tma(int v, int waves);
+void set_resident_enabled(int on);
+int64_t resident_launches();
 int residual_target(int mode, int64_t n, int64_t C, const void *x, int x_dtype, const float *base, const float *aux,
                     float *t, cudaStream_t st);
 int apply_decoded(int mode, int64_t n, int64_t C, const void *x, int x_dtype, const float *t, const float *dec,
@@ -158,6 +161,8 @@ CC_API void cc_set_pdl(int enable) { g_pdl = enable ? 1 : 0; }
 CC_API void cc_debug_fused_phase_a(int rows_per_group, int stages) { set_fused_phase_a(rows_per_group, stages); }
 CC_API void cc_set_lowrank_backend(int backend) { set_lowrank_backend(backend); }
 CC_API void cc_debug_lowrank_tma(int enable, int waves) { set_tc_tma(enable, waves); }
+CC_API void cc_debug_k1_resident(int enable) { set_resident_enabled(enable); }
+CC_API int64_t cc_debug_k1_resident_count(void) { return resident_launches(); }
 
 CC_API int64_t cc_topk_count(int64_t rows, int64_t cols, double keep_fraction) {
   if (rows < 1 || cols < 1 || !(keep_fraction > 0.0 && keep_fraction <= 1.0)) return CC_ERR_ARG;

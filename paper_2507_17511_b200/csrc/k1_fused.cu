@@ -4,6 +4,8 @@
 
 namespace cc {
 
+int resident_encode(const fused::Params &fp, int codec, int mode, int x_dtype, cudaStream_t st);
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -151,6 +153,10 @@ int fused_encode_segments(int codec, int mode, int scale_mode, int64_t n, int64_
   if ((int64_t)off > ws_bytes) {
     set_error("fused workspace too small");
     return CC_ERR_ARG;
+  }
+  {  // shards whose rows fit on chip: the single-pass resident kernel (k1_resident.cu)
+    const int rc = resident_encode(p, codec, mode, x_dtype, st);
+    if (rc != CC_ERR_UNSUPPORTED) return rc;
   }
   if (nseg > 1) return fused_dispatch_seg(p, codec, mode, x_dtype, Q, st);
 #define CC_FUSED_Q(MODE, CODEC, XT) \

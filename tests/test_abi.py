@@ -18,6 +18,11 @@ def test_library_loads_and_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), f"missing export {s}"
     assert set(syms) <= set(_lib.SIGNATURES), "binding table out of date"
+    dbg = _lib.header_symbols(_lib.DEBUG_HEADER)
+    assert dbg and not set(dbg) & set(syms), "debug knobs belong to the private header only"
+    assert set(syms) | set(dbg) == set(_lib.SIGNATURES)
+    for s in dbg:
+        assert hasattr(lib, s), f"missing export {s}"
 
 
 def test_header_constants_match_binding():
