@@ -4,11 +4,17 @@
 // read from HBM exactly once and every result written once: 18 + b/8 B per
 // element, the algorithmic traffic of SURVEY §8(d).
 //
-// Used when the CTA's rows fit on chip: ceil(n / G) rows x (4 C [+ 4 C]) B next to
-// the input ring, e.g. the per-rank shards of patch parallelism at P >= 2
-// ([2048, 3072] t-resident, [1024 / 512, 3072] t + base resident) and the
-// Ulysses senders ([512, 3072] in 8 column segments).  Larger shards take the
-// streaming two-pass kernel (k1_fused_impl.cuh).
+// Used when the CTA's residual rows fit on chip.  t lives in shared memory and,
+// for rows beyond what shared memory holds, in TENSOR MEMORY (256 KB per SM,
+// otherwise idle in this kernel): every thread parks its 8 values of such a row in
+// its warp's TMEM lane quarter with tcgen05.st and takes them back with tcgen05.ld.
+// Shared + tensor memory hold ~58 MB of t across 148 SMs, so even the P = 1 shard
+// [4096, 3072] (50 MB) stays on chip: phase B re-reads only base (L2-resident,
+// loaded evict_last in phase A).  Per shape:
+//   [512 / 1024, 3072]  t + base in shared memory (no re-read at all);
+//   [2048, 3072]        t in shared memory, base re-read;
+//   [4096, 3072]        t in shared + tensor memory, base re-read.
+// Larger shards take the streaming two-pass kernel (k1_fused_impl.cuh).
 //
 // CTA c owns the contiguous rows [c n / G, (c + 1) n / G) (static: every CTA moves
 // the same bytes, so the phases end together without a tile scheduler).
@@ -40,10 +46,9 @@ namespace cc {
 namespace k1r {
 
 using fused::ColConst;
-using fused::kCons;
-using fused::kCW;
-constexpr int kThreads = kCons + 32;  // 12 consumer warps + 1 producer warp
+constexpr int kNQ = 1;                // column quads per consumer thread (see Geo)
 constexpr int kNB = fused::kNB;       // 128-column blocks per row (24 at C = 3072)
+constexpr int kMaxSlots = 148;        // column-partial slots read per column in phase F (grid <= SMs)
 constexpr int kMaxSeg = fused::kMaxSeg;
 constexpr int kMaxStages = 8;
 constexpr size_t kSmemMax = 227 * 1024;
@@ -54,9 +59,11 @@ struct Params {
   int64_t n, C;
   int G4, G;
   int R;          // max rows per CTA (ceil(n / G))
+  int nsm;        // rows whose t lives in shared memory; rows nsm.. live in tensor memory
   int keep_base;  // base rows resident (else streamed through the ring in both phases)
-  int S;          // ring stages
-  uint32_t stage_bytes, st_base;                            // ring stage: x at 0, base at st_base
+  int S;          // phase-A ring stages
+  int SB;         // phase-B base slots (carved from the phase-A ring area)
+  uint32_t stage_bytes, st_base, st_fb;                     // ring stage: x at 0, base, feedback (TMEM rows)
   uint32_t off_t, off_b, off_ring, off_rp, off_rs, off_u;   // shared-memory layout
   uint32_t off_bar, off_red;
   double *colpart, *blkpart, *recpart, *record;  // [G][C], [G][nseg], [G][nseg][2], [nseg][2]
@@ -66,6 +73,8 @@ struct Params {
   int nseg, cw, cbs, bps, cb_row;
   unsigned int *bar1, *bar2, *ticket;
   int scale_mode;
+  unsigned long long *timer;  // profiling: [G][16] %globaltimer stamps, or null
+  int policy;                 // experiments: L2 hints of the phase-A loads (0 = production)
 };
 
 template <typename XT>
@@ -73,15 +82,96 @@ __device__ __forceinline__ void ld_x4(const XT *p, float (&v)[4]) {
   fused::unpack_x(p, v);
 }
 
+// ---- tensor memory (tcgen05) as a residual store --------------------------------
+__device__ __forceinline__ void tmem_alloc512(uint32_t *dst_smem) {  // warp-collective
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(dst_smem))
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc512(uint32_t taddr) {  // warp-collective
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// each lane writes / reads 4 NQ consecutive 32-bit columns of its own TMEM lane
+template <int NQ>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const float (&v)[NQ][4]) {
+  if constexpr (NQ == 1) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[0][0])), "r"(__float_as_uint(v[0][1])), "r"(__float_as_uint(v[0][2])),
+                 "r"(__float_as_uint(v[0][3]))
+                 : "memory");
+  } else {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[0][0])), "r"(__float_as_uint(v[0][1])), "r"(__float_as_uint(v[0][2])),
+                 "r"(__float_as_uint(v[0][3])), "r"(__float_as_uint(v[NQ - 1][0])), "r"(__float_as_uint(v[NQ - 1][1])),
+                 "r"(__float_as_uint(v[NQ - 1][2])), "r"(__float_as_uint(v[NQ - 1][3]))
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+template <int NQ>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[NQ][4]) {
+  uint32_t r[8];
+  if constexpr (NQ == 1) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr)
+                 : "memory");
+  } else {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr)
+                 : "memory");
+  }
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < NQ; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[j][q] = __uint_as_float(r[4 * j + q]);
+}
+
 __device__ __forceinline__ void stcs4(float *p, const float (&v)[4]) {
   __stcs(reinterpret_cast<float4 *>(p), make_float4(v[0], v[1], v[2], v[3]));
 }
 
-template <int MODE, int CODEC, typename XT>
-__global__ void __launch_bounds__(kThreads, 1) k1_resident(const __grid_constant__ Params p) {
+// A ring position: stage index and the parity of its current use, advanced
+// incrementally (no runtime division in the loops).
+struct RingPos {
+  int s = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next(int S) {
+    if (++s == S) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+// NQ column quads per consumer thread: 768 / NQ consumer threads cover the 3072
+// columns of a full row (quad j of thread tid = quad tid + j CONS).  NQ = 1 (24
+// consumer warps) hides latency best; NQ = 2 (12 warps) is the register-light form.
+template <int NQ>
+struct Geo {
+  static constexpr int CONS = 768 / NQ;
+  static constexpr int CW = CONS / 32;
+  static constexpr int THREADS = CONS + 32;  // + producer warp
+};
+
+// TMEM address of a consumer warp's 4 NQ columns of tensor-memory row m: warp w
+// reaches lanes 32 (w % 4) .. + 31; the CW / 4 warps sharing a lane quarter take 4 NQ
+// columns each, so a row uses 24 of the 512 columns (<= 21 rows).
+template <int NQ>
+__device__ __forceinline__ uint32_t tmem_off(int warp, int m) {
+  return ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(m * 24 + (warp >> 2) * 4 * NQ);
+}
+
+template <int MODE, int CODEC, typename XT, int NQ>
+__global__ void __launch_bounds__(Geo<NQ>::THREADS, 1) k1_resident(const __grid_constant__ Params p) {
+  constexpr int CONS = Geo<NQ>::CONS, CW = Geo<NQ>::CW;
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int cta = blockIdx.x, G = p.G, S = p.S;
+  const int cta = blockIdx.x, G = p.G, S = p.S, SB = p.SB;
   const int64_t n = p.n, C = p.C;
   const int64_t r0 = (int64_t)cta * n / G, r1 = (int64_t)(cta + 1) * n / G;
   const int nr = (int)(r1 - r0);
@@ -91,57 +181,99 @@ __global__ void __launch_bounds__(kThreads, 1) k1_resident(const __grid_constant
   const bool keep_base = kAux && p.keep_base;
   const bool ring_base = kAux && !p.keep_base;  // base through the ring (phase A if kWB, phase B always)
 
-  float *tS = reinterpret_cast<float *>(smem + p.off_t);   // [R][C]
+  float *tS = reinterpret_cast<float *>(smem + p.off_t);   // [nsm][C]
   float *bS = reinterpret_cast<float *>(smem + p.off_b);   // [R][C] (keep_base)
-  uint8_t *ring = smem + p.off_ring;                        // [S][stage_bytes]
+  uint8_t *ring = smem + p.off_ring;                        // [S][stage_bytes] / [SB][4 C]
   double *rp = reinterpret_cast<double *>(smem + p.off_rp); // [R][kNB]
   double *rs = reinterpret_cast<double *>(smem + p.off_rs); // [R][nseg] row sums
   float *uS = reinterpret_cast<float *>(smem + p.off_u);    // [R][nseg]
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + p.off_bar);
   uint64_t *empty = full + kMaxStages;
-  double *red = reinterpret_cast<double *>(smem + p.off_red);  // [kCW * 2 * 2 * kMaxSeg]
+  uint64_t *fullB = empty + kMaxStages;  // phase-B base slots
+  uint64_t *emptyB = fullB + kMaxStages;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(emptyB + kMaxStages);
+  double *red = reinterpret_cast<double *>(smem + p.off_red);  // [CW][32]
+  const bool use_tmem = p.nsm < p.R;
 
+  auto stamp = [&](int i) {
+    if (p.timer && tid == 0) p.timer[(size_t)cta * 16 + i] = fused::gtimer();
+  };
+  stamp(0);
+  if (p.timer && tid == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.timer[(size_t)cta * 16 + 8] = smid;
+  }
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kCW);
+      mbar_init(&empty[s], CW);
+    }
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], CW);
     }
     mbar_fence_init();
   }
+  if (use_tmem && warp == 0) tmem_alloc512(tmem_slot);  // the whole TMEM: one CTA per SM
+  tc_fence_before();
   __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = use_tmem ? *tmem_slot : 0u;
   const XT *X = reinterpret_cast<const XT *>(p.x);
 
-  if (warp == kCW) {  // ===================== producer warp =====================
+  if (warp == CW) {  // ===================== producer warp =====================
     if (lane == 0) {
-      const uint64_t pol_once = l2_policy_evict_first();
-      const uint64_t pol_again = l2_policy_evict_last();  // base rows re-read in phase B
+      const uint64_t pol_once = (p.policy & 4) ? fused::l2_policy_normal() : l2_policy_evict_first();
+      // base rows are re-read in phase B, but keeping them L2-resident (evict_last)
+      // slows phase A more than the re-read costs: [4096, 3072] 62.6 us with
+      // evict_last, 60.5 us with evict_first (scripts/k1_ab.py --policies)
+      const uint64_t pol_again = (p.policy & 1)   ? fused::l2_policy_normal()
+                                 : (p.policy & 2) ? l2_policy_evict_last()
+                                                  : l2_policy_evict_first();
+      const uint64_t pol_b = (p.policy & 8) ? fused::l2_policy_normal() : l2_policy_evict_first();
       const uint32_t xb = (uint32_t)(C * sizeof(XT)), fb = (uint32_t)(C * 4);
-      // phase A: one ring use per row
-      for (int k = 0; k < nr; ++k) {
-        const int s = k % S;
-        if (k >= S) mbar_wait(&empty[s], (uint32_t)((k / S) - 1) & 1u);
-        const int64_t row = r0 + k;
-        uint8_t *st = ring + (size_t)s * p.stage_bytes;
-        uint32_t bytes = xb;
-        if (kAux) bytes += fb;
-        if (kWB || keep_base) bytes += fb;
-        mbar_expect_tx(&full[s], bytes);
-        bulk_g2s(st, X + row * C, xb, &full[s], pol_once);
-        if (kAux) bulk_g2s(tS + (size_t)k * C, p.aux + row * C, fb, &full[s], pol_once);
+      uint32_t bytes = xb;
+      if (kAux) bytes += fb;
+      if (kWB || keep_base) bytes += fb;
+      // phase A: one ring use per row.  Rows with t in shared memory take their aux
+      // straight into the t slot; rows with t in tensor memory stage it in the ring.
+      RingPos w;
+      for (int k = 0; k < nr; ++k, w.next(S)) {
+        if (k >= S) mbar_wait(&empty[w.s], w.ph ^ 1u);
+        const int64_t off = (r0 + k) * C;
+        uint8_t *st = ring + (size_t)w.s * p.stage_bytes;
+        mbar_expect_tx(&full[w.s], bytes);
+        bulk_g2s(st, X + off, xb, &full[w.s], pol_once);
+        if (kAux) {
+          float *dst = k < p.nsm ? tS + (size_t)k * C : reinterpret_cast<float *>(st + p.st_fb);
+          bulk_g2s(dst, p.aux + off, fb, &full[w.s], pol_once);
+        }
         if (keep_base) {
-          bulk_g2s(bS + (size_t)k * C, p.base + row * C, fb, &full[s], pol_once);
+          bulk_g2s(bS + (size_t)k * C, p.base + off, fb, &full[w.s], pol_once);
         } else if (kWB) {
-          bulk_g2s(st + p.st_base, p.base + row * C, fb, &full[s], pol_again);
+          bulk_g2s(st + p.st_base, p.base + off, fb, &full[w.s], pol_again);
         }
       }
-      // phase B: base rows through the ring (uses nr .. 2 nr - 1), loaded while the
-      // consumers wait on the hand-offs
+      // phase B: base rows through SB slots carved from the ring area, newest first
+      // (the most recently loaded base rows are the likeliest L2 hits), loaded while
+      // the consumers wait on the hand-offs
       if (ring_base) {
-        for (int k = 0; k < nr; ++k) {
-          const int u = nr + k, s = u % S;
-          if (u >= S) mbar_wait(&empty[s], (uint32_t)((u / S) - 1) & 1u);
-          mbar_expect_tx(&full[s], fb);
-          bulk_g2s(ring + (size_t)s * p.stage_bytes, p.base + (r0 + k) * C, fb, &full[s], pol_once);
+        // the ring area is free once phase A's last min(S, nr) uses are released
+        RingPos q = w;
+        for (int i = 0; i < min(S, nr); ++i) {
+          if (--q.s < 0) {
+            q.s = S - 1;
+            q.ph ^= 1u;
+          }
+          mbar_wait(&empty[q.s], q.ph);
+        }
+        RingPos b;
+        for (int i = 0; i < nr; ++i, b.next(SB)) {
+          const int k = nr - 1 - i;
+          if (i >= SB) mbar_wait(&emptyB[b.s], b.ph ^ 1u);
+          mbar_expect_tx(&fullB[b.s], fb);
+          bulk_g2s(ring + (size_t)b.s * fb, p.base + (r0 + k) * C, fb, &fullB[b.s], pol_b);
         }
       }
     }
@@ -149,99 +281,111 @@ __global__ void __launch_bounds__(kThreads, 1) k1_resident(const __grid_constant
   }
 
   // ===================== consumer warps =====================
-  // column quads: thread tid owns quads tid and tid + kCons (columns 4 q .. 4 q + 3)
-  bool qact[2];
-  int qcol[2], qblk[2], qseg[2];
+  bool qact[NQ];
+  int qcol[NQ], qblk[NQ], qseg[NQ];
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int qd = tid + j * kCons;
+  for (int j = 0; j < NQ; ++j) {
+    const int qd = tid + j * CONS;
     qact[j] = qd < p.G4;
     qcol[j] = 4 * qd;
-    qblk[j] = j * kCW + warp;  // 128-column block of the quad
+    qblk[j] = j * CW + warp;  // 128-column block of the quad
     qseg[j] = nseg == 1 ? 0 : min(qblk[j] / p.bps, nseg - 1);
   }
-  double cs[2][4];
+  double cs[NQ][4];
 #pragma unroll
-  for (int j = 0; j < 2; ++j) cs[j][0] = cs[j][1] = cs[j][2] = cs[j][3] = 0.0;
+  for (int j = 0; j < NQ; ++j) cs[j][0] = cs[j][1] = cs[j][2] = cs[j][3] = 0.0;
 
   // ---------------- phase A ----------------
-  for (int k = 0; k < nr; ++k) {
-    const int s = k % S;
-    mbar_wait(&full[s], (uint32_t)(k / S) & 1u);
-    const uint8_t *st = ring + (size_t)s * p.stage_bytes;
-    const XT *xs = reinterpret_cast<const XT *>(st);
-    float *trow = tS + (size_t)k * C;
-    const float *brow = keep_base ? bS + (size_t)k * C : reinterpret_cast<const float *>(st + p.st_base);
-    double rsum[2] = {0.0, 0.0};
+  {
+    RingPos w;
+    for (int k = 0; k < nr; ++k, w.next(S)) {
+      mbar_wait(&full[w.s], w.ph);
+      if (k == 0) stamp(1);
+      const uint8_t *st = ring + (size_t)w.s * p.stage_bytes;
+      const XT *xs = reinterpret_cast<const XT *>(st);
+      const bool in_smem = k < p.nsm;
+      float *trow = tS + (size_t)k * C;
+      const float *arow = in_smem ? trow : reinterpret_cast<const float *>(st + p.st_fb);
+      const float *brow = keep_base ? bS + (size_t)k * C : reinterpret_cast<const float *>(st + p.st_base);
+      float *refrow = p.aux + (r0 + k) * C;
+      double rsum[NQ];
+      float tt[NQ][4];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      if (!qact[j]) continue;
-      const int o = qcol[j];
-      float xx[4], bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f}, t[4];
-      ld_x4(xs + o, xx);
-      if constexpr (kWB) fused::unpack_f(brow + o, bb);
-      if constexpr (kAux) fused::unpack_f(trow + o, aa);
-      double a[4];
+      for (int j = 0; j < NQ; ++j) {
+        rsum[j] = 0.0;
+        tt[j][0] = tt[j][1] = tt[j][2] = tt[j][3] = 0.f;
+        if (!qact[j]) continue;
+        const int o = qcol[j];
+        float xx[4], bb[4] = {0.f, 0.f, 0.f, 0.f}, aa[4] = {0.f, 0.f, 0.f, 0.f};
+        ld_x4(xs + o, xx);
+        if constexpr (kWB) fused::unpack_f(brow + o, bb);
+        if constexpr (kAux) fused::unpack_f(arow + o, aa);
+        double a[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        t[q] = target_of<MODE>(xx[q], bb[q], aa[q]);
-        a[q] = fabs((double)t[q]);
-        cs[j][q] += a[q];
+        for (int q = 0; q < 4; ++q) {
+          tt[j][q] = target_of<MODE>(xx[q], bb[q], aa[q]);
+          a[q] = fabs((double)tt[j][q]);
+          cs[j][q] += a[q];
+        }
+        rsum[j] = ((a[0] + a[1]) + a[2]) + a[3];
+        if (in_smem) *reinterpret_cast<float4 *>(trow + o) = make_float4(tt[j][0], tt[j][1], tt[j][2], tt[j][3]);
+        if constexpr (MODE == CC_NO_FEEDBACK) stcs4(refrow + o, xx);  // ref' = a* (pl:113)
       }
-      rsum[j] = ((a[0] + a[1]) + a[2]) + a[3];
-      *reinterpret_cast<float4 *>(trow + o) = make_float4(t[0], t[1], t[2], t[3]);
-      if constexpr (MODE == CC_NO_FEEDBACK) stcs4(p.aux + (r0 + k) * C + o, xx);  // ref' = a* (pl:113)
-    }
+      if (!in_smem) tmem_st<NQ>(tmem + tmem_off<NQ>(warp, k - p.nsm), tt);  // warp-collective
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const double v = warp_sum(rsum[j]);
-      if (lane == 0 && qblk[j] < kNB) rp[(size_t)k * kNB + qblk[j]] = v;
+      for (int j = 0; j < NQ; ++j) {
+        const double v = warp_sum(rsum[j]);
+        if (lane == 0 && qblk[j] < kNB) rp[(size_t)k * kNB + qblk[j]] = v;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[w.s]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
   }
+  if (use_tmem) tmem_wait_st();
+  stamp(2);
   // column partials of this CTA
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
+  for (int j = 0; j < NQ; ++j) {
     if (!qact[j]) continue;
     double *cp = p.colpart + (int64_t)cta * C + qcol[j];
     cp[0] = cs[j][0]; cp[1] = cs[j][1]; cp[2] = cs[j][2]; cp[3] = cs[j][3];
   }
-  fused::named_sync(1, kCons);
+  fused::named_sync(1, CONS);
   // row sums per segment (blocks of the segment in order), then CTA totals
-  for (int i = tid; i < nr * nseg; i += kCons) {
-    const int k = i / nseg, d = i % nseg;
+  for (int i = tid; i < nr * nseg; i += CONS) {
+    const int k = i / nseg, d = i - k * nseg;
     double acc = 0.0;
     for (int b = 0; b < p.bps; ++b) acc += rp[(size_t)k * kNB + d * p.bps + b];
     rs[i] = acc;
   }
-  fused::named_sync(1, kCons);
+  fused::named_sync(1, CONS);
   if (tid < nseg) {
     double tot = 0.0;
     for (int k = 0; k < nr; ++k) tot += rs[k * nseg + tid];
     p.blkpart[(size_t)cta * nseg + tid] = tot;
   }
   // ---- hand-off 1 ----
-  fused::named_sync(1, kCons);
+  fused::named_sync(1, CONS);
   if (tid == 0) {
     fused::arrive_release(p.bar1);
     fused::spin_until(p.bar1, (unsigned)G);
   }
-  fused::named_sync(1, kCons);
+  fused::named_sync(1, CONS);
+  stamp(3);
 
   // ---------------- phase F ----------------
   {
-    double *wpart = red;  // [kCW][32]
+    double *wpart = red;  // [CW][32]
     for (int64_t grp32 = cta; grp32 * 32 < C; grp32 += G) {
       const int64_t j = grp32 * 32 + lane;
       double acc = 0.0;
       if (j < C) {
-        constexpr int kB = 16;
-        for (int s0 = warp; s0 < G; s0 += kB * kCW) {
+        constexpr int kB = (kMaxSlots + CW - 1) / CW;  // one L2 round trip for all G slots
+        for (int s0 = warp; s0 < G; s0 += kB * CW) {
           double vals[kB];
 #pragma unroll
           for (int q = 0; q < kB; ++q) {
-            const int slot = s0 + q * kCW;
+            const int slot = s0 + q * CW;
             vals[q] = slot < G ? __ldcg(p.colpart + (int64_t)slot * C + j) : 0.0;
           }
 #pragma unroll
@@ -249,33 +393,34 @@ __global__ void __launch_bounds__(kThreads, 1) k1_resident(const __grid_constant
         }
       }
       wpart[warp * 32 + lane] = acc;
-      fused::named_sync(1, kCons);
+      fused::named_sync(1, CONS);
       if (warp == 0 && j < C) {
         double sacc = 0.0;
-        for (int w = 0; w < kCW; ++w) sacc += wpart[w * 32 + lane];
+        for (int w = 0; w < CW; ++w) sacc += wpart[w * 32 + lane];
         float v = (float)(sacc / (double)n);  // colmean (cx:148)
         if (p.scale_mode == CC_SCALE_PER_TOKEN) v = 1.0f;
         p.v[j] = v;
         const int d = (int)(j / p.cw);
         store_f32_bytes(p.body + d * p.body_stride + p.cbytes_seg + 4 * n + 4 * (j - (int64_t)d * p.cw), v);
       }
-      fused::named_sync(1, kCons);
+      fused::named_sync(1, CONS);
     }
   }
   // v published: arrive now, compute g / u of the own rows while the others finish
-  fused::named_sync(1, kCons);
+  fused::named_sync(1, CONS);
+  stamp(4);
   if (tid == 0) fused::arrive_release(p.bar2);
   {
     __shared__ double gseg[kMaxSeg];
-    for (int d = warp; d < nseg; d += kCW) {  // g_d = mean |t| over segment d, same order in every CTA
+    for (int d = warp; d < nseg; d += CW) {  // g_d = mean |t| over segment d, same order in every CTA
       double part = 0.0;
       for (int i = lane; i < G; i += 32) part += __ldcg(p.blkpart + (size_t)i * nseg + d);
       part = warp_sum(part);
       if (lane == 0) gseg[d] = part / ((double)n * (double)p.cw);
     }
-    fused::named_sync(1, kCons);
-    for (int i = tid; i < nr * nseg; i += kCons) {
-      const int k = i / nseg, d = i % nseg;
+    fused::named_sync(1, CONS);
+    for (int i = tid; i < nr * nseg; i += CONS) {
+      const int k = i / nseg, d = i - k * nseg;
       const double g = gseg[d], rsum = rs[i];
       float u;
       if (p.scale_mode == CC_SCALE_PER_CHANNEL) u = 1.0f;
@@ -288,12 +433,13 @@ __global__ void __launch_bounds__(kThreads, 1) k1_resident(const __grid_constant
   }
   // ---- hand-off 2: every CTA's v ----
   if (tid == 0) fused::spin_until(p.bar2, (unsigned)G);
-  fused::named_sync(1, kCons);
+  fused::named_sync(1, CONS);
+  stamp(5);
 
   // ---------------- phase B ----------------
-  ColConst cc[2];
+  ColConst cc[NQ];
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
+  for (int j = 0; j < NQ; ++j) {
     cc[j].ok = true;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -304,25 +450,43 @@ __global__ void __launch_bounds__(kThreads, 1) k1_resident(const __grid_constant
       cc[j].ok = cc[j].ok && fused::scale_in_range(fabsf(v));
     }
   }
-  constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
-  double err[2] = {0.0, 0.0}, tsq[2] = {0.0, 0.0};
-  for (int k = 0; k < nr; ++k) {
+  // code byte offset of each quad inside its segment's code row
+  int ccol[NQ];
+  uint8_t *cbase[NQ];
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) {
+    const int sg = qseg[j];
+    ccol[j] = (qcol[j] - sg * p.cw) * (CODEC == CC_SIGN1 ? 1 : CODEC == CC_QUANT2 ? 2 : 4) / 8;
+    cbase[j] = p.body + sg * p.body_stride;
+  }
+  double err[NQ], tsq[NQ];
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) err[j] = tsq[j] = 0.0;
+  RingPos bpos;
+  for (int i = 0; i < nr; ++i) {
+    const int k = nr - 1 - i;  // newest rows first (matches the producer's base order)
     const int64_t row = r0 + k;
     const float *brow = bS + (size_t)k * C;
-    int s = 0;
     if (ring_base) {
-      const int u = nr + k;
-      s = u % S;
-      mbar_wait(&full[s], (uint32_t)(u / S) & 1u);
-      brow = reinterpret_cast<const float *>(ring + (size_t)s * p.stage_bytes);
+      mbar_wait(&fullB[bpos.s], bpos.ph);
+      brow = reinterpret_cast<const float *>(ring + (size_t)bpos.s * C * 4);
     }
+    const bool in_smem = k < p.nsm;
     const float *trow = tS + (size_t)k * C;
+    float tt[NQ][4];
+    if (!in_smem) tmem_ld<NQ>(tmem + tmem_off<NQ>(warp, k - p.nsm), tt);  // warp-collective
+    float *obase = p.base + row * C, *oaux = p.aux + row * C;
+    const int64_t crow = row * p.cbs;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < NQ; ++j) {
       const int o = qcol[j];
       float t[4], bb[4] = {0.f, 0.f, 0.f, 0.f}, d[4], e[4];
       if (qact[j]) {
-        fused::unpack_f(trow + o, t);
+        if (in_smem) {
+          fused::unpack_f(trow + o, t);
+        } else {
+          t[0] = tt[j][0]; t[1] = tt[j][1]; t[2] = tt[j][2]; t[3] = tt[j][3];
+        }
         if constexpr (kAux) fused::unpack_f(brow + o, bb);
       } else {
         t[0] = t[1] = t[2] = t[3] = 0.f;
@@ -336,73 +500,79 @@ __global__ void __launch_bounds__(kThreads, 1) k1_resident(const __grid_constant
         float nb[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) nb[q] = MODE == CC_NAIVE ? d[q] : __fadd_rn(bb[q], d[q]);
-        stcs4(p.base + row * C + o, nb);
-        if constexpr (kWB) stcs4(p.aux + row * C + o, e);
+        stcs4(obase + o, nb);
+        if constexpr (kWB) stcs4(oaux + o, e);
       }
       // codes: segment d's code row lives in its own body
-      const int sg = qseg[j];
-      uint8_t *crow = p.body + sg * p.body_stride + row * p.cbs;
-      const int cl = o - sg * p.cw;  // column inside the segment
+      uint8_t *cp = cbase[j] + crow + ccol[j];
       if constexpr (CODEC == CC_SIGN1) {
         const uint32_t other = __shfl_down_sync(0xffffffffu, packed, 1);
-        if (qact[j] && (lane & 1) == 0) crow[cl >> 3] = (uint8_t)(packed | (other << 4));
+        if (qact[j] && (lane & 1) == 0) *cp = (uint8_t)(packed | (other << 4));
       } else if constexpr (CODEC == CC_QUANT2) {
-        if (qact[j]) crow[cl >> 2] = (uint8_t)packed;
+        if (qact[j]) *cp = (uint8_t)packed;
       } else {
-        if (qact[j]) *reinterpret_cast<uint16_t *>(crow + (cl >> 1)) = (uint16_t)packed;
+        if (qact[j]) *reinterpret_cast<uint16_t *>(cp) = (uint16_t)packed;
       }
     }
     if (ring_base) {
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) mbar_arrive(&emptyB[bpos.s]);
+      bpos.next(SB);
     }
   }
-  (void)bits;
+  if (use_tmem) {  // every consumer warp is done with tensor memory before it is freed
+    tc_fence_before();
+    fused::named_sync(1, CONS);
+    tc_fence_after();
+    if (warp == 0) tmem_dealloc512(tmem);
+  }
+  stamp(6);
 
   // ---------------- StepRecord ----------------
   {
     __shared__ unsigned last;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < NQ; ++j) {
       const double a = warp_sum(err[j]), b = warp_sum(tsq[j]);
       if (lane == 0) {
-        red[(warp * 2 + j) * 2] = a;
-        red[(warp * 2 + j) * 2 + 1] = b;
+        red[(warp * NQ + j) * 2] = a;
+        red[(warp * NQ + j) * 2 + 1] = b;
       }
     }
-    fused::named_sync(1, kCons);
+    fused::named_sync(1, CONS);
     if (tid < nseg) {
       double a = 0.0, b = 0.0;
-      for (int w = 0; w < kCW; ++w)
-        for (int j = 0; j < 2; ++j) {
-          const int blk = j * kCW + w;
+      for (int w = 0; w < CW; ++w)
+        for (int j = 0; j < NQ; ++j) {
+          const int blk = j * CW + w;
           if (nseg == 1 || (blk < kNB && blk / p.bps == tid)) {
-            a += red[(w * 2 + j) * 2];
-            b += red[(w * 2 + j) * 2 + 1];
+            a += red[(w * NQ + j) * 2];
+            b += red[(w * NQ + j) * 2 + 1];
           }
         }
       p.recpart[((size_t)cta * nseg + tid) * 2] = a;
       p.recpart[((size_t)cta * nseg + tid) * 2 + 1] = b;
     }
-    fused::named_sync(1, kCons);
+    fused::named_sync(1, CONS);
     if (tid == 0) last = fused::atom_add_acq_rel(p.ticket) == (unsigned)G - 1;
-    fused::named_sync(1, kCons);
+    fused::named_sync(1, CONS);
     if (last) {
+      // thread i < G holds CTA i's partials; warps sum them in a fixed order
       double vals[2 * kMaxSeg];
 #pragma unroll
       for (int q = 0; q < 2 * kMaxSeg; ++q)
         vals[q] = (q < 2 * nseg && tid < G) ? __ldcg(p.recpart + (size_t)tid * nseg * 2 + q) : 0.0;
-      fused::named_sync(1, kCons);
+      fused::named_sync(1, CONS);
 #pragma unroll
       for (int q = 0; q < 2 * kMaxSeg; ++q) {
         if (q >= 2 * nseg) break;
         const double v = warp_sum(vals[q]);
         if (lane == 0) red[warp * 2 * kMaxSeg + q] = v;
       }
-      fused::named_sync(1, kCons);
+      fused::named_sync(1, CONS);
       if (tid < 2 * nseg) {
         double a = 0.0;
-        for (int w = 0; w < kCW; ++w) a += red[w * 2 * kMaxSeg + tid];
+        for (int w = 0; w < CW; ++w) a += red[w * 2 * kMaxSeg + tid];
         p.record[tid] = a;
       }
       if (tid == 0) {  // every CTA is past both hand-offs: leave the control words zeroed
@@ -412,6 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_resident(const __grid_constant
       }
     }
   }
+  stamp(7);
 }
 
 // ---------------------------------------------------------------------------
@@ -423,7 +594,8 @@ std::atomic<int64_t> g_resident_launches{0};
 
 template <int MODE, int CODEC, typename XT>
 static int launch(Params &p, size_t smem, cudaStream_t st) {
-  auto kern = k1_resident<MODE, CODEC, XT>;
+  constexpr int NQ = kNQ;
+  auto kern = k1_resident<MODE, CODEC, XT, NQ>;
   static int smem_set = 0;
   if ((int)smem > smem_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -431,7 +603,8 @@ static int launch(Params &p, size_t smem, cudaStream_t st) {
     smem_set = (int)smem;
   }
   void *args[] = {&p};
-  const cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(p.G), dim3(kThreads), args, smem, st);
+  const cudaError_t e =
+      cudaLaunchCooperativeKernel((const void *)kern, dim3(p.G), dim3(Geo<NQ>::THREADS), args, smem, st);
   if (e != cudaSuccess) {
     set_error(std::string("k1_resident launch: ") + cudaGetErrorString(e));
     cudaGetLastError();
@@ -448,13 +621,15 @@ int64_t resident_launches() { return k1r::g_resident_launches.load(); }
 
 void set_resident_enabled(int on) { k1r::g_resident_enabled = on != 0; }
 
-// Shared-memory plan for a shard; false when the CTA's rows do not fit.
+// Shared / tensor-memory plan for a shard; false when the CTA's rows do not fit.
 static bool resident_plan(k1r::Params &q, int mode, int x_dtype) {
   using namespace k1r;
   const int64_t C = q.C;
   const size_t xb = (size_t)C * (x_dtype == CC_BF16 ? 2 : 4), fb = (size_t)C * 4;
   const bool aux = mode != CC_NAIVE;
-  auto layout = [&](int keep_base, int S) -> size_t {
+  constexpr int kTmemRows = 512 / 24;  // tensor-memory rows per CTA (tmem_off)
+  // returns the shared bytes of a layout with `nsm` shared-memory t rows
+  auto layout = [&](int keep_base, int S, int nsm) -> size_t {
     const size_t R = (size_t)q.R;
     size_t off = 0;
     auto take = [&](size_t b) {
@@ -464,28 +639,46 @@ static bool resident_plan(k1r::Params &q, int mode, int x_dtype) {
     };
     q.keep_base = keep_base;
     q.S = S;
-    // ring stage: x, plus base when base is streamed (phase A for feedback mode;
-    // phase B reuses stage starts for base rows)
+    q.nsm = nsm;
     const bool ring_base = aux && !keep_base;
-    q.st_base = (uint32_t)align_up(xb, 128);
-    const size_t stage_a = (mode == CC_WITH_FEEDBACK && ring_base) ? q.st_base + fb : xb;
-    q.stage_bytes = (uint32_t)align_up(std::max(stage_a, ring_base ? fb : (size_t)0), 128);
-    q.off_t = take(R * fb);
+    const bool tmem_rows = nsm < q.R;
+    // ring stage: x | base (feedback mode, base streamed) | aux (tensor-memory rows)
+    size_t st = align_up(xb, 128);
+    q.st_base = (uint32_t)st;
+    if (mode == CC_WITH_FEEDBACK && ring_base) st = align_up(st + fb, 128);
+    q.st_fb = (uint32_t)st;
+    if (aux && tmem_rows) st = align_up(st + fb, 128);
+    q.stage_bytes = (uint32_t)st;
+    size_t ring = (size_t)S * q.stage_bytes;
+    q.SB = 0;
+    if (ring_base) {  // phase-B base slots in the ring area (at least 2)
+      ring = std::max(ring, 2 * fb);
+      q.SB = (int)std::min<size_t>(kMaxStages, ring / fb);
+    }
+    q.off_t = take((size_t)nsm * fb);
     q.off_b = take(keep_base ? R * fb : 0);
-    q.off_ring = take((size_t)S * q.stage_bytes);
+    q.off_ring = take(ring);
     q.off_rp = take(R * kNB * 8);
     q.off_rs = take(R * q.nseg * 8);
     q.off_u = take(R * q.nseg * 4);
-    q.off_bar = take(2 * kMaxStages * 8);
-    q.off_red = take((size_t)kCW * 32 * 8);
+    q.off_bar = take(4 * kMaxStages * 8 + 16);
+    q.off_red = take((size_t)Geo<kNQ>::CW * 32 * 8);
     return off + 16 * 8 + 64;  // + static shared (gseg, last)
   };
+  const size_t budget = kSmemMax - 1024;
+  // 1. every row in shared memory (t, and base when it fits too)
   for (int keep_base : {aux ? 1 : 0, 0}) {
-    for (int S = kMaxStages; S >= 2; --S) {
-      const size_t bytes = layout(keep_base, S);
-      if (bytes <= kSmemMax - 1024) return true;
-    }
+    for (int S = kMaxStages; S >= 2; --S)
+      if (layout(keep_base, S, q.R) <= budget) return true;
     if (!aux) break;
+  }
+  // 2. overflow rows in tensor memory (base streamed): the deepest ring that leaves
+  //    with the most shared t rows for it
+  const int s_force = (q.policy >> 16) & 15;  // experiments: ring depth override
+  for (int S = s_force ? s_force : kMaxStages; S >= 2; --S) {
+    for (int nsm = q.R - 1; nsm >= std::max(0, q.R - kTmemRows); --nsm) {
+      if (layout(0, S, nsm) <= budget) return true;
+    }
   }
   return false;
 }
@@ -496,7 +689,7 @@ static bool resident_plan(k1r::Params &q, int mode, int x_dtype) {
 int resident_encode(const fused::Params &fp, int codec, int mode, int x_dtype, cudaStream_t st) {
   using namespace k1r;
   if (!g_resident_enabled) return CC_ERR_UNSUPPORTED;
-  if (fp.C > fused::kMaxC || fp.C % 128 != 0 || fp.G4 <= kCons) return CC_ERR_UNSUPPORTED;  // full-width rows only
+  if (fp.C > fused::kMaxC || fp.C % 128 != 0 || fp.G4 <= fused::kCons) return CC_ERR_UNSUPPORTED;  // wide rows only
   Params q{};
   q.x = fp.x;
   q.base = fp.base;
@@ -523,12 +716,14 @@ int resident_encode(const fused::Params &fp, int codec, int mode, int x_dtype, c
   q.bar2 = fp.bar + 32;
   q.ticket = fp.ticket;
   q.scale_mode = fp.scale_mode;
+  q.timer = fp.timer;
+  q.policy = fp.policy;
   if (fp.ctl_in_ws) return CC_ERR_UNSUPPORTED;  // needs the stream's zeroed control slot
   if (!resident_plan(q, mode, x_dtype)) return CC_ERR_UNSUPPORTED;
   size_t smem = 0;
   {
     // recompute the total from the chosen layout
-    smem = (size_t)q.off_red + (size_t)kCW * 32 * 8;
+    smem = (size_t)q.off_red + (size_t)Geo<kNQ>::CW * 32 * 8;
   }
 #define CC_RES(MODE, XT)                                                                     \
   do {                                                                                       \

@@ -49,6 +49,8 @@ def main():
     ap.add_argument("--layers", type=int, default=16)
     ap.add_argument("--codec", default="quant2bit")
     ap.add_argument("--mode", default="residual_with_feedback")
+    ap.add_argument("--per-sm", action="store_true")
+    ap.add_argument("--policies", default="", type=lambda v: [int(x) for x in v.split(",") if x])
     a = ap.parse_args()
     lib = _lib.load()
     torch.cuda.set_stream(torch.cuda.Stream())
@@ -87,7 +89,33 @@ def main():
             used = lib.cc_debug_k1_resident_count() - c0
             us = graph_time(enc, 2 * L)
             row[name] = {"us": round(us, 2), "GBs": round(algo / us / 1e3, 1), "resident_ran": bool(used)}
+        # per-phase timeline of the resident launch (globaltimer stamps per CTA, last of
+        # 2L back-to-back eager launches), [min, max] over CTAs in µs from the first start
         lib.cc_debug_k1_resident(1)
+        tbuf = torch.zeros(1024 * 16, dtype=torch.int64, device="cuda")
+        lib.cc_debug_fused_timer(_lib.ptr(tbuf))
+        for i in range(2 * L):
+            enc(i)
+        torch.cuda.synchronize()
+        lib.cc_debug_fused_timer(None)
+        tb = tbuf.view(1024, 16).cpu()
+        g = int((tb[:, 0] > 0).sum())
+        tb = tb[:g].double()
+        t0 = tb[:, 0].min()
+        names = ["start", "first_data", "A_done", "sync1", "F_done", "sync2", "B_done", "end"]
+        row["resident_timeline_us"] = {nm: [round(float((tb[:, i] - t0).min()) / 1e3, 2),
+                                            round(float((tb[:, i] - t0).max()) / 1e3, 2)]
+                                       for i, nm in enumerate(names)}
+        if a.per_sm:  # phase-A end per SM id (imbalance map)
+            sm = tb[:, 8].long()
+            ad = (tb[:, 2] - t0) / 1e3
+            order = torch.argsort(sm)
+            row["A_done_by_smid"] = [[int(sm[i]), round(float(ad[i]), 2)] for i in order.tolist()]
+        for pol in a.policies:
+            lib.cc_debug_fused_policy(pol)
+            enc(0)
+            row[f"resident_policy{pol}_us"] = round(graph_time(enc, 2 * L), 2)
+        lib.cc_debug_fused_policy(0)
         print(json.dumps(row), flush=True)
         out.append(row)
         del xs, sts
