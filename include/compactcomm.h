@@ -48,6 +48,7 @@ extern "C" {
 #define CC_ERR_PROTOCOL (-4)   /* pipeline.ProtocolError (pl:36)               */
 #define CC_ERR_CUDA (-5)       /* launch / runtime failure                      */
 #define CC_ERR_UNSUPPORTED (-6)
+#define CC_ERR_NCCL (-7)       /* transport.TransportError (tr:22)             */
 
 /* codec tags: identical numbering to compressors.py:56-62 */
 #define CC_RAW 0
@@ -195,6 +196,65 @@ CC_API int cc_lowrank_encode(int int4, int64_t rows, int64_t cols, int64_t rank,
                              const float *t, const float *q0, uint8_t *body, float *decoded,
                              void *workspace, int64_t workspace_bytes, void *stream);
 CC_API int64_t cc_lowrank_workspace_bytes(int64_t rows, int64_t cols, int64_t rank);
+
+/* ---- exchanges: K1 encode -> NCCL collective -> K2 decode, from C -----------
+ * The reference's seam is mesh._Device._run (mesh.py:188-236) over
+ * Transport.send/recv (transport.py:36-43); here one call runs one layer step of
+ * the patch-parallel all-gather or the Ulysses all-to-all on `stream`.
+ *
+ * Communicator: cc_comm_wrap() adopts an existing ncclComm_t (e.g. PyTorch's
+ * ProcessGroupNCCL._comm_ptr(); not destroyed by cc_comm_destroy), or
+ * cc_comm_get_unique_id() on one rank + cc_comm_init_rank() on every rank builds
+ * one (NCCL is loaded at run time: libnccl.so.2).  A NULL comm means world size 1.
+ *
+ * Layer objects own every device buffer of the step: the [rows, cols] f32
+ * reconstruction (this rank's row shard = the sender base, mesh:233), the
+ * sender's feedback / ref, the codec workspace, the StepRecord and the send /
+ * receive wire buffers (ncclCommRegister'd when NCCL offers it).  x is borrowed.
+ * Shards are contiguous row ranges, the last rank takes the remainder
+ * (mesh:125-135); warmup and identity steps move the raw activation in its own
+ * dtype (bf16 stays bf16: lossless).  Codecs: identity (CC_RAW), sign1 / quant2 /
+ * quant4 (any scale mode), top-k and N:M for the all-gather; the quantizers for
+ * the all-to-all (segmented K1: cols % 128 == 0, cols <= 3072, (cols/P) % 128 == 0). */
+typedef struct cc_comm cc_comm;
+typedef struct cc_allgather_layer cc_allgather_layer;
+typedef struct cc_alltoall_layer cc_alltoall_layer;
+typedef struct {
+  int codec;            /* CC_RAW (identity), CC_SIGN1, CC_QUANT2, CC_QUANT4, CC_TOPK, CC_NMBLOCK */
+  int scale_mode;       /* CC_SCALE_* (quantizers) */
+  double keep_fraction; /* top-k (cx:446-451) */
+  int nm_n, nm_m;       /* N:M block sparsifier (cx:429-443) */
+} cc_codec_spec;
+
+CC_API int cc_comm_get_unique_id(uint8_t *id_out /* 128 bytes */);
+CC_API int cc_comm_init_rank(const uint8_t *id, int nranks, int rank, cc_comm **out);
+CC_API int cc_comm_wrap(void *nccl_comm, cc_comm **out);
+CC_API int cc_comm_rank(const cc_comm *c);
+CC_API int cc_comm_size(const cc_comm *c);
+CC_API int cc_comm_destroy(cc_comm *c);
+
+/* patch parallelism (mesh.py:188-237): x_shard is this rank's [hi - lo, cols]
+ * rows (cc_allgather_shard).  After a step, cc_allgather_reconstruction() is the
+ * [rows, cols] f32 activation every rank agrees on bit for bit (mesh:237). */
+CC_API int cc_allgather_create(cc_comm *c, const cc_codec_spec *spec, int mode, int64_t rows, int64_t cols,
+                               int warmup, int x_dtype, cc_allgather_layer **out);
+CC_API int cc_allgather_step(cc_allgather_layer *layer, const void *x_shard, void *stream);
+CC_API float *cc_allgather_reconstruction(cc_allgather_layer *layer);
+CC_API float *cc_allgather_sender_base(cc_allgather_layer *layer);
+CC_API float *cc_allgather_sender_aux(cc_allgather_layer *layer);
+CC_API const uint8_t *cc_allgather_body(cc_allgather_layer *layer, int64_t *nbytes);
+CC_API const double *cc_allgather_record(cc_allgather_layer *layer);
+CC_API int cc_allgather_shard(cc_allgather_layer *layer, int64_t *lo, int64_t *hi);
+CC_API int cc_allgather_destroy(cc_allgather_layer *layer);
+
+/* Ulysses sequence parallelism: x_local [n_local, cols]; output
+ * [P * n_local, cols / P] = the full sequence for this rank's heads. */
+CC_API int cc_alltoall_create(cc_comm *c, const cc_codec_spec *spec, int mode, int64_t n_local, int64_t cols,
+                              int warmup, int x_dtype, cc_alltoall_layer **out);
+CC_API int cc_alltoall_step(cc_alltoall_layer *layer, const void *x_local, void *stream);
+CC_API float *cc_alltoall_output(cc_alltoall_layer *layer);
+CC_API float *cc_alltoall_sender_base(cc_alltoall_layer *layer);
+CC_API int cc_alltoall_destroy(cc_alltoall_layer *layer);
 
 /* ---- diagnostics ----------------------------------------------------------- */
 CC_API const char *cc_last_error(void);

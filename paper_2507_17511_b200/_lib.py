@@ -20,10 +20,18 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "compactcomm.h")
 
 # constants mirrored from include/compactcomm.h (checked by tests/test_abi.py)
 CC_OK, CC_ERR_ARG, CC_ERR_SHAPE, CC_ERR_PAYLOAD, CC_ERR_PROTOCOL, CC_ERR_CUDA, CC_ERR_UNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
+CC_ERR_NCCL = -7
 CC_RAW, CC_SIGN1, CC_QUANT2, CC_LOWRANK, CC_LOWRANK4, CC_NMBLOCK, CC_TOPK, CC_QUANT4 = 0, 1, 2, 3, 4, 5, 6, 16
 CC_NAIVE, CC_NO_FEEDBACK, CC_WITH_FEEDBACK = 0, 1, 2
 CC_F32, CC_BF16 = 0, 1
 CC_SCALE_RANK1, CC_SCALE_PER_TOKEN, CC_SCALE_PER_CHANNEL = 0, 1, 2
+
+
+class CodecSpec(ctypes.Structure):
+    """cc_codec_spec of include/compactcomm.h."""
+
+    _fields_ = [("codec", ctypes.c_int), ("scale_mode", ctypes.c_int), ("keep_fraction", ctypes.c_double),
+                ("nm_n", ctypes.c_int), ("nm_m", ctypes.c_int)]
 
 
 def nm_param(n, m):
@@ -52,6 +60,26 @@ SIGNATURES = {
     "cc_nm_encode_step": (_i32, [_i32, _i64, _i64, _i32, _i32, _p, _i32, _p, _p, _p, _p, _i64, _p, _p]),
     "cc_lowrank_encode": (_i32, [_i32, _i64, _i64, _i64, _i32, _p, _p, _p, _p, _p, _i64, _p]),
     "cc_lowrank_workspace_bytes": (_i64, [_i64, _i64, _i64]),
+    "cc_comm_get_unique_id": (_i32, [_p]),
+    "cc_comm_init_rank": (_i32, [_p, _i32, _i32, ctypes.POINTER(_p)]),
+    "cc_comm_wrap": (_i32, [_p, ctypes.POINTER(_p)]),
+    "cc_comm_rank": (_i32, [_p]),
+    "cc_comm_size": (_i32, [_p]),
+    "cc_comm_destroy": (_i32, [_p]),
+    "cc_allgather_create": (_i32, [_p, _p, _i32, _i64, _i64, _i32, _i32, ctypes.POINTER(_p)]),
+    "cc_allgather_step": (_i32, [_p, _p, _p]),
+    "cc_allgather_reconstruction": (_p, [_p]),
+    "cc_allgather_sender_base": (_p, [_p]),
+    "cc_allgather_sender_aux": (_p, [_p]),
+    "cc_allgather_body": (_p, [_p, ctypes.POINTER(_i64)]),
+    "cc_allgather_record": (_p, [_p]),
+    "cc_allgather_shard": (_i32, [_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "cc_allgather_destroy": (_i32, [_p]),
+    "cc_alltoall_create": (_i32, [_p, _p, _i32, _i64, _i64, _i32, _i32, ctypes.POINTER(_p)]),
+    "cc_alltoall_step": (_i32, [_p, _p, _p]),
+    "cc_alltoall_output": (_p, [_p]),
+    "cc_alltoall_sender_base": (_p, [_p]),
+    "cc_alltoall_destroy": (_i32, [_p]),
     "cc_last_error": (ctypes.c_char_p, []),
     "cc_version": (_i32, []),
     "cc_launch_count": (_i64, []),
@@ -119,6 +147,10 @@ def check(status, what=""):
         raise ValueError(text)
     if status == CC_ERR_UNSUPPORTED:
         raise NotImplementedError(text)
+    if status == CC_ERR_NCCL:
+        from . import comm
+
+        raise comm.TransportError(text)
     raise CudaError(text)
 
 

@@ -24,9 +24,17 @@ LIB = os.path.join(PKG, "lib", "libcompactcomm_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+def _nccl_include():
+    """nccl.h for the run-time-bound NCCL exchange (types only; no link)."""
+    for d in [os.environ.get("NCCL_INCLUDE", "")] + [os.path.join(p, "nvidia", "nccl", "include") for p in sys.path]:
+        if d and os.path.exists(os.path.join(d, "nccl.h")):
+            return d
+    return "/usr/include"
+
+
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
-         "-I" + os.path.join(ROOT, "include")]
+         "-I" + os.path.join(ROOT, "include"), "-I" + _nccl_include()]
 
 
 def _sources():
@@ -68,7 +76,7 @@ def build_library(force=False, verbose=False):
                 if verbose and log:
                     sys.stderr.write(log)
     if force or todo or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -42,6 +42,10 @@ from . import compressors as cx
 from . import pipeline as pl
 
 
+class TransportError(RuntimeError):
+    """A collective failed (the reference's transport.TransportError, tr:22)."""
+
+
 def shard_bounds(rows, devices):
     """Contiguous row shards; the last device takes the remainder (mesh:125-135)."""
     q = rows // devices
@@ -694,3 +698,171 @@ class UlyssesAllToAll:
                 st.feedback.copy_(tmp.feedback)
             if st.ref is not None:
                 st.ref.copy_(tmp.ref)
+
+
+# ---------------------------------------------------------------------------
+# The same exchanges through the C ABI (include/compactcomm.h "exchanges"): the
+# whole layer step — K1, the NCCL collective, K2 — is one library call, with
+# library-owned buffers; these classes only hold the handles.
+# ---------------------------------------------------------------------------
+
+class _DeviceArray:
+    """A library-owned device buffer seen by torch (CUDA array interface)."""
+
+    def __init__(self, ptr, shape, typestr="<f4"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def _as_tensor(ptr, shape, typestr="<f4"):
+    return torch.as_tensor(_DeviceArray(ptr, shape, typestr), device="cuda")
+
+
+class CComm:
+    """cc_comm: adopts an NCCL communicator (a torch ProcessGroupNCCL's by default)
+    or builds one from a unique id shared by the caller."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    @staticmethod
+    def from_process_group(group=None):
+        dist = _dist()
+        pg = group or dist.distributed_c10d._get_default_group()
+        ptr = pg._get_backend(torch.device("cuda", torch.cuda.current_device()))._comm_ptr()
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().cc_comm_wrap(ctypes.c_void_p(ptr), ctypes.byref(h)), "cc_comm_wrap")
+        return CComm(h)
+
+    @staticmethod
+    def unique_id():
+        buf = (ctypes.c_uint8 * 128)()
+        _lib.check(_lib.load().cc_comm_get_unique_id(buf), "cc_comm_get_unique_id")
+        return bytes(buf)
+
+    @staticmethod
+    def init_rank(uid, nranks, rank):
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().cc_comm_init_rank((ctypes.c_uint8 * 128)(*uid), nranks, rank, ctypes.byref(h)),
+                   "cc_comm_init_rank")
+        return CComm(h)
+
+    @property
+    def rank(self):
+        return _lib.load().cc_comm_rank(self.h)
+
+    @property
+    def size(self):
+        return _lib.load().cc_comm_size(self.h)
+
+    def destroy(self):
+        if self.h:
+            _lib.check(_lib.load().cc_comm_destroy(self.h), "cc_comm_destroy")
+            self.h = None
+
+
+def codec_spec_struct(codec):
+    tag = codec_tag(codec)
+    if cx.CompressorKind(codec.kind) == cx.CompressorKind.IDENTITY:
+        tag = _lib.CC_RAW
+    return _lib.CodecSpec(tag, cx._SCALE_MODES[getattr(codec, "scale_mode", "rank1")],
+                          float(codec.keep_fraction or 0.0), int(codec.n or 0), int(codec.m or 0))
+
+
+class CAllGather:
+    """Patch-parallel compressed all-gather layer through the C ABI
+    (cc_allgather_*): mesh.py:188-237 semantics, no Python on the step path."""
+
+    def __init__(self, rows, cols, codec, mode="residual_with_feedback", warmup=1, in_dtype=torch.bfloat16,
+                 comm=None):
+        self.rows, self.cols, self.codec = int(rows), int(cols), codec
+        self.comm = comm
+        self.in_dtype = in_dtype
+        spec = codec_spec_struct(codec)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().cc_allgather_create(comm.h if comm else None, ctypes.byref(spec),
+                                                   pl._MODE_CODE[pl.PipelineMode(mode)], self.rows, self.cols,
+                                                   int(warmup), cx.dtype_code(torch.empty(0, dtype=in_dtype)),
+                                                   ctypes.byref(h)), "cc_allgather_create")
+        self.h = h
+        lo, hi = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.load().cc_allgather_shard(h, ctypes.byref(lo), ctypes.byref(hi)))
+        self.lo, self.hi = lo.value, hi.value
+
+    def step(self, x_shard):
+        _check_dtype(x_shard, self.in_dtype)
+        if tuple(x_shard.shape) != (self.hi - self.lo, self.cols) or not x_shard.is_contiguous():
+            raise pl.ShapeError(f"shard must be contiguous [{self.hi - self.lo}, {self.cols}]")
+        _lib.check(_lib.load().cc_allgather_step(self.h, _lib.ptr(x_shard), _lib.stream_ptr()), "cc_allgather_step")
+        return self.reconstruction()
+
+    def reconstruction(self):
+        return _as_tensor(_lib.load().cc_allgather_reconstruction(self.h), (self.rows, self.cols))
+
+    def sender_base(self):
+        return _as_tensor(_lib.load().cc_allgather_sender_base(self.h), (self.hi - self.lo, self.cols))
+
+    def sender_aux(self):
+        p = _lib.load().cc_allgather_sender_aux(self.h)
+        return None if not p else _as_tensor(p, (self.hi - self.lo, self.cols))
+
+    def body(self):
+        nb = ctypes.c_int64()
+        p = _lib.load().cc_allgather_body(self.h, ctypes.byref(nb))
+        return _as_tensor(p, (max(nb.value, 1),), "|u1")[:nb.value]
+
+    def record(self):
+        return _as_tensor(_lib.load().cc_allgather_record(self.h), (2,), "<f8")
+
+    def digest(self):
+        torch.cuda.current_stream().synchronize()
+        return hashlib.blake2b(self.reconstruction().cpu().numpy().tobytes(), digest_size=16).digest()
+
+    def close(self):
+        if self.h:
+            _lib.check(_lib.load().cc_allgather_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class CAllToAll:
+    """Ulysses compressed all-to-all layer through the C ABI (cc_alltoall_*)."""
+
+    def __init__(self, n_local, cols, codec, mode="residual_with_feedback", warmup=1, in_dtype=torch.bfloat16,
+                 comm=None):
+        self.n, self.C = int(n_local), int(cols)
+        self.P = comm.size if comm else 1
+        self.in_dtype = in_dtype
+        spec = codec_spec_struct(codec)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().cc_alltoall_create(comm.h if comm else None, ctypes.byref(spec),
+                                                  pl._MODE_CODE[pl.PipelineMode(mode)], self.n, self.C, int(warmup),
+                                                  cx.dtype_code(torch.empty(0, dtype=in_dtype)), ctypes.byref(h)),
+                   "cc_alltoall_create")
+        self.h = h
+
+    def step(self, x_local):
+        _check_dtype(x_local, self.in_dtype)
+        if tuple(x_local.shape) != (self.n, self.C) or not x_local.is_contiguous():
+            raise pl.ShapeError(f"input must be contiguous [{self.n}, {self.C}]")
+        _lib.check(_lib.load().cc_alltoall_step(self.h, _lib.ptr(x_local), _lib.stream_ptr()), "cc_alltoall_step")
+        return self.output()
+
+    def output(self):
+        return _as_tensor(_lib.load().cc_alltoall_output(self.h), (self.P * self.n, self.C // self.P))
+
+    def close(self):
+        if self.h:
+            _lib.check(_lib.load().cc_alltoall_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -102,7 +102,7 @@ def _worker_patch(rank, world, port, rows, cols, codec, mode, topology, out_dir,
         dist.destroy_process_group()
 
 
-def _simulate_mesh(world, rows, cols, codec, mode):
+def _simulate_mesh(world, rows, cols, codec, mode, seed=99):
     """The reference mesh's all-gather semantics on the numpy oracle: per step the
     vstack of every shard's sender base (receivers mirror senders bit-exactly)."""
     bounds = O.shard_rows(rows, world)
@@ -110,7 +110,7 @@ def _simulate_mesh(world, rows, cols, codec, mode):
     chans = [O.Channel(mode, 1, np.zeros((hi - lo, cols), np.float32)) for lo, hi in bounds]
     rcv = [O.Channel(mode, 1, np.zeros((hi - lo, cols), np.float32)) for lo, hi in bounds]
     out = []
-    for t, x in enumerate(_inputs(rows, cols), start=1):
+    for t, x in enumerate(_inputs(rows, cols, seed), start=1):
         for (lo, hi), ch, rc in zip(bounds, chans, rcv):
             tag, body, _ = O.send(ch, x[lo:hi], oc)
             O.receive(rc, t, t <= 1, tag, body, oc)
