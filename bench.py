@@ -522,6 +522,7 @@ def run_b200(a, world, rank):
 
     consistency = check_consistency(exs, inputs, world)
     e2e = None if a.no_e2e else measure_e2e(exs, inputs, streams, world, K, L, rows, cols)
+    used_graph = graphs is not None
     sim = None
     if world == 1 and not a.no_sim:
         del graphs
@@ -555,7 +556,7 @@ def run_b200(a, world, rank):
         "exposed_comm_us_per_layer": exposed_us,
         "bf16_allgather_us_per_layer": bf16_ag,
         "compressed_allgather_us_per_layer": comp_ag,
-        "run": {"overlap": overlap, "cuda_graph": graphs is not None},
+        "run": {"overlap": overlap, "cuda_graph": used_graph},
         "kernels": {"k1_encode_ms": k1_ms, "k1_gbs": k1_gbs, "k2_decode_ms": k2_ms,
                     "k2_gbs": k2_bytes / (k2_ms / 1e3) / 1e9, "k2_frac": k2_bytes / (k2_ms / 1e3) / 1e9 / peak,
                     "timing": "CUDA events recorded inside the replayed graph around every K1 / K2 launch",

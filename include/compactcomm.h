@@ -122,7 +122,8 @@ CC_API int cc_encode_step_segmented(int codec, int mode, int scale_mode, int64_t
 
 /* Warmup / identity step (pl:89-97): base = x, feedback = 0, ref = x,
  * body = raw x as body_dtype (CC_F32 = the reference wire, CC_BF16 lossless
- * for bf16 inputs), record = {0, ||x||^2}. */
+ * for bf16 inputs), record = {0, 0}: compression_error = 0, so delta_hat = 1
+ * (pl:76-81) and the target norm is not computed on warmup steps. */
 CC_API int cc_warmup_step(int mode, int64_t rows, int64_t cols, const void *x, int x_dtype,
                           float *base, float *aux, void *body, int body_dtype, double *record,
                           void *stream);

@@ -67,6 +67,8 @@ class StepRecord:
 
     @property
     def target_sqnorm(self):
+        """||target||^2 (f64).  Not a reference field; 0.0 on warmup / identity steps,
+        whose record is {0, 0} (cc_warmup_step) since delta_hat is 1 there anyway."""
         return self._resolve()[1]
 
     @property
