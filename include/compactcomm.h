@@ -198,6 +198,19 @@ CC_API int cc_lowrank_encode(int int4, int64_t rows, int64_t cols, int64_t rank,
                              void *workspace, int64_t workspace_bytes, void *stream);
 CC_API int64_t cc_lowrank_workspace_bytes(int64_t rows, int64_t cols, int64_t rank);
 
+/* ---- the low-rank start block drawn on the device (cx:407, la:67-74) --------
+ * out [rows, cols] f32 = float32(numpy Generator(PCG64(SeedSequence(entropy,
+ * spawn_key))).standard_normal((rows, cols))), bit for bit (la:25-27 spawn_rng;
+ * keys of pl:190 / mesh:193).  key: DEVICE array of nwords (<= 16) uint32 =
+ * SeedSequence's assembled entropy: the entropy's little-endian 32-bit words,
+ * zero-padded to 4 words when a spawn key follows, then one word per spawn-key
+ * element (< 2^32).  step_word >= 0: key[step_word] += 1 after the draw
+ * (stream-ordered), so a step captured in a CUDA graph draws the next step's
+ * block on every replay; -1 leaves the key unchanged. */
+CC_API int64_t cc_gaussian_workspace_bytes(int64_t rows, int64_t cols);
+CC_API int cc_gaussian_keyed(int64_t rows, int64_t cols, uint32_t *key, int nwords, int step_word, float *out,
+                             void *workspace, int64_t workspace_bytes, void *stream);
+
 /* ---- exchanges: K1 encode -> NCCL collective -> K2 decode, from C -----------
  * The reference's seam is mesh._Device._run (mesh.py:188-236) over
  * Transport.send/recv (transport.py:36-43); here one call runs one layer step of

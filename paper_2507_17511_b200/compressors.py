@@ -534,10 +534,20 @@ def encode_lowrank(a, spec, rng, decoded=None):
     if not (1 <= r <= min(rows, cols)):
         raise ShapeError(f"rank {r} out of range for shape {(rows, cols)}")
     lib = _lib.load()
-    # Q0 is drawn on the host from the reference's PCG64 stream (cx:407) and goes up
-    # through a reused pinned staging ring (asynchronous H2D, no per-step host alloc)
-    q0 = subspace_init(rng, cols, r)
-    q0 = _stage_h2d(q0, t.device) if t.is_cuda else torch.from_numpy(q0).to(t.device)
+    from .linalg import DeviceKey
+
+    if isinstance(rng, DeviceKey):
+        # Q0 drawn on the device from the key's PCG64 stream, bit-identical to the host
+        # draw (cc_gaussian_keyed); no host work, so the step can be graph-captured
+        q0 = workspace(4 * cols * r, "lowrank_q0").view(torch.float32)[: cols * r]
+        gws = workspace(_lib.check(lib.cc_gaussian_workspace_bytes(cols, r)), "gauss")
+        _lib.check(lib.cc_gaussian_keyed(cols, r, _lib.ptr(rng.words), rng.nwords, rng.step_word, _lib.ptr(q0),
+                                         _lib.ptr(gws), gws.numel(), _lib.stream_ptr()), "gaussian_keyed")
+    else:
+        # Q0 drawn on the host from the caller's numpy Generator (cx:407) and uploaded
+        # through a reused pinned staging ring (asynchronous H2D, no per-step host alloc)
+        q0 = subspace_init(rng, cols, r)
+        q0 = _stage_h2d(q0, t.device) if t.is_cuda else torch.from_numpy(q0).to(t.device)
     tag = _lib.CC_LOWRANK4 if spec.int4_factors else _lib.CC_LOWRANK
     body = _empty_body(lib.cc_body_bytes(tag, rows, cols, r))
     ws = workspace(_lib.check(lib.cc_lowrank_workspace_bytes(rows, cols, r)), "lowrank")

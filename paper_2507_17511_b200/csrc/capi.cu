@@ -92,7 +92,52 @@ uint8_t *stream_control_block(cudaStream_t st) {
   return P.base + (size_t)(P.used++) * kSlotBytes;
 }
 
+// Library-owned zero-initialised scratch slabs of the persistent kernels that need
+// more than a control slot (top-k histograms): one 48 KB slab per (device,
+// stream) from a pool allocated on first use, left zeroed by every launch.  A
+// stream first seen during a capture still gets a slab as long as the pool
+// exists; null when it cannot be created (first use inside a capture).
+uint8_t *stream_zero_slab(cudaStream_t st, size_t bytes) {
+  constexpr size_t kSlabBytes = 48 * 1024;
+  constexpr int kSlabs = 128;
+  if (bytes > kSlabBytes) return nullptr;
+  struct Pool {
+    uint8_t *base = nullptr;
+    int used = 0;
+    std::unordered_map<cudaStream_t, int> slot;
+  };
+  static std::mutex mu;
+  static Pool pools[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  Pool &P = pools[dev];
+  if (!P.base) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    void *b = nullptr;
+    if (cudaMalloc(&b, kSlabBytes * kSlabs) != cudaSuccess || cudaMemset(b, 0, kSlabBytes * kSlabs) != cudaSuccess) {
+      cudaGetLastError();
+      if (b) cudaFree(b);
+      return nullptr;
+    }
+    P.base = static_cast<uint8_t *>(b);
+  }
+  auto it = P.slot.find(st);
+  if (it != P.slot.end()) return P.base + (size_t)it->second * kSlabBytes;
+  if (P.used == kSlabs) return nullptr;
+  P.slot.emplace(st, P.used);
+  return P.base + (size_t)(P.used++) * kSlabBytes;
+}
+
 int64_t topk_workspace_bytes(int64_t n, int64_t C, int64_t k);
+void set_topk_resident_enabled(int on);
+void set_topk_timer(void *buf);
+int64_t topk_resident_launches();
 int topk_encode(int64_t n, int64_t C, int64_t k, const float *t, uint8_t *body, float *decoded, void *ws,
                 int64_t ws_bytes, cudaStream_t st);
 int topk_encode_step(int mode, int64_t n, int64_t C, int64_t k, const void *x, int x_dtype, float *base, float *aux,
@@ -134,6 +179,9 @@ int residual_target(int mode, int64_t n, int64_t C, const void *x, int x_dtype, 
 int apply_decoded(int mode, int64_t n, int64_t C, const void *x, int x_dtype, const float *t, const float *dec,
                   float *base, float *aux, double *record, void *ws, int64_t ws_bytes, cudaStream_t st);
 
+int64_t gaussian_workspace_bytes(int64_t rows, int64_t cols);
+int gaussian_keyed(int64_t rows, int64_t cols, uint32_t *key, int nwords, int step_word, float *out, void *ws,
+                   int64_t ws_bytes, cudaStream_t st);
 }  // namespace cc
 
 using namespace cc;
@@ -163,6 +211,9 @@ CC_API void cc_set_lowrank_backend(int backend) { set_lowrank_backend(backend); 
 CC_API void cc_debug_lowrank_tma(int enable, int waves) { set_tc_tma(enable, waves); }
 CC_API void cc_debug_k1_resident(int enable) { set_resident_enabled(enable); }
 CC_API int64_t cc_debug_k1_resident_count(void) { return resident_launches(); }
+CC_API void cc_debug_topk_resident(int enable) { set_topk_resident_enabled(enable); }
+CC_API int64_t cc_debug_topk_resident_count(void) { return topk_resident_launches(); }
+CC_API void cc_debug_topk_timer(void *dev_buf) { set_topk_timer(dev_buf); }
 
 CC_API int64_t cc_topk_count(int64_t rows, int64_t cols, double keep_fraction) {
   if (rows < 1 || cols < 1 || !(keep_fraction > 0.0 && keep_fraction <= 1.0)) return CC_ERR_ARG;
@@ -353,6 +404,16 @@ CC_API int cc_lowrank_encode(int int4, int64_t rows, int64_t cols, int64_t rank,
   if (iterations < 1 || !t || !q0 || !body) { set_error("bad low-rank args"); return CC_ERR_ARG; }
   return lowrank_encode(int4, rows, cols, rank, iterations, t, q0, body, decoded, workspace, workspace_bytes,
                         (cudaStream_t)stream);
+}
+
+CC_API int64_t cc_gaussian_workspace_bytes(int64_t rows, int64_t cols) {
+  if (rows < 1 || cols < 1) return CC_ERR_SHAPE;
+  return cc::gaussian_workspace_bytes(rows, cols);
+}
+
+CC_API int cc_gaussian_keyed(int64_t rows, int64_t cols, uint32_t *key, int nwords, int step_word, float *out,
+                             void *workspace, int64_t workspace_bytes, void *stream) {
+  return cc::gaussian_keyed(rows, cols, key, nwords, step_word, out, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 CC_API int cc_encode(int codec, int scale_mode, int64_t rows, int64_t cols, int64_t param, const float *t,

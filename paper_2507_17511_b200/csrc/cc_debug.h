@@ -57,6 +57,15 @@ CC_API void cc_debug_k1_resident(int enable);
 /* launches of the shard-resident K1 since load (tests check which kernel ran) */
 CC_API int64_t cc_debug_k1_resident_count(void);
 
+/* K4 shard-resident top-k kernel (topk_resident.cu): 1 = use it for encode steps
+ * whenever it can launch (default), 0 = always the multi-kernel radix select. */
+CC_API void cc_debug_topk_resident(int enable);
+/* launches of the shard-resident top-k kernel since load */
+CC_API int64_t cc_debug_topk_resident_count(void);
+/* profiling only: device buffer of [grid][16] u64 %globaltimer stamps of the
+ * resident top-k kernel's phases (NULL disables) */
+CC_API void cc_debug_topk_timer(void *dev_buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -351,6 +351,7 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, 1) k1_resident(const __grid_
     cp[0] = cs[j][0]; cp[1] = cs[j][1]; cp[2] = cs[j][2]; cp[3] = cs[j][3];
   }
   fused::named_sync(1, CONS);
+  stamp(9);
   // row sums per segment (blocks of the segment in order), then CTA totals
   for (int i = tid; i < nr * nseg; i += CONS) {
     const int k = i / nseg, d = i - k * nseg;
@@ -366,9 +367,25 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, 1) k1_resident(const __grid_
   }
   // ---- hand-off 1 ----
   fused::named_sync(1, CONS);
+  stamp(10);
   if (tid == 0) {
-    fused::arrive_release(p.bar1);
-    fused::spin_until(p.bar1, (unsigned)G);
+    if (p.policy & 256) {
+      __threadfence();
+      atomicAdd(p.bar1, 1u);
+    } else {
+      fused::arrive_release(p.bar1);
+    }
+    stamp(11);
+    if (p.policy & 512) {
+      for (;;) {
+        unsigned v;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.bar1) : "memory");
+        if (v >= (unsigned)G) break;
+      }
+      __threadfence();
+    } else {
+      fused::spin_until(p.bar1, (unsigned)G);
+    }
   }
   fused::named_sync(1, CONS);
   stamp(3);
@@ -554,8 +571,10 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, 1) k1_resident(const __grid_
       p.recpart[((size_t)cta * nseg + tid) * 2 + 1] = b;
     }
     fused::named_sync(1, CONS);
+    stamp(12);
     if (tid == 0) last = fused::atom_add_acq_rel(p.ticket) == (unsigned)G - 1;
     fused::named_sync(1, CONS);
+    stamp(13);
     if (last) {
       // thread i < G holds CTA i's partials; warps sum them in a fixed order
       double vals[2 * kMaxSeg];

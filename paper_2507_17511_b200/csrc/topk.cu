@@ -791,8 +791,16 @@ int topk_encode(int64_t n, int64_t C, int64_t k, const float *t, uint8_t *body, 
   return cuda_status("topk_encode");
 }
 
+int topk_resident_encode_step(int mode, int64_t n, int64_t C, int64_t k, const void *x, int x_dtype, float *base,
+                              float *aux, uint8_t *body, void *ws, int64_t ws_bytes, double *record,
+                              cudaStream_t st);
+
 int topk_encode_step(int mode, int64_t n, int64_t C, int64_t k, const void *x, int x_dtype, float *base, float *aux,
                      uint8_t *body, void *ws, int64_t ws_bytes, double *record, cudaStream_t st) {
+  {  // one persistent launch when the grid can be co-resident (topk_resident.cu)
+    const int rc = topk_resident_encode_step(mode, n, C, k, x, x_dtype, base, aux, body, ws, ws_bytes, record, st);
+    if (rc != CC_ERR_UNSUPPORTED) return rc;
+  }
   const int64_t total = n * C;
   size_t need = 0;
   const int nH1 = h1_blocks(total);

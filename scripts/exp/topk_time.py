@@ -6,11 +6,14 @@ sys.path.insert(0, os.getcwd())
 import torch  # noqa: E402
 
 from paper_2507_17511_b200 import compressors as cx  # noqa: E402
+from paper_2507_17511_b200 import _lib  # noqa: E402
 from paper_2507_17511_b200 import pipeline as pl  # noqa: E402
 
 L = 16
-for rows in (4096, 512):
-    for keep in (0.01, 0.1):
+lib = _lib.load()
+for rows, keep, res in [(r, k, s) for r in (4096, 1024, 512) for k in (0.01, 0.1) for s in (1, 0)]:
+        lib.cc_debug_topk_resident(res)
+        c0 = lib.cc_debug_topk_resident_count()
         spec = cx.CompressorSpec(cx.CompressorKind.TOPK, keep_fraction=keep)
         g = torch.Generator(device="cuda").manual_seed(0)
         xs = [(torch.randn(rows, 3072, device="cuda", generator=g) * torch.rand(1, 3072, device="cuda", generator=g)
@@ -32,4 +35,34 @@ for rows in (4096, 512):
             gr.replay()
         b.record()
         torch.cuda.synchronize()
-        print(f"topk {rows}x3072 keep {keep}: {1e3 * a.elapsed_time(b) / (10 * L):.1f} us/step")
+        used = lib.cc_debug_topk_resident_count() - c0
+        print(f"topk {rows}x3072 keep {keep} resident={res} (ran {used}): {1e3 * a.elapsed_time(b) / (10 * L):.1f} us/step",
+              flush=True)
+        del xs, sts, gr
+
+# per-phase timeline of the resident kernel (globaltimer stamps per CTA)
+import json  # noqa: E402
+names = ["start", "A_done", "bar1", "find1", "lvl2", "bar2", "lvl3", "bar3", "count", "bar4", "write", "end"]
+for rows in (512, 1024, 4096):
+    lib.cc_debug_topk_resident(1)
+    spec = cx.CompressorSpec(cx.CompressorKind.TOPK, keep_fraction=0.01)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    xs = [(torch.randn(rows, 3072, device="cuda", generator=g) * torch.rand(1, 3072, device="cuda", generator=g)
+           * 3).to(torch.bfloat16) for _ in range(L)]
+    sts = [pl.LayerState("residual_with_feedback", 1, torch.zeros(rows, 3072, device="cuda")) for _ in range(L)]
+    for _ in range(2):
+        for s, x in zip(sts, xs):
+            pl.encode_step(s, x, spec)
+    tbuf = torch.zeros(1024 * 16, dtype=torch.int64, device="cuda")
+    lib.cc_debug_topk_timer(_lib.ptr(tbuf))
+    for s, x in zip(sts, xs):
+        pl.encode_step(s, x, spec)
+    torch.cuda.synchronize()
+    lib.cc_debug_topk_timer(None)
+    tb = tbuf.view(1024, 16).cpu()
+    G = int((tb[:, 0] > 0).sum())
+    tb = tb[:G].double()
+    t0 = tb[:, 0].min()
+    print(json.dumps({"rows": rows, "grid": G, "timeline_us": {
+        nm: [round(float((tb[:, i] - t0).min()) / 1e3, 2), round(float((tb[:, i] - t0).max()) / 1e3, 2)]
+        for i, nm in enumerate(names)}}), flush=True)

@@ -102,10 +102,10 @@ def main():
         g = int((tb[:, 0] > 0).sum())
         tb = tb[:g].double()
         t0 = tb[:, 0].min()
-        names = ["start", "first_data", "A_done", "sync1", "F_done", "sync2", "B_done", "end"]
+        names = ["start", "first_data", "A_done", "sync1", "F_done", "sync2", "B_done", "end", "smid", "colpart_done", "pre_arrive", "arrived", "rec_part", "ticket"]
         row["resident_timeline_us"] = {nm: [round(float((tb[:, i] - t0).min()) / 1e3, 2),
                                             round(float((tb[:, i] - t0).max()) / 1e3, 2)]
-                                       for i, nm in enumerate(names)}
+                                       for i, nm in enumerate(names) if nm != "smid"}
         if a.per_sm:  # phase-A end per SM id (imbalance map)
             sm = tb[:, 8].long()
             ad = (tb[:, 2] - t0) / 1e3
