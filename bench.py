@@ -530,8 +530,8 @@ def run_b200(a, world, rank):
         sim["ulysses8"] = sim_rank_measure("ulysses", 8, "sign1bit", L, rows, cols)
         sim["topk1pct_patch8"] = sim_rank_measure("patch", 8, "topk", L, rows, cols, spec_kw={"keep_fraction": 0.01})
         sim["topk10pct_patch8"] = sim_rank_measure("patch", 8, "topk", L, rows, cols, spec_kw={"keep_fraction": 0.1})
-        sim["lowrank_r8_patch4"] = sim_rank_measure("patch", 4, "lowrank", 8, rows, cols, steps=3, warmup=2,
-                                                    spec_kw={"rank": 8, "iterations": 2}, graph=False)
+        sim["lowrank_r8_patch4"] = sim_rank_measure("patch", 4, "lowrank", 8, rows, cols, steps=5, warmup=3,
+                                                    spec_kw={"rank": 8, "iterations": 2})
     cpu = None
     if not a.no_cpu and rank == 0:
         procs = a.cpu_procs or min(os.cpu_count() or 1, 16)
@@ -704,11 +704,14 @@ def sim_rank_measure(kind, P, codec, L, rows, cols, steps=5, warmup=3, spec_kw=N
         e.streams = streams
     inputs = [flux_inputs(rows, cols, lo, hi, layer, dev) for layer in range(L)]
 
+    # low-rank: every layer channel draws its start block (cx:407) on the device from
+    # the mesh key spawn_rng(seed, 6, rank, t) (mesh.py:193) with t advanced on the
+    # device (linalg.DeviceKey), so the step is captured and replayed like the others
+    keys = [la.DeviceKey(1000 * layer, 6, 0, 2, advance=True) for layer in range(L)] if lowrank else None
+
     def one_step(s):
         for layer, e in enumerate(exs):
-            # low-rank draws Q0 from the host PCG64 stream every step (cx:407), so it runs
-            # eagerly (host launch overhead included); the others replay CUDA graphs
-            e.step(inputs[layer][s % 2], rng=la.make_rng(1000 * layer + s) if lowrank else None)
+            e.step(inputs[layer][s % 2], rng=keys[layer] if lowrank else None)
 
     for s in range(warmup + 1):
         one_step(s)

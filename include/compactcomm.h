@@ -198,6 +198,18 @@ CC_API int cc_lowrank_encode(int int4, int64_t rows, int64_t cols, int64_t rank,
                              void *workspace, int64_t workspace_bytes, void *stream);
 CC_API int64_t cc_lowrank_workspace_bytes(int64_t rows, int64_t cols, int64_t rank);
 
+/* One low-rank encode_step (pl:84-121 with cx:394-426): t = target(x, base, aux)
+ * -> Q0 -> subspace iteration -> body -> base' / aux' and record (the decode is
+ * fused into the state update, bit-identical to the receiver's decode).  Q0 is
+ * either q0 (a host draw, la.gaussian_matrix(rng, cols, rank)) or drawn on the
+ * device from key (cc_gaussian_keyed below); exactly one of q0 / key is non-null.
+ * With a key every launch is stream-ordered device work (CUDA-graph capturable). */
+CC_API int64_t cc_lowrank_step_workspace_bytes(int64_t rows, int64_t cols, int64_t rank);
+CC_API int cc_lowrank_encode_step(int mode, int64_t rows, int64_t cols, int64_t rank, int iterations, int int4,
+                                  const void *x, int x_dtype, float *base, float *aux, const float *q0,
+                                  uint32_t *key, int nwords, int step_word, uint8_t *body, void *workspace,
+                                  int64_t workspace_bytes, double *record, void *stream);
+
 /* ---- the low-rank start block drawn on the device (cx:407, la:67-74) --------
  * out [rows, cols] f32 = float32(numpy Generator(PCG64(SeedSequence(entropy,
  * spawn_key))).standard_normal((rows, cols))), bit for bit (la:25-27 spawn_rng;

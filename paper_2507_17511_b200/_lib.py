@@ -61,6 +61,9 @@ SIGNATURES = {
     "cc_lowrank_encode": (_i32, [_i32, _i64, _i64, _i64, _i32, _p, _p, _p, _p, _p, _i64, _p]),
     "cc_lowrank_workspace_bytes": (_i64, [_i64, _i64, _i64]),
     "cc_gaussian_workspace_bytes": (_i64, [_i64, _i64]),
+    "cc_lowrank_step_workspace_bytes": (_i64, [_i64, _i64, _i64]),
+    "cc_lowrank_encode_step": (_i32, [_i32, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _p, _p, _p, _i32, _i32, _p,
+                                      _p, _i64, _p, _p]),
     "cc_gaussian_keyed": (_i32, [_i64, _i64, _p, _i32, _i32, _p, _p, _i64, _p]),
     "cc_comm_get_unique_id": (_i32, [_p]),
     "cc_comm_init_rank": (_i32, [_p, _i32, _i32, ctypes.POINTER(_p)]),
@@ -100,6 +103,7 @@ SIGNATURES = {
     "cc_debug_topk_resident": (None, [_i32]),
     "cc_debug_topk_resident_count": (_i64, []),
     "cc_debug_topk_timer": (None, [_p]),
+    "cc_debug_orth_stamps": (None, [_p]),
 }
 # private test / profiling knobs (csrc/cc_debug.h), not part of the public ABI
 DEBUG_HEADER = os.path.join(HERE, "csrc", "cc_debug.h")

@@ -137,6 +137,7 @@ uint8_t *stream_zero_slab(cudaStream_t st, size_t bytes) {
 int64_t topk_workspace_bytes(int64_t n, int64_t C, int64_t k);
 void set_topk_resident_enabled(int on);
 void set_topk_timer(void *buf);
+void set_orth1_stamps(void *buf);
 int64_t topk_resident_launches();
 int topk_encode(int64_t n, int64_t C, int64_t k, const float *t, uint8_t *body, float *decoded, void *ws,
                 int64_t ws_bytes, cudaStream_t st);
@@ -145,6 +146,10 @@ int topk_encode_step(int mode, int64_t n, int64_t C, int64_t k, const void *x, i
 int topk_decode(int count, const int64_t *rows, int64_t C, int64_t k, const uint8_t *const *bodies, int accumulate,
                 float *const *bases, cudaStream_t st);
 int64_t lowrank_workspace_bytes(int64_t n, int64_t C, int64_t r);
+int64_t lowrank_step_workspace_bytes(int64_t n, int64_t C, int64_t r);
+int lowrank_encode_step(int mode, int64_t n, int64_t C, int64_t r, int iters, int int4, const void *x, int x_dtype,
+                        float *base, float *aux, const float *q0_in, uint32_t *key, int nwords, int step_word,
+                        uint8_t *body, void *ws, int64_t ws_bytes, double *record, cudaStream_t st);
 int lowrank_encode(int int4, int64_t n, int64_t C, int64_t r, int iters, const float *t, const float *q0,
                    uint8_t *body, float *decoded, void *ws, int64_t ws_bytes, cudaStream_t st);
 int lowrank_decode(int int4, int count, const int64_t *rows, int64_t C, int64_t r, const uint8_t *const *bodies,
@@ -214,6 +219,7 @@ CC_API int64_t cc_debug_k1_resident_count(void) { return resident_launches(); }
 CC_API void cc_debug_topk_resident(int enable) { set_topk_resident_enabled(enable); }
 CC_API int64_t cc_debug_topk_resident_count(void) { return topk_resident_launches(); }
 CC_API void cc_debug_topk_timer(void *dev_buf) { set_topk_timer(dev_buf); }
+CC_API void cc_debug_orth_stamps(void *dev_buf) { set_orth1_stamps(dev_buf); }
 
 CC_API int64_t cc_topk_count(int64_t rows, int64_t cols, double keep_fraction) {
   if (rows < 1 || cols < 1 || !(keep_fraction > 0.0 && keep_fraction <= 1.0)) return CC_ERR_ARG;
@@ -414,6 +420,28 @@ CC_API int64_t cc_gaussian_workspace_bytes(int64_t rows, int64_t cols) {
 CC_API int cc_gaussian_keyed(int64_t rows, int64_t cols, uint32_t *key, int nwords, int step_word, float *out,
                              void *workspace, int64_t workspace_bytes, void *stream) {
   return cc::gaussian_keyed(rows, cols, key, nwords, step_word, out, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+CC_API int64_t cc_lowrank_step_workspace_bytes(int64_t rows, int64_t cols, int64_t rank) {
+  if (rows < 1 || cols < 1) return CC_ERR_SHAPE;
+  if (rank < 1 || rank > (rows < cols ? rows : cols)) return CC_ERR_SHAPE;
+  return lowrank_step_workspace_bytes(rows, cols, rank);
+}
+
+CC_API int cc_lowrank_encode_step(int mode, int64_t rows, int64_t cols, int64_t rank, int iterations, int int4,
+                                  const void *x, int x_dtype, float *base, float *aux, const float *q0,
+                                  uint32_t *key, int nwords, int step_word, uint8_t *body, void *workspace,
+                                  int64_t workspace_bytes, double *record, void *stream) {
+  if (rows < 1 || cols < 1) { set_error("empty shape"); return CC_ERR_SHAPE; }
+  if (rank < 1 || rank > (rows < cols ? rows : cols)) { set_error("rank out of range"); return CC_ERR_SHAPE; }
+  if (!valid_mode(mode) || (x_dtype != CC_F32 && x_dtype != CC_BF16)) { set_error("bad mode/dtype"); return CC_ERR_ARG; }
+  if (iterations < 1 || !x || !base || !body || !record || (mode != CC_NAIVE && !aux) || (!q0 == !key)) {
+    set_error("bad low-rank step args (exactly one of q0 / key)");
+    return CC_ERR_ARG;
+  }
+  if (key && (nwords < 1 || nwords > 16 || step_word >= nwords)) { set_error("bad key"); return CC_ERR_ARG; }
+  return lowrank_encode_step(mode, rows, cols, rank, iterations, int4, x, x_dtype, base, aux, q0, key, nwords,
+                             step_word, body, workspace, workspace_bytes, record, (cudaStream_t)stream);
 }
 
 CC_API int cc_encode(int codec, int scale_mode, int64_t rows, int64_t cols, int64_t param, const float *t,

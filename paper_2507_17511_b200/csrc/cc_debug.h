@@ -65,6 +65,9 @@ CC_API int64_t cc_debug_topk_resident_count(void);
 /* profiling only: device buffer of [grid][16] u64 %globaltimer stamps of the
  * resident top-k kernel's phases (NULL disables) */
 CC_API void cc_debug_topk_timer(void *dev_buf);
+/* profiling only: device buffer of 16 u64 clock64 stamps of the single-CTA
+ * CholQR2 (k_orth1) phases (NULL disables) */
+CC_API void cc_debug_orth_stamps(void *dev_buf);
 
 #ifdef __cplusplus
 }

@@ -356,8 +356,8 @@ __device__ void cgs2_block(const float *__restrict__ orig, double *__restrict__ 
 }
 
 // one warp: right-looking Cholesky of G (as k_chol) and R^-1 into Ri, lane c owns column c
-__device__ __forceinline__ void chol_rinv_warp(double (*G)[kMaxR + 1], double (*R)[kMaxR + 1],
-                                               double (*Ri)[kMaxR + 1], int r, int *bad) {
+template <int LD = kMaxR + 1>
+__device__ __forceinline__ void chol_rinv_warp(double (*G)[LD], double (*R)[LD], double (*Ri)[LD], int r, int *bad) {
   const int c = threadIdx.x & 31;
   for (int j = 0; j < r; ++j) {
     double piv = G[j][j];  // every lane reads the same pivot
@@ -444,6 +444,290 @@ __global__ void __launch_bounds__(kOrthThreads) k_orth(const float *__restrict__
   }
 }
 
+// ---------------------------------------------------------------------------
+// CholQR2 in ONE CTA for r <= 16 when the [m, r] block fits in shared memory (no
+// grid-wide synchronisation), with the two r-wide products on the f64 tensor
+// pipe (DMMA, mma.sync m8n8k4 f64: exact products, f64 accumulation):
+//   Gram   G = M^T M: warp w takes rows 4k.. of its share; per k-step ONE shared
+//          load per lane feeds both operands (A = M^T chunk, B = M chunk: the
+//          same element for a lane); the 16 warps' 8x8 tiles summed in order
+//   apply  M <- M R^-1 row tile by row tile (8 rows x r, k-steps of 4)
+// The block is kept column-major in f64 (odd column stride), padded to RP = 8 or
+// 16 columns with zeros; the warp Cholesky / R^-1 as in k_orth.  Same CholQR2
+// mathematics as k_orth, a different (fixed) summation order.
+// ---------------------------------------------------------------------------
+constexpr int kOrth1Threads = 512;
+
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// one warp, registers: G = R^T R (lane c holds column c of G / R) by RP compile-time
+// pivot steps with one rsqrt each (no division chain), then R^-1 by back
+// substitution with the reciprocal diagonal.  Rm / Ri in shared memory for the apply.
+template <int RP, int LD>
+__device__ __forceinline__ void chol_rinv_regs(const double (*G)[LD], double (*Rm)[LD], double (*Ri)[LD], int r,
+                                               int *bad) {
+  const int c = threadIdx.x & 31;
+  double g[RP];
+#pragma unroll
+  for (int a = 0; a < RP; ++a) g[a] = (c < r && a < r) ? G[a][c] : 0.0;
+  double invd[RP];
+#pragma unroll
+  for (int j = 0; j < RP; ++j) {
+    if (j >= r) break;
+    double piv = __shfl_sync(0xffffffffu, g[j], j);  // G[j][j] (Schur complement) from lane j
+    if (!(piv >= kDegenerate)) {
+      if (c == 0) *bad = 1;
+      piv = 1.0;
+    }
+    const double inv = rsqrt(piv);
+    invd[j] = inv;
+    const double rjc = c == j ? piv * inv : (c > j && c < r ? g[j] * inv : 0.0);  // R[j][c]
+    if (c < r) Rm[j][c] = rjc;
+#pragma unroll
+    for (int a = j + 1; a < RP; ++a) {
+      const double rja = __shfl_sync(0xffffffffu, rjc, a);  // R[j][a]
+      if (a < r && c >= a && c < r) g[a] -= rja * rjc;
+    }
+  }
+  __syncwarp();
+  if (c < r) {  // column c of R^-1: x[i] = (delta_ic - sum_{k>i} R[i][k] x[k]) / R[i][i]
+    double x[RP];
+#pragma unroll
+    for (int i = RP - 1; i >= 0; --i) {
+      double sacc = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = i + 1; k < RP; ++k)
+        if (k <= c) sacc -= Rm[i][k] * x[k];
+      x[i] = (i > c || i >= r) ? 0.0 : sacc * invd[i];
+    }
+#pragma unroll
+    for (int i = 0; i < RP; ++i) Ri[i][c] = x[i];
+  }
+}
+
+// r = 8: every lane of the warp factors the WHOLE 8x8 Gram in registers (the same
+// arithmetic in every lane, no shuffles, no shared-memory round trips in the
+// pivot chain); lane c < 8 then back-substitutes column c of R^-1.  The pivot
+// chain is 8 x (rsqrt + one multiply + an independent rank-1 update).
+__device__ __forceinline__ void chol8_regs(const double (*G)[17], double (*Rm)[17], double (*Ri)[17], int *bad) {
+  const int c = threadIdx.x & 31;
+  double g[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = a; b < 8; ++b) g[a][b] = G[a][b];
+  double invd[8];
+  bool degenerate = false;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    double piv = g[j][j];
+    if (!(piv >= kDegenerate)) {
+      degenerate = true;
+      piv = 1.0;
+    }
+    const double inv = rsqrt(piv);
+    invd[j] = inv;
+    g[j][j] = piv * inv;  // R[j][j]
+#pragma unroll
+    for (int b = j + 1; b < 8; ++b) g[j][b] *= inv;  // R[j][b]
+#pragma unroll
+    for (int a = j + 1; a < 8; ++a)
+#pragma unroll
+      for (int b = a; b < 8; ++b) g[a][b] -= g[j][a] * g[j][b];
+  }
+  if (degenerate && c == 0) *bad = 1;
+  if (c < 8) {
+#pragma unroll
+    for (int b = 0; b < 8; ++b) Rm[c][b] = b >= c ? g[c][b] : 0.0;
+    double x[8];  // column c of R^-1
+#pragma unroll
+    for (int i = 7; i >= 0; --i) {
+      double sacc = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = i + 1; k < 8; ++k)
+        if (k <= c) sacc -= g[i][k] * x[k];
+      x[i] = i > c ? 0.0 : sacc * invd[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) Ri[i][c] = x[i];
+  }
+}
+
+__device__ unsigned long long *g_orth1_stamps = nullptr;  // profiling: [16] clock64 stamps of block 0
+
+template <int RP>
+__global__ void __launch_bounds__(kOrth1Threads, 1) k_orth1(const float *__restrict__ Min, float *__restrict__ out,
+                                                             int64_t m, int r, double *__restrict__ scratch,
+                                                             unsigned long long seed) {
+  constexpr int W = kOrth1Threads / 32, RB = RP / 8;
+  extern __shared__ __align__(16) uint8_t o1sm[];
+  double *M = reinterpret_cast<double *>(o1sm);  // column-major [RP][mp], rows padded to a multiple of 8
+  const int64_t m8 = (m + 7) & ~int64_t(7);
+  const int64_t mp = m8 | 1;                     // odd stride: the rows of a column map to distinct banks
+  constexpr int LD = 17;  // r <= 16
+  __shared__ double G[16][LD], Rm[16][LD], Ri[16][LD];
+  __shared__ double part[W][RB * RB][64];
+  __shared__ double red[kOrth1Threads / 32], coef[kMaxR];
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;  // MMA fragment coordinates
+  unsigned long long *stp = g_orth1_stamps;
+  auto stamp = [&](int i) {
+    if (stp && tid == 0) stp[i] = clock64();
+  };
+  stamp(0);
+  if (r == RP && (reinterpret_cast<uintptr_t>(Min) & 15) == 0) {  // float4 loads, 4 in flight per thread
+    const int64_t nq = m8 * RP / 4;
+    for (int64_t q0 = tid; q0 < nq; q0 += 4 * kOrth1Threads) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t q = q0 + u * kOrth1Threads;
+        v[u] = (q < nq && 4 * q < m * RP) ? __ldg(reinterpret_cast<const float4 *>(Min) + q)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t q = q0 + u * kOrth1Threads;
+        if (q < nq) {
+          const int64_t i = 4 * q / RP;
+          const int k = (int)(4 * q % RP);
+          M[(k + 0) * mp + i] = v[u].x;
+          M[(k + 1) * mp + i] = v[u].y;
+          M[(k + 2) * mp + i] = v[u].z;
+          M[(k + 3) * mp + i] = v[u].w;
+        }
+      }
+    }
+  } else {
+    for (int64_t e = tid; e < m8 * RP; e += kOrth1Threads) {
+      const int64_t i = e / RP;
+      const int k = (int)(e % RP);
+      M[k * mp + i] = (i < m && k < r) ? (double)Min[i * r + k] : 0.0;
+    }
+  }
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  stamp(1);
+  const int64_t nks = m8 / 4;  // Gram k-steps of 4 rows
+  for (int pass = 0; pass < 2; ++pass) {
+    // ---- Gram on the tensor pipe: tiles (ra, rc) with ra <= rc ----
+    double acc[RB * RB][2];
+#pragma unroll
+    for (int t = 0; t < RB * RB; ++t) acc[t][0] = acc[t][1] = 0.0;
+    double acc2[RB * RB][2];  // second accumulator chain (odd k-step pairs)
+#pragma unroll
+    for (int t = 0; t < RB * RB; ++t) acc2[t][0] = acc2[t][1] = 0.0;
+    for (int64_t ks = warp; ks < nks; ks += 2 * W) {
+      const bool two = ks + W < nks;
+      double v[RB], v2[RB];
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        v[b] = M[(8 * b + gq) * mp + 4 * ks + tq];  // M[i][8b + gq]
+        v2[b] = two ? M[(8 * b + gq) * mp + 4 * (ks + W) + tq] : 0.0;
+      }
+#pragma unroll
+      for (int ra = 0; ra < RB; ++ra)
+#pragma unroll
+        for (int rc = ra; rc < RB; ++rc) {
+          dmma884(acc[ra * RB + rc][0], acc[ra * RB + rc][1], v[ra], v[rc]);
+          dmma884(acc2[ra * RB + rc][0], acc2[ra * RB + rc][1], v2[ra], v2[rc]);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < RB * RB; ++t) {
+      acc[t][0] += acc2[t][0];
+      acc[t][1] += acc2[t][1];
+    }
+#pragma unroll
+    for (int t = 0; t < RB * RB; ++t) {
+      part[warp][t][gq * 8 + 2 * tq] = acc[t][0];
+      part[warp][t][gq * 8 + 2 * tq + 1] = acc[t][1];
+    }
+    __syncthreads();
+    stamp(2 + 4 * pass);
+    for (int o = tid; o < RP * RP; o += kOrth1Threads) {  // G entry (a, c), a <= c: warps summed in order
+      const int a = o / RP, c = o % RP;
+      if (a <= c && c < r) {
+        const int t = (a / 8) * RB + c / 8;
+        double v = 0.0;
+        for (int w = 0; w < W; ++w) v += part[w][t][(a % 8) * 8 + (c % 8)];
+        G[a][c] = v;
+        G[c][a] = v;
+      }
+    }
+    for (int e = tid; e < 16 * LD; e += kOrth1Threads) {
+      Rm[e / LD][e % LD] = 0.0;
+      Ri[e / LD][e % LD] = 0.0;
+    }
+    __syncthreads();
+    stamp(3 + 4 * pass);
+    if (warp == 0) {
+      if (RP == 8 && r == 8) chol8_regs(G, Rm, Ri, &bad);
+      else chol_rinv_regs<RP, LD>(G, Rm, Ri, r, &bad);
+    }
+    __syncthreads();
+    stamp(4 + 4 * pass);
+    // ---- apply: M <- M R^-1 (8-row tiles; Ri zero beyond r) ----
+    double bfr[RB][RP / 4];  // B fragments: Ri[4 ks + tq][8 cb + gq]
+#pragma unroll
+    for (int cb = 0; cb < RB; ++cb)
+#pragma unroll
+      for (int ks = 0; ks < RP / 4; ++ks) bfr[cb][ks] = Ri[4 * ks + tq][8 * cb + gq];
+    const int64_t ntile = m8 / 8;
+    for (int64_t tile = warp; tile < ntile; tile += 2 * W) {  // two row tiles in flight
+      const bool two = tile + W < ntile;
+      const int64_t i = 8 * tile + gq, i2 = 8 * (tile + W) + gq;
+      double afr[RP / 4], afr2[RP / 4];
+#pragma unroll
+      for (int ks = 0; ks < RP / 4; ++ks) {
+        afr[ks] = M[(4 * ks + tq) * mp + i];  // A = M[i][4 ks + tq]
+        afr2[ks] = two ? M[(4 * ks + tq) * mp + i2] : 0.0;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int cb = 0; cb < RB; ++cb) {
+        double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < RP / 4; ++ks) {
+          dmma884(d0, d1, afr[ks], bfr[cb][ks]);
+          dmma884(e0, e1, afr2[ks], bfr[cb][ks]);
+        }
+        M[(8 * cb + 2 * tq) * mp + i] = d0;  // D[gq][2 tq], D[gq][2 tq + 1]
+        M[(8 * cb + 2 * tq + 1) * mp + i] = d1;
+        if (two) {
+          M[(8 * cb + 2 * tq) * mp + i2] = e0;
+          M[(8 * cb + 2 * tq + 1) * mp + i2] = e1;
+        }
+      }
+    }
+    __syncthreads();
+    stamp(5 + 4 * pass);
+  }
+  if (!bad) {
+    if (r == RP && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+      const int64_t nq = m * RP / 4;
+      for (int64_t q = tid; q < nq; q += kOrth1Threads) {
+        const int64_t i = 4 * q / RP;
+        const int k = (int)(4 * q % RP);
+        reinterpret_cast<float4 *>(out)[q] = make_float4((float)M[(k + 0) * mp + i], (float)M[(k + 1) * mp + i],
+                                                         (float)M[(k + 2) * mp + i], (float)M[(k + 3) * mp + i]);
+      }
+    } else {
+      for (int64_t e = tid; e < m * r; e += kOrth1Threads) out[e] = (float)M[(e % r) * mp + e / r];
+    }
+  } else {  // rank-deficient: CGS2 with random replacement columns (la:77-112)
+    cgs2_block(Min, scratch, out, m, r, seed, red, coef);
+  }
+  __syncthreads();
+  stamp(10);
+  if (stp && tid == 0) stp[11] = bad;
+}
+
 __global__ void k_to32(const double *__restrict__ in, float *__restrict__ out, int64_t cnt) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e < cnt) out[e] = (float)in[e];
@@ -527,6 +811,18 @@ __device__ __forceinline__ double factor_at(const uint8_t *body, int int4, int64
   return -range + (double)code * (2.0 * range / 15.0);  // cx:569-572
 }
 
+// factors -> f64 Uf [n, r] and the TRANSPOSED WfT [r, C] (coalesced per-column reads
+// in k_outer_apply); same values as k_unpack_factors
+__global__ void k_unpack_factors_t(const uint8_t *__restrict__ body, int int4, int64_t n, int64_t C, int r,
+                                   double *__restrict__ Uf, double *__restrict__ WfT) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n * r) Uf[e] = factor_at(body, int4, n, C, r, 0, e / r, (int)(e % r));
+  else if (e < (n + C) * r) {
+    const int64_t e2 = e - n * r;  // column-major over W: k = e2 / C, j = e2 % C
+    WfT[e2] = factor_at(body, int4, n, C, r, 1, e2 % C, (int)(e2 / C));
+  }
+}
+
 // factors -> f64 scratch (Uf [n, r], Wf [C, r]) once, then the outer product
 __global__ void k_unpack_factors(const uint8_t *__restrict__ body, int int4, int64_t n, int64_t C, int r,
                                  double *__restrict__ Uf, double *__restrict__ Wf) {
@@ -556,6 +852,83 @@ __global__ void __launch_bounds__(kThreads) k_outer(const double *__restrict__ U
     for (int k = 0; k < r; ++k) s += us[ii][k] * w[k];
     const int64_t e = (i0 + ii) * C + j;
     out[e] = acc ? __fadd_rn(out[e], (float)s) : (float)s;
+  }
+}
+
+// Sender-side state update of a low-rank step with the decode fused in: the
+// reconstruction d = f32(sum_k U[i,k] W[j,k]) in f64 from the body's factors (the
+// receiver's k_outer arithmetic, same summation order, so sender and receiver
+// bases stay bit-identical) applied directly: base' = base + d (naive: d),
+// feedback' = t - d, ref' = x (pipeline.py:107-113); StepRecord partials per CTA
+// (||d - t||^2, ||t||^2, pipeline.py:115-120).  No decoded tensor is materialised.
+// Thread = one column j (W's column from the transposed factor WfT [r][C]:
+// coalesced), kOARows rows per CTA with every row's loads in flight together.
+constexpr int kOARows = 16;
+template <int MODE, typename XT, int RM>
+__global__ void __launch_bounds__(kThreads) k_outer_apply(const double *__restrict__ Uf, const double *__restrict__ WfT,
+                                                           int64_t n, int64_t C, int r, const XT *__restrict__ x,
+                                                           const float *__restrict__ t, float *__restrict__ base,
+                                                           float *__restrict__ aux, double *__restrict__ part) {
+  __shared__ double us[kOARows][kMaxR];
+  __shared__ double se[kThreads / 32], st2[kThreads / 32];
+  const int64_t i0 = (int64_t)blockIdx.y * kOARows;
+  const int nr = (int)min64(kOARows, n - i0);
+  for (int e = threadIdx.x; e < kOARows * r; e += kThreads) {
+    const int ii = e / r, k = e % r;
+    us[ii][k] = ii < nr ? Uf[(i0 + ii) * r + k] : 0.0;
+  }
+  __syncthreads();
+  const int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  double err = 0.0, tsq = 0.0;
+  if (j < C) {
+    double w[RM];  // RM >= r, compile-time: W's column stays in registers
+#pragma unroll
+    for (int k = 0; k < RM; ++k) w[k] = k < r ? WfT[(int64_t)k * C + j] : 0.0;
+    float tt[kOARows], bb[kOARows], xx[kOARows];
+#pragma unroll
+    for (int ii = 0; ii < kOARows; ++ii) {  // every row's loads in flight together
+      const int64_t e = (i0 + ii) * C + j;
+      tt[ii] = ii < nr ? t[e] : 0.0f;
+      bb[ii] = (MODE != CC_NAIVE && ii < nr) ? base[e] : 0.0f;
+      xx[ii] = (MODE == CC_NO_FEEDBACK && ii < nr) ? Act<XT>::load1(x + e) : 0.0f;
+    }
+#pragma unroll
+    for (int ii = 0; ii < kOARows; ++ii) {
+      if (ii >= nr) break;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < RM; ++k)
+        if (k < r) s += us[ii][k] * w[k];
+      const float d = (float)s;
+      const int64_t e = (i0 + ii) * C + j;
+      const double df = (double)d - (double)tt[ii];
+      err += df * df;
+      tsq += (double)tt[ii] * (double)tt[ii];
+      if constexpr (MODE == CC_NAIVE) {
+        base[e] = d;
+      } else {
+        base[e] = __fadd_rn(bb[ii], d);
+        if constexpr (MODE == CC_WITH_FEEDBACK) aux[e] = __fsub_rn(tt[ii], d);
+        else aux[e] = xx[ii];
+      }
+    }
+  }
+  err = warp_sum(err);
+  tsq = warp_sum(tsq);
+  if ((threadIdx.x & 31) == 0) {
+    se[threadIdx.x >> 5] = err;
+    st2[threadIdx.x >> 5] = tsq;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < kThreads / 32; ++i) {
+      a += se[i];
+      b += st2[i];
+    }
+    const int64_t blk = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+    part[2 * blk] = a;
+    part[2 * blk + 1] = b;
   }
 }
 
@@ -605,9 +978,37 @@ int64_t lowrank_workspace_bytes(int64_t n, int64_t C, int64_t r) {
 
 static unsigned long long g_lr_seed = 0x5eed5eedULL;
 
+void set_orth1_stamps(void *buf) {
+  unsigned long long *p = reinterpret_cast<unsigned long long *>(buf);
+  cudaMemcpyToSymbol(lr::g_orth1_stamps, &p, sizeof(p));
+}
+
 // M (f32 [m, r]) -> orthonormal f32 columns written to out (may alias M)
 static void orth(const float *M, float *out, int64_t m, int r, const lr::Work &w, cudaStream_t st) {
   using namespace lr;
+  const int rp = r <= 8 ? 8 : 16;
+  const size_t need = (size_t)(((m + 7) & ~int64_t(7)) | 1) * rp * 8;
+  if (r <= 16) {  // one CTA, no grid sync, when the padded block fits in shared memory
+    const void *kern = rp == 8 ? (const void *)k_orth1<8> : (const void *)k_orth1<16>;
+    static size_t max_dyn[2] = {0, 0};
+    size_t &md = max_dyn[rp == 16];
+    if (md == 0) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, kern);
+      md = 227 * 1024 - fa.sharedSizeBytes - 1024;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)md);
+    }
+    if (need <= md) {
+      unsigned long long seed = g_lr_seed++;
+      double *scratch = w.M64;
+      void *args[] = {&M, &out, &m, &r, &scratch, &seed};
+      if (cudaLaunchKernel(kern, dim3(1), dim3(kOrth1Threads), args, need, st) == cudaSuccess) {
+        count_launch();
+        return;
+      }
+      cudaGetLastError();
+    }
+  }
   {
     const int nb = (int)cdiv(m, kGramRows);
     const size_t smem = sizeof(double) * (size_t)(kGramRows + 3 * kMaxR) * (kMaxR + 1);
@@ -708,6 +1109,101 @@ int lowrank_encode(int int4, int64_t n, int64_t C, int64_t r64, int iters, const
   }
   if (decoded) decode_into(body, int4, n, C, r, decoded, 0, w, st);
   return cuda_status("lowrank_encode");
+}
+
+int residual_target(int mode, int64_t n, int64_t C, const void *x, int x_dtype, const float *base, const float *aux,
+                    float *t, cudaStream_t st);
+int gaussian_keyed(int64_t rows, int64_t cols, uint32_t *key, int nwords, int step_word, float *out, void *ws,
+                   int64_t ws_bytes, cudaStream_t st);
+int64_t gaussian_workspace_bytes(int64_t rows, int64_t cols);
+int sum_parts(int nparts, const double *part, double *record, cudaStream_t st);
+
+// encode_step workspace: t [n, C] | Q0 [C, r] | gaussian scratch | encode workspace |
+// f64 factors [n + C, r] | record partials
+static size_t lr_step_layout(int64_t n, int64_t C, int64_t r, uint8_t *w, float **t, float **q0, void **gws,
+                             size_t *gbytes, void **ews, size_t *ebytes, double **Uf, double **part) {
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    uint8_t *q = w ? w + off : nullptr;
+    off = align_up(off + b, 256);
+    return q;
+  };
+  const size_t gb = (size_t)gaussian_workspace_bytes(C, r);
+  const size_t eb = (size_t)lowrank_workspace_bytes(n, C, r);
+  const int64_t nblk = cdiv(C, lr::kThreads) * cdiv(n, lr::kOARows);
+  uint8_t *pt = take(4 * (size_t)n * C), *pq = take(4 * (size_t)C * r), *pg = take(gb), *pe = take(eb);
+  uint8_t *pu = take(8 * (size_t)(n + C) * r), *pp = take(16 * (size_t)nblk);
+  if (w) {
+    *t = reinterpret_cast<float *>(pt);
+    *q0 = reinterpret_cast<float *>(pq);
+    *gws = pg;
+    *gbytes = gb;
+    *ews = pe;
+    *ebytes = eb;
+    *Uf = reinterpret_cast<double *>(pu);
+    *part = reinterpret_cast<double *>(pp);
+  }
+  return off;
+}
+
+int64_t lowrank_step_workspace_bytes(int64_t n, int64_t C, int64_t r) {
+  return (int64_t)lr_step_layout(n, C, r, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                 nullptr);
+}
+
+// One low-rank encode_step (pipeline.py:84-121 with cx:394-426): t = target ->
+// Q0 (host-drawn q0, or drawn on the device from `key`) -> subspace iteration ->
+// body -> fused decode + state update + record.  Every launch is stream-ordered
+// device work, so the step can be captured in a CUDA graph (with a device key).
+int lowrank_encode_step(int mode, int64_t n, int64_t C, int64_t r, int iters, int int4, const void *x, int x_dtype,
+                        float *base, float *aux, const float *q0_in, uint32_t *key, int nwords, int step_word,
+                        uint8_t *body, void *ws, int64_t ws_bytes, double *record, cudaStream_t st) {
+  if ((int64_t)lr_step_layout(n, C, r, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                              nullptr) > ws_bytes) {
+    set_error("low-rank step workspace too small");
+    return CC_ERR_ARG;
+  }
+  float *t, *q0;
+  void *gws, *ews;
+  size_t gb, eb;
+  double *Uf, *part;
+  lr_step_layout(n, C, r, reinterpret_cast<uint8_t *>(ws), &t, &q0, &gws, &gb, &ews, &eb, &Uf, &part);
+  int rc = residual_target(mode, n, C, x, x_dtype, base, aux, t, st);
+  if (rc) return rc;
+  if (key) {
+    rc = gaussian_keyed(C, r, key, nwords, step_word, q0, gws, (int64_t)gb, st);
+    if (rc) return rc;
+  } else {
+    q0 = const_cast<float *>(q0_in);
+  }
+  rc = lowrank_encode(int4, n, C, r, iters, t, q0, body, nullptr, ews, (int64_t)eb, st);
+  if (rc) return rc;
+  double *WfT = Uf + n * r;
+  lr::k_unpack_factors_t<<<(unsigned)cdiv((n + C) * r, 256), 256, 0, st>>>(body, int4, n, C, (int)r, Uf, WfT);
+  dim3 g((unsigned)cdiv(C, lr::kThreads), (unsigned)cdiv(n, lr::kOARows));
+#define CC_LA3(MODE, XT, RM) \
+  lr::k_outer_apply<MODE, XT, RM><<<g, lr::kThreads, 0, st>>>(Uf, WfT, n, C, (int)r, (const XT *)x, t, base, aux, part)
+#define CC_LA(MODE, XT)                   \
+  do {                                    \
+    if (r <= 8) CC_LA3(MODE, XT, 8);      \
+    else if (r <= 16) CC_LA3(MODE, XT, 16); \
+    else CC_LA3(MODE, XT, 32);            \
+  } while (0)
+  if (x_dtype == CC_F32) {
+    if (mode == CC_WITH_FEEDBACK) CC_LA(CC_WITH_FEEDBACK, float);
+    else if (mode == CC_NO_FEEDBACK) CC_LA(CC_NO_FEEDBACK, float);
+    else CC_LA(CC_NAIVE, float);
+  } else {
+    if (mode == CC_WITH_FEEDBACK) CC_LA(CC_WITH_FEEDBACK, __nv_bfloat16);
+    else if (mode == CC_NO_FEEDBACK) CC_LA(CC_NO_FEEDBACK, __nv_bfloat16);
+    else CC_LA(CC_NAIVE, __nv_bfloat16);
+  }
+#undef CC_LA
+#undef CC_LA3
+  count_launch(2);
+  rc = sum_parts((int)(g.x * g.y), part, record, st);
+  if (rc) return rc;
+  return cuda_status("lowrank_encode_step");
 }
 
 static void keep_default_pool() {

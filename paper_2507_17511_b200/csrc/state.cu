@@ -16,6 +16,41 @@ template <int MODE, typename XT>
 __global__ void __launch_bounds__(256) k_target(const XT *__restrict__ x, const float *__restrict__ base,
                                                 const float *__restrict__ aux, float *__restrict__ t, int64_t total) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) & (sizeof(XT) == 2 ? 7 : 15)) |
+                    (reinterpret_cast<uintptr_t>(base) & 15) | (reinterpret_cast<uintptr_t>(aux) & 15) |
+                    (reinterpret_cast<uintptr_t>(t) & 15)) == 0;
+  if (vec) {  // 128-bit accesses, two quads per thread in flight
+    const int64_t nq = total / 4;
+    for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < nq; q0 += 2 * stride) {
+      float4 xx[2], bb[2], aa[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t q = q0 + u * stride;
+        xx[u] = bb[u] = aa[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (q < nq) {
+          xx[u] = Act<XT>::load4(x + 4 * q);
+          if constexpr (MODE == CC_WITH_FEEDBACK) bb[u] = *reinterpret_cast<const float4 *>(base + 4 * q);
+          if constexpr (MODE != CC_NAIVE) aa[u] = *reinterpret_cast<const float4 *>(aux + 4 * q);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t q = q0 + u * stride;
+        if (q < nq)
+          *reinterpret_cast<float4 *>(t + 4 * q) =
+              make_float4(target_of<MODE>(xx[u].x, bb[u].x, aa[u].x), target_of<MODE>(xx[u].y, bb[u].y, aa[u].y),
+                          target_of<MODE>(xx[u].z, bb[u].z, aa[u].z), target_of<MODE>(xx[u].w, bb[u].w, aa[u].w));
+      }
+    }
+    for (int64_t e = 4 * nq + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+      const float xx = Act<XT>::load1(x + e);
+      float bb = 0.f, aa = 0.f;
+      if constexpr (MODE == CC_WITH_FEEDBACK) bb = base[e];
+      if constexpr (MODE != CC_NAIVE) aa = aux[e];
+      t[e] = target_of<MODE>(xx, bb, aa);
+    }
+    return;
+  }
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
     const float xx = Act<XT>::load1(x + e);
     float bb = 0.f, aa = 0.f;
@@ -84,6 +119,12 @@ __global__ void __launch_bounds__(256) k_sum_parts(int nparts, const double *__r
     record[0] = x;
     record[1] = y;
   }
+}
+
+int sum_parts(int nparts, const double *part, double *record, cudaStream_t st) {
+  k_sum_parts<<<1, 256, 0, st>>>(nparts, part, record);
+  count_launch();
+  return cuda_status("sum_parts");
 }
 
 int residual_target(int mode, int64_t n, int64_t C, const void *x, int x_dtype, const float *base, const float *aux,

@@ -727,10 +727,12 @@ static int fuse_find(int64_t total) {
 
 static int h1_blocks(int64_t total) { return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), sm_count() * 2)); }
 
+int64_t topk_resident_workspace_bytes();
+
 int64_t topk_workspace_bytes(int64_t n, int64_t C, int64_t) {
   size_t b = 0;
   carve_topk(nullptr, n * C, true, h1_blocks(n * C), &b);
-  return (int64_t)b;
+  return std::max<int64_t>((int64_t)b, topk_resident_workspace_bytes());
 }
 
 static const size_t kZeroBytes = 2 * 4 * topk::kBins + 4 * topk::kBins3 + 3 * 256;

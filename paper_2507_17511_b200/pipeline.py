@@ -183,6 +183,8 @@ def encode_step(state, a_star, codec, rng=None, body_out=None):
                                              _lib.ptr(state.base), _lib.ptr(aux), _lib.ptr(body), _lib.ptr(ws),
                                              ws.numel(), _lib.ptr(rec), stream), "nm encode_step")
             payload = cx.NMBlockPayload(rows, cols, body, n, m)
+        elif kind == cx.CompressorKind.LOWRANK:
+            payload = _encode_step_lowrank(state, x, codec, rng, mode, aux, rec, body_out)
         elif tag is not None:
             nbytes = lib.cc_body_bytes(tag, rows, cols, 0)
             body = _body_slice(body_out, nbytes)
@@ -195,6 +197,37 @@ def encode_step(state, a_star, codec, rng=None, body_out=None):
             payload = _encode_step_generic(state, x, codec, rng, mode, aux, rec, body_out)
     state.step = t
     return payload, StepRecord(t, payload.nominal_bits, rec)
+
+
+def _encode_step_lowrank(state, x, codec, rng, mode, aux, rec, body_out):
+    """One fused low-rank encode_step (cc_lowrank_encode_step): target, Q0, subspace
+    iteration (cx:394-426), body, and the state update with the decode fused in.  Q0
+    comes from the caller's numpy Generator (host draw, cx:407) or, for a
+    linalg.DeviceKey, is drawn on the device (no host work: graph-capturable)."""
+    from .linalg import DeviceKey
+
+    if rng is None:
+        raise ValueError("lowrank encoding needs an rng")
+    lib = _lib.load()
+    rows, cols = state.shape
+    r = codec.rank
+    if not (1 <= r <= min(rows, cols)):
+        raise ShapeError(f"rank {r} out of range for shape {(rows, cols)}")
+    tag = _lib.CC_LOWRANK4 if codec.int4_factors else _lib.CC_LOWRANK
+    body = _body_slice(body_out, lib.cc_body_bytes(tag, rows, cols, r))
+    ws = cx.workspace(_lib.check(lib.cc_lowrank_step_workspace_bytes(rows, cols, r)), "lowrank_step")
+    if isinstance(rng, DeviceKey):
+        q0, key, nwords, step_word = None, rng.words, rng.nwords, rng.step_word
+    else:
+        q0 = cx.subspace_init(rng, cols, r)
+        q0 = cx._stage_h2d(q0, x.device)
+        key, nwords, step_word = None, 0, -1
+    _lib.check(lib.cc_lowrank_encode_step(mode, rows, cols, r, codec.iterations, int(codec.int4_factors),
+                                          _lib.ptr(x), cx.dtype_code(x), _lib.ptr(state.base), _lib.ptr(aux),
+                                          _lib.ptr(q0), _lib.ptr(key), nwords, step_word, _lib.ptr(body),
+                                          _lib.ptr(ws), ws.numel(), _lib.ptr(rec), _lib.stream_ptr()),
+               "lowrank encode_step")
+    return cx.LowRankPayload(rows, cols, body, r, codec.int4_factors)
 
 
 def _encode_step_generic(state, x, codec, rng, mode, aux, rec, body_out):

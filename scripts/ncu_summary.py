@@ -51,24 +51,44 @@ def report(path, out):
     open(out, "w").write("\n".join(lines) + "\n")
 
 
+_SCALE = {"nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "second": 1e9,
+          "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "%": 1.0, "": 1.0, "inst": 1.0}
+
+
 def launches(path, out):
+    """Per-kernel means of a `ncu --metrics ... --csv` launch list (times in ns,
+    bytes in B whatever unit ncu chose; 'n/a' entries skipped)."""
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     h = rows[hi]
     ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+    ui = h.index("Metric Unit") if "Metric Unit" in h else None
     agg = collections.defaultdict(lambda: collections.defaultdict(list))
     for r in rows[hi + 1:]:
         if len(r) > vi:
-            agg[r[ki][:90]][r[mi]].append(float(r[vi].replace(",", "")))
+            try:
+                v = float(r[vi].replace(",", ""))
+            except ValueError:
+                continue
+            if ui is not None:
+                v *= _SCALE.get(r[ui], 1.0)
+            agg[r[ki][:90]][r[mi]].append(v)
     tot = sum(sum(d["gpu__time_duration.sum"]) for d in agg.values()) or 1
+    extra = sorted({m for d in agg.values() for m in d} - {"gpu__time_duration.sum", "dram__bytes_read.sum",
+                                                           "dram__bytes_write.sum"})
     lines = [f"# per-kernel launch list summary of {path} (cold-cache, serialised by ncu)", "",
-             f"{'kernel':90s} {'n':>4s} {'mean_us':>9s} {'share':>6s} {'dramR_MB':>9s} {'dramW_MB':>9s}"]
+             f"{'kernel':90s} {'n':>4s} {'mean_us':>9s} {'share':>6s} {'dramR_MB':>9s} {'dramW_MB':>9s}"
+             + "".join(f" {m[:28]:>28s}" for m in extra)]
     for k, d in sorted(agg.items(), key=lambda kv: -sum(kv[1]["gpu__time_duration.sum"])):
         t = d["gpu__time_duration.sum"]
-        rd = d.get("dram__bytes_read.sum", [0])
-        wr = d.get("dram__bytes_write.sum", [0])
+        if not t:
+            continue
+        rd = d.get("dram__bytes_read.sum") or [0]
+        wr = d.get("dram__bytes_write.sum") or [0]
         lines.append(f"{k:90s} {len(t):4d} {sum(t) / len(t) / 1e3:9.2f} {100 * sum(t) / tot:5.1f}% "
-                     f"{sum(rd) / len(rd) / 1e6:9.1f} {sum(wr) / len(wr) / 1e6:9.1f}")
+                     f"{sum(rd) / len(rd) / 1e6:9.1f} {sum(wr) / len(wr) / 1e6:9.1f}"
+                     + "".join(f" {sum(d[m]) / len(d[m]) if d.get(m) else float('nan'):28.2f}" for m in extra))
+    lines.append(f"\n# total device time of the listed launches: {tot / 1e3:.1f} us")
     open(out, "w").write("\n".join(lines) + "\n")
 
 

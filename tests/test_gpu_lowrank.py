@@ -207,3 +207,65 @@ def test_tma_staged_projections_equal_register_staged(shape, r):
     finally:
         lib.cc_debug_lowrank_tma(2, 0)
     assert all(torch.equal(bodies[0], b) for b in bodies[1:])
+
+
+@pytest.mark.parametrize("mode", ["residual_with_feedback", "residual_no_feedback", "naive"])
+@pytest.mark.parametrize("int4", [False, True])
+def test_fused_step_device_key_equals_host_rng(mode, int4):
+    """cc_lowrank_encode_step with the start block drawn on the device (DeviceKey,
+    advancing step word) is bit-identical to the same step with the host draw from
+    spawn_rng(seed, 5, t) (pl:190), and the receiver mirrors the sender."""
+    cx, pl, linalg = _mods()
+    n, c = 256, 3072
+    xs = synth.flux_like(n, c, 5, seed=21)
+    spec = _spec(8, 2, int4)
+    a = pl.LayerState(mode, 1, torch.zeros(n, c, device="cuda"))
+    b = pl.LayerState(mode, 1, torch.zeros(n, c, device="cuda"))
+    rcv = pl.LayerState(mode, 1, torch.zeros(n, c, device="cuda"))
+    key = linalg.DeviceKey(9, 5, 2, advance=True)  # the first compressed step is t = 2
+    for t, x in enumerate(xs, start=1):
+        xd = torch.from_numpy(x).cuda().to(torch.bfloat16)
+        pa, ra = pl.encode_step(a, xd, spec, rng=linalg.spawn_rng(9, 5, t))
+        pb, rb = pl.encode_step(b, xd, spec, rng=key)
+        assert pa.body_bytes() == pb.body_bytes(), f"step {t}"
+        assert torch.equal(a.base, b.base) and torch.equal(a.feedback, b.feedback)
+        assert ra.compression_error == rb.compression_error
+        pl.decode_step(rcv, pl.device_message(t, 1, pb))
+        assert torch.equal(rcv.base, b.base)
+
+
+def test_lowrank_exchange_graph_replay_equals_eager():
+    """The low-rank patch-parallel step (sim_world P=4, rank 0) captured in a CUDA
+    graph with an advancing device key: replays reproduce the eager steps bit for
+    bit (the key's step word advances on the device)."""
+    cx, pl, linalg = _mods()
+    from paper_2507_17511_b200.comm import PatchParallelExchange
+
+    rows, cols, P = 1024, 3072, 4
+    spec = _spec(8, 2)
+    xs = [torch.from_numpy(x).cuda().to(torch.bfloat16)[: rows // P].contiguous()
+          for x in synth.flux_like(rows, cols, 6, seed=5)]
+    ea = PatchParallelExchange(rows, cols, spec, sim_world=(P, 0))
+    eb = PatchParallelExchange(rows, cols, spec, sim_world=(P, 0))
+    ka = linalg.DeviceKey(3, 6, 0, 2, advance=True)
+    kb = linalg.DeviceKey(3, 6, 0, 2, advance=True)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for e, k in ((ea, ka), (eb, kb)):
+            e.step(xs[0], rng=k)
+            e.step(xs[1], rng=k)
+        outs_a = []
+        for i in range(2, 6):
+            ea.step(xs[i], rng=ka)
+            outs_a.append(ea.reconstruction().clone())
+        g = torch.cuda.CUDAGraph()
+        eb.step(xs[2], rng=kb)  # warm the step's workspaces outside the capture
+        got = [eb.reconstruction().clone()]
+        with torch.cuda.graph(g, stream=s):
+            eb.step(xs[3], rng=kb)
+            s.wait_stream(eb.streams.decode)
+        eb.after_capture()
+        g.replay()  # encodes xs[3] with the key advanced to t = 4 on the device
+    torch.cuda.synchronize()
+    got.append(eb.reconstruction().clone())
+    assert torch.equal(got[0], outs_a[0]) and torch.equal(got[1], outs_a[1])
