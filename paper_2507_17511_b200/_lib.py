@@ -104,6 +104,7 @@ SIGNATURES = {
     "cc_debug_topk_resident_count": (_i64, []),
     "cc_debug_topk_timer": (None, [_p]),
     "cc_debug_orth_stamps": (None, [_p]),
+    "cc_debug_orth_cluster": (None, [_i32]),
 }
 # private test / profiling knobs (csrc/cc_debug.h), not part of the public ABI
 DEBUG_HEADER = os.path.join(HERE, "csrc", "cc_debug.h")

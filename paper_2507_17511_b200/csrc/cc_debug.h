@@ -68,6 +68,9 @@ CC_API void cc_debug_topk_timer(void *dev_buf);
 /* profiling only: device buffer of 16 u64 clock64 stamps of the single-CTA
  * CholQR2 (k_orth1) phases (NULL disables) */
 CC_API void cc_debug_orth_stamps(void *dev_buf);
+/* low-rank orthogonalisation: 1 = thread-block-cluster CholQR2 (default),
+ * 0 = the single-CTA / cooperative-grid forms (A/B and cross-checks) */
+CC_API void cc_debug_orth_cluster(int enable);
 
 #ifdef __cplusplus
 }

@@ -542,7 +542,10 @@ __device__ __forceinline__ void chol8_regs(const double (*G)[17], double (*Rm)[1
   if (degenerate && c == 0) *bad = 1;
   if (c < 8) {
 #pragma unroll
-    for (int b = 0; b < 8; ++b) Rm[c][b] = b >= c ? g[c][b] : 0.0;
+    for (int a = 0; a < 8; ++a)  // row a of R by lane a (compile-time indices: g stays in registers)
+      if (a == c)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) Rm[a][b] = b >= a ? g[a][b] : 0.0;
     double x[8];  // column c of R^-1
 #pragma unroll
     for (int i = 7; i >= 0; --i) {
@@ -726,6 +729,127 @@ __global__ void __launch_bounds__(kOrth1Threads, 1) k_orth1(const float *__restr
   __syncthreads();
   stamp(10);
   if (stp && tid == 0) stp[11] = bad;
+}
+
+// ---------------------------------------------------------------------------
+// CholQR2 on a thread-block CLUSTER of kOrthCl CTAs (distributed shared memory):
+// CTA q keeps rows [q m8 / kOrthCl, ...) of the block (f64, column-major), so the
+// f64 tensor-pipe work (Gram, M R^-1) and the loads / stores are split kOrthCl
+// ways; per pass the CTAs' 8x8 Gram partials are exchanged through DSMEM (one
+// cluster barrier) and summed in the same order by every CTA, which then factors
+// the Gram redundantly (identical R^-1 everywhere, no broadcast).  r <= 16.
+// ---------------------------------------------------------------------------
+constexpr int kOrthCl = 8;
+constexpr int kOrthClThreads = 256;
+
+template <int RP>
+__global__ void __launch_bounds__(kOrthClThreads, 1) k_orth_cl(const float *__restrict__ Min, float *__restrict__ out,
+                                                                int64_t m, int r, double *__restrict__ scratch,
+                                                                unsigned long long seed) {
+  namespace cg = cooperative_groups;
+  constexpr int W = kOrthClThreads / 32, RB = RP / 8, LD = 17;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int q = (int)cluster.block_rank();
+  extern __shared__ __align__(16) uint8_t ocsm[];
+  const int64_t m8 = (m + 7) & ~int64_t(7);
+  const int64_t t0 = (int64_t)q * (m8 / 8) / kOrthCl, t1 = (int64_t)(q + 1) * (m8 / 8) / kOrthCl;  // 8-row tiles
+  const int64_t r0 = 8 * t0, nr = 8 * (t1 - t0);  // this CTA's rows [r0, r0 + nr)
+  const int64_t mp = nr | 1;
+  double *M = reinterpret_cast<double *>(ocsm);  // [RP][mp]
+  __shared__ double G[16][LD], Rm[16][LD], Ri[16][LD];
+  __shared__ double part[W][RB * RB][64];
+  __shared__ double cpart[2][RB * RB][64];  // this CTA's Gram partial per pass (read by the cluster)
+  __shared__ double red[kOrthClThreads / 32], coef[kMaxR];
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  for (int64_t e = tid; e < nr * RP; e += kOrthClThreads) {
+    const int64_t i = e / RP;
+    const int k = (int)(e % RP);
+    const int64_t gi = r0 + i;
+    M[k * mp + i] = (gi < m && k < r) ? (double)Min[gi * r + k] : 0.0;
+  }
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    double acc[RB * RB][2];
+#pragma unroll
+    for (int t = 0; t < RB * RB; ++t) acc[t][0] = acc[t][1] = 0.0;
+    for (int64_t ks = warp; ks < nr / 4; ks += W) {
+      double v[RB];
+#pragma unroll
+      for (int b = 0; b < RB; ++b) v[b] = M[(8 * b + gq) * mp + 4 * ks + tq];
+#pragma unroll
+      for (int ra = 0; ra < RB; ++ra)
+#pragma unroll
+        for (int rc = ra; rc < RB; ++rc) dmma884(acc[ra * RB + rc][0], acc[ra * RB + rc][1], v[ra], v[rc]);
+    }
+#pragma unroll
+    for (int t = 0; t < RB * RB; ++t) {
+      part[warp][t][gq * 8 + 2 * tq] = acc[t][0];
+      part[warp][t][gq * 8 + 2 * tq + 1] = acc[t][1];
+    }
+    __syncthreads();
+    for (int o = tid; o < RB * RB * 64; o += kOrthClThreads) {  // CTA partial: warps in order
+      double v = 0.0;
+      for (int w = 0; w < W; ++w) v += part[w][o / 64][o % 64];
+      cpart[pass][o / 64][o % 64] = v;
+    }
+    cluster.sync();  // every CTA's partial of this pass is published
+    for (int o = tid; o < RP * RP; o += kOrthClThreads) {  // G entry (a, c): CTAs summed in rank order
+      const int a = o / RP, c = o % RP;
+      if (a <= c && c < r) {
+        const int t = (a / 8) * RB + c / 8, idx = (a % 8) * 8 + (c % 8);
+        double v = 0.0;
+        for (int cq = 0; cq < kOrthCl; ++cq) {
+          const double *rp = cluster.map_shared_rank(&cpart[pass][0][0], cq);
+          v += rp[t * 64 + idx];
+        }
+        G[a][c] = v;
+        G[c][a] = v;
+      }
+    }
+    for (int e = tid; e < 16 * LD; e += kOrthClThreads) {
+      Rm[e / LD][e % LD] = 0.0;
+      Ri[e / LD][e % LD] = 0.0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      if (RP == 8 && r == 8) chol8_regs(G, Rm, Ri, &bad);
+      else chol_rinv_regs<RP, LD>(G, Rm, Ri, r, &bad);
+    }
+    __syncthreads();
+    double bfr[RB][RP / 4];
+#pragma unroll
+    for (int cb = 0; cb < RB; ++cb)
+#pragma unroll
+      for (int ks = 0; ks < RP / 4; ++ks) bfr[cb][ks] = Ri[4 * ks + tq][8 * cb + gq];
+    for (int64_t tile = warp; tile < nr / 8; tile += W) {
+      const int64_t i = 8 * tile + gq;
+      double afr[RP / 4];
+#pragma unroll
+      for (int ks = 0; ks < RP / 4; ++ks) afr[ks] = M[(4 * ks + tq) * mp + i];
+      __syncwarp();
+#pragma unroll
+      for (int cb = 0; cb < RB; ++cb) {
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < RP / 4; ++ks) dmma884(d0, d1, afr[ks], bfr[cb][ks]);
+        M[(8 * cb + 2 * tq) * mp + i] = d0;
+        M[(8 * cb + 2 * tq + 1) * mp + i] = d1;
+      }
+    }
+    __syncthreads();
+  }
+  if (!bad) {
+    for (int64_t e = tid; e < nr * r; e += kOrthClThreads) {
+      const int64_t i = e / r;
+      if (r0 + i < m) out[(r0 + i) * r + e % r] = (float)M[(e % r) * mp + i];
+    }
+  } else if (q == 0) {  // every CTA saw the same pivots: CTA 0 alone runs CGS2 (la:77-112)
+    cgs2_block(Min, scratch, out, m, r, seed, red, coef);
+  }
+  cluster.sync();  // no CTA exits while another may still read its partials
 }
 
 __global__ void k_to32(const double *__restrict__ in, float *__restrict__ out, int64_t cnt) {
@@ -977,6 +1101,8 @@ int64_t lowrank_workspace_bytes(int64_t n, int64_t C, int64_t r) {
 }
 
 static unsigned long long g_lr_seed = 0x5eed5eedULL;
+static int g_orth_cluster = 1;  // 1: cluster CholQR2 (k_orth_cl), 0: single CTA / grid forms (A/B)
+void set_orth_cluster(int on) { g_orth_cluster = on; }
 
 void set_orth1_stamps(void *buf) {
   unsigned long long *p = reinterpret_cast<unsigned long long *>(buf);
@@ -987,9 +1113,11 @@ void set_orth1_stamps(void *buf) {
 static void orth(const float *M, float *out, int64_t m, int r, const lr::Work &w, cudaStream_t st) {
   using namespace lr;
   const int rp = r <= 8 ? 8 : 16;
-  const size_t need = (size_t)(((m + 7) & ~int64_t(7)) | 1) * rp * 8;
-  if (r <= 16) {  // one CTA, no grid sync, when the padded block fits in shared memory
-    const void *kern = rp == 8 ? (const void *)k_orth1<8> : (const void *)k_orth1<16>;
+  if (r <= 16 && g_orth_cluster) {  // cluster of kOrthCl CTAs (DSMEM Gram exchange)
+    const int64_t m8 = (m + 7) & ~int64_t(7);
+    const int64_t rows_max = 8 * cdiv(m8 / 8, kOrthCl);
+    const size_t need = (size_t)(rows_max | 1) * rp * 8;
+    const void *kern = rp == 8 ? (const void *)k_orth_cl<8> : (const void *)k_orth_cl<16>;
     static size_t max_dyn[2] = {0, 0};
     size_t &md = max_dyn[rp == 16];
     if (md == 0) {
@@ -998,17 +1126,31 @@ static void orth(const float *M, float *out, int64_t m, int r, const lr::Work &w
       md = 227 * 1024 - fa.sharedSizeBytes - 1024;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)md);
     }
-    if (need <= md) {
+    if (need <= md && m >= 8 * kOrthCl) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(kOrthCl);
+      cfg.blockDim = dim3(kOrthClThreads);
+      cfg.dynamicSmemBytes = need;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = kOrthCl;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
       unsigned long long seed = g_lr_seed++;
       double *scratch = w.M64;
-      void *args[] = {&M, &out, &m, &r, &scratch, &seed};
-      if (cudaLaunchKernel(kern, dim3(1), dim3(kOrth1Threads), args, need, st) == cudaSuccess) {
+      const cudaError_t e = rp == 8 ? cudaLaunchKernelEx(&cfg, k_orth_cl<8>, M, out, m, r, scratch, seed)
+                                    : cudaLaunchKernelEx(&cfg, k_orth_cl<16>, M, out, m, r, scratch, seed);
+      if (e == cudaSuccess) {
         count_launch();
         return;
       }
       cudaGetLastError();
     }
   }
+  const size_t need = (size_t)(((m + 7) & ~int64_t(7)) | 1) * rp * 8;
   {
     const int nb = (int)cdiv(m, kGramRows);
     const size_t smem = sizeof(double) * (size_t)(kGramRows + 3 * kMaxR) * (kMaxR + 1);

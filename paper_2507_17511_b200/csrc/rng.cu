@@ -14,12 +14,17 @@
 //                 one u64 on the fast path (~99% of draws); the wedge / tail paths
 //                 consume further u64s, so the stream positions of the draws are
 //                 data dependent.
-// Parallel form (one CTA): every thread jumps to its slice of stream positions and
-// generates them; positions that fail the fast test are evaluated in parallel AS
-// IF a draw started there (value, u64s consumed); one thread then walks the short
-// list of such positions in order to find which really start a draw and how far
-// each shifts the draws after it; finally every output index maps to its position
-// (fast draw) or to an evaluated slow draw by a binary search over the shifts.
+// Parallel form (two launches):
+//   k_gauss_gen   CTA c generates stream positions [c P, (c + 1) P) by jump-ahead
+//                 (16 per thread) and lists the positions that fail the fast test;
+//                 the last CTA to finish (ticket) evaluates every listed position AS
+//                 IF a draw started there (value, u64s consumed), decides which of
+//                 them really start a draw (a listed position is skipped when a real
+//                 slow draw before it consumed it: short ranges, resolved in a few
+//                 parallel rounds) and, by a scan, the output index of each real slow
+//                 draw and the position shift of the draws after it
+//   k_gauss_out   every output index maps to its stream position (fast draw) or to
+//                 an evaluated slow draw, by a binary search over the shifts
 // Floating point follows numpy's C expression order with no contraction; exp /
 // log1p are CUDA's (<= 1 ulp from glibc), which can only matter when a wedge / tail
 // acceptance test or the f32 rounding of a tail value lands within an ulp.
@@ -33,7 +38,6 @@ namespace rng {
 using u128 = unsigned __int128;
 constexpr int kThreads = 1024;
 constexpr int kMaxWords = 16;
-constexpr int kSmemEvents = 4096;  // slow draws searched in shared memory (~1% of the draws)
 
 __device__ __forceinline__ u128 pcg_mult() {
   return ((u128)0x2360ED051FC65DA4ull << 64) | (u128)0x4385DF649FCCF645ull;
@@ -112,7 +116,23 @@ struct Shared {
 
 // one draw of random_standard_normal starting at stream position p (raw[p] = the
 // (p+1)-th output); returns the value and sets *next to the first unused position
-__device__ double draw_at(const uint64_t *raw, int64_t npos, const Shared &sh, int64_t p, int64_t *next) {
+// the ziggurat tables staged in shared memory (random per-lane indices: a gather from
+// shared memory instead of a serialised constant-cache access)
+struct Zig {
+  const uint64_t *ki;
+  const double *wi, *fi;
+};
+
+__device__ __forceinline__ void stage_tables(uint64_t *ki, double *wi, double *fi) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    ki[i] = zig::kKi[i];
+    wi[i] = zig::kWi[i];
+    fi[i] = zig::kFi[i];
+  }
+}
+
+__device__ double draw_at(const uint64_t *raw, int64_t npos, const Shared &sh, const Zig &zt, int64_t p,
+                          int64_t *next) {
   auto raw_at = [&](int64_t q) -> uint64_t {
     return q < npos ? __ldcg(raw + q) : pcg_out(pcg_advance(sh.state0, sh.inc, (uint64_t)q + 1));
   };
@@ -121,9 +141,9 @@ __device__ double draw_at(const uint64_t *raw, int64_t npos, const Shared &sh, i
     const int idx = (int)(r & 0xff);
     r >>= 8;
     const uint64_t sign = r & 1, rabs = (r >> 1) & 0x000fffffffffffffull;
-    double x = __dmul_rn((double)rabs, zig::kWi[idx]);
+    double x = __dmul_rn((double)rabs, zt.wi[idx]);
     if (sign) x = -x;
-    if (rabs < zig::kKi[idx]) {
+    if (rabs < zt.ki[idx]) {
       *next = p;
       return x;
     }
@@ -137,8 +157,8 @@ __device__ double draw_at(const uint64_t *raw, int64_t npos, const Shared &sh, i
         }
       }
     } else {
-      const double f = __dadd_rn(__dmul_rn(__dsub_rn(zig::kFi[idx - 1], zig::kFi[idx]), next_double(raw_at(p++))),
-                                 zig::kFi[idx]);
+      const double f = __dadd_rn(__dmul_rn(__dsub_rn(zt.fi[idx - 1], zt.fi[idx]), next_double(raw_at(p++))),
+                                 zt.fi[idx]);
       if (f < exp(__dmul_rn(__dmul_rn(-0.5, x), x))) {
         *next = p;
         return x;
@@ -148,135 +168,267 @@ __device__ double draw_at(const uint64_t *raw, int64_t npos, const Shared &sh, i
 }
 
 struct Work {
-  uint64_t *raw;    // [npos]
-  uint32_t *slow;   // [npos] positions failing the fast test, ascending
-  double *sval;     // [npos] value of a draw starting there
-  uint32_t *scons;  // [npos] u64s it consumes
-  uint32_t *ev_o;   // [npos] output index of each real slow draw
-  uint32_t *ev_sh;  // [npos] position shift (pos - out) of the draws after it
-  double *ev_v;     // [npos]
+  uint64_t *raw;      // [npos]
+  uint32_t *cand;     // [nblk][kGenPos] positions failing the fast test (per-CTA segment, ascending)
+  uint32_t *ncand;    // [nblk]
+  uint32_t *ev_o;     // [kMaxEv] output index of each real slow draw (ascending)
+  uint32_t *ev_sh;    // [kMaxEv] position shift (pos - out) of the draws after it
+  double *ev_v;       // [kMaxEv]
+  uint32_t *ctl;      // [0] ticket, [1] event count
+  uint32_t *sslow;    // [npos] sequential-walk fallback: all candidates in order
+  uint32_t *scons;    // [npos]
+  double *sval;       // [npos]
 };
 
-__global__ void __launch_bounds__(kThreads, 1) k_gauss(uint32_t *key, int nw, int step_word, int64_t M, int64_t npos,
-                                                       Work w, float *__restrict__ out) {
+constexpr int kGenThreads = 256, kGenPer = 16, kGenPos = kGenThreads * kGenPer;  // positions per CTA
+constexpr int kMaxCand = 2048;  // slow candidates resolved in shared memory (~0.7% of positions)
+constexpr int kMaxEv = kMaxCand;
+constexpr int kOutThreads = 256;
+
+__device__ __forceinline__ bool slow_pos(uint64_t r, const uint64_t *ki) {
+  return ((r >> 9) & 0x000fffffffffffffull) >= ki[r & 0xff];
+}
+
+__global__ void __launch_bounds__(kGenThreads) k_gauss_gen(const uint32_t *__restrict__ key, int nw, int64_t M,
+                                                            int64_t npos, Work w) {
   __shared__ Shared sh;
+  __shared__ uint32_t wcnt[kGenThreads / 32], s_last;
+  __shared__ uint32_t c_pos[kMaxCand];
+  __shared__ uint8_t c_cons[kMaxCand], c_real[kMaxCand];
+  __shared__ double c_val[kMaxCand];
+  __shared__ uint64_t tki[256];
+  __shared__ double twi[256], tfi[256];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  stage_tables(tki, twi, tfi);
+  const Zig zt{tki, twi, tfi};
   if (tid == 0) {
     uint32_t kw[kMaxWords];
     for (int i = 0; i < nw; ++i) kw[i] = key[i];
     seed_pcg(kw, nw, sh.state0, sh.inc);
   }
   __syncthreads();
-  // 1. raw stream: thread t generates positions [t cpt, (t + 1) cpt)
-  const int64_t cpt = (npos + kThreads - 1) / kThreads;
-  const int64_t p0 = min64(npos, (int64_t)tid * cpt), p1 = min64(npos, p0 + cpt);
-  uint32_t nslow = 0;
+  // ---- generate this thread's kGenPer positions ----
+  const int64_t p0 = (int64_t)blockIdx.x * kGenPos + (int64_t)tid * kGenPer;
+  uint32_t slowmask = 0;
   {
-    u128 s = pcg_advance(sh.state0, sh.inc, (uint64_t)p0);
+    u128 st = pcg_advance(sh.state0, sh.inc, (uint64_t)p0);
     const u128 m = pcg_mult(), inc = sh.inc;
-    for (int64_t p = p0; p < p1; ++p) {
-      s = s * m + inc;
-      const uint64_t r = pcg_out(s);
-      w.raw[p] = r;
-      const int idx = (int)(r & 0xff);
-      nslow += ((r >> 9) & 0x000fffffffffffffull) >= zig::kKi[idx];
+#pragma unroll
+    for (int k = 0; k < kGenPer; ++k) {
+      st = st * m + inc;
+      if (p0 + k < npos) {
+        const uint64_t r = pcg_out(st);
+        w.raw[p0 + k] = r;
+        slowmask |= (uint32_t)slow_pos(r, tki) << k;
+      }
     }
   }
-  // 2. ordered list of slow positions (block exclusive scan of the per-thread counts)
-  uint32_t incl = nslow;
+  // ---- this CTA's candidate list (ascending), per-CTA segment ----
+  const uint32_t nl = __popc(slowmask);
+  uint32_t incl = nl;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
-  if (lane == 31) sh.wsum[warp] = incl;
+  if (lane == 31) wcnt[warp] = incl;
   __syncthreads();
-  if (warp == 0) {
-    uint32_t v = sh.wsum[lane];
+  uint32_t off = incl - nl;
+  for (int i = 0; i < warp; ++i) off += wcnt[i];
+  uint32_t *seg = w.cand + (size_t)blockIdx.x * kGenPos;
+  for (uint32_t mm = slowmask; mm; mm &= mm - 1) seg[off++] = (uint32_t)(p0 + __ffs(mm) - 1);
+  if (tid == kGenThreads - 1) w.ncand[blockIdx.x] = off;
+  // ---- the last CTA resolves the slow draws ----
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&w.ctl[0], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // gather every CTA's candidates in position order
+  __shared__ uint32_t s_nc[1024];
+  for (unsigned b = tid; b < gridDim.x && b < 1024; b += kGenThreads) s_nc[b] = __ldcg(w.ncand + b);
+  __syncthreads();
+  uint32_t total = 0;
+  for (unsigned b = 0; b < gridDim.x; ++b) {
+    const uint32_t nb = b < 1024 ? s_nc[b] : __ldcg(w.ncand + b);
+    for (uint32_t i = tid; i < nb; i += kGenThreads)
+      if (total + i < (uint32_t)kMaxCand) c_pos[total + i] = __ldcg(w.cand + (size_t)b * kGenPos + i);
+    total += nb;
+  }
+  __syncthreads();
+  if (total > (uint32_t)kMaxCand) {  // never in practice (~1% of positions are slow): sequential walk
+    if (tid == 0) {
+      uint32_t n = 0;
+      for (unsigned b = 0; b < gridDim.x; ++b) {
+        const uint32_t nb = __ldcg(w.ncand + b);
+        for (uint32_t i = 0; i < nb; ++i) w.sslow[n++] = __ldcg(w.cand + (size_t)b * kGenPos + i);
+      }
+      int64_t pos = 0, j = 0;
+      uint32_t nev = 0;
+      for (uint32_t i = 0; i < n && j < M; ++i) {
+        const int64_t p = w.sslow[i];
+        if (p < pos) continue;
+        const int64_t run = p - pos;
+        if (j + run >= M) break;
+        j += run;
+        int64_t nx;
+        const double v = draw_at(w.raw, npos, sh, zt, p, &nx);
+        pos = nx;
+        if (nev < (uint32_t)kMaxEv) {
+          w.ev_o[nev] = (uint32_t)j;
+          w.ev_v[nev] = v;
+          w.ev_sh[nev] = (uint32_t)(pos - (j + 1));
+        }
+        ++nev;
+        ++j;
+      }
+      w.ctl[1] = nev;
+      w.ctl[0] = 0u;
+    }
+    return;
+  }
+  // evaluate every candidate as a draw start
+  for (uint32_t i = tid; i < total; i += kGenThreads) {
+    int64_t nx;
+    c_val[i] = draw_at(w.raw, npos, sh, zt, c_pos[i], &nx);
+    c_cons[i] = (uint8_t)min64(nx - (int64_t)c_pos[i], 255);  // a draw never takes 255 u64s
+    c_real[i] = 1u;
+  }
+  __syncthreads();
+  // real starts: a candidate is skipped iff a REAL candidate before it consumed it.
+  // Consumed ranges are a few positions long, so only the nearest preceding
+  // candidates can cover one; iterate to the fixed point (a couple of rounds).
+  __shared__ int changed;
+  for (int round = 0; round < 64; ++round) {
+    if (tid == 0) changed = 0;
+    __syncthreads();
+    uint32_t nr[16];
+    int nk = 0;
+    for (uint32_t k = tid; k < total; k += kGenThreads) {
+      uint32_t real = 1u;
+      for (int i = (int)k - 1; i >= 0; --i) {
+        if ((int64_t)c_pos[i] + 64 < (int64_t)c_pos[k]) break;  // no draw consumes 64 u64s
+        if (c_real[i] && c_pos[i] + c_cons[i] > c_pos[k]) {
+          real = 0u;
+          break;
+        }
+      }
+      if (nk < 16) nr[nk] = real;
+      ++nk;
+    }
+    __syncthreads();
+    nk = 0;
+    for (uint32_t k = tid; k < total; k += kGenThreads) {
+      const uint32_t real = nk < 16 ? nr[nk] : 1u;
+      ++nk;
+      if (real != c_real[k]) {
+        c_real[k] = real;
+        changed = 1;
+      }
+    }
+    __syncthreads();
+    if (!changed) break;
+  }
+  // output index of real candidate k: p_k minus the extra positions consumed by the
+  // real slow draws before it; shift after it = p_k + cons_k - (out_k + 1)
+  // block scan over the candidates (thread t: candidates [t K, t K + K)): events
+  // before each real one (event slot) and extra positions consumed before it
+  {
+    constexpr int K = kMaxCand / kGenThreads;
+    uint32_t ne = 0, ex = 0;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      const uint32_t k = tid * K + u;
+      if (k < total && c_real[k]) {
+        ++ne;
+        ex += c_cons[k] - 1u;
+      }
+    }
+    // pack (events, extra) into one 64-bit scan value
+    unsigned long long v = ((unsigned long long)ne << 40) | ex, incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += y;
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    sh.wsum[lane] = v;
-    if (lane == 31) sh.nslow = v;
-  }
-  __syncthreads();
-  {
-    uint32_t o = (warp ? sh.wsum[warp - 1] : 0u) + incl - nslow;
-    for (int64_t p = p0; p < p1; ++p) {
-      const uint64_t r = w.raw[p];
-      if (((r >> 9) & 0x000fffffffffffffull) >= zig::kKi[r & 0xff]) w.slow[o++] = (uint32_t)p;
+    __shared__ unsigned long long wsum64[kGenThreads / 32];
+    if (lane == 31) wsum64[warp] = incl;
+    __syncthreads();
+    unsigned long long before = incl - v;
+    for (int i = 0; i < warp; ++i) before += wsum64[i];
+    uint32_t slot = (uint32_t)(before >> 40), extra = (uint32_t)(before & ((1ull << 40) - 1));
+    __shared__ uint32_t s_nev;
+    if (tid == 0) s_nev = 0xffffffffu;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      const uint32_t k = tid * K + u;
+      if (k < total && c_real[k]) {
+        const int64_t o = (int64_t)c_pos[k] - extra;  // output index of this slow draw
+        extra += c_cons[k] - 1u;
+        if (o < M) {
+          w.ev_o[slot] = (uint32_t)o;
+          w.ev_v[slot] = c_val[k];
+          w.ev_sh[slot] = extra;  // shift (position - output) of the draws after it
+        } else {
+          atomicMin(&s_nev, slot);  // the first real slow draw at or past M ends the list
+        }
+        ++slot;
+      }
+    }
+    __syncthreads();
+    if (tid == kGenThreads - 1) {
+      w.ctl[1] = min(s_nev, slot);
+      w.ctl[0] = 0u;  // ticket ready for the next launch
     }
   }
-  __syncthreads();
-  const uint32_t ns = sh.nslow;
-  // 3. every slow position evaluated as a draw start
-  for (uint32_t i = tid; i < ns; i += kThreads) {
-    int64_t nx;
-    w.sval[i] = draw_at(w.raw, npos, sh, w.slow[i], &nx);
-    w.scons[i] = (uint32_t)(nx - w.slow[i]);
+}
+
+__global__ void __launch_bounds__(kOutThreads) k_gauss_out(uint32_t *key, int nw, int step_word, int64_t M,
+                                                            int64_t npos, Work w, float *__restrict__ out) {
+  __shared__ Shared sh;
+  __shared__ uint32_t s_o[kMaxEv], s_sh[kMaxEv];
+  __shared__ uint64_t tki[256];
+  __shared__ double twi[256], tfi[256];
+  const int tid = threadIdx.x;
+  stage_tables(tki, twi, tfi);
+  const Zig zt{tki, twi, tfi};
+  const uint32_t nev = min(__ldcg(w.ctl + 1), (uint32_t)kMaxEv);
+  for (uint32_t i = tid; i < nev; i += kOutThreads) {
+    s_o[i] = __ldcg(w.ev_o + i);
+    s_sh[i] = __ldcg(w.ev_sh + i);
   }
-  __syncthreads();
-  // 4. walk: which slow positions start a draw, and the position shift after each
   if (tid == 0) {
-    int64_t pos = 0, j = 0;
-    uint32_t nev = 0;
-    for (uint32_t i = 0; i < ns && j < M; ++i) {
-      const int64_t p = w.slow[i];
-      if (p < pos) continue;  // consumed inside an earlier slow draw
-      const int64_t run = p - pos;
-      if (j + run >= M) break;  // the remaining draws are all fast
-      j += run;
-      pos = p + w.scons[i];
-      w.ev_o[nev] = (uint32_t)j;
-      w.ev_v[nev] = w.sval[i];
-      w.ev_sh[nev] = (uint32_t)(pos - (j + 1));
-      ++nev;
-      ++j;
-    }
-    sh.nev = nev;
+    uint32_t kw[kMaxWords];
+    for (int i = 0; i < nw; ++i) kw[i] = key[i];
+    seed_pcg(kw, nw, sh.state0, sh.inc);  // only for draws past the generated positions
   }
   __syncthreads();
-  const uint32_t nev = sh.nev;
-  // the event indices and shifts in shared memory for the searches (global beyond)
-  __shared__ uint32_t s_o[kSmemEvents], s_sh[kSmemEvents];
-  const bool in_smem = nev <= (uint32_t)kSmemEvents;
-  if (in_smem) {
-    for (uint32_t i = tid; i < nev; i += kThreads) {
-      s_o[i] = __ldcg(w.ev_o + i);
-      s_sh[i] = __ldcg(w.ev_sh + i);
-    }
-  }
-  __syncthreads();
-  const uint32_t *eo = in_smem ? s_o : w.ev_o;
-  const uint32_t *esh = in_smem ? s_sh : w.ev_sh;
-  // 5. outputs: fast draw at position j + shift, or an evaluated slow draw
-  for (int64_t j = tid; j < M; j += kThreads) {
-    // last event with ev_o <= j
-    int lo = 0, hi = (int)nev;  // invariant: events [0, lo) have ev_o <= j
+  const int64_t j0 = (int64_t)blockIdx.x * kOutThreads * 4 + tid;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t j = j0 + u * kOutThreads;
+    if (j >= M) break;
+    int lo = 0, hi = (int)nev;  // events [0, lo) have ev_o <= j
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if ((int64_t)eo[mid] <= j) lo = mid + 1;
+      if ((int64_t)s_o[mid] <= j) lo = mid + 1;
       else hi = mid;
     }
     double v;
-    if (lo > 0 && (int64_t)eo[lo - 1] == j) {
+    if (lo > 0 && (int64_t)s_o[lo - 1] == j) {
       v = __ldcg(w.ev_v + lo - 1);
     } else {
-      const int64_t p = j + (lo > 0 ? (int64_t)esh[lo - 1] : 0);
+      const int64_t p = j + (lo > 0 ? (int64_t)s_sh[lo - 1] : 0);
       int64_t nx;
-      v = draw_at(w.raw, npos, sh, p, &nx);  // fast path (or past the generated positions)
+      v = draw_at(w.raw, npos, sh, zt, p, &nx);  // a fast draw (or past the generated positions)
     }
     out[j] = (float)v;
   }
-  if (tid == 0 && step_word >= 0) key[step_word] += 1u;  // the next step's key (graph replays)
+  if (blockIdx.x == 0 && tid == 0 && step_word >= 0) key[step_word] += 1u;  // the next step's key
 }
 
-// generated stream positions: ~1% of draws take the slow paths and consume a few
-// extra u64s, so M / 8 + 1024 spare positions are never exhausted in practice; a
-// draw that still reaches past them is evaluated from jump-ahead states (correct
-// as long as no slow draw starts beyond the generated positions)
 static int64_t npos_for(int64_t M) { return M + M / 8 + 1024; }
 
 static Work carve(void *ws, int64_t npos, size_t *bytes) {
@@ -288,13 +440,17 @@ static Work carve(void *ws, int64_t npos, size_t *bytes) {
     off = align_up(off + sz, 256);
     return q;
   };
+  const int64_t nblk = cdiv(npos, kGenPos);
   w.raw = reinterpret_cast<uint64_t *>(take(8 * npos));
-  w.slow = reinterpret_cast<uint32_t *>(take(4 * npos));
-  w.sval = reinterpret_cast<double *>(take(8 * npos));
+  w.cand = reinterpret_cast<uint32_t *>(take(4 * (size_t)nblk * kGenPos));
+  w.ncand = reinterpret_cast<uint32_t *>(take(4 * nblk));
+  w.ev_o = reinterpret_cast<uint32_t *>(take(4 * kMaxEv));
+  w.ev_sh = reinterpret_cast<uint32_t *>(take(4 * kMaxEv));
+  w.ev_v = reinterpret_cast<double *>(take(8 * kMaxEv));
+  w.ctl = reinterpret_cast<uint32_t *>(take(256));
+  w.sslow = reinterpret_cast<uint32_t *>(take(4 * npos));
   w.scons = reinterpret_cast<uint32_t *>(take(4 * npos));
-  w.ev_o = reinterpret_cast<uint32_t *>(take(4 * npos));
-  w.ev_sh = reinterpret_cast<uint32_t *>(take(4 * npos));
-  w.ev_v = reinterpret_cast<double *>(take(8 * npos));
+  w.sval = reinterpret_cast<double *>(take(8 * npos));
   if (bytes) *bytes = off;
   return w;
 }
@@ -325,8 +481,19 @@ int gaussian_keyed(int64_t rows, int64_t cols, uint32_t *key, int nwords, int st
     set_error("gaussian workspace too small");
     return CC_ERR_ARG;
   }
-  rng::k_gauss<<<1, rng::kThreads, 0, st>>>(key, nwords, step_word, M, npos, rng::carve(ws, npos, nullptr), out);
-  count_launch();
+  const rng::Work w = rng::carve(ws, npos, nullptr);
+  // the ticket word must start at zero: the workspace is the caller's, so zero it on
+  // first use of this workspace (every launch leaves it zero afterwards)
+  static thread_local const void *zeroed = nullptr;
+  if (zeroed != ws) {
+    cudaMemsetAsync(w.ctl, 0, 256, st);
+    zeroed = ws;
+  }
+  const unsigned nblk = (unsigned)cdiv(npos, rng::kGenPos);
+  rng::k_gauss_gen<<<nblk, rng::kGenThreads, 0, st>>>(key, nwords, M, npos, w);
+  rng::k_gauss_out<<<(unsigned)cdiv(M, 4 * rng::kOutThreads), rng::kOutThreads, 0, st>>>(key, nwords, step_word, M,
+                                                                                          npos, w, out);
+  count_launch(2);
   return cuda_status("gaussian_keyed");
 }
 

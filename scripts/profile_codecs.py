@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--keep", type=float, default=0.01)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--time", action="store_true", help="print CUDA-event µs per step instead of profiling")
+    ap.add_argument("--device-key", action="store_true", help="low-rank: draw Q0 on the device (linalg.DeviceKey)")
     a = ap.parse_args()
     n, c = a.rows, a.cols
     kind = cx.CompressorKind(a.codec)
@@ -41,13 +42,14 @@ def main():
     xs = [(torch.randn(n, c, device="cuda", generator=g) * torch.rand(1, c, device="cuda", generator=g) * 3)
           .to(torch.bfloat16) for _ in range(2)]
     st = pl.LayerState("residual_with_feedback", 1, torch.zeros(n, c, device="cuda"))
-    pl.encode_step(st, xs[0], spec, rng=la.make_rng(0))
-    pl.encode_step(st, xs[1], spec, rng=la.make_rng(1))
+    key = la.DeviceKey(7, 6, 0, 1, advance=True) if a.device_key else None
+    pl.encode_step(st, xs[0], spec, rng=key or la.make_rng(0))
+    pl.encode_step(st, xs[1], spec, rng=key or la.make_rng(1))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(a.reps):
-        pl.encode_step(st, xs[i % 2], spec, rng=la.make_rng(2 + i))
+        pl.encode_step(st, xs[i % 2], spec, rng=key or la.make_rng(2 + i))
     e1.record()
     torch.cuda.synchronize()
     if a.time:

@@ -269,3 +269,26 @@ def test_lowrank_exchange_graph_replay_equals_eager():
     torch.cuda.synchronize()
     got.append(eb.reconstruction().clone())
     assert torch.equal(got[0], outs_a[0]) and torch.equal(got[1], outs_a[1])
+
+
+@pytest.mark.parametrize("shape", [(256, 3072), (1024, 3072), (4096, 3072), (100, 999)], ids=lambda s: f"{s[0]}x{s[1]}")
+@pytest.mark.parametrize("r", [4, 8, 16])
+def test_orth_forms_agree(shape, r):
+    """The cluster CholQR2 (default) and the single-CTA / grid forms give the same
+    subspace: reconstruction errors agree to 1e-6 relative and both stay within the
+    reference tolerance of each other (different f64 summation orders only)."""
+    cx, _, linalg = _mods()
+    from paper_2507_17511_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(r + shape[0])
+    a = torch.from_numpy((rng.standard_normal(shape) * rng.random((1, shape[1])) * 2).astype(np.float32)).cuda()
+    errs = []
+    for cl in (1, 0):
+        lib.cc_debug_orth_cluster(cl)
+        try:
+            p = cx.encode_lowrank(a, _spec(r, 2), linalg.spawn_rng(4, 5, 2))
+        finally:
+            lib.cc_debug_orth_cluster(1)
+        errs.append(_relerr(p.decode().cpu().numpy(), a.cpu().numpy()))
+    assert abs(errs[0] - errs[1]) <= 1e-6 * max(1.0, errs[1])
