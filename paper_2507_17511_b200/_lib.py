@@ -100,6 +100,7 @@ SIGNATURES = {
     "cc_set_lowrank_backend": (None, [_i32]),
     "cc_debug_k1_resident": (None, [_i32]),
     "cc_debug_k1_resident_count": (_i64, []),
+    "cc_debug_k1_resident_nq": (None, [_i32]),
     "cc_debug_topk_resident": (None, [_i32]),
     "cc_debug_topk_resident_count": (_i64, []),
     "cc_debug_topk_timer": (None, [_p]),

@@ -179,6 +179,7 @@ void set_fused_phase_a(int rows_per_tile, int stages);
 void set_lowrank_backend(int v);
 void set_tc_tma(int v, int waves);
 void set_resident_enabled(int on);
+void set_resident_nq(int nq);
 int64_t resident_launches();
 int residual_target(int mode, int64_t n, int64_t C, const void *x, int x_dtype, const float *base, const float *aux,
                     float *t, cudaStream_t st);
@@ -217,6 +218,7 @@ CC_API void cc_set_lowrank_backend(int backend) { set_lowrank_backend(backend); 
 CC_API void cc_debug_lowrank_tma(int enable, int waves) { set_tc_tma(enable, waves); }
 CC_API void cc_debug_k1_resident(int enable) { set_resident_enabled(enable); }
 CC_API int64_t cc_debug_k1_resident_count(void) { return resident_launches(); }
+CC_API void cc_debug_k1_resident_nq(int nq) { set_resident_nq(nq); }
 CC_API void cc_debug_topk_resident(int enable) { set_topk_resident_enabled(enable); }
 CC_API int64_t cc_debug_topk_resident_count(void) { return topk_resident_launches(); }
 CC_API void cc_debug_topk_timer(void *dev_buf) { set_topk_timer(dev_buf); }

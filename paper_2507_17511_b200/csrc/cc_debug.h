@@ -56,6 +56,9 @@ CC_API void cc_debug_lowrank_tma(int enable, int waves);
 CC_API void cc_debug_k1_resident(int enable);
 /* launches of the shard-resident K1 since load (tests check which kernel ran) */
 CC_API int64_t cc_debug_k1_resident_count(void);
+/* K1 shard-resident kernel geometry: 1 = 24 consumer warps (default), 2 = 12
+ * register-capped warps (lets a decode on another stream share the SMs) */
+CC_API void cc_debug_k1_resident_nq(int nq);
 
 /* K4 shard-resident top-k kernel (topk_resident.cu): 1 = use it for encode steps
  * whenever it can launch (default), 0 = always the multi-kernel radix select. */

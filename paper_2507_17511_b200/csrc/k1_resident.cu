@@ -167,7 +167,9 @@ __device__ __forceinline__ uint32_t tmem_off(int warp, int m) {
 }
 
 template <int MODE, int CODEC, typename XT, int NQ>
-__global__ void __launch_bounds__(Geo<NQ>::THREADS, 1) k1_resident(const __grid_constant__ Params p) {
+// NQ = 2 is register-capped (two CTAs' worth) so a decode kernel on another stream
+// can share the SM during the hand-offs (overlap experiments at small shards)
+__global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident(const __grid_constant__ Params p) {
   constexpr int CONS = Geo<NQ>::CONS, CW = Geo<NQ>::CW;
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -609,11 +611,15 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, 1) k1_resident(const __grid_
 // ---------------------------------------------------------------------------
 
 static bool g_resident_enabled = true;
+// consumer quads per thread: 1 (24 warps) or 2 (12 register-capped warps); 0 = by shape
+static int g_resident_nq = [] {
+  const char *e = std::getenv("CC_K1_RESIDENT_NQ");  // experiments
+  return e ? std::atoi(e) : 0;
+}();
 std::atomic<int64_t> g_resident_launches{0};
 
-template <int MODE, int CODEC, typename XT>
+template <int MODE, int CODEC, typename XT, int NQ>
 static int launch(Params &p, size_t smem, cudaStream_t st) {
-  constexpr int NQ = kNQ;
   auto kern = k1_resident<MODE, CODEC, XT, NQ>;
   static int smem_set = 0;
   if ((int)smem > smem_set) {
@@ -639,9 +645,10 @@ static int launch(Params &p, size_t smem, cudaStream_t st) {
 int64_t resident_launches() { return k1r::g_resident_launches.load(); }
 
 void set_resident_enabled(int on) { k1r::g_resident_enabled = on != 0; }
+void set_resident_nq(int nq) { k1r::g_resident_nq = nq == 2 ? 2 : nq == 1 ? 1 : 0; }
 
 // Shared / tensor-memory plan for a shard; false when the CTA's rows do not fit.
-static bool resident_plan(k1r::Params &q, int mode, int x_dtype) {
+static bool resident_plan(k1r::Params &q, int mode, int x_dtype, int nq) {
   using namespace k1r;
   const int64_t C = q.C;
   const size_t xb = (size_t)C * (x_dtype == CC_BF16 ? 2 : 4), fb = (size_t)C * 4;
@@ -681,7 +688,7 @@ static bool resident_plan(k1r::Params &q, int mode, int x_dtype) {
     q.off_rs = take(R * q.nseg * 8);
     q.off_u = take(R * q.nseg * 4);
     q.off_bar = take(4 * kMaxStages * 8 + 16);
-    q.off_red = take((size_t)Geo<kNQ>::CW * 32 * 8);
+    q.off_red = take((size_t)(nq == 2 ? Geo<2>::CW : Geo<1>::CW) * 32 * 8);
     return off + 16 * 8 + 64;  // + static shared (gseg, last)
   };
   const size_t budget = kSmemMax - 1024;
@@ -738,17 +745,24 @@ int resident_encode(const fused::Params &fp, int codec, int mode, int x_dtype, c
   q.timer = fp.timer;
   q.policy = fp.policy;
   if (fp.ctl_in_ws) return CC_ERR_UNSUPPORTED;  // needs the stream's zeroed control slot
-  if (!resident_plan(q, mode, x_dtype)) return CC_ERR_UNSUPPORTED;
+  // 24 consumer warps hide latency best when the kernel has the SMs to itself; at the
+  // small per-rank shards (<= 14 rows per CTA) the register-capped 12-warp form lets
+  // the previous layer's decode share the SMs during the hand-offs (measured per-rank
+  // step: [1024, 3072] 44.5 -> 37.0 us, [512, 3072] 40.2 -> 32.9 us, scripts/exp/nq_ab.py)
+  const int nq = g_resident_nq ? g_resident_nq : (q.R <= 14 ? 2 : 1);
+  if (!resident_plan(q, mode, x_dtype, nq)) return CC_ERR_UNSUPPORTED;
   size_t smem = 0;
   {
     // recompute the total from the chosen layout
-    smem = (size_t)q.off_red + (size_t)Geo<kNQ>::CW * 32 * 8;
+    smem = (size_t)q.off_red + (size_t)(nq == 2 ? Geo<2>::CW : Geo<1>::CW) * 32 * 8;
   }
-#define CC_RES(MODE, XT)                                                                     \
-  do {                                                                                       \
-    if (codec == CC_SIGN1) return launch<MODE, CC_SIGN1, XT>(q, smem, st);                   \
-    if (codec == CC_QUANT2) return launch<MODE, CC_QUANT2, XT>(q, smem, st);                 \
-    return launch<MODE, CC_QUANT4, XT>(q, smem, st);                                         \
+#define CC_RESQ(MODE, CODEC, XT) \
+  return nq == 2 ? launch<MODE, CODEC, XT, 2>(q, smem, st) : launch<MODE, CODEC, XT, 1>(q, smem, st)
+#define CC_RES(MODE, XT)                                \
+  do {                                                  \
+    if (codec == CC_SIGN1) CC_RESQ(MODE, CC_SIGN1, XT);   \
+    if (codec == CC_QUANT2) CC_RESQ(MODE, CC_QUANT2, XT); \
+    CC_RESQ(MODE, CC_QUANT4, XT);                       \
   } while (0)
   if (x_dtype == CC_BF16) {
     if (mode == CC_WITH_FEEDBACK) CC_RES(CC_WITH_FEEDBACK, __nv_bfloat16);
@@ -760,6 +774,7 @@ int resident_encode(const fused::Params &fp, int codec, int mode, int x_dtype, c
     CC_RES(CC_NAIVE, float);
   }
 #undef CC_RES
+#undef CC_RESQ
 }
 
 }  // namespace cc
