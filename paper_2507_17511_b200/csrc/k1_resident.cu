@@ -72,6 +72,12 @@ struct Params {
   int64_t body_stride, cbytes_seg;
   int nseg, cw, cbs, bps, cb_row;
   unsigned int *bar1, *bar2, *ticket;
+  // row assignment: CTA c first takes the static rows [c stat, (c + 1) stat); with
+  // dyn, the rows from G stat on are claimed one at a time from *claim (faster SMs
+  // take more: balances the phases' ends) up to R rows per CTA in total
+  int dyn, stat;
+  unsigned int *claim;
+  uint32_t off_rows;  // shared-memory row list [R + 1]
   int scale_mode;
   unsigned long long *timer;  // profiling: [G][16] %globaltimer stamps, or null
   int policy;                 // experiments: L2 hints of the phase-A loads (0 = production)
@@ -175,9 +181,8 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cta = blockIdx.x, G = p.G, S = p.S, SB = p.SB;
   const int64_t n = p.n, C = p.C;
-  const int64_t r0 = (int64_t)cta * n / G, r1 = (int64_t)(cta + 1) * n / G;
-  const int nr = (int)(r1 - r0);
   const int nseg = p.nseg;
+  int *rowS = reinterpret_cast<int *>(smem + p.off_rows);  // [R + 1]: row of each slot, -1 ends
   constexpr bool kAux = MODE != CC_NAIVE;
   constexpr bool kWB = MODE == CC_WITH_FEEDBACK;
   const bool keep_base = kAux && p.keep_base;
@@ -241,9 +246,22 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
       // phase A: one ring use per row.  Rows with t in shared memory take their aux
       // straight into the t slot; rows with t in tensor memory stage it in the ring.
       RingPos w;
-      for (int k = 0; k < nr; ++k, w.next(S)) {
+      const int64_t s0 = (int64_t)cta * p.stat;
+      const int nstat = p.dyn ? p.stat : (int)((int64_t)(cta + 1) * n / G - (int64_t)cta * n / G);
+      const int64_t rbase = p.dyn ? s0 : (int64_t)cta * n / G;
+      int k = 0;
+      for (;; ++k, w.next(S)) {
+        int64_t row;
+        if (k < nstat) {
+          row = rbase + k;
+        } else {
+          if (!p.dyn || k >= p.R) break;
+          row = (int64_t)G * p.stat + atomicAdd(p.claim, 1u);
+          if (row >= n) break;
+        }
         if (k >= S) mbar_wait(&empty[w.s], w.ph ^ 1u);
-        const int64_t off = (r0 + k) * C;
+        rowS[k] = (int)row;
+        const int64_t off = row * C;
         uint8_t *st = ring + (size_t)w.s * p.stage_bytes;
         mbar_expect_tx(&full[w.s], bytes);
         bulk_g2s(st, X + off, xb, &full[w.s], pol_once);
@@ -257,13 +275,19 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
           bulk_g2s(st + p.st_base, p.base + off, fb, &full[w.s], pol_again);
         }
       }
+      const int nr = k;
+      // end of phase A: a ring use with no data (row -1)
+      if (k >= S) mbar_wait(&empty[w.s], w.ph ^ 1u);
+      rowS[k] = -1;
+      mbar_arrive(&full[w.s]);
+      w.next(S);
       // phase B: base rows through SB slots carved from the ring area, newest first
       // (the most recently loaded base rows are the likeliest L2 hits), loaded while
       // the consumers wait on the hand-offs
       if (ring_base) {
-        // the ring area is free once phase A's last min(S, nr) uses are released
+        // the ring area is free once phase A's last min(S, nr + 1) uses are released
         RingPos q = w;
-        for (int i = 0; i < min(S, nr); ++i) {
+        for (int i = 0; i < min(S, nr + 1); ++i) {
           if (--q.s < 0) {
             q.s = S - 1;
             q.ph ^= 1u;
@@ -275,7 +299,7 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
           const int k = nr - 1 - i;
           if (i >= SB) mbar_wait(&emptyB[b.s], b.ph ^ 1u);
           mbar_expect_tx(&fullB[b.s], fb);
-          bulk_g2s(ring + (size_t)b.s * fb, p.base + (r0 + k) * C, fb, &fullB[b.s], pol_b);
+          bulk_g2s(ring + (size_t)b.s * fb, p.base + (int64_t)rowS[k] * C, fb, &fullB[b.s], pol_b);
         }
       }
     }
@@ -298,18 +322,26 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
   for (int j = 0; j < NQ; ++j) cs[j][0] = cs[j][1] = cs[j][2] = cs[j][3] = 0.0;
 
   // ---------------- phase A ----------------
+  int nr = 0;
   {
     RingPos w;
-    for (int k = 0; k < nr; ++k, w.next(S)) {
+    for (int k = 0;; ++k, w.next(S)) {
       mbar_wait(&full[w.s], w.ph);
       if (k == 0) stamp(1);
+      const int rowk = rowS[k];
+      if (rowk < 0) {  // end of the CTA's rows
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[w.s]);
+        nr = k;
+        break;
+      }
       const uint8_t *st = ring + (size_t)w.s * p.stage_bytes;
       const XT *xs = reinterpret_cast<const XT *>(st);
       const bool in_smem = k < p.nsm;
       float *trow = tS + (size_t)k * C;
       const float *arow = in_smem ? trow : reinterpret_cast<const float *>(st + p.st_fb);
       const float *brow = keep_base ? bS + (size_t)k * C : reinterpret_cast<const float *>(st + p.st_base);
-      float *refrow = p.aux + (r0 + k) * C;
+      float *refrow = p.aux + (int64_t)rowk * C;
       double rsum[NQ];
       float tt[NQ][4];
 #pragma unroll
@@ -352,43 +384,48 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
     double *cp = p.colpart + (int64_t)cta * C + qcol[j];
     cp[0] = cs[j][0]; cp[1] = cs[j][1]; cp[2] = cs[j][2]; cp[3] = cs[j][3];
   }
-  fused::named_sync(1, CONS);
   stamp(9);
-  // row sums per segment (blocks of the segment in order), then CTA totals
-  for (int i = tid; i < nr * nseg; i += CONS) {
-    const int k = i / nseg, d = i - k * nseg;
-    double acc = 0.0;
-    for (int b = 0; b < p.bps; ++b) acc += rp[(size_t)k * kNB + d * p.bps + b];
-    rs[i] = acc;
-  }
-  fused::named_sync(1, CONS);
-  if (tid < nseg) {
-    double tot = 0.0;
-    for (int k = 0; k < nr; ++k) tot += rs[k * nseg + tid];
-    p.blkpart[(size_t)cta * nseg + tid] = tot;
+  // the CTA's |t| total(s) for g: with one segment straight from the column sums in
+  // registers (warp butterflies, warps in order) so the arrival does not wait for the
+  // row sums; those (needed only for u) are formed while the barrier completes
+  auto row_sums = [&]() {  // per segment (blocks of the segment in order)
+    for (int i = tid; i < nr * nseg; i += CONS) {
+      const int k = i / nseg, d = i - k * nseg;
+      double acc = 0.0;
+      for (int b = 0; b < p.bps; ++b) acc += rp[(size_t)k * kNB + d * p.bps + b];
+      rs[i] = acc;
+    }
+  };
+  if (nseg == 1) {
+    double tsum = 0.0;
+#pragma unroll
+    for (int j = 0; j < NQ; ++j)
+      if (qact[j]) tsum += ((cs[j][0] + cs[j][1]) + cs[j][2]) + cs[j][3];
+    tsum = warp_sum(tsum);
+    if (lane == 0) red[warp * 32] = tsum;
+    fused::named_sync(1, CONS);
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < CW; ++w) tot += red[w * 32];
+      p.blkpart[cta] = tot;
+    }
+  } else {
+    fused::named_sync(1, CONS);
+    row_sums();
+    fused::named_sync(1, CONS);
+    if (tid < nseg) {
+      double tot = 0.0;
+      for (int k = 0; k < nr; ++k) tot += rs[k * nseg + tid];
+      p.blkpart[(size_t)cta * nseg + tid] = tot;
+    }
   }
   // ---- hand-off 1 ----
   fused::named_sync(1, CONS);
   stamp(10);
-  if (tid == 0) {
-    if (p.policy & 256) {
-      __threadfence();
-      atomicAdd(p.bar1, 1u);
-    } else {
-      fused::arrive_release(p.bar1);
-    }
-    stamp(11);
-    if (p.policy & 512) {
-      for (;;) {
-        unsigned v;
-        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.bar1) : "memory");
-        if (v >= (unsigned)G) break;
-      }
-      __threadfence();
-    } else {
-      fused::spin_until(p.bar1, (unsigned)G);
-    }
-  }
+  if (tid == 0) fused::arrive_release(p.bar1);
+  stamp(11);
+  if (nseg == 1) row_sums();  // overlaps the barrier
+  if (tid == 0) fused::spin_until(p.bar1, (unsigned)G);
   fused::named_sync(1, CONS);
   stamp(3);
 
@@ -447,7 +484,7 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
       else if (g == 0.0) u = 1.0f;  // all-zero segment (cx:143-146)
       else u = (float)fmax((rsum / (double)p.cw) / g, kRowScaleFloor);  // cx:147
       uS[i] = u;
-      store_f32_bytes(p.body + d * p.body_stride + p.cbytes_seg + 4 * (r0 + k), u);
+      store_f32_bytes(p.body + d * p.body_stride + p.cbytes_seg + 4 * (int64_t)rowS[k], u);
     }
   }
   // ---- hand-off 2: every CTA's v ----
@@ -484,7 +521,7 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
   RingPos bpos;
   for (int i = 0; i < nr; ++i) {
     const int k = nr - 1 - i;  // newest rows first (matches the producer's base order)
-    const int64_t row = r0 + k;
+    const int64_t row = rowS[k];
     const float *brow = bS + (size_t)k * C;
     if (ring_base) {
       mbar_wait(&fullB[bpos.s], bpos.ph);
@@ -600,6 +637,7 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
         *p.ticket = 0u;
         *p.bar1 = 0u;
         *p.bar2 = 0u;
+        *p.claim = 0u;
       }
     }
   }
@@ -688,6 +726,7 @@ static bool resident_plan(k1r::Params &q, int mode, int x_dtype, int nq) {
     q.off_rs = take(R * q.nseg * 8);
     q.off_u = take(R * q.nseg * 4);
     q.off_bar = take(4 * kMaxStages * 8 + 16);
+    q.off_rows = take(4 * (R + 1));
     q.off_red = take((size_t)(nq == 2 ? Geo<2>::CW : Geo<1>::CW) * 32 * 8);
     return off + 16 * 8 + 64;  // + static shared (gseg, last)
   };
@@ -699,13 +738,28 @@ static bool resident_plan(k1r::Params &q, int mode, int x_dtype, int nq) {
     if (!aux) break;
   }
   // 2. overflow rows in tensor memory (base streamed): the deepest ring that leaves
-  //    with the most shared t rows for it
+  //    with the most shared t rows for it.  Experiment (policy bit 4096): a few rows
+  //    of headroom per CTA, ~80 % of the rows assigned statically and the rest claimed
+  //    one at a time, so faster SMs take more — phase A then ends together, but the
+  //    producer's claim round trips stall its ring and the step got slower ([4096,
+  //    3072] 59.3 -> 61.5-63.9 us, scripts/k1_ab.py): static rows are the default
   const int s_force = (q.policy >> 16) & 15;  // experiments: ring depth override
-  for (int S = s_force ? s_force : kMaxStages; S >= 2; --S) {
-    for (int nsm = q.R - 1; nsm >= std::max(0, q.R - kTmemRows); --nsm) {
-      if (layout(0, S, nsm) <= budget) return true;
+  const int R0 = q.R;
+  const bool no_dyn = (q.policy & 4096) == 0;
+  for (int extra : {6, 4, 2, 0}) {
+    if (no_dyn && extra) continue;
+    q.R = R0 + extra;
+    for (int S = s_force ? s_force : kMaxStages; S >= 2; --S) {
+      for (int nsm = q.R - 1; nsm >= std::max(0, q.R - kTmemRows); --nsm) {
+        if (layout(0, S, nsm) <= budget) {
+          q.dyn = extra > 0;
+          q.stat = extra > 0 ? (int)(0.8 * (double)q.n / q.G) : 0;
+          return true;
+        }
+      }
     }
   }
+  q.R = R0;
   return false;
 }
 
@@ -741,6 +795,9 @@ int resident_encode(const fused::Params &fp, int codec, int mode, int x_dtype, c
   q.bar1 = fp.bar;
   q.bar2 = fp.bar + 32;
   q.ticket = fp.ticket;
+  q.claim = reinterpret_cast<unsigned int *>(fp.ctr);  // control word 0 (left zero on exit)
+  q.dyn = 0;
+  q.stat = 0;
   q.scale_mode = fp.scale_mode;
   q.timer = fp.timer;
   q.policy = fp.policy;
