@@ -19,6 +19,8 @@
 
 #include <algorithm>
 #include <cooperative_groups.h>
+#include <mutex>
+#include <unordered_map>
 #include <curand_kernel.h>
 
 namespace cc {
@@ -988,18 +990,24 @@ __global__ void __launch_bounds__(kThreads) k_outer(const double *__restrict__ U
 // Thread = one column j (W's column from the transposed factor WfT [r][C]:
 // coalesced), kOARows rows per CTA with every row's loads in flight together.
 constexpr int kOARows = 16;
+// The factors come straight from the body (f16 / INT4 -> f64 exactly as the
+// receiver's k_unpack_factors does) and the last CTA (ticket on a zeroed slab
+// word) reduces the record partials in CTA order: one launch for decode + update +
+// record.
 template <int MODE, typename XT, int RM>
-__global__ void __launch_bounds__(kThreads) k_outer_apply(const double *__restrict__ Uf, const double *__restrict__ WfT,
-                                                           int64_t n, int64_t C, int r, const XT *__restrict__ x,
+__global__ void __launch_bounds__(kThreads) k_outer_apply(const uint8_t *__restrict__ body, int int4, int64_t n,
+                                                           int64_t C, int r, const XT *__restrict__ x,
                                                            const float *__restrict__ t, float *__restrict__ base,
-                                                           float *__restrict__ aux, double *__restrict__ part) {
+                                                           float *__restrict__ aux, double *__restrict__ part,
+                                                           unsigned int *ticket, double *__restrict__ record) {
   __shared__ double us[kOARows][kMaxR];
   __shared__ double se[kThreads / 32], st2[kThreads / 32];
+  __shared__ unsigned last;
   const int64_t i0 = (int64_t)blockIdx.y * kOARows;
   const int nr = (int)min64(kOARows, n - i0);
   for (int e = threadIdx.x; e < kOARows * r; e += kThreads) {
     const int ii = e / r, k = e % r;
-    us[ii][k] = ii < nr ? Uf[(i0 + ii) * r + k] : 0.0;
+    us[ii][k] = ii < nr ? factor_at(body, int4, n, C, r, 0, i0 + ii, k) : 0.0;
   }
   __syncthreads();
   const int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
@@ -1007,7 +1015,7 @@ __global__ void __launch_bounds__(kThreads) k_outer_apply(const double *__restri
   if (j < C) {
     double w[RM];  // RM >= r, compile-time: W's column stays in registers
 #pragma unroll
-    for (int k = 0; k < RM; ++k) w[k] = k < r ? WfT[(int64_t)k * C + j] : 0.0;
+    for (int k = 0; k < RM; ++k) w[k] = k < r ? factor_at(body, int4, n, C, r, 1, j, k) : 0.0;
     float tt[kOARows], bb[kOARows], xx[kOARows];
 #pragma unroll
     for (int ii = 0; ii < kOARows; ++ii) {  // every row's loads in flight together
@@ -1053,6 +1061,35 @@ __global__ void __launch_bounds__(kThreads) k_outer_apply(const double *__restri
     const int64_t blk = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
     part[2 * blk] = a;
     part[2 * blk + 1] = b;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1;
+  }
+  __syncthreads();
+  if (last) {  // fixed-order sum of every CTA's partials (as k_sum_parts)
+    __threadfence();
+    const int nparts = (int)(gridDim.x * gridDim.y);
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += kThreads) {
+      a += __ldcg(part + 2 * i);
+      b += __ldcg(part + 2 * i + 1);
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if ((threadIdx.x & 31) == 0) {
+      se[threadIdx.x >> 5] = a;
+      st2[threadIdx.x >> 5] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double x0 = 0.0, y0 = 0.0;
+      for (int w = 0; w < kThreads / 32; ++w) {
+        x0 += se[w];
+        y0 += st2[w];
+      }
+      record[0] = x0;
+      record[1] = y0;
+      *ticket = 0u;  // the slab word is zero again for the next launch
+    }
   }
 }
 
@@ -1259,6 +1296,40 @@ int gaussian_keyed(int64_t rows, int64_t cols, uint32_t *key, int nwords, int st
                    int64_t ws_bytes, cudaStream_t st);
 int64_t gaussian_workspace_bytes(int64_t rows, int64_t cols);
 int sum_parts(int nparts, const double *part, double *record, cudaStream_t st);
+uint8_t *stream_zero_slab(cudaStream_t st, size_t bytes);
+// low-rank words in the per-stream zeroed slab (after the top-k kernel's ~34 KB)
+constexpr size_t kLrTicketOff = 40 * 1024;
+constexpr size_t kSlabBytesNeeded = kLrTicketOff + 128;
+
+// A library-owned side stream + fork / join events per (device, caller stream),
+// created on first use outside a capture (null otherwise: no fork).
+struct SideStream {
+  cudaStream_t s;
+  cudaEvent_t fork, join;
+};
+static SideStream *side_stream(cudaStream_t st) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, SideStream> m;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t k = (uint64_t)reinterpret_cast<uintptr_t>(st) * 64 + (uint64_t)dev;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = m.find(k);
+  if (it != m.end()) return &it->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  SideStream ss{};
+  if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return &m.emplace(k, ss).first->second;
+}
 
 // encode_step workspace: t [n, C] | Q0 [C, r] | gaussian scratch | encode workspace |
 // f64 factors [n + C, r] | record partials
@@ -1310,9 +1381,22 @@ int lowrank_encode_step(int mode, int64_t n, int64_t C, int64_t r, int iters, in
   size_t gb, eb;
   double *Uf, *part;
   lr_step_layout(n, C, r, reinterpret_cast<uint8_t *>(ws), &t, &q0, &gws, &gb, &ews, &eb, &Uf, &part);
-  int rc = residual_target(mode, n, C, x, x_dtype, base, aux, t, st);
+  // the start block depends only on the key: draw it on a side stream while the
+  // target is formed (fork / join through events: also inside a graph capture)
+  SideStream *ss = key ? side_stream(st) : nullptr;
+  int rc;
+  if (key && ss) {
+    cudaEventRecord(ss->fork, st);
+    cudaStreamWaitEvent(ss->s, ss->fork, 0);
+    rc = gaussian_keyed(C, r, key, nwords, step_word, q0, gws, (int64_t)gb, ss->s);
+    if (rc) return rc;
+    cudaEventRecord(ss->join, ss->s);
+  }
+  rc = residual_target(mode, n, C, x, x_dtype, base, aux, t, st);
   if (rc) return rc;
-  if (key) {
+  if (key && ss) {
+    cudaStreamWaitEvent(st, ss->join, 0);
+  } else if (key) {
     rc = gaussian_keyed(C, r, key, nwords, step_word, q0, gws, (int64_t)gb, st);
     if (rc) return rc;
   } else {
@@ -1320,11 +1404,17 @@ int lowrank_encode_step(int mode, int64_t n, int64_t C, int64_t r, int iters, in
   }
   rc = lowrank_encode(int4, n, C, r, iters, t, q0, body, nullptr, ews, (int64_t)eb, st);
   if (rc) return rc;
-  double *WfT = Uf + n * r;
-  lr::k_unpack_factors_t<<<(unsigned)cdiv((n + C) * r, 256), 256, 0, st>>>(body, int4, n, C, (int)r, Uf, WfT);
+  (void)Uf;
+  uint8_t *slab = stream_zero_slab(st, kSlabBytesNeeded);
+  unsigned int *ticket = slab ? reinterpret_cast<unsigned int *>(slab + kLrTicketOff) : nullptr;
+  if (!ticket) {
+    set_error("low-rank step: no control slab (first use inside a capture)");
+    return CC_ERR_UNSUPPORTED;
+  }
   dim3 g((unsigned)cdiv(C, lr::kThreads), (unsigned)cdiv(n, lr::kOARows));
-#define CC_LA3(MODE, XT, RM) \
-  lr::k_outer_apply<MODE, XT, RM><<<g, lr::kThreads, 0, st>>>(Uf, WfT, n, C, (int)r, (const XT *)x, t, base, aux, part)
+#define CC_LA3(MODE, XT, RM)                                                                                    \
+  lr::k_outer_apply<MODE, XT, RM><<<g, lr::kThreads, 0, st>>>(body, int4, n, C, (int)r, (const XT *)x, t, base, \
+                                                              aux, part, ticket, record)
 #define CC_LA(MODE, XT)                   \
   do {                                    \
     if (r <= 8) CC_LA3(MODE, XT, 8);      \
@@ -1342,9 +1432,7 @@ int lowrank_encode_step(int mode, int64_t n, int64_t C, int64_t r, int iters, in
   }
 #undef CC_LA
 #undef CC_LA3
-  count_launch(2);
-  rc = sum_parts((int)(g.x * g.y), part, record, st);
-  if (rc) return rc;
+  count_launch();
   return cuda_status("lowrank_encode_step");
 }
 
