@@ -140,9 +140,13 @@ __device__ __forceinline__ void find_bin(const uint32_t *hist, uint32_t need, ui
   uint32_t incl = warp_incl(local);
   if (lane == 31) sm[w] = incl;
   __syncthreads();
-  uint32_t wpre = 0;
-  for (int i = 0; i < w; ++i) wpre += sm[i];
-  incl += wpre;
+  if (w == 0) {  // exclusive prefix of the warp totals, in place
+    const uint32_t v = lane < kWarps ? sm[lane] : 0u;
+    const uint32_t vi = warp_incl(v);
+    if (lane < kWarps) sm[lane] = vi - v;
+  }
+  __syncthreads();
+  incl += sm[w];
   uint32_t before = incl - local;
   if (before < need && incl >= need) {
 #pragma unroll
@@ -175,8 +179,10 @@ __device__ __forceinline__ void quad_vals(const float4 &v, float (&t)[4]) {
   t[3] = v.w;
 }
 
+// register-capped (112) so the previous layer's sparse decode (a small scatter kernel on
+// the decode stream) can share the SMs while this kernel waits at its barriers
 template <int MODE, typename XT>
-__global__ void __launch_bounds__(kThreads, 1) k4_resident(const __grid_constant__ Params p) {
+__global__ void __maxnreg__(112) k4_resident(const __grid_constant__ Params p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t *h = reinterpret_cast<uint32_t *>(smem);  // area U: x staging (fit), then histograms
   float *tS = reinterpret_cast<float *>(smem + p.off_t);
@@ -676,20 +682,22 @@ __global__ void __launch_bounds__(kThreads, 1) k4_resident(const __grid_constant
         mgt |= (uint32_t)((j < nv) & (key > T)) << j;
         meq |= (uint32_t)((j < nv) & (key == T)) << j;
       }
-      const uint32_t neq = __popc(meq);
-      const uint32_t ie = warp_incl(neq);
-      uint32_t er = eq_run + ie - neq;  // tie rank of this lane's first tie
       uint32_t msel = mgt;
+      if (__any_sync(0xffffffffu, meq != 0u)) {  // ties in this chunk: their ranks (lowest index first)
+        const uint32_t neq = __popc(meq);
+        const uint32_t ie = warp_incl(neq);
+        uint32_t er = eq_run + ie - neq;  // tie rank of this lane's first tie
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if ((meq >> j) & 1u) {
-          if (er < ties) msel |= 1u << j;
-          ++er;
-        }
+        for (int j = 0; j < 4; ++j)
+          if ((meq >> j) & 1u) {
+            if (er < ties) msel |= 1u << j;
+            ++er;
+          }
+        eq_run += __shfl_sync(0xffffffffu, ie, 31);
+      }
       const uint32_t ns = __popc(msel);
       const uint32_t is = warp_incl(ns);
       uint32_t pos = pos_run + is - ns;
-      eq_run += __shfl_sync(0xffffffffu, ie, 31);
       pos_run += __shfl_sync(0xffffffffu, is, 31);
       if (msel) {
         float bb[4] = {0.f, 0.f, 0.f, 0.f};
