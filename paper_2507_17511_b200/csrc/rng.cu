@@ -174,7 +174,8 @@ struct Work {
   uint32_t *ev_o;     // [kMaxEv] output index of each real slow draw (ascending)
   uint32_t *ev_sh;    // [kMaxEv] position shift (pos - out) of the draws after it
   double *ev_v;       // [kMaxEv]
-  uint32_t *ctl;      // [0] ticket, [1] event count
+  uint32_t *ctl;      // [1] event count (workspace)
+  uint32_t *ticket;   // last-CTA ticket: a library-owned zeroed word (left zero by every launch)
   uint32_t *sslow;    // [npos] sequential-walk fallback: all candidates in order
   uint32_t *scons;    // [npos]
   double *sval;       // [npos]
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gauss_gen(const uint32_t *__res
   // ---- the last CTA resolves the slow draws ----
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(&w.ctl[0], 1u) == gridDim.x - 1;
+  if (tid == 0) s_last = atomicAdd(w.ticket, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gauss_gen(const uint32_t *__res
         ++j;
       }
       w.ctl[1] = nev;
-      w.ctl[0] = 0u;
+      *w.ticket = 0u;
     }
     return;
   }
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gauss_gen(const uint32_t *__res
     __syncthreads();
     if (tid == kGenThreads - 1) {
       w.ctl[1] = min(s_nev, slot);
-      w.ctl[0] = 0u;  // ticket ready for the next launch
+      *w.ticket = 0u;  // ticket ready for the next launch
     }
   }
 }
@@ -457,6 +458,9 @@ static Work carve(void *ws, int64_t npos, size_t *bytes) {
 
 }  // namespace rng
 
+uint8_t *stream_zero_slab(cudaStream_t st, size_t bytes);
+constexpr size_t kGaussTicketOff = 44 * 1024;  // word in the per-stream zeroed slab (top-k: < 34 KB, low-rank: 40 KB)
+
 int64_t gaussian_workspace_bytes(int64_t rows, int64_t cols) {
   size_t b = 0;
   rng::carve(nullptr, rng::npos_for(rows * cols), &b);
@@ -481,14 +485,15 @@ int gaussian_keyed(int64_t rows, int64_t cols, uint32_t *key, int nwords, int st
     set_error("gaussian workspace too small");
     return CC_ERR_ARG;
   }
-  const rng::Work w = rng::carve(ws, npos, nullptr);
-  // the ticket word must start at zero: the workspace is the caller's, so zero it on
-  // first use of this workspace (every launch leaves it zero afterwards)
-  static thread_local const void *zeroed = nullptr;
-  if (zeroed != ws) {
-    cudaMemsetAsync(w.ctl, 0, 256, st);
-    zeroed = ws;
+  // the last-CTA ticket lives in the stream's zeroed slab (a caller workspace word
+  // would carry whatever the allocator's previous user left there)
+  uint8_t *slab = stream_zero_slab(st, kGaussTicketOff + 128);
+  if (!slab) {
+    set_error("gaussian: no control slab (first use inside a capture)");
+    return CC_ERR_UNSUPPORTED;
   }
+  rng::Work w = rng::carve(ws, npos, nullptr);
+  w.ticket = reinterpret_cast<uint32_t *>(slab + kGaussTicketOff);
   const unsigned nblk = (unsigned)cdiv(npos, rng::kGenPos);
   rng::k_gauss_gen<<<nblk, rng::kGenThreads, 0, st>>>(key, nwords, M, npos, w);
   rng::k_gauss_out<<<(unsigned)cdiv(M, 4 * rng::kOutThreads), rng::kOutThreads, 0, st>>>(key, nwords, step_word, M,

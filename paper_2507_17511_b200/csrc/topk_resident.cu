@@ -790,10 +790,10 @@ __global__ void __maxnreg__(112) k4_resident(const __grid_constant__ Params p) {
 // ---------------------------------------------------------------------------
 uint8_t *stream_zero_slab(cudaStream_t st, size_t bytes);
 
-static bool g_topk_resident = true;
+static int g_topk_resident = 1;  // 0 off, 1 when t fits on chip, 2 also when it does not (A/B)
 static unsigned long long *g_topk_timer = nullptr;
 void set_topk_timer(void *buf) { g_topk_timer = reinterpret_cast<unsigned long long *>(buf); }
-void set_topk_resident_enabled(int on) { g_topk_resident = on != 0; }
+void set_topk_resident_enabled(int on) { g_topk_resident = on; }
 std::atomic<int64_t> g_topk_resident_launches{0};
 int64_t topk_resident_launches() { return g_topk_resident_launches.load(); }
 
@@ -850,7 +850,7 @@ int topk_resident_encode_step(int mode, int64_t n, int64_t C, int64_t k, const v
   smem += 4 * (size_t)p.lcap;
   const bool t_on_chip = p.fit || (int64_t)p.nsm * 4 >= ne_max;
   // shards whose residual stays off chip: the multi-kernel select is faster there
-  if (!t_on_chip) return CC_ERR_UNSUPPORTED;
+  if (!t_on_chip && g_topk_resident < 2) return CC_ERR_UNSUPPORTED;
   Slab *slab = reinterpret_cast<Slab *>(stream_zero_slab(st, sizeof(Slab)));
   if (!slab) return CC_ERR_UNSUPPORTED;
   uint8_t *w = reinterpret_cast<uint8_t *>(ws);
@@ -863,8 +863,13 @@ int topk_resident_encode_step(int mode, int64_t n, int64_t C, int64_t k, const v
   p.cnt = reinterpret_cast<uint32_t *>(take(8 * (size_t)p.G));
   p.recpart = reinterpret_cast<double *>(take(16 * (size_t)p.G));
   p.cand = reinterpret_cast<uint32_t *>(take(4 * (size_t)kCandCap));
-  p.tout = mode == CC_WITH_FEEDBACK ? aux : nullptr;  // feedback' = t off the selection
-  p.write_t = mode == CC_WITH_FEEDBACK ? 1 : 0;
+  if (mode == CC_WITH_FEEDBACK) {  // feedback' = t off the selection
+    p.tout = aux;
+    p.write_t = 1;
+  } else {  // t kept nowhere else: scratch when it does not fit on chip
+    p.tout = t_on_chip ? nullptr : reinterpret_cast<float *>(take(4 * (size_t)total));
+    p.write_t = t_on_chip ? 0 : 1;
+  }
   if ((int64_t)off > ws_bytes) return CC_ERR_UNSUPPORTED;
   p.body = body;
   p.record = record;

@@ -11,7 +11,7 @@ from paper_2507_17511_b200 import pipeline as pl  # noqa: E402
 
 L = 16
 lib = _lib.load()
-for rows, keep, res in ([] if os.environ.get('TK_TIMELINE_ONLY') else [(r, k, s) for r in (4096, 1024, 512) for k in (0.01, 0.1) for s in (1, 0)]):
+for rows, keep, res in ([] if os.environ.get('TK_TIMELINE_ONLY') else [(r, k, s) for r in (4096, 1024, 512) for k in (0.01, 0.1) for s in ((2, 1, 0) if r == 4096 else (1, 0))]):
         lib.cc_debug_topk_resident(res)
         c0 = lib.cc_debug_topk_resident_count()
         spec = cx.CompressorSpec(cx.CompressorKind.TOPK, keep_fraction=keep)
