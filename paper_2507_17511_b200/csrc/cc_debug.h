@@ -24,7 +24,7 @@ CC_API void cc_debug_fused_stop(int phase);
 /* profiling only: device buffer of [grid][8] u64 %globaltimer stamps written by
  * every CTA of the persistent K1 at its phase boundaries (NULL disables). */
 CC_API void cc_debug_fused_timer(void *dev_buf);
-/* profiling only: experiment bits of the persistent K1 (0 = production path; see
+/* profiling only (effective in builds with -DCC_K1_EXPERIMENTS=1): experiment bits of the persistent K1 (0 = production path; see
  * k1_fused.cu Params::policy: L2 hints, skipped math / stores, workspace control words,
  * forced phase-A evict_first fraction in bits 8..11) */
 CC_API void cc_debug_fused_policy(int policy);

@@ -89,6 +89,14 @@ struct Params {
                // stored directly from registers (no output ring / TMA stores)
 };
 
+// Params::policy experiment bits (L2 hints, skipped math / stores for movement-only
+// timings) are compiled in only with -DCC_K1_EXPERIMENTS=1: in production builds every
+// K1_XP(p) test is a compile-time 0 and the branches vanish from the kernels.
+#ifndef CC_K1_EXPERIMENTS
+#define CC_K1_EXPERIMENTS 0
+#endif
+#define K1_XP(p) (CC_K1_EXPERIMENTS ? (p).policy : 0)
+
 __device__ __forceinline__ uint64_t l2_policy_normal() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
@@ -434,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
   // double-buffered by use parity, so the new tile's partials cannot collide).
   if (loader) {
    {  // phase A
-    const uint64_t pol_late = (p.policy & 4) ? l2_policy_normal() : l2_policy_evict_last();
+    const uint64_t pol_late = (K1_XP(p) & 4) ? l2_policy_normal() : l2_policy_evict_last();
     const uint64_t pol_early = l2_policy_evict_first();
     // Only the last ~kL2KeepBytes of phase A stay L2-resident (evict_last) for the
     // reverse-order phase B; earlier tiles are loaded evict_first so they do not
@@ -486,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
         }
       }
       __syncwarp();
-      if (old >= 0 && !(p.policy & 16)) finish_rows(s, old, ph ^ 1u);
+      if (old >= 0 && !(K1_XP(p) & 16)) finish_rows(s, old, ph ^ 1u);
       if (tile < 0) break;
       ++k;
       if (++s == SA) {
@@ -519,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     // Phase B.  The first S_in tiles are loaded while the consumers still run
     // the scale pass; their u windows follow once bar2 publishes u.
     // phase-B loads: evict_normal (measured ~1 us better than evict_first at [4096, 3072])
-    const uint64_t pol = (p.policy & 2) ? l2_policy_evict_first() : l2_policy_normal();
+    const uint64_t pol = (K1_XP(p) & 2) ? l2_policy_evict_first() : l2_policy_normal();
     // k = stage uses issued (stage k % SI), w = uses whose release has been awaited.
     // Claims run one tile ahead while plenty of work is left; in the end-game
     // (fewer than tail_mult x G tiles unclaimed) a CTA claims only when at most
@@ -637,13 +645,13 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
     if (p.stop_after) return;
     int o = 0;
     uint32_t ph = 0;
-    const bool hint = !(p.policy & 1);  // results are not re-read in this launch: evict_first
+    const bool hint = !(K1_XP(p) & 1);  // results are not re-read in this launch: evict_first
     const uint64_t spol = l2_policy_evict_first();
     for (;; o = (o + 1 == SO) ? 0 : o + 1, ph ^= (o == 0)) {
       mbar_wait(&outFull[o], ph);
       const long long tile = tileO[o];
       if (tile < 0) break;
-      if (lane == 0 && !(p.policy & 128)) {
+      if (lane == 0 && !(K1_XP(p) & 128)) {
         const uint8_t *so = out_ring + (size_t)o * LO.bytes;
         const int64_t r0 = (int64_t)tile * RB;
         const int nrows = (int)min64(RB, n - r0);
@@ -692,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       }
       const uint8_t *st = ring + (size_t)s * LA.bytes;
       const int nrows = (int)min64(RA, n - (int64_t)tile * RA);
-      if (grp < p.groups && !(p.policy & 8)) {
+      if (grp < p.groups && !(K1_XP(p) & 8)) {
         for (int r = grp; r < nrows; r += p.groups) {
           double rs[Q];
 #pragma unroll
@@ -850,7 +858,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       }
       const uint8_t *st = in_ring + (size_t)s * LI.bytes;
       const int64_t r0 = (int64_t)tile * RB;
-      const bool row_live = in_group && r0 + r < n && !(p.policy & 64);
+      const bool row_live = in_group && r0 + r < n && !(K1_XP(p) & 64);
       float xx[Q][4], bb[Q][4], aa[Q][4];
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
@@ -873,7 +881,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_fused(const __grid_constant__ 
       if (lane == 0) mbar_arrive(&emptyB[s]);  // inputs are in registers: the loader may refill
       if (k >= SO) mbar_wait(&outFree[o], pho ^ 1u);
       uint8_t *so = out_ring + (size_t)o * LO.bytes;
-      const bool direct = p.policy & 128;  // experiment: results straight to HBM (generic stores)
+      const bool direct = K1_XP(p) & 128;  // experiment: results straight to HBM (generic stores)
       float *obase = direct ? p.base + r0 * C : reinterpret_cast<float *>(so + LO.base);
       float *oaux = direct ? p.aux + r0 * C : reinterpret_cast<float *>(so + LO.aux);
       uint8_t *ocode = direct && nseg == 1 ? p.body + r0 * p.cb_row : so + LO.codes;

@@ -231,14 +231,14 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
 
   if (warp == CW) {  // ===================== producer warp =====================
     if (lane == 0) {
-      const uint64_t pol_once = (p.policy & 4) ? fused::l2_policy_normal() : l2_policy_evict_first();
+      const uint64_t pol_once = (K1_XP(p) & 4) ? fused::l2_policy_normal() : l2_policy_evict_first();
       // base rows are re-read in phase B, but keeping them L2-resident (evict_last)
       // slows phase A more than the re-read costs: [4096, 3072] 62.6 us with
       // evict_last, 60.5 us with evict_first (scripts/k1_ab.py --policies)
-      const uint64_t pol_again = (p.policy & 1)   ? fused::l2_policy_normal()
-                                 : (p.policy & 2) ? l2_policy_evict_last()
+      const uint64_t pol_again = (K1_XP(p) & 1)   ? fused::l2_policy_normal()
+                                 : (K1_XP(p) & 2) ? l2_policy_evict_last()
                                                   : l2_policy_evict_first();
-      const uint64_t pol_b = (p.policy & 8) ? fused::l2_policy_normal() : l2_policy_evict_first();
+      const uint64_t pol_b = (K1_XP(p) & 8) ? fused::l2_policy_normal() : l2_policy_evict_first();
       const uint32_t xb = (uint32_t)(C * sizeof(XT)), fb = (uint32_t)(C * 4);
       uint32_t bytes = xb;
       if (kAux) bytes += fb;

@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace cc {
 namespace tc {
@@ -487,9 +488,17 @@ static size_t tc_smem_bytes(int NP) {
 }
 
 // split-K plan: ~4 CTAs per SM (2 resident x 2 waves), >= 4 K chunks per CTA
+static int tc_ctas_per_sm() {
+  static const int v = [] {
+    const char *e = getenv("CC_TC_CTAS_PER_SM");  // experiments
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
+  return v;
+}
+
 static void tc_plan(int64_t M, int64_t K, int64_t *splits, int64_t *kper) {
   const int64_t tiles = cdiv(M, tc::kM);
-  int64_t sp = std::max<int64_t>(1, std::min<int64_t>(cdiv(4 * sm_count(), tiles), cdiv(K, 4 * tc::kKC)));
+  int64_t sp = std::max<int64_t>(1, std::min<int64_t>(cdiv(tc_ctas_per_sm() * sm_count(), tiles), cdiv(K, 4 * tc::kKC)));
   *kper = cdiv(cdiv(K, sp), tc::kKC) * tc::kKC;
   *splits = cdiv(K, *kper);
 }
