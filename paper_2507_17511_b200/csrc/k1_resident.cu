@@ -649,6 +649,14 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
 // ---------------------------------------------------------------------------
 
 static bool g_resident_enabled = true;
+// shared memory the 12-warp form leaves free for kernels sharing its SMs (the decode
+// needs none; an NCCL kernel at N > 1 may): measured on the per-rank sims, 0 / 48 /
+// 96 KB free: [2048, 3072] 45.9 / 44.5 / 43.7 us, [1024, 3072] 32.5 / 36.2 / 33.8 us
+// (the base rows stop fitting on chip), [512, 3072] 28.5 in all three: default 0
+static size_t g_share_smem = [] {
+  const char *e = std::getenv("CC_K1_SHARE_SMEM_KB");
+  return (size_t)(e ? std::atoi(e) : 0) * 1024;
+}();
 // consumer quads per thread: 1 (24 warps) or 2 (12 register-capped warps); 0 = by shape
 static int g_resident_nq = [] {
   const char *e = std::getenv("CC_K1_RESIDENT_NQ");  // experiments
@@ -730,7 +738,9 @@ static bool resident_plan(k1r::Params &q, int mode, int x_dtype, int nq) {
     q.off_red = take((size_t)(nq == 2 ? Geo<2>::CW : Geo<1>::CW) * 32 * 8);
     return off + 16 * 8 + 64;  // + static shared (gseg, last)
   };
-  const size_t budget = kSmemMax - 1024;
+  // the register-capped form shares its SMs (the previous layer's decode, NCCL's
+  // collective kernels at N > 1): it leaves kShareSmem of shared memory free
+  const size_t budget = kSmemMax - 1024 - (nq == 2 ? g_share_smem : 0);
   // 1. every row in shared memory (t, and base when it fits too)
   for (int keep_base : {aux ? 1 : 0, 0}) {
     for (int S = kMaxStages; S >= 2; --S)
