@@ -44,8 +44,9 @@ for rows, keep, res in ([] if os.environ.get('TK_TIMELINE_ONLY') else [(r, k, s)
 import json  # noqa: E402
 names = ["start", "A_done", "bar1", "find1", "bar2", "list_ready", "warp_counts", "lvl_a", "lvl_b", "selected", "write", "end"]
 import bench  # noqa: E402  (FLUX-like inputs of the benchmark)
-for rows, data, keep in [(r, d, k) for r in (512, 1024, 2048) for d in ("randscale", "flux") for k in (0.01, 0.1)]:
-    lib.cc_debug_topk_resident(1)
+rows_list = [int(r) for r in os.environ.get("TK_ROWS", "512,1024,2048").split(",")]
+for rows, data, keep in [(r, d, k) for r in rows_list for d in ("randscale", "flux") for k in (0.01, 0.1)]:
+    lib.cc_debug_topk_resident(2 if rows >= 4096 else 1)
     spec = cx.CompressorSpec(cx.CompressorKind.TOPK, keep_fraction=keep)
     g = torch.Generator(device="cuda").manual_seed(0)
     if data == "flux":  # two consecutive denoising steps per layer, alternated
