@@ -71,11 +71,11 @@ def parse(argv=None):
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sim", action="store_true", help="skip the single-GPU per-rank simulations of "
                     "the 2/4/8-GPU patch-parallel and 8-GPU Ulysses configs (`per_rank_sim`)")
-    ap.add_argument("--no-overlap", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true", help="K2 on the compute stream (default: its own "
+                    "decode stream, so layer l's decode overlaps layer l+1's K1: +3 %% at N=1, measured)")
     ap.add_argument("--pdl", type=int, default=None, help="programmatic dependent launch for K1/K2 "
                     "(1 on, 0 off; default: the library default)")
-    ap.add_argument("--overlap", action="store_true", help="run K2 on its own stream even at N=1 (the "
-                    "loopback receiver has no communication to hide; two HBM-bound kernels gain nothing)")
+    ap.add_argument("--overlap", action="store_true", help="(default) K2 on its own decode stream")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from Python instead of "
                                                              "replaying a captured CUDA graph per step")
     ap.add_argument("--cpu-procs", type=int, default=None, help="host processes for the CPU path "
@@ -389,7 +389,7 @@ def run_b200(a, world, rank):
     lo, hi = bounds[rank]
     n_own = hi - lo
     Ex = RingExchange if a.topology == "ring" else PatchParallelExchange
-    overlap = (world > 1 or a.overlap) and not a.no_overlap
+    overlap = not a.no_overlap
     exs = []
 
     def make_exchanges():

@@ -139,6 +139,9 @@ void set_topk_resident_enabled(int on);
 void set_topk_timer(void *buf);
 void set_orth1_stamps(void *buf);
 void set_orth_cluster(int on);
+namespace rng {
+void set_gauss_stamps(void *buf);
+}
 int64_t topk_resident_launches();
 int topk_encode(int64_t n, int64_t C, int64_t k, const float *t, uint8_t *body, float *decoded, void *ws,
                 int64_t ws_bytes, cudaStream_t st);
@@ -224,6 +227,7 @@ CC_API int64_t cc_debug_topk_resident_count(void) { return topk_resident_launche
 CC_API void cc_debug_topk_timer(void *dev_buf) { set_topk_timer(dev_buf); }
 CC_API void cc_debug_orth_stamps(void *dev_buf) { set_orth1_stamps(dev_buf); }
 CC_API void cc_debug_orth_cluster(int enable) { set_orth_cluster(enable); }
+CC_API void cc_debug_gauss_stamps(void *dev_buf) { rng::set_gauss_stamps(dev_buf); }
 
 CC_API int64_t cc_topk_count(int64_t rows, int64_t cols, double keep_fraction) {
   if (rows < 1 || cols < 1 || !(keep_fraction > 0.0 && keep_fraction <= 1.0)) return CC_ERR_ARG;

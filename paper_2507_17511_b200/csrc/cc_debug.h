@@ -74,6 +74,9 @@ CC_API void cc_debug_orth_stamps(void *dev_buf);
 /* low-rank orthogonalisation: 1 = thread-block-cluster CholQR2 (default),
  * 0 = the single-CTA / cooperative-grid forms (A/B and cross-checks) */
 CC_API void cc_debug_orth_cluster(int enable);
+/* profiling only: device buffer of 16 u64 %globaltimer stamps of the device Gaussian
+ * draw's phases (NULL disables) */
+CC_API void cc_debug_gauss_stamps(void *dev_buf);
 
 #ifdef __cplusplus
 }

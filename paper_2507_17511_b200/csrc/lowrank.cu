@@ -26,7 +26,7 @@
 namespace cc {
 int64_t tc_partial_floats(int64_t n, int64_t C, int r);
 int tc_project(int mode, const float *A, const float *S, float *D, float *Dpart, int64_t n, int64_t C, int r,
-               cudaStream_t st);
+               cudaStream_t st, __half *d16 = nullptr);
 int lowrank_backend();
 
 namespace lr {
@@ -747,7 +747,7 @@ constexpr int kOrthClThreads = 256;
 template <int RP>
 __global__ void __launch_bounds__(kOrthClThreads, 1) k_orth_cl(const float *__restrict__ Min, float *__restrict__ out,
                                                                 int64_t m, int r, double *__restrict__ scratch,
-                                                                unsigned long long seed) {
+                                                                unsigned long long seed, __half *__restrict__ out16) {
   namespace cg = cooperative_groups;
   constexpr int W = kOrthClThreads / 32, RB = RP / 8, LD = 17;
   cg::cluster_group cluster = cg::this_cluster();
@@ -847,6 +847,13 @@ __global__ void __launch_bounds__(kOrthClThreads, 1) k_orth_cl(const float *__re
     for (int64_t e = tid; e < nr * r; e += kOrthClThreads) {
       const int64_t i = e / r;
       if (r0 + i < m) out[(r0 + i) * r + e % r] = (float)M[(e % r) * mp + i];
+    }
+    if (out16) {  // the f16 body factor, column-major (cx:425): f16(f32(q)) as k_pack_f16
+      for (int64_t e = tid; e < nr * r; e += kOrthClThreads) {
+        const int k = (int)(e / nr);
+        const int64_t i = e % nr;
+        if (r0 + i < m) out16[(int64_t)k * m + r0 + i] = __float2half_rn((float)M[k * mp + i]);
+      }
     }
   } else if (q == 0) {  // every CTA saw the same pivots: CTA 0 alone runs CGS2 (la:77-112)
     cgs2_block(Min, scratch, out, m, r, seed, red, coef);
@@ -1147,7 +1154,9 @@ void set_orth1_stamps(void *buf) {
 }
 
 // M (f32 [m, r]) -> orthonormal f32 columns written to out (may alias M)
-static void orth(const float *M, float *out, int64_t m, int r, const lr::Work &w, cudaStream_t st) {
+// returns true when the f16 column-major copy (out16, optional) was written too
+static bool orth(const float *M, float *out, int64_t m, int r, const lr::Work &w, cudaStream_t st,
+                 __half *out16 = nullptr) {
   using namespace lr;
   const int rp = r <= 8 ? 8 : 16;
   if (r <= 16 && g_orth_cluster) {  // cluster of kOrthCl CTAs (DSMEM Gram exchange)
@@ -1178,16 +1187,38 @@ static void orth(const float *M, float *out, int64_t m, int r, const lr::Work &w
       cfg.numAttrs = 1;
       unsigned long long seed = g_lr_seed++;
       double *scratch = w.M64;
-      const cudaError_t e = rp == 8 ? cudaLaunchKernelEx(&cfg, k_orth_cl<8>, M, out, m, r, scratch, seed)
-                                    : cudaLaunchKernelEx(&cfg, k_orth_cl<16>, M, out, m, r, scratch, seed);
+      __half *o16 = out16;
+      const cudaError_t e = rp == 8 ? cudaLaunchKernelEx(&cfg, k_orth_cl<8>, M, out, m, r, scratch, seed, o16)
+                                    : cudaLaunchKernelEx(&cfg, k_orth_cl<16>, M, out, m, r, scratch, seed, o16);
       if (e == cudaSuccess) {
         count_launch();
-        return;
+        return true;
       }
       cudaGetLastError();
     }
   }
   const size_t need = (size_t)(((m + 7) & ~int64_t(7)) | 1) * rp * 8;
+  if (r <= 16) {  // one CTA (no cluster launch available): same mathematics, no grid sync
+    const void *kern = rp == 8 ? (const void *)k_orth1<8> : (const void *)k_orth1<16>;
+    static size_t max_dyn[2] = {0, 0};
+    size_t &md = max_dyn[rp == 16];
+    if (md == 0) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, kern);
+      md = 227 * 1024 - fa.sharedSizeBytes - 1024;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)md);
+    }
+    if (need <= md) {
+      unsigned long long seed = g_lr_seed++;
+      double *scratch = w.M64;
+      void *args[] = {&M, &out, &m, &r, &scratch, &seed};
+      if (cudaLaunchKernel(kern, dim3(1), dim3(kOrth1Threads), args, need, st) == cudaSuccess) {
+        count_launch();
+        return false;
+      }
+      cudaGetLastError();
+    }
+  }
   {
     const int nb = (int)cdiv(m, kGramRows);
     const size_t smem = sizeof(double) * (size_t)(kGramRows + 3 * kMaxR) * (kMaxR + 1);
@@ -1202,7 +1233,7 @@ static void orth(const float *M, float *out, int64_t m, int r, const lr::Work &w
     if (cudaLaunchCooperativeKernel((const void *)k_orth, dim3(nb), dim3(kOrthThreads), args, smem, st) ==
         cudaSuccess) {
       count_launch();
-      return;
+      return false;
     }
     cudaGetLastError();  // fall through to the multi-kernel CholQR2
   }
@@ -1218,6 +1249,7 @@ static void orth(const float *M, float *out, int64_t m, int r, const lr::Work &w
   k_cgs2_fallback<<<1, 1024, 0, st>>>(M, w.M64, m, r, w.flag, g_lr_seed++);
   k_to32<<<b1, 256, 0, st>>>(w.M64, out, cnt);
   count_launch(4 + 6);
+  return false;
 }
 
 static void aq(const float *A, const float *Q, float *Y, const lr::Work &w, int64_t n, int64_t C, int r,
@@ -1230,16 +1262,18 @@ static void aq(const float *A, const float *Q, float *Y, const lr::Work &w, int6
   count_launch();
 }
 
-static void aty(const float *A, const float *Y, float *Z, const lr::Work &w, int64_t n, int64_t C, int r,
-                cudaStream_t st) {
+// returns true when the f16 column-major copy (z16, optional) was written too
+static bool aty(const float *A, const float *Y, float *Z, const lr::Work &w, int64_t n, int64_t C, int r,
+                cudaStream_t st, __half *z16 = nullptr) {
   if (lowrank_backend() == 1) {
-    tc_project(1, A, Y, Z, w.TCpart, n, C, r, st);
-    return;
+    tc_project(1, A, Y, Z, w.TCpart, n, C, r, st, z16);
+    return z16 != nullptr;
   }
   dim3 g((unsigned)cdiv(C, lr::kColsATY), lr::kSplitATY);
   lr::k_aty<<<g, lr::kThreads, 0, st>>>(A, Y, w.Zpart, n, C, r);
   lr::k_zsum<<<(unsigned)cdiv(C * r, 256), 256, 0, st>>>(w.Zpart, Z, C, r);
   count_launch(2);
+  return false;
 }
 
 static void decode_into(const uint8_t *body, int int4, int64_t n, int64_t C, int r, float *out, int acc,
@@ -1271,13 +1305,20 @@ int lowrank_encode(int int4, int64_t n, int64_t C, int64_t r64, int iters, const
     orth(w.Z, w.Q, C, r, w, st);
   }
   aq(t, w.Q, w.Y, w, n, C, r, st);
-  orth(w.Y, w.U, n, r, w, st);                 // U = orth(A Q)       (cx:411)
-  aty(t, w.U, w.W, w, n, C, r, st);            // W = A^T U           (cx:419)
+  // f16 bodies: U and W are written into the body by the last orth / projection
+  // themselves when those paths can (column-major f16, cx:425), else packed here
+  __half *h = int4 ? nullptr : reinterpret_cast<__half *>(body);
+  const bool u_packed = orth(w.Y, w.U, n, r, w, st, h);       // U = orth(A Q)  (cx:411)
+  const bool w_packed = aty(t, w.U, w.W, w, n, C, r, st, h ? h + n * r : nullptr);  // W = A^T U (cx:419)
   if (!int4) {
-    __half *h = reinterpret_cast<__half *>(body);
-    lr::k_pack_f16<<<(unsigned)cdiv(n * r, 256), 256, 0, st>>>(w.U, n, r, h);
-    lr::k_pack_f16<<<(unsigned)cdiv(C * r, 256), 256, 0, st>>>(w.W, C, r, h + n * r);
-    count_launch(2);
+    if (!u_packed) {
+      lr::k_pack_f16<<<(unsigned)cdiv(n * r, 256), 256, 0, st>>>(w.U, n, r, h);
+      count_launch();
+    }
+    if (!w_packed) {
+      lr::k_pack_f16<<<(unsigned)cdiv(C * r, 256), 256, 0, st>>>(w.W, C, r, h + n * r);
+      count_launch();
+    }
   } else {
     float *ranges = reinterpret_cast<float *>(body);  // 2r f32: U ranges then W ranges
     lr::k_colmax<<<r, 256, 0, st>>>(w.U, n, r, ranges);

@@ -467,12 +467,15 @@ __global__ void __launch_bounds__(kTThreads) k_tc_gemm_tma(const __grid_constant
 }
 
 // fixed-order split reduction -> f32 result
-__global__ void k_tc_reduce(const float *__restrict__ Dpart, float *__restrict__ D, int64_t cnt, int splits) {
+// (+ optionally the f16 column-major copy of D [M, r], the body factor layout cx:425)
+__global__ void k_tc_reduce(const float *__restrict__ Dpart, float *__restrict__ D, int64_t cnt, int splits,
+                            __half *__restrict__ d16, int r) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= cnt) return;
   float s = 0.0f;
   for (int sp = 0; sp < splits; ++sp) s += Dpart[(int64_t)sp * cnt + e];
   D[e] = s;
+  if (d16) d16[(e % r) * (cnt / r) + e / r] = __float2half_rn(s);
 }
 
 }  // namespace tc
@@ -581,7 +584,7 @@ static void tc_launch(dim3 grid, size_t smem, cudaStream_t st, const float *A, c
 
 // D = A Q (mode 0) or A^T Y (mode 1) on the tensor cores; Dpart = scratch of tc_partial_floats()
 int tc_project(int mode, const float *A, const float *S, float *D, float *Dpart, int64_t n, int64_t C, int r,
-               cudaStream_t st) {
+               cudaStream_t st, __half *d16) {
   const int NP = r <= 16 ? 16 : 32;
   const int64_t M = mode == 0 ? n : C, K = mode == 0 ? C : n;
   int64_t nsplit, kper;
@@ -615,7 +618,7 @@ int tc_project(int mode, const float *A, const float *S, float *D, float *Dpart,
     else tc_launch<1, 32>(grid, smem, st, A, S, Dpart, n, C, r, kper, vec);
   }
   const int64_t cnt = M * r;
-  tc::k_tc_reduce<<<(unsigned)cdiv(cnt, 256), 256, 0, st>>>(Dpart, D, cnt, (int)nsplit);
+  tc::k_tc_reduce<<<(unsigned)cdiv(cnt, 256), 256, 0, st>>>(Dpart, D, cnt, (int)nsplit, d16, r);
   count_launch(2);
   return cuda_status("tc_project");
 }

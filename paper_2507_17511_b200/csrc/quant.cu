@@ -29,6 +29,7 @@
 #include "cc_internal.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace cc {
@@ -571,6 +572,68 @@ __global__ void __launch_bounds__(256) k_decode_vec(const __grid_constant__ Peer
   }
 }
 
+// the same decode in 128-thread blocks capped at 32 registers: small enough to share an
+// SM with a running K1 (800 threads x 72 registers), so a decode on another stream
+// fills K1's hand-off bubbles (overlapped steps)
+template <int CODEC, bool ACC>
+__global__ void __maxnreg__(32) k_decode_vec_small(const __grid_constant__ PeerBatch pb, int64_t C, int RB) {
+  constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
+  constexpr int U = kDecRows;  // rows in flight per thread
+  pdl_wait();  // PDL launches only: the bodies come from the previous kernel (K1 / the collective)
+  const int peer = blockIdx.z;
+  const int64_t n = pb.rows[peer];
+  const int64_t r0 = (int64_t)blockIdx.y * RB;
+  if (r0 >= n) return;
+  const uint8_t *codes = pb.body[peer];
+  float *base = pb.base[peer];
+  const int64_t cbytes = (n * C * bits + 7) / 8;
+  const uint8_t *ub = codes + cbytes;
+  const uint8_t *vb = ub + 4 * n;
+  const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (j0 >= C) return;
+  const int rows = (int)(RB < n - r0 ? (int64_t)RB : n - r0);
+  float vf[4];
+  bool col_ok = true;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    vf[q] = load_f32_bytes(vb + 4 * (j0 + q));
+    col_ok = col_ok && dec_scale_ok(fabsf(vf[q]));
+  }
+  for (int rr = 0; rr < rows; rr += U) {
+    float4 bv[U];
+    uint32_t cw[U];
+    float uf[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const bool ok = (rr + k) < rows;
+      const int64_t i = r0 + rr + k;
+      const int64_t e = i * C + j0;
+      if (ACC) bv[k] = ok ? *reinterpret_cast<const float4 *>(base + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      uf[k] = ok ? load_f32_bytes(ub + 4 * i) : 1.0f;
+      if (!ok) {
+        cw[k] = 0;
+        continue;
+      }
+      if constexpr (CODEC == CC_SIGN1) cw[k] = (codes[e >> 3] >> (e & 7)) & 0xfu;
+      else if constexpr (CODEC == CC_QUANT2) cw[k] = codes[e >> 2];
+      else cw[k] = *reinterpret_cast<const uint16_t *>(codes + (e >> 1));
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if ((rr + k) < rows) {
+        const int64_t e = (r0 + rr + k) * C + j0;
+        float d[4];
+        decode4<CODEC>(cw[k], uf[k], dec_scale_ok(fabsf(uf[k])), vf, col_ok, d);
+        float4 o;
+        if (ACC) o = make_float4(__fadd_rn(bv[k].x, d[0]), __fadd_rn(bv[k].y, d[1]), __fadd_rn(bv[k].z, d[2]),
+                                 __fadd_rn(bv[k].w, d[3]));
+        else o = make_float4(d[0], d[1], d[2], d[3]);
+        __stcs(reinterpret_cast<float4 *>(base + e), o);
+      }
+    }
+  }
+}
+
 template <int CODEC, bool ACC>
 __global__ void __launch_bounds__(256) k_decode_scalar(const __grid_constant__ PeerBatch pb, int64_t C) {
   constexpr int bits = CODEC == CC_SIGN1 ? 1 : (CODEC == CC_QUANT2 ? 2 : 4);
@@ -742,8 +805,20 @@ int quant_encode_step(int codec, int mode, int scale_mode, int64_t n, int64_t C,
   return CC_ERR_ARG;
 }
 
+static int g_dec_small = [] {
+  const char *e = std::getenv("CC_K2_SMALL");  // 1: the register-capped 128-thread decode
+  return e ? std::atoi(e) : 0;
+}();
+void set_decode_small(int on) { g_dec_small = on; }
+
 template <int CODEC, bool ACC>
 static void launch_decode(const PeerBatch &pb, int count, int64_t maxrows, int64_t C, bool vec, cudaStream_t st) {
+  if (vec && g_dec_small && C % 512 == 0) {
+    dim3 grid((unsigned)(C / 512), (unsigned)cdiv(maxrows, kDecRows), count);
+    k_decode_vec_small<CODEC, ACC><<<grid, 128, 0, st>>>(pb, C, kDecRows);
+    count_launch();
+    return;
+  }
   if (vec) {
     QPlan p;
     plan_shape(p, maxrows, C, true);

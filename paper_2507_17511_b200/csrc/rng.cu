@@ -190,6 +190,16 @@ __device__ __forceinline__ bool slow_pos(uint64_t r, const uint64_t *ki) {
   return ((r >> 9) & 0x000fffffffffffffull) >= ki[r & 0xff];
 }
 
+__device__ unsigned long long *g_gauss_stamps = nullptr;  // profiling: [16] %globaltimer stamps
+
+__device__ __forceinline__ void gstamp(int i) {
+  if (g_gauss_stamps && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_gauss_stamps[i] = t;
+  }
+}
+
 __global__ void __launch_bounds__(kGenThreads) k_gauss_gen(const uint32_t *__restrict__ key, int nw, int64_t M,
                                                             int64_t npos, Work w) {
   __shared__ Shared sh;
@@ -202,12 +212,14 @@ __global__ void __launch_bounds__(kGenThreads) k_gauss_gen(const uint32_t *__res
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   stage_tables(tki, twi, tfi);
   const Zig zt{tki, twi, tfi};
+  if (blockIdx.x == 0) gstamp(0);
   if (tid == 0) {
     uint32_t kw[kMaxWords];
     for (int i = 0; i < nw; ++i) kw[i] = key[i];
     seed_pcg(kw, nw, sh.state0, sh.inc);
   }
   __syncthreads();
+  if (blockIdx.x == 0) gstamp(1);
   // ---- generate this thread's kGenPer positions ----
   const int64_t p0 = (int64_t)blockIdx.x * kGenPos + (int64_t)tid * kGenPer;
   uint32_t slowmask = 0;
@@ -224,6 +236,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gauss_gen(const uint32_t *__res
       }
     }
   }
+  if (blockIdx.x == 0) gstamp(2);
   // ---- this CTA's candidate list (ascending), per-CTA segment ----
   const uint32_t nl = __popc(slowmask);
   uint32_t incl = nl;
@@ -246,6 +259,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gauss_gen(const uint32_t *__res
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  gstamp(3);
   // gather every CTA's candidates in position order
   __shared__ uint32_t s_nc[1024];
   for (unsigned b = tid; b < gridDim.x && b < 1024; b += kGenThreads) s_nc[b] = __ldcg(w.ncand + b);
@@ -289,6 +303,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gauss_gen(const uint32_t *__res
     }
     return;
   }
+  gstamp(4);
   // evaluate every candidate as a draw start
   for (uint32_t i = tid; i < total; i += kGenThreads) {
     int64_t nx;
@@ -297,6 +312,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gauss_gen(const uint32_t *__res
     c_real[i] = 1u;
   }
   __syncthreads();
+  gstamp(5);
   // real starts: a candidate is skipped iff a REAL candidate before it consumed it.
   // Consumed ranges are a few positions long, so only the nearest preceding
   // candidates can cover one; iterate to the fixed point (a couple of rounds).
@@ -333,6 +349,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gauss_gen(const uint32_t *__res
   }
   // output index of real candidate k: p_k minus the extra positions consumed by the
   // real slow draws before it; shift after it = p_k + cons_k - (out_k + 1)
+  gstamp(6);
   // block scan over the candidates (thread t: candidates [t K, t K + K)): events
   // before each real one (event slot) and extra positions consumed before it
   {
@@ -384,6 +401,8 @@ __global__ void __launch_bounds__(kGenThreads) k_gauss_gen(const uint32_t *__res
       *w.ticket = 0u;  // ticket ready for the next launch
     }
   }
+  __syncthreads();
+  gstamp(7);
 }
 
 __global__ void __launch_bounds__(kOutThreads) k_gauss_out(uint32_t *key, int nw, int step_word, int64_t M,
@@ -406,6 +425,7 @@ __global__ void __launch_bounds__(kOutThreads) k_gauss_out(uint32_t *key, int nw
     seed_pcg(kw, nw, sh.state0, sh.inc);  // only for draws past the generated positions
   }
   __syncthreads();
+  if (blockIdx.x == 0) gstamp(8);
   const int64_t j0 = (int64_t)blockIdx.x * kOutThreads * 4 + tid;
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -428,6 +448,15 @@ __global__ void __launch_bounds__(kOutThreads) k_gauss_out(uint32_t *key, int nw
     out[j] = (float)v;
   }
   if (blockIdx.x == 0 && tid == 0 && step_word >= 0) key[step_word] += 1u;  // the next step's key
+  if (blockIdx.x == 0) {
+    __syncthreads();
+    gstamp(9);
+  }
+}
+
+void set_gauss_stamps(void *buf) {
+  unsigned long long *p = reinterpret_cast<unsigned long long *>(buf);
+  cudaMemcpyToSymbol(g_gauss_stamps, &p, sizeof(p));
 }
 
 static int64_t npos_for(int64_t M) { return M + M / 8 + 1024; }
