@@ -73,10 +73,66 @@ class DeviceKey:
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.words = torch.tensor(words, dtype=torch.int64).to(torch.int32).to(dev)
 
+    def start_block(self, rows, cols):
+        """This step's start block [rows, cols] f32 on the device, drawn one step AHEAD.
+
+        An advancing key's next block depends only on the key, so every call also queues
+        the NEXT step's draw on a side stream (forked from the caller's stream, joined at
+        the start of the next call): the draw overlaps the rest of the step instead of
+        leading it.  The block is handed over by a stream-ordered copy (next -> current),
+        so a captured step stays correct however its graph is replayed.  The first call
+        draws its own block in line; non-advancing keys always draw in line.  Returns a
+        device tensor valid until the next call."""
+        import torch
+
+        from . import _lib
+
+        lib = _lib.load()
+        cur = torch.cuda.current_stream()
+        shape = (int(rows), int(cols))
+        if getattr(self, "_shape", None) != shape:  # (re)initialise the buffers
+            self._shape = shape
+            self._cur = torch.empty(shape, dtype=torch.float32, device=self.words.device)
+            self._next = torch.empty_like(self._cur)
+            self._ws = [torch.empty(_lib.check(lib.cc_gaussian_workspace_bytes(*shape)), dtype=torch.uint8,
+                                    device=self.words.device) for _ in range(2)]
+            self._side = torch.cuda.Stream(self.words.device)
+            self._ready = False
+
+        def draw(buf, ws):
+            _lib.check(lib.cc_gaussian_keyed(shape[0], shape[1], _lib.ptr(self.words), self.nwords, self.step_word,
+                                             _lib.ptr(buf), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()),
+                       "gaussian_keyed")
+
+        if not self.advance:
+            draw(self._cur, self._ws[0])
+            return self._cur
+        if self._ready:  # the block drawn ahead by the previous call (joined by its join())
+            self._cur.copy_(self._next)
+        else:
+            draw(self._cur, self._ws[0])
+        self._side.wait_stream(cur)  # `next` is free (copied above) and the key word is current
+        with torch.cuda.stream(self._side):
+            draw(self._next, self._ws[1])  # the next step's block (the key advances)
+        self._ready = True
+        return self._cur
+
+    def join(self):
+        """Join the draw-ahead side stream back into the caller's stream.  Called right
+        after the step's launches are queued: the draw (tens of us) finishes long before
+        the step (hundreds), so nothing waits, and a capture never ends with unjoined work."""
+        import torch
+
+        if getattr(self, "_ready", False) and self.advance:
+            torch.cuda.current_stream().wait_stream(self._side)
+
     def host_generator(self):
         """The numpy stream this key stands for at its current step (test helper; syncs)."""
+        import torch
+
+        torch.cuda.synchronize()
         words = [int(w) & 0xFFFFFFFF for w in self.words.cpu().tolist()]
         key = list(self.key)
-        if self.advance:
-            key[-1] = words[self.step_word]
+        if self.advance:  # a block drawn ahead has already advanced the device word
+            key[-1] = words[self.step_word] - (1 if getattr(self, "_ready", False) else 0)
         return spawn_rng(self.seed, *key)

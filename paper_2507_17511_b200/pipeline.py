@@ -216,8 +216,8 @@ def _encode_step_lowrank(state, x, codec, rng, mode, aux, rec, body_out):
     tag = _lib.CC_LOWRANK4 if codec.int4_factors else _lib.CC_LOWRANK
     body = _body_slice(body_out, lib.cc_body_bytes(tag, rows, cols, r))
     ws = cx.workspace(_lib.check(lib.cc_lowrank_step_workspace_bytes(rows, cols, r)), "lowrank_step")
-    if isinstance(rng, DeviceKey):
-        q0, key, nwords, step_word = None, rng.words, rng.nwords, rng.step_word
+    if isinstance(rng, DeviceKey):  # drawn on the device, one step ahead (DeviceKey.start_block)
+        q0, key, nwords, step_word = rng.start_block(cols, r), None, 0, -1
     else:
         q0 = cx.subspace_init(rng, cols, r)
         q0 = cx._stage_h2d(q0, x.device)
@@ -227,6 +227,8 @@ def _encode_step_lowrank(state, x, codec, rng, mode, aux, rec, body_out):
                                           _lib.ptr(q0), _lib.ptr(key), nwords, step_word, _lib.ptr(body),
                                           _lib.ptr(ws), ws.numel(), _lib.ptr(rec), _lib.stream_ptr()),
                "lowrank encode_step")
+    if isinstance(rng, DeviceKey):
+        rng.join()
     return cx.LowRankPayload(rows, cols, body, r, codec.int4_factors)
 
 

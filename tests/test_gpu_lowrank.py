@@ -235,16 +235,17 @@ def test_fused_step_device_key_equals_host_rng(mode, int4):
 
 
 def test_lowrank_exchange_graph_replay_equals_eager():
-    """The low-rank patch-parallel step (sim_world P=4, rank 0) captured in a CUDA
-    graph with an advancing device key: replays reproduce the eager steps bit for
-    bit (the key's step word advances on the device)."""
+    """The low-rank patch-parallel step (sim_world P=4, rank 0) captured in ONE CUDA graph
+    with an advancing device key (start blocks drawn one step ahead on a side stream) and
+    replayed three times: every replay equals the matching eager step bit for bit (the
+    key advances on the device, the drawn-ahead block is handed over in stream order)."""
     cx, pl, linalg = _mods()
     from paper_2507_17511_b200.comm import PatchParallelExchange
 
     rows, cols, P = 1024, 3072, 4
     spec = _spec(8, 2)
     xs = [torch.from_numpy(x).cuda().to(torch.bfloat16)[: rows // P].contiguous()
-          for x in synth.flux_like(rows, cols, 6, seed=5)]
+          for x in synth.flux_like(rows, cols, 4, seed=5)]
     ea = PatchParallelExchange(rows, cols, spec, sim_world=(P, 0))
     eb = PatchParallelExchange(rows, cols, spec, sim_world=(P, 0))
     ka = linalg.DeviceKey(3, 6, 0, 2, advance=True)
@@ -252,23 +253,25 @@ def test_lowrank_exchange_graph_replay_equals_eager():
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         for e, k in ((ea, ka), (eb, kb)):
-            e.step(xs[0], rng=k)
-            e.step(xs[1], rng=k)
-        outs_a = []
-        for i in range(2, 6):
-            ea.step(xs[i], rng=ka)
-            outs_a.append(ea.reconstruction().clone())
+            for i in range(3):
+                e.step(xs[i], rng=k)
+        ref = []
+        for _ in range(3):  # eager: steps 4, 5, 6 on the same input
+            ea.step(xs[3], rng=ka)
+            ref.append(ea.reconstruction().clone())
         g = torch.cuda.CUDAGraph()
-        eb.step(xs[2], rng=kb)  # warm the step's workspaces outside the capture
-        got = [eb.reconstruction().clone()]
         with torch.cuda.graph(g, stream=s):
             eb.step(xs[3], rng=kb)
             s.wait_stream(eb.streams.decode)
         eb.after_capture()
-        g.replay()  # encodes xs[3] with the key advanced to t = 4 on the device
+        got = []
+        for _ in range(3):
+            g.replay()
+            s.synchronize()
+            got.append(eb.reconstruction().clone())
     torch.cuda.synchronize()
-    got.append(eb.reconstruction().clone())
-    assert torch.equal(got[0], outs_a[0]) and torch.equal(got[1], outs_a[1])
+    for i in range(3):
+        assert torch.equal(got[i], ref[i]), f"replay {i + 1}"
 
 
 @pytest.mark.parametrize("shape", [(256, 3072), (1024, 3072), (4096, 3072), (100, 999)], ids=lambda s: f"{s[0]}x{s[1]}")
