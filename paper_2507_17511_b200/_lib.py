@@ -107,6 +107,9 @@ SIGNATURES = {
     "cc_debug_orth_stamps": (None, [_p]),
     "cc_debug_orth_cluster": (None, [_i32]),
     "cc_debug_gauss_stamps": (None, [_p]),
+    "cc_debug_lowrank_fused": (None, [_i32]),
+    "cc_debug_lowrank_fused_count": (_i64, []),
+    "cc_debug_lowrank_fused_stamps": (None, [_p]),
 }
 # private test / profiling knobs (csrc/cc_debug.h), not part of the public ABI
 DEBUG_HEADER = os.path.join(HERE, "csrc", "cc_debug.h")

@@ -139,6 +139,9 @@ void set_topk_resident_enabled(int on);
 void set_topk_timer(void *buf);
 void set_orth1_stamps(void *buf);
 void set_orth_cluster(int on);
+void set_lowrank_fused(int on);
+int64_t lowrank_fused_launches();
+void set_lowrank_fused_stamps(void *buf);
 namespace rng {
 void set_gauss_stamps(void *buf);
 }
@@ -227,6 +230,9 @@ CC_API int64_t cc_debug_topk_resident_count(void) { return topk_resident_launche
 CC_API void cc_debug_topk_timer(void *dev_buf) { set_topk_timer(dev_buf); }
 CC_API void cc_debug_orth_stamps(void *dev_buf) { set_orth1_stamps(dev_buf); }
 CC_API void cc_debug_orth_cluster(int enable) { set_orth_cluster(enable); }
+CC_API void cc_debug_lowrank_fused(int enable) { set_lowrank_fused(enable); }
+CC_API int64_t cc_debug_lowrank_fused_count(void) { return lowrank_fused_launches(); }
+CC_API void cc_debug_lowrank_fused_stamps(void *dev_buf) { set_lowrank_fused_stamps(dev_buf); }
 CC_API void cc_debug_gauss_stamps(void *dev_buf) { rng::set_gauss_stamps(dev_buf); }
 
 CC_API int64_t cc_topk_count(int64_t rows, int64_t cols, double keep_fraction) {

@@ -78,6 +78,15 @@ CC_API void cc_debug_orth_cluster(int enable);
  * draw's phases (NULL disables) */
 CC_API void cc_debug_gauss_stamps(void *dev_buf);
 
+/* low-rank encode_step as one persistent cluster launch (lr_step.cu): 1 = whenever it
+ * covers the shape (default), 0 = always the multi-kernel step (A/B and cross-checks) */
+CC_API void cc_debug_lowrank_fused(int enable);
+/* launches of the fused low-rank step since load */
+CC_API int64_t cc_debug_lowrank_fused_count(void);
+/* profiling only: device buffer of 32 u64 %globaltimer stamps of the fused low-rank
+ * step's phases (CTA 0; NULL disables) */
+CC_API void cc_debug_lowrank_fused_stamps(void *dev_buf);
+
 #ifdef __cplusplus
 }
 #endif

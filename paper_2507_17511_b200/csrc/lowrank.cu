@@ -16,6 +16,7 @@
 // Parity is tolerance-based (f64 summation order), see tests/test_gpu_lowrank.py.
 #include "cc_common.cuh"
 #include "cc_internal.h"
+#include "lr_dev.cuh"
 
 #include <algorithm>
 #include <cooperative_groups.h>
@@ -38,7 +39,6 @@ constexpr int kKChunk = 96;    // K chunk staged in shared memory
 constexpr int kColsATY = 32;   // columns of A per CTA in Z = A^T Y
 constexpr int kSplitATY = 4;   // row splits (partial Z, fixed-order reduction)
 constexpr int kGramRows = 128; // rows per CTA in the Gram partials
-constexpr double kDegenerate = 1e-12;  // la:13
 
 // ---------------------------------------------------------------------------
 // Y[n, r] = A[n, C] Q[C, r]   (f64 accumulate, f32 store: la.matmul)
@@ -309,53 +309,6 @@ __global__ void __launch_bounds__(1024) k_cgs2_fallback(const float *__restrict_
 // ---------------------------------------------------------------------------
 constexpr int kOrthThreads = 256;
 
-__device__ void cgs2_block(const float *__restrict__ orig, double *__restrict__ M, float *__restrict__ out,
-                           int64_t m, int r, unsigned long long seed, double *red, double *coef) {
-  auto block_sum = [&](double v) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    double s = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-    __syncthreads();
-    return s;
-  };
-  curandStatePhilox4_32_10_t rng;
-  curand_init(seed, threadIdx.x, 0, &rng);
-  for (int64_t e = threadIdx.x; e < m * r; e += blockDim.x) M[e] = (double)orig[e];
-  __syncthreads();
-  for (int j = 0; j < r; ++j) {
-    for (int attempt = 0;; ++attempt) {
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int k = 0; k < j; ++k) {
-          double part = 0.0;
-          for (int64_t i = threadIdx.x; i < m; i += blockDim.x) part += M[i * r + k] * M[i * r + j];
-          const double s = block_sum(part);
-          if (threadIdx.x == 0) coef[k] = s;
-        }
-        __syncthreads();
-        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-          double v = M[i * r + j];
-          for (int k = 0; k < j; ++k) v -= M[i * r + k] * coef[k];
-          M[i * r + j] = v;
-        }
-        __syncthreads();
-      }
-      double part = 0.0;
-      for (int64_t i = threadIdx.x; i < m; i += blockDim.x) part += M[i * r + j] * M[i * r + j];
-      const double nsq = block_sum(part);
-      if (nsq >= kDegenerate || attempt > 16) {
-        const double inv = 1.0 / sqrt(nsq);
-        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) M[i * r + j] *= inv;
-        __syncthreads();
-        break;
-      }
-      for (int64_t i = threadIdx.x; i < m; i += blockDim.x) M[i * r + j] = (double)curand_normal(&rng);
-      __syncthreads();
-    }
-  }
-  for (int64_t e = threadIdx.x; e < m * r; e += blockDim.x) out[e] = (float)M[e];
-}
 
 // one warp: right-looking Cholesky of G (as k_chol) and R^-1 into Ri, lane c owns column c
 template <int LD = kMaxR + 1>
@@ -460,107 +413,6 @@ __global__ void __launch_bounds__(kOrthThreads) k_orth(const float *__restrict__
 // ---------------------------------------------------------------------------
 constexpr int kOrth1Threads = 512;
 
-__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
-
-// one warp, registers: G = R^T R (lane c holds column c of G / R) by RP compile-time
-// pivot steps with one rsqrt each (no division chain), then R^-1 by back
-// substitution with the reciprocal diagonal.  Rm / Ri in shared memory for the apply.
-template <int RP, int LD>
-__device__ __forceinline__ void chol_rinv_regs(const double (*G)[LD], double (*Rm)[LD], double (*Ri)[LD], int r,
-                                               int *bad) {
-  const int c = threadIdx.x & 31;
-  double g[RP];
-#pragma unroll
-  for (int a = 0; a < RP; ++a) g[a] = (c < r && a < r) ? G[a][c] : 0.0;
-  double invd[RP];
-#pragma unroll
-  for (int j = 0; j < RP; ++j) {
-    if (j >= r) break;
-    double piv = __shfl_sync(0xffffffffu, g[j], j);  // G[j][j] (Schur complement) from lane j
-    if (!(piv >= kDegenerate)) {
-      if (c == 0) *bad = 1;
-      piv = 1.0;
-    }
-    const double inv = rsqrt(piv);
-    invd[j] = inv;
-    const double rjc = c == j ? piv * inv : (c > j && c < r ? g[j] * inv : 0.0);  // R[j][c]
-    if (c < r) Rm[j][c] = rjc;
-#pragma unroll
-    for (int a = j + 1; a < RP; ++a) {
-      const double rja = __shfl_sync(0xffffffffu, rjc, a);  // R[j][a]
-      if (a < r && c >= a && c < r) g[a] -= rja * rjc;
-    }
-  }
-  __syncwarp();
-  if (c < r) {  // column c of R^-1: x[i] = (delta_ic - sum_{k>i} R[i][k] x[k]) / R[i][i]
-    double x[RP];
-#pragma unroll
-    for (int i = RP - 1; i >= 0; --i) {
-      double sacc = (i == c) ? 1.0 : 0.0;
-#pragma unroll
-      for (int k = i + 1; k < RP; ++k)
-        if (k <= c) sacc -= Rm[i][k] * x[k];
-      x[i] = (i > c || i >= r) ? 0.0 : sacc * invd[i];
-    }
-#pragma unroll
-    for (int i = 0; i < RP; ++i) Ri[i][c] = x[i];
-  }
-}
-
-// r = 8: every lane of the warp factors the WHOLE 8x8 Gram in registers (the same
-// arithmetic in every lane, no shuffles, no shared-memory round trips in the
-// pivot chain); lane c < 8 then back-substitutes column c of R^-1.  The pivot
-// chain is 8 x (rsqrt + one multiply + an independent rank-1 update).
-__device__ __forceinline__ void chol8_regs(const double (*G)[17], double (*Rm)[17], double (*Ri)[17], int *bad) {
-  const int c = threadIdx.x & 31;
-  double g[8][8];
-#pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int b = a; b < 8; ++b) g[a][b] = G[a][b];
-  double invd[8];
-  bool degenerate = false;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    double piv = g[j][j];
-    if (!(piv >= kDegenerate)) {
-      degenerate = true;
-      piv = 1.0;
-    }
-    const double inv = rsqrt(piv);
-    invd[j] = inv;
-    g[j][j] = piv * inv;  // R[j][j]
-#pragma unroll
-    for (int b = j + 1; b < 8; ++b) g[j][b] *= inv;  // R[j][b]
-#pragma unroll
-    for (int a = j + 1; a < 8; ++a)
-#pragma unroll
-      for (int b = a; b < 8; ++b) g[a][b] -= g[j][a] * g[j][b];
-  }
-  if (degenerate && c == 0) *bad = 1;
-  if (c < 8) {
-#pragma unroll
-    for (int a = 0; a < 8; ++a)  // row a of R by lane a (compile-time indices: g stays in registers)
-      if (a == c)
-#pragma unroll
-        for (int b = 0; b < 8; ++b) Rm[a][b] = b >= a ? g[a][b] : 0.0;
-    double x[8];  // column c of R^-1
-#pragma unroll
-    for (int i = 7; i >= 0; --i) {
-      double sacc = (i == c) ? 1.0 : 0.0;
-#pragma unroll
-      for (int k = i + 1; k < 8; ++k)
-        if (k <= c) sacc -= g[i][k] * x[k];
-      x[i] = i > c ? 0.0 : sacc * invd[i];
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) Ri[i][c] = x[i];
-  }
-}
 
 __device__ unsigned long long *g_orth1_stamps = nullptr;  // profiling: [16] clock64 stamps of block 0
 
@@ -1340,7 +1192,7 @@ int sum_parts(int nparts, const double *part, double *record, cudaStream_t st);
 uint8_t *stream_zero_slab(cudaStream_t st, size_t bytes);
 // low-rank words in the per-stream zeroed slab (after the top-k kernel's ~34 KB)
 constexpr size_t kLrTicketOff = 40 * 1024;
-constexpr size_t kSlabBytesNeeded = kLrTicketOff + 128;
+constexpr size_t kSlabBytesNeeded = kLrTicketOff + 128;  // (lr_step.cu's words follow at +256)
 
 // A library-owned side stream + fork / join events per (device, caller stream),
 // created on first use outside a capture (null otherwise: no fork).
@@ -1372,10 +1224,17 @@ static SideStream *side_stream(cudaStream_t st) {
   return &m.emplace(k, ss).first->second;
 }
 
+int64_t lowrank_fused_workspace_bytes(int64_t n, int64_t C, int64_t r);
+bool lowrank_fused_may_run(int64_t n, int64_t C, int64_t r, int iters, int int4);
+int lowrank_step_fused(int mode, int64_t n, int64_t C, int64_t r, int iters, int int4, const void *x, int x_dtype,
+                       float *base, float *aux, const float *q0, uint8_t *body, void *ws, int64_t ws_bytes,
+                       double *record, cudaStream_t st);
+
 // encode_step workspace: t [n, C] | Q0 [C, r] | gaussian scratch | encode workspace |
-// f64 factors [n + C, r] | record partials
+// f64 factors [n + C, r] | record partials | fused-step workspace
 static size_t lr_step_layout(int64_t n, int64_t C, int64_t r, uint8_t *w, float **t, float **q0, void **gws,
-                             size_t *gbytes, void **ews, size_t *ebytes, double **Uf, double **part) {
+                             size_t *gbytes, void **ews, size_t *ebytes, double **Uf, double **part,
+                             void **fws = nullptr, size_t *fbytes = nullptr) {
   size_t off = 0;
   auto take = [&](size_t b) {
     uint8_t *q = w ? w + off : nullptr;
@@ -1387,6 +1246,12 @@ static size_t lr_step_layout(int64_t n, int64_t C, int64_t r, uint8_t *w, float 
   const int64_t nblk = cdiv(C, lr::kThreads) * cdiv(n, lr::kOARows);
   uint8_t *pt = take(4 * (size_t)n * C), *pq = take(4 * (size_t)C * r), *pg = take(gb), *pe = take(eb);
   uint8_t *pu = take(8 * (size_t)(n + C) * r), *pp = take(16 * (size_t)nblk);
+  const size_t fb = (size_t)lowrank_fused_workspace_bytes(n, C, r);
+  uint8_t *pf = take(fb);
+  if (w && fws) {
+    *fws = pf;
+    *fbytes = fb;
+  }
   if (w) {
     *t = reinterpret_cast<float *>(pt);
     *q0 = reinterpret_cast<float *>(pq);
@@ -1418,14 +1283,28 @@ int lowrank_encode_step(int mode, int64_t n, int64_t C, int64_t r, int iters, in
     return CC_ERR_ARG;
   }
   float *t, *q0;
-  void *gws, *ews;
-  size_t gb, eb;
+  void *gws, *ews, *fws;
+  size_t gb, eb, fb;
   double *Uf, *part;
-  lr_step_layout(n, C, r, reinterpret_cast<uint8_t *>(ws), &t, &q0, &gws, &gb, &ews, &eb, &Uf, &part);
+  lr_step_layout(n, C, r, reinterpret_cast<uint8_t *>(ws), &t, &q0, &gws, &gb, &ews, &eb, &Uf, &part, &fws, &fb);
+  int rc;
+  // the whole step as one persistent cluster launch (lr_step.cu) when it covers the shape
+  bool drawn = false;
+  if (lowrank_fused_may_run(n, C, r, iters, int4)) {
+    const float *qs = q0_in;
+    if (key) {
+      rc = gaussian_keyed(C, r, key, nwords, step_word, q0, gws, (int64_t)gb, st);
+      if (rc) return rc;
+      qs = q0;
+      drawn = true;
+    }
+    rc = lowrank_step_fused(mode, n, C, r, iters, int4, x, x_dtype, base, aux, qs, body, fws, (int64_t)fb, record, st);
+    if (rc == CC_OK) return cuda_status("lowrank_encode_step (fused)");
+    if (rc != 1) return rc;
+  }
   // the start block depends only on the key: draw it on a side stream while the
   // target is formed (fork / join through events: also inside a graph capture)
-  SideStream *ss = key ? side_stream(st) : nullptr;
-  int rc;
+  SideStream *ss = (key && !drawn) ? side_stream(st) : nullptr;
   if (key && ss) {
     cudaEventRecord(ss->fork, st);
     cudaStreamWaitEvent(ss->s, ss->fork, 0);
@@ -1437,6 +1316,7 @@ int lowrank_encode_step(int mode, int64_t n, int64_t C, int64_t r, int iters, in
   if (rc) return rc;
   if (key && ss) {
     cudaStreamWaitEvent(st, ss->join, 0);
+  } else if (key && drawn) {
   } else if (key) {
     rc = gaussian_keyed(C, r, key, nwords, step_word, q0, gws, (int64_t)gb, st);
     if (rc) return rc;

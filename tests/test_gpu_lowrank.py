@@ -295,3 +295,164 @@ def test_orth_forms_agree(shape, r):
             lib.cc_debug_orth_cluster(1)
         errs.append(_relerr(p.decode().cpu().numpy(), a.cpu().numpy()))
     assert abs(errs[0] - errs[1]) <= 1e-6 * max(1.0, errs[1])
+
+
+# ---------------------------------------------------------------------------
+# The fused single-launch step (lr_step.cu): used by encode_step whenever the shard
+# is large enough for its cluster grid (n >= 8 x clusters, C % 256 == 0, r <= 8, f16
+# factors).  Checked against the multi-kernel step (same algorithm, different
+# summation orders), the reference oracle channel, the receiver, and graph replay.
+# ---------------------------------------------------------------------------
+def _lib_handle():
+    from paper_2507_17511_b200 import _lib
+
+    return _lib.load()
+
+
+def _run_steps(mode, xs, spec, key_seed, fused, dtype=torch.bfloat16):
+    _, pl, linalg = _mods()
+    lib = _lib_handle()
+    n, c = xs[0].shape
+    lib.cc_debug_lowrank_fused(fused)
+    n0 = lib.cc_debug_lowrank_fused_count()
+    try:
+        snd = pl.LayerState(mode, 1, torch.zeros(n, c, device="cuda"))
+        rcv = pl.LayerState(mode, 1, torch.zeros(n, c, device="cuda"))
+        key = linalg.DeviceKey(key_seed, 5, 2, advance=True)
+        out = []
+        for t, x in enumerate(xs, start=1):
+            xd = torch.from_numpy(x).cuda().to(dtype)
+            base0, aux0 = snd.base.clone(), snd._aux().clone() if snd._aux() is not None else None
+            p, rec = pl.encode_step(snd, xd, spec, rng=key)
+            if t > 1:
+                dec = p.decode()
+                if mode == "residual_with_feedback":
+                    target = (xd.float() - base0) + aux0
+                    assert torch.equal(snd.feedback, target - dec)  # feedback conservation
+                    assert torch.equal(snd.base, base0 + dec)
+                elif mode == "naive":
+                    assert torch.equal(snd.base, dec)
+            pl.decode_step(rcv, pl.device_message(t, 1, p))
+            assert torch.equal(rcv.base, snd.base)
+            out.append((_relerr(snd.base.cpu().numpy(), x), rec.compression_error))
+        used = lib.cc_debug_lowrank_fused_count() - n0
+    finally:
+        lib.cc_debug_lowrank_fused(1)
+    return out, used
+
+
+@pytest.mark.parametrize("case", [
+    ((1024, 3072), 8, 2, "residual_with_feedback", torch.bfloat16),
+    ((512, 3072), 4, 1, "residual_no_feedback", torch.float32),
+    ((768, 2048), 8, 3, "naive", torch.bfloat16),
+    ((1000, 1024), 6, 2, "residual_with_feedback", torch.float32),
+], ids=lambda c: f"{c[0][0]}x{c[0][1]}-r{c[1]}T{c[2]}-{c[3]}")
+def test_fused_step_matches_multikernel(case):
+    shape, r, iters, mode, dtype = case
+    xs = synth.flux_like(shape[0], shape[1], 5, seed=r + iters)
+    spec = _spec(r, iters)
+    fused, used = _run_steps(mode, xs, spec, 17, 1, dtype)
+    multi, used0 = _run_steps(mode, xs, spec, 17, 0, dtype)
+    assert used == len(xs) - 1 and used0 == 0  # the fused kernel ran every compressed step
+    for t, ((ef, cf), (em, cm)) in enumerate(zip(fused, multi)):
+        assert abs(ef - em) <= 1e-4 * max(1.0, em), (t, ef, em)
+        assert abs(cf - cm) <= 1e-4 * max(1.0, cm), (t, cf, cm)
+
+
+def test_fused_step_vs_reference_channel():
+    """Trajectory of the fused step against the oracle's restatement of the reference
+    channel (pl:84-121 with cx:394-426, host PCG64 Q0 from the same keys)."""
+    cx, pl, linalg = _mods()
+    lib = _lib_handle()
+    n, c = 1024, 3072
+    xs = synth.flux_like(n, c, 4, seed=3)
+    spec = _spec(8, 2)
+    snd = pl.LayerState("residual_with_feedback", 1, torch.zeros(n, c, device="cuda"))
+    och = O.Channel(O.WITH_FEEDBACK, 1, np.zeros((n, c), np.float32))
+    n0 = lib.cc_debug_lowrank_fused_count()
+    for t, x in enumerate(xs, start=1):
+        pl.encode_step(snd, x, spec, rng=linalg.spawn_rng(11, 5, t))
+        O.send(och, x, O.Codec(O.LOWRANK, rank=8, iters=2), rng=linalg.spawn_rng(11, 5, t))
+        assert _relerr(snd.base.cpu().numpy(), och.base) < 1e-3, t
+    assert lib.cc_debug_lowrank_fused_count() - n0 == len(xs) - 1
+
+
+def test_fused_step_device_key_equals_host_rng_at_shard_shape():
+    """[1024, 3072] (the P = 4 shard): the fused kernel with the device-drawn start
+    block equals the fused kernel with the host draw of the same key, bit for bit."""
+    cx, pl, linalg = _mods()
+    n, c = 1024, 3072
+    xs = synth.flux_like(n, c, 4, seed=8)
+    spec = _spec(8, 2)
+    a = pl.LayerState("residual_with_feedback", 1, torch.zeros(n, c, device="cuda"))
+    b = pl.LayerState("residual_with_feedback", 1, torch.zeros(n, c, device="cuda"))
+    key = linalg.DeviceKey(9, 5, 2, advance=True)
+    for t, x in enumerate(xs, start=1):
+        xd = torch.from_numpy(x).cuda().to(torch.bfloat16)
+        pa, ra = pl.encode_step(a, xd, spec, rng=linalg.spawn_rng(9, 5, t))
+        pb, rb = pl.encode_step(b, xd, spec, rng=key)
+        assert pa.body_bytes() == pb.body_bytes(), f"step {t}"
+        assert torch.equal(a.base, b.base) and torch.equal(a.feedback, b.feedback)
+        assert ra.compression_error == rb.compression_error
+
+
+def test_fused_step_rank_deficient_uses_replacement():
+    """A rank-3 residual with r = 8: the Gram of A^T A Q is singular, every CTA sees the
+    same degenerate pivot and CTA 0's CGS2 with replacement columns takes over inside
+    the launch; the rank-3 part is still recovered (cx:402-404, T/test_compressors.py:144)."""
+    cx, pl, linalg = _mods()
+    lib = _lib_handle()
+    g = np.random.default_rng(2)
+    n, c = 1024, 3072
+    a = (g.standard_normal((n, 3)) @ g.standard_normal((3, c))).astype(np.float32)
+    snd = pl.LayerState("naive", 1, torch.zeros(n, c, device="cuda"))
+    pl.encode_step(snd, a, _spec(8, 2), rng=linalg.spawn_rng(1, 5, 1))  # warmup (raw)
+    n0 = lib.cc_debug_lowrank_fused_count()
+    pl.encode_step(snd, a, _spec(8, 2), rng=linalg.spawn_rng(1, 5, 2))
+    assert lib.cc_debug_lowrank_fused_count() - n0 == 1
+    assert _relerr(snd.base.cpu().numpy(), a) < 2e-3
+
+
+@pytest.mark.parametrize("fused", [1, 0])
+def test_fused_exchange_graph_replay_equals_eager(fused):
+    """The P = 4 patch-parallel low-rank step at the benchmarked shard ([1024, 3072]:
+    the fused kernel) captured in one CUDA graph and replayed three times equals the
+    matching eager steps bit for bit."""
+    cx, pl, linalg = _mods()
+    from paper_2507_17511_b200.comm import PatchParallelExchange
+
+    lib = _lib_handle()
+    lib.cc_debug_lowrank_fused(fused)
+    rows, cols, P = 4096, 3072, 4
+    spec = _spec(8, 2)
+    xs = [torch.from_numpy(x).cuda().to(torch.bfloat16)[: rows // P].contiguous()
+          for x in synth.flux_like(rows, cols, 4, seed=6)]
+    ea = PatchParallelExchange(rows, cols, spec, sim_world=(P, 0))
+    eb = PatchParallelExchange(rows, cols, spec, sim_world=(P, 0))
+    ka = linalg.DeviceKey(3, 6, 0, 2, advance=True)
+    kb = linalg.DeviceKey(3, 6, 0, 2, advance=True)
+    n0 = lib.cc_debug_lowrank_fused_count()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for e, k in ((ea, ka), (eb, kb)):
+            for i in range(3):
+                e.step(xs[i], rng=k)
+        ref = []
+        for _ in range(3):  # eager: steps 4, 5, 6 on the same input
+            ea.step(xs[3], rng=ka)
+            ref.append(ea.reconstruction().clone())
+        g = torch.cuda.CUDAGraph()  # one step per graph (the exchange's documented capture unit)
+        with torch.cuda.graph(g, stream=s):
+            eb.step(xs[3], rng=kb)
+            s.wait_stream(eb.streams.decode)
+        eb.after_capture()
+        got = []
+        for _ in range(3):
+            g.replay()
+            s.synchronize()
+            got.append(eb.reconstruction().clone())
+    torch.cuda.synchronize()
+    lib.cc_debug_lowrank_fused(1)
+    assert (lib.cc_debug_lowrank_fused_count() - n0 >= 8) == bool(fused)  # 4 warm + 3 eager + 1 captured
+    for i in range(3):
+        assert torch.equal(got[i], ref[i]), f"replay {i + 1}"
