@@ -796,53 +796,9 @@ __device__ __forceinline__ double factor_at(const uint8_t *body, int int4, int64
   return -range + (double)code * (2.0 * range / 15.0);  // cx:569-572
 }
 
-// factors -> f64 Uf [n, r] and the TRANSPOSED WfT [r, C] (coalesced per-column reads
-// in k_outer_apply); same values as k_unpack_factors
-__global__ void k_unpack_factors_t(const uint8_t *__restrict__ body, int int4, int64_t n, int64_t C, int r,
-                                   double *__restrict__ Uf, double *__restrict__ WfT) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < n * r) Uf[e] = factor_at(body, int4, n, C, r, 0, e / r, (int)(e % r));
-  else if (e < (n + C) * r) {
-    const int64_t e2 = e - n * r;  // column-major over W: k = e2 / C, j = e2 % C
-    WfT[e2] = factor_at(body, int4, n, C, r, 1, e2 % C, (int)(e2 / C));
-  }
-}
-
-// factors -> f64 scratch (Uf [n, r], Wf [C, r]) once, then the outer product
-__global__ void k_unpack_factors(const uint8_t *__restrict__ body, int int4, int64_t n, int64_t C, int r,
-                                 double *__restrict__ Uf, double *__restrict__ Wf) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < n * r) Uf[e] = factor_at(body, int4, n, C, r, 0, e / r, (int)(e % r));
-  else if (e < (n + C) * r) {
-    const int64_t e2 = e - n * r;
-    Wf[e2] = factor_at(body, int4, n, C, r, 1, e2 / r, (int)(e2 % r));
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) k_outer(const double *__restrict__ Uf, const double *__restrict__ Wf,
-                                                     int64_t n, int64_t C, int r, float *__restrict__ out, int acc) {
-  __shared__ double us[8][kMaxR];
-  const int64_t i0 = (int64_t)blockIdx.y * 8;
-  for (int e = threadIdx.x; e < 8 * r; e += kThreads) {
-    const int ii = e / r, k = e % r;
-    us[ii][k] = (i0 + ii < n) ? Uf[(i0 + ii) * r + k] : 0.0;
-  }
-  __syncthreads();
-  const int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (j >= C) return;
-  double w[kMaxR];
-  for (int k = 0; k < r; ++k) w[k] = Wf[j * r + k];
-  for (int ii = 0; ii < 8 && i0 + ii < n; ++ii) {
-    double s = 0.0;
-    for (int k = 0; k < r; ++k) s += us[ii][k] * w[k];
-    const int64_t e = (i0 + ii) * C + j;
-    out[e] = acc ? __fadd_rn(out[e], (float)s) : (float)s;
-  }
-}
-
 // Sender-side state update of a low-rank step with the decode fused in: the
 // reconstruction d = f32(sum_k U[i,k] W[j,k]) in f64 from the body's factors (the
-// receiver's k_outer arithmetic, same summation order, so sender and receiver
+// receiver's k_lr_decode arithmetic, same summation order, so sender and receiver
 // bases stay bit-identical) applied directly: base' = base + d (naive: d),
 // feedback' = t - d, ref' = x (pipeline.py:107-113); StepRecord partials per CTA
 // (||d - t||^2, ||t||^2, pipeline.py:115-120).  No decoded tensor is materialised.
@@ -1128,12 +1084,126 @@ static bool aty(const float *A, const float *Y, float *Z, const lr::Work &w, int
   return false;
 }
 
+namespace lr {
+// ---------------------------------------------------------------------------
+// Batched receiver decode (cx:286-288 for every peer of the step in one launch):
+// base (+)= f32(U W^T), the factors read straight from each body (f16 / INT4 ->
+// f64 as factor_at), f64 accumulation in k order (the sender's k_outer_apply /
+// lr_step.cu arithmetic: bases stay bit-identical).  Block = kDecRows rows x
+// kDecThreads x CPT columns of one peer (blockIdx.z); W's columns stay in
+// registers, U's rows in shared memory; 4 rows of base loads in flight.
+// ---------------------------------------------------------------------------
+constexpr int kDecRows = 16;
+constexpr int kDecThreads = 128;
+constexpr int kDecMax = 16;  // peers per launch
+struct DecBatch {
+  const uint8_t *body[kDecMax];
+  float *base[kDecMax];
+  int64_t rows[kDecMax];
+};
+
+template <int RM, int CPT>
+__global__ void __launch_bounds__(kDecThreads) k_lr_decode(const DecBatch B, int int4, int64_t C, int r, int acc) {
+  const int pi = (int)blockIdx.z;
+  const int64_t n = B.rows[pi];
+  const int64_t i0 = (int64_t)blockIdx.y * kDecRows;
+  if (i0 >= n) return;
+  const uint8_t *body = B.body[pi];
+  __shared__ double us[kDecRows][RM];
+  const int nr = (int)min64(kDecRows, n - i0);
+  for (int e = threadIdx.x; e < kDecRows * RM; e += kDecThreads) {
+    const int ii = e / RM, k = e % RM;
+    us[ii][k] = (ii < nr && k < r) ? factor_at(body, int4, n, C, r, 0, i0 + ii, k) : 0.0;
+  }
+  __syncthreads();
+  const int64_t j0 = ((int64_t)blockIdx.x * kDecThreads + threadIdx.x) * CPT;
+  if (j0 >= C) return;
+  double w[CPT][RM];
+#pragma unroll
+  for (int jj = 0; jj < CPT; ++jj)
+#pragma unroll
+    for (int k = 0; k < RM; ++k) w[jj][k] = (j0 + jj < C && k < r) ? factor_at(body, int4, n, C, r, 1, j0 + jj, k) : 0.0;
+  float *out = B.base[pi];
+  const bool vec = CPT == 4 && j0 + 4 <= C && ((reinterpret_cast<uintptr_t>(out + j0) | (uintptr_t)(C * 4)) & 15) == 0;
+  for (int ib = 0; ib < nr; ib += 4) {
+    float o[4][CPT];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // the base rows' loads in flight together
+      const int ii = ib + u;
+#pragma unroll
+      for (int jj = 0; jj < CPT; ++jj) o[u][jj] = 0.f;
+      if (acc && ii < nr) {
+        const float *src = out + (i0 + ii) * C + j0;
+        if (vec) {
+          const float4 v = *reinterpret_cast<const float4 *>(src);
+          o[u][0] = v.x;
+          o[u][1] = v.y;
+          o[u][2] = v.z;
+          o[u][3] = v.w;
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < CPT; ++jj)
+            if (j0 + jj < C) o[u][jj] = src[jj];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int ii = ib + u;
+      if (ii >= nr) break;
+#pragma unroll
+      for (int jj = 0; jj < CPT; ++jj) {
+        double sacc = 0.0;  // k_lr_decode's order: k = 0 .. r-1
+#pragma unroll
+        for (int k = 0; k < RM; ++k)
+          if (k < r) sacc += us[ii][k] * w[jj][k];
+        const float d = (float)sacc;
+        o[u][jj] = acc ? __fadd_rn(o[u][jj], d) : d;
+      }
+      float *dst = out + (i0 + ii) * C + j0;
+      if (vec) {
+        *reinterpret_cast<float4 *>(dst) = make_float4(o[u][0], o[u][1], o[u][2], o[u][3]);
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < CPT; ++jj)
+          if (j0 + jj < C) dst[jj] = o[u][jj];
+      }
+    }
+  }
+}
+}  // namespace lr
+
+// every body of the step (same C, r) decoded into its base in one launch per kDecMax
+static void decode_batch(const uint8_t *const *bodies, float *const *bases, const int64_t *rows, int count, int int4,
+                         int64_t C, int r, int acc, cudaStream_t st) {
+  for (int b0 = 0; b0 < count; b0 += lr::kDecMax) {
+    const int m = std::min(count - b0, lr::kDecMax);
+    lr::DecBatch B{};
+    int64_t maxn = 0;
+    for (int i = 0; i < m; ++i) {
+      B.body[i] = bodies[b0 + i];
+      B.base[i] = bases[b0 + i];
+      B.rows[i] = rows[b0 + i];
+      maxn = std::max(maxn, rows[b0 + i]);
+    }
+    const dim3 blk(lr::kDecThreads);
+    if (r <= 8) {
+      const dim3 g((unsigned)cdiv(C, lr::kDecThreads * 4), (unsigned)cdiv(maxn, lr::kDecRows), (unsigned)m);
+      lr::k_lr_decode<8, 4><<<g, blk, 0, st>>>(B, int4, C, r, acc);
+    } else if (r <= 16) {
+      const dim3 g((unsigned)cdiv(C, lr::kDecThreads * 2), (unsigned)cdiv(maxn, lr::kDecRows), (unsigned)m);
+      lr::k_lr_decode<16, 2><<<g, blk, 0, st>>>(B, int4, C, r, acc);
+    } else {
+      const dim3 g((unsigned)cdiv(C, lr::kDecThreads), (unsigned)cdiv(maxn, lr::kDecRows), (unsigned)m);
+      lr::k_lr_decode<32, 1><<<g, blk, 0, st>>>(B, int4, C, r, acc);
+    }
+    count_launch();
+  }
+}
+
 static void decode_into(const uint8_t *body, int int4, int64_t n, int64_t C, int r, float *out, int acc,
-                        const lr::Work &w, cudaStream_t st) {
-  lr::k_unpack_factors<<<(unsigned)cdiv((n + C) * r, 256), 256, 0, st>>>(body, int4, n, C, r, w.Uf, w.Wf);
-  dim3 g((unsigned)cdiv(C, lr::kThreads), (unsigned)cdiv(n, 8));
-  lr::k_outer<<<g, lr::kThreads, 0, st>>>(w.Uf, w.Wf, n, C, r, out, acc);
-  count_launch(2);
+                        const lr::Work &, cudaStream_t st) {
+  decode_batch(&body, &out, &n, 1, int4, C, r, acc, st);
 }
 
 int lowrank_encode(int int4, int64_t n, int64_t C, int64_t r64, int iters, const float *t, const float *q0,
@@ -1357,35 +1427,9 @@ int lowrank_encode_step(int mode, int64_t n, int64_t C, int64_t r, int iters, in
   return cuda_status("lowrank_encode_step");
 }
 
-static void keep_default_pool() {
-  static bool done[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t keep = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  }
-  done[dev] = true;
-}
-
 int lowrank_decode(int int4, int count, const int64_t *rows, int64_t C, int64_t r, const uint8_t *const *bodies,
                    int accumulate, float *const *bases, cudaStream_t st) {
-  // factor scratch: allocated per call from the device's default pool, which keeps its
-  // memory across synchronizations (otherwise every event sync trims it and the next
-  // allocation maps fresh pages on the host's critical path)
-  keep_default_pool();
-  int64_t maxn = 0;
-  for (int i = 0; i < count; ++i) maxn = std::max(maxn, rows[i]);
-  double *scratch = nullptr;
-  const size_t bytes = 8 * (size_t)(maxn + C) * r;
-  if (cudaMallocAsync(&scratch, bytes, st) != cudaSuccess) return cuda_status("lowrank_decode alloc");
-  lr::Work w{};
-  w.Uf = scratch;
-  w.Wf = scratch + maxn * r;
-  for (int i = 0; i < count; ++i)
-    decode_into(bodies[i], int4, rows[i], C, (int)r, bases[i], accumulate ? 1 : 0, w, st);
-  cudaFreeAsync(scratch, st);
+  decode_batch(bodies, bases, rows, count, int4, C, (int)r, accumulate ? 1 : 0, st);
   return cuda_status("lowrank_decode");
 }
 

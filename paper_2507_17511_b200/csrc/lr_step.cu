@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
   gbar();  // W visible
   stamp();
 
-  // ---- state update from the body's factors (the receiver's k_outer arithmetic):
+  // ---- state update from the body's factors (the receiver's k_lr_decode arithmetic):
   // thread = 2 columns of the slice, every row of the band
   double err = 0.0;
   if (tid < CS / 2) {
@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
         float dd[2], tt[2];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          double s = 0.0;  // k_outer's order: k = 0 .. r-1
+          double s = 0.0;  // k_lr_decode's order: k = 0 .. r-1
 #pragma unroll
           for (int k = 0; k < 8; ++k)
             if (k < r) s += uu[k] * w[j][k];
