@@ -1096,6 +1096,7 @@ namespace lr {
 constexpr int kDecRows = 16;
 constexpr int kDecThreads = 128;
 constexpr int kDecMax = 16;  // peers per launch
+constexpr int kDecBatch = 4; // rows of base loads in flight per thread (8: measured slower)
 struct DecBatch {
   const uint8_t *body[kDecMax];
   float *base[kDecMax];
@@ -1125,10 +1126,10 @@ __global__ void __launch_bounds__(kDecThreads) k_lr_decode(const DecBatch B, int
     for (int k = 0; k < RM; ++k) w[jj][k] = (j0 + jj < C && k < r) ? factor_at(body, int4, n, C, r, 1, j0 + jj, k) : 0.0;
   float *out = B.base[pi];
   const bool vec = CPT == 4 && j0 + 4 <= C && ((reinterpret_cast<uintptr_t>(out + j0) | (uintptr_t)(C * 4)) & 15) == 0;
-  for (int ib = 0; ib < nr; ib += 4) {
-    float o[4][CPT];
+  for (int ib = 0; ib < nr; ib += kDecBatch) {
+    float o[kDecBatch][CPT];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {  // the base rows' loads in flight together
+    for (int u = 0; u < kDecBatch; ++u) {  // the base rows' loads in flight together
       const int ii = ib + u;
 #pragma unroll
       for (int jj = 0; jj < CPT; ++jj) o[u][jj] = 0.f;
@@ -1148,7 +1149,7 @@ __global__ void __launch_bounds__(kDecThreads) k_lr_decode(const DecBatch B, int
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kDecBatch; ++u) {
       const int ii = ib + u;
       if (ii >= nr) break;
 #pragma unroll

@@ -36,6 +36,7 @@
 #include "lr_dev.cuh"
 
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 namespace cc {
 
@@ -776,7 +777,10 @@ int lowrank_step_fused(int mode, int64_t n, int64_t C, int64_t r, int iters, int
   at[1].id = cudaLaunchAttributeCooperative;
   at[1].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  // CC_LRS_NONCOOP=1 (profiling only: ncu cannot replay a cooperative cluster launch):
+  // the same grid without the co-residency check (it fits an otherwise idle GPU)
+  static const bool noncoop = getenv("CC_LRS_NONCOOP") && atoi(getenv("CC_LRS_NONCOOP")) == 1;
+  cfg.numAttrs = noncoop ? 1 : 2;
   void *args[] = {&p};
   const cudaError_t e = cudaLaunchKernelExC(&cfg, kern, args);
   if (e != cudaSuccess) {
