@@ -103,14 +103,54 @@ __device__ __forceinline__ void tri8(int e, int &a, int &b) {
   b = a + e;
 }
 
+// one warp, lane c < r holds column c of the Gram: right-looking Cholesky with one rsqrt
+// per pivot and shuffles for row j of R (16 live registers: the kernel runs at 128);
+// writes R (upper, zero elsewhere) and 1 / diag(R).  No R^-1: M R^-1 is a row-wise
+// forward substitution (solve_row).
+__device__ __forceinline__ void chol8_lane(const double (*G)[LD], double (*R)[LD], double *invd, int r, int *bad) {
+  const int c = threadIdx.x & 31;
+  double g[8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a) g[a] = (c < r && a < r) ? G[a][c] : 0.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j >= r) break;  // uniform
+    double piv = __shfl_sync(0xffffffffu, g[j], j);  // Schur complement G[j][j] from lane j
+    if (!(piv >= lr::kDegenerate)) {
+      if (c == 0) *bad = 1;
+      piv = 1.0;
+    }
+    const double inv = rsqrt(piv);
+    const double rjc = c == j ? piv * inv : (c > j && c < r ? g[j] * inv : 0.0);  // R[j][c]
+    if (c < 8) R[j][c] = rjc;
+    if (c == j) invd[j] = inv;
+#pragma unroll
+    for (int a = j + 1; a < 8; ++a) {
+      const double rja = __shfl_sync(0xffffffffu, rjc, a);  // R[j][a]
+      if (a < r && c >= a && c < r) g[a] -= rja * rjc;
+    }
+  }
+}
+
+// x <- x R^-1 for one row (forward substitution, columns beyond r zero)
+__device__ __forceinline__ void solve_row(double (&x)[8], const double (*R)[LD], const double *invd, int r) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    double s = x[c];
+#pragma unroll
+    for (int k = 0; k < c; ++k) s -= x[k] * R[k][c];
+    x[c] = c < r ? s * invd[c] : 0.0;
+  }
+}
+
 template <int MODE, typename XT>
 __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) uint8_t sm[];
-  __shared__ double Gm[8][LD], Rm[8][LD], Ri[8][LD], Ri1[8][LD], Rc[8][8];
+  __shared__ double Gm[8][LD], Rf[2][8][LD], Rinvd[2][8];  // Gram; R and 1/diag(R) of the passes
   __shared__ double red[kWarps], coef[lr::kMaxRank], rsum[2][kWarps];
-  __shared__ int bad_s, one_s;
+  __shared__ int bad_s, one_s, qpass;  // qpass: CholQR passes the Q side's next product applies
   __shared__ unsigned last_s;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, tq = lane & 3;
@@ -158,9 +198,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
   for (int e = tid; e < kMaxBand * 8; e += kThreads) yb[e] = 0.0;
   for (int64_t e = (int64_t)nb * S + tid; e < (int64_t)p.nbm * S; e += kThreads) T[e] = 0.0;
 
-  // ---- CholQR2 of rows M[0, nrows) x 8 (f64, row-major); Gram over rows [g0, g1).
-  // Leaves R1^-1 in Ri1, R2^-1 in Ri; returns the (grid-uniform) degenerate flag.
+  // ---- CholQR of rows M[0, nrows) x 8 (f64, row-major), Gram over rows [g0, g1): pass
+  // 1 always, pass 2 when R's diagonal spread is >= kOnePass.  Leaves R (Rf[pass]) and
+  // 1 / diag(R) for the passes taken (their count in np_s); returns the (grid-uniform)
+  // degenerate flag.
   int gpar = 0;
+  __shared__ int np_s;
   auto orth_rows = [&](double *M, int nrows, int g0, int g1) -> bool {
     if (tid == 0) bad_s = 0;
     for (int pass = 0; pass < 2; ++pass) {
@@ -186,10 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
         for (int u = 0; u < kGsPer; ++u) s += v[u];
         gs[h][e] = s;
       }
-      for (int e = tid; e < 8 * LD; e += kThreads) {
-        Rm[e / LD][e % LD] = 0.0;
-        Ri[e / LD][e % LD] = 0.0;
-      }
+      for (int e = tid; e < 8 * LD; e += kThreads) Rf[pass][e / LD][e % LD] = 0.0;
       __syncthreads();
       if (tid < 36) {
         double s = 0.0;
@@ -202,56 +242,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
       }
       __syncthreads();
       if (warp == 0) {
-        if (r == 8) lr::chol8_regs(Gm, Rm, Ri, &bad_s);
-        else lr::chol_rinv_regs<8, LD>(Gm, Rm, Ri, r, &bad_s);
+        chol8_lane(Gm, Rf[pass], Rinvd[pass], r, &bad_s);
+        __syncwarp();
         if (pass == 0 && lane == 0) {  // R's diagonal spread bounds kappa: CholQR's loss of
           double mx = 0.0, mn = 1e300;  // orthogonality ~ eps kappa^2 is below f32 rounding for a
-          for (int j = 0; j < r; ++j) {  // spread < 100: the second pass is skipped (uniform)
-            mx = fmax(mx, Rm[j][j]);
-            mn = fmin(mn, Rm[j][j]);
+          for (int j = 0; j < r; ++j) {  // spread < kOnePass: the second pass is skipped (uniform)
+            mx = fmax(mx, Rf[0][j][j]);
+            mn = fmin(mn, Rf[0][j][j]);
           }
           one_s = mx < kOnePass * mn;
+          np_s = one_s ? 1 : 2;
         }
       }
       __syncthreads();
       stamp();
-      const int row = tid >> 3, col = tid & 7;  // M <- M R^-1 (R^-1 zero below / beyond r)
-      double v = 0.0;
-      if (row < nrows) {
+      if (tid < nrows) {  // M <- M R^-1, one row per thread
+        double x[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v += M[row * 8 + k] * Ri[k][col];
+        for (int k = 0; k < 8; k += 2) {
+          const double2 v = *reinterpret_cast<const double2 *>(M + tid * 8 + k);
+          x[k] = v.x;
+          x[k + 1] = v.y;
+        }
+        solve_row(x, Rf[pass], Rinvd[pass], r);
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) *reinterpret_cast<double2 *>(M + tid * 8 + k) = make_double2(x[k], x[k + 1]);
       }
-      if (pass == 0 && tid < 8 * LD) Ri1[tid / LD][tid % LD] = Ri[tid / LD][tid % LD];
       __syncthreads();
-      if (row < nrows) M[row * 8 + col] = v;
-      if (pass == 0 && one_s) {  // one pass: R2^-1 = I
-        if (tid < 8 * LD) Ri[tid / LD][tid % LD] = (tid / LD == tid % LD && tid / LD < r) ? 1.0 : 0.0;
-        __syncthreads();
-        break;
-      }
-      __syncthreads();
+      if (pass == 0 && one_s) break;  // uniform
     }
     return bad_s != 0;
   };
 
-  // ---- Q side: Q = Z R1^-1 R2^-1 is never materialised: the owners factor the Gram
-  // of their rows of Z (Z64 / Zg already published), every CTA forms Rc = R1^-1 R2^-1
-  // and the next A Q is computed as (A Z) Rc.  Fallback: CTA 0's CGS2 replaces Z64 by
-  // the orthonormal Q (from src, the f32 matrix) and Rc = I.
+  // ---- Q side: Q = Z R1^-1 [R2^-1] is never materialised: the owners factor the Gram of
+  // their rows of Z (Z64 / Zg already published), every CTA holds the same R's and the
+  // next A Q is computed as (A Z) R1^-1 [R2^-1] row by row.  Fallback: CTA 0's CGS2
+  // replaces Z64 by the orthonormal Q (from src, the f32 matrix), no solve.
   int salt = 0;
   auto orth_q = [&](const float *src) {
     const bool bad = orth_rows(Mv, nv, 0, nv);
-    if (tid < 64) {
-      const int a = tid >> 3, cc = tid & 7;
-      double v = 0.0;
-      if (!bad) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v += Ri1[a][k] * Ri[k][cc];
-      } else {
-        v = a == cc && a < r ? 1.0 : 0.0;
-      }
-      Rc[a][cc] = v;
-    }
+    if (tid == 0) qpass = bad ? 0 : np_s;
     if (bad) {  // uniform
       if (b == 0) {
         lr::cgs2_block(src, p.M64, p.Qf, C, r, p.seed + 7919ull * (unsigned)salt, red, coef);
@@ -267,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
     __syncthreads();
   };
 
-  // ---- yb <- f32((A Z) Rc) for the band (rows < nb), every CTA of the cluster
+  // ---- yb <- f32((A Z) R1^-1 [R2^-1]) for the band (rows < nb), every CTA of the cluster
   const int KS = CS / 4, KW = KS / kWarps;  // k-steps of 4 columns: per slice, per warp
   const int MT = (nb + 7) / 8;
   auto y_phase = [&](bool from_q0) {
@@ -320,17 +350,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
       }
     }
     cluster.sync();  // the four column-slice partials of the band are published
-    double yz = 0.0;
     if (tid < nb * 8) {
+      double yz = 0.0;
 #pragma unroll
       for (int qq = 0; qq < kCL; ++qq) yz += cluster.map_shared_rank(yp, qq)[tid];
+      yb[tid] = yz;
     }
-    // Rc's rows / columns beyond r are zero: (A Z) Rc in the row's registers via shuffles
-    const int cc = tid & 7;
-    double y = 0.0;
+    __syncthreads();
+    if (tid < nb) {  // (A Z) R1^-1 [R2^-1], rounded to f32 (la.matmul stores f32)
+      double x[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) y += __shfl_sync(0xffffffffu, yz, (lane & ~7) | k) * Rc[k][cc];
-    if (tid < nb * 8) yb[tid] = (double)(float)y;  // la.matmul stores f32
+      for (int k = 0; k < 8; k += 2) {
+        const double2 v = *reinterpret_cast<const double2 *>(yb + tid * 8 + k);
+        x[k] = v.x;
+        x[k + 1] = v.y;
+      }
+      if (qpass >= 1) solve_row(x, Rf[0], Rinvd[0], r);
+      if (qpass >= 2) solve_row(x, Rf[1], Rinvd[1], r);
+#pragma unroll
+      for (int k = 0; k < 8; k += 2)
+        *reinterpret_cast<double2 *>(yb + tid * 8 + k) = make_double2((double)(float)x[k], (double)(float)x[k + 1]);
+    }
     __syncthreads();
   };
 
@@ -388,9 +428,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
 
   // ---- orth(Q0) (cx:407) is not formed: QR is invariant under a right factor that is
   // upper triangular (orth(M R^-1) = orth(M)), so orth(A^T A orth(Q0)) = orth(A^T A Q0)
-  // and the first product reads the Gaussian block itself (Rc = I).  Q0 is well
+  // and the first product reads the Gaussian block itself (no solve).  Q0 is well
   // conditioned (never degenerate), so the only difference is rounding.
-  if (tid < 64) Rc[tid >> 3][tid & 7] = ((tid >> 3) == (tid & 7) && (tid >> 3) < r) ? 1.0 : 0.0;
+  if (tid == 0) qpass = 0;
 
   // ---- the residual block: t = target(x, base, feedback) -> f64 in shared memory.
   // Software-pipelined in register halves of kTh quads: the loads of one half are in
