@@ -509,6 +509,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
     const int i = u0 + (e >> 3), k = e & 7;
     if (k < r) p.Yg[(rb0 + i) * r + k] = (float)yb[i * 8 + k];
   }
+  // the last reads of the cluster peers' shared memory are done: no CTA of the cluster
+  // may exit before every peer has passed this point (waited on at the end)
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   const bool ubad = orth_rows(yb, nb, u0, u1);
   if (ubad) {  // uniform: every CTA factored the same Gram
     if (b == 0) lr::cgs2_block(p.Yg, p.M64, p.Uf, n, r, p.seed + 104729ull, red, coef);
@@ -658,6 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
     }
   }
   stamp();
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 size_t smem_bytes(int nbm, int64_t C) {

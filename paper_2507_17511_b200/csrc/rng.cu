@@ -345,7 +345,9 @@ __global__ void __launch_bounds__(kGenThreads) k_gauss_gen(const uint32_t *__res
       }
     }
     __syncthreads();
-    if (!changed) break;
+    const int ch = changed;
+    __syncthreads();  // every thread has read the flag before thread 0 clears it for the next round
+    if (!ch) break;
   }
   // output index of real candidate k: p_k minus the extra positions consumed by the
   // real slow draws before it; shift after it = p_k + cons_k - (out_k + 1)
