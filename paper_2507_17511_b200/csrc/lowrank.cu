@@ -745,14 +745,6 @@ __global__ void k_colmax(const float *__restrict__ F, int64_t m, int r, float *_
   }
 }
 
-__device__ __forceinline__ uint32_t int4_code(float f, float range) {
-  if (!(range > 0.0f)) return 0u;  // zero column: code 0 (cx:561-562)
-  const double rg = (double)range;
-  const double step = 2.0 * rg / 15.0;
-  double c = rint(((double)f + rg) / step);  // half-even like np.rint
-  c = c < 0.0 ? 0.0 : (c > 15.0 ? 15.0 : c);
-  return (uint32_t)c;
-}
 
 // nibble stream: U column-major then W column-major, low nibble first
 __global__ void k_pack_int4(const float *__restrict__ U, const float *__restrict__ W, int64_t n, int64_t C, int r,

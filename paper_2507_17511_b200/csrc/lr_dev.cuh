@@ -114,6 +114,19 @@ __device__ __forceinline__ void chol8_regs(const double (*G)[17], double (*Rm)[1
   }
 }
 
+// INT4 factor code / value (cx:556-572): per-column symmetric 16 levels, np.rint half-even
+__device__ __forceinline__ uint32_t int4_code(float f, float range) {
+  if (!(range > 0.0f)) return 0u;  // zero column: code 0 (cx:561-562)
+  const double rg = (double)range;
+  const double step = 2.0 * rg / 15.0;
+  double c = rint(((double)f + rg) / step);  // half-even like np.rint
+  c = c < 0.0 ? 0.0 : (c > 15.0 ? 15.0 : c);
+  return (uint32_t)c;
+}
+__device__ __forceinline__ double int4_value(uint32_t code, float range) {
+  return -(double)range + (double)code * (2.0 * (double)range / 15.0);  // cx:569-572, as factor_at
+}
+
 static __device__ __noinline__ void cgs2_block(const float *__restrict__ orig, double *__restrict__ M, float *__restrict__ out,
                            int64_t m, int r, unsigned long long seed, double *red, double *coef) {
   auto block_sum = [&](double v) {

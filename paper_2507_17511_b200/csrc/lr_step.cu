@@ -58,6 +58,7 @@ constexpr int kZPer = 20;       // clusters per half in the A^T Y reduction (ncl
 struct Params {
   int64_t n, C;
   int r, iters, ncl, nbm;  // nbm: rows of the shared-memory block (max band, multiple of 8)
+  int int4;                // INT4 factors (per-column ranges, cx:556-566) instead of f16
   const void *x;
   float *base, *aux;
   const float *q0;
@@ -72,6 +73,7 @@ struct Params {
   double *Zp;    // [ncl][C][8] per-cluster partials of A^T Y
   double *Gp;    // [2][G][36] Gram partials (alternating)
   double *Rp;    // [G][2] StepRecord partials
+  float *Mx;     // [2][G][8] per-CTA column maxima of |U| / |W| (INT4 ranges)
   double *M64;   // [max(n, C)][r] CGS2 scratch
   unsigned *ctl; // zeroed slab: [0] barrier counter, [32] exit counter
   unsigned long long seed;
@@ -150,7 +152,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ double Gm[8][LD], Rf[2][8][LD], Rinvd[2][8];  // Gram; R and 1/diag(R) of the passes
   __shared__ double red[kWarps], coef[lr::kMaxRank], rsum[2][kWarps];
-  __shared__ int bad_s, one_s, qpass;  // qpass: CholQR passes the Q side's next product applies
+  __shared__ int bad_s, one_s, qpass;
+  __shared__ float rng_s[16];  // INT4 ranges: U columns, then W columns  // qpass: CholQR passes the Q side's next product applies
   __shared__ unsigned last_s;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, tq = lane & 3;
@@ -159,11 +162,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
   const int r = p.r;
   const int CS = (int)(C / kCL), S = CS + 4;  // S = 4 mod 16 doubles: conflict-free MMA fragments
   const int64_t cs0 = (int64_t)q * CS;
-  const int64_t rb0 = (int64_t)c * n / p.ncl, rb1 = (int64_t)(c + 1) * n / p.ncl;
+  // row partitions on even boundaries (the last part takes an odd remainder): an INT4
+  // body byte (two consecutive rows of a factor column) is always written by one CTA
+  auto even_split = [](int64_t total, int parts, int i) -> int64_t {
+    return i >= parts ? total : 2 * ((int64_t)i * (total / 2) / parts);
+  };
+  const int64_t rb0 = even_split(n, p.ncl, c), rb1 = even_split(n, p.ncl, c + 1);
   const int nb = (int)(rb1 - rb0);
-  const int64_t v0 = (int64_t)b * C / G, v1 = (int64_t)(b + 1) * C / G;
+  const int64_t v0 = even_split(C, G, b), v1 = even_split(C, G, b + 1);
   const int nv = (int)(v1 - v0);
-  const int u0 = q * nb / kCL, u1 = (q + 1) * nb / kCL;
+  const int u0 = (int)even_split(nb, kCL, q), u1 = (int)even_split(nb, kCL, q + 1);
 
   double *T = reinterpret_cast<double *>(sm);      // [nbm][S]  the residual block (f64)
   double *ysc = T + (size_t)p.nbm * S;             // [8][4][32][2] warp-tree partials
@@ -526,9 +534,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
   }
   __syncthreads();
   __half *h = reinterpret_cast<__half *>(p.body);
-  for (int e = tid; e < (u1 - u0) * r; e += kThreads) {  // body U: column-major f16 (cx:425)
-    const int k = e / (u1 - u0), i = u0 + e % (u1 - u0);
-    h[(int64_t)k * n + rb0 + i] = __float2half_rn((float)yb[i * 8 + k]);
+  if (!p.int4) {
+    for (int e = tid; e < (u1 - u0) * r; e += kThreads) {  // body U: column-major f16 (cx:425)
+      const int k = e / (u1 - u0), i = u0 + e % (u1 - u0);
+      h[(int64_t)k * n + rb0 + i] = __float2half_rn((float)yb[i * 8 + k]);
+    }
+  } else if (tid < 8) {  // |U| column maxima of this CTA's quarter of the band (cx:559)
+    float mx = 0.0f;
+    for (int i = u0; i < u1; ++i) mx = fmaxf(mx, fabsf((float)yb[i * 8 + tid]));
+    p.Mx[(size_t)b * 8 + tid] = mx;
   }
   stamp();
 
@@ -536,12 +550,50 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
   z_phase();
   gbar();
   z_reduce(p.W64);
-  for (int e = tid; e < nv * r; e += kThreads) {
-    const int i = e % nv, k = e / nv;
-    h[n * r + (int64_t)k * C + v0 + i] = __float2half_rn((float)Mv[i * 8 + k]);
+  if (!p.int4) {
+    for (int e = tid; e < nv * r; e += kThreads) {
+      const int i = e % nv, k = e / nv;
+      h[n * r + (int64_t)k * C + v0 + i] = __float2half_rn((float)Mv[i * 8 + k]);
+    }
+    for (int e = tid; e < nb * 8; e += kThreads) yb[e] = (double)__double2half(yb[e]);
+  } else if (tid < 8) {  // |W| column maxima of the owned rows
+    float mx = 0.0f;
+    for (int i = 0; i < nv; ++i) mx = fmaxf(mx, fabsf((float)Mv[i * 8 + tid]));
+    p.Mx[(size_t)(G + b) * 8 + tid] = mx;
   }
-  for (int e = tid; e < nb * 8; e += kThreads) yb[e] = (double)__double2half(yb[e]);
-  gbar();  // W visible
+  gbar();  // W (and the INT4 column maxima) visible
+  if (p.int4) {
+    // ranges = max over every CTA's maxima (order-free: identical in every CTA)
+    if (tid < 16) {
+      const float *mx = p.Mx + (size_t)(tid >> 3) * G * 8 + (tid & 7);
+      float v = 0.0f;
+      for (int i = 0; i < G; ++i) v = fmaxf(v, __ldcg(mx + (size_t)i * 8));
+      rng_s[tid] = v;
+      if (b == 0 && (tid & 7) < r) reinterpret_cast<float *>(p.body)[(tid >> 3) * r + (tid & 7)] = v;
+    }
+    __syncthreads();
+    uint8_t *nib = p.body + 8 * r;
+    for (int e = tid; e < ((u1 - u0 + 1) >> 1) * r; e += kThreads) {  // U codes, two rows per byte
+      const int pr = (u1 - u0 + 1) >> 1;
+      const int k = e / pr, i = u0 + 2 * (e % pr);
+      uint32_t byte = lr::int4_code((float)yb[i * 8 + k], rng_s[k]);
+      if (i + 1 < u1) byte |= lr::int4_code((float)yb[(i + 1) * 8 + k], rng_s[k]) << 4;
+      nib[((int64_t)k * n + rb0 + i) >> 1] = (uint8_t)byte;
+    }
+    for (int e = tid; e < ((nv + 1) >> 1) * r; e += kThreads) {  // W codes of the owned rows
+      const int pr = (nv + 1) >> 1;
+      const int k = e / pr, i = 2 * (e % pr);
+      uint32_t byte = lr::int4_code((float)Mv[i * 8 + k], rng_s[8 + k]);
+      if (i + 1 < nv) byte |= lr::int4_code((float)Mv[(i + 1) * 8 + k], rng_s[8 + k]) << 4;
+      nib[(n * r + (int64_t)k * C + v0 + i) >> 1] = (uint8_t)byte;
+    }
+    __syncthreads();  // the U codes above read yb
+    for (int e = tid; e < nb * 8; e += kThreads) {  // the band's U as the receiver decodes it
+      const int k = e & 7;
+      yb[e] = k < r ? lr::int4_value(lr::int4_code((float)yb[e], rng_s[k]), rng_s[k]) : 0.0;
+    }
+    __syncthreads();
+  }
   stamp();
 
   // ---- state update from the body's factors (the receiver's k_lr_decode arithmetic):
@@ -556,8 +608,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
 #pragma unroll
       for (int k = 0; k < 8; k += 2) {
         const double2 v = __ldcg(reinterpret_cast<const double2 *>(wr + k));
-        w[j][k] = (double)__double2half(v.x);
-        w[j][k + 1] = (double)__double2half(v.y);
+        if (p.int4) {
+          w[j][k] = k < r ? lr::int4_value(lr::int4_code((float)v.x, rng_s[8 + k]), rng_s[8 + k]) : 0.0;
+          w[j][k + 1] = k + 1 < r ? lr::int4_value(lr::int4_code((float)v.y, rng_s[9 + k]), rng_s[9 + k]) : 0.0;
+        } else {
+          w[j][k] = (double)__double2half(v.x);
+          w[j][k + 1] = (double)__double2half(v.y);
+        }
       }
     }
     for (int row0 = 0; row0 < nb; row0 += 4) {
@@ -692,7 +749,7 @@ static size_t lrs_layout(int64_t n, int64_t C, int64_t r, int ncl, uint8_t *w, l
   const int64_t m = std::max(n, C);
   uint8_t *qg = take(8 * C * 8), *wg = take(8 * C * 8), *zg = take(4 * C * r), *qf = take(4 * C * r), *yg = take(4 * n * r),
           *uf = take(4 * n * r), *zp = take(8 * (size_t)ncl * C * 8), *gp = take(8 * 2 * (size_t)G * 36),
-          *rp = take(16 * (size_t)G), *m64 = take(8 * m * r);
+          *rp = take(16 * (size_t)G), *m64 = take(8 * m * r), *mx = take(4 * 2 * (size_t)G * 8);
   if (w && p) {
     p->Z64 = reinterpret_cast<double *>(qg);
     p->W64 = reinterpret_cast<double *>(wg);
@@ -704,6 +761,7 @@ static size_t lrs_layout(int64_t n, int64_t C, int64_t r, int ncl, uint8_t *w, l
     p->Gp = reinterpret_cast<double *>(gp);
     p->Rp = reinterpret_cast<double *>(rp);
     p->M64 = reinterpret_cast<double *>(m64);
+    p->Mx = reinterpret_cast<float *>(mx);
   }
   return off;
 }
@@ -730,7 +788,10 @@ static const void *lrs_pick(int mode, int x_dtype) {
 }
 
 bool lowrank_fused_may_run(int64_t n, int64_t C, int64_t r, int iters, int int4) {
-  return g_lrs_enable && !int4 && r >= 1 && r <= 8 && iters >= 1 && C % (lrs::kCL * 64) == 0 && n >= 8;
+  // INT4 bodies pack two consecutive entries of a factor column per byte: with n even every
+  // byte stays inside one CTA's rows (odd n: the multi-kernel step)
+  return g_lrs_enable && r >= 1 && r <= 8 && iters >= 1 && C % (lrs::kCL * 64) == 0 && n >= 8 &&
+         !(int4 && (n & 1));
 }
 
 // Returns CC_OK after launching the fused step, 1 when the shape / options are not
@@ -783,9 +844,20 @@ int lowrank_step_fused(int mode, int64_t n, int64_t C, int64_t r, int iters, int
     ncl = mc > 0 ? std::min(mc, kLrsMaxClusters) : -1;
   }
   if (ncl < 1) return 1;
-  const int nbm = (int)(8 * cdiv(cdiv(n, ncl), 8));
   const int G = ncl * lrs::kCL;
-  if (nbm > lrs::kMaxBand || n < (int64_t)ncl * 8 || cdiv(C, G) + 1 > lrs::kMaxVec) return 1;
+  // the kernel's even row partitions (bands of n over the clusters, vector rows of C over the CTAs)
+  auto max_part = [](int64_t total, int parts) {
+    int64_t mx = 0;
+    for (int i = 0; i < parts; ++i) {
+      const int64_t a = i >= parts ? total : 2 * ((int64_t)i * (total / 2) / parts);
+      const int64_t b = i + 1 >= parts ? total : 2 * ((int64_t)(i + 1) * (total / 2) / parts);
+      mx = std::max(mx, b - a);
+    }
+    return mx;
+  };
+  const int64_t band = max_part(n, ncl);
+  const int nbm = (int)(8 * cdiv(band, 8));
+  if (nbm > lrs::kMaxBand || n < (int64_t)ncl * 8 || max_part(C, G) > lrs::kMaxVec) return 1;
   const size_t smem = lrs::smem_bytes(nbm, C);
   if ((int64_t)lrs_layout(n, C, r, ncl, nullptr, nullptr) > ws_bytes) return 1;
   uint8_t *slab = stream_zero_slab(st, kLrsCtlOff + 256);
@@ -795,6 +867,7 @@ int lowrank_step_fused(int mode, int64_t n, int64_t C, int64_t r, int iters, int
   p.C = C;
   p.r = (int)r;
   p.iters = iters;
+  p.int4 = int4;
   p.ncl = ncl;
   p.nbm = nbm;
   p.x = x;

@@ -15,10 +15,12 @@ from paper_2507_17511_b200 import _lib, compressors as cx, pipeline as pl, linal
 
 lib = _lib.load()
 n0 = lib.cc_debug_lowrank_fused_count()
-for (n, c), r, it, mode, dt in (((1024, 3072), 8, 2, "residual_with_feedback", torch.bfloat16),
-                                ((520, 2048), 5, 1, "residual_no_feedback", torch.float32),
-                                ((300, 1024), 8, 3, "naive", torch.bfloat16)):
-    spec = cx.CompressorSpec(cx.CompressorKind.LOWRANK, rank=r, iterations=it)
+for (n, c), r, it, mode, dt, i4 in (((1024, 3072), 8, 2, "residual_with_feedback", torch.bfloat16, False),
+                                    ((520, 2048), 5, 1, "residual_no_feedback", torch.float32, False),
+                                    ((300, 1024), 8, 3, "naive", torch.bfloat16, False),
+                                    ((1024, 3072), 8, 2, "residual_with_feedback", torch.bfloat16, True),
+                                    ((522, 2048), 3, 1, "naive", torch.float32, True)):
+    spec = cx.CompressorSpec(cx.CompressorKind.LOWRANK, rank=r, iterations=it, int4_factors=i4)
     snd = pl.LayerState(mode, 1, torch.zeros(n, c, device="cuda"))
     rcv = pl.LayerState(mode, 1, torch.zeros(n, c, device="cuda"))
     key = la.DeviceKey(3, 5, 2, advance=True)
@@ -26,7 +28,7 @@ for (n, c), r, it, mode, dt in (((1024, 3072), 8, 2, "residual_with_feedback", t
         p, _ = pl.encode_step(snd, torch.from_numpy(x).cuda().to(dt), spec, rng=key)
         pl.decode_step(rcv, pl.device_message(t, 1, p))
     torch.cuda.synchronize()
-    print("ok", n, c, r, it, mode, flush=True)
+    print("ok", n, c, r, it, mode, "int4" if i4 else "f16", flush=True)
 g = np.random.default_rng(2)
 a = (g.standard_normal((1024, 3)) @ g.standard_normal((3, 3072))).astype(np.float32)
 snd = pl.LayerState("naive", 1, torch.zeros(1024, 3072, device="cuda"))
