@@ -203,8 +203,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
   };
   stamp();
 
+  if (tid == 0 && (reinterpret_cast<uintptr_t>(p.q0 + cs0 * r) & 15) == 0)
+    prefetch_l2(p.q0 + cs0 * r, (uint32_t)(CS * r * 4));  // the first A Q's B operand
   for (int e = tid; e < kMaxBand * 8; e += kThreads) yb[e] = 0.0;
   for (int64_t e = (int64_t)nb * S + tid; e < (int64_t)p.nbm * S; e += kThreads) T[e] = 0.0;
+
+  // B fragments of the next A Z (the warp's k-steps of the slice's rows of Z64): loaded
+  // right after the first Gram barrier of the Q-side orth (Z64 is complete then), so their
+  // L2 round trip overlaps the Gram sum and the Cholesky
+  const int KS = CS / 4, KW = KS / kWarps;  // k-steps of 4 columns: per slice, per warp
+  const int ks0 = warp * KW;
+  double bpre[kMaxKW];
+  bool have_pre = false;
+  auto preload_b = [&]() {
+#pragma unroll
+    for (int u = 0; u < kMaxKW; ++u) bpre[u] = u < KW ? __ldcg(p.Z64 + (cs0 + 4 * (ks0 + u) + tq) * 8 + gq) : 0.0;
+    have_pre = true;
+  };
 
   // ---- CholQR of rows M[0, nrows) x 8 (f64, row-major), Gram over rows [g0, g1): pass
   // 1 always, pass 2 when R's diagonal spread is >= kOnePass.  Leaves R (Rf[pass]) and
@@ -212,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
   // degenerate flag.
   int gpar = 0;
   __shared__ int np_s;
-  auto orth_rows = [&](double *M, int nrows, int g0, int g1) -> bool {
+  auto orth_rows = [&](double *M, int nrows, int g0, int g1, bool pre) -> bool {
     if (tid == 0) bad_s = 0;
     for (int pass = 0; pass < 2; ++pass) {
       double *gp = p.Gp + (size_t)(gpar & 1) * G * 36;
@@ -226,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
       }
       gbar();
       stamp();
+      if (pre && pass == 0) preload_b();
       if (tid < kGsChunks * 36) {  // fixed-order sum of the G partials: chunks of CTAs, then the chunks
         const int e = tid % 36, h = tid / 36;
         const int k0 = h * G / kGsChunks, k1 = (h + 1) * G / kGsChunks;
@@ -288,9 +304,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
   // replaces Z64 by the orthonormal Q (from src, the f32 matrix), no solve.
   int salt = 0;
   auto orth_q = [&](const float *src) {
-    const bool bad = orth_rows(Mv, nv, 0, nv);
+    const bool bad = orth_rows(Mv, nv, 0, nv, true);
     if (tid == 0) qpass = bad ? 0 : np_s;
-    if (bad) {  // uniform
+    if (bad) {  // uniform (Z64 is rewritten: the preloaded fragments are stale)
+      have_pre = false;
       if (b == 0) {
         lr::cgs2_block(src, p.M64, p.Qf, C, r, p.seed + 7919ull * (unsigned)salt, red, coef);
         __syncthreads();
@@ -306,15 +323,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
   };
 
   // ---- yb <- f32((A Z) R1^-1 [R2^-1]) for the band (rows < nb), every CTA of the cluster
-  const int KS = CS / 4, KW = KS / kWarps;  // k-steps of 4 columns: per slice, per warp
   const int MT = (nb + 7) / 8;
   auto y_phase = [&](bool from_q0) {
     double acc[4][2];
 #pragma unroll
     for (int m = 0; m < 4; ++m) acc[m][0] = acc[m][1] = 0.0;
-    const int ks0 = warp * KW;
     double bq[kMaxKW];  // the warp's B fragments (Z rows of its k-steps), all loads in flight
-    if (from_q0) {
+    if (have_pre && !from_q0) {  // loaded during the orth (the fallback rewrote Z64: reload)
+#pragma unroll
+      for (int u = 0; u < kMaxKW; ++u) bq[u] = bpre[u];
+    } else if (from_q0) {
 #pragma unroll
       for (int u = 0; u < kMaxKW; ++u)
         bq[u] = (u < KW && gq < r) ? (double)__ldg(p.q0 + (cs0 + 4 * (ks0 + u) + tq) * r + gq) : 0.0;
@@ -322,6 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
 #pragma unroll
       for (int u = 0; u < kMaxKW; ++u) bq[u] = u < KW ? __ldcg(p.Z64 + (cs0 + 4 * (ks0 + u) + tq) * 8 + gq) : 0.0;
     }
+    have_pre = false;
 #pragma unroll
     for (int u = 0; u < kMaxKW; ++u) {
       if (u >= KW) break;
@@ -520,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lr_step(const Params p) {
   // the last reads of the cluster peers' shared memory are done: no CTA of the cluster
   // may exit before every peer has passed this point (waited on at the end)
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-  const bool ubad = orth_rows(yb, nb, u0, u1);
+  const bool ubad = orth_rows(yb, nb, u0, u1, false);
   if (ubad) {  // uniform: every CTA factored the same Gram
     if (b == 0) lr::cgs2_block(p.Yg, p.M64, p.Uf, n, r, p.seed + 104729ull, red, coef);
     gbar();
