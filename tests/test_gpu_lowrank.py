@@ -462,3 +462,40 @@ def test_fused_exchange_graph_replay_equals_eager(fused):
     assert (lib.cc_debug_lowrank_fused_count() - n0 >= 8) == bool(fused)  # 4 warm + 3 eager + 1 captured
     for i in range(3):
         assert torch.equal(got[i], ref[i]), f"replay {i + 1}"
+
+
+@pytest.mark.parametrize("n", [256, 1024], ids=["multi-kernel", "fused"])
+def test_cabi_step_with_device_key_equals_host_rng(n):
+    """cc_lowrank_encode_step called through the C ABI with a device key (the start
+    block drawn inside the call, the key's step word advanced on the device) equals
+    the step with the host draw of the same key, bit for bit, on both step forms."""
+    cx, pl, linalg = _mods()
+    from paper_2507_17511_b200 import _lib
+
+    lib = _lib.load()
+    c, r = 3072, 8
+    xs = synth.flux_like(n, c, 3, seed=2)
+    spec = _spec(r, 2)
+    a = pl.LayerState("residual_with_feedback", 1, torch.zeros(n, c, device="cuda"))
+    b = pl.LayerState("residual_with_feedback", 1, torch.zeros(n, c, device="cuda"))
+    key = linalg.DeviceKey(9, 5, 2, advance=True)
+    ws = torch.empty(lib.cc_lowrank_step_workspace_bytes(n, c, r), dtype=torch.uint8, device="cuda")
+    body = torch.empty(lib.cc_body_bytes(_lib.CC_LOWRANK, n, c, r), dtype=torch.uint8, device="cuda")
+    rec = torch.empty(2, dtype=torch.float64, device="cuda")
+    n0 = lib.cc_debug_lowrank_fused_count()
+    for t, x in enumerate(xs, start=1):
+        xd = torch.from_numpy(x).cuda().to(torch.bfloat16)
+        pa, ra = pl.encode_step(a, xd, spec, rng=linalg.spawn_rng(9, 5, t))
+        if t == 1:
+            pl.encode_step(b, xd, spec)  # warmup: raw
+            continue
+        _lib.check(lib.cc_lowrank_encode_step(2, n, c, r, 2, 0, _lib.ptr(xd), cx.dtype_code(xd), _lib.ptr(b.base),
+                                              _lib.ptr(b.feedback), None, _lib.ptr(key.words), key.nwords,
+                                              key.step_word, _lib.ptr(body), _lib.ptr(ws), ws.numel(),
+                                              _lib.ptr(rec), _lib.stream_ptr()), "step")
+        b.step = t
+        torch.cuda.synchronize()
+        assert body.cpu().numpy().tobytes() == pa.body_bytes(), f"step {t}"
+        assert torch.equal(a.base, b.base) and torch.equal(a.feedback, b.feedback)
+        assert float(rec[0]) == ra.compression_error
+    assert (lib.cc_debug_lowrank_fused_count() - n0 > 0) == (n == 1024)
