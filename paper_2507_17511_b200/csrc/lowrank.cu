@@ -17,6 +17,7 @@
 #include "cc_common.cuh"
 #include "cc_internal.h"
 #include "lr_dev.cuh"
+#include "cc_async.cuh"
 
 #include <algorithm>
 #include <cooperative_groups.h>
@@ -1164,8 +1165,66 @@ __global__ void __launch_bounds__(kDecThreads) k_lr_decode(const DecBatch B, int
     }
   }
 }
+
+// TMA form (r <= 8, accumulate): the CTA's tile of every base row (16 rows x 512
+// columns, 32 KB) arrives by 1-D bulk copies on one mbarrier while the factors load,
+// so the base reads are in flight without holding registers; thread = 2 columns.
+constexpr int kDtRows = 16, kDtCols = 512, kDtThreads = 256;
+__global__ void __launch_bounds__(kDtThreads) k_lr_decode_tma(const DecBatch B, int int4, int64_t C, int r) {
+  const int pi = (int)blockIdx.z;
+  const int64_t n = B.rows[pi];
+  const int64_t i0 = (int64_t)blockIdx.y * kDtRows;
+  if (i0 >= n) return;
+  const int64_t jb = (int64_t)blockIdx.x * kDtCols;
+  const uint8_t *body = B.body[pi];
+  float *out = B.base[pi];
+  __shared__ __align__(128) float tile[kDtRows][kDtCols];
+  __shared__ double us[kDtRows][8];
+  __shared__ __align__(8) uint64_t bar;
+  const int nr = (int)min64(kDtRows, n - i0);
+  const int nc = (int)min64(kDtCols, C - jb);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar, (uint32_t)(nr * nc * 4));
+    for (int i = 0; i < nr; ++i) bulk_g2s(&tile[i][0], out + (i0 + i) * C + jb, (uint32_t)(nc * 4), &bar,
+                                          l2_policy_evict_first());
+  }
+  for (int e = threadIdx.x; e < kDtRows * 8; e += kDtThreads) {
+    const int ii = e >> 3, k = e & 7;
+    us[ii][k] = (ii < nr && k < r) ? factor_at(body, int4, n, C, r, 0, i0 + ii, k) : 0.0;
+  }
+  const int j0 = 2 * threadIdx.x;
+  double w[2][8];
+#pragma unroll
+  for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[jj][k] = (j0 + jj < nc && k < r) ? factor_at(body, int4, n, C, r, 1, jb + j0 + jj, k) : 0.0;
+  __syncthreads();  // us, and the barrier's initialisation
+  mbar_wait(&bar, 0);
+  if (j0 < nc) {
+    for (int ii = 0; ii < nr; ++ii) {
+      float o[2];
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        double sacc = 0.0;  // k_lr_decode's order: k = 0 .. r-1
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < r) sacc += us[ii][k] * w[jj][k];
+        o[jj] = __fadd_rn(tile[ii][j0 + jj], (float)sacc);
+      }
+      float *dst = out + (i0 + ii) * C + jb + j0;
+      if (j0 + 2 <= nc) __stcs(reinterpret_cast<float2 *>(dst), make_float2(o[0], o[1]));
+      else dst[0] = o[0];
+    }
+  }
+}
 }  // namespace lr
 
+static int g_dec_tma = [] {
+  const char *e = getenv("CC_LR_DECODE_TMA");  // A/B: 0 = the register-staged decode
+  return e ? atoi(e) : 1;
+}();
 // every body of the step (same C, r) decoded into its base in one launch per kDecMax
 static void decode_batch(const uint8_t *const *bodies, float *const *bases, const int64_t *rows, int count, int int4,
                          int64_t C, int r, int acc, cudaStream_t st) {
@@ -1180,7 +1239,13 @@ static void decode_batch(const uint8_t *const *bodies, float *const *bases, cons
       maxn = std::max(maxn, rows[b0 + i]);
     }
     const dim3 blk(lr::kDecThreads);
-    if (r <= 8) {
+    bool tma_ok = acc && r <= 8 && (C % 4) == 0 && g_dec_tma;
+    for (int i = 0; i < m && tma_ok; ++i)
+      tma_ok = (reinterpret_cast<uintptr_t>(B.base[i]) & 15) == 0;
+    if (tma_ok) {
+      const dim3 g((unsigned)cdiv(C, lr::kDtCols), (unsigned)cdiv(maxn, lr::kDtRows), (unsigned)m);
+      lr::k_lr_decode_tma<<<g, lr::kDtThreads, 0, st>>>(B, int4, C, r);
+    } else if (r <= 8) {
       const dim3 g((unsigned)cdiv(C, lr::kDecThreads * 4), (unsigned)cdiv(maxn, lr::kDecRows), (unsigned)m);
       lr::k_lr_decode<8, 4><<<g, blk, 0, st>>>(B, int4, C, r, acc);
     } else if (r <= 16) {
