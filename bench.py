@@ -444,12 +444,20 @@ def run_b200(a, world, rank):
                     g.replay()
             barrier(world)
         except Exception as exc:  # e.g. a collective that cannot be captured: measure eagerly
+            import traceback
+            traceback.print_exc()
             print(f"bench: CUDA-graph capture failed ({type(exc).__name__}: {exc}); timing eager launches",
                   file=sys.stderr, flush=True)
             graphs = None
             torch.cuda.synchronize()
             streams = make_exchanges()  # host step counters advanced inside the failed capture
             warm_up()
+
+    if graphs is None:  # eager timing: plain events (external ones only time graph replays)
+        k1ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
+                for _ in range(2)]
+        k2ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
+                for _ in range(2)]
 
     def run(kind, steps):
         for s in range(steps):
@@ -485,7 +493,10 @@ def run_b200(a, world, rank):
     #      state copies, replayed back to back: K1 / K2 as they run in a graph step
     k1s, k2s = [], []
     for s in range(K):
-        run("timed", 1) if graphs is None else graphs["timed"][s % 2].replay()
+        if graphs is None:
+            one_step(s % 2, k1=k1ev[s % 2], k2=k2ev[s % 2])
+        else:
+            graphs["timed"][s % 2].replay()
         torch.cuda.synchronize()
         k1s += [b.elapsed_time(e) for b, e in k1ev[s % 2]]
         k2s += [b.elapsed_time(e) for b, e in k2ev[s % 2]]

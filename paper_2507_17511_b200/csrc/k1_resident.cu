@@ -141,6 +141,36 @@ __device__ __forceinline__ void stcs4(float *p, const float (&v)[4]) {
   __stcs(reinterpret_cast<float4 *>(p), make_float4(v[0], v[1], v[2], v[3]));
 }
 
+// The 2-bit fast path of fused::quantize4<CC_QUANT2> with fewer instructions (same
+// decisions and values, bit for bit): code bit 1 = !neg, bit 0 = big ^ neg, and
+// d = (+-2 | +-0.5) * RN(u v); elements in the guard band, and rows / columns with
+// extreme scales, take the exact f64 path (compressors.py:379-391).
+__device__ __forceinline__ uint32_t quant2_lean(const float (&t)[4], float uf, const fused::ColConst &cc,
+                                                float (&d)[4]) {
+  uint32_t packed = 0;
+  bool ambiguous = !(cc.ok && fused::scale_in_range(fabsf(uf)));
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float ax = fabsf(t[q]);
+    const bool big = ax > __fmul_rn(uf, cc.vhi[q]);
+    ambiguous |= !big && !(ax < __fmul_rn(uf, cc.vlo[q]));
+    const bool neg = t[q] < 0.0f;
+    const float lv = big ? 2.0f : 0.5f;
+    d[q] = __fmul_rn(neg ? -lv : lv, __fmul_rn(uf, cc.v[q]));
+    packed |= ((neg ? 0u : 2u) | ((uint32_t)big ^ (uint32_t)neg)) << (2 * q);
+  }
+  if (__builtin_expect(ambiguous, 0)) {
+    packed = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const fused::CodeVal r = fused::quantize1_exact<CC_QUANT2>(t[q], (double)uf, (double)cc.v[q]);
+      d[q] = r.d;
+      packed |= r.code << (2 * q);
+    }
+  }
+  return packed;
+}
+
 // A ring position: stage index and the parity of its current use, advanced
 // incrementally (no runtime division in the loops).
 struct RingPos {
@@ -505,6 +535,10 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
       cc[j].vlo[q] = __fmul_rd(__fmul_rd(v, 1.25f), 0.99999904632568359375f);  // (1 - 2^-20)
       cc[j].ok = cc[j].ok && fused::scale_in_range(fabsf(v));
     }
+    // keep the column constants in registers: left to itself the compiler re-derives
+    // vhi / vlo (4 directed-rounding multiplies per element) in every row
+#pragma unroll
+    for (int q = 0; q < 4; ++q) asm volatile("" : "+f"(cc[j].v[q]), "+f"(cc[j].vhi[q]), "+f"(cc[j].vlo[q]));
   }
   // code byte offset of each quad inside its segment's code row
   int ccol[NQ];
@@ -531,8 +565,10 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
     const float *trow = tS + (size_t)k * C;
     float tt[NQ][4];
     if (!in_smem) tmem_ld<NQ>(tmem + tmem_off<NQ>(warp, k - p.nsm), tt);  // warp-collective
-    float *obase = p.base + row * C, *oaux = p.aux + row * C;
-    const int64_t crow = row * p.cbs;
+    // 32-bit offsets: a resident shard holds < 2^31 elements (it fits on chip)
+    const uint32_t ro = (uint32_t)row * (uint32_t)C;
+    float *obase = p.base + ro, *oaux = p.aux + ro;
+    const uint32_t crow = (uint32_t)row * (uint32_t)p.cbs;
 #pragma unroll
     for (int j = 0; j < NQ; ++j) {
       const int o = qcol[j];
@@ -548,7 +584,9 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
         t[0] = t[1] = t[2] = t[3] = 0.f;
       }
       const float uf = uS[k * nseg + qseg[j]];
-      const uint32_t packed = fused::quantize4<CODEC>(t, uf, fused::scale_in_range(fabsf(uf)), cc[j], d);
+      uint32_t packed;
+      if constexpr (CODEC == CC_QUANT2) packed = quant2_lean(t, uf, cc[j], d);
+      else packed = fused::quantize4<CODEC>(t, uf, fused::scale_in_range(fabsf(uf)), cc[j], d);
 #pragma unroll
       for (int q = 0; q < 4; ++q) e[q] = __fsub_rn(t[q], d[q]);
       if (qact[j]) {
@@ -560,7 +598,7 @@ __global__ void __launch_bounds__(Geo<NQ>::THREADS, NQ == 2 ? 2 : 1) k1_resident
         if constexpr (kWB) stcs4(oaux + o, e);
       }
       // codes: segment d's code row lives in its own body
-      uint8_t *cp = cbase[j] + crow + ccol[j];
+      uint8_t *cp = cbase[j] + (crow + (uint32_t)ccol[j]);
       if constexpr (CODEC == CC_SIGN1) {
         const uint32_t other = __shfl_down_sync(0xffffffffu, packed, 1);
         if (qact[j] && (lane & 1) == 0) *cp = (uint8_t)(packed | (other << 4));
