@@ -520,8 +520,7 @@ __global__ void __launch_bounds__(256) k_decode_vec(const __grid_constant__ Peer
   pdl_wait();  // PDL launches only: the bodies come from the previous kernel (K1 / the collective)
   const int peer = blockIdx.z;
   const int64_t n = pb.rows[peer];
-  const int64_t r0 = (int64_t)blockIdx.y * RB;
-  if (r0 >= n) return;
+  if ((int64_t)blockIdx.y * RB >= n) return;
   const uint8_t *codes = pb.body[peer];
   float *base = pb.base[peer];
   const int64_t cbytes = (n * C * bits + 7) / 8;
@@ -529,7 +528,6 @@ __global__ void __launch_bounds__(256) k_decode_vec(const __grid_constant__ Peer
   const uint8_t *vb = ub + 4 * n;
   const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (j0 >= C) return;
-  const int rows = (int)(RB < n - r0 ? (int64_t)RB : n - r0);
   float vf[4];
   bool col_ok = true;
 #pragma unroll
@@ -537,36 +535,40 @@ __global__ void __launch_bounds__(256) k_decode_vec(const __grid_constant__ Peer
     vf[q] = load_f32_bytes(vb + 4 * (j0 + q));
     col_ok = col_ok && dec_scale_ok(fabsf(vf[q]));
   }
-  for (int rr = 0; rr < rows; rr += U) {
-    float4 bv[U];
-    uint32_t cw[U];
-    float uf[U];
+  // row blocks blockIdx.y, + gridDim.y, ... (one block each unless the grid is capped)
+  for (int64_t r0 = (int64_t)blockIdx.y * RB; r0 < n; r0 += (int64_t)gridDim.y * RB) {
+    const int rows = (int)(RB < n - r0 ? (int64_t)RB : n - r0);
+    for (int rr = 0; rr < rows; rr += U) {
+      float4 bv[U];
+      uint32_t cw[U];
+      float uf[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const bool ok = (rr + k) < rows;
-      const int64_t i = r0 + rr + k;
-      const int64_t e = i * C + j0;
-      if (ACC) bv[k] = ok ? *reinterpret_cast<const float4 *>(base + e) : make_float4(0.f, 0.f, 0.f, 0.f);
-      uf[k] = ok ? load_f32_bytes(ub + 4 * i) : 1.0f;
-      if (!ok) {
-        cw[k] = 0;
-        continue;
+      for (int k = 0; k < U; ++k) {
+        const bool ok = (rr + k) < rows;
+        const int64_t i = r0 + rr + k;
+        const int64_t e = i * C + j0;
+        if (ACC) bv[k] = ok ? *reinterpret_cast<const float4 *>(base + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        uf[k] = ok ? load_f32_bytes(ub + 4 * i) : 1.0f;
+        if (!ok) {
+          cw[k] = 0;
+          continue;
+        }
+        if constexpr (CODEC == CC_SIGN1) cw[k] = (codes[e >> 3] >> (e & 7)) & 0xfu;
+        else if constexpr (CODEC == CC_QUANT2) cw[k] = codes[e >> 2];
+        else cw[k] = *reinterpret_cast<const uint16_t *>(codes + (e >> 1));
       }
-      if constexpr (CODEC == CC_SIGN1) cw[k] = (codes[e >> 3] >> (e & 7)) & 0xfu;
-      else if constexpr (CODEC == CC_QUANT2) cw[k] = codes[e >> 2];
-      else cw[k] = *reinterpret_cast<const uint16_t *>(codes + (e >> 1));
-    }
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      if ((rr + k) < rows) {
-        const int64_t e = (r0 + rr + k) * C + j0;
-        float d[4];
-        decode4<CODEC>(cw[k], uf[k], dec_scale_ok(fabsf(uf[k])), vf, col_ok, d);
-        float4 o;
-        if (ACC) o = make_float4(__fadd_rn(bv[k].x, d[0]), __fadd_rn(bv[k].y, d[1]), __fadd_rn(bv[k].z, d[2]),
-                                 __fadd_rn(bv[k].w, d[3]));
-        else o = make_float4(d[0], d[1], d[2], d[3]);
-        __stcs(reinterpret_cast<float4 *>(base + e), o);
+      for (int k = 0; k < U; ++k) {
+        if ((rr + k) < rows) {
+          const int64_t e = (r0 + rr + k) * C + j0;
+          float d[4];
+          decode4<CODEC>(cw[k], uf[k], dec_scale_ok(fabsf(uf[k])), vf, col_ok, d);
+          float4 o;
+          if (ACC) o = make_float4(__fadd_rn(bv[k].x, d[0]), __fadd_rn(bv[k].y, d[1]), __fadd_rn(bv[k].z, d[2]),
+                                   __fadd_rn(bv[k].w, d[3]));
+          else o = make_float4(d[0], d[1], d[2], d[3]);
+          __stcs(reinterpret_cast<float4 *>(base + e), o);
+        }
       }
     }
   }
@@ -810,6 +812,11 @@ static int g_dec_small = [] {
   return e ? std::atoi(e) : 0;
 }();
 void set_decode_small(int on) { g_dec_small = on; }
+// experiments: CTAs per SM of the batched decode grid (0 = one CTA per row block)
+static int g_dec_ctas_per_sm = [] {
+  const char *e = std::getenv("CC_K2_CTAS_PER_SM");
+  return e ? std::atoi(e) : 0;
+}();
 
 template <int CODEC, bool ACC>
 static void launch_decode(const PeerBatch &pb, int count, int64_t maxrows, int64_t C, bool vec, cudaStream_t st) {
@@ -822,7 +829,12 @@ static void launch_decode(const PeerBatch &pb, int count, int64_t maxrows, int64
   if (vec) {
     QPlan p;
     plan_shape(p, maxrows, C, true);
-    dim3 grid(p.nStrips, (unsigned)cdiv(maxrows, kDecRows), count);
+    int64_t gy = cdiv(maxrows, kDecRows);
+    if (g_dec_ctas_per_sm > 0) {  // capped grid (row blocks strided): leaves room on every SM for a K1
+      const int64_t cap = (int64_t)g_dec_ctas_per_sm * sm_count() / ((int64_t)p.nStrips * count);
+      gy = std::max<int64_t>(1, std::min(gy, cap));
+    }
+    dim3 grid(p.nStrips, (unsigned)gy, count);
     if (pdl_enabled()) {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = grid;
