@@ -700,6 +700,10 @@ static int g_resident_nq = [] {
   const char *e = std::getenv("CC_K1_RESIDENT_NQ");  // experiments
   return e ? std::atoi(e) : 0;
 }();
+static int g_resident_grid = [] {  // persistent grid size: 0 = by shape (below), -1 = every SM
+  const char *e = std::getenv("CC_K1_RESIDENT_GRID");
+  return e ? std::atoi(e) : 0;
+}();
 std::atomic<int64_t> g_resident_launches{0};
 
 template <int MODE, int CODEC, typename XT, int NQ>
@@ -825,7 +829,17 @@ int resident_encode(const fused::Params &fp, int codec, int mode, int x_dtype, c
   q.n = fp.n;
   q.C = fp.C;
   q.G4 = fp.G4;
-  q.G = (int)std::min<int64_t>(fp.G, fp.n);
+  // Grid: leave SMs free for the receiver decode that runs beside this K1 on the
+  // decode stream (the previous layer's K2, or the peers' at N > 1) — a K1 CTA holds
+  // ~all of an SM's shared memory, so the decode can only overlap on SMs K1 leaves
+  // empty.  Measured (graph-replayed steps, scripts/exp/k2cap_ab.py and bench.py):
+  // P = 1 [4096, 3072] 148 -> 136 CTAs: 76.6 -> 73.5 us per layer-step (K1 alone
+  // 60.8 -> 62.4 us); per-rank P = 2 / 4 / 8 at 128 CTAs: 49.0 -> 42.3, 33.7 -> 33.4,
+  // 27.1 -> 25.7 us.  CC_K1_RESIDENT_GRID overrides (-1 = every SM).
+  int G = fp.G;
+  if (g_resident_grid > 0) G = std::min(g_resident_grid, fp.G);
+  else if (g_resident_grid == 0 && fp.G >= 128) G = fp.G - (cdiv(fp.n, fp.G) >= 20 ? 12 : 20);
+  q.G = (int)std::min<int64_t>(G, fp.n);
   q.R = (int)cdiv(fp.n, q.G);
   q.nseg = fp.nseg;
   q.cw = fp.cw;
@@ -854,8 +868,15 @@ int resident_encode(const fused::Params &fp, int codec, int mode, int x_dtype, c
   // small per-rank shards (<= 14 rows per CTA) the register-capped 12-warp form lets
   // the previous layer's decode share the SMs during the hand-offs (measured per-rank
   // step: [1024, 3072] 44.5 -> 37.0 us, [512, 3072] 40.2 -> 32.9 us, scripts/exp/nq_ab.py)
-  const int nq = g_resident_nq ? g_resident_nq : (q.R <= 14 ? 2 : 1);
-  if (!resident_plan(q, mode, x_dtype, nq)) return CC_ERR_UNSUPPORTED;
+  int nq = g_resident_nq ? g_resident_nq : (q.R <= 14 ? 2 : 1);
+  if (!resident_plan(q, mode, x_dtype, nq)) {
+    // the reduced grid's rows do not fit on chip: every SM (more room per row)
+    if (q.G >= (int)std::min<int64_t>(fp.G, fp.n) || g_resident_grid > 0) return CC_ERR_UNSUPPORTED;
+    q.G = (int)std::min<int64_t>(fp.G, fp.n);
+    q.R = (int)cdiv(fp.n, q.G);
+    nq = g_resident_nq ? g_resident_nq : (q.R <= 14 ? 2 : 1);
+    if (!resident_plan(q, mode, x_dtype, nq)) return CC_ERR_UNSUPPORTED;
+  }
   size_t smem = 0;
   {
     // recompute the total from the chosen layout
