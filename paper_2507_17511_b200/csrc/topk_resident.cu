@@ -35,6 +35,7 @@
 // HBM bytes per element: x 2 + base 4 + aux 4 read, feedback 4 written (+ the
 // selection's O(f) bytes): 14 B, one pass.  Histograms, list counter and barrier
 // words live in a library-owned per-stream slab that every launch leaves zeroed.
+#include <cstdlib>
 #include "cc_async.cuh"
 #include "cc_common.cuh"
 #include "cc_internal.h"
@@ -818,7 +819,16 @@ int topk_resident_encode_step(int mode, int64_t n, int64_t C, int64_t k, const v
   p.total = total;
   p.k = k;
   p.noct = total / 8;
-  p.G = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), cdiv(total, 2048)));
+  // SMs left to the sparse decode running beside this kernel on the decode stream (the
+  // previous layer's peers): it only overlaps on SMs this kernel leaves empty.  Worth it
+  // for heavy decodes: per-rank P = 8 [512, 3072] 10 %: 47.9 -> 41.8 us per layer with 16
+  // SMs free; 1 %: 32.7 -> 33.1 (kept at 0).  CC_TOPK_RESIDENT_RESERVE overrides.
+  static const int reserve_env = [] {
+    const char *e = std::getenv("CC_TOPK_RESIDENT_RESERVE");
+    return e ? std::atoi(e) : -1;
+  }();
+  const int reserve = reserve_env >= 0 ? reserve_env : (k * 20 >= total ? 16 : 0);
+  p.G = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, sm_count() - reserve), cdiv(total, 2048)));
   if (p.G > 255) return CC_ERR_UNSUPPORTED;  // the candidate tag is 8 bits
   // largest CTA range (the last one takes the tail)
   const int64_t ne_max = 8 * cdiv(p.noct, p.G) + 8;
