@@ -14,20 +14,28 @@ from paper_2507_17511_b200 import comm  # noqa: E402
 from paper_2507_17511_b200 import compressors as cx  # noqa: E402
 
 
-def green_stream(nsm):
-    torch.cuda.init()
-    err, dev = drv.cuDeviceGet(0)
-    err, res = drv.cuDeviceGetDevResource(dev, drv.CUdevResourceType.CU_DEV_RESOURCE_TYPE_SM)
-    err, groups, n, rem = drv.cuDevSmResourceSplitByCount(1, res, 0, nsm)
-    assert err == drv.CUresult.CUDA_SUCCESS, err
-    err, desc = drv.cuDevResourceGenerateDesc([groups[0]], 1)
+def _ctx_stream(dev, res):
+    err, desc = drv.cuDevResourceGenerateDesc([res], 1)
     assert err == drv.CUresult.CUDA_SUCCESS, err
     err, g = drv.cuGreenCtxCreate(desc, dev, drv.CUgreenCtxCreate_flags.CU_GREEN_CTX_DEFAULT_STREAM)
     assert err == drv.CUresult.CUDA_SUCCESS, err
     err, st = drv.cuGreenCtxStreamCreate(g, drv.CUstream_flags.CU_STREAM_NON_BLOCKING, 0)
     assert err == drv.CUresult.CUDA_SUCCESS, err
-    print("green ctx SMs", groups[0].sm.smCount, file=sys.stderr)
     return torch.cuda.ExternalStream(int(st)), g
+
+
+def green_stream(nsm, split_rest=False):
+    """(decode stream on nsm SMs, [compute stream on the remaining SMs])"""
+    torch.cuda.init()
+    err, dev = drv.cuDeviceGet(0)
+    err, res = drv.cuDeviceGetDevResource(dev, drv.CUdevResourceType.CU_DEV_RESOURCE_TYPE_SM)
+    err, groups, n, rem = drv.cuDevSmResourceSplitByCount(1, res, 0, nsm)
+    assert err == drv.CUresult.CUDA_SUCCESS, err
+    print("green ctx SMs", groups[0].sm.smCount, "rest", rem.sm.smCount, file=sys.stderr)
+    out = [_ctx_stream(dev, groups[0])]
+    if split_rest:
+        out.append(_ctx_stream(dev, rem))
+    return out
 
 
 def main():
@@ -35,14 +43,18 @@ def main():
     L, rows, cols = 57, 4096, 3072
     dev = torch.device("cuda", 0)
     spec = cx.CompressorSpec(cx.CompressorKind.QUANT2BIT)
+    split = len(sys.argv) > 2 and sys.argv[2] == "split"
+    keep = None
+    if nsm > 0:
+        keep = green_stream(nsm, split)
+        if split:
+            torch.cuda.set_stream(keep[1][0])  # K1 (compute) on the complementary SMs
     exs = [comm.PatchParallelExchange(rows, cols, spec) for _ in range(L)]
     for e in exs[1:]:
         e.streams = exs[0].streams
     S = exs[0].streams
-    keep = None
     if nsm > 0:
-        gs, keep = green_stream(nsm)
-        S._decode = gs
+        S._decode = keep[0][0]
     inputs = [bench.flux_inputs(rows, cols, 0, rows, l, dev) for l in range(L)]
 
     def one(par):
@@ -58,7 +70,7 @@ def main():
         gr = []
         for p in (0, 1):
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, stream=S.compute if split else None):
                 one(p)
                 torch.cuda.current_stream().wait_stream(S.decode)
             gr.append(g)
